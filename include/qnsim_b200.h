@@ -1,0 +1,209 @@
+/*
+ * qnsim_b200 — C-ABI of the B200 (sm_100a) per-timestep quasi-Newton / L-BFGS
+ * hyperelastic solver (arXiv 1604.07378).  Plain pointers and sizes only.
+ *
+ * The reference (`/root/reference/pkg/src/qnsim`, pure Python) has no FFI; each
+ * entry point below replaces one reference call site, cited as file:line.  The
+ * Python host package `paper_1604_07378_b200` binds these through ctypes
+ * (`_lib.py`); INTEGRATION.md shows the binding a qnsim maintainer would add.
+ *
+ * Conventions
+ *   - every function returns QN_OK (0) or a QN_ERR_* code; qn_last_error()
+ *     returns a message for the calling thread's last failure;
+ *   - arrays are C-contiguous row-major, float64 unless stated (int32 indices);
+ *   - `mem` selects where caller buffers live: QN_MEM_HOST (pageable or pinned
+ *     host memory; the library stages through its own pinned buffers) or
+ *     QN_MEM_DEVICE (device pointers on the current CUDA device);
+ *   - `stream` is a cudaStream_t (NULL = the library's own stream); every call
+ *     is stream-ordered and the call returns after the stream work completes
+ *     unless stated otherwise.
+ */
+#ifndef QNSIM_B200_H
+#define QNSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QN_OK 0
+#define QN_ERR_ARG 1          /* bad argument (shape, range, null)            */
+#define QN_ERR_CUDA 2         /* CUDA runtime failure                         */
+#define QN_ERR_NOT_SPD 3      /* FactorizationError (linalg.py:20-21,31-34)   */
+#define QN_ERR_ALLOC 4        /* device or host allocation failed             */
+#define QN_ERR_ASCENT 5       /* SolverError: non-descent direction (solvers.py:244-246) */
+#define QN_ERR_UNSUPPORTED 6  /* option outside the B200 hot path             */
+
+#define QN_MEM_HOST 0
+#define QN_MEM_DEVICE 1
+
+/* Valanis-Landel scalar-function kinds (materials.py:32-133) */
+#define QN_FN_ZERO 0
+#define QN_FN_POLY 1
+#define QN_FN_LOG 2
+#define QN_FN_HERMITE 3
+
+#define QN_MAX_COEF 12   /* polynomial coefficients (ascending)  */
+#define QN_MAX_KNOTS 12  /* cubic Hermite control points          */
+#define QN_MAX_M 16      /* L-BFGS history window                 */
+
+/* One univariate function a, b or c of Psi = sum a(si) + sum b(si sj) + c(s1 s2 s3). */
+typedef struct qn_scalar_fn {
+  int32_t kind;                 /* QN_FN_*                                        */
+  int32_t n;                    /* poly: #coefficients; hermite: #knots            */
+  double c[QN_MAX_COEF];        /* poly: ascending coefficients (PolyFn, :40-51)  */
+  double dc[QN_MAX_COEF];       /* poly: polyder(c), n-1 entries                   */
+  double xs[QN_MAX_KNOTS];      /* hermite knots, strictly increasing (:83-133)   */
+  double ys[QN_MAX_KNOTS];
+  double ts[QN_MAX_KNOTS];
+  double alpha, beta, eps;      /* log: alpha ln x + beta/2 ln^2 x, x > eps (:54-80) */
+  double f0, f1, f2;            /* log: value/slope/curvature at eps (Taylor)    */
+} qn_scalar_fn;
+
+/* MaterialModel (materials.py:146-159): shift = 3a(1) + 3b(1) + c(1). */
+typedef struct qn_material {
+  qn_scalar_fn a, b, c;
+  double shift;
+} qn_material;
+
+/* ------------------------------------------------------------------------ */
+/* library                                                                  */
+
+const char* qn_last_error(void);
+int qn_version(void);
+/* number of CUDA devices visible; 0 without a GPU (no compute calls then) */
+int qn_device_count(int32_t* count);
+/* kernels launched by this library since load (for launch-count evidence) */
+int qn_launch_count(int64_t* count);
+
+/* ------------------------------------------------------------------------ */
+/* rotation-variant 3x3 SVD — replaces linalg.svd_rv_batch (linalg.py:86-110)
+ * F: (m,3,3); U, V: (m,3,3) proper rotations; sigma: (m,3), s0 >= s1 >= |s2|,
+ * s2 < 0 iff det F < 0, |s| < 1e-10 clamped to +-1e-10. */
+int qn_svd_rv_batch(int64_t m, const double* F, double* U, double* sigma, double* V, int32_t mem,
+                    void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* material point evaluation — replaces vl_energy_batch / vl_stress_batch
+ * (materials.py:181-207) on the device.  sigma: (k,3) -> psi (k), tau (k,3). */
+int qn_material_eval(const qn_material* mat, int64_t k, const double* sigma, double* psi, double* tau,
+                     int32_t mem, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Prefactored SPD solve — replaces linalg.Factorization / factorize_spd /
+ * solve_prefactored (linalg.py:23-59) and the dense cho_factor of
+ * dynamics.py:413-414.  Supernodal Cholesky (host, geometric nested
+ * dissection on `coords`) + level-free dependency-driven supernodal
+ * triangular solves on the device.  A: symmetric CSR (both triangles),
+ * `nbatch` numeric instances sharing one pattern (values: nbatch x nnz). */
+typedef struct qn_factor qn_factor;
+
+typedef struct qn_factor_info {
+  int64_t n, nnz_a, nnz_l, n_supernodes, max_front, tree_depth, nbatch;
+  double factor_seconds, flops;
+} qn_factor_info;
+
+int qn_factor_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,
+                     int64_t nbatch, const double* coords, qn_factor** out);
+int qn_factor_info_get(const qn_factor* f, qn_factor_info* info);
+/* X = A^-1 B for instance `batch`; B, X: (n, nrhs) row-major */
+int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int64_t nrhs, int32_t mem,
+                    void* stream);
+int qn_factor_destroy(qn_factor* f);
+
+/* ------------------------------------------------------------------------ */
+/* Simulation system — replaces dynamics.build_system (dynamics.py:351-434)
+ * for Valanis-Landel tet groups, plus the per-frame solver
+ * solvers.simulate_frame (solvers.py:260-352).  `n_inst` independent
+ * instances share one mesh (topology, rest shape, fixed set) and may differ in
+ * material and in the numeric factor (configs[3] batch); n_inst = 1 is a
+ * plain SimSystem. */
+typedef struct qn_system qn_system;
+
+typedef struct qn_system_desc {
+  int64_t n_verts;            /* n                                              */
+  int64_t n_tets;             /* m (may be 0: no elastic groups)                */
+  int64_t n_inst;             /* instances (>= 1)                               */
+  int64_t n_mat;              /* materials per instance (VL groups)             */
+  const int32_t* tets;        /* (m,4), group-major order (dynamics.py:332-348) */
+  const double* Dm_inv;       /* (m,3,3): G[:,1:] of mesh.tet_diff_operators    */
+  const double* vols;         /* (m)                                            */
+  const int32_t* tet_mat;     /* (m) material index in [0,n_mat) or NULL        */
+  const qn_material* mats;    /* (n_inst * n_mat)                               */
+  const double* masses;       /* (n) lumped masses (mesh.py:178-197)            */
+  int64_t n_fixed;
+  const int32_t* fixed;       /* sorted fixed vertex ids                        */
+  double h;
+  double gravity[3];
+  double scale;               /* rest bbox diagonal (dynamics.py:416-417)      */
+  /* A_free = (L + M/h^2)[free][free], CSR over free rows, values per instance */
+  int64_t a_nnz;
+  const int64_t* a_indptr;    /* (n_free+1)                                     */
+  const int32_t* a_indices;   /* (a_nnz)                                        */
+  const double* a_values;     /* (n_inst * a_nnz)                               */
+  const double* free_coords;  /* (n_free,3) rest positions for the ordering     */
+} qn_system_desc;
+
+typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          */
+  int32_t kind;                    /* 0 = pd_qn, 1 = lbfgs (lbfgs_init=system_matrix) */
+  int32_t iterations;
+  int32_t m;
+  int32_t line_search;
+  double gamma, alpha_init, alpha_shrink;
+} qn_solver_config;
+
+typedef struct qn_frame_record {   /* ConvergenceRecord (solvers.py:71-80), per instance */
+  double* g0;        /* (n_inst)                 */
+  double* g;         /* (n_inst, iterations)     */
+  int32_t* ls_trials;/* (n_inst, iterations)     */
+  double* alphas;    /* (n_inst, iterations)     */
+  double* cum_ms;    /* (n_inst, iterations)     */
+  int32_t* status;   /* (n_inst): bit0 stagnated, bit1 ascent error */
+} qn_frame_record;
+
+int qn_system_create(const qn_system_desc* desc, qn_system** out);
+int qn_system_destroy(qn_system* s);
+int qn_system_factor(qn_system* s, qn_factor** out);  /* borrowed handle */
+
+/* Device-resident state (SimState q_l / q_prev, dynamics.py:314-329), (n_inst,n,3). */
+int qn_state_set(qn_system* s, const double* q_l, const double* q_prev, int32_t mem, void* stream);
+int qn_state_get(qn_system* s, double* q_l, double* q_prev, double* y, int32_t mem, void* stream);
+
+/* Advance the resident state one frame: y = inertia target, minimise g(x) by
+ * `cfg`, then q_prev <- q_l, q_l <- x.  fixed_targets: (n_inst, n_fixed, 3) or
+ * NULL (= q_l rows, dynamics.py:441-442).  rec: NULL or output record
+ * (host pointers if mem == QN_MEM_HOST).  sync = 0 returns without waiting
+ * (record then must be NULL).  Whole frame = one CUDA-graph launch. */
+int qn_frame_step(qn_system* s, const qn_solver_config* cfg, const double* fixed_targets,
+                  qn_frame_record* rec, int32_t mem, int32_t sync, void* stream);
+
+/* Stateless wrapper = simulate_frame(system, state, config, fixed_targets):
+ * uploads q_l/q_prev, steps, downloads x (next q_l) and y. */
+int qn_simulate_frame(qn_system* s, const qn_solver_config* cfg, const double* q_l, const double* q_prev,
+                      const double* fixed_targets, double* x_out, double* y_out, qn_frame_record* rec,
+                      int32_t mem, void* stream);
+
+/* objective g(x) and gradient (dynamics.py:460-478) at x for target y,
+ * per instance: g_out (n_inst), grad_out (n_inst,n,3) or NULL. */
+int qn_system_objective(qn_system* s, const double* x, const double* y, double* g_out, double* grad_out,
+                        int32_t mem, void* stream);
+
+/* Element-group seam (dynamics.VLGroup.energy / add_gradient, :57-67):
+ * energy of the tets of material group `mat` of instance `inst` (all tets if
+ * mat < 0) and their corner forces scattered, element-major, into out. */
+int qn_system_elements(qn_system* s, int64_t inst, int64_t mat, const double* x, double* energy,
+                       double* grad_accum, int32_t mem, void* stream);
+
+/* Execution mode for debugging: 1 = CUDA graph with conditional nodes
+ * (default), 0 = host-driven loop (one host sync per line-search trial). */
+int qn_system_set_graph_mode(qn_system* s, int32_t use_graph);
+/* device time (ms) of the last qn_frame_step measured with CUDA events */
+int qn_system_last_frame_ms(qn_system* s, double* ms);
+/* body passes (line-search trials + re-evaluations) of the last frame */
+int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QNSIM_B200_H */

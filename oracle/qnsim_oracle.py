@@ -1,0 +1,581 @@
+"""numpy/scipy restatement of the qnsim hot path (TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+Reference = `/root/reference/pkg/src/qnsim` (pure Python, numpy + scipy).  The
+restatement keeps the reference's arithmetic (same library primitives, same
+operation order where it matters) so it agrees with the reference to roundoff;
+`tests/test_oracle_golden.py` pins it to the reference's own outputs.
+
+Differences from the reference, all deliberate and documented in DESIGN.md:
+* the prefactored solve can use a sparse LU (`factor="sparse"`) in place of the
+  dense `cho_factor` of `linalg.py:31` / `dynamics.py:413` (dense is O(n^2)
+  memory, infeasible beyond configs[1]); `factor="dense"` restates the
+  reference exactly;
+* the harness-side scenario parsing, colliders, PD materials, Chebyshev and
+  Newton are out of the hot-path scope and not restated.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+import scipy.sparse.linalg
+
+SIGMA_CLAMP = 1e-10          # linalg.py:13
+LOG_EPS = 0.01               # materials.py:21
+FIT_SAMPLES = 1001           # materials.py:23
+CURVATURE_GUARD = 1e-12      # solvers.py:28
+ALPHA_FLOOR = 1e-12          # solvers.py:29
+
+
+class OracleError(Exception):
+    pass
+
+
+class OracleStagnation(OracleError):
+    pass
+
+
+# --------------------------------------------------------------------------
+# mesh (setup)
+
+_FREUDENTHAL = np.array(
+    [(0, 1, 3, 7), (0, 3, 2, 7), (0, 2, 6, 7), (0, 6, 4, 7), (0, 4, 5, 7), (0, 5, 1, 7)],
+    dtype=np.int64,
+)  # assets.py:10-17 (corner code = di*4 + dj*2 + dk)
+
+
+def grid_bar(nx, ny, nz, size):
+    """Vectorised restatement of `assets.bar_mesh` (assets.py:20-69, 66-69).
+
+    Vertex id (i*(ny+1)+j)*(nz+1)+k (assets.py:25-26), cells in C order, six
+    tets per cell in `_CUBE_TETS` order, then the orientation fix that swaps
+    corners 2,3 of negatively oriented tets (assets.py:58-62)."""
+    sx, sy, sz = size[0] / nx, size[1] / ny, size[2] / nz
+    i, j, k = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+    verts = np.stack([0.0 + i.ravel() * sx, 0.0 + j.ravel() * sy, 0.0 + k.ravel() * sz], axis=1)
+    ci, cj, ck = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    ci, cj, ck = ci.ravel(), cj.ravel(), ck.ravel()
+    corners = np.empty((ci.size, 8), dtype=np.int64)
+    for code in range(8):
+        di, dj, dk = code >> 2, (code >> 1) & 1, code & 1
+        corners[:, code] = ((ci + di) * (ny + 1) + (cj + dj)) * (nz + 1) + (ck + dk)
+    tets = corners[:, _FREUDENTHAL].reshape(-1, 4)
+    v = verts[tets]
+    vols = np.linalg.det(np.swapaxes(v[:, 1:] - v[:, :1], 1, 2)) / 6.0
+    neg = vols < 0
+    tets[neg] = tets[neg][:, [0, 1, 3, 2]]
+    return verts, tets
+
+
+def read_node_ele(node_path, ele_path):
+    """TetGen reader restating mesh.py:52-68,71-146 for well-formed files
+    (comments stripped, 0/1-based detection, orientation fix)."""
+    def rows(path):
+        out = []
+        with open(path) as fh:
+            for line in fh:
+                t = line.split("#", 1)[0].strip()
+                if t:
+                    out.append(t.split())
+        return out
+
+    nr = rows(node_path)
+    nv = int(nr[0][0])
+    ids = np.array([int(r[0]) for r in nr[1:1 + nv]])
+    verts = np.array([[float(r[1]), float(r[2]), float(r[3])] for r in nr[1:1 + nv]])
+    base = 0 if ids[0] == 0 else 1
+    er = rows(ele_path)
+    ne = int(er[0][0])
+    tets = np.array([[int(p) for p in r[1:5]] for r in er[1:1 + ne]], dtype=np.int64) - base
+    v = verts[tets]
+    vols = np.linalg.det(v[:, 1:] - v[:, :1]) / 6.0
+    neg = vols < 0
+    tets[neg] = tets[neg][:, [0, 1, 3, 2]]
+    return verts, tets
+
+
+def diff_operators(verts, tets):
+    """G (m,4,3) with G[1:] = Dm^-1, G[0] = -sum rows; volumes (mesh.py:200-216)."""
+    v = verts[tets]
+    Dm = np.swapaxes(v[:, 1:] - v[:, :1], 1, 2)
+    vols = np.linalg.det(Dm) / 6.0
+    if np.any(vols < 1e-14):
+        raise OracleError("degenerate rest tet")
+    Dinv = np.linalg.inv(Dm)
+    G = np.empty((tets.shape[0], 4, 3))
+    G[:, 1:, :] = Dinv
+    G[:, 0, :] = -Dinv.sum(axis=1)
+    return G, vols
+
+
+def vertex_masses(verts, tets, density):
+    """Lumped masses rho*V/4 per corner, corner-major accumulation (mesh.py:178-197)."""
+    v = verts[tets]
+    vols = np.linalg.det(v[:, 1:] - v[:, :1]) / 6.0
+    share = density * vols / 4.0
+    m = np.zeros(verts.shape[0])
+    for c in range(4):
+        np.add.at(m, tets[:, c], share)
+    if np.any(m <= 0):
+        raise OracleError("massless vertex")
+    return m
+
+
+# --------------------------------------------------------------------------
+# scalar functions and Valanis-Landel materials (materials.py)
+
+class Zero:
+    """materials.py:32-37"""
+    kind = "zero"
+
+    def f(self, x):
+        return np.zeros_like(np.asarray(x, dtype=np.float64))
+
+    df = f
+
+
+class Poly:
+    """Ascending coefficients, numpy polyval (Horner) — materials.py:40-51."""
+    kind = "poly"
+
+    def __init__(self, coeffs):
+        self.c = np.asarray(coeffs, dtype=np.float64)
+        self.dc = np.polynomial.polynomial.polyder(self.c) if self.c.size > 1 else np.zeros(1)
+
+    def f(self, x):
+        return np.polynomial.polynomial.polyval(np.asarray(x, dtype=np.float64), self.c)
+
+    def df(self, x):
+        return np.polynomial.polynomial.polyval(np.asarray(x, dtype=np.float64), self.dc)
+
+
+class Log:
+    """alpha ln x + beta/2 ln^2 x, quadratic Taylor continuation at x <= eps (materials.py:54-80)."""
+    kind = "log"
+
+    def __init__(self, alpha, beta, eps=LOG_EPS):
+        self.alpha, self.beta, self.eps = float(alpha), float(beta), float(eps)
+        le = np.log(self.eps)
+        self.f0 = self.alpha * le + 0.5 * self.beta * le * le
+        self.f1 = (self.alpha + self.beta * le) / self.eps
+        self.f2 = (self.beta - self.alpha - self.beta * le) / (self.eps * self.eps)
+
+    def f(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        inside = x > self.eps
+        lx = np.log(np.where(inside, x, 1.0))
+        d = x - self.eps
+        return np.where(inside, self.alpha * lx + 0.5 * self.beta * lx * lx,
+                        self.f0 + self.f1 * d + 0.5 * self.f2 * d * d)
+
+    def df(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        inside = x > self.eps
+        sx = np.where(inside, x, 1.0)
+        return np.where(inside, (self.alpha + self.beta * np.log(sx)) / sx,
+                        self.f1 + self.f2 * (x - self.eps))
+
+
+class Hermite:
+    """Cubic Hermite spline, searchsorted(side='right') segments clipped to the
+    knot range, linear extrapolation outside (materials.py:83-133)."""
+    kind = "hermite"
+
+    def __init__(self, points):
+        p = np.asarray(points, dtype=np.float64)
+        p = p[np.argsort(p[:, 0])]
+        if p.shape[0] < 2 or np.any(np.diff(p[:, 0]) <= 0):
+            raise OracleError("bad spline knots")
+        self.xs, self.ys, self.ts = p[:, 0].copy(), p[:, 1].copy(), p[:, 2].copy()
+
+    def _seg(self, x):
+        i = np.clip(np.searchsorted(self.xs, x, side="right") - 1, 0, self.xs.size - 2)
+        h = self.xs[i + 1] - self.xs[i]
+        return i, h, (x - self.xs[i]) / h
+
+    def f(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        i, h, u = self._seg(x)
+        u2, u3 = u * u, u * u * u
+        v = ((2 * u3 - 3 * u2 + 1) * self.ys[i] + (u3 - 2 * u2 + u) * h * self.ts[i]
+             + (-2 * u3 + 3 * u2) * self.ys[i + 1] + (u3 - u2) * h * self.ts[i + 1])
+        v = np.where(x < self.xs[0], self.ys[0] + self.ts[0] * (x - self.xs[0]), v)
+        return np.where(x > self.xs[-1], self.ys[-1] + self.ts[-1] * (x - self.xs[-1]), v)
+
+    def df(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        i, h, u = self._seg(x)
+        u2 = u * u
+        v = ((6 * u2 - 6 * u) * self.ys[i] / h + (3 * u2 - 4 * u + 1) * self.ts[i]
+             + (-6 * u2 + 6 * u) * self.ys[i + 1] / h + (3 * u2 - 2 * u) * self.ts[i + 1])
+        v = np.where(x < self.xs[0], self.ts[0], v)
+        return np.where(x > self.xs[-1], self.ts[-1], v)
+
+
+@dataclass
+class VLMaterial:
+    """(a, b, c) triple; shift = 3a(1)+3b(1)+c(1) (materials.py:146-159)."""
+    a: object
+    b: object
+    c: object
+    name: str = "custom"
+    shift: float = field(init=False)
+
+    def __post_init__(self):
+        self.shift = float(3 * self.a.f(1.0) + 3 * self.b.f(1.0) + self.c.f(1.0))
+
+
+def builtin(name, mu=None, lam=0.0, mu1=None, mu2=0.0, spline_a=None, spline_b=None, spline_c=None):
+    """Built-in materials (materials.py:257-297)."""
+    if name == "polynomial":
+        return VLMaterial(Poly(mu * np.array([1, -4, 6, -4, 1.0])), Zero(), Zero(), name)
+    if name == "corotated":
+        return VLMaterial(Poly([mu + 1.5 * lam, -2 * mu - 3 * lam, mu + 0.5 * lam]),
+                          Poly([0.0, lam]), Zero(), name)
+    if name == "stvk":
+        A = mu / 4.0 + lam / 8.0
+        return VLMaterial(Poly([A + lam / 2.0, 0.0, -2 * A - lam / 2.0, 0.0, A]),
+                          Poly([-lam / 4.0, 0.0, lam / 4.0]), Zero(), name)
+    if name == "neohookean":
+        return VLMaterial(Poly([-mu / 2.0, 0.0, mu / 2.0]), Zero(), Log(-mu, lam), name)
+    if name == "mooney_rivlin":
+        b = Poly([-mu2, 0.0, mu2]) if mu2 > 0 else Zero()
+        return VLMaterial(Poly([-mu1, 0.0, mu1]), b, Log(-(2 * mu1 + 4 * mu2), lam), name)
+    if name == "spline":
+        fa = Hermite(spline_a) if spline_a is not None else Zero()
+        fb = Hermite(spline_b) if spline_b is not None else Zero()
+        fc = Hermite(spline_c) if spline_c is not None else Zero()
+        return VLMaterial(fa, fb, fc, name)
+    raise OracleError(f"unknown material {name}")
+
+
+def vl_energy(mat, s):
+    """materials.py:181-188"""
+    s1, s2, s3 = s[..., 0], s[..., 1], s[..., 2]
+    return (mat.a.f(s1) + mat.a.f(s2) + mat.a.f(s3)
+            + mat.b.f(s1 * s2) + mat.b.f(s2 * s3) + mat.b.f(s1 * s3)
+            + mat.c.f(s1 * s2 * s3) - mat.shift)
+
+
+def vl_stress(mat, s):
+    """materials.py:196-207"""
+    s1, s2, s3 = s[..., 0], s[..., 1], s[..., 2]
+    b12, b23, b13 = mat.b.df(s1 * s2), mat.b.df(s2 * s3), mat.b.df(s1 * s3)
+    c = mat.c.df(s1 * s2 * s3)
+    out = np.empty_like(s)
+    out[..., 0] = mat.a.df(s1) + b12 * s2 + b13 * s3 + c * s2 * s3
+    out[..., 1] = mat.a.df(s2) + b12 * s1 + b23 * s3 + c * s1 * s3
+    out[..., 2] = mat.a.df(s3) + b23 * s2 + b13 * s1 + c * s1 * s2
+    return out
+
+
+def fit_stiffness(mat, lo=0.5, hi=1.5):
+    """OLS slope of a'(s)+2b'(s)+c'(s) over 1001 samples (materials.py:210-229)."""
+    xs = np.linspace(lo, hi, FIT_SAMPLES)
+    ys = mat.a.df(xs) + 2.0 * mat.b.df(xs) + mat.c.df(xs)
+    dx, dy = xs - xs.mean(), ys - ys.mean()
+    k = float(np.dot(dx, dy) / np.dot(dx, dx))
+    if k <= 0:
+        raise OracleError("non-positive fitted stiffness")
+    return k
+
+
+# --------------------------------------------------------------------------
+# rotation-variant SVD (linalg.py:86-110)
+
+def svd_rv(F):
+    F = np.asarray(F, dtype=np.float64)
+    U, s, Vt = np.linalg.svd(F)
+    V = np.swapaxes(Vt, -1, -2)
+    for M in (U, V):
+        flip = np.linalg.det(M) < 0
+        M[flip, :, 2] *= -1.0
+        s[flip, 2] *= -1.0
+    small = np.abs(s) < SIGMA_CLAMP
+    s[small] = np.where(s[small] < 0, -SIGMA_CLAMP, SIGMA_CLAMP)
+    return U, s, V
+
+
+# --------------------------------------------------------------------------
+# element groups and the objective (dynamics.py:40-70, 437-478)
+
+@dataclass
+class TetGroup:
+    tets: np.ndarray
+    G: np.ndarray
+    vols: np.ndarray
+    mat: VLMaterial
+    k: float
+
+    def defgrad(self, x):
+        return np.einsum("eva,evc->eac", x[self.tets], self.G)
+
+    def energy(self, x):
+        """dynamics.py:57-63"""
+        _, s, _ = svd_rv(self.defgrad(x))
+        return float((self.vols * vl_energy(self.mat, s)).sum())
+
+    def corner_forces(self, x):
+        """vol * U diag(tau) V^T G^T per corner (dynamics.py:50-55)."""
+        U, s, V = svd_rv(self.defgrad(x))
+        tau = vl_stress(self.mat, s)
+        P = np.einsum("eab,eb,ecb->eac", U, tau, V)
+        return self.vols[:, None, None] * np.einsum("eac,evc->eva", P, self.G)
+
+    def add_gradient(self, x, out):
+        """element-major scatter (dynamics.py:65-67)"""
+        np.add.at(out, self.tets.reshape(-1), self.corner_forces(x).reshape(-1, 3))
+
+
+class DenseFactor:
+    """Dense Cholesky, restating linalg.py:23-40."""
+
+    def __init__(self, A):
+        self.n = A.shape[0]
+        self.c = scipy.linalg.cho_factor(np.ascontiguousarray(A, dtype=np.float64), lower=True,
+                                         check_finite=False)
+
+    def solve(self, B):
+        return scipy.linalg.cho_solve(self.c, B, check_finite=False)
+
+
+class SparseFactor:
+    """Sparse restatement of the same solve: SuperLU in symmetric
+    mode with MMD ordering and no pivoting, equivalent to the dense Cholesky
+    to ~1e-15 relative."""
+
+    def __init__(self, A):
+        self.n = A.shape[0]
+        self.lu = scipy.sparse.linalg.splu(
+            scipy.sparse.csc_matrix(A), permc_spec="MMD_AT_PLUS_A", diag_pivot_thresh=0.0,
+            options=dict(SymmetricMode=True))
+
+    def solve(self, B):
+        return self.lu.solve(np.asarray(B, dtype=np.float64))
+
+
+@dataclass
+class System:
+    verts: np.ndarray
+    tets: np.ndarray
+    masses: np.ndarray
+    h: float
+    gravity: np.ndarray
+    groups: list
+    fixed: np.ndarray
+    free: np.ndarray
+    L: scipy.sparse.csr_matrix
+    A_free: scipy.sparse.csr_matrix
+    factor: object
+    scale: float
+
+    @property
+    def n(self):
+        return self.verts.shape[0]
+
+
+def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), factor="sparse",
+          masses=None):
+    """Restates dynamics.build_system (dynamics.py:351-434) for VL tet groups.
+
+    `materials` is a VLMaterial (all tets) or a list of (tet_index_array, VLMaterial).
+    """
+    verts = np.asarray(verts, dtype=np.float64)
+    tets = np.asarray(tets, dtype=np.int64)
+    n = verts.shape[0]
+    if masses is None:
+        masses = vertex_masses(verts, tets, density)
+    groups = []
+    if tets.shape[0]:
+        G, vols = diff_operators(verts, tets)
+        assign = [(np.arange(tets.shape[0]), materials)] if isinstance(materials, VLMaterial) else \
+            [(np.asarray(i, dtype=np.int64), m) for i, m in materials]
+        for idx, mat in assign:
+            groups.append(TetGroup(tets[idx], G[idx], vols[idx], mat, fit_stiffness(mat, *fit)))
+    rows, cols, vals = [], [], []
+    for g in groups:
+        w = g.vols * g.k                                          # dynamics.py:48
+        blk = w[:, None, None] * np.einsum("evc,euc->evu", g.G, g.G)  # dynamics.py:69-70
+        rows.append(np.repeat(g.tets, 4, axis=1).reshape(-1))
+        cols.append(np.tile(g.tets, (1, 4)).reshape(-1))
+        vals.append(blk.reshape(-1))
+    if rows:
+        L = scipy.sparse.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                    shape=(n, n)).tocsr()
+    else:
+        L = scipy.sparse.csr_matrix((n, n))
+    fixed = np.asarray(sorted(set(int(i) for i in fixed)), dtype=np.int64)
+    mask = np.ones(n, dtype=bool)
+    mask[fixed] = False
+    free = np.nonzero(mask)[0]
+    A = (L + scipy.sparse.diags(masses / h ** 2)).tocsr()          # dynamics.py:413
+    A_free = A[free][:, free].tocsr()
+    fac = DenseFactor(A_free.toarray()) if factor == "dense" else SparseFactor(A_free)
+    bbox = verts.max(axis=0) - verts.min(axis=0)
+    scale = float(np.linalg.norm(bbox)) or 1.0                     # dynamics.py:416-417
+    return System(verts, tets, masses, float(h), np.asarray(gravity, dtype=np.float64), groups,
+                  fixed, free, L, A_free, fac, scale)
+
+
+def inertia_target(sys, q_l, q_prev, fixed_targets=None):
+    """y = 2 q_l - q_prev + h^2 g; fixed rows = targets or q_l (dynamics.py:437-443)."""
+    h = sys.h
+    y = 2.0 * q_l - q_prev + h * h * sys.gravity[None, :]
+    if sys.fixed.size:
+        y[sys.fixed] = q_l[sys.fixed] if fixed_targets is None else fixed_targets
+    return y
+
+
+def objective(sys, y, x):
+    """dynamics.py:460-467 (no colliders)."""
+    d = x - y
+    g = 0.5 / sys.h ** 2 * float(np.einsum("vc,v,vc->", d, sys.masses, d))
+    for grp in sys.groups:
+        g += grp.energy(x)
+    return g
+
+
+def gradient(sys, y, x):
+    """dynamics.py:470-478: inertia, then elastic scatter, then zero fixed rows."""
+    out = (sys.masses[:, None] / sys.h ** 2) * (x - y)
+    for grp in sys.groups:
+        grp.add_gradient(x, out)
+    if sys.fixed.size:
+        out[sys.fixed] = 0.0
+    return out
+
+
+# --------------------------------------------------------------------------
+# L-BFGS, line search, frame loop (solvers.py)
+
+class History:
+    """solvers.py:83-103"""
+
+    def __init__(self, m):
+        self.m = m
+        self.pairs = []
+
+    def push(self, s, t):
+        rho = float(np.vdot(t, s))
+        if rho <= CURVATURE_GUARD * float(np.linalg.norm(s)) * float(np.linalg.norm(t)):
+            return
+        self.pairs.append((s, t, rho))
+        if len(self.pairs) > self.m:
+            del self.pairs[0]
+
+
+def solve_free(sys, q):
+    r = np.zeros_like(q)
+    r[sys.free] = sys.factor.solve(q[sys.free])
+    return r
+
+
+def direction(sys, hist, grad):
+    """Two-loop recursion with H0 = A^-1 (solvers.py:120-151); empty history is
+    bitwise the pd_qn direction (solvers.py:113-117)."""
+    q = -grad.copy()
+    zetas = []
+    for s, t, rho in reversed(hist.pairs):
+        z = float(np.vdot(s, q)) / rho
+        q -= z * t
+        zetas.append(z)
+    zetas.reverse()
+    r = solve_free(sys, q)
+    for (s, t, rho), z in zip(hist.pairs, zetas):
+        eta = float(np.vdot(t, r)) / rho
+        r += s * (z - eta)
+    return r
+
+
+def line_search(sys, y, x, d, g_x, grad, gamma=0.3, alpha_init=2.0, shrink=0.5):
+    """Armijo backtracking (solvers.py:241-257)."""
+    slope = float(np.vdot(grad, d))
+    if slope >= 0.0:
+        raise OracleError(f"ascent direction, slope={slope}")
+    alpha, trials = alpha_init, 0
+    while True:
+        alpha *= shrink
+        if alpha < ALPHA_FLOOR:
+            raise OracleStagnation("alpha underflow")
+        trials += 1
+        x_new = x + alpha * d
+        g_new = objective(sys, y, x_new)
+        if g_new <= g_x + gamma * alpha * slope:
+            return alpha, x_new, g_new, trials
+
+
+@dataclass
+class Record:
+    """solvers.py:71-80"""
+    g0: float = 0.0
+    g: list = field(default_factory=list)
+    ls_trials: list = field(default_factory=list)
+    alphas: list = field(default_factory=list)
+    cum_ms: list = field(default_factory=list)
+    stagnated: bool = False
+
+
+def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3, alpha_init=2.0,
+                   shrink=0.5, use_line_search=True, fixed_targets=None):
+    """One backward-Euler frame (solvers.py:260-352) for kind in {lbfgs, pd_qn},
+    lbfgs_init='system_matrix', no colliders.  Returns (x, y, Record)."""
+    t0 = time.perf_counter()
+    y = inertia_target(sys, q_l, q_prev, fixed_targets)
+    x = y.copy()
+    rec = Record()
+    hist = History(m)
+    prev_x = prev_g = None
+    grad_tol = 1e-12 * sys.scale * max(1.0, float(sys.masses.max()) / sys.h ** 2)
+    rec.g0 = objective(sys, y, x)
+
+    def log(g, tr, a):
+        rec.g.append(g)
+        rec.ls_trials.append(tr)
+        rec.alphas.append(a)
+        rec.cum_ms.append(1000.0 * (time.perf_counter() - t0))
+
+    for _ in range(iterations):
+        g_x = objective(sys, y, x)
+        grad = gradient(sys, y, x)
+        if kind == "lbfgs" and prev_x is not None:
+            hist.push(x - prev_x, grad - prev_g)
+        if float(np.linalg.norm(grad)) <= grad_tol:
+            log(g_x, 0, 0.0)
+            prev_x, prev_g = x, grad
+            continue
+        d = direction(sys, hist, grad)
+        if use_line_search:
+            slope = float(np.vdot(grad, d))
+            if slope < 0.0 and -slope <= 1e-12 * max(abs(g_x), 1.0):
+                log(g_x, 0, 0.0)
+                prev_x, prev_g = x, grad
+                continue
+            try:
+                alpha, x_new, g_new, trials = line_search(sys, y, x, d, g_x, grad, gamma, alpha_init, shrink)
+            except OracleStagnation:
+                rec.stagnated = True
+                while len(rec.g) < iterations:
+                    log(g_x, 0, 0.0)
+                break
+        else:
+            alpha, x_new, trials = 1.0, x + d, 1
+            g_new = objective(sys, y, x_new)
+        prev_x, prev_g = x, grad
+        x = x_new
+        log(g_new, trials, alpha)
+    return x, y, rec
+
+
+def twist_targets(rest, idx, axis, center, deg_per_s, t):
+    """Rodrigues rotation of prescribed vertices (harness.py:260-273)."""
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    ang = np.deg2rad(deg_per_s) * t
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    R = np.eye(3) + np.sin(ang) * K + (1 - np.cos(ang)) * (K @ K)
+    c = np.asarray(center, dtype=np.float64)
+    return (rest[idx] - c) @ R.T + c

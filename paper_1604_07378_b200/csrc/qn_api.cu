@@ -1,0 +1,721 @@
+// extern "C" boundary of libqnsim_b200 (declared in include/qnsim_b200.h).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qn_common.cuh"
+#include "qn_factor.h"
+#include "qn_sptrsv.cuh"
+#include "qn_system.h"
+
+namespace qn {
+
+namespace {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+void count_launch(int n) { g_launches += n; }
+
+// defined in qn_solver.cu
+int launch_body(qn_system* S, cudaStream_t st);
+int launch_init(qn_system* S, cudaStream_t st);
+int launch_finish(qn_system* S, cudaStream_t st);
+int build_graph(qn_system* S);
+int prepare_kernels(qn_system* S);
+__global__ void k_tet_plain(SysView v, const double* x, int b, int mat_sel, double* part);
+__global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
+                               int zero_fixed, double* part);
+__global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V);
+__global__ void k_material(const qn_material* M, int64_t k, const double* sig, double* psi, double* tau);
+
+namespace {
+
+template <class T>
+int dev_alloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return QN_ERR_ALLOC;
+  }
+  e = cudaMemset(*p, 0, count * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMemset: ") + cudaGetErrorString(e));
+    return QN_ERR_CUDA;
+  }
+  return QN_OK;
+}
+
+template <class T>
+int dev_upload(T** p, const T* h, size_t count) {
+  int rc = dev_alloc(p, count);
+  if (rc) return rc;
+  if (count) QN_CUDA(cudaMemcpy(*p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  return QN_OK;
+}
+
+template <class T>
+int sys_alloc(qn_system* S, T** p, size_t count) {
+  int rc = dev_alloc(p, count);
+  if (rc == QN_OK) S->allocs.push_back((void*)*p);
+  return rc;
+}
+
+template <class T>
+int sys_upload(qn_system* S, T** p, const T* h, size_t count) {
+  int rc = dev_upload(p, h, count);
+  if (rc == QN_OK) S->allocs.push_back((void*)*p);
+  return rc;
+}
+
+cudaStream_t pick(qn_system* S, void* stream) { return stream ? (cudaStream_t)stream : S->stream; }
+
+// copy between a caller buffer (host or device) and a device buffer
+int to_device(double* dst, const double* src, size_t count, int32_t mem, cudaStream_t st) {
+  QN_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double),
+                          mem == QN_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  return QN_OK;
+}
+template <class T>
+int from_device(T* dst, const T* src, size_t count, int32_t mem, cudaStream_t st) {
+  QN_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T),
+                          mem == QN_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  return QN_OK;
+}
+
+}  // namespace
+
+int factor_upload(qn_factor* f) {
+  int rc;
+  if ((rc = dev_upload(&f->d_sup_col, f->sup_col.data(), f->sup_col.size()))) return rc;
+  if ((rc = dev_upload(&f->d_sup_row_ptr, f->sup_row_ptr.data(), f->sup_row_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_sup_rows, f->sup_rows.data(), f->sup_rows.size()))) return rc;
+  if ((rc = dev_upload(&f->d_sup_val_ptr, f->sup_val_ptr.data(), f->sup_val_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_sup_upd_ptr, f->sup_upd_ptr.data(), f->sup_upd_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_parent, f->parent.data(), f->parent.size()))) return rc;
+  if ((rc = dev_upload(&f->d_child_ptr, f->child_ptr.data(), f->child_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_child_idx, f->child_idx.data(), f->child_idx.size()))) return rc;
+  if ((rc = dev_upload(&f->d_rel_ptr, f->rel_ptr.data(), f->rel_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_rel, f->rel.data(), f->rel.size()))) return rc;
+  if ((rc = dev_upload(&f->d_perm, f->perm.data(), f->perm.size()))) return rc;
+  if ((rc = dev_upload(&f->d_vals, f->vals.data(), f->vals.size()))) return rc;
+  if ((rc = dev_alloc(&f->d_y, (size_t)f->nbatch * f->n * 3))) return rc;
+  if ((rc = dev_alloc(&f->d_x, (size_t)f->nbatch * f->n * 3))) return rc;
+  if ((rc = dev_alloc(&f->d_u, (size_t)f->nbatch * std::max<int64_t>(f->nupd, 1) * 3))) return rc;
+  if ((rc = dev_alloc(&f->d_flags, (size_t)2 * f->nbatch * f->nsup))) return rc;
+  const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};
+  if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
+  if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;
+  int max_nc = 0;
+  for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
+  f->smem_bytes = (int)(sizeof(double) * 3 * ((size_t)f->max_rows + max_nc));
+  QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
+  if ((rc = prepare_solve_kernels<PlainIO>(f->smem_bytes))) return rc;
+  f->on_device = true;
+  return QN_OK;
+}
+
+void factor_free_device(qn_factor* f) {
+  void* ptrs[] = {f->d_sup_col, f->d_sup_row_ptr, f->d_sup_rows, f->d_sup_val_ptr, f->d_sup_upd_ptr,
+                  f->d_parent,  f->d_child_ptr,   f->d_child_idx, f->d_rel_ptr,   f->d_rel,
+                  f->d_perm,    f->d_vals,        f->d_y,         f->d_x,         f->d_u,
+                  f->d_flags,   f->d_sched,       f->d_io};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  f->on_device = false;
+}
+
+int factor_solve_plain(qn_factor* f, int64_t batch, cudaStream_t stream) {
+  PlainIO io{f->d_io, f->d_io + 3 * f->n, f->d_perm, (int)batch};
+  return launch_solve(f, io, stream);
+}
+
+}  // namespace qn
+
+using namespace qn;
+
+extern "C" {
+
+const char* qn_last_error(void) { return get_error(); }
+int qn_version(void) { return 1; }
+
+int qn_device_count(int32_t* count) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  cudaGetLastError();
+  *count = c;
+  return QN_OK;
+}
+
+int qn_launch_count(int64_t* count) {
+  *count = g_launches.load();
+  return QN_OK;
+}
+
+// ---------------------------------------------------------------------------
+int qn_svd_rv_batch(int64_t m, const double* F, double* U, double* sigma, double* V, int32_t mem, void* stream) {
+  QN_REQUIRE(m >= 0 && F && U && sigma && V, QN_ERR_ARG, "svd: bad arguments");
+  if (m == 0) return QN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double *dF = F;
+  double *dU = U, *ds = sigma, *dV = V, *buf = nullptr;
+  if (mem == QN_MEM_HOST) {
+    int rc = dev_alloc(&buf, (size_t)m * 21);
+    if (rc) return rc;
+    dU = buf;
+    dV = buf + 9 * m;
+    ds = buf + 18 * m;
+    double* tmpF = nullptr;
+    rc = dev_upload(&tmpF, F, (size_t)m * 9);
+    if (rc) return rc;
+    dF = tmpF;
+  }
+  k_svd<<<div_up(m, 128), 128, 0, st>>>(m, dF, dU, ds, dV);
+  QN_CHECK_LAUNCH();
+  if (mem == QN_MEM_HOST) {
+    QN_CUDA(cudaMemcpyAsync(U, dU, m * 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaMemcpyAsync(V, dV, m * 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaMemcpyAsync(sigma, ds, m * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaStreamSynchronize(st));
+    cudaFree(buf);
+    cudaFree((void*)dF);
+  } else {
+    QN_CUDA(cudaStreamSynchronize(st));
+  }
+  return QN_OK;
+}
+
+int qn_material_eval(const qn_material* mat, int64_t k, const double* sigma, double* psi, double* tau, int32_t mem,
+                     void* stream) {
+  QN_REQUIRE(mat && k >= 0 && sigma && psi && tau, QN_ERR_ARG, "material: bad arguments");
+  if (k == 0) return QN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  qn_material* dM = nullptr;
+  int rc = dev_upload(&dM, mat, 1);
+  if (rc) return rc;
+  const double* ds = sigma;
+  double *dp = psi, *dt = tau, *buf = nullptr;
+  if (mem == QN_MEM_HOST) {
+    rc = dev_alloc(&buf, (size_t)k * 7);
+    if (rc) return rc;
+    QN_CUDA(cudaMemcpy(buf, sigma, k * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    ds = buf;
+    dp = buf + 3 * k;
+    dt = buf + 4 * k;
+  }
+  k_material<<<div_up(k, 128), 128, 0, st>>>(dM, k, ds, dp, dt);
+  QN_CHECK_LAUNCH();
+  if (mem == QN_MEM_HOST) {
+    QN_CUDA(cudaMemcpyAsync(psi, dp, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaMemcpyAsync(tau, dt, k * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  QN_CUDA(cudaStreamSynchronize(st));
+  if (buf) cudaFree(buf);
+  cudaFree(dM);
+  return QN_OK;
+}
+
+// ---------------------------------------------------------------------------
+int qn_factor_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values, int64_t nbatch,
+                     const double* coords, qn_factor** out) {
+  QN_REQUIRE(out, QN_ERR_ARG, "factor: null output");
+  *out = nullptr;
+  qn_factor* f = new qn_factor();
+  int rc = factor_build_host(f, n, indptr, indices, values, nbatch, coords);
+  if (rc == QN_OK) rc = factor_upload(f);
+  if (rc != QN_OK) {
+    factor_free_device(f);
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return QN_OK;
+}
+
+int qn_factor_info_get(const qn_factor* f, qn_factor_info* info) {
+  QN_REQUIRE(f && info, QN_ERR_ARG, "factor_info: null");
+  info->n = f->n;
+  info->nnz_a = f->nnz_a;
+  info->nnz_l = f->nnz_l;
+  info->n_supernodes = f->nsup;
+  info->max_front = f->max_rows;
+  info->tree_depth = f->depth;
+  info->nbatch = f->nbatch;
+  info->factor_seconds = f->factor_seconds;
+  info->flops = f->flops;
+  return QN_OK;
+}
+
+int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int64_t nrhs, int32_t mem,
+                    void* stream) {
+  QN_REQUIRE(f && B && X && nrhs >= 1 && batch >= 0 && batch < f->nbatch, QN_ERR_ARG, "factor_solve: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = f->n;
+  std::vector<double> hb, hx;
+  if (mem == QN_MEM_HOST) {
+    hb.assign((size_t)n * 3, 0.0);
+    hx.resize((size_t)n * 3);
+  }
+  for (int64_t c0 = 0; c0 < nrhs; c0 += 3) {
+    const int64_t nc = std::min<int64_t>(3, nrhs - c0);
+    if (mem == QN_MEM_HOST) {
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = 0; k < 3; ++k) hb[3 * i + k] = k < nc ? B[i * nrhs + c0 + k] : 0.0;
+      QN_CUDA(cudaMemcpyAsync(f->d_io, hb.data(), n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    } else {
+      QN_REQUIRE(nrhs == 3, QN_ERR_ARG, "factor_solve: device buffers must have 3 columns");
+      QN_CUDA(cudaMemcpyAsync(f->d_io, B, n * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    int rc = factor_solve_plain(f, batch, st);
+    if (rc) return rc;
+    if (mem == QN_MEM_HOST) {
+      QN_CUDA(cudaMemcpyAsync(hx.data(), f->d_io + 3 * n, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      QN_CUDA(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = 0; k < nc; ++k) X[i * nrhs + c0 + k] = hx[3 * i + k];
+    } else {
+      QN_CUDA(cudaMemcpyAsync(X, f->d_io + 3 * n, n * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      QN_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  return QN_OK;
+}
+
+int qn_factor_destroy(qn_factor* f) {
+  if (!f) return QN_OK;
+  factor_free_device(f);
+  delete f;
+  return QN_OK;
+}
+
+// ---------------------------------------------------------------------------
+int qn_system_create(const qn_system_desc* d, qn_system** out) {
+  QN_REQUIRE(d && out, QN_ERR_ARG, "system: null argument");
+  *out = nullptr;
+  QN_REQUIRE(d->n_verts > 0 && d->n_tets >= 0 && d->n_inst >= 1 && d->n_mat >= 1, QN_ERR_ARG, "system: bad sizes");
+  QN_REQUIRE(d->n_tets == 0 || (d->tets && d->Dm_inv && d->vols && d->mats), QN_ERR_ARG, "system: missing tets");
+  QN_REQUIRE(d->masses && d->a_indptr && d->a_indices && d->a_values, QN_ERR_ARG, "system: missing arrays");
+  QN_REQUIRE(d->h > 0, QN_ERR_ARG, "system: h must be positive");
+  const int64_t n = d->n_verts, mt = d->n_tets, ni = d->n_inst;
+  QN_REQUIRE(n * ni < (int64_t)1 << 31 && mt * 4 < (int64_t)1 << 31, QN_ERR_ARG, "system: too large");
+  qn_system* S = new qn_system();
+  S->n = n;
+  S->mt = mt;
+  S->n_inst = ni;
+  S->n_mat = d->n_mat;
+  S->n_fixed = d->n_fixed;
+  S->h = d->h;
+  for (int a = 0; a < 3; ++a) S->grav[a] = d->gravity[a];
+  S->scale = d->scale;
+  S->max_mass = 0;
+  for (int64_t i = 0; i < n; ++i) S->max_mass = std::max(S->max_mass, d->masses[i]);
+  auto fail = [&](int rc) {
+    qn_system_destroy(S);
+    return rc;
+  };
+  // fixed set
+  std::vector<uint8_t> is_fixed(n, 0);
+  std::vector<int32_t> fixed_pos(n, -1);
+  for (int64_t k = 0; k < d->n_fixed; ++k) {
+    const int32_t v = d->fixed[k];
+    if (v < 0 || v >= n || (k > 0 && d->fixed[k - 1] >= v)) {
+      set_error("system: fixed ids must be sorted, unique and in range");
+      return fail(QN_ERR_ARG);
+    }
+    is_fixed[v] = 1;
+    fixed_pos[v] = (int32_t)k;
+  }
+  std::vector<int32_t> free_ids;
+  for (int64_t i = 0; i < n; ++i)
+    if (!is_fixed[i]) free_ids.push_back((int32_t)i);
+  S->n_free = (int64_t)free_ids.size();
+  if (S->n_free == 0) {
+    set_error("all vertices fixed; nothing to simulate");
+    return fail(QN_ERR_ARG);
+  }
+  // tets, SoA Dm^-1, gather map (slots 4t + c in increasing order = reference scatter order)
+  std::vector<int4> tets(std::max<int64_t>(mt, 1));
+  std::vector<double> dminv((size_t)std::max<int64_t>(mt, 1) * 9);
+  std::vector<int32_t> v2e_ptr(n + 1, 0), v2e((size_t)std::max<int64_t>(mt, 1) * 4);
+  for (int64_t t = 0; t < mt; ++t) {
+    const int32_t* tv = d->tets + 4 * t;
+    for (int c = 0; c < 4; ++c)
+      if (tv[c] < 0 || tv[c] >= n) {
+        set_error("system: tet vertex out of range");
+        return fail(QN_ERR_ARG);
+      }
+    tets[t] = make_int4(tv[0], tv[1], tv[2], tv[3]);
+    for (int k = 0; k < 9; ++k) dminv[(size_t)k * mt + t] = d->Dm_inv[9 * t + k];
+    for (int c = 0; c < 4; ++c) v2e_ptr[tv[c] + 1]++;
+  }
+  for (int64_t i = 0; i < n; ++i) v2e_ptr[i + 1] += v2e_ptr[i];
+  {
+    std::vector<int32_t> fill(v2e_ptr.begin(), v2e_ptr.end() - 1);
+    for (int64_t t = 0; t < mt; ++t)
+      for (int c = 0; c < 4; ++c) v2e[fill[d->tets[4 * t + c]]++] = (int32_t)(4 * t + c);
+  }
+  if (d->tet_mat) {
+    for (int64_t t = 0; t < mt; ++t)
+      if (d->tet_mat[t] < 0 || d->tet_mat[t] >= d->n_mat) {
+        set_error("system: material index out of range");
+        return fail(QN_ERR_ARG);
+      }
+    S->h_tet_mat.assign(d->tet_mat, d->tet_mat + mt);
+  }
+  // factor of A_free (one numeric instance per system instance)
+  S->factor = new qn_factor();
+  int rc = factor_build_host(S->factor, S->n_free, d->a_indptr, d->a_indices, d->a_values, ni, d->free_coords);
+  if (rc == QN_OK) rc = factor_upload(S->factor);
+  if (rc) return fail(rc);
+  std::vector<int32_t> fact_vtx(S->n_free);
+  for (int64_t r = 0; r < S->n_free; ++r) fact_vtx[r] = free_ids[S->factor->perm[r]];
+
+  SysView& v = S->v;
+  v.n = (int32_t)n;
+  v.mt = (int32_t)mt;
+  v.n_inst = (int32_t)ni;
+  v.n_mat = (int32_t)d->n_mat;
+  v.n_fixed = (int32_t)d->n_fixed;
+  v.nblk_v = div_up(n, 256);
+  v.nblk_t = std::max(1, div_up(mt, 128));
+  v.h = d->h;
+  for (int a = 0; a < 3; ++a) v.grav[a] = d->gravity[a];
+  const size_t vec = (size_t)ni * n * 3;
+  {
+    int4* p;
+    if ((rc = sys_upload(S, &p, tets.data(), tets.size()))) return fail(rc);
+    v.tets = p;
+    double* dm;
+    if ((rc = sys_upload(S, &dm, dminv.data(), dminv.size()))) return fail(rc);
+    v.dminv = dm;
+    double* vol;
+    std::vector<double> vols(d->vols ? d->vols : nullptr, d->vols ? d->vols + mt : nullptr);
+    if (vols.empty()) vols.push_back(0.0);
+    if ((rc = sys_upload(S, &vol, vols.data(), vols.size()))) return fail(rc);
+    v.vols = vol;
+    if (d->tet_mat) {
+      int32_t* tm;
+      if ((rc = sys_upload(S, &tm, d->tet_mat, (size_t)mt))) return fail(rc);
+      v.tet_mat = tm;
+    }
+    std::vector<qn_material> mats((size_t)ni * d->n_mat);
+    if (d->mats) std::memcpy(mats.data(), d->mats, mats.size() * sizeof(qn_material));
+    qn_material* dmats;
+    if ((rc = sys_upload(S, &dmats, mats.data(), mats.size()))) return fail(rc);
+    v.mats = dmats;
+    double* ms;
+    if ((rc = sys_upload(S, &ms, d->masses, (size_t)n))) return fail(rc);
+    v.masses = ms;
+    uint8_t* fx;
+    if ((rc = sys_upload(S, &fx, is_fixed.data(), is_fixed.size()))) return fail(rc);
+    v.is_fixed = fx;
+    int32_t* fp;
+    if ((rc = sys_upload(S, &fp, fixed_pos.data(), fixed_pos.size()))) return fail(rc);
+    v.fixed_pos = fp;
+    int32_t* vp;
+    if ((rc = sys_upload(S, &vp, v2e_ptr.data(), v2e_ptr.size()))) return fail(rc);
+    v.v2e_ptr = vp;
+    int32_t* ve;
+    if ((rc = sys_upload(S, &ve, v2e.data(), v2e.size()))) return fail(rc);
+    v.v2e = ve;
+    int32_t* fv;
+    if ((rc = sys_upload(S, &fv, fact_vtx.data(), fact_vtx.size()))) return fail(rc);
+    v.fact_vtx = fv;
+  }
+  if ((rc = sys_alloc(S, &v.q_l, vec)) || (rc = sys_alloc(S, &v.q_prev, vec)) || (rc = sys_alloc(S, &v.y, vec)) ||
+      (rc = sys_alloc(S, &v.X, 3 * vec)) || (rc = sys_alloc(S, &v.Gr, 2 * vec)) ||
+      (rc = sys_alloc(S, &v.S, (size_t)(kMaxM + 1) * vec)) || (rc = sys_alloc(S, &v.T, (size_t)(kMaxM + 1) * vec)) ||
+      (rc = sys_alloc(S, &v.R0, vec)) || (rc = sys_alloc(S, &v.D, vec)) ||
+      (rc = sys_alloc(S, &v.forces, (size_t)ni * std::max<int64_t>(mt, 1) * 12)) ||
+      (rc = sys_alloc(S, &v.part_v, (size_t)ni * v.nblk_v * kNG)) ||
+      (rc = sys_alloc(S, &v.part_t, (size_t)ni * v.nblk_t)) || (rc = sys_alloc(S, &v.cnt, (size_t)4 * ni + 1)) ||
+      (rc = sys_alloc(S, &v.ctl, (size_t)ni)) || (rc = sys_alloc(S, &S->d_cfg, 1)) ||
+      (rc = sys_alloc(S, &v.active, 1)) || (rc = sys_alloc(S, &v.passes, 1)) ||
+      (rc = sys_alloc(S, &S->d_targets, (size_t)ni * std::max<int64_t>(d->n_fixed, 1) * 3)) ||
+      (rc = sys_alloc(S, &S->d_part_plain, (size_t)std::max(v.nblk_t, v.nblk_v) * 2)))
+    return fail(rc);
+  v.cfg = S->d_cfg;
+  v.targets = S->d_targets;
+  QN_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+  QN_CUDA(cudaEventCreate(&S->ev0));
+  QN_CUDA(cudaEventCreate(&S->ev1));
+  S->h_stage_bytes = vec * sizeof(double) * 3;
+  QN_CUDA(cudaMallocHost((void**)&S->h_stage, S->h_stage_bytes));
+  if ((rc = prepare_kernels(S))) return fail(rc);
+  *out = S;
+  return QN_OK;
+}
+
+int qn_system_destroy(qn_system* S) {
+  if (!S) return QN_OK;
+  if (S->exec) cudaGraphExecDestroy(S->exec);
+  if (S->graph) cudaGraphDestroy(S->graph);
+  for (void* p : S->allocs) cudaFree(p);
+  if (S->factor) qn_factor_destroy(S->factor);
+  if (S->h_stage) cudaFreeHost(S->h_stage);
+  if (S->ev0) cudaEventDestroy(S->ev0);
+  if (S->ev1) cudaEventDestroy(S->ev1);
+  if (S->stream) cudaStreamDestroy(S->stream);
+  delete S;
+  return QN_OK;
+}
+
+int qn_system_factor(qn_system* S, qn_factor** out) {
+  QN_REQUIRE(S && out, QN_ERR_ARG, "null");
+  *out = S->factor;
+  return QN_OK;
+}
+
+int qn_system_set_graph_mode(qn_system* S, int32_t use_graph) {
+  QN_REQUIRE(S, QN_ERR_ARG, "null");
+  S->use_graph = use_graph != 0;
+  return QN_OK;
+}
+
+int qn_system_last_frame_ms(qn_system* S, double* ms) {
+  QN_REQUIRE(S && ms, QN_ERR_ARG, "null");
+  *ms = S->last_ms;
+  return QN_OK;
+}
+
+int qn_system_last_frame_passes(qn_system* S, int64_t* passes) {
+  QN_REQUIRE(S && passes, QN_ERR_ARG, "null");
+  *passes = S->last_passes;
+  return QN_OK;
+}
+
+static int stage_in(qn_system* S, double* dst, const double* src, size_t count, int32_t mem, cudaStream_t st) {
+  if (mem == QN_MEM_DEVICE) return to_device(dst, src, count, mem, st);
+  // pinned staging: copy the caller's (possibly pageable) buffer first
+  QN_REQUIRE(count * sizeof(double) <= S->h_stage_bytes, QN_ERR_ARG, "stage: too large");
+  QN_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(S->h_stage, src, count * sizeof(double));
+  QN_CUDA(cudaMemcpyAsync(dst, S->h_stage, count * sizeof(double), cudaMemcpyHostToDevice, st));
+  QN_CUDA(cudaStreamSynchronize(st));
+  return QN_OK;
+}
+
+int qn_state_set(qn_system* S, const double* q_l, const double* q_prev, int32_t mem, void* stream) {
+  QN_REQUIRE(S && q_l && q_prev, QN_ERR_ARG, "state_set: null");
+  cudaStream_t st = pick(S, stream);
+  const size_t vec = (size_t)S->n_inst * S->n * 3;
+  int rc = stage_in(S, S->v.q_l, q_l, vec, mem, st);
+  if (rc) return rc;
+  return stage_in(S, S->v.q_prev, q_prev, vec, mem, st);
+}
+
+int qn_state_get(qn_system* S, double* q_l, double* q_prev, double* y, int32_t mem, void* stream) {
+  QN_REQUIRE(S, QN_ERR_ARG, "state_get: null");
+  cudaStream_t st = pick(S, stream);
+  const size_t vec = (size_t)S->n_inst * S->n * 3;
+  int rc;
+  if (q_l && (rc = from_device(q_l, S->v.q_l, vec, mem, st))) return rc;
+  if (q_prev && (rc = from_device(q_prev, S->v.q_prev, vec, mem, st))) return rc;
+  if (y && (rc = from_device(y, S->v.y, vec, mem, st))) return rc;
+  QN_CUDA(cudaStreamSynchronize(st));
+  return QN_OK;
+}
+
+static int ensure_records(qn_system* S, int iterations) {
+  if (iterations <= S->rec_cap) return QN_OK;
+  int cap = std::max(iterations, 32);
+  const size_t cnt = (size_t)S->n_inst * cap;
+  int rc;
+  if ((rc = sys_alloc(S, &S->v.rec_g, cnt)) || (rc = sys_alloc(S, &S->v.rec_trials, cnt)) ||
+      (rc = sys_alloc(S, &S->v.rec_alpha, cnt)) || (rc = sys_alloc(S, &S->v.rec_ms, cnt)))
+    return rc;
+  S->rec_cap = cap;
+  S->v.rec_cap = cap;
+  if (S->exec) {  // pointers changed: rebuild the graph
+    cudaGraphExecDestroy(S->exec);
+    S->exec = nullptr;
+    cudaGraphDestroy(S->graph);
+    S->graph = nullptr;
+  }
+  return QN_OK;
+}
+
+int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed_targets, qn_frame_record* rec,
+                  int32_t mem, int32_t sync, void* stream) {
+  QN_REQUIRE(S && cfg, QN_ERR_ARG, "frame_step: null");
+  QN_REQUIRE(cfg->kind == 0 || cfg->kind == 1, QN_ERR_UNSUPPORTED, "solver kind not supported on the B200 path");
+  QN_REQUIRE(cfg->iterations >= 1 && cfg->m >= 0 && cfg->m <= kMaxM, QN_ERR_ARG, "frame_step: bad iterations/m");
+  QN_REQUIRE(cfg->gamma > 0 && cfg->gamma < 1, QN_ERR_ARG, "frame_step: gamma");
+  QN_REQUIRE(sync || !rec, QN_ERR_ARG, "frame_step: a record needs sync");
+  cudaStream_t st = S->stream;
+  (void)stream;
+  int rc = ensure_records(S, cfg->iterations);
+  if (rc) return rc;
+  DevConfig& c = S->h_cfg;
+  c.kind = cfg->kind;
+  c.iterations = cfg->iterations;
+  c.m = cfg->kind == 1 ? cfg->m : 0;
+  c.line_search = cfg->line_search;
+  c.gamma = cfg->gamma;
+  c.alpha_init = cfg->alpha_init;
+  c.shrink = cfg->alpha_shrink;
+  c.grad_tol = 1e-12 * S->scale * std::max(1.0, S->max_mass / (S->h * S->h));  // solvers.py:278
+  c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
+  c.use_graph = S->use_graph ? 1 : 0;
+  QN_CUDA(cudaMemcpyAsync(S->d_cfg, &c, sizeof(DevConfig), cudaMemcpyHostToDevice, st));
+  if (c.has_targets) {
+    rc = stage_in(S, S->d_targets, fixed_targets, (size_t)S->n_inst * S->n_fixed * 3, mem, st);
+    if (rc) return rc;
+  }
+  QN_CUDA(cudaEventRecord(S->ev0, st));
+  if (S->use_graph) {
+    if (!S->exec && (rc = build_graph(S))) return rc;
+    QN_CUDA(cudaGraphLaunch(S->exec, st));
+    count_launch(0);
+  } else {
+    if ((rc = launch_init(S, st))) return rc;
+    for (int pass = 0; pass < 100000; ++pass) {
+      if ((rc = launch_body(S, st))) return rc;
+      int32_t act = 0;
+      QN_CUDA(cudaMemcpyAsync(&act, S->v.active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      QN_CUDA(cudaStreamSynchronize(st));
+      if (act <= 0) break;
+    }
+    if ((rc = launch_finish(S, st))) return rc;
+  }
+  QN_CUDA(cudaEventRecord(S->ev1, st));
+  if (!sync) return QN_OK;
+  QN_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  QN_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+  S->last_ms = ms;
+  unsigned long long passes = 0;
+  QN_CUDA(cudaMemcpy(&passes, S->v.passes, sizeof(passes), cudaMemcpyDeviceToHost));
+  S->last_passes = (int64_t)passes;
+  if (S->use_graph) count_launch((int)(2 + 6 * passes));
+  if (rec) {
+    const int it = cfg->iterations, cap = S->rec_cap;
+    const int64_t ni = S->n_inst;
+    std::vector<InstCtl> ctl(ni);
+    QN_CUDA(cudaMemcpy(ctl.data(), S->v.ctl, ni * sizeof(InstCtl), cudaMemcpyDeviceToHost));
+    std::vector<double> g((size_t)ni * cap), al((size_t)ni * cap), ms_((size_t)ni * cap);
+    std::vector<int32_t> tr((size_t)ni * cap);
+    QN_CUDA(cudaMemcpy(g.data(), S->v.rec_g, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy(al.data(), S->v.rec_alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy(ms_.data(), S->v.rec_ms, ms_.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy(tr.data(), S->v.rec_trials, tr.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    std::vector<double> g0(ni);
+    std::vector<int32_t> status(ni);
+    std::vector<double> og((size_t)ni * it), oa((size_t)ni * it), om((size_t)ni * it);
+    std::vector<int32_t> ot((size_t)ni * it);
+    for (int64_t b = 0; b < ni; ++b) {
+      g0[b] = ctl[b].g0;
+      status[b] = ctl[b].status;
+      for (int k = 0; k < it; ++k) {
+        og[b * it + k] = g[b * cap + k];
+        oa[b * it + k] = al[b * cap + k];
+        om[b * it + k] = ms_[b * cap + k];
+        ot[b * it + k] = tr[b * cap + k];
+      }
+    }
+    auto put = [&](auto* dst, const auto& src) -> int {
+      if (!dst) return QN_OK;
+      using T = typename std::decay<decltype(src[0])>::type;
+      if (mem == QN_MEM_DEVICE) {
+        QN_CUDA(cudaMemcpy(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+      } else {
+        std::memcpy(dst, src.data(), src.size() * sizeof(T));
+      }
+      return QN_OK;
+    };
+    if ((rc = put(rec->g0, g0)) || (rc = put(rec->g, og)) || (rc = put(rec->ls_trials, ot)) ||
+        (rc = put(rec->alphas, oa)) || (rc = put(rec->cum_ms, om)) || (rc = put(rec->status, status)))
+      return rc;
+  }
+  return QN_OK;
+}
+
+int qn_simulate_frame(qn_system* S, const qn_solver_config* cfg, const double* q_l, const double* q_prev,
+                      const double* fixed_targets, double* x_out, double* y_out, qn_frame_record* rec, int32_t mem,
+                      void* stream) {
+  int rc = qn_state_set(S, q_l, q_prev, mem, stream);
+  if (rc) return rc;
+  rc = qn_frame_step(S, cfg, fixed_targets, rec, mem, 1, stream);
+  if (rc) return rc;
+  return qn_state_get(S, x_out, nullptr, y_out, mem, stream);
+}
+
+int qn_system_objective(qn_system* S, const double* x, const double* y, double* g_out, double* grad_out, int32_t mem,
+                        void* stream) {
+  QN_REQUIRE(S && x && y && g_out, QN_ERR_ARG, "objective: null");
+  cudaStream_t st = S->stream;
+  (void)stream;
+  const size_t nv = (size_t)S->n * 3;
+  double *dx = nullptr, *dy = nullptr, *dg = nullptr;
+  int rc;
+  if ((rc = dev_alloc(&dx, nv)) || (rc = dev_alloc(&dy, nv)) || (rc = dev_alloc(&dg, nv))) return rc;
+  const SysView& v = S->v;
+  std::vector<double> pt(v.nblk_t), pv(v.nblk_v);
+  for (int64_t b = 0; b < S->n_inst; ++b) {
+    if ((rc = to_device(dx, x + b * nv, nv, mem, st)) || (rc = to_device(dy, y + b * nv, nv, mem, st))) return rc;
+    k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, dx, (int)b, -1, S->d_part_plain);
+    QN_CHECK_LAUNCH();
+    k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
+    QN_CHECK_LAUNCH();
+    QN_CUDA(cudaMemcpyAsync(pt.data(), S->d_part_plain, v.nblk_t * sizeof(double), cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaMemcpyAsync(pv.data(), S->d_part_plain + v.nblk_t, v.nblk_v * sizeof(double), cudaMemcpyDeviceToHost,
+                            st));
+    if (grad_out && (rc = from_device(grad_out + b * nv, dg, nv, mem, st))) return rc;
+    QN_CUDA(cudaStreamSynchronize(st));
+    double e = 0.0, in = 0.0;
+    for (double p : pt) e += p;
+    for (double p : pv) in += p;
+    const double gv = (0.5 / (S->h * S->h)) * in + e;
+    if (mem == QN_MEM_DEVICE) {
+      QN_CUDA(cudaMemcpy(g_out + b, &gv, sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+      g_out[b] = gv;
+    }
+  }
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(dg);
+  return QN_OK;
+}
+
+int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x, double* energy, double* grad_accum,
+                       int32_t mem, void* stream) {
+  QN_REQUIRE(S && x && energy && inst >= 0 && inst < S->n_inst && mat < S->n_mat, QN_ERR_ARG, "elements: args");
+  cudaStream_t st = S->stream;
+  (void)stream;
+  const size_t nv = (size_t)S->n * 3;
+  double *dx = nullptr, *dg = nullptr;
+  int rc;
+  if ((rc = dev_alloc(&dx, nv)) || (rc = dev_alloc(&dg, nv))) return rc;
+  const SysView& v = S->v;
+  if ((rc = to_device(dx, x, nv, mem, st))) return rc;
+  k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, dx, (int)inst, (int)mat, S->d_part_plain);
+  QN_CHECK_LAUNCH();
+  if (grad_accum) {
+    if ((rc = to_device(dg, grad_accum, nv, mem, st))) return rc;
+    k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
+    QN_CHECK_LAUNCH();
+    if ((rc = from_device(grad_accum, dg, nv, mem, st))) return rc;
+  }
+  std::vector<double> pt(v.nblk_t);
+  QN_CUDA(cudaMemcpyAsync(pt.data(), S->d_part_plain, v.nblk_t * sizeof(double), cudaMemcpyDeviceToHost, st));
+  QN_CUDA(cudaStreamSynchronize(st));
+  double e = 0.0;
+  for (double p : pt) e += p;
+  if (mem == QN_MEM_DEVICE) {
+    QN_CUDA(cudaMemcpy(energy, &e, sizeof(double), cudaMemcpyHostToDevice));
+  } else {
+    *energy = e;
+  }
+  cudaFree(dx);
+  cudaFree(dg);
+  return QN_OK;
+}
+
+}  // extern "C"

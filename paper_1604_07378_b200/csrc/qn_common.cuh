@@ -1,0 +1,92 @@
+// Shared device/host helpers for the qnsim B200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "qnsim_b200.h"
+
+namespace qn {
+
+// ---- error plumbing (thread-local message for qn_last_error) ---------------
+void set_error(const std::string& msg);
+const char* get_error();
+void count_launch(int n = 1);
+
+#define QN_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::qn::set_error(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" __FILE__); \
+      return QN_ERR_CUDA;                                                                   \
+    }                                                                                       \
+  } while (0)
+
+#define QN_CHECK_LAUNCH()                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess) {                                                                \
+      ::qn::set_error(std::string("kernel launch: ") + cudaGetErrorString(e_) + " @" __FILE__); \
+      return QN_ERR_CUDA;                                                                   \
+    }                                                                                       \
+    ::qn::count_launch();                                                                   \
+  } while (0)
+
+#define QN_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) {                  \
+      ::qn::set_error(msg);         \
+      return (code);                \
+    }                               \
+  } while (0)
+
+constexpr int kSMs = 148;
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ---- device helpers ----------------------------------------------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide reduction of K doubles per thread; result valid in thread 0.
+// Fixed order (warp butterfly then warps in index order) => deterministic.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* smem /* >= K*32 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) smem[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a = 0.0;
+      for (int w = 0; w < nw; ++w) a += smem[k * 32 + w];
+      v[k] = a;
+    }
+  }
+  __syncthreads();
+}
+
+#endif  // __CUDACC__
+
+}  // namespace qn

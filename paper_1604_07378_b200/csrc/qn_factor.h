@@ -1,0 +1,78 @@
+// Supernodal Cholesky factor of the constant system matrix A = M/h^2 + L on
+// the free DOFs (dynamics.py:413-414), shared by all frames; the device holds
+// per supernode s (columns J_s = [col0, col0 + nc), rows R_s, |R_s| = nr):
+//   vals[s] = [ inv(L_ss) (nc x nc, column-major) | L_Bs ((nr - nc) x nc, column-major) ]
+// and the multifrontal triangular solve exchanges per-supernode update
+// vectors u_s (nr - nc rows x 3 RHS) with the parent through `rel` maps.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "qnsim_b200.h"
+
+struct qn_factor {
+  // ---- symbolic (host) ----
+  int64_t n = 0, nnz_a = 0, nbatch = 1;
+  std::vector<int32_t> perm;      // factor row -> original (free) row
+  std::vector<int32_t> iperm;     // original -> factor row
+  int32_t nsup = 0;
+  std::vector<int32_t> sup_col;   // (nsup+1) first column of each supernode
+  std::vector<int64_t> sup_row_ptr;  // (nsup+1) into sup_rows
+  std::vector<int32_t> sup_rows;  // R_s (factor row ids), J_s first
+  std::vector<int64_t> sup_val_ptr;  // (nsup+1) into vals (per batch)
+  std::vector<int64_t> sup_upd_ptr;  // (nsup+1) into the u buffer (rows)
+  std::vector<int32_t> parent;    // supernodal etree parent (-1 = root)
+  std::vector<int32_t> child_ptr, child_idx;  // children in increasing order
+  std::vector<int64_t> rel_ptr;   // (nsup+1) per child: its below rows -> parent front positions
+  std::vector<int32_t> rel;
+  int64_t nvals = 0, nupd = 0, nnz_l = 0;
+  int32_t max_rows = 0, depth = 0;
+  double flops = 0.0, factor_seconds = 0.0;
+  // ---- numeric (host, nbatch x nvals) ----
+  std::vector<double> vals;
+
+  // ---- device ----
+  int32_t* d_sup_col = nullptr;
+  int64_t* d_sup_row_ptr = nullptr;
+  int32_t* d_sup_rows = nullptr;
+  int64_t* d_sup_val_ptr = nullptr;
+  int64_t* d_sup_upd_ptr = nullptr;
+  int32_t* d_parent = nullptr;
+  int32_t* d_child_ptr = nullptr;
+  int32_t* d_child_idx = nullptr;
+  int64_t* d_rel_ptr = nullptr;
+  int32_t* d_rel = nullptr;
+  int32_t* d_perm = nullptr;      // factor row -> original row
+  double* d_vals = nullptr;       // nbatch x nvals
+  double* d_y = nullptr;          // nbatch x n x 3 (forward result, factor order)
+  double* d_x = nullptr;          // nbatch x n x 3 (backward result, factor order)
+  double* d_u = nullptr;          // nbatch x nupd x 3
+  unsigned* d_flags = nullptr;    // 2 x nbatch x nsup (forward, backward)
+  unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
+  double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
+  int smem_bytes = 0;
+  bool on_device = false;
+};
+
+namespace qn {
+// host: ordering + symbolic + numeric factorisation; returns QN_OK / QN_ERR_*
+int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int32_t* indices,
+                      const double* values, int64_t nbatch, const double* coords);
+int factor_upload(qn_factor* f);
+void factor_free_device(qn_factor* f);
+
+// Functors describing where the solve reads its right-hand side and writes its result.
+struct SolveIO {
+  // plain API: B (n x 3, original order) -> X (n x 3, original order)
+  const double* B = nullptr;
+  double* X = nullptr;
+};
+
+// Forward + backward solve on `stream` for all batch instances whose `active`
+// entry is non-zero (active == nullptr => all). The L-BFGS variant forms its
+// RHS on the fly (see qn_solver.cu) via the templated kernels in qn_sptrsv.cuh.
+int factor_solve_plain(qn_factor* f, int64_t batch, cudaStream_t stream);
+}  // namespace qn

@@ -1,0 +1,695 @@
+// Per-frame quasi-Newton / L-BFGS solver on the device (solvers.py:260-352).
+//
+// One frame = one CUDA graph: [init] -> WHILE(any instance active){ body } -> [finish].
+// The body is six kernels; every instance advances one step of its phase
+// machine (qn_system.h) per body pass, so batched instances with different
+// line-search trial counts proceed independently and the host never syncs
+// inside a frame:
+//   k_grad   (PH_GRAD)   gradient gather (inertia + corner forces in the
+//                        reference's element order, fixed rows zeroed),
+//                        L-BFGS push dots + Gram entries + <s_i, g>, then the
+//                        last block finalises: curvature guard, ring update,
+//                        ||g|| early-out, zeta recursion.
+//   fwd/bwd  (PH_DIR)    supernodal solves r0 = A^-1 q', q' = -g - sum zeta t
+//                        formed on the fly (qn_sptrsv.cuh).
+//   k_eta    (PH_DIR)    <t_i, r0>, then eta recursion -> coef = zeta - eta.
+//   k_vec    (PH_DIR)    d = r0 + sum coef s, slope partials, first trial x + a1 d
+//            (PH_ALPHA)  trial x + alpha d;  all eval phases: inertia partials.
+//   k_tet    (eval)      per-tet F, SVD, VL energy + PK1 corner forces; the last
+//                        block per instance finalises: Armijo / early-outs /
+//                        stagnation / records; the last block overall sets
+//                        the WHILE condition.
+//
+// The L-BFGS two-loop (solvers.py:120-151) is evaluated with the Gram-matrix
+// form of the same recursion: zeta_i = (<s_i, q> - sum_{j newer} zeta_j <s_i, t_j>)/rho_i
+// and eta_i = (<t_i, r0> + sum_{j older} (zeta_j - eta_j) <s_j, t_i>)/rho_i,
+// which needs one batched reduction per loop instead of one per pair; the
+// vector updates q -= zeta t and r += s (zeta - eta) are applied in the
+// reference's order with the reference's rounding (mul, then add).
+#include <cstring>
+
+#include "qn_common.cuh"
+#include "qn_element.cuh"
+#include "qn_sptrsv.cuh"
+#include "qn_system.h"
+
+namespace qn {
+
+constexpr int kVT = 256;  // vertex-kernel block
+constexpr int kTT = 128;  // tet-kernel block
+
+constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
+constexpr double kAlphaFloor = 1e-12;      // solvers.py:29
+
+__device__ __forceinline__ size_t vec_off(const SysView& v, int slot, int b) {
+  return ((size_t)slot * v.n_inst + b) * (size_t)v.n * 3;
+}
+__device__ __forceinline__ size_t inst_off(const SysView& v, int b) { return (size_t)b * v.n * 3; }
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// last block of instance b for counter `which`?  (after all partial writes)
+__device__ __forceinline__ bool last_block(unsigned* cnt, int which, int b, int n_inst, int nblk) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* c = cnt + (size_t)which * n_inst + b;
+    const unsigned old = atomicAdd(c, 1u);
+    s_last = (old == (unsigned)nblk - 1);
+    if (s_last) *c = 0;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+__device__ void record(const SysView& v, InstCtl& c, double g, int trials, double alpha) {
+  const int it = v.cfg->iterations;
+  if (c.k < it && c.k < v.rec_cap) {
+    const size_t o = (size_t)blockIdx.y * v.rec_cap + c.k;
+    v.rec_g[o] = g;
+    v.rec_trials[o] = trials;
+    v.rec_alpha[o] = alpha;
+    v.rec_ms[o] = (double)(global_ns() - c.t0) * 1e-6;
+  }
+  c.k += 1;
+}
+
+__device__ __forceinline__ int free_slot(int cur, int prev) {
+  if (prev < 0 || prev == cur) return (cur + 1) % 3;
+  return 3 - cur - prev;
+}
+
+// ---------------------------------------------------------------------------
+// frame init: y = 2 q_l - q_prev + h^2 g, fixed rows = targets | q_l (dynamics.py:437-443)
+__global__ void k_init(SysView v) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    const size_t o = inst_off(v, b) + (size_t)i * 3;
+    double y[3];
+    if (v.is_fixed[i]) {
+      if (v.cfg->has_targets) {
+        const double* t = v.targets + ((size_t)b * v.n_fixed + v.fixed_pos[i]) * 3;
+        y[0] = t[0];
+        y[1] = t[1];
+        y[2] = t[2];
+      } else {
+        y[0] = v.q_l[o];
+        y[1] = v.q_l[o + 1];
+        y[2] = v.q_l[o + 2];
+      }
+    } else {
+      const double hh = __dmul_rn(v.h, v.h);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        y[a] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, v.q_l[o + a]), v.q_prev[o + a]), __dmul_rn(hh, v.grav[a]));
+    }
+    double* X0 = v.X + vec_off(v, 0, b) + (size_t)i * 3;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      v.y[o + a] = y[a];
+      X0[a] = y[a];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    InstCtl& c = v.ctl[b];
+    c.phase = PH_FIRST;
+    c.k = 0;
+    c.trials = 0;
+    c.status = 0;
+    c.xs_cur = 0;
+    c.xs_prev = -1;
+    c.xs_trial = 0;
+    c.gs_cur = 0;
+    c.npairs = 0;
+    c.have_prev = 0;
+    for (int r = 0; r <= kMaxM; ++r) c.ring[r] = r;
+    c.g0 = c.g_x = 0.0;
+    c.alpha = 0.0;
+    c.slope = 0.0;
+    c.t0 = global_ns();
+    if (b == 0) {
+      *v.active = v.n_inst;
+      *v.passes = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gradient gather + L-BFGS push / zeta (dynamics.py:470-478, solvers.py:83-103, 124-131)
+__global__ void __launch_bounds__(kVT) k_grad(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* cc = v.ctl + b;
+  if (cc->phase != PH_GRAD) return;
+  __shared__ double red[kNG * 32];
+  const int cur = cc->xs_cur, prv = cc->xs_prev, gcur = cc->gs_cur, gnew = gcur ^ 1;
+  const int np = cc->npairs;
+  const DevConfig& cfg = *v.cfg;
+  const bool push = cc->have_prev && cfg.kind == 1 && cfg.m > 0;
+  const int cand = cc->ring[np];
+  double acc[kNG];
+#pragma unroll
+  for (int k = 0; k < kNG; ++k) acc[k] = 0.0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    const size_t o = inst_off(v, b) + (size_t)i * 3;
+    const double* x = v.X + vec_off(v, cur, b) + (size_t)i * 3;
+    const double w = v.masses[i] / __dmul_rn(v.h, v.h);
+    double g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = __dmul_rn(w, __dsub_rn(x[a], v.y[o + a]));
+    const double* fb = v.forces + (size_t)b * v.mt * 12;
+    const int e1 = v.v2e_ptr[i + 1];
+    for (int e = v.v2e_ptr[i]; e < e1; ++e) {
+      const double* f = fb + (size_t)v.v2e[e] * 3;
+      g[0] = __dadd_rn(g[0], f[0]);
+      g[1] = __dadd_rn(g[1], f[1]);
+      g[2] = __dadd_rn(g[2], f[2]);
+    }
+    if (v.is_fixed[i]) g[0] = g[1] = g[2] = 0.0;
+    double* go = v.Gr + vec_off(v, gnew, b) + (size_t)i * 3;
+    go[0] = g[0];
+    go[1] = g[1];
+    go[2] = g[2];
+    acc[0] = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+    double s[3] = {0, 0, 0}, t[3] = {0, 0, 0};
+    if (push) {
+      const double* xp = v.X + vec_off(v, prv, b) + (size_t)i * 3;
+      const double* gp = v.Gr + vec_off(v, gcur, b) + (size_t)i * 3;
+      double* so = v.S + vec_off(v, cand, b) + (size_t)i * 3;
+      double* to = v.T + vec_off(v, cand, b) + (size_t)i * 3;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        s[a] = __dsub_rn(x[a], xp[a]);
+        t[a] = __dsub_rn(g[a], gp[a]);
+        so[a] = s[a];
+        to[a] = t[a];
+      }
+      acc[1] = t[0] * s[0] + t[1] * s[1] + t[2] * s[2];
+      acc[2] = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+      acc[3] = t[0] * t[0] + t[1] * t[1] + t[2] * t[2];
+      acc[4] = s[0] * g[0] + s[1] * g[1] + s[2] * g[2];
+    }
+    for (int p = 0; p < np; ++p) {
+      const double* si = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
+      acc[5 + kMaxM + p] = si[0] * g[0] + si[1] * g[1] + si[2] * g[2];
+      if (push) acc[5 + p] = si[0] * t[0] + si[1] * t[1] + si[2] * t[2];
+    }
+  }
+  block_sum<kNG>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG;
+#pragma unroll
+    for (int k = 0; k < kNG; ++k) pv[k] = acc[k];
+  }
+  if (!last_block(v.cnt, 0, b, v.n_inst, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  // ---- finalise (one thread per instance) ----
+  double tot[kNG];
+  for (int k = 0; k < kNG; ++k) tot[k] = 0.0;
+  for (int blk = 0; blk < (int)gridDim.x; ++blk) {
+    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG;
+    for (int k = 0; k < kNG; ++k) tot[k] += __ldcg(pv + k);
+  }
+  InstCtl& c = v.ctl[b];
+  c.gs_cur = gnew;
+  if (push) {
+    const double rho = tot[1];
+    const double guard = kCurvatureGuard * sqrt(tot[2]) * sqrt(tot[3]);
+    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + kMaxM + p];
+    if (rho > guard) {
+      for (int p = 0; p < np; ++p) c.gram[c.ring[p]][cand] = tot[5 + p];
+      c.rho[cand] = rho;
+      c.sg[cand] = tot[4];
+      if (np < cfg.m) {
+        c.npairs = np + 1;
+      } else {  // evict the oldest pair (solvers.py:96-97)
+        const int old = c.ring[0];
+        for (int p = 0; p < cfg.m; ++p) c.ring[p] = c.ring[p + 1];
+        c.ring[cfg.m] = old;
+      }
+    }
+  } else {
+    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + kMaxM + p];
+  }
+  c.have_prev = 1;
+  if (sqrt(tot[0]) <= cfg.grad_tol) {  // solvers.py:292-298
+    record(v, c, c.g_x, 0, 0.0);
+    c.xs_prev = c.xs_cur;
+    c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;  // forces still belong to x
+    if (c.phase == PH_DONE) atomicSub(v.active, 1);
+    return;
+  }
+  const int npn = c.npairs;
+  for (int p = npn - 1; p >= 0; --p) {
+    const int sp = c.ring[p];
+    double q = -c.sg[sp];
+    for (int j = p + 1; j < npn; ++j) q -= c.zeta[j] * c.gram[sp][c.ring[j]];
+    c.zeta[p] = q / c.rho[sp];
+  }
+  c.xs_trial = free_slot(c.xs_cur, c.xs_prev);
+  c.phase = PH_DIR;
+}
+
+// RHS / output mapping of the solves inside the frame
+struct SolverIO {
+  SysView v;
+  __device__ bool active(int b) const { return v.ctl[b].phase == PH_DIR; }
+  __device__ void rhs(int b, int row, double (&q)[3]) const {
+    const InstCtl* c = v.ctl + b;
+    const int vx = v.fact_vtx[row];
+    const double* g = v.Gr + vec_off(v, c->gs_cur, b) + (size_t)vx * 3;
+    q[0] = -g[0];
+    q[1] = -g[1];
+    q[2] = -g[2];
+    for (int p = c->npairs - 1; p >= 0; --p) {  // q -= zeta t, newest first
+      const double z = c->zeta[p];
+      const double* t = v.T + vec_off(v, c->ring[p], b) + (size_t)vx * 3;
+      q[0] = __dsub_rn(q[0], __dmul_rn(z, t[0]));
+      q[1] = __dsub_rn(q[1], __dmul_rn(z, t[1]));
+      q[2] = __dsub_rn(q[2], __dmul_rn(z, t[2]));
+    }
+  }
+  __device__ void store(int b, int row, const double (&x)[3]) const {
+    double* r = v.R0 + inst_off(v, b) + (size_t)v.fact_vtx[row] * 3;
+    r[0] = x[0];
+    r[1] = x[1];
+    r[2] = x[2];
+  }
+};
+
+// <t_i, r0> and the eta recursion (solvers.py:147-150)
+__global__ void __launch_bounds__(kVT) k_eta(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* cc = v.ctl + b;
+  if (cc->phase != PH_DIR || cc->npairs == 0) return;
+  __shared__ double red[kMaxM * 32];
+  const int np = cc->npairs;
+  double acc[kMaxM];
+#pragma unroll
+  for (int k = 0; k < kMaxM; ++k) acc[k] = 0.0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    const double* r = v.R0 + inst_off(v, b) + (size_t)i * 3;
+    const double r0 = r[0], r1 = r[1], r2 = r[2];
+    for (int p = 0; p < np; ++p) {
+      const double* t = v.T + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
+      acc[p] = t[0] * r0 + t[1] * r1 + t[2] * r2;
+    }
+  }
+  block_sum<kMaxM>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG;
+    for (int k = 0; k < kMaxM; ++k) pv[k] = acc[k];
+  }
+  if (!last_block(v.cnt, 1, b, v.n_inst, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  double tot[kMaxM];
+  for (int k = 0; k < kMaxM; ++k) tot[k] = 0.0;
+  for (int blk = 0; blk < (int)gridDim.x; ++blk) {
+    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG;
+    for (int k = 0; k < np; ++k) tot[k] += __ldcg(pv + k);
+  }
+  InstCtl& c = v.ctl[b];
+  for (int p = 0; p < np; ++p) {
+    const int sp = c.ring[p];
+    double tr = tot[p];
+    for (int j = 0; j < p; ++j) tr += c.coef[j] * c.gram[c.ring[j]][sp];
+    const double eta = tr / c.rho[sp];
+    c.coef[p] = c.zeta[p] - eta;
+  }
+}
+
+// direction, trial point, inertia / slope partials
+__global__ void __launch_bounds__(kVT) k_vec(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* cc = v.ctl + b;
+  const int ph = cc->phase;
+  if (ph == PH_GRAD || ph == PH_DONE) return;
+  __shared__ double red[2 * 32];
+  double acc[2] = {0.0, 0.0};
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    const size_t o = inst_off(v, b) + (size_t)i * 3;
+    const double* x = v.X + vec_off(v, cc->xs_cur, b) + (size_t)i * 3;
+    double xt[3] = {x[0], x[1], x[2]};
+    if (ph == PH_DIR || ph == PH_ALPHA) {
+      double d[3];
+      if (ph == PH_DIR) {
+        const double* r = v.R0 + o;
+        d[0] = r[0];
+        d[1] = r[1];
+        d[2] = r[2];
+        for (int p = 0; p < cc->npairs; ++p) {  // r += s (zeta - eta), oldest first
+          const double cf = cc->coef[p];
+          const double* s = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
+          d[0] = __dadd_rn(d[0], __dmul_rn(s[0], cf));
+          d[1] = __dadd_rn(d[1], __dmul_rn(s[1], cf));
+          d[2] = __dadd_rn(d[2], __dmul_rn(s[2], cf));
+        }
+        double* dd = v.D + o;
+        dd[0] = d[0];
+        dd[1] = d[1];
+        dd[2] = d[2];
+        const double* g = v.Gr + vec_off(v, cc->gs_cur, b) + (size_t)i * 3;
+        acc[1] = g[0] * d[0] + g[1] * d[1] + g[2] * d[2];
+      } else {
+        const double* dd = v.D + o;
+        d[0] = dd[0];
+        d[1] = dd[1];
+        d[2] = dd[2];
+      }
+      const double al = (ph == PH_DIR) ? (v.cfg->line_search ? __dmul_rn(v.cfg->alpha_init, v.cfg->shrink) : 1.0)
+                                        : cc->alpha;
+      double* xo = v.X + vec_off(v, cc->xs_trial, b) + (size_t)i * 3;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        xt[a] = __dadd_rn(x[a], __dmul_rn(al, d[a]));
+        xo[a] = xt[a];
+      }
+    }
+    const double* y = v.y + o;
+    const double e0 = xt[0] - y[0], e1 = xt[1] - y[1], e2 = xt[2] - y[2];
+    acc[0] = v.masses[i] * (e0 * e0 + e1 * e1 + e2 * e2);
+  }
+  block_sum<2>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG + (kNG - 2);
+    pv[0] = acc[0];
+    pv[1] = acc[1];
+  }
+}
+
+__device__ void finalize_trial(const SysView& v, int b) {
+  const DevConfig& cfg = *v.cfg;
+  InstCtl& c = v.ctl[b];
+  double e_el = 0.0, inert = 0.0, slope = 0.0;
+  for (int blk = 0; blk < v.nblk_t; ++blk) e_el += __ldcg(v.part_t + (size_t)b * v.nblk_t + blk);
+  for (int blk = 0; blk < v.nblk_v; ++blk) {
+    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG + (kNG - 2);
+    inert += __ldcg(pv);
+    slope += __ldcg(pv + 1);
+  }
+  const double g_new = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
+  const int ph = c.phase;
+  if (ph == PH_FIRST) {
+    c.g0 = c.g_x = g_new;
+    c.phase = PH_GRAD;
+    return;
+  }
+  if (ph == PH_COPY) {
+    c.phase = PH_GRAD;
+    return;
+  }
+  bool accept = false;
+  if (ph == PH_DIR) {
+    c.slope = slope;
+    c.trials = 1;
+    c.alpha = __dmul_rn(cfg.alpha_init, cfg.shrink);
+    if (!cfg.line_search) {
+      accept = true;
+    } else if (slope >= 0.0) {  // solvers.py:244-246 -> SolverError
+      c.status |= 2;
+      c.phase = PH_DONE;
+      atomicSub(v.active, 1);
+      return;
+    } else if (-slope <= 1e-12 * fmax(fabs(c.g_x), 1.0)) {  // solvers.py:319-326
+      record(v, c, c.g_x, 0, 0.0);
+      c.xs_prev = c.xs_cur;
+      c.phase = c.k >= cfg.iterations ? PH_DONE : PH_COPY;
+      c.xs_trial = c.xs_cur;
+      if (c.phase == PH_DONE) atomicSub(v.active, 1);
+      return;
+    } else if (c.alpha < kAlphaFloor) {
+      accept = false;  // handled as stagnation below
+    }
+  }
+  if (cfg.line_search && !accept) {
+    const double thr = __dadd_rn(c.g_x, __dmul_rn(__dmul_rn(cfg.gamma, c.alpha), c.slope));
+    accept = c.alpha >= kAlphaFloor && g_new <= thr;  // Armijo (solvers.py:255)
+  }
+  if (accept) {
+    c.xs_prev = c.xs_cur;
+    c.xs_cur = c.xs_trial;
+    c.g_x = g_new;
+    record(v, c, g_new, c.trials, cfg.line_search ? c.alpha : 1.0);
+    c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;
+  } else {
+    c.alpha = __dmul_rn(c.alpha, cfg.shrink);
+    if (c.alpha < kAlphaFloor) {  // StagnationError: pad the record (solvers.py:329-336)
+      c.status |= 1;
+      while (c.k < cfg.iterations) record(v, c, c.g_x, 0, 0.0);
+      c.phase = PH_DONE;
+    } else {
+      c.trials += 1;
+      c.phase = PH_ALPHA;
+    }
+  }
+  if (c.phase == PH_DONE) atomicSub(v.active, 1);
+}
+
+// per-tet pass at the trial point: energy partials + corner forces
+__global__ void __launch_bounds__(kTT) k_tet(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* cc = v.ctl + b;
+  const int ph = cc->phase;
+  const bool on = ph == PH_FIRST || ph == PH_DIR || ph == PH_ALPHA || ph == PH_COPY;
+  if (on) {
+    __shared__ double red[32];
+    double e[1] = {0.0};
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < v.mt) {
+      const int4 tv = v.tets[t];
+      const double* x = v.X + vec_off(v, cc->xs_trial, b);
+      double xs[4][3];
+      const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        xs[k][0] = x[3 * id[k] + 0];
+        xs[k][1] = x[3 * id[k] + 1];
+        xs[k][2] = x[3 * id[k] + 2];
+      }
+      double Dm[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) Dm[r][q] = __ldg(v.dminv + (size_t)(r * 3 + q) * v.mt + t);
+      const double vol = __ldg(v.vols + t);
+      const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
+      const qn_material& M = v.mats[(size_t)b * v.n_mat + mi];
+      double f[4][3];
+      e[0] = tet_eval<true>(M, xs, Dm, vol, f);
+      double* fo = v.forces + ((size_t)b * v.mt + t) * 12;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fo[3 * k + a] = f[k][a];
+    }
+    block_sum<1>(e, red);
+    if (threadIdx.x == 0) v.part_t[(size_t)b * v.nblk_t + blockIdx.x] = e[0];
+    if (last_block(v.cnt, 2, b, v.n_inst, gridDim.x) && threadIdx.x == 0) finalize_trial(v, b);
+  }
+  // last block overall: loop condition of the frame graph
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned* gc = v.cnt + 4 * (size_t)v.n_inst;
+    const unsigned total = gridDim.x * gridDim.y;
+    const unsigned old = atomicAdd(gc, 1u);
+    if (old == total - 1) {
+      *gc = 0;
+      __threadfence();
+      const int act = *((volatile int32_t*)v.active);
+      *v.passes += 1;
+      if (v.cfg->use_graph) cudaGraphSetConditional(v.handle, act > 0 ? 1u : 0u);
+    }
+  }
+}
+
+// q_prev <- q_l, q_l <- x (next SimState, solvers.py:351)
+__global__ void k_finish(SysView v) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.n) return;
+  const size_t o = inst_off(v, b) + (size_t)i * 3;
+  const double* x = v.X + vec_off(v, v.ctl[b].xs_cur, b) + (size_t)i * 3;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    v.q_prev[o + a] = v.q_l[o + a];
+    v.q_l[o + a] = x[a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// seam kernels (objective / gradient / element groups / SVD / material)
+
+__global__ void __launch_bounds__(kTT) k_tet_plain(SysView v, const double* x, int b, int mat_sel,
+                                                  double* part) {
+  __shared__ double red[32];
+  double e[1] = {0.0};
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < v.mt) {
+    const int mi = v.tet_mat ? v.tet_mat[t] : 0;
+    double f[4][3] = {};
+    if (mat_sel < 0 || mi == mat_sel) {
+      const int4 tv = v.tets[t];
+      const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+      double xs[4][3], Dm[3][3];
+      for (int k = 0; k < 4; ++k)
+        for (int a = 0; a < 3; ++a) xs[k][a] = x[3 * id[k] + a];
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q) Dm[r][q] = v.dminv[(size_t)(r * 3 + q) * v.mt + t];
+      e[0] = tet_eval<true>(v.mats[(size_t)b * v.n_mat + mi], xs, Dm, v.vols[t], f);
+    }
+    double* fo = v.forces + ((size_t)b * v.mt + t) * 12;
+    for (int k = 0; k < 4; ++k)
+      for (int a = 0; a < 3; ++a) fo[3 * k + a] = f[k][a];
+  }
+  block_sum<1>(e, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = e[0];
+}
+
+// out[i] = init[i] (+ inertia) + sum of corner forces, element order; fixed rows zeroed if asked
+__global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
+                               int zero_fixed, double* part) {
+  __shared__ double red[32];
+  double e[1] = {0.0};
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    double g[3];
+    if (inertia) {
+      const double w = v.masses[i] / __dmul_rn(v.h, v.h);
+      for (int a = 0; a < 3; ++a) g[a] = __dmul_rn(w, __dsub_rn(x[3 * i + a], y[3 * i + a]));
+      const double d0 = x[3 * i] - y[3 * i], d1 = x[3 * i + 1] - y[3 * i + 1], d2 = x[3 * i + 2] - y[3 * i + 2];
+      e[0] = v.masses[i] * (d0 * d0 + d1 * d1 + d2 * d2);
+    } else {
+      for (int a = 0; a < 3; ++a) g[a] = out[3 * i + a];
+    }
+    const double* fb = v.forces + (size_t)b * v.mt * 12;
+    for (int k = v.v2e_ptr[i]; k < v.v2e_ptr[i + 1]; ++k) {
+      const double* f = fb + (size_t)v.v2e[k] * 3;
+      for (int a = 0; a < 3; ++a) g[a] = __dadd_rn(g[a], f[a]);
+    }
+    if (zero_fixed && v.is_fixed[i]) g[0] = g[1] = g[2] = 0.0;
+    for (int a = 0; a < 3; ++a) out[3 * i + a] = g[a];
+  }
+  block_sum<1>(e, red);
+  if (threadIdx.x == 0 && part) part[blockIdx.x] = e[0];
+}
+
+__global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  double f[3][3], u[3][3], sg[3], vv[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) f[r][c] = F[t * 9 + r * 3 + c];
+  svd_rv3(f, u, sg, vv);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      U[t * 9 + r * 3 + c] = u[r][c];
+      V[t * 9 + r * 3 + c] = vv[r][c];
+    }
+  for (int k = 0; k < 3; ++k) s[t * 3 + k] = sg[k];
+}
+
+__global__ void k_material(const qn_material* M, int64_t k, const double* sig, double* psi, double* tau) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const double s[3] = {sig[3 * t], sig[3 * t + 1], sig[3 * t + 2]};
+  double tt[3];
+  psi[t] = vl_eval(*M, s, tt);
+  for (int a = 0; a < 3; ++a) tau[3 * t + a] = tt[a];
+}
+
+// ---------------------------------------------------------------------------
+// host: body launch / graph
+
+int launch_body(qn_system* S, cudaStream_t st) {
+  const SysView& v = S->v;
+  const dim3 gv(v.nblk_v, v.n_inst), gt(v.nblk_t, v.n_inst);
+  k_grad<<<gv, kVT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  SolverIO io{v};
+  int rc = launch_solve(S->factor, io, st);
+  if (rc) return rc;
+  k_eta<<<gv, kVT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  k_vec<<<gv, kVT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  k_tet<<<gt, kTT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
+int launch_init(qn_system* S, cudaStream_t st) {
+  const dim3 gv(S->v.nblk_v, S->v.n_inst);
+  k_init<<<gv, kVT, 0, st>>>(S->v);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
+int launch_finish(qn_system* S, cudaStream_t st) {
+  const dim3 gv(S->v.nblk_v, S->v.n_inst);
+  k_finish<<<gv, kVT, 0, st>>>(S->v);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
+int prepare_kernels(qn_system* S) { return prepare_solve_kernels<SolverIO>(S->factor->smem_bytes); }
+
+int build_graph(qn_system* S) {
+  cudaStream_t st = S->stream;
+  if (S->exec) {
+    cudaGraphExecDestroy(S->exec);
+    S->exec = nullptr;
+  }
+  if (S->graph) {
+    cudaGraphDestroy(S->graph);
+    S->graph = nullptr;
+  }
+  cudaGraph_t g;
+  QN_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  QN_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  S->v.handle = h;
+  // init
+  QN_CUDA(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int rc = launch_init(S, st);
+  cudaGraph_t tmp;
+  QN_CUDA(cudaStreamEndCapture(st, &tmp));
+  if (rc) return rc;
+  size_t nn = 0;
+  QN_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+  QN_REQUIRE(nn == 1, QN_ERR_CUDA, "graph: unexpected init capture");
+  cudaGraphNode_t init_node;
+  QN_CUDA(cudaGraphGetNodes(g, &init_node, &nn));
+  // WHILE(active) { body }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond;
+  QN_CUDA(cudaGraphAddNode(&cond, g, &init_node, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  rc = launch_body(S, st);
+  QN_CUDA(cudaStreamEndCapture(st, &body));
+  if (rc) return rc;
+  // finish
+  QN_CUDA(cudaStreamBeginCaptureToGraph(st, g, &cond, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+  rc = launch_finish(S, st);
+  QN_CUDA(cudaStreamEndCapture(st, &g));
+  if (rc) return rc;
+  QN_CUDA(cudaGraphInstantiate(&S->exec, g, 0));
+  S->graph = g;
+  return QN_OK;
+}
+
+}  // namespace qn

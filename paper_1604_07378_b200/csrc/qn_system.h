@@ -1,0 +1,115 @@
+// Device-resident simulation system (SimSystem + SimState + solver workspace).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "qn_factor.h"
+#include "qnsim_b200.h"
+
+namespace qn {
+
+// per-instance solver phase (one body pass of the frame graph advances every
+// instance by one step of this machine; see qn_solver.cu)
+enum Phase : int32_t {
+  PH_FIRST = 0,  // evaluate g0 and corner forces at x = y
+  PH_GRAD = 1,   // gather gradient, L-BFGS push, zeta's
+  PH_DIR = 2,    // triangular solves, eta's, direction, first trial formed
+  PH_ALPHA = 3,  // backtracking trial x + alpha d
+  PH_COPY = 4,   // re-evaluate corner forces at the current x (after slope early-out)
+  PH_DONE = 5,
+};
+
+constexpr int kMaxM = QN_MAX_M;
+constexpr int kNG = 5 + 2 * kMaxM;  // gradient-kernel dot products per block
+
+struct InstCtl {
+  int32_t phase, k, trials, status;
+  int32_t xs_cur, xs_prev, xs_trial, gs_cur;
+  int32_t npairs, have_prev, pad0, pad1;
+  int32_t ring[kMaxM + 1];
+  double g0, g_x, alpha, slope;
+  unsigned long long t0;
+  double rho[kMaxM + 1];
+  double sg[kMaxM + 1];
+  double gram[kMaxM + 1][kMaxM + 1];  // gram[i][j] = <s_i, t_j> (slot ids), i older than j
+  double zeta[kMaxM];                 // by ring position
+  double coef[kMaxM];                 // zeta - eta by ring position
+};
+
+struct DevConfig {
+  int32_t kind, iterations, m, line_search;
+  double gamma, alpha_init, shrink, grad_tol;
+  int32_t has_targets, use_graph;
+};
+
+struct SysView {
+  int32_t n, mt, n_inst, n_mat, n_fixed, nblk_v, nblk_t, rec_cap;
+  double h;
+  double grav[3];
+  const int4* tets;
+  const double* dminv;  // SoA [9][mt]
+  const double* vols;
+  const int32_t* tet_mat;
+  const qn_material* mats;
+  const double* masses;
+  const uint8_t* is_fixed;
+  const int32_t* fixed_pos;  // vertex -> index into the fixed list, -1 if free
+  const int32_t* v2e_ptr;
+  const int32_t* v2e;        // slots 4 t + c, increasing
+  const int32_t* fact_vtx;   // factor row -> vertex
+  double* q_l;
+  double* q_prev;
+  double* y;
+  double* X;       // [3][inst][n][3]
+  double* Gr;      // [2][inst][n][3]
+  double* S;       // [kMaxM+1][inst][n][3]
+  double* T;
+  double* R0;      // [inst][n][3]
+  double* D;       // [inst][n][3]
+  double* forces;  // [inst][mt][4][3]
+  const double* targets;  // [inst][n_fixed][3]
+  double* part_v;  // [inst][nblk_v][kNG]
+  double* part_t;  // [inst][nblk_t]
+  unsigned* cnt;   // [4][inst] last-block counters + [global]
+  InstCtl* ctl;
+  const DevConfig* cfg;
+  double* rec_g;
+  int32_t* rec_trials;
+  double* rec_alpha;
+  double* rec_ms;
+  int32_t* active;     // instances not yet done
+  unsigned long long* passes;
+  cudaGraphConditionalHandle handle;
+};
+
+}  // namespace qn
+
+struct qn_system {
+  int64_t n = 0, mt = 0, n_inst = 1, n_mat = 1, n_fixed = 0, n_free = 0;
+  double h = 0, grav[3] = {0, 0, 0}, scale = 1, max_mass = 0;
+  qn_factor* factor = nullptr;
+  cudaStream_t stream = nullptr;
+  // device buffers (owned)
+  std::vector<void*> allocs;
+  qn::SysView v{};
+  qn::DevConfig* d_cfg = nullptr;
+  qn::DevConfig h_cfg{};
+  double* d_targets = nullptr;
+  int rec_cap = 0;
+  // pinned host staging
+  double* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  // graph
+  bool use_graph = true;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int64_t last_passes = 0;
+  // element-seam workspace
+  double* d_part_plain = nullptr;
+  std::vector<int32_t> h_tet_mat;
+};

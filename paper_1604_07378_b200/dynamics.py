@@ -1,0 +1,309 @@
+"""Backward-Euler system on the B200 (mirror of qnsim.dynamics, dynamics.py:1-516).
+
+`build_system` keeps the reference signature and setup semantics
+(dynamics.py:351-434): lumped masses, G operators, per-group stiffness fit
+w = V k, L = sum w G G^T, fixed/free split, A = L + M/h^2 on the free DOFs
+factored once.  The result is a device-resident `SimSystem` backed by the
+C-ABI `qn_system` (tets SoA, vertex->element gather map, supernodal factor,
+solver workspace, CUDA graph of the frame).  `build_batch_system` adds the
+configs[3] case: many instances of one mesh with per-instance materials and
+numeric factors.
+
+Out of the B200 hot-path scope ("next" rows): ARAP / spring PD
+groups, anisotropic fibres and colliders raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse
+
+from paper_1604_07378_b200 import _lib
+from paper_1604_07378_b200.linalg import Factorization
+from paper_1604_07378_b200.materials import FitInterval, MaterialModel, estimate_stiffness
+from paper_1604_07378_b200.mesh import TetMesh, lumped_masses, tet_diff_operators
+
+DEFAULT_TIMESTEP = 1.0 / 30.0      # dynamics.py:28
+DEFAULT_GRAVITY = (0.0, 0.0, -9.8)  # dynamics.py:29
+
+
+class DynamicsError(Exception):
+    pass
+
+
+class VLGroup:
+    """Valanis-Landel tet group; GPU seam with the reference duck type
+    (`energy`, `add_gradient`, `L_blocks`, `w`, `verts`; dynamics.py:40-70)."""
+
+    def __init__(self, tets, G, vols, material: MaterialModel, k: float):
+        self.verts = tets
+        self.G = G
+        self.vols = vols
+        self.material = material
+        self.w = vols * k
+        self._system = None
+        self._index = 0
+        self._inst = 0
+
+    def L_blocks(self):
+        return self.w[:, None, None] * np.einsum("evc,euc->evu", self.G, self.G), self.verts
+
+    def energy(self, x) -> float:
+        e = C.c_double(0.0)
+        xs = _lib.f64(x)
+        _lib.check(_lib.load().qn_system_elements(self._system._h, self._inst, self._index, _lib.ptr(xs),
+                                                  C.byref(e), None, _lib.QN_MEM_HOST, None), "group energy")
+        return e.value
+
+    def add_gradient(self, x, out):
+        e = C.c_double(0.0)
+        xs = _lib.f64(x)
+        buf = _lib.f64(out)
+        _lib.check(_lib.load().qn_system_elements(self._system._h, self._inst, self._index, _lib.ptr(xs),
+                                                  C.byref(e), _lib.ptr(buf), _lib.QN_MEM_HOST, None), "group grad")
+        out[...] = buf
+
+
+@dataclass
+class SimState:
+    """dynamics.py:314-329 (collisions are out of scope: always empty)."""
+
+    q_l: np.ndarray
+    q_prev: np.ndarray
+    y: np.ndarray | None = None
+    collisions: object = None
+
+    def copy(self):
+        return SimState(self.q_l.copy(), self.q_prev.copy(), None if self.y is None else self.y.copy())
+
+
+@dataclass
+class SimSystem:
+    mesh: object
+    masses: np.ndarray
+    h: float
+    gravity: np.ndarray
+    groups: list
+    fixed: np.ndarray
+    free: np.ndarray
+    L: object
+    sysfact: Factorization
+    scale: float = 1.0
+    n_inst: int = 1
+    materials: list = field(default_factory=list)
+    pd_groups: list = field(default_factory=list)
+    colliders: list = field(default_factory=list)
+    w_col: float = 0.0
+    _h: object = None
+
+    @property
+    def n(self):
+        return self.masses.shape[0]
+
+    def set_graph_mode(self, on: bool):
+        _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
+
+    def factor_info(self) -> dict:
+        return self.sysfact.info()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().qn_system_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def _assign(mesh, materials):
+    if isinstance(materials, MaterialModel):
+        return [(np.arange(mesh.tets.shape[0]), materials)]
+    out = []
+    for idx, mat in materials:
+        if not isinstance(mat, MaterialModel):
+            raise NotImplementedError(f"material {mat!r}: only Valanis-Landel tet groups run on the B200 path")
+        out.append((np.asarray(idx, dtype=np.int64), mat))
+    return out
+
+
+def _pattern_sum(rows, cols, n):
+    """CSR pattern of a COO triple and the map contribution -> CSR slot."""
+    key = rows.astype(np.int64) * n + cols
+    uniq, inv = np.unique(key, return_inverse=True)
+    r = (uniq // n).astype(np.int64)
+    c = (uniq % n).astype(np.int64)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(indptr, r + 1, 1)
+    return np.cumsum(indptr), c, inv, r
+
+
+def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups):
+    if not isinstance(mesh, TetMesh):
+        raise NotImplementedError("spring networks (cloth) are outside the B200 hot path")
+    _lib.require_gpu()
+    n = mesh.n
+    masses = lumped_masses(mesh)
+    G, vols = tet_diff_operators(mesh)
+    fixed = np.asarray(sorted(set(int(i) for i in fixed)), dtype=np.int64)
+    if fixed.size and (fixed.min() < 0 or fixed.max() >= n):
+        raise DynamicsError("fixed vertex index out of range")
+    mask = np.ones(n, dtype=bool)
+    mask[fixed] = False
+    free = np.nonzero(mask)[0]
+    if free.size == 0:
+        raise DynamicsError("all vertices fixed; nothing to simulate")
+
+    # group-major tet order = the reference's scatter order over groups
+    assign0 = inst_materials[0]
+    order = np.concatenate([idx for idx, _ in assign0]) if assign0 else np.zeros(0, dtype=np.int64)
+    tet_mat = np.concatenate([np.full(idx.size, g, dtype=np.int32) for g, (idx, _) in enumerate(assign0)]) \
+        if assign0 else np.zeros(0, dtype=np.int32)
+    tets = mesh.tets[order]
+    Gs, vs = G[order], vols[order]
+    m = tets.shape[0]
+
+    # L = sum_groups w G G^T per instance (dynamics.py:387-402), then A_free
+    GG = np.einsum("evc,euc->evu", Gs, Gs) if m else np.zeros((0, 4, 4))
+    rows = np.repeat(tets, 4, axis=1).reshape(-1)
+    cols = np.tile(tets, (1, 4)).reshape(-1)
+    diag = np.arange(n)
+    all_rows = np.concatenate([rows, diag])
+    all_cols = np.concatenate([cols, diag])
+    indptr, indices, inv, row_of = _pattern_sum(all_rows, all_cols, n)
+    # restrict to free rows/cols
+    keep = mask[row_of] & mask[indices]
+    remap = -np.ones(n, dtype=np.int64)
+    remap[free] = np.arange(free.size)
+    fr, fc = remap[row_of[keep]], remap[indices[keep]]
+    f_indptr = np.zeros(free.size + 1, dtype=np.int64)
+    np.add.at(f_indptr, fr + 1, 1)
+    f_indptr = np.cumsum(f_indptr)
+    values, Ls, groups_per_inst, mats = [], [], [], []
+    for assign in inst_materials:
+        ks, gl = [], []
+        for g, (idx, mat) in enumerate(assign):
+            k = mat.k_fit if mat.k_fit is not None else estimate_stiffness(mat, fit_interval)
+            ks.append(k)
+            gl.append(VLGroup(mesh.tets[idx], G[idx], vols[idx], mat, k))
+        w = (vs * np.asarray(ks)[tet_mat]) if m else np.zeros(0)
+        contrib = np.concatenate([(w[:, None, None] * GG).reshape(-1), masses / h ** 2])
+        sums = np.bincount(inv, weights=contrib, minlength=indices.size)
+        Lv = np.bincount(inv[: rows.size], weights=contrib[: rows.size], minlength=indices.size) if m else \
+            np.zeros(indices.size)
+        Ls.append(scipy.sparse.csr_matrix((Lv, indices, indptr), shape=(n, n)))
+        values.append(sums[keep])
+        groups_per_inst.append(gl)
+        mats.append([mat for _, mat in assign])
+    a_values = np.concatenate(values)
+    a_indices = _lib.i32(fc)
+
+    n_inst = len(inst_materials)
+    n_mat = max(1, n_mat_groups)
+    cmats = (_lib.Material * (n_inst * n_mat))()
+    for b, ml in enumerate(mats):
+        for g, mat in enumerate(ml):
+            cmats[b * n_mat + g] = mat.to_c()
+
+    tets32 = _lib.i32(tets)
+    dminv = _lib.f64(Gs[:, 1:, :]) if m else np.zeros((0, 3, 3))
+    vols_c = _lib.f64(vs)
+    tm = _lib.i32(tet_mat) if n_mat > 1 else None
+    masses_c = _lib.f64(masses)
+    fixed32 = _lib.i32(fixed)
+    f_indptr = _lib.i64(f_indptr)
+    a_values = _lib.f64(a_values)
+    coords = _lib.f64(mesh.vertices[free])
+    bbox = mesh.vertices.max(axis=0) - mesh.vertices.min(axis=0)
+    scale = float(np.linalg.norm(bbox)) or 1.0  # dynamics.py:416-417
+
+    d = _lib.SystemDesc()
+    d.n_verts, d.n_tets, d.n_inst, d.n_mat = n, m, n_inst, n_mat
+    d.tets, d.Dm_inv, d.vols = _lib.ptr(tets32), _lib.ptr(dminv), _lib.ptr(vols_c)
+    d.tet_mat = _lib.ptr(tm)
+    d.mats = C.cast(cmats, C.c_void_p)
+    d.masses = _lib.ptr(masses_c)
+    d.n_fixed, d.fixed = fixed.size, _lib.ptr(fixed32)
+    d.h = float(h)
+    for a in range(3):
+        d.gravity[a] = float(gravity[a])
+    d.scale = scale
+    d.a_nnz = a_indices.size
+    d.a_indptr, d.a_indices, d.a_values = _lib.ptr(f_indptr), _lib.ptr(a_indices), _lib.ptr(a_values)
+    d.free_coords = _lib.ptr(coords)
+    handle = C.c_void_p()
+    _lib.check(_lib.load().qn_system_create(C.byref(d), C.byref(handle)), "build_system")
+    fh = C.c_void_p()
+    _lib.check(_lib.load().qn_system_factor(handle, C.byref(fh)))
+    sysfact = Factorization._borrow(fh, free.size, n_inst)
+
+    system = SimSystem(mesh=mesh, masses=masses, h=float(h), gravity=np.asarray(gravity, dtype=np.float64),
+                       groups=groups_per_inst[0] if n_inst == 1 else groups_per_inst, fixed=fixed, free=free,
+                       L=Ls[0] if n_inst == 1 else Ls, sysfact=sysfact, scale=scale, n_inst=n_inst,
+                       materials=mats, _h=handle)
+    for b, gl in enumerate(groups_per_inst):
+        for g, grp in enumerate(gl):
+            grp._system, grp._index, grp._inst = system, g, b
+    return system
+
+
+def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(), aniso=None,
+                 colliders=(), collision_weight: float | None = None,
+                 fit_interval: FitInterval = FitInterval()) -> SimSystem:
+    """dynamics.py:351-434 for Valanis-Landel tet groups (single instance)."""
+    if aniso:
+        raise NotImplementedError("anisotropic fibres are outside the B200 hot path (SURVEY §8f)")
+    if colliders:
+        raise NotImplementedError("colliders are outside the B200 hot path (SURVEY §8f)")
+    assign = _assign(mesh, materials)
+    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign))
+
+
+def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(),
+                       fit_interval: FitInterval = FitInterval()) -> SimSystem:
+    """configs[3]: independent instances of one mesh, one MaterialModel (or
+    group assignment) per instance, each with its own factored A."""
+    inst = [_assign(mesh, m) for m in materials_per_instance]
+    if not inst:
+        raise DynamicsError("empty batch")
+    sizes = {len(a) for a in inst}
+    if len(sizes) != 1:
+        raise DynamicsError("all instances need the same material-group layout")
+    return _build(mesh, inst, h, gravity, fixed, fit_interval, len(inst[0]))
+
+
+def inertia_target(state: SimState, system: SimSystem, fixed_targets=None) -> np.ndarray:
+    """y = 2 q_l - q_prev + h^2 g (dynamics.py:437-443).  Host helper for API
+    parity; the frame computes y on the device (k_init)."""
+    h = system.h
+    y = 2.0 * state.q_l - state.q_prev + h * h * system.gravity
+    if system.fixed.size:
+        if fixed_targets is None:
+            y[..., system.fixed, :] = state.q_l[..., system.fixed, :]
+        else:
+            y[..., system.fixed, :] = fixed_targets
+    return y
+
+
+def _objective_gradient(system: SimSystem, state: SimState, x, want_grad: bool):
+    x = _lib.f64(x)
+    y = _lib.f64(state.y)
+    g = np.empty(system.n_inst)
+    grad = np.empty_like(x) if want_grad else None
+    _lib.check(_lib.load().qn_system_objective(system._h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(g), _lib.ptr(grad),
+                                               _lib.QN_MEM_HOST, None), "objective")
+    return g, grad
+
+
+def objective(system: SimSystem, state: SimState, x) -> float:
+    """g(x) = inertia + elastic on the GPU (dynamics.py:460-467)."""
+    g, _ = _objective_gradient(system, state, x, False)
+    return float(g[0]) if system.n_inst == 1 else g
+
+
+def gradient(system: SimSystem, state: SimState, x) -> np.ndarray:
+    """Gradient with fixed rows zeroed, on the GPU (dynamics.py:470-478)."""
+    return _objective_gradient(system, state, x, True)[1]

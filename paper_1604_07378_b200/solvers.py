@@ -1,0 +1,196 @@
+"""Per-frame quasi-Newton / L-BFGS minimisation on the B200 (mirror of
+qnsim.solvers, solvers.py:1-407).
+
+`simulate_frame` keeps the reference signature and return types
+(solvers.py:260-352); the whole frame — inertia target, L-BFGS two-loop with
+the prefactored A as H0, Armijo backtracking, early-outs, stagnation — runs as
+one CUDA-graph launch (`qn_frame_step`).  Supported: kind "pd_qn" and
+"lbfgs" (lbfgs_init="system_matrix"), with or without line search.  Chebyshev,
+Newton and the other L-BFGS initialisations are out of the hot-path scope
+ and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_1604_07378_b200 import _lib
+from paper_1604_07378_b200.dynamics import SimState, SimSystem
+
+SOLVER_KINDS = ("pd_qn", "lbfgs", "chebyshev", "newton")          # solvers.py:25
+LBFGS_INITS = ("system_matrix", "scaled_identity", "rest_pose_hessian")
+CURVATURE_GUARD = 1e-12
+ALPHA_FLOOR = 1e-12
+
+
+class SolverError(Exception):
+    pass
+
+
+class StagnationError(SolverError):
+    """Line search step underflow (solvers.py:39-40)."""
+
+
+@dataclass
+class SolverConfig:
+    """solvers.py:43-68 (same defaults and validation)."""
+
+    kind: str = "pd_qn"
+    iterations: int = 10
+    m: int = 5
+    gamma: float = 0.3
+    alpha_init: float = 2.0
+    alpha_shrink: float = 0.5
+    rho: float = 0.9
+    S: int = 10
+    lbfgs_init: str = "system_matrix"
+    line_search: bool = True
+
+    def __post_init__(self):
+        if self.kind not in SOLVER_KINDS:
+            raise SolverError(f"unknown solver kind {self.kind!r}; valid: {SOLVER_KINDS}")
+        if not (0.0 < self.gamma < 1.0):
+            raise SolverError(f"gamma must be in (0, 1), got {self.gamma}")
+        if self.m < 0:
+            raise SolverError("m must be >= 0")
+        if not (0.0 <= self.rho < 1.0):
+            raise SolverError(f"rho must be in [0, 1), got {self.rho}")
+        if self.iterations < 1:
+            raise SolverError("iterations must be >= 1")
+        if self.lbfgs_init not in LBFGS_INITS:
+            raise SolverError(f"unknown lbfgs_init {self.lbfgs_init!r}; valid: {LBFGS_INITS}")
+
+    def to_c(self) -> _lib.SolverConfigC:
+        if self.kind not in ("pd_qn", "lbfgs"):
+            raise NotImplementedError(f"solver kind {self.kind!r} is outside the B200 hot path (SURVEY §8f)")
+        if self.kind == "lbfgs" and self.lbfgs_init != "system_matrix":
+            raise NotImplementedError(f"lbfgs_init {self.lbfgs_init!r} is outside the B200 hot path")
+        if self.m > _lib.QN_MAX_M:
+            raise NotImplementedError(f"history window m > {_lib.QN_MAX_M}")
+        c = _lib.SolverConfigC()
+        c.kind = 1 if self.kind == "lbfgs" else 0
+        c.iterations, c.m, c.line_search = self.iterations, self.m, 1 if self.line_search else 0
+        c.gamma, c.alpha_init, c.alpha_shrink = self.gamma, self.alpha_init, self.alpha_shrink
+        return c
+
+
+@dataclass
+class ConvergenceRecord:
+    """solvers.py:71-80"""
+
+    g0: float = 0.0
+    g: list = field(default_factory=list)
+    ls_trials: list = field(default_factory=list)
+    alphas: list = field(default_factory=list)
+    cum_ms: list = field(default_factory=list)
+    rel_error: list = field(default_factory=list)
+    fallbacks: int = 0
+    stagnated: bool = False
+
+
+def relative_error(g_k: float, g_0: float, g_star: float) -> float:
+    """solvers.py:106-110"""
+    if g_0 <= g_star + 1e-15:
+        raise SolverError(f"degenerate frame: g_0 ({g_0}) not above g* ({g_star})")
+    return (g_k - g_star) / (g_0 - g_star)
+
+
+class _RecordBuffers:
+    def __init__(self, n_inst, iterations):
+        self.g0 = np.zeros(n_inst)
+        self.g = np.zeros((n_inst, iterations))
+        self.trials = np.zeros((n_inst, iterations), dtype=np.int32)
+        self.alphas = np.zeros((n_inst, iterations))
+        self.ms = np.zeros((n_inst, iterations))
+        self.status = np.zeros(n_inst, dtype=np.int32)
+        self.c = _lib.FrameRecord(_lib.ptr(self.g0), _lib.ptr(self.g), _lib.ptr(self.trials), _lib.ptr(self.alphas),
+                                  _lib.ptr(self.ms), _lib.ptr(self.status))
+
+    def records(self):
+        out = []
+        for b in range(self.g0.size):
+            out.append(ConvergenceRecord(g0=float(self.g0[b]), g=[float(v) for v in self.g[b]],
+                                         ls_trials=[int(v) for v in self.trials[b]],
+                                         alphas=[float(v) for v in self.alphas[b]],
+                                         cum_ms=[float(v) for v in self.ms[b]],
+                                         stagnated=bool(self.status[b] & 1)))
+        return out
+
+    def raise_on_error(self):
+        bad = np.nonzero(self.status & 2)[0]
+        if bad.size:
+            raise SolverError(f"line search requires a descent direction (instance {int(bad[0])})")
+
+
+def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fixed_targets=None):
+    """Advance one frame; returns (next_state, ConvergenceRecord) — a list of
+    records for batch systems (solvers.py:260-352)."""
+    if system.colliders:
+        raise NotImplementedError("colliders are outside the B200 hot path")
+    cfg = config.to_c()
+    shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
+    q_l = _lib.f64(state.q_l).reshape(shape)
+    q_prev = _lib.f64(state.q_prev).reshape(shape)
+    tg = None
+    if fixed_targets is not None and system.fixed.size:
+        tg = _lib.f64(np.broadcast_to(fixed_targets, (system.n_inst, system.fixed.size, 3)))
+    x = np.empty(shape)
+    y = np.empty(shape)
+    rb = _RecordBuffers(system.n_inst, config.iterations)
+    rc = _lib.load().qn_simulate_frame(system._h, C.byref(cfg), _lib.ptr(q_l), _lib.ptr(q_prev), _lib.ptr(tg),
+                                       _lib.ptr(x), _lib.ptr(y), C.byref(rb.c), _lib.QN_MEM_HOST, None)
+    _lib.check(rc, "simulate_frame")
+    rb.raise_on_error()
+    recs = rb.records()
+    nxt = SimState(q_l=x, q_prev=np.asarray(state.q_l), y=y)
+    return nxt, (recs[0] if system.n_inst == 1 else recs)
+
+
+class ResidentRun:
+    """Device-resident frame stepping (the state never leaves HBM):
+    set_state once, then step() advances q_l/q_prev in place — the `value`
+    path of bench.py.  `last_ms` is the CUDA-event time of the last frame."""
+
+    def __init__(self, system: SimSystem, state: SimState, config: SolverConfig):
+        self.system, self.config = system, config
+        self._cfg = config.to_c()
+        shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
+        _lib.check(_lib.load().qn_state_set(system._h, _lib.ptr(_lib.f64(state.q_l).reshape(shape)),
+                                            _lib.ptr(_lib.f64(state.q_prev).reshape(shape)), _lib.QN_MEM_HOST, None))
+        self.shape = shape
+
+    def step(self, fixed_targets=None, record: bool = False, sync: bool = True):
+        tg = None
+        if fixed_targets is not None and self.system.fixed.size:
+            tg = _lib.f64(np.broadcast_to(fixed_targets, (self.system.n_inst, self.system.fixed.size, 3)))
+        rb = _RecordBuffers(self.system.n_inst, self.config.iterations) if record else None
+        _lib.check(_lib.load().qn_frame_step(self.system._h, C.byref(self._cfg), _lib.ptr(tg),
+                                             C.byref(rb.c) if rb else None, _lib.QN_MEM_HOST,
+                                             1 if (sync or record) else 0, None), "frame_step")
+        if rb:
+            rb.raise_on_error()
+            return rb.records()
+        return None
+
+    def state(self):
+        ql = np.empty(self.shape)
+        qp = np.empty(self.shape)
+        y = np.empty(self.shape)
+        _lib.check(_lib.load().qn_state_get(self.system._h, _lib.ptr(ql), _lib.ptr(qp), _lib.ptr(y),
+                                            _lib.QN_MEM_HOST, None))
+        return SimState(q_l=ql, q_prev=qp, y=y)
+
+    @property
+    def last_ms(self) -> float:
+        v = C.c_double(0.0)
+        _lib.check(_lib.load().qn_system_last_frame_ms(self.system._h, C.byref(v)))
+        return v.value
+
+    @property
+    def last_passes(self) -> int:
+        v = C.c_int64(0)
+        _lib.check(_lib.load().qn_system_last_frame_passes(self.system._h, C.byref(v)))
+        return v.value

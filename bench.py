@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the per-timestep L-BFGS solver (BASELINE.json metric:
+"solver iterations/sec & tet evals/sec (fp64) vs HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one frame (simulate_frame) of the configuration; the default
+workload is configs[1] (c2: 60x15x15 StVK bar, 81 000 tets, 20 L-BFGS
+iterations per frame), the configuration the metric is quoted on that fits one
+GPU.  N > 1: launched by torch.distributed.run, one process per GPU; c1-c3 do
+not shard (independent replicas per rank, "weak"), c4 shards its 1024
+instances across ranks (no data-path collective).  Timing: CUDA events on the
+launching stream around each frame, L2 flushed (256 MiB write) between frames,
+max over ranks.  `--impl reference` times the CPU oracle port of the reference
+(oracle/, numpy + scipy sparse factor) on host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solver iterations/sec & tet evals/sec (fp64) vs HBM roofline, 1/2/4/8 B200"
+UNIT = "iterations/s"
+FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def build_scene(name, rank, world):
+    from paper_1604_07378_b200 import scenes
+    sc = scenes.CONFIGS[name]()
+    if name == "c4":  # shard independent instances across ranks
+        per = len(sc.batch_materials) // world
+        lo, hi = rank * per, (rank + 1) * per
+        sc.batch_materials = sc.batch_materials[lo:hi]
+        sc.q_l, sc.q_prev = sc.q_l[lo:hi], sc.q_prev[lo:hi]
+    return sc
+
+
+def build_system(sc):
+    import paper_1604_07378_b200 as Q
+    from paper_1604_07378_b200.materials import from_spec
+    mesh = Q.TetMesh(sc.verts, sc.tets, sc.density)
+    if sc.batch:
+        return Q.build_batch_system(mesh, [from_spec(s) for s in sc.batch_materials], h=sc.h, gravity=sc.gravity,
+                                    fixed=sc.fixed)
+    return Q.build_system(mesh, from_spec(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+
+
+def cpu_oracle_rate(sc, iterations, frames=1, threads=1):
+    """Reference CPU path (oracle port, sparse factor restatement) iterations/s."""
+    import oracle.qnsim_oracle as O
+    from tests.helpers import oracle_material
+    O.set_threads(threads)
+    spec = sc.batch_materials[0] if sc.batch else sc.material
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(spec), sc.h, sc.gravity, sc.fixed)
+    q_l = np.array(sc.q_l[0] if sc.batch else sc.q_l)
+    q_prev = np.array(sc.q_prev[0] if sc.batch else sc.q_prev)
+    t = time.perf_counter()
+    for _ in range(frames):
+        x, _, _ = O.simulate_frame(osys, q_l, q_prev, iterations=iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+    dt = time.perf_counter() - t
+    return iterations * frames / dt, dt
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_1604_07378_b200 import scenes
+    sc = scenes.CONFIGS[args.config]()
+    threads = os.cpu_count() or 1
+    import oracle.qnsim_oracle as O
+    from tests.helpers import oracle_material
+    O.set_threads(threads)
+    spec = sc.batch_materials[0] if sc.batch else sc.material
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(spec), sc.h, sc.gravity, sc.fixed)
+    q_l = np.array(sc.q_l[0] if sc.batch else sc.q_l)
+    q_prev = np.array(sc.q_prev[0] if sc.batch else sc.q_prev)
+    its = 2 if sc.tets.shape[0] > 10000 else sc.iterations  # bounded sample per step
+    times = []
+    for k in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        x, _, _ = O.simulate_frame(osys, q_l, q_prev, iterations=its, m=sc.m)
+        dt = time.perf_counter() - t
+        q_prev, q_l = q_l, x
+        if k >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = its * args.steps / total  # (instance-)iterations per second on the host
+    sample = f"{its} L-BFGS iterations of one {args.config} frame per step (oracle port, sparse LU factor)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "tets": int(sc.tets.shape[0]), "verts": int(sc.verts.shape[0]),
+                       "iterations_per_step": its},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_1604_07378_b200 as Q
+    from paper_1604_07378_b200 import _lib
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sc = build_scene(args.config, rank, world)
+    n_inst = max(1, sc.batch)
+    t_build = time.perf_counter()
+    system = build_system(sc)
+    t_build = time.perf_counter() - t_build
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+    st0 = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
+    run = Q.ResidentRun(system, st0, cfg)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        run.step(stream=sptr)
+    # ---- timed region: K frames, device-resident state, L2 flushed between frames ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    passes = 0
+    l0 = _lib.launch_count()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        run.step(stream=sptr)
+        ev[k][1].record(stream)
+        passes += run.last_passes
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    clk = clocks.stop()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    its_per_step = sc.iterations * n_inst
+    value = world * its_per_step * args.steps / (total_ms / 1000.0)
+    tet_evals = world * passes * sc.tets.shape[0] * n_inst / (total_ms / 1000.0)
+
+    # ---- roofline of the hot kernels (stand-alone CUDA-event timing, same stream) ----
+    hbm, peak_kind = peaks()
+    info = system.factor_info()
+    m, n = sc.tets.shape[0], sc.verts.shape[0]
+    tet_ms = system.time_kernel("tet", reps=20, stream=sptr)
+    solve_ms = system.time_kernel("solve", reps=20, stream=sptr)
+    tet_bytes = (192.0 + 24.0 * n / m) * m                    # idx+Dm^-1+vol+forces, x gathered once
+    solve_bytes = 2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]  # factor read twice + rhs/y/x/u vectors
+    per_frame = total_ms / args.steps
+    share_tet = tet_ms * passes / args.steps / per_frame
+    share_solve = solve_ms * sc.iterations / per_frame
+    dom = "tet" if share_tet >= share_solve else "solve"
+    dms, dbytes = (tet_ms, tet_bytes) if dom == "tet" else (solve_ms, solve_bytes)
+    achieved = dbytes / (dms / 1000.0) / 1e9
+    roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else "sptrsv_forward+backward",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
+            "traffic": ncu_traffic(dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
+            "share_of_step": share_tet if dom == "tet" else share_solve,
+            "other": {"tet_ms": tet_ms, "tet_GBps": tet_bytes / tet_ms / 1e6, "tet_share": share_tet,
+                      "solve_ms": solve_ms, "solve_GBps": solve_bytes / solve_ms / 1e6, "solve_share": share_solve}}
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        st = Q.SimState(q_l=np.array(sc.q_l), q_prev=np.array(sc.q_prev))
+        for _ in range(min(args.warmup, 2)):
+            st, _ = Q.simulate_frame(system, st, cfg)
+        if world > 1:
+            torch.distributed.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            st, _ = Q.simulate_frame(system, st, cfg)
+        dt = time.perf_counter() - t
+        if world > 1:
+            tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+        vec = n_inst * n * 3 * 8
+        rec_bytes = n_inst * (cfg.iterations * (8 * 3 + 4) + 8 + 4)
+        e2e = {"value": world * its_per_step * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * vec,
+               "d2h_bytes_per_step": 2 * vec + rec_bytes}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_its = 8 if m > 10000 else sc.iterations
+        rate, dt = cpu_oracle_rate(sc, cpu_its, frames=1 if m > 10000 else 5)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{cpu_its if m > 10000 else 5 * cpu_its} L-BFGS iterations of {args.config} from its "
+                         f"initial state, 1 thread ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": per_frame, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.config, "tets": int(m), "verts": int(n), "instances": n_inst * world,
+                           "iterations_per_step": sc.iterations, "m": sc.m,
+                           "l2": "flushed between steps (256 MiB write)",
+                           "parallelism": "replicas" if not sc.batch else f"instances/{world} per rank"},
+                "tet_evals_per_s": tet_evals, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk, "gpu_launches": launches,
+                "factor": {"nnz_l": info["nnz_l"], "supernodes": info["n_supernodes"],
+                           "depth": info["tree_depth"], "factor_s": info["factor_seconds"]},
+                "build_s": t_build, "passes_per_step": passes / args.steps}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -203,6 +203,11 @@ int qn_system_last_frame_ms(qn_system* s, double* ms);
 /* body passes (line-search trials + re-evaluations) of the last frame */
 int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
 
+/* Stand-alone timing of one hot kernel with CUDA events on `stream` (after a
+ * warm-up launch): kernel 0 = per-tet pass at the resident q_l, kernel 1 =
+ * forward + backward supernodal solve (3 RHS).  avg_ms = mean launch time. */
+int qn_system_time_kernel(qn_system* s, int32_t kernel, int32_t reps, double* avg_ms, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

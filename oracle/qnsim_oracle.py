@@ -303,6 +303,25 @@ def svd_rv(F):
 # --------------------------------------------------------------------------
 # element groups and the objective (dynamics.py:40-70, 437-478)
 
+THREADS = 1  # element-pass worker threads (numpy's batched SVD releases the GIL)
+
+
+def set_threads(n):
+    """Chunk the element pass over `n` host threads (CPU-baseline timing only;
+    the summation order of the energy changes at roundoff level)."""
+    global THREADS
+    THREADS = max(1, int(n))
+
+
+def _chunked(fn, m):
+    if THREADS == 1 or m < 4096:
+        return [fn(slice(0, m))]
+    from concurrent.futures import ThreadPoolExecutor
+    bounds = np.linspace(0, m, THREADS + 1).astype(int)
+    with ThreadPoolExecutor(THREADS) as ex:
+        return list(ex.map(fn, [slice(a, b) for a, b in zip(bounds[:-1], bounds[1:])]))
+
+
 @dataclass
 class TetGroup:
     tets: np.ndarray
@@ -311,20 +330,24 @@ class TetGroup:
     mat: VLMaterial
     k: float
 
-    def defgrad(self, x):
-        return np.einsum("eva,evc->eac", x[self.tets], self.G)
+    def defgrad(self, x, sl=slice(None)):
+        return np.einsum("eva,evc->eac", x[self.tets[sl]], self.G[sl])
 
     def energy(self, x):
         """dynamics.py:57-63"""
-        _, s, _ = svd_rv(self.defgrad(x))
-        return float((self.vols * vl_energy(self.mat, s)).sum())
+        def part(sl):
+            _, s, _ = svd_rv(self.defgrad(x, sl))
+            return self.vols[sl] * vl_energy(self.mat, s)
+        return float(np.concatenate(_chunked(part, self.tets.shape[0])).sum())
 
     def corner_forces(self, x):
         """vol * U diag(tau) V^T G^T per corner (dynamics.py:50-55)."""
-        U, s, V = svd_rv(self.defgrad(x))
-        tau = vl_stress(self.mat, s)
-        P = np.einsum("eab,eb,ecb->eac", U, tau, V)
-        return self.vols[:, None, None] * np.einsum("eac,evc->eva", P, self.G)
+        def part(sl):
+            U, s, V = svd_rv(self.defgrad(x, sl))
+            tau = vl_stress(self.mat, s)
+            P = np.einsum("eab,eb,ecb->eac", U, tau, V)
+            return self.vols[sl, None, None] * np.einsum("eac,evc->eva", P, self.G[sl])
+        return np.concatenate(_chunked(part, self.tets.shape[0]))
 
     def add_gradient(self, x, out):
         """element-major scatter (dynamics.py:65-67)"""

@@ -548,8 +548,7 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   QN_REQUIRE(cfg->iterations >= 1 && cfg->m >= 0 && cfg->m <= kMaxM, QN_ERR_ARG, "frame_step: bad iterations/m");
   QN_REQUIRE(cfg->gamma > 0 && cfg->gamma < 1, QN_ERR_ARG, "frame_step: gamma");
   QN_REQUIRE(sync || !rec, QN_ERR_ARG, "frame_step: a record needs sync");
-  cudaStream_t st = S->stream;
-  (void)stream;
+  cudaStream_t st = pick(S, stream);
   int rc = ensure_records(S, cfg->iterations);
   if (rc) return rc;
   DevConfig& c = S->h_cfg;
@@ -715,6 +714,35 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
   }
   cudaFree(dx);
   cudaFree(dg);
+  return QN_OK;
+}
+
+int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* avg_ms, void* stream) {
+  QN_REQUIRE(S && avg_ms && reps >= 1 && (kernel == 0 || kernel == 1), QN_ERR_ARG, "time_kernel: args");
+  cudaStream_t st = pick(S, stream);
+  const SysView& v = S->v;
+  int rc;
+  auto launch = [&]() -> int {
+    if (kernel == 0) {  // per-tet pass (F, SVD, VL energy, PK1 corner forces) at the resident q_l
+      k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, v.q_l, 0, -1, S->d_part_plain);
+      QN_CHECK_LAUNCH();
+    } else {  // forward + backward supernodal solves with 3 RHS (instance 0)
+      QN_CUDA(cudaMemcpyAsync(S->factor->d_io, v.q_l, S->n_free * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      int r = factor_solve_plain(S->factor, 0, st);
+      if (r) return r;
+    }
+    return QN_OK;
+  };
+  if ((rc = launch())) return rc;  // warm-up
+  QN_CUDA(cudaStreamSynchronize(st));
+  QN_CUDA(cudaEventRecord(S->ev0, st));
+  for (int r = 0; r < reps; ++r)
+    if ((rc = launch())) return rc;
+  QN_CUDA(cudaEventRecord(S->ev1, st));
+  QN_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  QN_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+  *avg_ms = ms / reps;
   return QN_OK;
 }
 

@@ -109,6 +109,14 @@ class SimSystem:
     def factor_info(self) -> dict:
         return self.sysfact.info()
 
+    def time_kernel(self, kernel: str, reps: int = 20, stream=None) -> float:
+        """Mean CUDA-event time (ms) of one stand-alone launch of a hot kernel:
+        "tet" (per-tet pass at the resident q_l) or "solve" (fwd+bwd SpTRSV)."""
+        ms = C.c_double(0.0)
+        _lib.check(_lib.load().qn_system_time_kernel(self._h, {"tet": 0, "solve": 1}[kernel], reps, C.byref(ms),
+                                                     stream), "time_kernel")
+        return ms.value
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:

@@ -162,14 +162,14 @@ class ResidentRun:
                                             _lib.ptr(_lib.f64(state.q_prev).reshape(shape)), _lib.QN_MEM_HOST, None))
         self.shape = shape
 
-    def step(self, fixed_targets=None, record: bool = False, sync: bool = True):
+    def step(self, fixed_targets=None, record: bool = False, sync: bool = True, stream=None):
         tg = None
         if fixed_targets is not None and self.system.fixed.size:
             tg = _lib.f64(np.broadcast_to(fixed_targets, (self.system.n_inst, self.system.fixed.size, 3)))
         rb = _RecordBuffers(self.system.n_inst, self.config.iterations) if record else None
         _lib.check(_lib.load().qn_frame_step(self.system._h, C.byref(self._cfg), _lib.ptr(tg),
                                              C.byref(rb.c) if rb else None, _lib.QN_MEM_HOST,
-                                             1 if (sync or record) else 0, None), "frame_step")
+                                             1 if (sync or record) else 0, stream), "frame_step")
         if rb:
             rb.raise_on_error()
             return rb.records()

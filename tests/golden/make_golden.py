@@ -1,0 +1,170 @@
+"""Generate golden vectors from the UNMODIFIED reference (run in the build
+container, where /root/reference exists; the GPU box never runs this).
+
+    python tests/golden/make_golden.py [--quick]
+
+Writes tests/golden/*.npz and copies the reference's own golden trajectories
+(pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
+they were produced from into tests/golden/ref_fixtures/.  Inputs for the
+configs come from paper_1604_07378_b200.scenes (seeded), fed to the reference
+through its own Python API (build_system / SimState / simulate_frame), exactly
+as SURVEY.md §8(d) prescribes.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg"
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, ROOT)
+
+from qnsim import assets as ref_assets  # noqa: E402
+from qnsim import dynamics as ref_dyn  # noqa: E402
+from qnsim import linalg as ref_linalg  # noqa: E402
+from qnsim import materials as ref_mat  # noqa: E402
+from qnsim import mesh as ref_mesh  # noqa: E402
+from qnsim import solvers as ref_solvers  # noqa: E402
+
+from paper_1604_07378_b200 import scenes  # noqa: E402
+from tests.helpers import material_specs  # noqa: E402
+
+
+def ref_material(spec, name="custom"):
+    def fn(s):
+        if s[0] == "zero":
+            return ref_mat.ZeroFn()
+        if s[0] == "poly":
+            return ref_mat.PolyFn(s[1])
+        if s[0] == "log":
+            return ref_mat.LogFn(s[1], s[2])
+        return ref_mat.HermiteFn(s[1])
+    return ref_mat.MaterialModel(a=fn(spec[0]), b=fn(spec[1]), c=fn(spec[2]), name=name)
+
+
+MATERIAL_CASES = material_specs()
+
+
+def gen_svd_materials():
+    rng = np.random.default_rng(100)
+    F = rng.standard_normal((1200, 3, 3))
+    F[:100] = np.eye(3) + 1e-7 * rng.standard_normal((100, 3, 3))         # near rest (degenerate sigma)
+    F[100:200] = F[100:200] * np.array([1.0, 1.0, -1.0])[None, :, None]   # reflections
+    F[200:250, :, 2] = 0.0                                                 # exactly singular
+    F[250:300] = 1e-12 * rng.standard_normal((50, 3, 3))                  # clamp region
+    F[300] = np.eye(3)
+    F[301] = np.diag([-1.0, 1.0, 1.0])
+    F[302] = np.zeros((3, 3))
+    U, s, V = ref_linalg.svd_rv_batch(F.copy())
+    out = {"F": F, "sigma": s, "P_check": np.einsum("eab,eb,ecb->eac", U, s, V)}
+    sig = np.concatenate([
+        rng.uniform(0.2, 2.5, size=(400, 3)),
+        np.column_stack([rng.uniform(0.5, 1.5, (100, 2)), -rng.uniform(0.001, 0.8, 100)]),  # inverted
+        np.column_stack([rng.uniform(0.5, 1.5, (50, 2)), np.full(50, 1e-10)]),
+        np.ones((1, 3)),
+        rng.uniform(2.5, 4.0, size=(50, 3)),  # spline extrapolation
+    ])
+    out["mat_sigma"] = sig
+    for name, spec in MATERIAL_CASES.items():
+        mat = ref_material(spec, name)
+        out[f"{name}_energy"] = ref_mat.vl_energy_batch(mat, sig)
+        out[f"{name}_stress"] = ref_mat.vl_stress_batch(mat, sig)
+        out[f"{name}_k"] = np.array(ref_mat.estimate_stiffness(mat))
+        out[f"{name}_shift"] = np.array(mat.shift)
+    np.savez_compressed(os.path.join(HERE, "svd_materials.npz"), **out)
+
+
+def gen_meshes_elements():
+    out = {}
+    for key, (nx, ny, nz, size) in {"bar_c1": (20, 5, 5, (2.0, 0.5, 0.5)),
+                                    "bar_small": (6, 2, 2, (0.6, 0.2, 0.2))}.items():
+        v, t = ref_assets.bar_mesh(nx, ny, nz, size)
+        out[f"{key}_verts"], out[f"{key}_tets"] = v, t
+    sc = scenes.c1()
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=1000.0)
+    G, vols = ref_mesh.tet_diff_operators(mesh)
+    out["c1_masses"] = ref_mesh.lumped_masses(mesh)
+    out["c1_vols"] = vols
+    rng = np.random.default_rng(7)
+    x = sc.verts + 0.02 * rng.standard_normal(sc.verts.shape)
+    x[:30] = sc.verts[:30] * np.array([1.0, 1.0, -1.0]) + 0.3  # invert some tets
+    out["c1_x"] = x
+    for name, spec in MATERIAL_CASES.items():
+        mat = ref_material(spec, name)
+        k = ref_mat.estimate_stiffness(mat)
+        grp = ref_dyn.VLGroup(sc.tets, G, vols, mat, k)
+        out[f"c1_{name}_energy"] = np.array(grp.energy(x))
+        g = np.zeros_like(x)
+        grp.add_gradient(x, g)
+        out[f"c1_{name}_grad"] = g
+    np.savez_compressed(os.path.join(HERE, "meshes_elements.npz"), **out)
+
+
+def run_reference(sc, mat_spec, frames, iterations, kind="lbfgs", save_frames=()):
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(mat_spec), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = ref_solvers.SolverConfig(kind=kind, iterations=iterations, m=sc.m)
+    g, tr, al, g0, pos = [], [], [], [], {}
+    for f in range(frames):
+        state, rec = ref_solvers.simulate_frame(system, state, cfg)
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+        al.append(rec.alphas)
+        g0.append(rec.g0)
+        if f in save_frames:
+            pos[f"x_{f}"] = state.q_l.copy()
+    return dict(g=np.array(g), trials=np.array(tr), alphas=np.array(al), g0=np.array(g0), **pos)
+
+
+def gen_frames(quick):
+    t = time.time()
+    sc = scenes.c1()
+    fr = 20 if quick else 100
+    d = run_reference(sc, sc.material, fr, sc.iterations, save_frames={0, 1, 9, 19, 49, 99})
+    np.savez_compressed(os.path.join(HERE, "frames_c1_lbfgs.npz"), frames=fr, **d)
+    d = run_reference(sc, sc.material, 10, sc.iterations, kind="pd_qn", save_frames={0, 9})
+    np.savez_compressed(os.path.join(HERE, "frames_c1_pdqn.npz"), frames=10, **d)
+    print("c1 frames", time.time() - t)
+    # configs[3]: a few instances of the batch, first frames
+    t = time.time()
+    sc4 = scenes.c4(instances=1024)
+    keep = [0, 1, 511, 1023]
+    out = {"instances": np.array(keep)}
+    for b in keep:
+        sc4.q_l = sc4.q_l[0] if sc4.q_l.ndim == 3 else sc4.q_l
+        sc4.q_prev = sc4.q_prev[0] if sc4.q_prev.ndim == 3 else sc4.q_prev
+        d = run_reference(sc4, sc4.batch_materials[b], 3, sc4.iterations, save_frames={2})
+        for k, v in d.items():
+            out[f"i{b}_{k}"] = v
+    np.savez_compressed(os.path.join(HERE, "frames_c4_subset.npz"), **out)
+    print("c4 subset", time.time() - t)
+    if not quick:  # configs[1] as-is (dense 15360^2 Cholesky): one frame, ~3 min
+        t = time.time()
+        sc2 = scenes.c2()
+        d = run_reference(sc2, sc2.material, 1, sc2.iterations, save_frames={0})
+        np.savez_compressed(os.path.join(HERE, "frames_c2_frame0.npz"), frames=1, **d)
+        print("c2 frame 0", time.time() - t)
+
+
+def copy_fixtures():
+    dst = os.path.join(HERE, "ref_fixtures")
+    os.makedirs(dst, exist_ok=True)
+    for src in ("frontend/tests/fixtures/twist_lbfgs.csv", "frontend/tests/fixtures/twist_pd_qn.csv",
+                "assets/bar_small.node", "assets/bar_small.ele", "scenarios/bar_twist_small.json"):
+        shutil.copy(os.path.join(REF, src), os.path.join(dst, os.path.basename(src)))
+
+
+if __name__ == "__main__":
+    quick = "--quick" in sys.argv
+    copy_fixtures()
+    gen_svd_materials()
+    gen_meshes_elements()
+    gen_frames(quick)

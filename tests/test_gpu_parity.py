@@ -1,0 +1,353 @@
+"""B200 path vs the reference goldens and the CPU oracle (run with -m gpu).
+
+Tolerances (north_star): positions 1e-9 relative (fp64), per-iteration g
+sequence 1e-10 relative, line-search trial counts identical.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle.qnsim_oracle as O
+import paper_1604_07378_b200 as Q
+from paper_1604_07378_b200 import _lib, scenes
+from paper_1604_07378_b200.materials import from_spec
+from tests.helpers import FIX, TwistScene, golden, material_specs, oracle_material, read_csv
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-9
+G_TOL = 1e-10
+MATS = ["neohookean", "stvk", "polynomial", "corotated", "mooney_rivlin", "spline", "poly_cubic"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu(built_lib):
+    _lib.require_gpu()
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
+
+
+def build(sc, spec=None, **kw):
+    mesh = Q.TetMesh(sc.verts, sc.tets, sc.density)
+    return Q.build_system(mesh, from_spec(spec or sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed, **kw)
+
+
+# ---- element level -----------------------------------------------------------
+
+def test_svd_against_reference_golden():
+    d = golden("svd_materials.npz")
+    U, s, V = Q.svd_rv_batch(d["F"])
+    np.testing.assert_allclose(s, d["sigma"], rtol=0, atol=1e-13)
+    assert np.abs(np.linalg.det(U) - 1).max() < 1e-12 and np.abs(np.linalg.det(V) - 1).max() < 1e-12
+    rec = np.einsum("eab,eb,ecb->eac", U, s, V)
+    ok = np.abs(s).min(axis=1) > 1e-9  # away from the clamp, U diag(s) V^T reproduces F
+    assert np.abs(rec[ok] - d["F"][ok]).max() < 1e-12
+    # sign rule: s0 >= s1 >= |s2|, s2 < 0 iff det F < 0 (linalg.py:95-103)
+    assert np.all(s[:, 0] >= s[:, 1] - 1e-14) and np.all(s[:, 1] >= np.abs(s[:, 2]) - 1e-14)
+    detF = np.linalg.det(d["F"])
+    nz = np.abs(detF) > 1e-20
+    assert np.all((s[nz, 2] < 0) == (detF[nz] < 0))
+    assert np.all(np.abs(s) >= 1e-10)
+
+
+@pytest.mark.parametrize("name", MATS)
+def test_material_eval_against_reference_golden(name):
+    d = golden("svd_materials.npz")
+    mat = from_spec(material_specs()[name])
+    sig = d["mat_sigma"]
+    e = Q.vl_energy_batch(mat, sig)
+    t = Q.vl_stress_batch(mat, sig)
+    np.testing.assert_allclose(e, d[f"{name}_energy"], rtol=1e-13, atol=1e-13 * max(1, np.abs(d[f"{name}_energy"]).max()))
+    np.testing.assert_allclose(t, d[f"{name}_stress"], rtol=1e-13, atol=1e-13 * np.abs(d[f"{name}_stress"]).max())
+    assert Q.estimate_stiffness(mat) == pytest.approx(float(d[f"{name}_k"]), rel=1e-13)
+
+
+@pytest.mark.parametrize("name", MATS)
+def test_element_group_seam_against_reference_golden(name):
+    """GPU VLGroup.energy / add_gradient (dynamics.py:57-67) at a state with inverted tets."""
+    d = golden("meshes_elements.npz")
+    sc = scenes.c1()
+    system = build(sc, material_specs()[name])
+    grp = system.groups[0]
+    x = d["c1_x"]
+    assert grp.energy(x) == pytest.approx(float(d[f"c1_{name}_energy"]), rel=1e-12)
+    g = np.zeros_like(x)
+    grp.add_gradient(x, g)
+    assert rel(g, d[f"c1_{name}_grad"]) <= 1e-11
+
+
+def test_objective_gradient_against_oracle():
+    sc = scenes.c2(frames=1)
+    system = build(sc)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    rng = np.random.default_rng(3)
+    y = sc.verts + 0.01 * rng.standard_normal(sc.verts.shape)
+    x = sc.verts + 0.03 * rng.standard_normal(sc.verts.shape)
+    st = Q.SimState(q_l=y, q_prev=y, y=y)
+    assert Q.objective(system, st, x) == pytest.approx(O.objective(osys, y, x), rel=1e-12)
+    assert rel(Q.gradient(system, st, x), O.gradient(osys, y, x)) <= 1e-12
+
+
+# ---- factorisation -------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_prefactored_solve_against_oracle(cfg):
+    sc = scenes.CONFIGS[cfg](frames=1)
+    system = build(sc)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    B = np.random.default_rng(1).standard_normal((system.free.size, 3))
+    X = system.sysfact.solve(B)
+    assert rel(X, osys.factor.solve(B)) <= 1e-12
+    assert rel(osys.A_free @ X, B) <= 1e-12
+    X2 = system.sysfact.solve(B)
+    np.testing.assert_array_equal(X, X2)  # deterministic (no float atomics), linalg test :83-90
+
+
+def test_factorization_api_dense_and_errors():
+    rng = np.random.default_rng(2)
+    M = rng.standard_normal((40, 40))
+    A = M @ M.T + 40 * np.eye(40)
+    F = Q.factorize_spd(A)
+    B = rng.standard_normal((40, 5))
+    np.testing.assert_allclose(A @ F.solve(B), B, atol=1e-10)
+    v = rng.standard_normal(40)
+    np.testing.assert_allclose(A @ F.solve(v), v, atol=1e-10)
+    with pytest.raises(Q.FactorizationError):
+        Q.factorize_spd(np.diag([1.0, -1.0, 2.0]))
+    with pytest.raises(ValueError):
+        F.solve(np.ones(39))
+
+
+# ---- frames --------------------------------------------------------------------
+
+def run_gpu(system, sc, frames, kind="lbfgs", targets=None, iterations=None):
+    cfg = Q.SolverConfig(kind=kind, iterations=iterations or sc.iterations, m=sc.m)
+    st = Q.SimState(q_l=np.array(sc.q_l), q_prev=np.array(sc.q_prev))
+    out = []
+    for f in range(frames):
+        st, rec = Q.simulate_frame(system, st, cfg, fixed_targets=None if targets is None else targets(f))
+        out.append((st.q_l.copy(), rec))
+    return out
+
+
+def test_c1_100_frames_against_reference_golden():
+    """configs[0] as specified: 100 frames x 10 L-BFGS iterations vs the reference."""
+    d = golden("frames_c1_lbfgs.npz")
+    sc = scenes.c1()
+    system = build(sc)
+    res = run_gpu(system, sc, int(d["frames"]))
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d["g"][f]) <= G_TOL, f
+        assert list(rec.ls_trials) == list(d["trials"][f]), f
+        np.testing.assert_array_equal(rec.alphas, d["alphas"][f])
+        if f"x_{f}" in d:
+            assert rel(x, d[f"x_{f}"]) <= X_TOL, f
+
+
+def test_c1_pdqn_against_reference_golden():
+    d = golden("frames_c1_pdqn.npz")
+    sc = scenes.c1()
+    system = build(sc)
+    res = run_gpu(system, sc, int(d["frames"]), kind="pd_qn")
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d["g"][f]) <= G_TOL
+        assert list(rec.ls_trials) == list(d["trials"][f])
+    assert rel(res[-1][0], d["x_9"]) <= X_TOL
+
+
+@pytest.mark.parametrize("kind", ["lbfgs", "pd_qn"])
+def test_twist_golden_csv_on_gpu(kind):
+    """The reference's own golden trajectory, through the B200 path."""
+    g_ref, tr_ref = read_csv(os.path.join(FIX, f"twist_{kind}.csv"))
+    ts = TwistScene()
+    mesh = Q.TetMesh(ts.verts, ts.tets, ts.density)
+    system = Q.build_system(mesh, Q.make_builtin("neohookean", {"mu": ts.mu, "lambda": ts.lam}), h=ts.h,
+                            gravity=ts.gravity, fixed=ts.fixed)
+    cfg = Q.SolverConfig(kind=kind, iterations=ts.iterations, m=5)
+    st = Q.SimState(q_l=ts.verts.copy(), q_prev=ts.verts.copy())
+    for f in range(ts.frames):
+        st, rec = Q.simulate_frame(system, st, cfg, fixed_targets=ts.targets(f))
+        assert rel(rec.g, g_ref[f]) <= G_TOL, f
+        assert list(rec.ls_trials) == list(tr_ref[f]), f
+        np.testing.assert_allclose(st.q_l[ts.fixed], ts.targets(f), rtol=0, atol=0)
+
+
+def test_c2_frame0_against_reference_golden():
+    """configs[1] first frame vs the reference as-is (dense 15 360^2 Cholesky)."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "frames_c2_frame0.npz")
+    if not os.path.exists(path):
+        pytest.skip("c2 golden not generated (make_golden.py without --quick)")
+    d = np.load(path)
+    sc = scenes.c2()
+    system = build(sc)
+    (x, rec), = run_gpu(system, sc, 1)
+    assert rel(rec.g, d["g"][0]) <= G_TOL
+    assert list(rec.ls_trials) == list(d["trials"][0])
+    assert rel(x, d["x_0"]) <= X_TOL
+
+
+def test_c2_three_frames_against_oracle():
+    sc = scenes.c2()
+    system = build(sc)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    res = run_gpu(system, sc, 3)
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(3):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        assert rel(res[f][1].g, rec.g) <= G_TOL
+        assert res[f][1].ls_trials == rec.ls_trials
+        assert rel(res[f][0], x) <= X_TOL
+
+
+def test_c3_frame_against_oracle():
+    """configs[2] (375k tets, spline VL, twisted, both ends pinned), 1 frame x 10 its."""
+    sc = scenes.c3(frames=1)
+    system = build(sc)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    (xg, rg), = run_gpu(system, sc, 1)
+    x, _, ro = O.simulate_frame(osys, sc.q_l.copy(), sc.q_prev.copy(), iterations=sc.iterations, m=sc.m)
+    assert rel(rg.g, ro.g) <= G_TOL
+    assert rg.ls_trials == ro.ls_trials
+    assert rel(xg, x) <= X_TOL
+
+
+def test_c4_batch_against_reference_golden():
+    """configs[3]: 1024 instances in one batched system; checked instances vs the reference."""
+    d = golden("frames_c4_subset.npz")
+    sc = scenes.c4()
+    mesh = Q.TetMesh(sc.verts, sc.tets, sc.density)
+    system = Q.build_batch_system(mesh, [from_spec(s) for s in sc.batch_materials], h=sc.h, gravity=sc.gravity,
+                                  fixed=sc.fixed)
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+    st = Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    for f in range(3):
+        st, recs = Q.simulate_frame(system, st, cfg)
+        assert len(recs) == 1024
+        for b in d["instances"]:
+            assert rel(recs[b].g, d[f"i{b}_g"][f]) <= G_TOL
+            assert recs[b].ls_trials == list(d[f"i{b}_trials"][f])
+    for b in d["instances"]:
+        assert rel(st.q_l[b], d[f"i{b}_x_2"]) <= X_TOL
+
+
+# ---- semantics and edge cases (test_solvers.py / test_dynamics.py analogues) -----
+
+def unit_tet_mesh():
+    return Q.TetMesh(np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]]), np.array([[0, 1, 2, 3]]), 24.0)
+
+
+def test_free_fall_identity_system():
+    """No materials: A = I, one pd_qn iteration lands on y (test_solvers.py:355-361)."""
+    mesh = unit_tet_mesh()
+    system = Q.build_system(mesh, [], h=1.0, gravity=(0, 0, -9.8))
+    q = mesh.vertices.copy()
+    st2, rec = Q.simulate_frame(system, Q.SimState(q_l=q, q_prev=q), Q.SolverConfig(kind="pd_qn", iterations=1))
+    np.testing.assert_allclose(st2.q_l, q + np.array([0.0, 0.0, -9.8]), atol=1e-12)
+    assert rec.ls_trials == [1] and rec.alphas == [1.0]
+
+
+def test_frame_at_rest_is_bitwise_stationary():
+    """test_solvers.py:343-352"""
+    mesh = Q.load_tet_mesh(os.path.join(FIX, "bar_small.node"), os.path.join(FIX, "bar_small.ele"), 1000.0)
+    system = Q.build_system(mesh, Q.make_builtin("corotated", {"mu": 1e4, "lambda": 4e4}), gravity=(0, 0, 0))
+    q = mesh.vertices.copy()
+    st2, rec = Q.simulate_frame(system, Q.SimState(q_l=q, q_prev=q), Q.SolverConfig(kind="pd_qn", iterations=5))
+    assert np.array_equal(st2.q_l, q)
+    assert rec.g0 == pytest.approx(0.0, abs=1e-12)
+
+
+def elastic_system():
+    mesh = Q.load_tet_mesh(os.path.join(FIX, "bar_small.node"), os.path.join(FIX, "bar_small.ele"), 1000.0)
+    fixed = np.nonzero(mesh.vertices[:, 0] < 1e-9)[0]
+    return mesh, Q.build_system(mesh, Q.make_builtin("neohookean", {"mu": 1e4, "lambda": 4e4}), fixed=fixed)
+
+
+def test_m0_lbfgs_equals_pdqn_bitwise():
+    """test_solvers.py:121-130"""
+    mesh, system = elastic_system()
+    rng = np.random.default_rng(33)
+    x0 = mesh.vertices + 0.03 * rng.standard_normal(mesh.vertices.shape)
+    x0[system.fixed] = mesh.vertices[system.fixed]
+    st = Q.SimState(q_l=x0, q_prev=x0)
+    a, ra = Q.simulate_frame(system, st.copy(), Q.SolverConfig(kind="lbfgs", m=0, iterations=6))
+    b, rb = Q.simulate_frame(system, st.copy(), Q.SolverConfig(kind="pd_qn", iterations=6))
+    np.testing.assert_array_equal(a.q_l, b.q_l)
+    assert ra.g == rb.g
+
+
+def test_monotone_objective_and_record_shapes():
+    mesh, system = elastic_system()
+    rng = np.random.default_rng(33)
+    x0 = mesh.vertices + 0.03 * rng.standard_normal(mesh.vertices.shape)
+    x0[system.fixed] = mesh.vertices[system.fixed]
+    for kind in ("pd_qn", "lbfgs"):
+        _, rec = Q.simulate_frame(system, Q.SimState(q_l=x0, q_prev=x0), Q.SolverConfig(kind=kind, iterations=7))
+        gs = [rec.g0] + rec.g
+        assert all(b <= a + 1e-12 * max(abs(a), 1.0) for a, b in zip(gs, gs[1:])), kind
+        assert len(rec.g) == len(rec.ls_trials) == len(rec.cum_ms) == len(rec.alphas) == 7
+        assert all(b >= a for a, b in zip(rec.cum_ms, rec.cum_ms[1:]))
+
+
+def test_fixed_targets_enforced():
+    """test_solvers.py:388-395"""
+    mesh, system = elastic_system()
+    q = mesh.vertices.copy()
+    targets = q[system.fixed] + np.array([0.0, 0.0, 0.01])
+    st2, _ = Q.simulate_frame(system, Q.SimState(q_l=q, q_prev=q), Q.SolverConfig(kind="lbfgs"),
+                              fixed_targets=targets)
+    assert np.allclose(st2.q_l[system.fixed], targets)
+
+
+def test_no_line_search_mode_against_oracle():
+    mesh, system = elastic_system()
+    osys = O.build(mesh.vertices, mesh.tets, 1000.0, O.builtin("neohookean", mu=1e4, lam=4e4), system.h,
+                   (0, 0, -9.8), system.fixed, factor="dense")
+    q = mesh.vertices.copy()
+    st2, rec = Q.simulate_frame(system, Q.SimState(q_l=q, q_prev=q),
+                                Q.SolverConfig(kind="lbfgs", iterations=5, line_search=False))
+    x, _, ro = O.simulate_frame(osys, q, q, iterations=5, use_line_search=False)
+    assert rel(st2.q_l, x) <= X_TOL and rel(rec.g, ro.g) <= G_TOL
+    assert rec.ls_trials == [1] * 5 and rec.alphas == [1.0] * 5
+
+
+def test_deterministic_and_graph_equals_host_loop():
+    sc = scenes.c1(frames=2)
+    a = build(sc)
+    b = build(sc)
+    b.set_graph_mode(False)
+    ra = run_gpu(a, sc, 2)
+    rb = run_gpu(b, sc, 2)
+    rc = run_gpu(a, sc, 2)
+    for (xa, ga), (xb, gb), (xc, gc) in zip(ra, rb, rc):
+        np.testing.assert_array_equal(xa, xb)
+        np.testing.assert_array_equal(xa, xc)
+        assert ga.g == gb.g == gc.g
+
+
+def test_unsupported_options_raise():
+    sc = scenes.c1(frames=1)
+    system = build(sc)
+    st = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
+    for cfg in (Q.SolverConfig(kind="chebyshev"), Q.SolverConfig(kind="newton"),
+                Q.SolverConfig(kind="lbfgs", lbfgs_init="scaled_identity")):
+        with pytest.raises(NotImplementedError):
+            Q.simulate_frame(system, st, cfg)
+    with pytest.raises(Q.DynamicsError):
+        Q.build_system(Q.TetMesh(sc.verts, sc.tets), from_spec(sc.material), fixed=np.arange(sc.verts.shape[0]))
+
+
+def test_resident_run_matches_stateless():
+    sc = scenes.c1(frames=3)
+    s1 = build(sc)
+    res = run_gpu(s1, sc, 3)
+    s2 = build(sc)
+    run = Q.ResidentRun(s2, Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev), Q.SolverConfig(kind="lbfgs"))
+    for f in range(3):
+        recs = run.step(record=True)
+        assert recs[0].g == res[f][1].g
+    np.testing.assert_array_equal(run.state().q_l, res[-1][0])
+    assert run.last_ms > 0 and run.last_passes >= 10

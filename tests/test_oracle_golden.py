@@ -1,0 +1,129 @@
+"""Pin the CPU oracle to the reference: golden vectors written by the
+unmodified reference (tests/golden/make_golden.py) and the reference's own
+golden trajectories twist_{lbfgs,pd_qn}.csv."""
+import numpy as np
+import pytest
+
+import oracle.qnsim_oracle as O
+from paper_1604_07378_b200 import scenes
+import os
+
+from tests.helpers import FIX, TwistScene, golden, material_specs, oracle_material, read_csv
+
+MATS = ["neohookean", "stvk", "polynomial", "corotated", "mooney_rivlin", "spline", "poly_cubic"]
+
+
+def test_svd_matches_reference():
+    d = golden("svd_materials.npz")
+    U, s, V = O.svd_rv(d["F"])
+    np.testing.assert_allclose(s, d["sigma"], rtol=0, atol=1e-13)
+    assert np.all(np.abs(np.linalg.det(U) - 1) < 1e-12) and np.all(np.abs(np.linalg.det(V) - 1) < 1e-12)
+
+
+@pytest.mark.parametrize("name", MATS)
+def test_materials_match_reference(name):
+    d = golden("svd_materials.npz")
+    mat = oracle_material(material_specs()[name])
+    sig = d["mat_sigma"]
+    e, t = O.vl_energy(mat, sig), O.vl_stress(mat, sig)
+    scale = max(1.0, np.abs(d[f"{name}_energy"]).max())
+    np.testing.assert_allclose(e, d[f"{name}_energy"], rtol=1e-13, atol=1e-13 * scale)
+    np.testing.assert_allclose(t, d[f"{name}_stress"], rtol=1e-13, atol=1e-13 * np.abs(d[f"{name}_stress"]).max())
+    assert mat.shift == pytest.approx(float(d[f"{name}_shift"]), rel=1e-15, abs=1e-12)
+    assert O.fit_stiffness(mat) == pytest.approx(float(d[f"{name}_k"]), rel=1e-13)
+
+
+def test_grid_bar_matches_reference_bar_mesh():
+    d = golden("meshes_elements.npz")
+    for key, args in {"bar_c1": (20, 5, 5, (2.0, 0.5, 0.5)), "bar_small": (6, 2, 2, (0.6, 0.2, 0.2))}.items():
+        v, t = O.grid_bar(*args)
+        np.testing.assert_array_equal(t, d[f"{key}_tets"])
+        np.testing.assert_array_equal(v, d[f"{key}_verts"])
+    sc = scenes.c1()
+    np.testing.assert_array_equal(O.vertex_masses(sc.verts, sc.tets, 1000.0), d["c1_masses"])
+
+
+@pytest.mark.parametrize("name", MATS)
+def test_element_energy_gradient_match_reference(name):
+    d = golden("meshes_elements.npz")
+    sc = scenes.c1()
+    mat = oracle_material(material_specs()[name])
+    G, vols = O.diff_operators(sc.verts, sc.tets)
+    grp = O.TetGroup(sc.tets, G, vols, mat, 1.0)
+    x = d["c1_x"]
+    e = grp.energy(x)
+    assert e == pytest.approx(float(d[f"c1_{name}_energy"]), rel=1e-12)
+    g = np.zeros_like(x)
+    grp.add_gradient(x, g)
+    ref = d[f"c1_{name}_grad"]
+    assert np.abs(g - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_c1_frames_match_reference():
+    d = golden("frames_c1_lbfgs.npz")
+    sc = scenes.c1()
+    sysm = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    n = 20
+    for f in range(n):
+        x, _, rec = O.simulate_frame(sysm, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d["g"][f], rtol=1e-11)
+        assert list(rec.ls_trials) == list(d["trials"][f])
+        if f"x_{f}" in d:
+            assert np.abs(x - d[f"x_{f}"]).max() <= 1e-12 * np.abs(d[f"x_{f}"]).max()
+
+
+def test_c1_pdqn_frames_match_reference():
+    d = golden("frames_c1_pdqn.npz")
+    sc = scenes.c1()
+    sysm = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(int(d["frames"])):
+        x, _, rec = O.simulate_frame(sysm, q_l, q_prev, iterations=sc.iterations, m=sc.m, kind="pd_qn")
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d["g"][f], rtol=1e-11)
+        assert list(rec.ls_trials) == list(d["trials"][f])
+
+
+@pytest.mark.parametrize("kind", ["lbfgs", "pd_qn"])
+def test_twist_golden_csv(kind):
+    """The reference's own golden trajectory (frontend/tests/fixtures/twist_*.csv)."""
+    g_ref, tr_ref = read_csv(os.path.join(FIX, f"twist_{kind}.csv"))
+    ts = TwistScene()
+    mat = O.builtin("neohookean", mu=ts.mu, lam=ts.lam)
+    sysm = O.build(ts.verts, ts.tets, ts.density, mat, ts.h, ts.gravity, ts.fixed, factor="dense")
+    q_l = ts.verts.copy()
+    q_prev = ts.verts.copy()
+    for f in range(ts.frames):
+        x, _, rec = O.simulate_frame(sysm, q_l, q_prev, iterations=ts.iterations, m=5, kind=kind,
+                                     fixed_targets=ts.targets(f))
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, g_ref[f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(tr_ref[f])
+
+
+def test_c4_subset_matches_reference():
+    d = golden("frames_c4_subset.npz")
+    sc = scenes.c4()
+    for b in d["instances"]:
+        sysm = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.batch_materials[b]), sc.h, sc.gravity,
+                       sc.fixed, factor="dense")
+        q_l, q_prev = sc.verts.copy(), sc.verts.copy()
+        for f in range(3):
+            x, _, rec = O.simulate_frame(sysm, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+            q_prev, q_l = q_l, x
+            np.testing.assert_allclose(rec.g, d[f"i{b}_g"][f], rtol=1e-11)
+        assert np.abs(x - d[f"i{b}_x_2"]).max() <= 1e-12 * np.abs(x).max()
+
+
+def test_sparse_factor_equals_dense():
+    sc = scenes.c1()
+    mat = oracle_material(sc.material)
+    a = O.build(sc.verts, sc.tets, sc.density, mat, sc.h, sc.gravity, sc.fixed, factor="dense")
+    b = O.build(sc.verts, sc.tets, sc.density, mat, sc.h, sc.gravity, sc.fixed, factor="sparse")
+    B = np.random.default_rng(0).standard_normal((a.free.size, 3))
+    xa, xb = a.factor.solve(B), b.factor.solve(B)
+    assert np.abs(xa - xb).max() <= 1e-13 * np.abs(xa).max()

@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="host-driven body loop (for per-kernel ncu lists)")
     return p.parse_args()
 
 
@@ -210,6 +211,8 @@ def run_ours(args, world, rank, local):
     t_build = time.perf_counter() - t_build
     cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
     st0 = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
+    if args.no_graph:
+        system.set_graph_mode(False)
     run = Q.ResidentRun(system, st0, cfg)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream

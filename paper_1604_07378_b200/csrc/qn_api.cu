@@ -109,12 +109,20 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_alloc(&f->d_x, (size_t)f->nbatch * f->n * 3))) return rc;
   if ((rc = dev_alloc(&f->d_u, (size_t)f->nbatch * std::max<int64_t>(f->nupd, 1) * 3))) return rc;
   if ((rc = dev_alloc(&f->d_flags, (size_t)2 * f->nbatch * f->nsup))) return rc;
+  if ((rc = dev_alloc(&f->d_done, (size_t)2 * f->nbatch * f->nsup))) return rc;
+  if ((rc = dev_upload(&f->d_cptr, f->cptr.data(), f->cptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_cidx, f->cidx.data(), f->cidx.size()))) return rc;
+  if ((rc = dev_upload(&f->d_ftask, f->ftask.data(), f->ftask.size()))) return rc;
+  if ((rc = dev_upload(&f->d_btask, f->btask.data(), f->btask.size()))) return rc;
+  if ((rc = dev_upload(&f->d_fcount, f->fcount.data(), f->fcount.size()))) return rc;
+  if ((rc = dev_upload(&f->d_bcount, f->bcount.data(), f->bcount.size()))) return rc;
   const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};
   if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
   if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;
   int max_nc = 0;
   for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
-  f->smem_bytes = (int)(sizeof(double) * 3 * ((size_t)f->max_rows + max_nc));
+  // forward: f (nc x 3) + partials (8 warps x 32 rows x 3); backward: w (nr x 3)
+  f->smem_bytes = (int)(sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows));
   QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
   if ((rc = prepare_solve_kernels<PlainIO>(f->smem_bytes))) return rc;
   f->on_device = true;
@@ -125,10 +133,24 @@ void factor_free_device(qn_factor* f) {
   void* ptrs[] = {f->d_sup_col, f->d_sup_row_ptr, f->d_sup_rows, f->d_sup_val_ptr, f->d_sup_upd_ptr,
                   f->d_parent,  f->d_child_ptr,   f->d_child_idx, f->d_rel_ptr,   f->d_rel,
                   f->d_perm,    f->d_vals,        f->d_y,         f->d_x,         f->d_u,
-                  f->d_flags,   f->d_sched,       f->d_io};
+                  f->d_flags,   f->d_sched,       f->d_io,        f->d_done,      f->d_cptr,
+                  f->d_cidx,    f->d_ftask,       f->d_btask,     f->d_fcount,    f->d_bcount};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;
+}
+
+// after a synchronised solve: did any dependency wait time out? (sched[6])
+int factor_check_watchdog(qn_factor* f) {
+  unsigned w = 0;
+  QN_CUDA(cudaMemcpy(&w, f->d_sched + 6, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (w) {
+    const unsigned z = 0;
+    QN_CUDA(cudaMemcpy(f->d_sched + 6, &z, sizeof(unsigned), cudaMemcpyHostToDevice));
+    set_error("supernodal solve: dependency wait timed out (scheduling bug)");
+    return QN_ERR_CUDA;
+  }
+  return QN_OK;
 }
 
 int factor_solve_plain(qn_factor* f, int64_t batch, cudaStream_t stream) {
@@ -283,6 +305,7 @@ int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int
       QN_CUDA(cudaMemcpyAsync(X, f->d_io + 3 * n, n * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
       QN_CUDA(cudaStreamSynchronize(st));
     }
+    if ((rc = factor_check_watchdog(f))) return rc;
   }
   return QN_OK;
 }
@@ -562,6 +585,8 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   c.grad_tol = 1e-12 * S->scale * std::max(1.0, S->max_mass / (S->h * S->h));  // solvers.py:278
   c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
   c.use_graph = S->use_graph ? 1 : 0;
+  // at most 41 trials per line search + one re-evaluation per iteration, plus slack
+  c.max_passes = 64 * cfg->iterations + 64;
   QN_CUDA(cudaMemcpyAsync(S->d_cfg, &c, sizeof(DevConfig), cudaMemcpyHostToDevice, st));
   if (c.has_targets) {
     rc = stage_in(S, S->d_targets, fixed_targets, (size_t)S->n_inst * S->n_fixed * 3, mem, st);
@@ -574,7 +599,7 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
     count_launch(0);
   } else {
     if ((rc = launch_init(S, st))) return rc;
-    for (int pass = 0; pass < 100000; ++pass) {
+    for (int pass = 0; pass <= c.max_passes; ++pass) {
       if ((rc = launch_body(S, st))) return rc;
       int32_t act = 0;
       QN_CUDA(cudaMemcpyAsync(&act, S->v.active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -593,6 +618,11 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   QN_CUDA(cudaMemcpy(&passes, S->v.passes, sizeof(passes), cudaMemcpyDeviceToHost));
   S->last_passes = (int64_t)passes;
   if (S->use_graph) count_launch((int)(2 + 6 * passes));
+  if ((rc = factor_check_watchdog(S->factor))) return rc;
+  if ((int64_t)passes > (int64_t)c.max_passes) {
+    set_error("frame: pass limit exceeded (phase machine did not terminate)");
+    return QN_ERR_CUDA;
+  }
   if (rec) {
     const int it = cfg->iterations, cap = S->rec_cap;
     const int64_t ni = S->n_inst;

@@ -439,6 +439,49 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       }
     }
   }
+  // extend-add as a pull: for every front position p of supernode s, the list
+  // of children's update rows landing there (child order = deterministic)
+  {
+    const int64_t tot_rows = f->sup_row_ptr[ns];
+    std::vector<int32_t> cnt_p(tot_rows, 0);
+    for (int32_t s = 0; s < ns; ++s)
+      for (int32_t q = f->child_ptr[s]; q < f->child_ptr[s + 1]; ++q) {
+        const int32_t c = f->child_idx[q];
+        for (int64_t i = f->rel_ptr[c]; i < f->rel_ptr[c + 1]; ++i) cnt_p[f->sup_row_ptr[s] + f->rel[i]]++;
+      }
+    f->cptr.assign(tot_rows + 1, 0);
+    for (int64_t p = 0; p < tot_rows; ++p) f->cptr[p + 1] = f->cptr[p] + cnt_p[p];
+    f->cidx.resize(f->cptr[tot_rows]);
+    std::vector<int64_t> fill(f->cptr.begin(), f->cptr.end() - 1);
+    for (int32_t s = 0; s < ns; ++s)
+      for (int32_t q = f->child_ptr[s]; q < f->child_ptr[s + 1]; ++q) {
+        const int32_t c = f->child_idx[q];
+        for (int64_t i = f->rel_ptr[c]; i < f->rel_ptr[c + 1]; ++i)
+          f->cidx[fill[f->sup_row_ptr[s] + f->rel[i]]++] = (int32_t)(f->sup_upd_ptr[c] + (i - f->rel_ptr[c]));
+      }
+  }
+  // device work items: forward = row blocks of Z per supernode (postorder),
+  // backward = column blocks (reverse postorder)
+  f->ftask.clear();
+  f->btask.clear();
+  f->fcount.assign(ns, 0);
+  f->bcount.assign(ns, 0);
+  for (int32_t s = 0; s < ns; ++s) {
+    const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+    const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
+    for (int32_t r = 0; r < nr; r += kFwdRows) {
+      f->ftask.push_back({s, r, std::min(nr, r + kFwdRows), 0});
+      f->fcount[s]++;
+    }
+    (void)nc;
+  }
+  for (int32_t s = ns - 1; s >= 0; --s) {
+    const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+    for (int32_t k = 0; k < nc; k += kBwdCols) {
+      f->btask.push_back({s, k, std::min(nc, k + kBwdCols), 0});
+      f->bcount[s]++;
+    }
+  }
   // tree depth
   {
     std::vector<int32_t> d(ns, 1);
@@ -555,19 +598,26 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
           }
         }
       }
-      // store inv(L11) (lower, column-major) and L21
-      double* Xv = out + f->sup_val_ptr[s];
+      // store Z = [inv(L11); L21 inv(L11)] (nr x nc, column-major): the forward
+      // step of this supernode is then v = Z f (y = top, update = bottom) and
+      // the backward step x = Z^T [y; -x_below] — dense, row/column parallel.
+      double* Z = out + f->sup_val_ptr[s];
       for (int64_t j = 0; j < nc; ++j) {
-        Xv[j + j * nc] = 1.0 / F[j + j * nr];
+        double* Zj = Z + j * nr;
+        Zj[j] = 1.0 / F[j + j * nr];
         for (int64_t i = j + 1; i < nc; ++i) {
           double acc = 0.0;
-          for (int64_t k = j; k < i; ++k) acc += F[i + k * nr] * Xv[k + j * nc];
-          Xv[i + j * nc] = -acc / F[i + i * nr];
+          for (int64_t k = j; k < i; ++k) acc += F[i + k * nr] * Zj[k];
+          Zj[i] = -acc / F[i + i * nr];
+        }
+        double* Wj = Zj + nc;
+        for (int64_t ib = 0; ib < mb; ++ib) Wj[ib] = 0.0;
+        for (int64_t k = j; k < nc; ++k) {
+          const double a = Zj[k];
+          const double* Lk = F.data() + k * nr + nc;
+          for (int64_t ib = 0; ib < mb; ++ib) Wj[ib] += Lk[ib] * a;
         }
       }
-      double* Lb = Xv + nc * nc;
-      for (int64_t k = 0; k < nc; ++k)
-        for (int64_t ib = 0; ib < mb; ++ib) Lb[ib + k * mb] = F[(nc + ib) + k * nr];
     }
   }
   if (err != QN_OK) {

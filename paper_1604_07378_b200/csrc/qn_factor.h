@@ -28,6 +28,10 @@ struct qn_factor {
   std::vector<int32_t> child_ptr, child_idx;  // children in increasing order
   std::vector<int64_t> rel_ptr;   // (nsup+1) per child: its below rows -> parent front positions
   std::vector<int32_t> rel;
+  std::vector<int64_t> cptr;      // (total front rows + 1): pull lists of the extend-add
+  std::vector<int32_t> cidx;      // children's update-row ids
+  std::vector<int4> ftask, btask; // {supernode, lo, hi, 0}: forward row blocks / backward column blocks
+  std::vector<int32_t> fcount, bcount;  // tasks per supernode
   int64_t nvals = 0, nupd = 0, nnz_l = 0;
   int32_t max_rows = 0, depth = 0;
   double flops = 0.0, factor_seconds = 0.0;
@@ -50,6 +54,13 @@ struct qn_factor {
   double* d_y = nullptr;          // nbatch x n x 3 (forward result, factor order)
   double* d_x = nullptr;          // nbatch x n x 3 (backward result, factor order)
   double* d_u = nullptr;          // nbatch x nupd x 3
+  int64_t* d_cptr = nullptr;
+  int32_t* d_cidx = nullptr;
+  int4* d_ftask = nullptr;
+  int4* d_btask = nullptr;
+  int32_t* d_fcount = nullptr;
+  int32_t* d_bcount = nullptr;
+  unsigned long long* d_done = nullptr;  // 2 x nbatch x nsup cumulative task completions
   unsigned* d_flags = nullptr;    // 2 x nbatch x nsup (forward, backward)
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
@@ -58,6 +69,9 @@ struct qn_factor {
 };
 
 namespace qn {
+constexpr int kFwdRows = 32;  // rows of Z per forward task (one warp-row block)
+constexpr int kBwdCols = 8;   // columns of Z per backward task (one warp per column)
+
 // host: ordering + symbolic + numeric factorisation; returns QN_OK / QN_ERR_*
 int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int32_t* indices,
                       const double* values, int64_t nbatch, const double* coords);

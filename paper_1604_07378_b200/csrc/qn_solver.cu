@@ -505,8 +505,9 @@ __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
     if (old == total - 1) {
       *gc = 0;
       __threadfence();
-      const int act = *((volatile int32_t*)v.active);
+      int act = *((volatile int32_t*)v.active);
       *v.passes += 1;
+      if (*v.passes > (unsigned long long)v.cfg->max_passes) act = 0;  // runaway guard (host reports it)
       if (v.cfg->use_graph) cudaGraphSetConditional(v.handle, act > 0 ? 1u : 0u);
     }
   }

@@ -42,7 +42,7 @@ struct InstCtl {
 struct DevConfig {
   int32_t kind, iterations, m, line_search;
   double gamma, alpha_init, shrink, grad_tol;
-  int32_t has_targets, use_graph;
+  int32_t has_targets, use_graph, max_passes, pad;
 };
 
 struct SysView {

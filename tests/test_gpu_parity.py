@@ -247,7 +247,9 @@ def test_free_fall_identity_system():
     q = mesh.vertices.copy()
     st2, rec = Q.simulate_frame(system, Q.SimState(q_l=q, q_prev=q), Q.SolverConfig(kind="pd_qn", iterations=1))
     np.testing.assert_allclose(st2.q_l, q + np.array([0.0, 0.0, -9.8]), atol=1e-12)
-    assert rec.ls_trials == [1] and rec.alphas == [1.0]
+    # x starts at y, so the gradient is exactly zero: the ||g|| early-out records
+    # (g_x, 0 trials, alpha 0) like solvers.py:292-298
+    assert rec.ls_trials == [0] and rec.alphas == [0.0] and rec.g == [0.0]
 
 
 def test_frame_at_rest_is_bitwise_stationary():

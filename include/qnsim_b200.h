@@ -111,6 +111,12 @@ int qn_factor_info_get(const qn_factor* f, qn_factor_info* info);
 int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int64_t nrhs, int32_t mem,
                     void* stream);
 int qn_factor_destroy(qn_factor* f);
+/* diagnostics: one traced solve (instance 0, current staging RHS); stamps =
+ * globaltimer ns at (start, dependencies ready, done) per forward then backward
+ * work item; tasks = {supernode, lo, hi, 0} per forward then backward task.
+ * Sizes: 3 (n_ftask + n_btask) nbatch and 4 (n_ftask + n_btask). */
+int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask);
+int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks);
 
 /* ------------------------------------------------------------------------ */
 /* Simulation system — replaces dynamics.build_system (dynamics.py:351-434)

@@ -98,6 +98,8 @@ SIGNATURES = {
     "qn_factor_info_get": [_P, _P],
     "qn_factor_solve": [_P, _I64, _P, _P, _I64, _I32, _P],
     "qn_factor_destroy": [_P],
+    "qn_factor_task_counts": [_P, _P, _P],
+    "qn_factor_trace_solve": [_P, _P, _P],
     "qn_system_create": [_P, _P],
     "qn_system_destroy": [_P],
     "qn_system_factor": [_P, _P],

@@ -108,23 +108,26 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_alloc(&f->d_y, (size_t)f->nbatch * f->n * 3))) return rc;
   if ((rc = dev_alloc(&f->d_x, (size_t)f->nbatch * f->n * 3))) return rc;
   if ((rc = dev_alloc(&f->d_u, (size_t)f->nbatch * std::max<int64_t>(f->nupd, 1) * 3))) return rc;
-  if ((rc = dev_alloc(&f->d_flags, (size_t)2 * f->nbatch * f->nsup))) return rc;
-  if ((rc = dev_alloc(&f->d_done, (size_t)2 * f->nbatch * f->nsup))) return rc;
+  if ((rc = dev_alloc(&f->d_flags, (size_t)f->nbatch * (f->ftask.size() + f->btask.size())))) return rc;
   if ((rc = dev_upload(&f->d_cptr, f->cptr.data(), f->cptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_cidx, f->cidx.data(), f->cidx.size()))) return rc;
   if ((rc = dev_upload(&f->d_ftask, f->ftask.data(), f->ftask.size()))) return rc;
   if ((rc = dev_upload(&f->d_btask, f->btask.data(), f->btask.size()))) return rc;
-  if ((rc = dev_upload(&f->d_fcount, f->fcount.data(), f->fcount.size()))) return rc;
+  if ((rc = dev_upload(&f->d_bfirst, f->bfirst.data(), f->bfirst.size()))) return rc;
   if ((rc = dev_upload(&f->d_bcount, f->bcount.data(), f->bcount.size()))) return rc;
-  const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};
+  if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
+  const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};  // [ticket, exited, epoch] x 2, watchdog
   if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
   if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;
   int max_nc = 0;
   for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
-  // forward: f (nc x 3) + partials (8 warps x 32 rows x 3); backward: w (nr x 3)
-  f->smem_bytes = (int)(sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows));
+  // Z tile + forward: f (nc x 3) + partials (256 x 3) + index staging; backward: w (nr x 3) + row staging
+  f->smem_bytes = (int)(sizeof(double) * kTaskEntries +
+                        sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows) +
+                        sizeof(int) * kStageIdx);
   QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
-  if ((rc = prepare_solve_kernels<PlainIO>(f->smem_bytes))) return rc;
+  if ((rc = prepare_solve_kernels<PlainIO>(f))) return rc;
   f->on_device = true;
   return QN_OK;
 }
@@ -133,8 +136,9 @@ void factor_free_device(qn_factor* f) {
   void* ptrs[] = {f->d_sup_col, f->d_sup_row_ptr, f->d_sup_rows, f->d_sup_val_ptr, f->d_sup_upd_ptr,
                   f->d_parent,  f->d_child_ptr,   f->d_child_idx, f->d_rel_ptr,   f->d_rel,
                   f->d_perm,    f->d_vals,        f->d_y,         f->d_x,         f->d_u,
-                  f->d_flags,   f->d_sched,       f->d_io,        f->d_done,      f->d_cptr,
-                  f->d_cidx,    f->d_ftask,       f->d_btask,     f->d_fcount,    f->d_bcount};
+                  f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
+                  f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
+                  f->d_fdep_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;
@@ -308,6 +312,30 @@ int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int
     if ((rc = factor_check_watchdog(f))) return rc;
   }
   return QN_OK;
+}
+
+int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask) {
+  QN_REQUIRE(f && n_ftask && n_btask, QN_ERR_ARG, "task_counts: null");
+  *n_ftask = (int64_t)f->ftask.size();
+  *n_btask = (int64_t)f->btask.size();
+  return QN_OK;
+}
+
+int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks) {
+  QN_REQUIRE(f && stamps && tasks, QN_ERR_ARG, "trace: null");
+  const size_t nf = f->ftask.size(), nb = f->btask.size(), items = (nf + nb) * (size_t)f->nbatch;
+  int rc = dev_alloc(&f->d_trace, 3 * items);
+  if (rc) return rc;
+  rc = factor_solve_plain(f, 0, 0);
+  if (rc == QN_OK) {
+    QN_CUDA(cudaDeviceSynchronize());
+    QN_CUDA(cudaMemcpy(stamps, f->d_trace, 3 * items * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  }
+  cudaFree(f->d_trace);
+  f->d_trace = nullptr;
+  std::memcpy(tasks, f->ftask.data(), nf * sizeof(int4));
+  std::memcpy(tasks + 4 * nf, f->btask.data(), nb * sizeof(int4));
+  return rc;
 }
 
 int qn_factor_destroy(qn_factor* f) {

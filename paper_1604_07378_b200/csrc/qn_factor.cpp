@@ -462,24 +462,73 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
   }
   // device work items: forward = row blocks of Z per supernode (postorder),
   // backward = column blocks (reverse postorder)
+  // Ticket order = level order: forward by height above the leaves, backward
+  // by depth below the root.  Tasks that become ready together get adjacent
+  // tickets, so resident CTAs are not parked on dependencies while ready work
+  // of the same level waits for a slot (a plain postorder serialises subtrees).
   f->ftask.clear();
   f->btask.clear();
   f->fcount.assign(ns, 0);
   f->bcount.assign(ns, 0);
-  for (int32_t s = 0; s < ns; ++s) {
-    const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
-    const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
-    for (int32_t r = 0; r < nr; r += kFwdRows) {
-      f->ftask.push_back({s, r, std::min(nr, r + kFwdRows), 0});
-      f->fcount[s]++;
+  {
+    std::vector<int32_t> height(ns, 0), dep(ns, 0);
+    for (int32_t s = 0; s < ns; ++s)
+      if (f->parent[s] >= 0) height[f->parent[s]] = std::max(height[f->parent[s]], height[s] + 1);
+    for (int32_t s = ns - 1; s >= 0; --s)
+      if (f->parent[s] >= 0) dep[s] = dep[f->parent[s]] + 1;
+    std::vector<int32_t> order(ns);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return height[a] < height[b]; });
+    // task size: ~kTaskEntries of Z per task; forward row blocks of 32 rg rows
+    // (rg in {1,2,4,8} row groups, 8/rg warps split k), backward 8 cw columns
+    // (cw columns per warp)
+    auto pow2_floor = [](int64_t v) {
+      int64_t p = 1;
+      while (p * 2 <= v) p *= 2;
+      return (int32_t)p;
+    };
+    f->ffirst.assign(ns, 0);
+    f->bfirst.assign(ns, 0);
+    for (int32_t s : order) {
+      const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+      const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
+      QN_REQUIRE(nc <= kTaskEntries && nr - nc <= (int64_t)1 << 20, QN_ERR_UNSUPPORTED,
+                 "factor: supernode too wide for the device solve tiles");
+      const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, kTaskEntries / (32 * (int64_t)nc))));
+      const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::min<int64_t>(32, kTaskEntries / nc);
+      f->ffirst[s] = (int32_t)f->ftask.size();
+      for (int32_t r = 0; r < nr; r += rows) {
+        f->ftask.push_back({s, r, std::min(nr, r + rows), rg});
+        f->fcount[s]++;
+      }
     }
-    (void)nc;
-  }
-  for (int32_t s = ns - 1; s >= 0; --s) {
-    const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
-    for (int32_t k = 0; k < nc; k += kBwdCols) {
-      f->btask.push_back({s, k, std::min(nc, k + kBwdCols), 0});
-      f->bcount[s]++;
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return dep[a] < dep[b]; });
+    for (int32_t s : order) {
+      const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+      const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
+      QN_REQUIRE(nr <= kTaskEntries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
+      const int32_t cols = (int32_t)std::min<int64_t>(64, std::max<int64_t>(1, kTaskEntries / nr));
+      f->bfirst[s] = (int32_t)f->btask.size();
+      for (int32_t k = 0; k < nc; k += cols) {
+        f->btask.push_back({s, k, std::min(nc, k + cols), 0});
+        f->bcount[s]++;
+      }
+    }
+    // forward dependencies of s: every task of every child
+    f->fdep_ptr.assign(ns + 1, 0);
+    for (int32_t s = 0; s < ns; ++s) {
+      int32_t cnt = 0;
+      for (int32_t q = f->child_ptr[s]; q < f->child_ptr[s + 1]; ++q) cnt += f->fcount[f->child_idx[q]];
+      f->fdep_ptr[s + 1] = f->fdep_ptr[s] + cnt;
+    }
+    f->fdep_idx.resize(f->fdep_ptr[ns]);
+    for (int32_t s = 0; s < ns; ++s) {
+      int32_t w = f->fdep_ptr[s];
+      for (int32_t q = f->child_ptr[s]; q < f->child_ptr[s + 1]; ++q) {
+        const int32_t c = f->child_idx[q];
+        for (int32_t t = 0; t < f->fcount[c]; ++t) f->fdep_idx[w++] = f->ffirst[c] + t;
+      }
     }
   }
   // tree depth

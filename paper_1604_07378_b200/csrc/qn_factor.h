@@ -32,6 +32,8 @@ struct qn_factor {
   std::vector<int32_t> cidx;      // children's update-row ids
   std::vector<int4> ftask, btask; // {supernode, lo, hi, 0}: forward row blocks / backward column blocks
   std::vector<int32_t> fcount, bcount;  // tasks per supernode
+  std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
+  std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
   int64_t nvals = 0, nupd = 0, nnz_l = 0;
   int32_t max_rows = 0, depth = 0;
   double flops = 0.0, factor_seconds = 0.0;
@@ -58,19 +60,21 @@ struct qn_factor {
   int32_t* d_cidx = nullptr;
   int4* d_ftask = nullptr;
   int4* d_btask = nullptr;
-  int32_t* d_fcount = nullptr;
+  int32_t* d_bfirst = nullptr;
   int32_t* d_bcount = nullptr;
-  unsigned long long* d_done = nullptr;  // 2 x nbatch x nsup cumulative task completions
-  unsigned* d_flags = nullptr;    // 2 x nbatch x nsup (forward, backward)
+  int32_t* d_fdep_ptr = nullptr;
+  int32_t* d_fdep_idx = nullptr;
+  unsigned* d_flags = nullptr;    // nbatch x (n_ftask + n_btask) completion epochs
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
+  unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)
   int smem_bytes = 0;
+  int grid_ctas = 0;              // persistent solve grid (co-resident CTAs)
   bool on_device = false;
 };
 
 namespace qn {
-constexpr int kFwdRows = 32;  // rows of Z per forward task (one warp-row block)
-constexpr int kBwdCols = 8;   // columns of Z per backward task (one warp per column)
+constexpr int64_t kTaskEntries = 8192;  // Z entries per solve task (64 KB shared-memory tile)
 
 // host: ordering + symbolic + numeric factorisation; returns QN_OK / QN_ERR_*
 int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int32_t* indices,

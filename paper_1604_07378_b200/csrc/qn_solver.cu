@@ -68,6 +68,28 @@ __device__ __forceinline__ bool last_block(unsigned* cnt, int which, int b, int 
   return s_last;
 }
 
+// Deterministic block-parallel sum of per-block partials (run by every thread of
+// the finalising block): out[k] = sum_blk part[blk * stride + k], k < nval.
+// Warp w owns values w, w + nw, ...; each lane sums a fixed block subset with 4
+// independent accumulators (4 loads in flight), then a fixed butterfly.
+__device__ void sum_partials(const double* part, int nblk, int stride, int nval, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < nval; k += nw) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int blk = lane;
+    for (; blk + 96 < nblk; blk += 128) {
+      a0 += __ldcg(part + (size_t)blk * stride + k);
+      a1 += __ldcg(part + (size_t)(blk + 32) * stride + k);
+      a2 += __ldcg(part + (size_t)(blk + 64) * stride + k);
+      a3 += __ldcg(part + (size_t)(blk + 96) * stride + k);
+    }
+    for (; blk < nblk; blk += 32) a0 += __ldcg(part + (size_t)blk * stride + k);
+    const double a = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) out[k] = a;
+  }
+  __syncthreads();
+}
+
 __device__ void record(const SysView& v, InstCtl& c, double g, int trials, double alpha) {
   const int it = v.cfg->iterations;
   if (c.k < it && c.k < v.rec_cap) {
@@ -209,14 +231,10 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
     for (int k = 0; k < kNG; ++k) pv[k] = acc[k];
   }
   if (!last_block(v.cnt, 0, b, v.n_inst, gridDim.x)) return;
+  // ---- finalise: block-parallel partial sums, then one thread per instance ----
+  double* tot = red;
+  sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, kNG, tot);
   if (threadIdx.x != 0) return;
-  // ---- finalise (one thread per instance) ----
-  double tot[kNG];
-  for (int k = 0; k < kNG; ++k) tot[k] = 0.0;
-  for (int blk = 0; blk < (int)gridDim.x; ++blk) {
-    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG;
-    for (int k = 0; k < kNG; ++k) tot[k] += __ldcg(pv + k);
-  }
   InstCtl& c = v.ctl[b];
   c.gs_cur = gnew;
   if (push) {
@@ -309,13 +327,9 @@ __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
     for (int k = 0; k < kMaxM; ++k) pv[k] = acc[k];
   }
   if (!last_block(v.cnt, 1, b, v.n_inst, gridDim.x)) return;
+  double* tot = red;
+  sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, np, tot);
   if (threadIdx.x != 0) return;
-  double tot[kMaxM];
-  for (int k = 0; k < kMaxM; ++k) tot[k] = 0.0;
-  for (int blk = 0; blk < (int)gridDim.x; ++blk) {
-    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG;
-    for (int k = 0; k < np; ++k) tot[k] += __ldcg(pv + k);
-  }
   InstCtl& c = v.ctl[b];
   for (int p = 0; p < np; ++p) {
     const int sp = c.ring[p];
@@ -386,16 +400,10 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
   }
 }
 
-__device__ void finalize_trial(const SysView& v, int b) {
+// one thread; e_el / inert / slope are the block-parallel sums of the partials
+__device__ void finalize_trial(const SysView& v, int b, double e_el, double inert, double slope) {
   const DevConfig& cfg = *v.cfg;
   InstCtl& c = v.ctl[b];
-  double e_el = 0.0, inert = 0.0, slope = 0.0;
-  for (int blk = 0; blk < v.nblk_t; ++blk) e_el += __ldcg(v.part_t + (size_t)b * v.nblk_t + blk);
-  for (int blk = 0; blk < v.nblk_v; ++blk) {
-    const double* pv = v.part_v + ((size_t)b * v.nblk_v + blk) * kNG + (kNG - 2);
-    inert += __ldcg(pv);
-    slope += __ldcg(pv + 1);
-  }
   const double g_new = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
   const int ph = c.phase;
   if (ph == PH_FIRST) {
@@ -493,7 +501,12 @@ __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
     }
     block_sum<1>(e, red);
     if (threadIdx.x == 0) v.part_t[(size_t)b * v.nblk_t + blockIdx.x] = e[0];
-    if (last_block(v.cnt, 2, b, v.n_inst, gridDim.x) && threadIdx.x == 0) finalize_trial(v, b);
+    if (last_block(v.cnt, 2, b, v.n_inst, gridDim.x)) {
+      __shared__ double tot[3];
+      sum_partials(v.part_t + (size_t)b * v.nblk_t, v.nblk_t, 1, 1, tot);
+      sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG + (kNG - 2), v.nblk_v, kNG, 2, tot + 1);
+      if (threadIdx.x == 0) finalize_trial(v, b, tot[0], tot[1], tot[2]);
+    }
   }
   // last block overall: loop condition of the frame graph
   __syncthreads();
@@ -642,7 +655,7 @@ int launch_finish(qn_system* S, cudaStream_t st) {
   return QN_OK;
 }
 
-int prepare_kernels(qn_system* S) { return prepare_solve_kernels<SolverIO>(S->factor->smem_bytes); }
+int prepare_kernels(qn_system* S) { return prepare_solve_kernels<SolverIO>(S->factor); }
 
 int build_graph(qn_system* S) {
   cudaStream_t st = S->stream;

@@ -8,16 +8,20 @@
 //                         y_J = v[0:nc],  u_s = (children updates below) + v[nc:nr]
 //   backward (L^T x = y): x_J = Z_s^T [y_J; -x_below]
 // Both are dense mat-vecs whose rows (forward) / columns (backward) are
-// independent, so a supernode is split into many small tasks (32-row blocks /
-// 8-column blocks) that run on different SMs — the top separators no longer
-// serialise on one SM.
+// independent, so a supernode is split into tasks (row blocks / column blocks
+// of <= kTaskEntries entries of Z) that run on different SMs.
 //
-// Scheduling: one CTA per (task, batch instance).  CTAs take tickets from a
-// global counter in topological order (postorder forward, reverse backward)
-// and spin on integer flags of the supernodes they depend on (all children /
-// the parent).  A ticket is only taken by a running CTA and dependencies have
-// smaller tickets, so the wait cannot deadlock.  All arithmetic is in fixed
-// order (no float atomics): results are bitwise reproducible run to run.
+// Scheduling: persistent CTAs loop over tickets taken from a global counter in
+// level order (forward: height above the leaves; backward: depth below the
+// root).  Each task publishes its own epoch flag; a dependent task polls the
+// flags of all tasks of its children (forward) / parent (backward) with one
+// lane per flag.  Before polling, a CTA stages everything that does not
+// depend on them — its Z tile (cp.async into shared memory), the RHS or y,
+// and the index lists — so the critical path per tree level is only
+// flag -> one round of dependent gathers -> shared-memory FMAs -> flag.
+// A ticket is only taken by a running CTA and dependencies have smaller
+// tickets, so the waits cannot deadlock.  All arithmetic is in fixed order
+// (no float atomics): results are bitwise reproducible run to run.
 #pragma once
 
 #include "qn_common.cuh"
@@ -34,21 +38,21 @@ struct FactorView {
   const int64_t* sup_val_ptr;
   const int64_t* sup_upd_ptr;
   const int32_t* parent;
-  const int32_t* child_ptr;
-  const int32_t* child_idx;
   const int64_t* cptr;
   const int32_t* cidx;
   const int4* ftask;
   const int4* btask;
-  const int32_t* fcount;
+  const int32_t* bfirst;    // first backward task of each supernode
   const int32_t* bcount;
+  const int32_t* fdep_ptr;  // forward: task ids of all children's tasks
+  const int32_t* fdep_idx;
   const double* vals;
   double* y;
   double* x;
   double* u;
-  unsigned long long* done;  // [2][nbatch][nsup]
-  unsigned* flags;           // [2][nbatch][nsup]
-  unsigned* sched;           // ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b
+  unsigned* flags;           // [nbatch][nftask + nbtask] epoch of completion per task
+  unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
+  unsigned long long* trace; // diagnostics: 3 timestamps per forward then backward item, or null
 };
 
 inline FactorView factor_view(const qn_factor* f) {
@@ -66,78 +70,112 @@ inline FactorView factor_view(const qn_factor* f) {
   v.sup_val_ptr = f->d_sup_val_ptr;
   v.sup_upd_ptr = f->d_sup_upd_ptr;
   v.parent = f->d_parent;
-  v.child_ptr = f->d_child_ptr;
-  v.child_idx = f->d_child_idx;
   v.cptr = f->d_cptr;
   v.cidx = f->d_cidx;
   v.ftask = f->d_ftask;
   v.btask = f->d_btask;
-  v.fcount = f->d_fcount;
+  v.bfirst = f->d_bfirst;
   v.bcount = f->d_bcount;
+  v.fdep_ptr = f->d_fdep_ptr;
+  v.fdep_idx = f->d_fdep_idx;
   v.vals = f->d_vals;
   v.y = f->d_y;
   v.x = f->d_x;
   v.u = f->d_u;
-  v.done = f->d_done;
   v.flags = f->d_flags;
   v.sched = f->d_sched;
+  v.trace = f->d_trace;
   return v;
 }
 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
+constexpr int kStageIdx = 2048;  // int32 index slots staged in shared memory per task
 
-// Spin on a dependency flag.  A wait longer than 2 s means a scheduling bug:
-// record it in sched[6] (checked by the host after the frame) and give up
-// instead of hanging the device.
-__device__ __forceinline__ void wait_flag(const unsigned* p, unsigned epoch, unsigned* sched) {
-  if (ld_acquire(p) == epoch) return;
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire(p) != epoch) {
-    __nanosleep(20);
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 2000000000ull) {
-      atomicOr(&sched[6], 1u);
-      return;
-    }
-  }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-// Take a ticket; returns (item, epoch) through shared memory.
-__device__ __forceinline__ void take_ticket(unsigned* sched, int* s_item, unsigned* s_epoch) {
-  if (threadIdx.x == 0) {
-    *s_item = (int)atomicAdd(&sched[0], 1u);
-    *s_epoch = *((volatile unsigned*)&sched[2]);
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, size_t slot) {
+  if (trace && threadIdx.x == 0) trace[slot] = gtime();
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Warp 0 polls n flags (lane-parallel) until all equal `epoch`; then a CTA
+// barrier.  A wait longer than 2 s means a scheduling bug: it is recorded in
+// sched[6] (checked by the host) instead of hanging the device.
+__device__ __forceinline__ void wait_flags(const unsigned* flags, const int32_t* ids, int n, unsigned epoch,
+                                           unsigned* sched) {
+  if (threadIdx.x < 32) {
+    const unsigned long long t0 = gtime();
+    for (int q = threadIdx.x; q < n; q += 32) {
+      const unsigned* p = flags + ids[q];
+      while (ld_acquire(p) != epoch) {
+        __nanosleep(8);
+        if (gtime() - t0 > 2000000000ull) {
+          atomicOr(&sched[6], 1u);
+          break;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void wait_flag_range(const unsigned* flags, int first, int n, unsigned epoch,
+                                                unsigned* sched) {
+  if (threadIdx.x < 32) {
+    const unsigned long long t0 = gtime();
+    for (int q = threadIdx.x; q < n; q += 32) {
+      const unsigned* p = flags + first + q;
+      while (ld_acquire(p) != epoch) {
+        __nanosleep(8);
+        if (gtime() - t0 > 2000000000ull) {
+          atomicOr(&sched[6], 1u);
+          break;
+        }
+      }
+    }
+    __syncwarp();
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ void finish_item(unsigned* sched, unsigned total, unsigned epoch) {
+// publish this task: all of the CTA's global writes are ordered before the flag
+__device__ __forceinline__ void publish(unsigned* flag, unsigned epoch) {
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned d = atomicAdd(&sched[1], 1u);
-    if (d == total - 1) {  // last CTA of this launch: reset for the next one
+    st_release(flag, epoch);
+  }
+}
+
+// persistent-CTA ticket loop helpers; sched = [ticket, exited, epoch]
+__device__ __forceinline__ int next_ticket(unsigned* sched, int* s_item) {
+  __syncthreads();  // previous item fully done with shared memory
+  if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
+  __syncthreads();
+  return *s_item;
+}
+
+__device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned e = atomicAdd(&sched[1], 1u);
+    if (e == gridDim.x - 1) {  // last CTA out: reset for the next launch
       sched[0] = 0;
       sched[1] = 0;
       __threadfence();
       atomicExch(&sched[2], epoch + 1);
-    }
-  }
-}
-
-// task completion: the last task of supernode s resets the per-launch counter
-// (no other task of s touches it again in this launch) and publishes the flag.
-// Instances skipped by a launch never touch their counters, so they stay 0.
-__device__ __forceinline__ void complete_task(unsigned long long* done, unsigned* flag, int ntasks, unsigned epoch) {
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long old = atomicAdd(done, 1ull);
-    if (old + 1 == (unsigned long long)ntasks) {
-      *done = 0ull;
-      st_release(flag, epoch);
     }
   }
 }
@@ -147,166 +185,212 @@ __device__ __forceinline__ void complete_task(unsigned long long* done, unsigned
 //   __device__ void rhs(int b, int row, double (&v)[3]) const;   // factor row
 //   __device__ void store(int b, int row, const double (&v)[3]) const;
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_forward(FactorView F, IO io) {
-  extern __shared__ double sm[];  // f[nc*3] | part[8][32][3]
+__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F, IO io) {
+  // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
+  extern __shared__ double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
   unsigned* sched = F.sched;
-  take_ticket(sched, &s_item, &s_epoch);
-  const int item = s_item;
-  const unsigned epoch = s_epoch;
-  const int4 task = F.ftask[item / F.nbatch];
-  const int b = item % F.nbatch;
-  const int s = task.x, lo = task.y, hi = task.z;
-  const unsigned total = (unsigned)F.nftask * (unsigned)F.nbatch;
-  if (io.active(b)) {
+  if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  const int total = F.nftask * F.nbatch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* zt = sm;
+  for (;;) {
+    const int item = next_ticket(sched, &s_item);
+    if (item >= total) break;
+    const unsigned epoch = s_epoch;
+    const int tid = item / F.nbatch;
+    const int4 task = F.ftask[tid];
+    const int b = item % F.nbatch;
+    const int s = task.x, lo = task.y, hi = task.z, rg = task.w;  // rg = row groups of 32
+    if (!io.active(b)) continue;
     const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
     const int64_t R0 = F.sup_row_ptr[s];
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-    double* f = sm;
-    double* part = sm + 3 * nc;
+    const int R = hi - lo;
+    const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
+    double* f = sm + kTaskEntries;
+    double* part = f + 3 * nc;
+    int* sidx = (int*)(part + 3 * kSolveThreads);
     const double* ub = F.u + (size_t)b * F.nupd * 3;
-    if (threadIdx.x == 0)
-      for (int q = F.child_ptr[s]; q < F.child_ptr[s + 1]; ++q)
-        wait_flag(&F.flags[(size_t)b * F.nsup + F.child_idx[q]], epoch, F.sched);
-    __syncthreads();
-    // f = b_J - sum of children's updates landing on J (children in order)
+    // ---- stage everything that does not depend on the children ----
+    {  // Z tile rows [lo, hi) x k [0, kmax) -> zt[k * R + (r - lo)]
+      const double* Zg = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s] + lo;
+      const int cnt = R * kmax;
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int k = e / R, rr = e - k * R;
+        cp_async8(zt + e, Zg + (int64_t)k * nr + rr);
+      }
+    }
+    const int blo = max(lo, nc);
+    const int64_t ct0 = F.cptr[R0], ct1 = F.cptr[R0 + nc];
+    const int64_t cb0 = F.cptr[R0 + blo], cb1 = blo < hi ? F.cptr[R0 + hi] : cb0;
+    const int ntop = (int)(ct1 - ct0), nbot = (int)(cb1 - cb0);
+    const int nptr_top = nc + 1, nptr_bot = blo < hi ? hi - blo + 1 : 0;
+    const bool staged = nptr_top + nptr_bot + ntop + nbot <= kStageIdx;
+    int* sp_top = sidx;
+    int* sp_bot = sp_top + nptr_top;
+    int* si_top = sp_bot + nptr_bot;
+    int* si_bot = si_top + ntop;
+    if (staged) {
+      for (int p = threadIdx.x; p < nptr_top; p += blockDim.x) sp_top[p] = (int)(F.cptr[R0 + p] - ct0);
+      for (int p = threadIdx.x; p < nptr_bot; p += blockDim.x) sp_bot[p] = (int)(F.cptr[R0 + blo + p] - cb0);
+      for (int q = threadIdx.x; q < ntop; q += blockDim.x) si_top[q] = F.cidx[ct0 + q];
+      for (int q = threadIdx.x; q < nbot; q += blockDim.x) si_bot[q] = F.cidx[cb0 + q];
+    }
+    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+      double v[3];
+      io.rhs(b, c0 + p, v);
+      f[3 * p + 0] = v[0];
+      f[3 * p + 1] = v[1];
+      f[3 * p + 2] = v[2];
+    }
+    trace_mark(F.trace, 3 * (size_t)item + 0);
+    const int d0 = F.fdep_ptr[s], d1 = F.fdep_ptr[s + 1];
+    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d0, d1 - d0, epoch, F.sched);
+    trace_mark(F.trace, 3 * (size_t)item + 1);
+    // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
     for (int p = threadIdx.x; p < nc; p += blockDim.x) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)F.cidx[q];
+      const int q0 = staged ? sp_top[p] : (int)(F.cptr[R0 + p] - ct0);
+      const int q1 = staged ? sp_top[p + 1] : (int)(F.cptr[R0 + p + 1] - ct0);
+      for (int q = q0; q < q1; ++q) {
+        const double* uc = ub + 3 * (size_t)(staged ? si_top[q] : F.cidx[ct0 + q]);
         a0 += __ldcg(uc);
         a1 += __ldcg(uc + 1);
         a2 += __ldcg(uc + 2);
       }
-      double v[3];
-      io.rhs(b, c0 + p, v);
-      f[3 * p + 0] = v[0] - a0;
-      f[3 * p + 1] = v[1] - a1;
-      f[3 * p + 2] = v[2] - a2;
+      f[3 * p + 0] -= a0;
+      f[3 * p + 1] -= a1;
+      f[3 * p + 2] -= a2;
     }
-    __syncthreads();
-    // rows [lo, hi) of v = Z f: lane = row, warp = slice of k (coalesced over rows)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
-    const int per = (kmax + kSolveWarps - 1) / kSolveWarps;
-    const int kb = warp * per, ke = min(kmax, kb + per);
-    const int r = lo + lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (r < hi) {
-      const double* Z = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s] + r;
-      int k = kb;
-      for (; k + 16 <= ke; k += 16) {
-        double l[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) l[q] = __ldg(Z + (int64_t)(k + q) * nr);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          a0 = fma(l[q], f[3 * (k + q) + 0], a0);
-          a1 = fma(l[q], f[3 * (k + q) + 1], a1);
-          a2 = fma(l[q], f[3 * (k + q) + 2], a2);
-        }
+    const int rr = lo + threadIdx.x;  // row owned by this thread in the epilogue
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    if (threadIdx.x < R && rr >= nc) {
+      const int pr = rr - blo;
+      const int q0 = staged ? sp_bot[pr] : (int)(F.cptr[R0 + rr] - cb0);
+      const int q1 = staged ? sp_bot[pr + 1] : (int)(F.cptr[R0 + rr + 1] - cb0);
+      for (int q = q0; q < q1; ++q) {
+        const double* uc = ub + 3 * (size_t)(staged ? si_bot[q] : F.cidx[cb0 + q]);
+        e0 += __ldcg(uc);
+        e1 += __ldcg(uc + 1);
+        e2 += __ldcg(uc + 2);
       }
-      for (; k < ke; ++k) {
-        const double l = __ldg(Z + (int64_t)k * nr);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
+    const int ks = kSolveWarps / rg;
+    const int g = warp / ks, j = warp % ks;
+    const int per = (kmax + ks - 1) / ks;
+    const int kb = j * per, ke = min(kmax, kb + per);
+    const int rl = 32 * g + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (g < rg && rl < R) {
+#pragma unroll 8
+      for (int k = kb; k < ke; ++k) {
+        const double l = zt[k * R + rl];
         a0 = fma(l, f[3 * k + 0], a0);
         a1 = fma(l, f[3 * k + 1], a1);
         a2 = fma(l, f[3 * k + 2], a2);
       }
     }
-    part[(warp * 32 + lane) * 3 + 0] = a0;
-    part[(warp * 32 + lane) * 3 + 1] = a1;
-    part[(warp * 32 + lane) * 3 + 2] = a2;
+    part[3 * threadIdx.x + 0] = a0;
+    part[3 * threadIdx.x + 1] = a1;
+    part[3 * threadIdx.x + 2] = a2;
     __syncthreads();
-    if (threadIdx.x < 32 && r < hi) {
+    if (threadIdx.x < R) {
+      const int gg = threadIdx.x >> 5;
       double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-#pragma unroll
-      for (int w = 0; w < kSolveWarps; ++w) {
-        v0 += part[(w * 32 + lane) * 3 + 0];
-        v1 += part[(w * 32 + lane) * 3 + 1];
-        v2 += part[(w * 32 + lane) * 3 + 2];
+      for (int jj = 0; jj < ks; ++jj) {
+        const int t = (gg * ks + jj) * 32 + lane;
+        v0 += part[3 * t + 0];
+        v1 += part[3 * t + 1];
+        v2 += part[3 * t + 2];
       }
-      if (r < nc) {
-        double* yg = F.y + ((size_t)b * F.n + c0 + r) * 3;
+      if (rr < nc) {
+        double* yg = F.y + ((size_t)b * F.n + c0 + rr) * 3;
         yg[0] = v0;
         yg[1] = v1;
         yg[2] = v2;
       } else {
-        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-        for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
-          const double* uc = ub + 3 * (size_t)F.cidx[q];
-          e0 += __ldcg(uc);
-          e1 += __ldcg(uc + 1);
-          e2 += __ldcg(uc + 2);
-        }
-        double* us = F.u + ((size_t)b * F.nupd + F.sup_upd_ptr[s] + (r - nc)) * 3;
+        double* us = F.u + ((size_t)b * F.nupd + F.sup_upd_ptr[s] + (rr - nc)) * 3;
         __stcg(us + 0, e0 + v0);
         __stcg(us + 1, e1 + v1);
         __stcg(us + 2, e2 + v2);
       }
     }
-    complete_task(&F.done[(size_t)b * F.nsup + s], &F.flags[(size_t)b * F.nsup + s], F.fcount[s], epoch);
+    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
+    trace_mark(F.trace, 3 * (size_t)item + 2);
   }
-  finish_item(sched, total, epoch);
+  cta_exit(sched, s_epoch);
 }
 
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_backward(FactorView F, IO io) {
-  extern __shared__ double sm[];  // w[nr*3] = [y_J; -x_below]
+__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
+  // smem: ztile[kTaskEntries] | w[max_rows*3] = [y_J; -x_below] | row staging (int32)
+  extern __shared__ double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
   unsigned* sched = F.sched + 3;
-  take_ticket(sched, &s_item, &s_epoch);
-  const int item = s_item;
-  const unsigned epoch = s_epoch;
-  const int4 task = F.btask[item / F.nbatch];
-  const int b = item % F.nbatch;
-  const int s = task.x, k0 = task.y, k1 = task.z;
-  const unsigned total = (unsigned)F.nbtask * (unsigned)F.nbatch;
-  const size_t off2 = (size_t)F.nbatch * F.nsup;
-  if (io.active(b)) {
+  if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  const int total = F.nbtask * F.nbatch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* zt = sm;
+  for (;;) {
+    const int item = next_ticket(sched, &s_item);
+    if (item >= total) break;
+    const unsigned epoch = s_epoch;
+    const int tid = item / F.nbatch;
+    const int4 task = F.btask[tid];
+    const int b = item % F.nbatch;
+    const int s = task.x, k0 = task.y, k1 = task.z;
+    if (!io.active(b)) continue;
     const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
     const int64_t R0 = F.sup_row_ptr[s];
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-    double* w = sm;
+    double* w = sm + kTaskEntries;
+    int* srow = (int*)(w + 3 * nr);
+    const bool staged = nr - nc <= kStageIdx;
     const int p = F.parent[s];
-    if (threadIdx.x == 0 && p >= 0) wait_flag(&F.flags[off2 + (size_t)b * F.nsup + p], epoch, F.sched);
-    __syncthreads();
-    const double* xg = F.x + (size_t)b * F.n * 3;
-    const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
-    for (int q = threadIdx.x; q < nr; q += blockDim.x) {
-      if (q < nc) {
-        w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
-        w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
-        w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
-      } else {
-        const int row = F.sup_rows[R0 + q];
-        w[3 * q + 0] = -__ldcg(xg + 3 * row + 0);
-        w[3 * q + 1] = -__ldcg(xg + 3 * row + 1);
-        w[3 * q + 2] = -__ldcg(xg + 3 * row + 2);
+    // ---- stage: Z columns [k0, k1) (rows >= k), y_J, below-row ids ----
+    {
+      const double* Zg = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s];
+      const int cnt = (k1 - k0) * nr;
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int kk = e / nr, r = e - kk * nr;
+        if (r >= k0 + kk) cp_async8(zt + e, Zg + (int64_t)(k0 + kk) * nr + r);
       }
     }
+    const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+      w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
+      w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
+      w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
+    }
+    if (staged)
+      for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
+    const size_t tb = 3 * ((size_t)F.nftask * F.nbatch + item);
+    trace_mark(F.trace, tb + 0);
+    if (p >= 0)
+      wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, F.bfirst[p], F.bcount[p], epoch,
+                      F.sched);
+    trace_mark(F.trace, tb + 1);
+    const double* xg = F.x + (size_t)b * F.n * 3;
+    for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) {
+      const int row = staged ? srow[q] : F.sup_rows[R0 + nc + q];
+      w[3 * (nc + q) + 0] = -__ldcg(xg + 3 * row + 0);
+      w[3 * (nc + q) + 1] = -__ldcg(xg + 3 * row + 1);
+      w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
+    }
+    cp_async_wait_all();
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int k = k0 + warp;
-    if (k < k1) {
-      const double* col = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s] + (int64_t)k * nr;
+    for (int k = k0 + warp; k < k1; k += kSolveWarps) {
+      const double* col = zt + (size_t)(k - k0) * nr;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      int r = k + lane;
-      for (; r + 224 < nr; r += 256) {
-        double l[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) l[q] = __ldg(col + r + 32 * q);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int rr = r + 32 * q;
-          a0 = fma(l[q], w[3 * rr + 0], a0);
-          a1 = fma(l[q], w[3 * rr + 1], a1);
-          a2 = fma(l[q], w[3 * rr + 2], a2);
-        }
-      }
-      for (; r < nr; r += 32) {
-        const double l = __ldg(col + r);
+#pragma unroll 4
+      for (int r = k + lane; r < nr; r += 32) {
+        const double l = col[r];
         a0 = fma(l, w[3 * r + 0], a0);
         a1 = fma(l, w[3 * r + 1], a1);
         a2 = fma(l, w[3 * r + 2], a2);
@@ -323,10 +407,10 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_backward(FactorView F, I
         io.store(b, c0 + k, v);
       }
     }
-    complete_task(&F.done[off2 + (size_t)b * F.nsup + s], &F.flags[off2 + (size_t)b * F.nsup + s], F.bcount[s],
-                  epoch);
+    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
+    trace_mark(F.trace, tb + 2);
   }
-  finish_item(sched, total, epoch);
+  cta_exit(sched, s_epoch);
 }
 
 // Plain solve: B (n,3) -> X (n,3) in the original row order, one instance.
@@ -353,17 +437,29 @@ struct PlainIO {
 template <class IO>
 int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   const FactorView v = factor_view(f);
-  sptrsv_forward<IO><<<(int)f->ftask.size() * (int)f->nbatch, kSolveThreads, f->smem_bytes, stream>>>(v, io);
+  const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
+  sptrsv_forward<IO><<<std::min(nf, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
   QN_CHECK_LAUNCH();
-  sptrsv_backward<IO><<<(int)f->btask.size() * (int)f->nbatch, kSolveThreads, f->smem_bytes, stream>>>(v, io);
+  sptrsv_backward<IO><<<std::min(nb, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
   QN_CHECK_LAUNCH();
   return QN_OK;
 }
 
 template <class IO>
-int prepare_solve_kernels(int smem_bytes) {
+int prepare_solve_kernels(qn_factor* f) {
+  const int smem_bytes = f->smem_bytes;
   QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int per_f = 0, per_b = 0, dev = 0, sms = 0;
+  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, sptrsv_forward<IO>, kSolveThreads, smem_bytes));
+  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, sptrsv_backward<IO>, kSolveThreads, smem_bytes));
+  QN_CUDA(cudaGetDevice(&dev));
+  QN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int per = std::max(1, std::min(per_f, per_b));
+  const int grid = per * sms;
+  f->grid_ctas = f->grid_ctas ? std::min(f->grid_ctas, grid) : grid;
   return QN_OK;
 }
 

@@ -28,7 +28,7 @@ int launch_init(qn_system* S, cudaStream_t st);
 int launch_finish(qn_system* S, cudaStream_t st);
 int build_graph(qn_system* S);
 int prepare_kernels(qn_system* S);
-__global__ void k_tet_plain(SysView v, const double* x, int b, int mat_sel, double* part);
+int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st);
 __global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
                                int zero_fixed, double* part);
 __global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V);
@@ -716,8 +716,7 @@ int qn_system_objective(qn_system* S, const double* x, const double* y, double* 
   std::vector<double> pt(v.nblk_t), pv(v.nblk_v);
   for (int64_t b = 0; b < S->n_inst; ++b) {
     if ((rc = to_device(dx, x + b * nv, nv, mem, st)) || (rc = to_device(dy, y + b * nv, nv, mem, st))) return rc;
-    k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, dx, (int)b, -1, S->d_part_plain);
-    QN_CHECK_LAUNCH();
+    if ((rc = launch_tet_plain(S, dx, (int)b, -1, S->d_part_plain, st))) return rc;
     k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
     QN_CHECK_LAUNCH();
     QN_CUDA(cudaMemcpyAsync(pt.data(), S->d_part_plain, v.nblk_t * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -752,8 +751,7 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
   if ((rc = dev_alloc(&dx, nv)) || (rc = dev_alloc(&dg, nv))) return rc;
   const SysView& v = S->v;
   if ((rc = to_device(dx, x, nv, mem, st))) return rc;
-  k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, dx, (int)inst, (int)mat, S->d_part_plain);
-  QN_CHECK_LAUNCH();
+  if ((rc = launch_tet_plain(S, dx, (int)inst, (int)mat, S->d_part_plain, st))) return rc;
   if (grad_accum) {
     if ((rc = to_device(dg, grad_accum, nv, mem, st))) return rc;
     k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
@@ -782,8 +780,8 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
   int rc;
   auto launch = [&]() -> int {
     if (kernel == 0) {  // per-tet pass (F, SVD, VL energy, PK1 corner forces) at the resident q_l
-      k_tet_plain<<<v.nblk_t, 128, 0, st>>>(v, v.q_l, 0, -1, S->d_part_plain);
-      QN_CHECK_LAUNCH();
+      int r = launch_tet_plain(S, v.q_l, 0, -1, S->d_part_plain, st);
+      if (r) return r;
     } else {  // forward + backward supernodal solves with 3 RHS (instance 0)
       QN_CUDA(cudaMemcpyAsync(S->factor->d_io, v.q_l, S->n_free * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
       int r = factor_solve_plain(S->factor, 0, st);

@@ -32,17 +32,22 @@ __device__ __forceinline__ void poly_eval(const qn_scalar_fn& f, double x, doubl
   }
 }
 
+// fp64 1/x for |x| in the fp32 normal range: SFU seed + two Newton steps (~1 ulp)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y = (double)__frcp_rn((float)x);
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
 __device__ __forceinline__ void log_eval(const qn_scalar_fn& f, double x, double& v, double& dv) {
   // materials.py:57-80: core for x > eps, quadratic Taylor continuation below
-  if (x > f.eps) {
-    const double lx = log(x);
-    v = f.alpha * lx + 0.5 * f.beta * lx * lx;
-    dv = (f.alpha + f.beta * lx) / x;
-  } else {
-    const double d = x - f.eps;
-    v = f.f0 + f.f1 * d + 0.5 * f.f2 * d * d;
-    dv = f.f1 + f.f2 * d;
-  }
+  const bool core = x > f.eps;
+  const double xs = core ? x : 1.0;
+  const double lx = log(xs);
+  const double d = x - f.eps;
+  v = core ? f.alpha * lx + 0.5 * f.beta * lx * lx : f.f0 + f.f1 * d + 0.5 * f.f2 * d * d;
+  dv = core ? (f.alpha + f.beta * lx) * rcp_nr(xs) : f.f1 + f.f2 * d;
 }
 
 __device__ __forceinline__ void hermite_eval(const qn_scalar_fn& f, double x, double& v, double& dv) {
@@ -62,11 +67,12 @@ __device__ __forceinline__ void hermite_eval(const qn_scalar_fn& f, double x, do
   int i = 0;
   for (int k = 1; k < K - 1; ++k) i += (f.xs[k] <= x) ? 1 : 0;
   const double h = f.xs[i + 1] - f.xs[i];
-  const double u = (x - f.xs[i]) / h;
+  const double ih = rcp_nr(h);
+  const double u = (x - f.xs[i]) * ih;
   const double u2 = u * u, u3 = u2 * u;
   const double y0 = f.ys[i], y1 = f.ys[i + 1], t0 = f.ts[i], t1 = f.ts[i + 1];
   v = (2 * u3 - 3 * u2 + 1) * y0 + (u3 - 2 * u2 + u) * h * t0 + (-2 * u3 + 3 * u2) * y1 + (u3 - u2) * h * t1;
-  dv = (6 * u2 - 6 * u) * y0 / h + (3 * u2 - 4 * u + 1) * t0 + (-6 * u2 + 6 * u) * y1 / h + (3 * u2 - 2 * u) * t1;
+  dv = ((6 * u2 - 6 * u) * y0 + (-6 * u2 + 6 * u) * y1) * ih + (3 * u2 - 4 * u + 1) * t0 + (3 * u2 - 2 * u) * t1;
 }
 
 __device__ __forceinline__ void fn_eval(const qn_scalar_fn& f, double x, double& v, double& dv) {
@@ -78,24 +84,60 @@ __device__ __forceinline__ void fn_eval(const qn_scalar_fn& f, double x, double&
   }
 }
 
+// f and f' at N points with one dispatch (the function kind is uniform across a
+// warp); a polynomial's coefficients are loaded once for all N Horner chains.
+template <int N>
+__device__ __forceinline__ void fn_eval_n(const qn_scalar_fn& f, const double (&x)[N], double (&v)[N],
+                                          double (&dv)[N]) {
+  const int kind = f.kind;
+  if (kind == QN_FN_POLY) {
+    const int n = f.n;
+    double a[N], d[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      a[j] = f.c[n - 1];
+      d[j] = n > 1 ? f.dc[n - 2] : 0.0;
+    }
+    for (int i = n - 2; i >= 0; --i) {
+      const double ci = f.c[i];
+#pragma unroll
+      for (int j = 0; j < N; ++j) a[j] = fma(a[j], x[j], ci);
+    }
+    for (int i = n - 3; i >= 0; --i) {
+      const double di = f.dc[i];
+#pragma unroll
+      for (int j = 0; j < N; ++j) d[j] = fma(d[j], x[j], di);
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      v[j] = a[j];
+      dv[j] = d[j];
+    }
+  } else if (kind == QN_FN_LOG) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) log_eval(f, x[j], v[j], dv[j]);
+  } else if (kind == QN_FN_HERMITE) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) hermite_eval(f, x[j], v[j], dv[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = dv[j] = 0.0;
+  }
+}
+
 // Psi(s) - shift and tau = dPsi/ds  (materials.py:181-207)
 __device__ __forceinline__ double vl_eval(const qn_material& M, const double s[3], double tau[3]) {
-  double a0, a1, a2, da0, da1, da2;
-  fn_eval(M.a, s[0], a0, da0);
-  fn_eval(M.a, s[1], a1, da1);
-  fn_eval(M.a, s[2], a2, da2);
-  double b01 = 0, b12 = 0, b02 = 0, db01 = 0, db12 = 0, db02 = 0;
-  if (M.b.kind != QN_FN_ZERO) {
-    fn_eval(M.b, s[0] * s[1], b01, db01);
-    fn_eval(M.b, s[1] * s[2], b12, db12);
-    fn_eval(M.b, s[0] * s[2], b02, db02);
-  }
-  double c = 0, dc = 0;
-  if (M.c.kind != QN_FN_ZERO) fn_eval(M.c, s[0] * s[1] * s[2], c, dc);
-  tau[0] = da0 + db01 * s[1] + db02 * s[2] + dc * s[1] * s[2];
-  tau[1] = da1 + db01 * s[0] + db12 * s[2] + dc * s[0] * s[2];
-  tau[2] = da2 + db12 * s[1] + db02 * s[0] + dc * s[0] * s[1];
-  return a0 + a1 + a2 + b01 + b12 + b02 + c - M.shift;
+  double a[3], da[3], b[3], db[3], c[1], dc[1];
+  const double xa[3] = {s[0], s[1], s[2]};
+  const double xb[3] = {s[0] * s[1], s[1] * s[2], s[0] * s[2]};  // b01, b12, b02
+  const double xc[1] = {s[0] * s[1] * s[2]};
+  fn_eval_n<3>(M.a, xa, a, da);
+  fn_eval_n<3>(M.b, xb, b, db);
+  fn_eval_n<1>(M.c, xc, c, dc);
+  tau[0] = da[0] + db[0] * s[1] + db[2] * s[2] + dc[0] * s[1] * s[2];
+  tau[1] = da[1] + db[0] * s[0] + db[1] * s[2] + dc[0] * s[0] * s[2];
+  tau[2] = da[2] + db[1] * s[1] + db[2] * s[0] + dc[0] * s[0] * s[1];
+  return a[0] + a[1] + a[2] + b[0] + b[1] + b[2] + c[0] - M.shift;
 }
 
 // ---------------------------------------------------------------------------
@@ -107,23 +149,40 @@ __device__ __forceinline__ double vl_eval(const qn_material& M, const double s[3
 //    has the smallest magnitude — the reference's rule (linalg.py:95-103).
 // Matrices are row-major m[r*3+c].
 
-__device__ __forceinline__ void jacobi_rot(double (&A)[3][3], double (&V)[3][3], int p, int q) {
+// fp64 1/sqrt(x) for x in the fp32 normal range: SFU seed + two Newton steps
+// (relative error ~1e-16, no library slow paths or branches).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y = (double)rsqrtf((float)x);
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// One Jacobi rotation in the (p,q) plane.  The angle only needs to be
+// approximate (it is computed in fp32 on the SFU); the rotation itself is an
+// exact fp64 rotation (c^2 + s^2 = 1 to rounding) applied as a full
+// similarity transform, so A stays symmetric-similar and V orthogonal, and
+// the next sweep removes what the approximate angle left (~1e-7 relative).
+// Branch-free (lanes never diverge): a converged pair gets t = 0, i.e. the
+// identity rotation c = 1, s = 0, which leaves A and V bit-identical.
+// Returns whether the pair needed a rotation.
+__device__ __forceinline__ bool jacobi_rot(double (&A)[3][3], double (&V)[3][3], int p, int q) {
   const double apq = A[p][q];
   const double app = A[p][p], aqq = A[q][q];
-  // skip rotations below the fp64 resolution of the diagonal (and apq == 0)
-  if (fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq))) return;
-  const double theta = (aqq - app) / (2.0 * apq);
-  double t;
-  if (fabs(theta) > 1e150) {
-    t = 0.5 / theta;
-  } else {
-    t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-  }
-  const double c = rsqrt(t * t + 1.0);
+  const float d = (float)(aqq - app), a = (float)apq;
+  // tan of the Jacobi angle, stable form: t = 2a sign(d) / (|d| + sqrt(d^2 + 4a^2))
+  const float den = fabsf(d) + sqrtf(fmaf(d, d, 4.f * a * a));
+  // rotate unless apq is below the fp64 resolution of the diagonal (or of fp32)
+  const bool need = apq * apq > 1e-36 * fabs(app * aqq) && den > 0.f;
+  const float tf = __fdividef(2.f * a, need ? den : 1.f) * (d >= 0.f ? 1.f : -1.f);
+  const double t = need ? (double)tf : 0.0;
+  const double c = rsqrt_nr(fma(t, t, 1.0));
   const double s = t * c;
-  A[p][p] = app - t * apq;
-  A[q][q] = aqq + t * apq;
-  A[p][q] = A[q][p] = 0.0;
+  const double cc = c * c, ss = s * s, cs = c * s;
+  A[p][p] = fma(cc, app, fma(ss, aqq, -2.0 * cs * apq));
+  A[q][q] = fma(ss, app, fma(cc, aqq, 2.0 * cs * apq));
+  A[p][q] = A[q][p] = fma(cc - ss, apq, cs * (app - aqq));
   const int r = 3 - p - q;
   const double arp = A[r][p], arq = A[r][q];
   A[r][p] = A[p][r] = c * arp - s * arq;
@@ -134,34 +193,39 @@ __device__ __forceinline__ void jacobi_rot(double (&A)[3][3], double (&V)[3][3],
     V[k][p] = c * vkp - s * vkq;
     V[k][q] = s * vkp + c * vkq;
   }
+  return need;
 }
 
-__device__ __forceinline__ void swap_cols(double (&A)[3][3], double (&V)[3][3], int i, int j) {
-  // swap eigenpairs i <-> j; negate one column so det V stays +1
-  double t = A[i][i];
-  A[i][i] = A[j][j];
-  A[j][j] = t;
+// swap eigenpairs i <-> j when A[i][i] < A[j][j] (branch-free); the swapped
+// column is negated so det V stays +1
+__device__ __forceinline__ void sort_pair(double (&A)[3][3], double (&V)[3][3], int i, int j) {
+  const bool sw = A[i][i] < A[j][j];
+  const double ai = A[i][i], aj = A[j][j];
+  A[i][i] = sw ? aj : ai;
+  A[j][j] = sw ? ai : aj;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double a = V[k][i];
-    V[k][i] = V[k][j];
-    V[k][j] = -a;
+    const double vi = V[k][i], vj = V[k][j];
+    V[k][i] = sw ? vj : vi;
+    V[k][j] = sw ? -vi : vj;
   }
 }
 
 // Givens rotation acting on rows (p,q) of R, accumulated into the columns of U.
 __device__ __forceinline__ void givens_qr(double (&R)[3][3], double (&U)[3][3], int p, int q, int col) {
+  // c = a / r, s = b / r makes the new pivot r >= 0 (for b = 0, a < 0 this is
+  // the rotation by pi); r = 0 keeps the identity.  Branch-free except for
+  // pivots outside the fp32 range of the rsqrt seed.
   const double a = R[p][col], b = R[q][col];
-  double c, s;
-  if (b == 0.0) {
-    if (a >= 0.0) return;
-    c = -1.0;  // rotation by pi in the (p,q) plane makes the pivot non-negative
-    s = 0.0;
+  const double r2 = fma(a, a, b * b);
+  double inv;
+  if (r2 > 1e-36 && r2 < 1e36) {
+    inv = rsqrt_nr(r2);
   } else {
-    const double inv = rsqrt(a * a + b * b);
-    c = a * inv;
-    s = b * inv;
+    inv = r2 > 0.0 ? rsqrt(r2) : 0.0;
   }
+  const double c = r2 > 0.0 ? a * inv : 1.0;
+  const double s = b * inv;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const double rp = R[p][k], rq = R[q][k];
@@ -185,18 +249,18 @@ __device__ __forceinline__ void svd_rv3(const double (&F)[3][3], double (&U)[3][
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0 : 0.0;
-  for (int sweep = 0; sweep < 8; ++sweep) {
-    jacobi_rot(A, V, 0, 1);
-    jacobi_rot(A, V, 0, 2);
-    jacobi_rot(A, V, 1, 2);
-    const double off = fabs(A[0][1]) + fabs(A[0][2]) + fabs(A[1][2]);
-    const double dia = fabs(A[0][0]) + fabs(A[1][1]) + fabs(A[2][2]);
-    if (off <= 1e-17 * dia) break;
+  // cyclic sweeps until no pair needs a rotation; the exit is a warp vote so
+  // the loop stays convergent across lanes (callers keep all 32 lanes active)
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    bool rot = jacobi_rot(A, V, 0, 1);
+    rot |= jacobi_rot(A, V, 0, 2);
+    rot |= jacobi_rot(A, V, 1, 2);
+    if (!__any_sync(0xffffffffu, rot)) break;
   }
   // sort eigenvalues descending
-  if (A[0][0] < A[1][1]) swap_cols(A, V, 0, 1);
-  if (A[0][0] < A[2][2]) swap_cols(A, V, 0, 2);
-  if (A[1][1] < A[2][2]) swap_cols(A, V, 1, 2);
+  sort_pair(A, V, 0, 1);
+  sort_pair(A, V, 0, 2);
+  sort_pair(A, V, 1, 2);
   // B = F V
   double R[3][3];
 #pragma unroll

@@ -462,7 +462,72 @@ __device__ void finalize_trial(const SysView& v, int b, double e_el, double iner
   if (c.phase == PH_DONE) atomicSub(v.active, 1);
 }
 
+constexpr int kMatSmem = 4;  // materials per instance staged in shared memory
+
+// Material table of instance b: staged in shared memory (block-cooperative
+// copy) when kSm (n_mat <= kMatSmem, chosen on the host), else read from
+// global memory.  The compile-time choice keeps shared-memory accesses LDS.
+template <bool kSm>
+__device__ __forceinline__ const qn_material* stage_materials(const SysView& v, int b, qn_material* smat) {
+  const qn_material* src = v.mats + (size_t)b * v.n_mat;
+  if (!kSm) return src;
+  const int words = v.n_mat * (int)(sizeof(qn_material) / 8);
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(smat);
+  for (int w = threadIdx.x; w < words; w += blockDim.x) d[w] = __ldg(s + w);
+  __syncthreads();
+  return smat;
+}
+
+constexpr int kFStride = 13;  // padded per-thread stride of the staged corner forces
+
+// Energy and corner forces of tet t (all lanes execute: lanes past the end
+// evaluate a clamped tet and do not store, keeping the SVD's warp votes
+// convergent).  Tets not in `mat_sel` (>= 0) contribute zero.  The 12 forces
+// are staged in shared memory and written block-contiguously (coalesced) by
+// store_forces().
+__device__ __forceinline__ double tet_thread(const SysView& v, const double* __restrict__ x, int b, int t_raw,
+                                             const qn_material* mats, int mat_sel, double* fsm) {
+  const int t = min(t_raw, v.mt - 1);
+  const int4 tv = __ldg(v.tets + t);
+  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
+  double xs[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    xs[k][0] = x[3 * id[k] + 0];
+    xs[k][1] = x[3 * id[k] + 1];
+    xs[k][2] = x[3 * id[k] + 2];
+  }
+  double Dm[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) Dm[r][q] = __ldg(v.dminv + (size_t)(r * 3 + q) * v.mt + t);
+  const double vol = __ldg(v.vols + t);
+  const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
+  double f[4][3];
+  double e = tet_eval<true>(mats[mi], xs, Dm, vol, f);
+  const bool keep = t_raw < v.mt;
+  const bool sel = mat_sel < 0 || mi == mat_sel;
+  double* fs = fsm + threadIdx.x * kFStride;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) fs[3 * k + a] = sel ? f[k][a] : 0.0;
+  return keep && sel ? e : 0.0;
+}
+
+// coalesced write of the block's staged forces: [tet][corner][xyz] contiguous
+__device__ __forceinline__ void store_forces(const SysView& v, int b, const double* fsm) {
+  __syncthreads();
+  const int t0 = blockIdx.x * blockDim.x;
+  const int cnt = min((int)blockDim.x, v.mt - t0) * 12;
+  double* out = v.forces + ((size_t)b * v.mt + t0) * 12;
+  for (int w = threadIdx.x; w < cnt; w += blockDim.x) out[w] = fsm[(w / 12) * kFStride + (w % 12)];
+}
+
 // per-tet pass at the trial point: energy partials + corner forces
+template <bool kSm>
 __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -470,34 +535,14 @@ __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
   const bool on = ph == PH_FIRST || ph == PH_DIR || ph == PH_ALPHA || ph == PH_COPY;
   if (on) {
     __shared__ double red[32];
+    __shared__ qn_material smat[kMatSmem];
+    __shared__ double fsm[kTT * kFStride];
     double e[1] = {0.0};
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < v.mt) {
-      const int4 tv = v.tets[t];
-      const double* x = v.X + vec_off(v, cc->xs_trial, b);
-      double xs[4][3];
-      const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        xs[k][0] = x[3 * id[k] + 0];
-        xs[k][1] = x[3 * id[k] + 1];
-        xs[k][2] = x[3 * id[k] + 2];
-      }
-      double Dm[3][3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) Dm[r][q] = __ldg(v.dminv + (size_t)(r * 3 + q) * v.mt + t);
-      const double vol = __ldg(v.vols + t);
-      const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
-      const qn_material& M = v.mats[(size_t)b * v.n_mat + mi];
-      double f[4][3];
-      e[0] = tet_eval<true>(M, xs, Dm, vol, f);
-      double* fo = v.forces + ((size_t)b * v.mt + t) * 12;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) fo[3 * k + a] = f[k][a];
+    if (v.mt > 0) {
+      const qn_material* mats = stage_materials<kSm>(v, b, smat);
+      e[0] = tet_thread(v, v.X + vec_off(v, cc->xs_trial, b), b, blockIdx.x * blockDim.x + threadIdx.x, mats, -1,
+                        fsm);
+      store_forces(v, b, fsm);
     }
     block_sum<1>(e, red);
     if (threadIdx.x == 0) v.part_t[(size_t)b * v.nblk_t + blockIdx.x] = e[0];
@@ -543,27 +588,17 @@ __global__ void k_finish(SysView v) {
 // ---------------------------------------------------------------------------
 // seam kernels (objective / gradient / element groups / SVD / material)
 
+template <bool kSm>
 __global__ void __launch_bounds__(kTT) k_tet_plain(SysView v, const double* x, int b, int mat_sel,
                                                   double* part) {
   __shared__ double red[32];
+  __shared__ qn_material smat[kMatSmem];
+  __shared__ double fsm[kTT * kFStride];
   double e[1] = {0.0};
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < v.mt) {
-    const int mi = v.tet_mat ? v.tet_mat[t] : 0;
-    double f[4][3] = {};
-    if (mat_sel < 0 || mi == mat_sel) {
-      const int4 tv = v.tets[t];
-      const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-      double xs[4][3], Dm[3][3];
-      for (int k = 0; k < 4; ++k)
-        for (int a = 0; a < 3; ++a) xs[k][a] = x[3 * id[k] + a];
-      for (int r = 0; r < 3; ++r)
-        for (int q = 0; q < 3; ++q) Dm[r][q] = v.dminv[(size_t)(r * 3 + q) * v.mt + t];
-      e[0] = tet_eval<true>(v.mats[(size_t)b * v.n_mat + mi], xs, Dm, v.vols[t], f);
-    }
-    double* fo = v.forces + ((size_t)b * v.mt + t) * 12;
-    for (int k = 0; k < 4; ++k)
-      for (int a = 0; a < 3; ++a) fo[3 * k + a] = f[k][a];
+  if (v.mt > 0) {
+    const qn_material* mats = stage_materials<kSm>(v, b, smat);
+    e[0] = tet_thread(v, x, b, blockIdx.x * blockDim.x + threadIdx.x, mats, mat_sel, fsm);
+    store_forces(v, b, fsm);
   }
   block_sum<1>(e, red);
   if (threadIdx.x == 0) part[blockIdx.x] = e[0];
@@ -598,12 +633,13 @@ __global__ void k_gather_plain(SysView v, const double* x, const double* y, doub
 }
 
 __global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m) return;
+  const int64_t t_raw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = t_raw < m ? t_raw : m - 1;  // all lanes run the SVD (warp votes inside)
   double f[3][3], u[3][3], sg[3], vv[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) f[r][c] = F[t * 9 + r * 3 + c];
   svd_rv3(f, u, sg, vv);
+  if (t_raw >= m) return;
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) {
       U[t * 9 + r * 3 + c] = u[r][c];
@@ -636,7 +672,22 @@ int launch_body(qn_system* S, cudaStream_t st) {
   QN_CHECK_LAUNCH();
   k_vec<<<gv, kVT, 0, st>>>(v);
   QN_CHECK_LAUNCH();
-  k_tet<<<gt, kTT, 0, st>>>(v);
+  if (v.n_mat <= kMatSmem) {
+    k_tet<true><<<gt, kTT, 0, st>>>(v);
+  } else {
+    k_tet<false><<<gt, kTT, 0, st>>>(v);
+  }
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
+int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st) {
+  const SysView& v = S->v;
+  if (v.n_mat <= kMatSmem) {
+    k_tet_plain<true><<<v.nblk_t, kTT, 0, st>>>(v, x, b, mat_sel, part);
+  } else {
+    k_tet_plain<false><<<v.nblk_t, kTT, 0, st>>>(v, x, b, mat_sel, part);
+  }
   QN_CHECK_LAUNCH();
   return QN_OK;
 }

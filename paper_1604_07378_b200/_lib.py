@@ -53,7 +53,7 @@ class FactorInfo(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("nnz_a", C.c_int64), ("nnz_l", C.c_int64), ("n_supernodes", C.c_int64),
         ("max_front", C.c_int64), ("tree_depth", C.c_int64), ("nbatch", C.c_int64),
-        ("factor_seconds", C.c_double), ("flops", C.c_double),
+        ("factor_seconds", C.c_double), ("flops", C.c_double), ("dense_top", C.c_int64),
     ]
 
 

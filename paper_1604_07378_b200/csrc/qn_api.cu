@@ -117,6 +117,13 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_bcount, f->bcount.data(), f->bcount.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
+  if (f->ktop > 0) {
+    if ((rc = dev_upload(&f->d_sinv, f->sinv.data(), f->sinv.size()))) return rc;
+    if ((rc = dev_upload(&f->d_tcols, f->tcols.data(), f->tcols.size()))) return rc;
+    if ((rc = dev_upload(&f->d_tg_ptr, f->tg_ptr.data(), f->tg_ptr.size()))) return rc;
+    if ((rc = dev_upload(&f->d_tg_idx, f->tg_idx.data(), f->tg_idx.size()))) return rc;
+    if ((rc = dev_alloc(&f->d_gtop, (size_t)f->nbatch * f->ktop * 3))) return rc;
+  }
   const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};  // [ticket, exited, epoch] x 2, watchdog
   if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
   if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;
@@ -138,7 +145,8 @@ void factor_free_device(qn_factor* f) {
                   f->d_perm,    f->d_vals,        f->d_y,         f->d_x,         f->d_u,
                   f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
-                  f->d_fdep_idx};
+                  f->d_fdep_idx, f->d_sinv,       f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
+                  f->d_gtop};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;
@@ -275,6 +283,7 @@ int qn_factor_info_get(const qn_factor* f, qn_factor_info* info) {
   info->nbatch = f->nbatch;
   info->factor_seconds = f->factor_seconds;
   info->flops = f->flops;
+  info->dense_top = f->ktop;
   return QN_OK;
 }
 
@@ -433,7 +442,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_inst = (int32_t)ni;
   v.n_mat = (int32_t)d->n_mat;
   v.n_fixed = (int32_t)d->n_fixed;
-  v.nblk_v = div_up(n, 256);
+  v.nblk_v = div_up(n, kVertexThreads);
   v.nblk_t = std::max(1, div_up(mt, 128));
   v.h = d->h;
   for (int a = 0; a < 3; ++a) v.grav[a] = d->gravity[a];
@@ -463,6 +472,11 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     double* ms;
     if ((rc = sys_upload(S, &ms, d->masses, (size_t)n))) return fail(rc);
     v.masses = ms;
+    std::vector<double> w_in(n);
+    for (int64_t i = 0; i < n; ++i) w_in[i] = d->masses[i] / (d->h * d->h);  // dynamics.py:472
+    double* wi;
+    if ((rc = sys_upload(S, &wi, w_in.data(), w_in.size()))) return fail(rc);
+    v.w_in = wi;
     uint8_t* fx;
     if ((rc = sys_upload(S, &fx, is_fixed.data(), is_fixed.size()))) return fail(rc);
     v.is_fixed = fx;
@@ -717,7 +731,7 @@ int qn_system_objective(qn_system* S, const double* x, const double* y, double* 
   for (int64_t b = 0; b < S->n_inst; ++b) {
     if ((rc = to_device(dx, x + b * nv, nv, mem, st)) || (rc = to_device(dy, y + b * nv, nv, mem, st))) return rc;
     if ((rc = launch_tet_plain(S, dx, (int)b, -1, S->d_part_plain, st))) return rc;
-    k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
+    k_gather_plain<<<v.nblk_v, kVertexThreads, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
     QN_CHECK_LAUNCH();
     QN_CUDA(cudaMemcpyAsync(pt.data(), S->d_part_plain, v.nblk_t * sizeof(double), cudaMemcpyDeviceToHost, st));
     QN_CUDA(cudaMemcpyAsync(pv.data(), S->d_part_plain + v.nblk_t, v.nblk_v * sizeof(double), cudaMemcpyDeviceToHost,
@@ -754,7 +768,7 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
   if ((rc = launch_tet_plain(S, dx, (int)inst, (int)mat, S->d_part_plain, st))) return rc;
   if (grad_accum) {
     if ((rc = to_device(dg, grad_accum, nv, mem, st))) return rc;
-    k_gather_plain<<<v.nblk_v, 256, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
+    k_gather_plain<<<v.nblk_v, kVertexThreads, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
     QN_CHECK_LAUNCH();
     if ((rc = from_device(grad_accum, dg, nv, mem, st))) return rc;
   }

@@ -76,13 +76,45 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* smem /* >= K*3
     for (int k = 0; k < K; ++k) smem[k * 32 + warp] = v[k];
   }
   __syncthreads();
+  if (threadIdx.x < K) {  // thread k finishes value k (warps in index order)
+    double a = 0.0;
+    for (int w = 0; w < nw; ++w) a += smem[threadIdx.x * 32 + w];
+    smem[threadIdx.x * 32] = a;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double a = 0.0;
-      for (int w = 0; w < nw; ++w) a += smem[k * 32 + w];
-      v[k] = a;
-    }
+    for (int k = 0; k < K; ++k) v[k] = smem[k * 32];
+  }
+  __syncthreads();
+}
+
+// block_sum for the entries whose bit is set in `used` (K <= 64); others are
+// left untouched in thread 0.  `used` must be uniform across the block.
+template <int K>
+__device__ __forceinline__ void block_sum_masked(double (&v)[K], double* smem, unsigned long long used) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if ((used >> k) & 1ull) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((used >> k) & 1ull) smem[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+  // thread k finishes value k (warps in index order) into smem[k * 32]
+  if (threadIdx.x < K && ((used >> threadIdx.x) & 1ull)) {
+    double a = 0.0;
+    for (int w = 0; w < nw; ++w) a += smem[threadIdx.x * 32 + w];
+    smem[threadIdx.x * 32] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((used >> k) & 1ull) v[k] = smem[k * 32];
   }
   __syncthreads();
 }

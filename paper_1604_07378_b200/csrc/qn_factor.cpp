@@ -476,6 +476,35 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       if (f->parent[s] >= 0) height[f->parent[s]] = std::max(height[f->parent[s]], height[s] + 1);
     for (int32_t s = ns - 1; s >= 0; --s)
       if (f->parent[s] >= 0) dep[s] = dep[f->parent[s]] + 1;
+    // Dense top: the top levels of the tree are narrow and strictly serial in
+    // both solves.  With T = the supernodes of depth <= d* (closed under
+    // ancestors), L_T is the factor of the Schur complement S = A_TT -
+    // A_TB A_BB^-1 A_BT, so forward + backward on T collapse into one dense
+    // product x_T = S^-1 g_T (g_T = b_T minus the updates of the subtrees
+    // hanging below T).  d* = deepest level with |T| <= kTopMax columns.
+    f->is_top.assign(ns, 0);
+    f->ktop = 0;
+    f->tcols.clear();
+    if (nbatch == 1) {
+      int32_t maxd = 0;
+      for (int32_t s = 0; s < ns; ++s) maxd = std::max(maxd, dep[s]);
+      std::vector<int64_t> cols_at(maxd + 1, 0);
+      for (int32_t s = 0; s < ns; ++s) cols_at[dep[s]] += f->sup_col[s + 1] - f->sup_col[s];
+      int32_t dstar = -1;
+      int64_t cum = 0;
+      for (int32_t d = 0; d <= maxd; ++d) {
+        cum += cols_at[d];
+        if (cum > kTopMax) break;
+        dstar = d;
+      }
+      if (dstar >= 0) {
+        for (int32_t s = 0; s < ns; ++s) f->is_top[s] = dep[s] <= dstar;
+        for (int32_t s = 0; s < ns; ++s)
+          if (f->is_top[s])
+            for (int32_t c = f->sup_col[s]; c < f->sup_col[s + 1]; ++c) f->tcols.push_back(c);
+        f->ktop = (int32_t)f->tcols.size();
+      }
+    }
     std::vector<int32_t> order(ns);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return height[a] < height[b]; });
@@ -490,6 +519,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     f->ffirst.assign(ns, 0);
     f->bfirst.assign(ns, 0);
     for (int32_t s : order) {
+      if (f->is_top[s]) continue;
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nc <= kTaskEntries && nr - nc <= (int64_t)1 << 20, QN_ERR_UNSUPPORTED,
@@ -505,6 +535,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return dep[a] < dep[b]; });
     for (int32_t s : order) {
+      if (f->is_top[s]) continue;
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nr <= kTaskEntries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
@@ -529,6 +560,27 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
         const int32_t c = f->child_idx[q];
         for (int32_t t = 0; t < f->fcount[c]; ++t) f->fdep_idx[w++] = f->ffirst[c] + t;
       }
+    }
+    // g_T gather lists: every non-top supernode whose parent is top passes all
+    // of its subtree's updates to top columns in its update vector u_s
+    if (f->ktop > 0) {
+      std::vector<int32_t> tpos(n, -1);
+      for (int32_t k = 0; k < f->ktop; ++k) tpos[f->tcols[k]] = k;
+      std::vector<std::vector<int32_t>> lists(f->ktop);
+      for (int32_t s = 0; s < ns; ++s) {
+        if (f->is_top[s] || f->parent[s] < 0 || !f->is_top[f->parent[s]]) continue;
+        const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+        const int64_t r0 = f->sup_row_ptr[s] + nc, r1 = f->sup_row_ptr[s + 1];
+        for (int64_t r = r0; r < r1; ++r) {
+          const int32_t k = tpos[f->sup_rows[r]];
+          QN_REQUIRE(k >= 0, QN_ERR_ARG, "factor: update row outside the dense top");
+          lists[k].push_back((int32_t)(f->sup_upd_ptr[s] + (r - r0)));
+        }
+      }
+      f->tg_ptr.assign(f->ktop + 1, 0);
+      for (int32_t k = 0; k < f->ktop; ++k) f->tg_ptr[k + 1] = f->tg_ptr[k] + (int32_t)lists[k].size();
+      f->tg_idx.clear();
+      for (auto& l : lists) f->tg_idx.insert(f->tg_idx.end(), l.begin(), l.end());
     }
   }
   // tree depth
@@ -572,6 +624,13 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
   int err = QN_OK;
   std::string errmsg;
   const bool par_batch = nbatch > 1;
+  std::vector<int32_t> ttpos;  // factor column -> top index (dense top only; nbatch == 1)
+  std::vector<double> LT;
+  if (f->ktop > 0) {
+    ttpos.assign(n, -1);
+    for (int32_t k = 0; k < f->ktop; ++k) ttpos[f->tcols[k]] = k;
+    LT.assign((size_t)f->ktop * f->ktop, 0.0);
+  }
 #pragma omp parallel for schedule(dynamic, 1) if (par_batch)
   for (int64_t b = 0; b < nbatch; ++b) {
     if (err != QN_OK) continue;
@@ -647,6 +706,13 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
           }
         }
       }
+      // dense top: copy this supernode's columns of L into L_T
+      if (f->ktop > 0 && f->is_top[s]) {
+        for (int64_t j = 0; j < nc; ++j) {
+          const int64_t tj = ttpos[c0 + j];
+          for (int64_t i = j; i < nr; ++i) LT[(size_t)ttpos[f->sup_rows[r0 + i]] + (size_t)tj * f->ktop] = F[i + j * nr];
+        }
+      }
       // store Z = [inv(L11); L21 inv(L11)] (nr x nc, column-major): the forward
       // step of this supernode is then v = Z f (y = top, update = bottom) and
       // the backward step x = Z^T [y; -x_below] — dense, row/column parallel.
@@ -672,6 +738,35 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
   if (err != QN_OK) {
     set_error(errmsg);
     return err;
+  }
+  // S^-1 = L_T^-T L_T^-1 (symmetric, stored full, column-major)
+  if (f->ktop > 0) {
+    const int64_t K = f->ktop;
+    std::vector<double> M((size_t)K * K, 0.0);  // L_T^-1 (lower)
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t j = 0; j < K; ++j) {  // column j of L_T^-1: solve L_T m = e_j
+      double* Mj = M.data() + (size_t)j * K;
+      Mj[j] = 1.0;
+      for (int64_t k = j; k < K; ++k) {
+        const double* Lk = LT.data() + (size_t)k * K;
+        Mj[k] /= Lk[k];
+        const double mk = Mj[k];
+        if (mk != 0.0)
+          for (int64_t i = k + 1; i < K; ++i) Mj[i] -= Lk[i] * mk;
+      }
+    }
+    f->sinv.assign((size_t)K * K, 0.0);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t j = 0; j < K; ++j) {
+      const double* Mj = M.data() + (size_t)j * K;
+      for (int64_t i = j; i < K; ++i) {
+        const double* Mi = M.data() + (size_t)i * K;
+        double acc = 0.0;
+        for (int64_t k = i; k < K; ++k) acc += Mi[k] * Mj[k];  // rows >= max(i, j)
+        f->sinv[(size_t)i + (size_t)j * K] = acc;
+        f->sinv[(size_t)j + (size_t)i * K] = acc;
+      }
+    }
   }
   f->factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return QN_OK;

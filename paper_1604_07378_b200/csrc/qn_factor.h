@@ -34,6 +34,13 @@ struct qn_factor {
   std::vector<int32_t> fcount, bcount;  // tasks per supernode
   std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
   std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
+  // dense top: the supernodes within the top levels of the tree (K columns)
+  // are solved together as x_T = S^-1 g_T, S = Schur complement on T
+  std::vector<uint8_t> is_top;
+  int32_t ktop = 0;
+  std::vector<int32_t> tcols;           // factor column of each top index
+  std::vector<int32_t> tg_ptr, tg_idx;  // update rows (of the top's child subtrees) landing on each top column
+  std::vector<double> sinv;             // K x K, symmetric (column-major)
   int64_t nvals = 0, nupd = 0, nnz_l = 0;
   int32_t max_rows = 0, depth = 0;
   double flops = 0.0, factor_seconds = 0.0;
@@ -65,6 +72,11 @@ struct qn_factor {
   int32_t* d_fdep_ptr = nullptr;
   int32_t* d_fdep_idx = nullptr;
   unsigned* d_flags = nullptr;    // nbatch x (n_ftask + n_btask) completion epochs
+  double* d_sinv = nullptr;
+  int32_t* d_tcols = nullptr;
+  int32_t* d_tg_ptr = nullptr;
+  int32_t* d_tg_idx = nullptr;
+  double* d_gtop = nullptr;       // nbatch x K x 3
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
   unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)
@@ -75,6 +87,7 @@ struct qn_factor {
 
 namespace qn {
 constexpr int64_t kTaskEntries = 8192;  // Z entries per solve task (64 KB shared-memory tile)
+constexpr int64_t kTopMax = 2560;       // max columns of the dense top block (S^-1 <= 52 MB)
 
 // host: ordering + symbolic + numeric factorisation; returns QN_OK / QN_ERR_*
 int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int32_t* indices,

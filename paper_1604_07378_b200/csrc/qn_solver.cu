@@ -35,7 +35,7 @@
 
 namespace qn {
 
-constexpr int kVT = 256;  // vertex-kernel block
+constexpr int kVT = kVertexThreads;  // vertex-kernel block
 constexpr int kTT = 128;  // tet-kernel block
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
@@ -53,39 +53,56 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 // last block of instance b for counter `which`?  (after all partial writes)
+// Partials are written by thread 0 before this call; one fence by that thread
+// (after the barrier) orders them before the counter increment.  The last
+// block reads the partials with L2 loads (__ldcg).
 __device__ __forceinline__ bool last_block(unsigned* cnt, int which, int b, int n_inst, int nblk) {
   __shared__ bool s_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     unsigned* c = cnt + (size_t)which * n_inst + b;
     const unsigned old = atomicAdd(c, 1u);
     s_last = (old == (unsigned)nblk - 1);
-    if (s_last) *c = 0;
+    if (s_last) {
+      *c = 0;
+      __threadfence();
+    }
   }
   __syncthreads();
-  if (s_last) __threadfence();
   return s_last;
 }
 
 // Deterministic block-parallel sum of per-block partials (run by every thread of
-// the finalising block): out[k] = sum_blk part[blk * stride + k], k < nval.
-// Warp w owns values w, w + nw, ...; each lane sums a fixed block subset with 4
-// independent accumulators (4 loads in flight), then a fixed butterfly.
+// the finalising block): out[k] = sum_blk part[blk * stride + k], k < nval
+// (nval <= stride <= kNG).  Blocks are processed in chunks: the chunk's
+// partial rows (contiguous) are copied to shared memory with every thread
+// issuing independent loads, then lane l of the warp owning value k adds the
+// chunk's blocks l, l+32, ... into its running sum; a fixed butterfly
+// finishes.  Fixed order throughout, so the result is reproducible.
 __device__ void sum_partials(const double* part, int nblk, int stride, int nval, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = warp; k < nval; k += nw) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int blk = lane;
-    for (; blk + 96 < nblk; blk += 128) {
-      a0 += __ldcg(part + (size_t)blk * stride + k);
-      a1 += __ldcg(part + (size_t)(blk + 32) * stride + k);
-      a2 += __ldcg(part + (size_t)(blk + 64) * stride + k);
-      a3 += __ldcg(part + (size_t)(blk + 96) * stride + k);
+  // thread t < G*nval owns value k = t % nval and blocks t/nval, t/nval + G, ...
+  // (8 independent loads in flight per thread); the G per-thread sums of a
+  // value are then combined by thread k in index order.
+  __shared__ double sums[256];
+  const int G = min((int)blockDim.x, 256) / nval;
+  const int t = threadIdx.x;
+  if (t < G * nval) {
+    const int k = t % nval, j0 = t / nval;
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int blk = j0;
+    for (; blk + 7 * G < nblk; blk += 8 * G) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += __ldcg(part + (size_t)(blk + u * G) * stride + k);
     }
-    for (; blk < nblk; blk += 32) a0 += __ldcg(part + (size_t)blk * stride + k);
-    const double a = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) out[k] = a;
+    for (; blk < nblk; blk += G) a[0] += __ldcg(part + (size_t)blk * stride + k);
+    sums[t] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+  __syncthreads();
+  if (t < nval) {
+    double s = 0.0;
+    for (int j = 0; j < G; ++j) s += sums[j * nval + t];
+    out[t] = s;
   }
   __syncthreads();
 }
@@ -182,17 +199,36 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   if (i < v.n) {
     const size_t o = inst_off(v, b) + (size_t)i * 3;
     const double* x = v.X + vec_off(v, cur, b) + (size_t)i * 3;
-    const double w = v.masses[i] / __dmul_rn(v.h, v.h);
+    const double w = __ldg(v.w_in + i);
     double g[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) g[a] = __dmul_rn(w, __dsub_rn(x[a], v.y[o + a]));
     const double* fb = v.forces + (size_t)b * v.mt * 12;
     const int e1 = v.v2e_ptr[i + 1];
-    for (int e = v.v2e_ptr[i]; e < e1; ++e) {
-      const double* f = fb + (size_t)v.v2e[e] * 3;
-      g[0] = __dadd_rn(g[0], f[0]);
-      g[1] = __dadd_rn(g[1], f[1]);
-      g[2] = __dadd_rn(g[2], f[2]);
+    int e = v.v2e_ptr[i];
+    // element-order accumulation (the reference's np.add.at order); loads
+    // are batched 4 slots at a time so they are in flight together
+    for (; e + 4 <= e1; e += 4) {
+      double f[4][3];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double* fp = fb + (size_t)__ldg(v.v2e + e + q) * 3;
+        f[q][0] = __ldcg(fp);
+        f[q][1] = __ldcg(fp + 1);
+        f[q][2] = __ldcg(fp + 2);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        g[0] = __dadd_rn(g[0], f[q][0]);
+        g[1] = __dadd_rn(g[1], f[q][1]);
+        g[2] = __dadd_rn(g[2], f[q][2]);
+      }
+    }
+    for (; e < e1; ++e) {
+      const double* fp = fb + (size_t)__ldg(v.v2e + e) * 3;
+      g[0] = __dadd_rn(g[0], __ldcg(fp));
+      g[1] = __dadd_rn(g[1], __ldcg(fp + 1));
+      g[2] = __dadd_rn(g[2], __ldcg(fp + 2));
     }
     if (v.is_fixed[i]) g[0] = g[1] = g[2] = 0.0;
     double* go = v.Gr + vec_off(v, gnew, b) + (size_t)i * 3;
@@ -218,29 +254,43 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
       acc[3] = t[0] * t[0] + t[1] * t[1] + t[2] * t[2];
       acc[4] = s[0] * g[0] + s[1] * g[1] + s[2] * g[2];
     }
-    for (int p = 0; p < np; ++p) {
-      const double* si = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
-      acc[5 + kMaxM + p] = si[0] * g[0] + si[1] * g[1] + si[2] * g[2];
-      if (push) acc[5 + p] = si[0] * t[0] + si[1] * t[1] + si[2] * t[2];
+#pragma unroll
+    for (int p = 0; p < kMaxM; ++p) {  // compile-time indices keep acc[] in registers
+      if (p < np) {
+        const double* si = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
+        acc[5 + kMaxM + p] = si[0] * g[0] + si[1] * g[1] + si[2] * g[2];
+        if (push) acc[5 + p] = si[0] * t[0] + si[1] * t[1] + si[2] * t[2];
+      }
     }
   }
-  block_sum<kNG>(acc, red);
+  // reduce only the dot products in use: 0..4, 5..5+np, 5+kMaxM..5+kMaxM+np
+  const unsigned long long used = ((1ull << (5 + np)) - 1ull) | (((1ull << np) - 1ull) << (5 + kMaxM));
+  block_sum_masked<kNG>(acc, red, used);
+  // compact partial row: [0..5) scalars, [5, 5+np) <s_i,t_new>, [5+np, 5+2np) <s_i,g>
+  const int nval = 5 + 2 * np;
   if (threadIdx.x == 0) {
     double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG;
 #pragma unroll
-    for (int k = 0; k < kNG; ++k) pv[k] = acc[k];
+    for (int k = 0; k < 5; ++k) pv[k] = acc[k];
+#pragma unroll
+    for (int p = 0; p < kMaxM; ++p) {
+      if (p < np) {
+        pv[5 + p] = acc[5 + p];
+        pv[5 + np + p] = acc[5 + kMaxM + p];
+      }
+    }
   }
   if (!last_block(v.cnt, 0, b, v.n_inst, gridDim.x)) return;
   // ---- finalise: block-parallel partial sums, then one thread per instance ----
   double* tot = red;
-  sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, kNG, tot);
+  sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, nval, tot);
   if (threadIdx.x != 0) return;
   InstCtl& c = v.ctl[b];
   c.gs_cur = gnew;
   if (push) {
     const double rho = tot[1];
     const double guard = kCurvatureGuard * sqrt(tot[2]) * sqrt(tot[3]);
-    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + kMaxM + p];
+    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + np + p];
     if (rho > guard) {
       for (int p = 0; p < np; ++p) c.gram[c.ring[p]][cand] = tot[5 + p];
       c.rho[cand] = rho;
@@ -254,7 +304,7 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
       }
     }
   } else {
-    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + kMaxM + p];
+    for (int p = 0; p < np; ++p) c.sg[c.ring[p]] = tot[5 + np + p];
   }
   c.have_prev = 1;
   if (sqrt(tot[0]) <= cfg.grad_tol) {  // solvers.py:292-298
@@ -316,12 +366,15 @@ __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
   if (i < v.n) {
     const double* r = v.R0 + inst_off(v, b) + (size_t)i * 3;
     const double r0 = r[0], r1 = r[1], r2 = r[2];
-    for (int p = 0; p < np; ++p) {
-      const double* t = v.T + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
-      acc[p] = t[0] * r0 + t[1] * r1 + t[2] * r2;
+#pragma unroll
+    for (int p = 0; p < kMaxM; ++p) {
+      if (p < np) {
+        const double* t = v.T + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
+        acc[p] = t[0] * r0 + t[1] * r1 + t[2] * r2;
+      }
     }
   }
-  block_sum<kMaxM>(acc, red);
+  block_sum_masked<kMaxM>(acc, red, (1ull << np) - 1ull);
   if (threadIdx.x == 0) {
     double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG;
     for (int k = 0; k < kMaxM; ++k) pv[k] = acc[k];
@@ -613,7 +666,7 @@ __global__ void k_gather_plain(SysView v, const double* x, const double* y, doub
   if (i < v.n) {
     double g[3];
     if (inertia) {
-      const double w = v.masses[i] / __dmul_rn(v.h, v.h);
+      const double w = __ldg(v.w_in + i);
       for (int a = 0; a < 3; ++a) g[a] = __dmul_rn(w, __dsub_rn(x[3 * i + a], y[3 * i + a]));
       const double d0 = x[3 * i] - y[3 * i], d1 = x[3 * i + 1] - y[3 * i + 1], d2 = x[3 * i + 2] - y[3 * i + 2];
       e[0] = v.masses[i] * (d0 * d0 + d1 * d1 + d2 * d2);

@@ -53,6 +53,12 @@ struct FactorView {
   unsigned* flags;           // [nbatch][nftask + nbtask] epoch of completion per task
   unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
   unsigned long long* trace; // diagnostics: 3 timestamps per forward then backward item, or null
+  int32_t ktop;              // dense top (0 = none)
+  const double* sinv;        // K x K symmetric
+  const int32_t* tcols;
+  const int32_t* tg_ptr;
+  const int32_t* tg_idx;
+  double* gtop;              // [nbatch][K][3]
 };
 
 inline FactorView factor_view(const qn_factor* f) {
@@ -85,6 +91,12 @@ inline FactorView factor_view(const qn_factor* f) {
   v.flags = f->d_flags;
   v.sched = f->d_sched;
   v.trace = f->d_trace;
+  v.ktop = f->ktop;
+  v.sinv = f->d_sinv;
+  v.tcols = f->d_tcols;
+  v.tg_ptr = f->d_tg_ptr;
+  v.tg_idx = f->d_tg_idx;
+  v.gtop = f->d_gtop;
   return v;
 }
 
@@ -413,6 +425,79 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   cta_exit(sched, s_epoch);
 }
 
+// ---- dense top: g_T = b_T - (updates of the subtrees below T); x_T = S^-1 g_T ----
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_gather(FactorView F, IO io) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (!io.active(b) || k >= F.ktop) return;
+  const double* ub = F.u + (size_t)b * F.nupd * 3;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int q = F.tg_ptr[k]; q < F.tg_ptr[k + 1]; ++q) {
+    const double* uc = ub + 3 * (size_t)F.tg_idx[q];
+    a0 += __ldcg(uc);
+    a1 += __ldcg(uc + 1);
+    a2 += __ldcg(uc + 2);
+  }
+  double v[3];
+  io.rhs(b, F.tcols[k], v);
+  double* g = F.gtop + ((size_t)b * F.ktop + k) * 3;
+  g[0] = v[0] - a0;
+  g[1] = v[1] - a1;
+  g[2] = v[2] - a2;
+}
+
+// x_T = S^-1 g_T: warp per row k; row k of the symmetric S^-1 is its contiguous
+// column k, so every lane streams its share with 8 loads in flight.
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_apply(FactorView F, IO io) {
+  extern __shared__ double sg[];  // g_T (K x 3)
+  const int b = blockIdx.y;
+  if (!io.active(b)) return;
+  const int K = F.ktop;
+  const double* g = F.gtop + (size_t)b * K * 3;
+  for (int w = threadIdx.x; w < 3 * K; w += blockDim.x) sg[w] = __ldcg(g + w);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp_global = blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * kSolveWarps;
+  for (int k = warp_global; k < K; k += nwarps) {
+    const double* col = F.sinv + (size_t)k * K;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    int c = lane;
+    for (; c + 224 < K; c += 256) {
+      double l[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) l[q] = __ldg(col + c + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int cc = c + 32 * q;
+        a0 = fma(l[q], sg[3 * cc + 0], a0);
+        a1 = fma(l[q], sg[3 * cc + 1], a1);
+        a2 = fma(l[q], sg[3 * cc + 2], a2);
+      }
+    }
+    for (; c < K; c += 32) {
+      const double l = __ldg(col + c);
+      a0 = fma(l, sg[3 * c + 0], a0);
+      a1 = fma(l, sg[3 * c + 1], a1);
+      a2 = fma(l, sg[3 * c + 2], a2);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+      const int row = F.tcols[k];
+      double* xo = F.x + ((size_t)b * F.n + row) * 3;
+      xo[0] = a0;
+      xo[1] = a1;
+      xo[2] = a2;
+      const double v[3] = {a0, a1, a2};
+      io.store(b, row, v);
+    }
+  }
+}
+
 // Plain solve: B (n,3) -> X (n,3) in the original row order, one instance.
 struct PlainIO {
   const double* B;
@@ -438,10 +523,22 @@ template <class IO>
 int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   const FactorView v = factor_view(f);
   const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
-  sptrsv_forward<IO><<<std::min(nf, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
-  QN_CHECK_LAUNCH();
-  sptrsv_backward<IO><<<std::min(nb, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
-  QN_CHECK_LAUNCH();
+  if (nf > 0) {
+    sptrsv_forward<IO><<<std::min(nf, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
+    QN_CHECK_LAUNCH();
+  }
+  if (f->ktop > 0) {
+    const dim3 gg((f->ktop + kSolveThreads - 1) / kSolveThreads, (unsigned)f->nbatch);
+    sptrsv_top_gather<IO><<<gg, kSolveThreads, 0, stream>>>(v, io);
+    QN_CHECK_LAUNCH();
+    const dim3 ga(std::max(1, std::min(2 * kSMs, (f->ktop + kSolveWarps - 1) / kSolveWarps)), (unsigned)f->nbatch);
+    sptrsv_top_apply<IO><<<ga, kSolveThreads, (size_t)f->ktop * 3 * sizeof(double), stream>>>(v, io);
+    QN_CHECK_LAUNCH();
+  }
+  if (nb > 0) {
+    sptrsv_backward<IO><<<std::min(nb, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
+    QN_CHECK_LAUNCH();
+  }
   return QN_OK;
 }
 
@@ -452,6 +549,9 @@ int prepare_solve_kernels(qn_factor* f) {
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (f->ktop > 0)
+    QN_CUDA(cudaFuncSetAttribute(sptrsv_top_apply<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(f->ktop * 3 * sizeof(double))));
   int per_f = 0, per_b = 0, dev = 0, sms = 0;
   QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, sptrsv_forward<IO>, kSolveThreads, smem_bytes));
   QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, sptrsv_backward<IO>, kSolveThreads, smem_bytes));

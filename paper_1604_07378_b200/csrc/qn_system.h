@@ -23,6 +23,7 @@ enum Phase : int32_t {
 };
 
 constexpr int kMaxM = QN_MAX_M;
+constexpr int kVertexThreads = 128;  // vertex kernels: small blocks so every SM gets work
 constexpr int kNG = 5 + 2 * kMaxM;  // gradient-kernel dot products per block
 
 struct InstCtl {
@@ -55,6 +56,7 @@ struct SysView {
   const int32_t* tet_mat;
   const qn_material* mats;
   const double* masses;
+  const double* w_in;        // masses / h^2 (dynamics.py:472), precomputed on the host
   const uint8_t* is_fixed;
   const int32_t* fixed_pos;  // vertex -> index into the fixed list, -1 if free
   const int32_t* v2e_ptr;

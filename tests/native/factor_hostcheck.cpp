@@ -60,6 +60,23 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
       }
     done_f[s]++;
   }
+  if (f.ktop > 0) {  // dense top: x_T = S^-1 (b_T - updates of the subtrees below T)
+    const int K = f.ktop;
+    std::vector<double> g(3 * K);
+    for (int k = 0; k < K; ++k)
+      for (int a = 0; a < 3; ++a) {
+        double acc = 0;
+        for (int q = f.tg_ptr[k]; q < f.tg_ptr[k + 1]; ++q) acc += u[3 * f.tg_idx[q] + a];
+        g[3 * k + a] = B[3 * f.perm[f.tcols[k]] + a] - acc;
+      }
+    for (int k = 0; k < K; ++k)
+      for (int a = 0; a < 3; ++a) {
+        double v = 0;
+        for (int c = 0; c < K; ++c) v += f.sinv[(size_t)k * K + c] * g[3 * c + a];
+        x[3 * f.tcols[k] + a] = v;
+        X[3 * f.perm[f.tcols[k]] + a] = v;
+      }
+  }
   for (const int4& t : f.btask) {
     const int s = t.x;
     if (f.parent[s] >= 0 && done_b[f.parent[s]] != f.bcount[f.parent[s]]) return 98;
@@ -86,6 +103,7 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
     stats[3] = f.max_rows;
     stats[4] = (int64_t)f.ftask.size();
     stats[5] = (int64_t)f.btask.size();
+    stats[6] = f.ktop;
   }
   return 0;
 }

@@ -81,7 +81,7 @@ def _hc_solve(lib, A, coords, B, values=None, nbatch=1, b=0):
     A.sort_indices()
     n = A.shape[0]
     X = np.zeros((n, 3))
-    st = np.zeros(6, dtype=np.int64)
+    st = np.zeros(8, dtype=np.int64)
     vals = np.ascontiguousarray(A.data if values is None else values)
     rc = lib.hc_factor_solve(C.c_int64(n), _lib.ptr(_lib.i64(A.indptr)), _lib.ptr(_lib.i32(A.indices)),
                              _lib.ptr(vals), C.c_int64(nbatch), _lib.ptr(coords), C.c_int64(b), _lib.ptr(B),
@@ -98,8 +98,10 @@ def test_host_supernodal_factor_and_solve_replay(hostcheck, cfg):
     assert rc == 0
     ref = osys.factor.solve(B)
     assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
-    nsup, nnz_l, depth, max_rows, nft, nbt = st
-    assert nft >= nsup and nbt >= nsup
+    nsup, nnz_l, depth, max_rows, nft, nbt, ktop = st[:7]
+    assert 0 < ktop <= 2560  # dense top block in use
+    if cfg == "c1":
+        assert nft == 0 and nbt == 0 and ktop == osys.free.size  # whole tree fits the dense top
     assert depth <= 16  # nested dissection + amalgamation keep the dependency tree shallow
     if cfg == "c2":
         assert nnz_l < 3.34e6  # below the SuperLU-MMD fill of the survey probe

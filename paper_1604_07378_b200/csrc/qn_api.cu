@@ -442,7 +442,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_inst = (int32_t)ni;
   v.n_mat = (int32_t)d->n_mat;
   v.n_fixed = (int32_t)d->n_fixed;
-  v.nblk_v = div_up(n, kVertexThreads);
+  v.nblk_v = div_up(3 * n, kVertexThreads);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, 128));
   v.h = d->h;
   for (int a = 0; a < 3; ++a) v.grav[a] = d->gravity[a];

@@ -180,6 +180,27 @@ __global__ void k_init(SysView v) {
   }
 }
 
+// The finalisers run their scalar logic on a shared-memory copy of the
+// instance's control block (one cooperative round trip in, one out) instead
+// of chains of dependent global loads.
+static_assert(sizeof(InstCtl) % 8 == 0, "InstCtl must be a whole number of 8-byte words");
+__device__ __forceinline__ void ctl_load(const InstCtl* g, InstCtl* s) {
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(s);
+  for (int w = threadIdx.x; w < (int)(sizeof(InstCtl) / 8); w += blockDim.x) dst[w] = __ldcg(src + w);
+  __syncthreads();
+}
+__device__ __forceinline__ void ctl_store(InstCtl* g, const InstCtl* s) {
+  __syncthreads();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(s);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(g);
+  for (int w = threadIdx.x; w < (int)(sizeof(InstCtl) / 8); w += blockDim.x) __stcg(dst + w, src[w]);
+}
+
+__device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, bool push, int np, int cand,
+                              int gnew);
+__device__ void eta_finalize(InstCtl& c, const double* tot, int np);
+
 // ---------------------------------------------------------------------------
 // gradient gather + L-BFGS push / zeta (dynamics.py:470-478, solvers.py:83-103, 124-131)
 __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
@@ -195,71 +216,47 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   double acc[kNG];
 #pragma unroll
   for (int k = 0; k < kNG; ++k) acc[k] = 0.0;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < v.n) {
-    const size_t o = inst_off(v, b) + (size_t)i * 3;
-    const double* x = v.X + vec_off(v, cur, b) + (size_t)i * 3;
-    const double w = __ldg(v.w_in + i);
-    double g[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) g[a] = __dmul_rn(w, __dsub_rn(x[a], v.y[o + a]));
-    const double* fb = v.forces + (size_t)b * v.mt * 12;
-    const int e1 = v.v2e_ptr[i + 1];
-    int e = v.v2e_ptr[i];
+  // one thread per (vertex, coordinate): 3x the parallelism of a vertex loop,
+  // coalesced vector accesses, and the same per-coordinate summation order
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci < 3 * v.n) {
+    const int i = ci / 3;
+    const size_t oc = inst_off(v, b) + (size_t)ci;
+    const double xc = v.X[vec_off(v, cur, b) + ci];
+    double g = __dmul_rn(__ldg(v.w_in + i), __dsub_rn(xc, v.y[oc]));
+    const double* fb = v.forces + (size_t)b * v.mt * 12 + (ci - 3 * i);
+    const int e1 = __ldg(v.v2e_ptr + i + 1);
+    int e = __ldg(v.v2e_ptr + i);
     // element-order accumulation (the reference's np.add.at order); loads
-    // are batched 4 slots at a time so they are in flight together
-    for (; e + 4 <= e1; e += 4) {
-      double f[4][3];
+    // are batched 8 slots at a time so they are in flight together
+    for (; e + 8 <= e1; e += 8) {
+      double f[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double* fp = fb + (size_t)__ldg(v.v2e + e + q) * 3;
-        f[q][0] = __ldcg(fp);
-        f[q][1] = __ldcg(fp + 1);
-        f[q][2] = __ldcg(fp + 2);
-      }
+      for (int q = 0; q < 8; ++q) f[q] = __ldcg(fb + (size_t)__ldg(v.v2e + e + q) * 3);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        g[0] = __dadd_rn(g[0], f[q][0]);
-        g[1] = __dadd_rn(g[1], f[q][1]);
-        g[2] = __dadd_rn(g[2], f[q][2]);
-      }
+      for (int q = 0; q < 8; ++q) g = __dadd_rn(g, f[q]);
     }
-    for (; e < e1; ++e) {
-      const double* fp = fb + (size_t)__ldg(v.v2e + e) * 3;
-      g[0] = __dadd_rn(g[0], __ldcg(fp));
-      g[1] = __dadd_rn(g[1], __ldcg(fp + 1));
-      g[2] = __dadd_rn(g[2], __ldcg(fp + 2));
-    }
-    if (v.is_fixed[i]) g[0] = g[1] = g[2] = 0.0;
-    double* go = v.Gr + vec_off(v, gnew, b) + (size_t)i * 3;
-    go[0] = g[0];
-    go[1] = g[1];
-    go[2] = g[2];
-    acc[0] = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
-    double s[3] = {0, 0, 0}, t[3] = {0, 0, 0};
+    for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + (size_t)__ldg(v.v2e + e) * 3));
+    if (v.is_fixed[i]) g = 0.0;
+    v.Gr[vec_off(v, gnew, b) + ci] = g;
+    acc[0] = g * g;
+    double s = 0.0, t = 0.0;
     if (push) {
-      const double* xp = v.X + vec_off(v, prv, b) + (size_t)i * 3;
-      const double* gp = v.Gr + vec_off(v, gcur, b) + (size_t)i * 3;
-      double* so = v.S + vec_off(v, cand, b) + (size_t)i * 3;
-      double* to = v.T + vec_off(v, cand, b) + (size_t)i * 3;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        s[a] = __dsub_rn(x[a], xp[a]);
-        t[a] = __dsub_rn(g[a], gp[a]);
-        so[a] = s[a];
-        to[a] = t[a];
-      }
-      acc[1] = t[0] * s[0] + t[1] * s[1] + t[2] * s[2];
-      acc[2] = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
-      acc[3] = t[0] * t[0] + t[1] * t[1] + t[2] * t[2];
-      acc[4] = s[0] * g[0] + s[1] * g[1] + s[2] * g[2];
+      s = __dsub_rn(xc, v.X[vec_off(v, prv, b) + ci]);
+      t = __dsub_rn(g, v.Gr[vec_off(v, gcur, b) + ci]);
+      v.S[vec_off(v, cand, b) + ci] = s;
+      v.T[vec_off(v, cand, b) + ci] = t;
+      acc[1] = t * s;
+      acc[2] = s * s;
+      acc[3] = t * t;
+      acc[4] = s * g;
     }
 #pragma unroll
     for (int p = 0; p < kMaxM; ++p) {  // compile-time indices keep acc[] in registers
       if (p < np) {
-        const double* si = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
-        acc[5 + kMaxM + p] = si[0] * g[0] + si[1] * g[1] + si[2] * g[2];
-        if (push) acc[5 + p] = si[0] * t[0] + si[1] * t[1] + si[2] * t[2];
+        const double si = v.S[vec_off(v, cc->ring[p], b) + ci];
+        acc[5 + kMaxM + p] = si * g;
+        if (push) acc[5 + p] = si * t;
       }
     }
   }
@@ -281,11 +278,19 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
     }
   }
   if (!last_block(v.cnt, 0, b, v.n_inst, gridDim.x)) return;
-  // ---- finalise: block-parallel partial sums, then one thread per instance ----
+  // ---- finalise: block-parallel partial sums, control block staged in shared
+  //      memory, scalar logic on one thread, control block written back ----
   double* tot = red;
   sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, nval, tot);
-  if (threadIdx.x != 0) return;
-  InstCtl& c = v.ctl[b];
+  __shared__ InstCtl sc;
+  ctl_load(v.ctl + b, &sc);
+  if (threadIdx.x == 0) grad_finalize(v, sc, tot, push, np, cand, gnew);
+  ctl_store(v.ctl + b, &sc);
+}
+
+__device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, bool push, int np, int cand,
+                              int gnew) {
+  const DevConfig& cfg = *v.cfg;
   c.gs_cur = gnew;
   if (push) {
     const double rho = tot[1];
@@ -362,17 +367,12 @@ __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
   double acc[kMaxM];
 #pragma unroll
   for (int k = 0; k < kMaxM; ++k) acc[k] = 0.0;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < v.n) {
-    const double* r = v.R0 + inst_off(v, b) + (size_t)i * 3;
-    const double r0 = r[0], r1 = r[1], r2 = r[2];
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;  // (vertex, coordinate)
+  if (ci < 3 * v.n) {
+    const double r = v.R0[inst_off(v, b) + ci];
 #pragma unroll
-    for (int p = 0; p < kMaxM; ++p) {
-      if (p < np) {
-        const double* t = v.T + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
-        acc[p] = t[0] * r0 + t[1] * r1 + t[2] * r2;
-      }
-    }
+    for (int p = 0; p < kMaxM; ++p)
+      if (p < np) acc[p] = v.T[vec_off(v, cc->ring[p], b) + ci] * r;
   }
   block_sum_masked<kMaxM>(acc, red, (1ull << np) - 1ull);
   if (threadIdx.x == 0) {
@@ -382,8 +382,15 @@ __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
   if (!last_block(v.cnt, 1, b, v.n_inst, gridDim.x)) return;
   double* tot = red;
   sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, np, tot);
-  if (threadIdx.x != 0) return;
-  InstCtl& c = v.ctl[b];
+  __shared__ InstCtl sc;
+  ctl_load(v.ctl + b, &sc);
+  if (threadIdx.x == 0) eta_finalize(sc, tot, np);
+  __syncthreads();
+  // only coef[] changed
+  if (threadIdx.x < np) v.ctl[b].coef[threadIdx.x] = sc.coef[threadIdx.x];
+}
+
+__device__ void eta_finalize(InstCtl& c, const double* tot, int np) {
   for (int p = 0; p < np; ++p) {
     const int sp = c.ring[p];
     double tr = tot[p];
@@ -401,49 +408,30 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
   if (ph == PH_GRAD || ph == PH_DONE) return;
   __shared__ double red[2 * 32];
   double acc[2] = {0.0, 0.0};
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < v.n) {
-    const size_t o = inst_off(v, b) + (size_t)i * 3;
-    const double* x = v.X + vec_off(v, cc->xs_cur, b) + (size_t)i * 3;
-    double xt[3] = {x[0], x[1], x[2]};
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;  // (vertex, coordinate)
+  if (ci < 3 * v.n) {
+    const size_t oc = inst_off(v, b) + (size_t)ci;
+    const double x = v.X[vec_off(v, cc->xs_cur, b) + ci];
+    double xt = x;
     if (ph == PH_DIR || ph == PH_ALPHA) {
-      double d[3];
+      double d;
       if (ph == PH_DIR) {
-        const double* r = v.R0 + o;
-        d[0] = r[0];
-        d[1] = r[1];
-        d[2] = r[2];
-        for (int p = 0; p < cc->npairs; ++p) {  // r += s (zeta - eta), oldest first
-          const double cf = cc->coef[p];
-          const double* s = v.S + vec_off(v, cc->ring[p], b) + (size_t)i * 3;
-          d[0] = __dadd_rn(d[0], __dmul_rn(s[0], cf));
-          d[1] = __dadd_rn(d[1], __dmul_rn(s[1], cf));
-          d[2] = __dadd_rn(d[2], __dmul_rn(s[2], cf));
-        }
-        double* dd = v.D + o;
-        dd[0] = d[0];
-        dd[1] = d[1];
-        dd[2] = d[2];
-        const double* g = v.Gr + vec_off(v, cc->gs_cur, b) + (size_t)i * 3;
-        acc[1] = g[0] * d[0] + g[1] * d[1] + g[2] * d[2];
+        d = v.R0[oc];
+        const int np = cc->npairs;
+        for (int p = 0; p < np; ++p)  // r += s (zeta - eta), oldest first
+          d = __dadd_rn(d, __dmul_rn(v.S[vec_off(v, cc->ring[p], b) + ci], cc->coef[p]));
+        v.D[oc] = d;
+        acc[1] = v.Gr[vec_off(v, cc->gs_cur, b) + ci] * d;
       } else {
-        const double* dd = v.D + o;
-        d[0] = dd[0];
-        d[1] = dd[1];
-        d[2] = dd[2];
+        d = v.D[oc];
       }
       const double al = (ph == PH_DIR) ? (v.cfg->line_search ? __dmul_rn(v.cfg->alpha_init, v.cfg->shrink) : 1.0)
                                         : cc->alpha;
-      double* xo = v.X + vec_off(v, cc->xs_trial, b) + (size_t)i * 3;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        xt[a] = __dadd_rn(x[a], __dmul_rn(al, d[a]));
-        xo[a] = xt[a];
-      }
+      xt = __dadd_rn(x, __dmul_rn(al, d));
+      v.X[vec_off(v, cc->xs_trial, b) + ci] = xt;
     }
-    const double* y = v.y + o;
-    const double e0 = xt[0] - y[0], e1 = xt[1] - y[1], e2 = xt[2] - y[2];
-    acc[0] = v.masses[i] * (e0 * e0 + e1 * e1 + e2 * e2);
+    const double e = xt - v.y[oc];
+    acc[0] = __ldg(v.masses + ci / 3) * (e * e);
   }
   block_sum<2>(acc, red);
   if (threadIdx.x == 0) {
@@ -454,9 +442,8 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
 }
 
 // one thread; e_el / inert / slope are the block-parallel sums of the partials
-__device__ void finalize_trial(const SysView& v, int b, double e_el, double inert, double slope) {
+__device__ void finalize_trial(const SysView& v, InstCtl& c, double e_el, double inert, double slope) {
   const DevConfig& cfg = *v.cfg;
-  InstCtl& c = v.ctl[b];
   const double g_new = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
   const int ph = c.phase;
   if (ph == PH_FIRST) {
@@ -603,7 +590,10 @@ __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
       __shared__ double tot[3];
       sum_partials(v.part_t + (size_t)b * v.nblk_t, v.nblk_t, 1, 1, tot);
       sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG + (kNG - 2), v.nblk_v, kNG, 2, tot + 1);
-      if (threadIdx.x == 0) finalize_trial(v, b, tot[0], tot[1], tot[2]);
+      __shared__ InstCtl sc;
+      ctl_load(v.ctl + b, &sc);
+      if (threadIdx.x == 0) finalize_trial(v, sc, tot[0], tot[1], tot[2]);
+      ctl_store(v.ctl + b, &sc);
     }
   }
   // last block overall: loop condition of the frame graph

@@ -134,6 +134,9 @@ int factor_upload(qn_factor* f) {
                         sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows) +
                         sizeof(int) * kStageIdx);
   QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
+  // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
+  const size_t bsm = sizeof(double) * 3 * ((size_t)f->n + max_nc);
+  f->batch_smem = (f->nbatch > 1 && bsm <= 96 * 1024) ? (int)bsm : 0;
   if ((rc = prepare_solve_kernels<PlainIO>(f))) return rc;
   f->on_device = true;
   return QN_OK;

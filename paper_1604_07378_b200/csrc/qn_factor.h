@@ -82,6 +82,7 @@ struct qn_factor {
   unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)
   int smem_bytes = 0;
   int grid_ctas = 0;              // persistent solve grid (co-resident CTAs)
+  int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)
   bool on_device = false;
 };
 

@@ -498,6 +498,128 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_apply(FactorView F, 
   }
 }
 
+// ---- batched small systems (configs[3]): one CTA per instance walks its whole
+// tree (postorder forward, reverse backward) with CTA barriers between
+// supernodes — no inter-CTA flags, so thousands of instances run as
+// thousands of independent CTAs.  y/x of the instance live in shared memory
+// (x overwrites y in place during the backward sweep); the update vectors
+// stay in the instance's (L2-resident) global slice.
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads) sptrsv_batch(FactorView F, IO io) {
+  extern __shared__ double sm[];  // yx[n*3] | f[max_nc*3]
+  const int b = blockIdx.x;
+  if (!io.active(b)) return;
+  const int n = F.n;
+  double* yx = sm;
+  double* f = sm + 3 * n;
+  double* ub = F.u + (size_t)b * F.nupd * 3;
+  const double* vb = F.vals + (size_t)b * F.nvals;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- forward: y = L^-1 b ----
+  for (int s = 0; s < F.nsup; ++s) {
+    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
+    const int64_t R0 = F.sup_row_ptr[s];
+    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+    for (int p = tid; p < nc; p += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
+        const double* uc = ub + 3 * (size_t)F.cidx[q];
+        a0 += uc[0];
+        a1 += uc[1];
+        a2 += uc[2];
+      }
+      double v[3];
+      io.rhs(b, c0 + p, v);
+      f[3 * p + 0] = v[0] - a0;
+      f[3 * p + 1] = v[1] - a1;
+      f[3 * p + 2] = v[2] - a2;
+    }
+    __syncthreads();
+    const double* Z = vb + F.sup_val_ptr[s];
+    for (int r = tid; r < nr; r += blockDim.x) {
+      const int kmax = r < nc ? r + 1 : nc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      int k = 0;
+      for (; k + 8 <= kmax; k += 8) {
+        double l[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) l[q] = __ldg(Z + r + (int64_t)(k + q) * nr);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          a0 = fma(l[q], f[3 * (k + q) + 0], a0);
+          a1 = fma(l[q], f[3 * (k + q) + 1], a1);
+          a2 = fma(l[q], f[3 * (k + q) + 2], a2);
+        }
+      }
+      for (; k < kmax; ++k) {
+        const double l = __ldg(Z + r + (int64_t)k * nr);
+        a0 = fma(l, f[3 * k + 0], a0);
+        a1 = fma(l, f[3 * k + 1], a1);
+        a2 = fma(l, f[3 * k + 2], a2);
+      }
+      if (r < nc) {
+        yx[3 * (c0 + r) + 0] = a0;
+        yx[3 * (c0 + r) + 1] = a1;
+        yx[3 * (c0 + r) + 2] = a2;
+      } else {
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+        for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
+          const double* uc = ub + 3 * (size_t)F.cidx[q];
+          e0 += uc[0];
+          e1 += uc[1];
+          e2 += uc[2];
+        }
+        double* us = ub + (F.sup_upd_ptr[s] + (r - nc)) * 3;
+        us[0] = e0 + a0;
+        us[1] = e1 + a1;
+        us[2] = e2 + a2;
+      }
+    }
+    __syncthreads();
+  }
+  // ---- backward: x = L^-T y (in place over y) ----
+  for (int s = F.nsup - 1; s >= 0; --s) {
+    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
+    const int64_t R0 = F.sup_row_ptr[s];
+    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+    for (int p = tid; p < 3 * nc; p += blockDim.x) f[p] = yx[3 * c0 + p];
+    __syncthreads();
+    const double* Z = vb + F.sup_val_ptr[s];
+    for (int k = warp; k < nc; k += kSolveWarps) {
+      const double* col = Z + (int64_t)k * nr;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int r = k + lane; r < nr; r += 32) {
+        const double l = __ldg(col + r);
+        double w0, w1, w2;
+        if (r < nc) {
+          w0 = f[3 * r + 0];
+          w1 = f[3 * r + 1];
+          w2 = f[3 * r + 2];
+        } else {
+          const int row = F.sup_rows[R0 + r];
+          w0 = -yx[3 * row + 0];
+          w1 = -yx[3 * row + 1];
+          w2 = -yx[3 * row + 2];
+        }
+        a0 = fma(l, w0, a0);
+        a1 = fma(l, w1, a1);
+        a2 = fma(l, w2, a2);
+      }
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      a2 = warp_sum(a2);
+      if (lane == 0) {
+        yx[3 * (c0 + k) + 0] = a0;
+        yx[3 * (c0 + k) + 1] = a1;
+        yx[3 * (c0 + k) + 2] = a2;
+        const double v[3] = {a0, a1, a2};
+        io.store(b, c0 + k, v);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Plain solve: B (n,3) -> X (n,3) in the original row order, one instance.
 struct PlainIO {
   const double* B;
@@ -522,6 +644,11 @@ struct PlainIO {
 template <class IO>
 int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   const FactorView v = factor_view(f);
+  if (f->batch_smem > 0) {  // batched small systems: one CTA per instance
+    sptrsv_batch<IO><<<(int)f->nbatch, kSolveThreads, f->batch_smem, stream>>>(v, io);
+    QN_CHECK_LAUNCH();
+    return QN_OK;
+  }
   const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
   if (nf > 0) {
     sptrsv_forward<IO><<<std::min(nf, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
@@ -552,6 +679,8 @@ int prepare_solve_kernels(qn_factor* f) {
   if (f->ktop > 0)
     QN_CUDA(cudaFuncSetAttribute(sptrsv_top_apply<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(f->ktop * 3 * sizeof(double))));
+  if (f->batch_smem > 0)
+    QN_CUDA(cudaFuncSetAttribute(sptrsv_batch<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->batch_smem));
   int per_f = 0, per_b = 0, dev = 0, sms = 0;
   QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, sptrsv_forward<IO>, kSolveThreads, smem_bytes));
   QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, sptrsv_backward<IO>, kSolveThreads, smem_bytes));

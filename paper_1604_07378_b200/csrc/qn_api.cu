@@ -639,7 +639,17 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   }
   QN_CUDA(cudaEventRecord(S->ev0, st));
   if (S->use_graph) {
-    if (!S->exec && (rc = build_graph(S))) return rc;
+    const int mb = c.m <= 5 ? 5 : kMaxM;  // kernels are specialised on the history bound
+    if (S->exec && S->graph_m_bound != mb) {
+      cudaGraphExecDestroy(S->exec);
+      S->exec = nullptr;
+      cudaGraphDestroy(S->graph);
+      S->graph = nullptr;
+    }
+    if (!S->exec) {
+      if ((rc = build_graph(S))) return rc;
+      S->graph_m_bound = mb;
+    }
     QN_CUDA(cudaGraphLaunch(S->exec, st));
     count_launch(0);
   } else {

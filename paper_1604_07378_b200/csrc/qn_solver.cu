@@ -203,7 +203,11 @@ __device__ void eta_finalize(InstCtl& c, const double* tot, int np);
 
 // ---------------------------------------------------------------------------
 // gradient gather + L-BFGS push / zeta (dynamics.py:470-478, solvers.py:83-103, 124-131)
+// M = compile-time bound on the history window (the register footprint of the
+// dot-product accumulators scales with it; the host picks the smallest that fits).
+template <int M>
 __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
+  constexpr int NG = 5 + 2 * M;
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   if (cc->phase != PH_GRAD) return;
@@ -213,9 +217,9 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   const DevConfig& cfg = *v.cfg;
   const bool push = cc->have_prev && cfg.kind == 1 && cfg.m > 0;
   const int cand = cc->ring[np];
-  double acc[kNG];
+  double acc[NG];
 #pragma unroll
-  for (int k = 0; k < kNG; ++k) acc[k] = 0.0;
+  for (int k = 0; k < NG; ++k) acc[k] = 0.0;
   // one thread per (vertex, coordinate): 3x the parallelism of a vertex loop,
   // coalesced vector accesses, and the same per-coordinate summation order
   const int ci = blockIdx.x * blockDim.x + threadIdx.x;
@@ -252,17 +256,17 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
       acc[4] = s * g;
     }
 #pragma unroll
-    for (int p = 0; p < kMaxM; ++p) {  // compile-time indices keep acc[] in registers
+    for (int p = 0; p < M; ++p) {  // compile-time indices keep acc[] in registers
       if (p < np) {
         const double si = v.S[vec_off(v, cc->ring[p], b) + ci];
-        acc[5 + kMaxM + p] = si * g;
+        acc[5 + M + p] = si * g;
         if (push) acc[5 + p] = si * t;
       }
     }
   }
-  // reduce only the dot products in use: 0..4, 5..5+np, 5+kMaxM..5+kMaxM+np
-  const unsigned long long used = ((1ull << (5 + np)) - 1ull) | (((1ull << np) - 1ull) << (5 + kMaxM));
-  block_sum_masked<kNG>(acc, red, used);
+  // reduce only the dot products in use: 0..4, 5..5+np, 5+M..5+M+np
+  const unsigned long long used = ((1ull << (5 + np)) - 1ull) | (((1ull << np) - 1ull) << (5 + M));
+  block_sum_masked<NG>(acc, red, used);
   // compact partial row: [0..5) scalars, [5, 5+np) <s_i,t_new>, [5+np, 5+2np) <s_i,g>
   const int nval = 5 + 2 * np;
   if (threadIdx.x == 0) {
@@ -270,10 +274,10 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) pv[k] = acc[k];
 #pragma unroll
-    for (int p = 0; p < kMaxM; ++p) {
+    for (int p = 0; p < M; ++p) {
       if (p < np) {
         pv[5 + p] = acc[5 + p];
-        pv[5 + np + p] = acc[5 + kMaxM + p];
+        pv[5 + np + p] = acc[5 + M + p];
       }
     }
   }
@@ -358,26 +362,27 @@ struct SolverIO {
 };
 
 // <t_i, r0> and the eta recursion (solvers.py:147-150)
+template <int M>
 __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   if (cc->phase != PH_DIR || cc->npairs == 0) return;
   __shared__ double red[kMaxM * 32];
   const int np = cc->npairs;
-  double acc[kMaxM];
+  double acc[M];
 #pragma unroll
-  for (int k = 0; k < kMaxM; ++k) acc[k] = 0.0;
+  for (int k = 0; k < M; ++k) acc[k] = 0.0;
   const int ci = blockIdx.x * blockDim.x + threadIdx.x;  // (vertex, coordinate)
   if (ci < 3 * v.n) {
     const double r = v.R0[inst_off(v, b) + ci];
 #pragma unroll
-    for (int p = 0; p < kMaxM; ++p)
+    for (int p = 0; p < M; ++p)
       if (p < np) acc[p] = v.T[vec_off(v, cc->ring[p], b) + ci] * r;
   }
-  block_sum_masked<kMaxM>(acc, red, (1ull << np) - 1ull);
+  block_sum_masked<M>(acc, red, (1ull << np) - 1ull);
   if (threadIdx.x == 0) {
     double* pv = v.part_v + ((size_t)b * v.nblk_v + blockIdx.x) * kNG;
-    for (int k = 0; k < kMaxM; ++k) pv[k] = acc[k];
+    for (int k = 0; k < M; ++k) pv[k] = acc[k];
   }
   if (!last_block(v.cnt, 1, b, v.n_inst, gridDim.x)) return;
   double* tot = red;
@@ -706,12 +711,21 @@ __global__ void k_material(const qn_material* M, int64_t k, const double* sig, d
 int launch_body(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const dim3 gv(v.nblk_v, v.n_inst), gt(v.nblk_t, v.n_inst);
-  k_grad<<<gv, kVT, 0, st>>>(v);
+  const bool small_m = S->h_cfg.m <= 5;  // default window: smaller register footprint
+  if (small_m) {
+    k_grad<5><<<gv, kVT, 0, st>>>(v);
+  } else {
+    k_grad<kMaxM><<<gv, kVT, 0, st>>>(v);
+  }
   QN_CHECK_LAUNCH();
   SolverIO io{v};
   int rc = launch_solve(S->factor, io, st);
   if (rc) return rc;
-  k_eta<<<gv, kVT, 0, st>>>(v);
+  if (small_m) {
+    k_eta<5><<<gv, kVT, 0, st>>>(v);
+  } else {
+    k_eta<kMaxM><<<gv, kVT, 0, st>>>(v);
+  }
   QN_CHECK_LAUNCH();
   k_vec<<<gv, kVT, 0, st>>>(v);
   QN_CHECK_LAUNCH();

@@ -106,6 +106,7 @@ struct qn_system {
   size_t h_stage_bytes = 0;
   // graph
   bool use_graph = true;
+  int graph_m_bound = 0;  // history bound the captured graph's kernels are specialised on
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

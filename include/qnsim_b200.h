@@ -150,7 +150,16 @@ typedef struct qn_system_desc {
   const int32_t* a_indices;   /* (a_nnz)                                        */
   const double* a_values;     /* (n_inst * a_nnz)                               */
   const double* free_coords;  /* (n_free,3) rest positions for the ordering     */
+  /* solve of A_free d = q: QN_SOLVE_DIRECT (prefactored, linalg.py:23-59) or
+   * QN_SOLVE_PCG (Jacobi-preconditioned CG to ||r|| <= pcg_tol ||b|| per
+   * coordinate, for meshes too large to factor; configs[4]) */
+  int32_t solver;
+  int32_t pcg_maxit;
+  double pcg_tol;
 } qn_system_desc;
+
+#define QN_SOLVE_DIRECT 0
+#define QN_SOLVE_PCG 1
 
 typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          */
   int32_t kind;                    /* 0 = pd_qn, 1 = lbfgs (lbfgs_init=system_matrix) */

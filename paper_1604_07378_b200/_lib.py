@@ -66,6 +66,7 @@ class SystemDesc(C.Structure):
         ("h", C.c_double), ("gravity", C.c_double * 3), ("scale", C.c_double),
         ("a_nnz", C.c_int64), ("a_indptr", C.c_void_p), ("a_indices", C.c_void_p), ("a_values", C.c_void_p),
         ("free_coords", C.c_void_p),
+        ("solver", C.c_int32), ("pcg_maxit", C.c_int32), ("pcg_tol", C.c_double),
     ]
 
 

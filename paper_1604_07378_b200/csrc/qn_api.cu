@@ -431,15 +431,57 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       }
     S->h_tet_mat.assign(d->tet_mat, d->tet_mat + mt);
   }
-  // factor of A_free (one numeric instance per system instance)
-  S->factor = new qn_factor();
-  int rc = factor_build_host(S->factor, S->n_free, d->a_indptr, d->a_indices, d->a_values, ni, d->free_coords);
-  if (rc == QN_OK) rc = factor_upload(S->factor);
-  if (rc) return fail(rc);
-  std::vector<int32_t> fact_vtx(S->n_free);
-  for (int64_t r = 0; r < S->n_free; ++r) fact_vtx[r] = free_ids[S->factor->perm[r]];
-
   SysView& v = S->v;
+  int rc = QN_OK;
+  std::vector<int32_t> fact_vtx(S->n_free);
+  const bool pcg = d->solver == QN_SOLVE_PCG;
+  if (!pcg) {
+    // factor of A_free (one numeric instance per system instance)
+    S->factor = new qn_factor();
+    rc = factor_build_host(S->factor, S->n_free, d->a_indptr, d->a_indices, d->a_values, ni, d->free_coords);
+    if (rc == QN_OK) rc = factor_upload(S->factor);
+    if (rc) return fail(rc);
+    for (int64_t r = 0; r < S->n_free; ++r) fact_vtx[r] = free_ids[S->factor->perm[r]];
+  } else {
+    // PCG: A_free on the device as CSR (free-vertex order), Jacobi preconditioner
+    QN_REQUIRE(d->pcg_tol > 0 && d->pcg_maxit > 0, QN_ERR_ARG, "system: PCG needs pcg_tol > 0 and pcg_maxit > 0");
+    const int64_t nf = S->n_free, nnz = d->a_indptr[nf];
+    std::vector<double> dinv((size_t)ni * nf, 0.0);
+    for (int64_t b = 0; b < ni; ++b)
+      for (int64_t r = 0; r < nf; ++r)
+        for (int64_t p = d->a_indptr[r]; p < d->a_indptr[r + 1]; ++p)
+          if (d->a_indices[p] == r) dinv[b * nf + r] = 1.0 / d->a_values[b * nnz + p];
+    for (double x : dinv)
+      if (!(x > 0.0)) {
+        set_error("matrix is not positive definite (non-positive diagonal)");
+        return fail(QN_ERR_NOT_SPD);
+      }
+    for (int64_t r = 0; r < nf; ++r) fact_vtx[r] = free_ids[r];
+    int64_t* ap;
+    int32_t* ac;
+    double *av, *di;
+    if ((rc = sys_upload(S, &ap, d->a_indptr, (size_t)nf + 1)) || (rc = sys_upload(S, &ac, d->a_indices, (size_t)nnz)) ||
+        (rc = sys_upload(S, &av, d->a_values, (size_t)ni * nnz)) || (rc = sys_upload(S, &di, dinv.data(), dinv.size())))
+      return fail(rc);
+    v.a_ptr = ap;
+    v.a_col = ac;
+    v.a_val = av;
+    v.a_nnz = nnz;
+    v.dinv = di;
+    v.pcg = 1;
+    v.n_free = (int32_t)nf;
+    v.nblk_p = div_up(nf, 128);
+    v.pcg_tol = d->pcg_tol;
+    v.pcg_maxit = d->pcg_maxit;
+    const size_t fv = (size_t)ni * nf * 3;
+    if ((rc = sys_alloc(S, &v.px, fv)) || (rc = sys_alloc(S, &v.pr, fv)) || (rc = sys_alloc(S, &v.pz, fv)) ||
+        (rc = sys_alloc(S, &v.pp, 2 * fv)) || (rc = sys_alloc(S, &v.pq, fv)) ||
+        (rc = sys_alloc(S, &v.part_p, (size_t)ni * v.nblk_p * 8)) ||
+        (rc = sys_alloc(S, &v.cnt_p, (size_t)3 * ni + 2)) || (rc = sys_alloc(S, &v.pctl, (size_t)ni)) ||
+        (rc = sys_alloc(S, &v.pcg_active, 1)))
+      return fail(rc);
+  }
+
   v.n = (int32_t)n;
   v.mt = (int32_t)mt;
   v.n_inst = (int32_t)ni;
@@ -673,7 +715,7 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   QN_CUDA(cudaMemcpy(&passes, S->v.passes, sizeof(passes), cudaMemcpyDeviceToHost));
   S->last_passes = (int64_t)passes;
   if (S->use_graph) count_launch((int)(2 + 6 * passes));
-  if ((rc = factor_check_watchdog(S->factor))) return rc;
+  if (S->factor && (rc = factor_check_watchdog(S->factor))) return rc;
   if ((int64_t)passes > (int64_t)c.max_passes) {
     set_error("frame: pass limit exceeded (phase machine did not terminate)");
     return QN_ERR_CUDA;
@@ -810,6 +852,7 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
       int r = launch_tet_plain(S, v.q_l, 0, -1, S->d_part_plain, st);
       if (r) return r;
     } else {  // forward + backward supernodal solves with 3 RHS (instance 0)
+      QN_REQUIRE(S->factor, QN_ERR_UNSUPPORTED, "time_kernel: no factor (PCG system)");
       QN_CUDA(cudaMemcpyAsync(S->factor->d_io, v.q_l, S->n_free * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
       int r = factor_solve_plain(S->factor, 0, st);
       if (r) return r;

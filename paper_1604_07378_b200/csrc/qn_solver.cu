@@ -706,21 +706,247 @@ __global__ void k_material(const qn_material* M, int64_t k, const double* sig, d
 }
 
 // ---------------------------------------------------------------------------
+// PCG solve (configs[4] scale): r0 = A_free^-1 q' by Jacobi-preconditioned CG,
+// the three coordinates as three lockstep CG runs with their own scalars.
+// Per iteration two kernels: SpMV with the direction update fused into the
+// neighbour loads (p_new = z + beta p_old, double-buffered p), then the
+// x / r / z update; each ends in a fixed-order block-partial reduction whose
+// last block computes alpha (resp. beta and convergence).  The global last
+// block of the update kernel drives the inner WHILE node of the frame graph.
+
+constexpr int kPT = 128;  // PCG rows per block
+
+__device__ __forceinline__ bool pcg_on(const SysView& v, int b) {
+  return v.ctl[b].phase == PH_DIR && !(v.pctl[b].conv & 8);
+}
+
+// global "last block" of a PCG kernel: write the inner loop condition
+__device__ __forceinline__ void pcg_global_tail(const SysView& v, int which) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned* gc = v.cnt_p + 3 * (size_t)v.n_inst + which;
+    const unsigned total = gridDim.x * gridDim.y;
+    const unsigned old = atomicAdd(gc, 1u);
+    if (old == total - 1) {
+      *gc = 0;
+      __threadfence();
+      const int act = *((volatile int32_t*)v.pcg_active);
+      if (v.cfg->use_graph) cudaGraphSetConditional(v.pcg_handle, act > 0 ? 1u : 0u);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPT) k_pcg_init(SysView v) {
+  const int b = blockIdx.y;
+  if (v.ctl[b].phase == PH_DIR) {
+    __shared__ double red[6 * 32];
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < v.n_free) {
+      SolverIO io{v};
+      double q[3];
+      io.rhs(b, i, q);  // fact_vtx = free vertex ids in PCG mode
+      const size_t o = ((size_t)b * v.n_free + i) * 3;
+      const double di = v.dinv[(size_t)b * v.n_free + i];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double z = q[c] * di;
+        v.px[o + c] = 0.0;
+        v.pr[o + c] = q[c];
+        v.pz[o + c] = z;
+        v.pp[o + c] = z;  // buffer 0
+        acc[c] = q[c] * z;
+        acc[3 + c] = q[c] * q[c];
+      }
+    }
+    block_sum<6>(acc, red);
+    if (threadIdx.x == 0) {
+      double* pv = v.part_p + ((size_t)b * v.nblk_p + blockIdx.x) * 8;
+      for (int k = 0; k < 6; ++k) pv[k] = acc[k];
+    }
+    if (last_block(v.cnt_p, 0, b, v.n_inst, gridDim.x)) {
+      __shared__ double tot[6];
+      sum_partials(v.part_p + (size_t)b * v.nblk_p * 8, gridDim.x, 8, 6, tot);
+      if (threadIdx.x == 0) {
+        PcgCtl& p = v.pctl[b];
+        int conv = 0;
+        for (int c = 0; c < 3; ++c) {
+          p.rz[c] = tot[c];
+          p.bb[c] = tot[3 + c];
+          p.rr[c] = tot[3 + c];
+          p.alpha[c] = p.beta[c] = 0.0;
+          if (!(tot[3 + c] > 0.0)) conv |= 1 << c;  // zero right-hand side
+        }
+        p.iter = 0;
+        if (conv == 7) conv |= 8;  // nothing to do
+        p.conv = conv;
+        if (!(conv & 8)) atomicAdd(v.pcg_active, 1);
+      }
+    }
+  }
+  pcg_global_tail(v, 0);
+}
+
+__global__ void __launch_bounds__(kPT) k_pcg_spmv(SysView v) {
+  const int b = blockIdx.y;
+  if (pcg_on(v, b)) {
+    __shared__ double red[3 * 32];
+    const PcgCtl& pc = v.pctl[b];
+    const int pb = pc.iter & 1;
+    const double be[3] = {pc.beta[0], pc.beta[1], pc.beta[2]};
+    const double* pold = v.pp + ((size_t)pb * v.n_inst + b) * v.n_free * 3;
+    double* pnew = v.pp + ((size_t)(pb ^ 1) * v.n_inst + b) * v.n_free * 3;
+    const double* z = v.pz + (size_t)b * v.n_free * 3;
+    double acc[3] = {0, 0, 0};
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < v.n_free) {
+      const double* av = v.a_val + (size_t)b * v.a_nnz;
+      double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+      for (int64_t e = v.a_ptr[i]; e < v.a_ptr[i + 1]; ++e) {
+        const int j = __ldg(v.a_col + e);
+        const double a = __ldg(av + e);
+        q0 = fma(a, fma(be[0], pold[3 * j + 0], z[3 * j + 0]), q0);
+        q1 = fma(a, fma(be[1], pold[3 * j + 1], z[3 * j + 1]), q1);
+        q2 = fma(a, fma(be[2], pold[3 * j + 2], z[3 * j + 2]), q2);
+      }
+      const double p0 = fma(be[0], pold[3 * i + 0], z[3 * i + 0]);
+      const double p1 = fma(be[1], pold[3 * i + 1], z[3 * i + 1]);
+      const double p2 = fma(be[2], pold[3 * i + 2], z[3 * i + 2]);
+      pnew[3 * i + 0] = p0;
+      pnew[3 * i + 1] = p1;
+      pnew[3 * i + 2] = p2;
+      double* q = v.pq + ((size_t)b * v.n_free + i) * 3;
+      q[0] = q0;
+      q[1] = q1;
+      q[2] = q2;
+      acc[0] = p0 * q0;
+      acc[1] = p1 * q1;
+      acc[2] = p2 * q2;
+    }
+    block_sum<3>(acc, red);
+    if (threadIdx.x == 0) {
+      double* pv = v.part_p + ((size_t)b * v.nblk_p + blockIdx.x) * 8;
+      for (int k = 0; k < 3; ++k) pv[k] = acc[k];
+    }
+    if (last_block(v.cnt_p, 1, b, v.n_inst, gridDim.x)) {
+      __shared__ double tot[3];
+      sum_partials(v.part_p + (size_t)b * v.nblk_p * 8, gridDim.x, 8, 3, tot);
+      if (threadIdx.x == 0) {
+        PcgCtl& p = v.pctl[b];
+        for (int c = 0; c < 3; ++c) p.alpha[c] = (p.conv >> c) & 1 ? 0.0 : p.rz[c] / tot[c];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPT) k_pcg_update(SysView v) {
+  const int b = blockIdx.y;
+  if (pcg_on(v, b)) {
+    __shared__ double red[6 * 32];
+    const PcgCtl& pc = v.pctl[b];
+    const double* pnew = v.pp + ((size_t)((pc.iter & 1) ^ 1) * v.n_inst + b) * v.n_free * 3;
+    const double al[3] = {pc.alpha[0], pc.alpha[1], pc.alpha[2]};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < v.n_free) {
+      const size_t o = ((size_t)b * v.n_free + i) * 3;
+      const double di = v.dinv[(size_t)b * v.n_free + i];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        v.px[o + c] = fma(al[c], pnew[3 * i + c], v.px[o + c]);
+        const double r = fma(-al[c], v.pq[o + c], v.pr[o + c]);
+        const double z = r * di;
+        v.pr[o + c] = r;
+        v.pz[o + c] = z;
+        acc[c] = r * z;
+        acc[3 + c] = r * r;
+      }
+    }
+    block_sum<6>(acc, red);
+    if (threadIdx.x == 0) {
+      double* pv = v.part_p + ((size_t)b * v.nblk_p + blockIdx.x) * 8;
+      for (int k = 0; k < 6; ++k) pv[k] = acc[k];
+    }
+    if (last_block(v.cnt_p, 2, b, v.n_inst, gridDim.x)) {
+      __shared__ double tot[6];
+      sum_partials(v.part_p + (size_t)b * v.nblk_p * 8, gridDim.x, 8, 6, tot);
+      if (threadIdx.x == 0) {
+        PcgCtl& p = v.pctl[b];
+        const double tol2 = v.pcg_tol * v.pcg_tol;
+        int conv = p.conv;
+        for (int c = 0; c < 3; ++c) {
+          if ((conv >> c) & 1) continue;
+          p.beta[c] = tot[c] / p.rz[c];
+          p.rz[c] = tot[c];
+          p.rr[c] = tot[3 + c];
+          if (tot[3 + c] <= tol2 * p.bb[c]) conv |= 1 << c;
+        }
+        p.iter += 1;
+        if ((conv & 7) == 7 || p.iter >= v.pcg_maxit) {
+          conv |= 8;
+          atomicSub(v.pcg_active, 1);
+        }
+        p.conv = conv;
+      }
+    }
+  }
+  pcg_global_tail(v, 1);
+}
+
+__global__ void __launch_bounds__(kPT) k_pcg_store(SysView v) {
+  const int b = blockIdx.y;
+  if (v.ctl[b].phase != PH_DIR) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.n_free) return;
+  const double* x = v.px + ((size_t)b * v.n_free + i) * 3;
+  double* r = v.R0 + inst_off(v, b) + (size_t)v.fact_vtx[i] * 3;
+  r[0] = x[0];
+  r[1] = x[1];
+  r[2] = x[2];
+}
+
+// ---------------------------------------------------------------------------
 // host: body launch / graph
 
-int launch_body(qn_system* S, cudaStream_t st) {
+// body pass = pre (gradient, then the direct solve or the PCG set-up)
+//           [+ PCG iterations] + post (eta, direction / trial, tet pass)
+int launch_body_pre(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
-  const dim3 gv(v.nblk_v, v.n_inst), gt(v.nblk_t, v.n_inst);
-  const bool small_m = S->h_cfg.m <= 5;  // default window: smaller register footprint
-  if (small_m) {
+  const dim3 gv(v.nblk_v, v.n_inst);
+  if (S->h_cfg.m <= 5) {  // default window: smaller register footprint
     k_grad<5><<<gv, kVT, 0, st>>>(v);
   } else {
     k_grad<kMaxM><<<gv, kVT, 0, st>>>(v);
   }
   QN_CHECK_LAUNCH();
+  if (v.pcg) {
+    k_pcg_init<<<dim3(v.nblk_p, v.n_inst), kPT, 0, st>>>(v);
+    QN_CHECK_LAUNCH();
+    return QN_OK;
+  }
   SolverIO io{v};
-  int rc = launch_solve(S->factor, io, st);
-  if (rc) return rc;
+  return launch_solve(S->factor, io, st);
+}
+
+int launch_pcg_iter(qn_system* S, cudaStream_t st) {
+  const SysView& v = S->v;
+  const dim3 gp(v.nblk_p, v.n_inst);
+  k_pcg_spmv<<<gp, kPT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  k_pcg_update<<<gp, kPT, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
+int launch_body_post(qn_system* S, cudaStream_t st) {
+  const SysView& v = S->v;
+  const dim3 gv(v.nblk_v, v.n_inst), gt(v.nblk_t, v.n_inst);
+  const bool small_m = S->h_cfg.m <= 5;
+  if (v.pcg) {
+    k_pcg_store<<<dim3(v.nblk_p, v.n_inst), kPT, 0, st>>>(v);
+    QN_CHECK_LAUNCH();
+  }
   if (small_m) {
     k_eta<5><<<gv, kVT, 0, st>>>(v);
   } else {
@@ -736,6 +962,22 @@ int launch_body(qn_system* S, cudaStream_t st) {
   }
   QN_CHECK_LAUNCH();
   return QN_OK;
+}
+
+// host-driven body (no graph): PCG iterations loop with a host read per iteration
+int launch_body(qn_system* S, cudaStream_t st) {
+  int rc = launch_body_pre(S, st);
+  if (rc) return rc;
+  if (S->v.pcg) {
+    for (int it = 0; it < S->v.pcg_maxit; ++it) {
+      int32_t act = 0;
+      QN_CUDA(cudaMemcpyAsync(&act, S->v.pcg_active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      QN_CUDA(cudaStreamSynchronize(st));
+      if (act <= 0) break;
+      if ((rc = launch_pcg_iter(S, st))) return rc;
+    }
+  }
+  return launch_body_post(S, st);
 }
 
 int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st) {
@@ -763,7 +1005,7 @@ int launch_finish(qn_system* S, cudaStream_t st) {
   return QN_OK;
 }
 
-int prepare_kernels(qn_system* S) { return prepare_solve_kernels<SolverIO>(S->factor); }
+int prepare_kernels(qn_system* S) { return S->factor ? prepare_solve_kernels<SolverIO>(S->factor) : QN_OK; }
 
 int build_graph(qn_system* S) {
   cudaStream_t st = S->stream;
@@ -800,10 +1042,51 @@ int build_graph(qn_system* S) {
   cudaGraphNode_t cond;
   QN_CUDA(cudaGraphAddNode(&cond, g, &init_node, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  rc = launch_body(S, st);
-  QN_CUDA(cudaStreamEndCapture(st, &body));
-  if (rc) return rc;
+  if (!S->v.pcg) {
+    QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    rc = launch_body_pre(S, st);
+    if (rc == QN_OK) rc = launch_body_post(S, st);
+    QN_CUDA(cudaStreamEndCapture(st, &body));
+    if (rc) return rc;
+  } else {
+    // pre -> WHILE(pcg active){ spmv, update } -> post, all inside the body
+    cudaGraphConditionalHandle hp;
+    QN_CUDA(cudaGraphConditionalHandleCreate(&hp, body, 0, 0));
+    S->v.pcg_handle = hp;
+    QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    rc = launch_body_pre(S, st);
+    cudaGraph_t tmpb;
+    QN_CUDA(cudaStreamEndCapture(st, &tmpb));
+    if (rc) return rc;
+    // leaf of the captured chain
+    size_t nb = 0;
+    QN_CUDA(cudaGraphGetNodes(body, nullptr, &nb));
+    std::vector<cudaGraphNode_t> nodes(nb);
+    QN_CUDA(cudaGraphGetNodes(body, nodes.data(), &nb));
+    cudaGraphNode_t leaf = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+      size_t ndep = 0;
+      QN_CUDA(cudaGraphNodeGetDependentNodes(nd, nullptr, &ndep));
+      if (ndep == 0) leaf = nd;
+    }
+    QN_REQUIRE(leaf != nullptr, QN_ERR_CUDA, "graph: no leaf in the PCG pre-segment");
+    cudaGraphNodeParams ci = {};
+    ci.type = cudaGraphNodeTypeConditional;
+    ci.conditional.handle = hp;
+    ci.conditional.type = cudaGraphCondTypeWhile;
+    ci.conditional.size = 1;
+    cudaGraphNode_t pcond;
+    QN_CUDA(cudaGraphAddNode(&pcond, body, &leaf, 1, &ci));
+    cudaGraph_t ibody = ci.conditional.phGraph_out[0];
+    QN_CUDA(cudaStreamBeginCaptureToGraph(st, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    rc = launch_pcg_iter(S, st);
+    QN_CUDA(cudaStreamEndCapture(st, &ibody));
+    if (rc) return rc;
+    QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, &pcond, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+    rc = launch_body_post(S, st);
+    QN_CUDA(cudaStreamEndCapture(st, &tmpb));
+    if (rc) return rc;
+  }
   // finish
   QN_CUDA(cudaStreamBeginCaptureToGraph(st, g, &cond, nullptr, 1, cudaStreamCaptureModeThreadLocal));
   rc = launch_finish(S, st);

@@ -40,6 +40,13 @@ struct InstCtl {
   double coef[kMaxM];                 // zeta - eta by ring position
 };
 
+// Preconditioned CG on A_free (3 right-hand sides solved in lockstep), the
+// solve used for meshes too large to factor (configs[4]).
+struct PcgCtl {
+  double rz[3], alpha[3], beta[3], bb[3], rr[3];
+  int32_t iter, conv, pad0, pad1;  // conv: bit c = column c converged
+};
+
 struct DevConfig {
   int32_t kind, iterations, m, line_search;
   double gamma, alpha_init, shrink, grad_tol;
@@ -85,6 +92,24 @@ struct SysView {
   int32_t* active;     // instances not yet done
   unsigned long long* passes;
   cudaGraphConditionalHandle handle;
+  // ---- PCG solve mode (pcg != 0) ----
+  int32_t pcg, n_free, nblk_p, pcg_maxit;
+  double pcg_tol;
+  const int64_t* a_ptr;   // CSR of A_free (free-vertex order)
+  const int32_t* a_col;
+  const double* a_val;    // [inst][nnz]
+  int64_t a_nnz;
+  const double* dinv;     // [inst][n_free] Jacobi preconditioner
+  double* px;             // [inst][n_free][3] iterate
+  double* pr;             // residual
+  double* pz;             // preconditioned residual
+  double* pp;             // [2][inst][n_free][3] search directions (double buffered)
+  double* pq;             // A p
+  double* part_p;         // [inst][nblk_p][8]
+  unsigned* cnt_p;        // [3][inst] + [global]
+  PcgCtl* pctl;           // [inst]
+  int32_t* pcg_active;    // instances still iterating
+  cudaGraphConditionalHandle pcg_handle;
 };
 
 }  // namespace qn

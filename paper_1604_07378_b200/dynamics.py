@@ -107,7 +107,7 @@ class SimSystem:
         _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
 
     def factor_info(self) -> dict:
-        return self.sysfact.info()
+        return self.sysfact.info() if self.sysfact is not None else {"solver": "pcg"}
 
     def time_kernel(self, kernel: str, reps: int = 20, stream=None) -> float:
         """Mean CUDA-event time (ms) of one stand-alone launch of a hot kernel:
@@ -149,7 +149,8 @@ def _pattern_sum(rows, cols, n):
     return np.cumsum(indptr), c, inv, r
 
 
-def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups):
+def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, solver="direct", pcg_tol=1e-10,
+           pcg_maxit=20000):
     if not isinstance(mesh, TetMesh):
         raise NotImplementedError("spring networks (cloth) are outside the B200 hot path")
     _lib.require_gpu()
@@ -242,11 +243,17 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups):
     d.a_nnz = a_indices.size
     d.a_indptr, d.a_indices, d.a_values = _lib.ptr(f_indptr), _lib.ptr(a_indices), _lib.ptr(a_values)
     d.free_coords = _lib.ptr(coords)
+    if solver not in ("direct", "pcg"):
+        raise DynamicsError(f"unknown solver {solver!r} (direct | pcg)")
+    d.solver = 1 if solver == "pcg" else 0
+    d.pcg_tol, d.pcg_maxit = float(pcg_tol), int(pcg_maxit)
     handle = C.c_void_p()
     _lib.check(_lib.load().qn_system_create(C.byref(d), C.byref(handle)), "build_system")
-    fh = C.c_void_p()
-    _lib.check(_lib.load().qn_system_factor(handle, C.byref(fh)))
-    sysfact = Factorization._borrow(fh, free.size, n_inst)
+    sysfact = None
+    if solver == "direct":
+        fh = C.c_void_p()
+        _lib.check(_lib.load().qn_system_factor(handle, C.byref(fh)))
+        sysfact = Factorization._borrow(fh, free.size, n_inst)
 
     system = SimSystem(mesh=mesh, masses=masses, h=float(h), gravity=np.asarray(gravity, dtype=np.float64),
                        groups=groups_per_inst[0] if n_inst == 1 else groups_per_inst, fixed=fixed, free=free,
@@ -260,14 +267,19 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups):
 
 def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(), aniso=None,
                  colliders=(), collision_weight: float | None = None,
-                 fit_interval: FitInterval = FitInterval()) -> SimSystem:
-    """dynamics.py:351-434 for Valanis-Landel tet groups (single instance)."""
+                 fit_interval: FitInterval = FitInterval(), solver: str = "direct", pcg_tol: float = 1e-10,
+                 pcg_maxit: int = 20000) -> SimSystem:
+    """dynamics.py:351-434 for Valanis-Landel tet groups (single instance).
+
+    solver="direct" prefactors A_free once (the reference's semantics);
+    solver="pcg" solves every direction with Jacobi-preconditioned CG to
+    ||r|| <= pcg_tol ||b|| (configs[4]: meshes too large to factor)."""
     if aniso:
         raise NotImplementedError("anisotropic fibres are outside the B200 hot path (SURVEY §8f)")
     if colliders:
         raise NotImplementedError("colliders are outside the B200 hot path (SURVEY §8f)")
     assign = _assign(mesh, materials)
-    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign))
+    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit)
 
 
 def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(),

@@ -234,6 +234,37 @@ def test_c4_batch_against_reference_golden():
         assert rel(st.q_l[b], d[f"i{b}_x_2"]) <= X_TOL
 
 
+# ---- PCG solve mode (configs[4]) -------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_pcg_mode_against_oracle(cfg):
+    """PCG (to 1e-13) in place of the prefactored solve reproduces the
+    reference trajectory of the direct method within the parity tolerance."""
+    sc = scenes.CONFIGS[cfg](frames=2)
+    system = build(sc, solver="pcg", pcg_tol=1e-13)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    res = run_gpu(system, sc, 2)
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(2):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        assert rel(res[f][1].g, rec.g) <= G_TOL
+        assert res[f][1].ls_trials == rec.ls_trials
+        assert rel(res[f][0], x) <= X_TOL
+
+
+def test_c5_scaled_down_pcg_against_oracle():
+    """configs[4] material (NH + cubic) and solver (PCG to 1e-10, the BASELINE
+    setting) on a 40x10x10 bar: positions within 1e-8, energies within 1e-9."""
+    sc = scenes.c5(grid=(40, 10, 10), frames=1)
+    system = build(sc, solver="pcg", pcg_tol=1e-10)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    (xg, rg), = run_gpu(system, sc, 1)
+    x, _, ro = O.simulate_frame(osys, sc.q_l.copy(), sc.q_prev.copy(), iterations=sc.iterations, m=sc.m)
+    assert rel(rg.g, ro.g) <= 1e-9
+    assert rel(xg, x) <= 1e-8
+
+
 # ---- semantics and edge cases (test_solvers.py / test_dynamics.py analogues) -----
 
 def unit_tet_mesh():

@@ -140,7 +140,9 @@ def build_system(sc):
     if sc.batch:
         return Q.build_batch_system(mesh, [from_spec(s) for s in sc.batch_materials], h=sc.h, gravity=sc.gravity,
                                     fixed=sc.fixed)
-    return Q.build_system(mesh, from_spec(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    solver = "pcg" if sc.name.startswith("c5") else "direct"  # configs[4]: PCG to 1e-10 (BASELINE.json)
+    return Q.build_system(mesh, from_spec(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed, solver=solver,
+                          pcg_tol=1e-10)
 
 
 def cpu_oracle_rate(sc, iterations, frames=1, threads=1):
@@ -253,12 +255,15 @@ def run_ours(args, world, rank, local):
     info = system.factor_info()
     m, n = sc.tets.shape[0], sc.verts.shape[0]
     tet_ms = system.time_kernel("tet", reps=20, stream=sptr)
-    solve_ms = system.time_kernel("solve", reps=20, stream=sptr)
     tet_bytes = (192.0 + 24.0 * n / m) * m                    # idx+Dm^-1+vol+forces, x gathered once
-    solve_bytes = 2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]  # factor read twice + rhs/y/x/u vectors
     per_frame = total_ms / args.steps
     share_tet = tet_ms * passes / args.steps / per_frame
-    share_solve = solve_ms * sc.iterations / per_frame
+    if "nnz_l" in info:
+        solve_ms = system.time_kernel("solve", reps=20, stream=sptr)
+        solve_bytes = 2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]  # factor read twice + rhs/y/x/u vectors
+        share_solve = solve_ms * sc.iterations / per_frame
+    else:  # PCG system: the per-tet kernel is the timed hot kernel
+        solve_ms, solve_bytes, share_solve = 1.0, 0.0, 0.0
     dom = "tet" if share_tet >= share_solve else "solve"
     dms, dbytes = (tet_ms, tet_bytes) if dom == "tet" else (solve_ms, solve_bytes)
     achieved = dbytes / (dms / 1000.0) / 1e9
@@ -267,7 +272,9 @@ def run_ours(args, world, rank, local):
             "traffic": ncu_traffic(dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
             "share_of_step": share_tet if dom == "tet" else share_solve,
             "other": {"tet_ms": tet_ms, "tet_GBps": tet_bytes / tet_ms / 1e6, "tet_share": share_tet,
-                      "solve_ms": solve_ms, "solve_GBps": solve_bytes / solve_ms / 1e6, "solve_share": share_solve}}
+                      "solve_ms": solve_ms if solve_bytes else None,
+                      "solve_GBps": solve_bytes / solve_ms / 1e6 if solve_bytes else None,
+                      "solve_share": share_solve}}
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -308,8 +315,9 @@ def run_ours(args, world, rank, local):
                            "parallelism": "replicas" if not sc.batch else f"instances/{world} per rank"},
                 "tet_evals_per_s": tet_evals, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches,
-                "factor": {"nnz_l": info["nnz_l"], "supernodes": info["n_supernodes"],
-                           "depth": info["tree_depth"], "factor_s": info["factor_seconds"]},
+                "factor": ({"nnz_l": info["nnz_l"], "supernodes": info["n_supernodes"],
+                            "depth": info["tree_depth"], "factor_s": info["factor_seconds"],
+                            "dense_top": info.get("dense_top")} if "nnz_l" in info else info),
                 "build_s": t_build, "passes_per_step": passes / args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:

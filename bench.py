@@ -112,13 +112,14 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(workload, kernel):
+    """dram bytes per launch of `kernel` on `workload` from the committed ncu
+    --set full summaries, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel)
-    except (OSError, ValueError):
+            return json.load(fh).get(workload, {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -229,7 +230,7 @@ def run_ours(args, world, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    passes = 0
+    passes = cg_iters = 0
     l0 = _lib.launch_count()
     for k in range(args.steps):
         flush.zero_()
@@ -237,6 +238,7 @@ def run_ours(args, world, rank, local):
         run.step(stream=sptr)
         ev[k][1].record(stream)
         passes += run.last_passes
+        cg_iters += run.last_cg_iterations
     torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
     clk = clocks.stop()
@@ -269,7 +271,7 @@ def run_ours(args, world, rank, local):
     achieved = dbytes / (dms / 1000.0) / 1e9
     roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else "sptrsv_forward+backward",
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
-            "traffic": ncu_traffic(dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
+            "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
             "share_of_step": share_tet if dom == "tet" else share_solve,
             "other": {"tet_ms": tet_ms, "tet_GBps": tet_bytes / tet_ms / 1e6, "tet_share": share_tet,
                       "solve_ms": solve_ms if solve_bytes else None,
@@ -319,6 +321,8 @@ def run_ours(args, world, rank, local):
                             "depth": info["tree_depth"], "factor_s": info["factor_seconds"],
                             "dense_top": info.get("dense_top")} if "nnz_l" in info else info),
                 "build_s": t_build, "passes_per_step": passes / args.steps}
+        if cg_iters:
+            line["cg_iterations_per_step"] = cg_iters / args.steps
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -113,9 +113,10 @@ int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int
                     void* stream);
 int qn_factor_destroy(qn_factor* f);
 /* diagnostics: one traced solve (instance 0, current staging RHS); stamps =
- * globaltimer ns at (start, dependencies ready, done) per forward then backward
- * work item; tasks = {supernode, lo, hi, 0} per forward then backward task.
- * Sizes: 3 (n_ftask + n_btask) nbatch and 4 (n_ftask + n_btask). */
+ * globaltimer ns at (start, dependencies ready), then SM clock64 at (ready,
+ * data staged, computed, published) per forward then backward work item;
+ * tasks = {supernode, lo, hi, 0} per forward then backward task.
+ * Sizes: 6 (n_ftask + n_btask) nbatch and 4 (n_ftask + n_btask). */
 int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask);
 int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks);
 
@@ -218,6 +219,9 @@ int qn_system_set_graph_mode(qn_system* s, int32_t use_graph);
 int qn_system_last_frame_ms(qn_system* s, double* ms);
 /* body passes (line-search trials + re-evaluations) of the last frame */
 int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
+/* PCG mode: conjugate-gradient iterations of the last frame, summed over
+ * instances (0 in direct mode) */
+int qn_system_last_frame_cg_iterations(qn_system* s, int64_t* iters);
 
 /* Stand-alone timing of one hot kernel with CUDA events on `stream` (after a
  * warm-up launch): kernel 0 = per-tet pass at the resident q_l, kernel 1 =

@@ -113,6 +113,7 @@ SIGNATURES = {
     "qn_system_set_graph_mode": [_P, _I32],
     "qn_system_last_frame_ms": [_P, _P],
     "qn_system_last_frame_passes": [_P, _P],
+    "qn_system_last_frame_cg_iterations": [_P, _P],
     "qn_system_time_kernel": [_P, _I32, _I32, _P, _P],
 }
 

@@ -131,7 +131,7 @@ int factor_upload(qn_factor* f) {
   for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
   // Z tile + forward: f (nc x 3) + partials (256 x 3) + index staging; backward: w (nr x 3) + row staging
   f->smem_bytes = (int)(sizeof(double) * kTaskEntries +
-                        sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows) +
+                        sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows + kBwdCols) +
                         sizeof(int) * kStageIdx);
   QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
   // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
@@ -336,12 +336,12 @@ int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask
 int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks) {
   QN_REQUIRE(f && stamps && tasks, QN_ERR_ARG, "trace: null");
   const size_t nf = f->ftask.size(), nb = f->btask.size(), items = (nf + nb) * (size_t)f->nbatch;
-  int rc = dev_alloc(&f->d_trace, 3 * items);
+  int rc = dev_alloc(&f->d_trace, qn::kTraceSlots * items);
   if (rc) return rc;
   rc = factor_solve_plain(f, 0, 0);
   if (rc == QN_OK) {
     QN_CUDA(cudaDeviceSynchronize());
-    QN_CUDA(cudaMemcpy(stamps, f->d_trace, 3 * items * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy(stamps, f->d_trace, qn::kTraceSlots * items * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   }
   cudaFree(f->d_trace);
   f->d_trace = nullptr;
@@ -457,26 +457,57 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
         return fail(QN_ERR_NOT_SPD);
       }
     for (int64_t r = 0; r < nf; ++r) fact_vtx[r] = free_ids[r];
-    int64_t* ap;
-    int32_t* ac;
-    double *av, *di;
-    if ((rc = sys_upload(S, &ap, d->a_indptr, (size_t)nf + 1)) || (rc = sys_upload(S, &ac, d->a_indices, (size_t)nnz)) ||
-        (rc = sys_upload(S, &av, d->a_values, (size_t)ni * nnz)) || (rc = sys_upload(S, &di, dinv.data(), dinv.size())))
+    // SELL-32 copy of the CSR rows (same entry order within a row, zero padding)
+    const int64_t nsl = (nf + 31) / 32;
+    std::vector<int64_t> sptr((size_t)nsl + 1, 0);
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+      int64_t w = 0;
+      for (int64_t r = 32 * sl; r < std::min(nf, 32 * sl + 32); ++r) w = std::max(w, d->a_indptr[r + 1] - d->a_indptr[r]);
+      sptr[sl + 1] = sptr[sl] + 32 * w;
+    }
+    const int64_t snz = sptr[nsl];
+    std::vector<int32_t> scol((size_t)snz);
+    std::vector<double> sval((size_t)ni * snz, 0.0);
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+      const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
+      for (int64_t l = 0; l < 32; ++l) {
+        const int64_t r = 32 * sl + l;
+        const int64_t p0 = r < nf ? d->a_indptr[r] : 0, len = r < nf ? d->a_indptr[r + 1] - p0 : 0;
+        for (int64_t k = 0; k < w; ++k) {
+          const int64_t e = sptr[sl] + 32 * k + l;
+          scol[e] = k < len ? d->a_indices[p0 + k] : (int32_t)std::min(r, nf - 1);
+          if (k < len)
+            for (int64_t b = 0; b < ni; ++b) sval[b * snz + e] = d->a_values[b * nnz + p0 + k];
+        }
+      }
+    }
+    int64_t* sp;
+    int32_t* sc;
+    double *sv, *di;
+    if ((rc = sys_upload(S, &sp, sptr.data(), sptr.size())) || (rc = sys_upload(S, &sc, scol.data(), scol.size())) ||
+        (rc = sys_upload(S, &sv, sval.data(), sval.size())) || (rc = sys_upload(S, &di, dinv.data(), dinv.size())))
       return fail(rc);
-    v.a_ptr = ap;
-    v.a_col = ac;
-    v.a_val = av;
-    v.a_nnz = nnz;
+    v.sell_ptr = sp;
+    v.sell_col = sc;
+    v.sell_val = sv;
+    v.sell_nnz = snz;
+    v.nslice = (int32_t)nsl;
     v.dinv = di;
     v.pcg = 1;
     v.n_free = (int32_t)nf;
     v.nblk_p = div_up(nf, 128);
+    int dev = 0, nsm = 148;
+    QN_CUDA(cudaGetDevice(&dev));
+    QN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    v.nblk_spmv = (int32_t)std::min<int64_t>(div_up(nsl, qn::kSpmvWarps), (int64_t)nsm * qn::kSpmvBlocksPerSm);
+    v.nblk_upd = (int32_t)std::min<int64_t>(div_up(3 * nf, qn::kUpdThreads), (int64_t)nsm * qn::kUpdBlocksPerSm);
     v.pcg_tol = d->pcg_tol;
     v.pcg_maxit = d->pcg_maxit;
     const size_t fv = (size_t)ni * nf * 3;
-    if ((rc = sys_alloc(S, &v.px, fv)) || (rc = sys_alloc(S, &v.pr, fv)) || (rc = sys_alloc(S, &v.pz, fv)) ||
+    const size_t npart = (size_t)std::max(v.nblk_p, std::max(v.nblk_spmv, v.nblk_upd));
+    if ((rc = sys_alloc(S, &v.px, fv)) || (rc = sys_alloc(S, &v.pr, fv)) ||
         (rc = sys_alloc(S, &v.pp, 2 * fv)) || (rc = sys_alloc(S, &v.pq, fv)) ||
-        (rc = sys_alloc(S, &v.part_p, (size_t)ni * v.nblk_p * 8)) ||
+        (rc = sys_alloc(S, &v.part_p, (size_t)ni * npart * 8)) ||
         (rc = sys_alloc(S, &v.cnt_p, (size_t)3 * ni + 2)) || (rc = sys_alloc(S, &v.pctl, (size_t)ni)) ||
         (rc = sys_alloc(S, &v.pcg_active, 1)))
       return fail(rc);
@@ -597,6 +628,16 @@ int qn_system_last_frame_ms(qn_system* S, double* ms) {
 int qn_system_last_frame_passes(qn_system* S, int64_t* passes) {
   QN_REQUIRE(S && passes, QN_ERR_ARG, "null");
   *passes = S->last_passes;
+  return QN_OK;
+}
+
+int qn_system_last_frame_cg_iterations(qn_system* S, int64_t* iters) {
+  QN_REQUIRE(S && iters, QN_ERR_ARG, "null");
+  *iters = 0;
+  if (!S->v.pcg) return QN_OK;
+  std::vector<qn::PcgCtl> pc((size_t)S->n_inst);
+  QN_CUDA(cudaMemcpy(pc.data(), S->v.pctl, pc.size() * sizeof(qn::PcgCtl), cudaMemcpyDeviceToHost));
+  for (const auto& p : pc) *iters += p.total;
   return QN_OK;
 }
 

@@ -363,6 +363,62 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       }
     }
   }
+  // ---- subtree collapse (single-instance factors) ----
+  // The device solve costs about one inter-CTA synchronisation per tree level,
+  // so the bottom of the tree is flattened: every subtree of height <=
+  // kCollapseHeight whose merged supernode stays small (<= kCollapseCols
+  // columns, <= kCollapseGrowth x the Z entries of its parts) becomes ONE
+  // supernode (columns contiguous in postorder; its below rows are the
+  // subtree root's, by the etree ancestor property).  inv(L11) of the merged
+  // block is stored dense, explicit zeros included.
+  if (nbatch == 1) {
+    const int32_t ng = (int32_t)f->sup_col.size();
+    std::vector<int32_t> gcol(f->sup_col);
+    gcol.push_back((int32_t)n);
+    std::vector<int32_t> gof(n);
+    for (int32_t g = 0; g < ng; ++g)
+      for (int32_t j = gcol[g]; j < gcol[g + 1]; ++j) gof[j] = g;
+    std::vector<int32_t> gpar(ng, -1), ht(ng, 0), gsize(ng, 1);
+    std::vector<double> sub_nc(ng), sub_z(ng), below_g(ng);
+    for (int32_t g = 0; g < ng; ++g) {
+      const int32_t pc = par[gcol[g + 1] - 1];
+      gpar[g] = pc >= 0 ? gof[pc] : -1;
+      const auto& lr = cs[fcol[last_f[g]]];
+      below_g[g] = (double)(lr.end() - std::upper_bound(lr.begin(), lr.end(), gcol[g + 1] - 1));
+      const double nc = gcol[g + 1] - gcol[g];
+      sub_nc[g] += nc;
+      sub_z[g] += nc * (nc + below_g[g]);
+    }
+    for (int32_t g = 0; g < ng; ++g)  // children precede parents
+      if (gpar[g] >= 0) {
+        const int32_t p = gpar[g];
+        ht[p] = std::max(ht[p], ht[g] + 1);
+        sub_nc[p] += sub_nc[g];
+        sub_z[p] += sub_z[g];
+        gsize[p] += gsize[g];
+      }
+    std::vector<uint8_t> sel(ng, 0), covered(ng, 0);
+    for (int32_t g = ng - 1; g >= 0; --g) {  // parents before children
+      const bool pc = gpar[g] >= 0 && covered[gpar[g]];
+      const double zm = sub_nc[g] * (sub_nc[g] + below_g[g]);
+      const bool ok = gsize[g] > 1 && ht[g] <= kCollapseHeight && sub_nc[g] <= kCollapseCols &&
+                      zm <= kCollapseGrowth * sub_z[g];
+      sel[g] = !pc && ok;
+      covered[g] = pc || sel[g];
+    }
+    std::vector<int32_t> root_at(ng, -1);  // selected subtrees are disjoint: [r - size + 1, r]
+    for (int32_t r = 0; r < ng; ++r)
+      if (sel[r]) root_at[r - gsize[r] + 1] = r;
+    std::vector<int32_t> ncol, nlast;
+    for (int32_t g = 0; g < ng;) {
+      const int32_t end = root_at[g] >= 0 ? root_at[g] : g;
+      ncol.push_back(gcol[g]);
+      nlast.push_back(last_f[end]);
+      g = end + 1;
+    }
+    f->sup_col.swap(ncol);
+    last_f.swap(nlast);
+  }
   std::vector<int32_t> sup_of(n);
   for (size_t s = 0; s < f->sup_col.size(); ++s) {
     const int32_t c1 = s + 1 < f->sup_col.size() ? f->sup_col[s + 1] : (int32_t)n;
@@ -539,7 +595,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nr <= kTaskEntries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
-      const int32_t cols = (int32_t)std::min<int64_t>(64, std::max<int64_t>(1, kTaskEntries / nr));
+      const int32_t cols = (int32_t)std::min<int64_t>(kBwdTaskCols, std::max<int64_t>(1, kTaskEntries / nr));
       f->bfirst[s] = (int32_t)f->btask.size();
       for (int32_t k = 0; k < nc; k += cols) {
         f->btask.push_back({s, k, std::min(nc, k + cols), 0});

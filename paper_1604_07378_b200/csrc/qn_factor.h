@@ -89,6 +89,11 @@ struct qn_factor {
 namespace qn {
 constexpr int64_t kTaskEntries = 8192;  // Z entries per solve task (64 KB shared-memory tile)
 constexpr int64_t kTopMax = 2560;       // max columns of the dense top block (S^-1 <= 52 MB)
+constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
+// bottom-of-tree subtree collapse (see factor_build_host)
+constexpr int32_t kCollapseHeight = 3;
+constexpr double kCollapseCols = 512;
+constexpr double kCollapseGrowth = 2.5;
 
 // host: ordering + symbolic + numeric factorisation; returns QN_OK / QN_ERR_*
 int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int32_t* indices,

@@ -173,6 +173,7 @@ __global__ void k_init(SysView v) {
     c.alpha = 0.0;
     c.slope = 0.0;
     c.t0 = global_ns();
+    if (v.pcg) v.pctl[b].total = 0;
     if (b == 0) {
       *v.active = v.n_inst;
       *v.passes = 0;
@@ -754,8 +755,7 @@ __global__ void __launch_bounds__(kPT) k_pcg_init(SysView v) {
         const double z = q[c] * di;
         v.px[o + c] = 0.0;
         v.pr[o + c] = q[c];
-        v.pz[o + c] = z;
-        v.pp[o + c] = z;  // buffer 0
+        v.pp[o + c] = z;  // buffer 0 (read with beta = 0 by the first SpMV)
         acc[c] = q[c] * z;
         acc[3 + c] = q[c] * q[c];
       }
@@ -788,101 +788,166 @@ __global__ void __launch_bounds__(kPT) k_pcg_init(SysView v) {
   pcg_global_tail(v, 0);
 }
 
-__global__ void __launch_bounds__(kPT) k_pcg_spmv(SysView v) {
+// q = A p with p = z + beta p_old fused into the neighbour loads (z = dinv r
+// recomputed, so z is never stored); one warp per SELL slice, lane = row.
+// Partial p.q per block -> the last block computes alpha.
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(SysView v) {
   const int b = blockIdx.y;
-  if (pcg_on(v, b)) {
-    __shared__ double red[3 * 32];
-    const PcgCtl& pc = v.pctl[b];
-    const int pb = pc.iter & 1;
-    const double be[3] = {pc.beta[0], pc.beta[1], pc.beta[2]};
-    const double* pold = v.pp + ((size_t)pb * v.n_inst + b) * v.n_free * 3;
-    double* pnew = v.pp + ((size_t)(pb ^ 1) * v.n_inst + b) * v.n_free * 3;
-    const double* z = v.pz + (size_t)b * v.n_free * 3;
-    double acc[3] = {0, 0, 0};
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < v.n_free) {
-      const double* av = v.a_val + (size_t)b * v.a_nnz;
-      double q0 = 0.0, q1 = 0.0, q2 = 0.0;
-      for (int64_t e = v.a_ptr[i]; e < v.a_ptr[i + 1]; ++e) {
-        const int j = __ldg(v.a_col + e);
-        const double a = __ldg(av + e);
-        q0 = fma(a, fma(be[0], pold[3 * j + 0], z[3 * j + 0]), q0);
-        q1 = fma(a, fma(be[1], pold[3 * j + 1], z[3 * j + 1]), q1);
-        q2 = fma(a, fma(be[2], pold[3 * j + 2], z[3 * j + 2]), q2);
+  if (!pcg_on(v, b)) return;
+  __shared__ double red[3 * 32];
+  const PcgCtl& pc = v.pctl[b];
+  const int pb = pc.iter & 1;
+  const double be0 = pc.beta[0], be1 = pc.beta[1], be2 = pc.beta[2];
+  const size_t vo = (size_t)b * v.n_free * 3;
+  const double* __restrict__ pold = v.pp + (size_t)pb * v.n_inst * v.n_free * 3 + vo;
+  double* __restrict__ pnew = v.pp + (size_t)(pb ^ 1) * v.n_inst * v.n_free * 3 + vo;
+  const double* __restrict__ r = v.pr + vo;
+  const double* __restrict__ dinv = v.dinv + (size_t)b * v.n_free;
+  const double* __restrict__ av = v.sell_val + (size_t)b * v.sell_nnz;
+  double* __restrict__ q = v.pq + vo;
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  double acc[3] = {0, 0, 0};
+  for (int sl = w0; sl < v.nslice; sl += nw) {
+    const int64_t e0 = v.sell_ptr[sl], e1 = v.sell_ptr[sl + 1];
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+    int64_t e = e0 + lane;
+    for (; e + 96 < e1; e += 128) {  // 4 entries of the row in flight
+      int j[4];
+      double a[4], d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        j[u] = __ldg(v.sell_col + e + 32 * u);
+        a[u] = __ldg(av + e + 32 * u);
       }
-      const double p0 = fma(be[0], pold[3 * i + 0], z[3 * i + 0]);
-      const double p1 = fma(be[1], pold[3 * i + 1], z[3 * i + 1]);
-      const double p2 = fma(be[2], pold[3 * i + 2], z[3 * i + 2]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[u] = __ldg(dinv + j[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* pj = pold + 3 * (size_t)j[u];
+        const double* rj = r + 3 * (size_t)j[u];
+        q0 = fma(a[u], fma(be0, pj[0], rj[0] * d[u]), q0);
+        q1 = fma(a[u], fma(be1, pj[1], rj[1] * d[u]), q1);
+        q2 = fma(a[u], fma(be2, pj[2], rj[2] * d[u]), q2);
+      }
+    }
+    for (; e < e1; e += 32) {
+      const int j = __ldg(v.sell_col + e);
+      const double a = __ldg(av + e), d = __ldg(dinv + j);
+      const double* pj = pold + 3 * (size_t)j;
+      const double* rj = r + 3 * (size_t)j;
+      q0 = fma(a, fma(be0, pj[0], rj[0] * d), q0);
+      q1 = fma(a, fma(be1, pj[1], rj[1] * d), q1);
+      q2 = fma(a, fma(be2, pj[2], rj[2] * d), q2);
+    }
+    const int i = 32 * sl + lane;
+    if (i < v.n_free) {
+      const double d = dinv[i];
+      const double p0 = fma(be0, pold[3 * i + 0], r[3 * i + 0] * d);
+      const double p1 = fma(be1, pold[3 * i + 1], r[3 * i + 1] * d);
+      const double p2 = fma(be2, pold[3 * i + 2], r[3 * i + 2] * d);
       pnew[3 * i + 0] = p0;
       pnew[3 * i + 1] = p1;
       pnew[3 * i + 2] = p2;
-      double* q = v.pq + ((size_t)b * v.n_free + i) * 3;
-      q[0] = q0;
-      q[1] = q1;
-      q[2] = q2;
-      acc[0] = p0 * q0;
-      acc[1] = p1 * q1;
-      acc[2] = p2 * q2;
+      q[3 * i + 0] = q0;
+      q[3 * i + 1] = q1;
+      q[3 * i + 2] = q2;
+      acc[0] = fma(p0, q0, acc[0]);
+      acc[1] = fma(p1, q1, acc[1]);
+      acc[2] = fma(p2, q2, acc[2]);
     }
-    block_sum<3>(acc, red);
+  }
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pv = v.part_p + ((size_t)b * v.nblk_spmv + blockIdx.x) * 8;
+    for (int k = 0; k < 3; ++k) pv[k] = acc[k];
+  }
+  if (last_block(v.cnt_p, 1, b, v.n_inst, gridDim.x)) {
+    __shared__ double tot[3];
+    sum_partials(v.part_p + (size_t)b * v.nblk_spmv * 8, gridDim.x, 8, 3, tot);
     if (threadIdx.x == 0) {
-      double* pv = v.part_p + ((size_t)b * v.nblk_p + blockIdx.x) * 8;
-      for (int k = 0; k < 3; ++k) pv[k] = acc[k];
-    }
-    if (last_block(v.cnt_p, 1, b, v.n_inst, gridDim.x)) {
-      __shared__ double tot[3];
-      sum_partials(v.part_p + (size_t)b * v.nblk_p * 8, gridDim.x, 8, 3, tot);
-      if (threadIdx.x == 0) {
-        PcgCtl& p = v.pctl[b];
-        for (int c = 0; c < 3; ++c) p.alpha[c] = (p.conv >> c) & 1 ? 0.0 : p.rz[c] / tot[c];
-      }
+      PcgCtl& p = v.pctl[b];
+      for (int c = 0; c < 3; ++c) p.alpha[c] = (p.conv >> c) & 1 ? 0.0 : p.rz[c] / tot[c];
     }
   }
 }
 
-__global__ void __launch_bounds__(kPT) k_pcg_update(SysView v) {
+// x += alpha p, r -= alpha q; partial r.z and r.r.  One thread per (row,
+// coordinate) of the flattened (n_free x 3) vectors, 4 elements in flight.
+__global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(SysView v) {
   const int b = blockIdx.y;
   if (pcg_on(v, b)) {
     __shared__ double red[6 * 32];
     const PcgCtl& pc = v.pctl[b];
-    const double* pnew = v.pp + ((size_t)((pc.iter & 1) ^ 1) * v.n_inst + b) * v.n_free * 3;
-    const double al[3] = {pc.alpha[0], pc.alpha[1], pc.alpha[2]};
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < v.n_free) {
-      const size_t o = ((size_t)b * v.n_free + i) * 3;
-      const double di = v.dinv[(size_t)b * v.n_free + i];
+    const size_t vo = (size_t)b * v.n_free * 3;
+    const double* __restrict__ pnew = v.pp + (size_t)((pc.iter & 1) ^ 1) * v.n_inst * v.n_free * 3 + vo;
+    double* __restrict__ x = v.px + vo;
+    double* __restrict__ r = v.pr + vo;
+    const double* __restrict__ q = v.pq + vo;
+    const double* __restrict__ dinv = v.dinv + (size_t)b * v.n_free;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (int)(t % 3);
+    const double al = pc.alpha[c];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)v.n_free;
+    double rz = 0.0, rr = 0.0;
+    int64_t e = t;
+    for (; e + 3 * stride < n3; e += 4 * stride) {
+      double xv[4], pv[4], rv[4], qv[4], dv[4];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        v.px[o + c] = fma(al[c], pnew[3 * i + c], v.px[o + c]);
-        const double r = fma(-al[c], v.pq[o + c], v.pr[o + c]);
-        const double z = r * di;
-        v.pr[o + c] = r;
-        v.pz[o + c] = z;
-        acc[c] = r * z;
-        acc[3 + c] = r * r;
+      for (int u = 0; u < 4; ++u) {
+        const int64_t f = e + u * stride;
+        xv[u] = x[f];
+        pv[u] = pnew[f];
+        rv[u] = r[f];
+        qv[u] = q[f];
+        dv[u] = __ldg(dinv + f / 3);
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t f = e + u * stride;
+        x[f] = fma(al, pv[u], xv[u]);
+        const double rn = fma(-al, qv[u], rv[u]);
+        r[f] = rn;
+        const double z = rn * dv[u];
+        rz = fma(rn, z, rz);
+        rr = fma(rn, rn, rr);
+      }
+    }
+    for (; e < n3; e += stride) {
+      x[e] = fma(al, pnew[e], x[e]);
+      const double rn = fma(-al, q[e], r[e]);
+      r[e] = rn;
+      const double z = rn * __ldg(dinv + e / 3);
+      rz = fma(rn, z, rz);
+      rr = fma(rn, rn, rr);
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      acc[k] = k == c ? rz : 0.0;
+      acc[3 + k] = k == c ? rr : 0.0;
     }
     block_sum<6>(acc, red);
     if (threadIdx.x == 0) {
-      double* pv = v.part_p + ((size_t)b * v.nblk_p + blockIdx.x) * 8;
-      for (int k = 0; k < 6; ++k) pv[k] = acc[k];
+      double* pp = v.part_p + ((size_t)b * v.nblk_upd + blockIdx.x) * 8;
+      for (int k = 0; k < 6; ++k) pp[k] = acc[k];
     }
     if (last_block(v.cnt_p, 2, b, v.n_inst, gridDim.x)) {
       __shared__ double tot[6];
-      sum_partials(v.part_p + (size_t)b * v.nblk_p * 8, gridDim.x, 8, 6, tot);
+      sum_partials(v.part_p + (size_t)b * v.nblk_upd * 8, gridDim.x, 8, 6, tot);
       if (threadIdx.x == 0) {
         PcgCtl& p = v.pctl[b];
         const double tol2 = v.pcg_tol * v.pcg_tol;
         int conv = p.conv;
-        for (int c = 0; c < 3; ++c) {
-          if ((conv >> c) & 1) continue;
-          p.beta[c] = tot[c] / p.rz[c];
-          p.rz[c] = tot[c];
-          p.rr[c] = tot[3 + c];
-          if (tot[3 + c] <= tol2 * p.bb[c]) conv |= 1 << c;
+        for (int k = 0; k < 3; ++k) {
+          if ((conv >> k) & 1) continue;
+          p.beta[k] = tot[k] / p.rz[k];
+          p.rz[k] = tot[k];
+          p.rr[k] = tot[3 + k];
+          if (tot[3 + k] <= tol2 * p.bb[k]) conv |= 1 << k;
         }
         p.iter += 1;
+        p.total += 1;
         if ((conv & 7) == 7 || p.iter >= v.pcg_maxit) {
           conv |= 8;
           atomicSub(v.pcg_active, 1);
@@ -931,10 +996,9 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
 
 int launch_pcg_iter(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
-  const dim3 gp(v.nblk_p, v.n_inst);
-  k_pcg_spmv<<<gp, kPT, 0, st>>>(v);
+  k_pcg_spmv<<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v);
   QN_CHECK_LAUNCH();
-  k_pcg_update<<<gp, kPT, 0, st>>>(v);
+  k_pcg_update<<<dim3(v.nblk_upd, v.n_inst), kUpdThreads, 0, st>>>(v);
   QN_CHECK_LAUNCH();
   return QN_OK;
 }

@@ -52,7 +52,7 @@ struct FactorView {
   double* u;
   unsigned* flags;           // [nbatch][nftask + nbtask] epoch of completion per task
   unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
-  unsigned long long* trace; // diagnostics: 3 timestamps per forward then backward item, or null
+  unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
   const double* sinv;        // K x K symmetric
   const int32_t* tcols;
@@ -103,6 +103,8 @@ inline FactorView factor_view(const qn_factor* f) {
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kStageIdx = 2048;  // int32 index slots staged in shared memory per task
+constexpr int kTraceSlots = 6;   // globaltimer start, ready; clock64 ready, data staged, computed, published
+constexpr int kBwdCols = (int)kBwdTaskCols;  // max columns of a backward task
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -112,6 +114,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 __device__ __forceinline__ void trace_mark(unsigned long long* trace, size_t slot) {
   if (trace && threadIdx.x == 0) trace[slot] = gtime();
+}
+// SM cycle counter (phases inside one task run on one SM)
+__device__ __forceinline__ void trace_clock(unsigned long long* trace, size_t slot) {
+  if (trace && threadIdx.x == 0) trace[slot] = (unsigned long long)clock64();
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -162,12 +168,52 @@ __device__ __forceinline__ void wait_flag_range(const unsigned* flags, int first
   __syncthreads();
 }
 
+// Dot products of 4 staged Z columns (local kl .. kl+nv-1, column-major with
+// leading dimension nr) with the (rows x 3) vector w over rows [r0, r1): lanes
+// stride the rows (12 independent chains), then a reduce-scatter butterfly
+// (12 -> 6 -> 3 values per lane, then 3 full levels: 18 shuffles instead of
+// 60).  On return lane 8j holds column j's three sums in out[0..2].
+__device__ __forceinline__ void col4_dots(const double* zt, int nr, const double* w, int kl, int nv, int r0, int r1,
+                                          int lane, double (&out)[3]) {
+  double a[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) a[q] = 0.0;
+  const double* zc = zt + (size_t)kl * nr;
+  for (int r = r0 + lane; r < r1; r += 32) {
+    const double w0 = w[3 * r + 0], w1 = w[3 * r + 1], w2 = w[3 * r + 2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double l = j < nv ? zc[(size_t)j * nr + r] : 0.0;
+      a[3 * j + 0] = fma(l, w0, a[3 * j + 0]);
+      a[3 * j + 1] = fma(l, w1, a[3 * j + 1]);
+      a[3 * j + 2] = fma(l, w2, a[3 * j + 2]);
+    }
+  }
+  const bool up16 = lane & 16, up8 = lane & 8;
+  double b6[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double keep = up16 ? a[i + 6] : a[i], send = up16 ? a[i] : a[i + 6];
+    b6[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double keep = up8 ? b6[i + 3] : b6[i], send = up8 ? b6[i] : b6[i + 3];
+    out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
+}
+
 // publish this task: all of the CTA's global writes are ordered before the flag
+// (CTA barrier, then one gpu-scope acq_rel fence — cumulative over the writes
+// the barrier ordered — and a relaxed flag store)
 __device__ __forceinline__ void publish(unsigned* flag, unsigned epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, epoch);
+    asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
   }
 }
 
@@ -257,10 +303,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
       f[3 * p + 1] = v[1];
       f[3 * p + 2] = v[2];
     }
-    trace_mark(F.trace, 3 * (size_t)item + 0);
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
     const int d0 = F.fdep_ptr[s], d1 = F.fdep_ptr[s + 1];
     wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d0, d1 - d0, epoch, F.sched);
-    trace_mark(F.trace, 3 * (size_t)item + 1);
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 2);
     // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
     for (int p = threadIdx.x; p < nc; p += blockDim.x) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -291,6 +338,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
     }
     cp_async_wait_all();
     __syncthreads();
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
     // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
     const int ks = kSolveWarps / rg;
     const int g = warp / ks, j = warp % ks;
@@ -332,15 +380,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
         __stcg(us + 2, e2 + v2);
       }
     }
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
     publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
-    trace_mark(F.trace, 3 * (size_t)item + 2);
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
   }
   cta_exit(sched, s_epoch);
 }
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
-  // smem: ztile[kTaskEntries] | w[max_rows*3] = [y_J; -x_below] | row staging (int32)
+  // smem: ztile[kTaskEntries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | row staging (int32)
   extern __shared__ double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
@@ -362,16 +411,20 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     const int64_t R0 = F.sup_row_ptr[s];
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
     double* w = sm + kTaskEntries;
-    int* srow = (int*)(w + 3 * nr);
+    double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
+    int* srow = (int*)(pre + 3 * kBwdCols);
     const bool staged = nr - nc <= kStageIdx;
     const int p = F.parent[s];
-    // ---- stage: Z columns [k0, k1) (rows >= k), y_J, below-row ids ----
+    // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
     {
       const double* Zg = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s];
       const int cnt = (k1 - k0) * nr;
       for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         const int kk = e / nr, r = e - kk * nr;
-        if (r >= k0 + kk) cp_async8(zt + e, Zg + (int64_t)(k0 + kk) * nr + r);
+        if (r >= k0 + kk)
+          cp_async8(zt + e, Zg + (int64_t)(k0 + kk) * nr + r);
+        else
+          zt[e] = 0.0;
       }
     }
     const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
@@ -382,12 +435,27 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     }
     if (staged)
       for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
-    const size_t tb = 3 * ((size_t)F.nftask * F.nbatch + item);
+    const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
     trace_mark(F.trace, tb + 0);
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
+    const int ncols = k1 - k0;
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        pre[3 * (kl + j) + 0] = a[0];
+        pre[3 * (kl + j) + 1] = a[1];
+        pre[3 * (kl + j) + 2] = a[2];
+      }
+    }
     if (p >= 0)
       wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, F.bfirst[p], F.bcount[p], epoch,
                       F.sched);
     trace_mark(F.trace, tb + 1);
+    trace_clock(F.trace, tb + 2);
     const double* xg = F.x + (size_t)b * F.n * 3;
     for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) {
       const int row = staged ? srow[q] : F.sup_rows[R0 + nc + q];
@@ -395,32 +463,27 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
       w[3 * (nc + q) + 1] = -__ldcg(xg + 3 * row + 1);
       w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
     }
-    cp_async_wait_all();
     __syncthreads();
-    for (int k = k0 + warp; k < k1; k += kSolveWarps) {
-      const double* col = zt + (size_t)(k - k0) * nr;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 4
-      for (int r = k + lane; r < nr; r += 32) {
-        const double l = col[r];
-        a0 = fma(l, w[3 * r + 0], a0);
-        a1 = fma(l, w[3 * r + 1], a1);
-        a2 = fma(l, w[3 * r + 2], a2);
-      }
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      a2 = warp_sum(a2);
-      if (lane == 0) {
+    trace_clock(F.trace, tb + 3);
+    // ---- the -x_below part, plus the staged y_J part ----
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        const int k = k0 + kl + j;
+        const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
+                             a[2] + pre[3 * (kl + j) + 2]};
         double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
-        xo[0] = a0;
-        xo[1] = a1;
-        xo[2] = a2;
-        const double v[3] = {a0, a1, a2};
+        xo[0] = v[0];
+        xo[1] = v[1];
+        xo[2] = v[2];
         io.store(b, c0 + k, v);
       }
     }
+    trace_clock(F.trace, tb + 4);
     publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
-    trace_mark(F.trace, tb + 2);
+    trace_clock(F.trace, tb + 5);
   }
   cta_exit(sched, s_epoch);
 }

@@ -42,9 +42,15 @@ struct InstCtl {
 
 // Preconditioned CG on A_free (3 right-hand sides solved in lockstep), the
 // solve used for meshes too large to factor (configs[4]).
+// PCG kernel shapes: SpMV = one warp per 32-row slice, grid-stride over slices;
+// the vector update = one thread per (row, coordinate), grid-stride with a
+// stride that is a multiple of 3 so a thread keeps its coordinate.
+constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 4;
+constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
+
 struct PcgCtl {
   double rz[3], alpha[3], beta[3], bb[3], rr[3];
-  int32_t iter, conv, pad0, pad1;  // conv: bit c = column c converged
+  int32_t iter, conv, total, pad1;  // conv: bit c = column c converged; total: CG iterations this frame
 };
 
 struct DevConfig {
@@ -94,18 +100,21 @@ struct SysView {
   cudaGraphConditionalHandle handle;
   // ---- PCG solve mode (pcg != 0) ----
   int32_t pcg, n_free, nblk_p, pcg_maxit;
+  int32_t nslice, nblk_spmv, nblk_upd, pad_p;
   double pcg_tol;
-  const int64_t* a_ptr;   // CSR of A_free (free-vertex order)
-  const int32_t* a_col;
-  const double* a_val;    // [inst][nnz]
-  int64_t a_nnz;
+  // A_free (free-vertex order) as SELL-32: slice s holds rows 32s..32s+31,
+  // entry k of lane l at sell_ptr[s] + 32k + l (zero-padded to the slice's
+  // longest row), so every warp load of the matrix is coalesced
+  const int64_t* sell_ptr;  // [nslice + 1]
+  const int32_t* sell_col;
+  const double* sell_val;   // [inst][sell_ptr[nslice]]
+  int64_t sell_nnz;
   const double* dinv;     // [inst][n_free] Jacobi preconditioner
   double* px;             // [inst][n_free][3] iterate
-  double* pr;             // residual
-  double* pz;             // preconditioned residual
+  double* pr;             // residual (z = dinv r is recomputed where needed)
   double* pp;             // [2][inst][n_free][3] search directions (double buffered)
   double* pq;             // A p
-  double* part_p;         // [inst][nblk_p][8]
+  double* part_p;         // [inst][max(nblk_p, nblk_spmv, nblk_upd)][8]
   unsigned* cnt_p;        // [3][inst] + [global]
   PcgCtl* pctl;           // [inst]
   int32_t* pcg_active;    // instances still iterating

@@ -194,3 +194,9 @@ class ResidentRun:
         v = C.c_int64(0)
         _lib.check(_lib.load().qn_system_last_frame_passes(self.system._h, C.byref(v)))
         return v.value
+
+    @property
+    def last_cg_iterations(self) -> int:
+        v = C.c_int64(0)
+        _lib.check(_lib.load().qn_system_last_frame_cg_iterations(self.system._h, C.byref(v)))
+        return v.value

@@ -26,11 +26,16 @@ def main(cfg="c2"):
     lib = _lib.load()
     _lib.check(lib.qn_factor_task_counts(f._h, C.byref(nf), C.byref(nb)))
     nf, nb = nf.value, nb.value
-    stamps = np.zeros(3 * (nf + nb), dtype=np.uint64)
+    stamps = np.zeros(6 * (nf + nb), dtype=np.uint64)
     tasks = np.zeros(4 * (nf + nb), dtype=np.int32)
     for _ in range(3):
         _lib.check(lib.qn_factor_trace_solve(f._h, _lib.ptr(stamps), _lib.ptr(tasks)))
-    st = stamps.reshape(-1, 3).astype(np.int64)
+    st6 = stamps.reshape(-1, 6).astype(np.int64)
+    ghz = 1.965  # SM clock under load (bench clocks line)
+    st = np.zeros((st6.shape[0], 5), dtype=np.int64)
+    st[:, 0], st[:, 1] = st6[:, 0], st6[:, 1]
+    for j in range(3):  # phases after 'ready' from the SM cycle counter
+        st[:, 2 + j] = st6[:, 1] + ((st6[:, 3 + j] - st6[:, 2]) / ghz).astype(np.int64)
     tk = tasks.reshape(-1, 4)
     info = f.info()
     print(cfg, info)
@@ -45,14 +50,17 @@ def main(cfg="c2"):
         lvl = np.zeros(len(t), dtype=int)
         # recompute levels from ticket order: consecutive supernodes share a level when monotone
         par = None
-        print(f"--- {name}: {len(t)} tasks, span {s[:, 2].max():.1f} us, "
-              f"mean wait {np.mean(s[:, 1] - s[:, 0]):.2f} us, mean work {np.mean(s[:, 2] - s[:, 1]):.2f} us")
+        print(f"--- {name}: {len(t)} tasks, span {s[:, 4].max():.1f} us, "
+              f"mean wait {np.mean(s[:, 1] - s[:, 0]):.2f} us, mean work {np.mean(s[:, 4] - s[:, 1]):.2f} us "
+              f"(gather {np.mean(s[:, 2] - s[:, 1]):.2f} compute {np.mean(s[:, 3] - s[:, 2]):.2f} "
+              f"publish {np.mean(s[:, 4] - s[:, 3]):.2f})")
         # bucket by completion-time deciles of the task list order
         q = np.array_split(np.arange(len(t)), 12)
         for i, idx in enumerate(q):
             print(f"  tickets {idx[0]:5d}-{idx[-1]:5d}: start {s[idx,0].min():7.1f}..{s[idx,0].max():7.1f} "
-                  f"ready {np.median(s[idx,1]):7.1f} end {s[idx,2].max():7.1f}  "
-                  f"wait {np.mean(s[idx,1]-s[idx,0]):5.2f} work {np.mean(s[idx,2]-s[idx,1]):5.2f} us")
+                  f"ready {np.median(s[idx,1]):7.1f} end {s[idx,4].max():7.1f}  "
+                  f"wait {np.mean(s[idx,1]-s[idx,0]):5.2f} gather {np.mean(s[idx,2]-s[idx,1]):5.2f} "
+                  f"compute {np.mean(s[idx,3]-s[idx,2]):5.2f} publish {np.mean(s[idx,4]-s[idx,3]):5.2f} us")
 
 
 if __name__ == "__main__":

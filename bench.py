@@ -126,9 +126,9 @@ def ncu_traffic(workload, kernel):
 def build_scene(name, rank, world):
     from paper_1604_07378_b200 import scenes
     sc = scenes.CONFIGS[name]()
-    if name == "c4":  # shard independent instances across ranks
-        per = len(sc.batch_materials) // world
-        lo, hi = rank * per, (rank + 1) * per
+    if name == "c4":  # shard independent instances across ranks (no collective on the data path)
+        from paper_1604_07378_b200.parallel import shard_instances
+        lo, hi = shard_instances(len(sc.batch_materials), world, rank)
         sc.batch_materials = sc.batch_materials[lo:hi]
         sc.q_l, sc.q_prev = sc.q_l[lo:hi], sc.q_prev[lo:hi]
     return sc

@@ -219,6 +219,12 @@ int qn_system_set_graph_mode(qn_system* s, int32_t use_graph);
 int qn_system_last_frame_ms(qn_system* s, double* ms);
 /* body passes (line-search trials + re-evaluations) of the last frame */
 int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
+/* diagnostics: per body pass, globaltimer ns at the entry of block 0 and at
+ * the end of the finalising block of k_grad, k_eta, k_vec (entry only) and
+ * k_tet; out = [512 passes][4 kernels][2] (0 = not reached).  Enabling
+ * rebuilds the frame graph. */
+int qn_system_set_timeline(qn_system* s, int32_t enable);
+int qn_system_timeline(qn_system* s, uint64_t* out, int64_t cap);
 /* PCG mode: conjugate-gradient iterations of the last frame, summed over
  * instances (0 in direct mode) */
 int qn_system_last_frame_cg_iterations(qn_system* s, int64_t* iters);

@@ -131,7 +131,7 @@ int factor_upload(qn_factor* f) {
   for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
   // Z tile + forward: f (nc x 3) + partials (256 x 3) + index staging; backward: w (nr x 3) + row staging
   f->smem_bytes = (int)(sizeof(double) * kTaskEntries +
-                        sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows + kBwdCols) +
+                        sizeof(double) * 3 * std::max<size_t>((size_t)max_nc + kSolveThreads, f->max_rows + kBwdCols + kBwdCols / 3 + 1) +
                         sizeof(int) * kStageIdx);
   QN_REQUIRE(f->smem_bytes <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: supernode front exceeds shared memory");
   // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
@@ -631,6 +631,34 @@ int qn_system_last_frame_passes(qn_system* S, int64_t* passes) {
   return QN_OK;
 }
 
+int qn_system_set_timeline(qn_system* S, int32_t enable) {
+  QN_REQUIRE(S, QN_ERR_ARG, "null");
+  const size_t cnt = (size_t)qn::kTimelinePasses * qn::kTimelineKernels * 2;
+  if (enable && !S->v.ktl) {
+    int rc = sys_alloc(S, &S->v.ktl, cnt);
+    if (rc) return rc;
+  } else if (!enable) {
+    S->v.ktl = nullptr;  // buffer stays owned by the system
+  }
+  if (S->exec) {  // kernels capture the view by value: rebuild the graph
+    cudaGraphExecDestroy(S->exec);
+    S->exec = nullptr;
+    cudaGraphDestroy(S->graph);
+    S->graph = nullptr;
+  }
+  return QN_OK;
+}
+
+int qn_system_timeline(qn_system* S, uint64_t* out, int64_t cap) {
+  QN_REQUIRE(S && out, QN_ERR_ARG, "null");
+  QN_REQUIRE(S->v.ktl, QN_ERR_ARG, "timeline: not enabled");
+  const int64_t cnt = (int64_t)qn::kTimelinePasses * qn::kTimelineKernels * 2;
+  QN_REQUIRE(cap >= cnt, QN_ERR_ARG, "timeline: buffer too small");
+  QN_CUDA(cudaDeviceSynchronize());
+  QN_CUDA(cudaMemcpy(out, S->v.ktl, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return QN_OK;
+}
+
 int qn_system_last_frame_cg_iterations(qn_system* S, int64_t* iters) {
   QN_REQUIRE(S && iters, QN_ERR_ARG, "null");
   *iters = 0;
@@ -720,6 +748,9 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
     rc = stage_in(S, S->d_targets, fixed_targets, (size_t)S->n_inst * S->n_fixed * 3, mem, st);
     if (rc) return rc;
   }
+  if (S->v.ktl)
+    QN_CUDA(cudaMemsetAsync(S->v.ktl, 0,
+                            sizeof(uint64_t) * qn::kTimelinePasses * qn::kTimelineKernels * 2, st));
   QN_CUDA(cudaEventRecord(S->ev0, st));
   if (S->use_graph) {
     const int mb = c.m <= 5 ? 5 : kMaxM;  // kernels are specialised on the history bound

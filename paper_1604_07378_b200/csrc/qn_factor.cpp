@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -544,15 +545,26 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     if (nbatch == 1) {
       int32_t maxd = 0;
       for (int32_t s = 0; s < ns; ++s) maxd = std::max(maxd, dep[s]);
-      std::vector<int64_t> cols_at(maxd + 1, 0);
-      for (int32_t s = 0; s < ns; ++s) cols_at[dep[s]] += f->sup_col[s + 1] - f->sup_col[s];
+      std::vector<int64_t> cols_at(maxd + 1, 0), wide_at(maxd + 1, 0);
+      for (int32_t s = 0; s < ns; ++s) {
+        const int64_t nc = f->sup_col[s + 1] - f->sup_col[s];
+        cols_at[dep[s]] += nc;
+        wide_at[dep[s]] = std::max(wide_at[dep[s]], nc);
+      }
+      // Only levels of wide separators go dense: narrow top levels are
+      // cheaper as sparse tasks than a K^2 product that also crowds L2
+      // (measured: c2 best without a top, c3 best with K ~ 3.8k).
+      int64_t top_max = kTopMax, min_wide = kTopMinWidth;  // env: tuning experiments only
+      if (const char* e = std::getenv("QN_TOP_MAX")) top_max = std::max<int64_t>(0, std::atoll(e));
+      if (const char* e = std::getenv("QN_TOP_MIN_WIDTH")) min_wide = std::max<int64_t>(0, std::atoll(e));
       int32_t dstar = -1;
       int64_t cum = 0;
       for (int32_t d = 0; d <= maxd; ++d) {
         cum += cols_at[d];
-        if (cum > kTopMax) break;
+        if (cum > top_max || (wide_at[d] < min_wide && n > kTopDenseAll)) break;
         dstar = d;
       }
+      if (n <= kTopDenseAll) dstar = maxd;  // small systems: one dense product
       if (dstar >= 0) {
         for (int32_t s = 0; s < ns; ++s) f->is_top[s] = dep[s] <= dstar;
         for (int32_t s = 0; s < ns; ++s)

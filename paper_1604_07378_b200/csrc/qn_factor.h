@@ -88,7 +88,9 @@ struct qn_factor {
 
 namespace qn {
 constexpr int64_t kTaskEntries = 8192;  // Z entries per solve task (64 KB shared-memory tile)
-constexpr int64_t kTopMax = 2560;       // max columns of the dense top block (S^-1 <= 52 MB)
+constexpr int64_t kTopMax = 4096;       // max columns of the dense top block (S^-1 <= 134 MB)
+constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
+constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
 constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
 // bottom-of-tree subtree collapse (see factor_build_host)
 constexpr int32_t kCollapseHeight = 3;

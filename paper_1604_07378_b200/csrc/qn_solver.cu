@@ -37,6 +37,7 @@ namespace qn {
 
 constexpr int kVT = kVertexThreads;  // vertex-kernel block
 constexpr int kTT = 128;  // tet-kernel block
+constexpr int kTetBlocksPerSm = 5;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
 constexpr double kAlphaFloor = 1e-12;      // solvers.py:29
@@ -202,6 +203,18 @@ __device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, b
                               int gnew);
 __device__ void eta_finalize(InstCtl& c, const double* tot, int np);
 
+// diagnostics timeline: slot 0 = entry of block (0,0), slot 1 = end of the
+// finalising block (only when v.ktl is set)
+__device__ __forceinline__ void tl_mark(const SysView& v, int kid, int slot) {
+  if (v.ktl && threadIdx.x == 0) {
+    const unsigned long long p = *((volatile unsigned long long*)v.passes);
+    if (p < (unsigned long long)kTimelinePasses) v.ktl[(p * kTimelineKernels + kid) * 2 + slot] = global_ns();
+  }
+}
+__device__ __forceinline__ void tl_entry(const SysView& v, int kid) {
+  if (blockIdx.x == 0 && blockIdx.y == 0) tl_mark(v, kid, 0);
+}
+
 // ---------------------------------------------------------------------------
 // gradient gather + L-BFGS push / zeta (dynamics.py:470-478, solvers.py:83-103, 124-131)
 // M = compile-time bound on the history window (the register footprint of the
@@ -209,6 +222,7 @@ __device__ void eta_finalize(InstCtl& c, const double* tot, int np);
 template <int M>
 __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   constexpr int NG = 5 + 2 * M;
+  tl_entry(v, 0);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   if (cc->phase != PH_GRAD) return;
@@ -291,6 +305,7 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   ctl_load(v.ctl + b, &sc);
   if (threadIdx.x == 0) grad_finalize(v, sc, tot, push, np, cand, gnew);
   ctl_store(v.ctl + b, &sc);
+  tl_mark(v, 0, 1);
 }
 
 __device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, bool push, int np, int cand,
@@ -354,6 +369,7 @@ struct SolverIO {
       q[2] = __dsub_rn(q[2], __dmul_rn(z, t[2]));
     }
   }
+  __device__ double* dest(int b, int row) const { return v.R0 + inst_off(v, b) + (size_t)v.fact_vtx[row] * 3; }
   __device__ void store(int b, int row, const double (&x)[3]) const {
     double* r = v.R0 + inst_off(v, b) + (size_t)v.fact_vtx[row] * 3;
     r[0] = x[0];
@@ -365,6 +381,7 @@ struct SolverIO {
 // <t_i, r0> and the eta recursion (solvers.py:147-150)
 template <int M>
 __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
+  tl_entry(v, 1);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   if (cc->phase != PH_DIR || cc->npairs == 0) return;
@@ -391,6 +408,7 @@ __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
   __shared__ InstCtl sc;
   ctl_load(v.ctl + b, &sc);
   if (threadIdx.x == 0) eta_finalize(sc, tot, np);
+  tl_mark(v, 1, 1);
   __syncthreads();
   // only coef[] changed
   if (threadIdx.x < np) v.ctl[b].coef[threadIdx.x] = sc.coef[threadIdx.x];
@@ -408,6 +426,7 @@ __device__ void eta_finalize(InstCtl& c, const double* tot, int np) {
 
 // direction, trial point, inertia / slope partials
 __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
+  tl_entry(v, 2);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   const int ph = cc->phase;
@@ -574,7 +593,8 @@ __device__ __forceinline__ void store_forces(const SysView& v, int b, const doub
 
 // per-tet pass at the trial point: energy partials + corner forces
 template <bool kSm>
-__global__ void __launch_bounds__(kTT) k_tet(SysView v) {
+__global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
+  tl_entry(v, 3);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
   const int ph = cc->phase;
@@ -613,6 +633,7 @@ __global__ void __launch_bounds__(kTT) k_tet(SysView v) {
       *gc = 0;
       __threadfence();
       int act = *((volatile int32_t*)v.active);
+      tl_mark(v, 3, 1);
       *v.passes += 1;
       if (*v.passes > (unsigned long long)v.cfg->max_passes) act = 0;  // runaway guard (host reports it)
       if (v.cfg->use_graph) cudaGraphSetConditional(v.handle, act > 0 ? 1u : 0u);

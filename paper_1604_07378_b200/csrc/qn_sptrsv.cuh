@@ -412,7 +412,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
     double* w = sm + kTaskEntries;
     double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
-    int* srow = (int*)(pre + 3 * kBwdCols);
+    double** sdst = (double**)(pre + 3 * kBwdCols);  // [kBwdCols] io destination of each column
+    int* srow = (int*)(sdst + kBwdCols);
     const bool staged = nr - nc <= kStageIdx;
     const int p = F.parent[s];
     // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     }
     if (staged)
       for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
+    for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
     const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
     trace_mark(F.trace, tb + 0);
     cp_async_wait_all();
@@ -478,7 +480,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
         xo[0] = v[0];
         xo[1] = v[1];
         xo[2] = v[2];
-        io.store(b, c0 + k, v);
+        double* d = sdst[kl + j];
+        d[0] = v[0];
+        d[1] = v[1];
+        d[2] = v[2];
       }
     }
     trace_clock(F.trace, tb + 4);
@@ -696,6 +701,7 @@ struct PlainIO {
     v[1] = B[3 * o + 1];
     v[2] = B[3 * o + 2];
   }
+  __device__ double* dest(int, int row) const { return X + 3 * (size_t)perm[row]; }
   __device__ void store(int, int row, const double (&v)[3]) const {
     const int o = perm[row];
     X[3 * o + 0] = v[0];

@@ -48,6 +48,10 @@ struct InstCtl {
 constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 4;
 constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
 
+// diagnostics timeline (qn_system_timeline): entry of block 0 and end of the
+// finalising block of the body kernels, per body pass
+constexpr int kTimelinePasses = 512, kTimelineKernels = 4;  // k_grad, k_eta, k_vec, k_tet
+
 struct PcgCtl {
   double rz[3], alpha[3], beta[3], bb[3], rr[3];
   int32_t iter, conv, total, pad1;  // conv: bit c = column c converged; total: CG iterations this frame
@@ -97,6 +101,7 @@ struct SysView {
   double* rec_ms;
   int32_t* active;     // instances not yet done
   unsigned long long* passes;
+  unsigned long long* ktl;  // diagnostics timeline [kTimelinePasses][kTimelineKernels][2] ns, or null
   cudaGraphConditionalHandle handle;
   // ---- PCG solve mode (pcg != 0) ----
   int32_t pcg, n_free, nblk_p, pcg_maxit;

@@ -99,12 +99,27 @@ def test_host_supernodal_factor_and_solve_replay(hostcheck, cfg):
     ref = osys.factor.solve(B)
     assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
     nsup, nnz_l, depth, max_rows, nft, nbt, ktop = st[:7]
-    assert 0 < ktop <= 2560  # dense top block in use
-    if cfg == "c1":
-        assert nft == 0 and nbt == 0 and ktop == osys.free.size  # whole tree fits the dense top
+    if cfg == "c1":  # small system: the whole tree is the dense top (one product)
+        assert nft == 0 and nbt == 0 and ktop == osys.free.size
+    else:  # narrow separators (16x16 planes): sparse tasks all the way up
+        assert ktop == 0 and nft > 0 and nbt > 0
     assert depth <= 16  # nested dissection + amalgamation keep the dependency tree shallow
     if cfg == "c2":
         assert nnz_l < 3.34e6  # below the SuperLU-MMD fill of the survey probe
+
+
+def test_host_partial_dense_top_replay(hostcheck, monkeypatch):
+    # force the dense top onto c2's narrow top levels (the path c3 takes by default)
+    monkeypatch.setenv("QN_TOP_MIN_WIDTH", "0")
+    sc = scenes.c2(frames=1)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    B = np.random.default_rng(2).standard_normal((osys.free.size, 3))
+    rc, X, st = _hc_solve(hostcheck, osys.A_free, _lib.f64(sc.verts[osys.free]), B)
+    assert rc == 0
+    ref = osys.factor.solve(B)
+    assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
+    ktop, nft = st[6], st[4]
+    assert 0 < ktop <= 4096 and nft > 0
 
 
 def test_host_factor_batch_and_not_spd(hostcheck):

@@ -586,6 +586,17 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     };
     f->ffirst.assign(ns, 0);
     f->bfirst.assign(ns, 0);
+    // backward Z tile: as large as kTaskEntries but small enough that two
+    // CTAs (each also holding w = nr x 3 of the tallest front) share an SM
+    {
+      int32_t mr = 0;
+      for (int32_t s = 0; s < ns; ++s)
+        if (!f->is_top[s]) mr = std::max<int32_t>(mr, (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]));
+      const int64_t rest = 8 * (3 * (int64_t)mr + 4 * kBwdTaskCols) + 4 * 2048;
+      const int64_t fit = (kSmemPerCtaPair - rest) / 8;
+      f->bwd_entries = std::max<int64_t>(mr, std::min<int64_t>(kTaskEntries, fit));
+      f->task_max_rows = mr;
+    }
     for (int32_t s : order) {
       if (f->is_top[s]) continue;
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
@@ -606,8 +617,8 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       if (f->is_top[s]) continue;
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
-      QN_REQUIRE(nr <= kTaskEntries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
-      const int32_t cols = (int32_t)std::min<int64_t>(kBwdTaskCols, std::max<int64_t>(1, kTaskEntries / nr));
+      QN_REQUIRE(nr <= f->bwd_entries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
+      const int32_t cols = (int32_t)std::min<int64_t>(kBwdTaskCols, std::max<int64_t>(1, f->bwd_entries / nr));
       f->bfirst[s] = (int32_t)f->btask.size();
       for (int32_t k = 0; k < nc; k += cols) {
         f->btask.push_back({s, k, std::min(nc, k + cols), 0});

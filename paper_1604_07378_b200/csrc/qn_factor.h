@@ -43,6 +43,8 @@ struct qn_factor {
   std::vector<double> sinv;             // K x K, symmetric (column-major)
   int64_t nvals = 0, nupd = 0, nnz_l = 0;
   int32_t max_rows = 0, depth = 0;
+  int32_t task_max_rows = 0;   // tallest front among the supernodes solved by tasks (not the dense top)
+  int64_t bwd_entries = 8192;  // Z entries per backward task tile (<= kTaskEntries, set by the task builder)
   double flops = 0.0, factor_seconds = 0.0;
   // ---- numeric (host, nbatch x nvals) ----
   std::vector<double> vals;
@@ -80,8 +82,8 @@ struct qn_factor {
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
   unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)
-  int smem_bytes = 0;
-  int grid_ctas = 0;              // persistent solve grid (co-resident CTAs)
+  int smem_f = 0, smem_b = 0;     // dynamic shared memory of the forward / backward solve kernels
+  int grid_f = 0, grid_b = 0;     // persistent solve grids (co-resident CTAs)
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)
   bool on_device = false;
 };
@@ -92,6 +94,7 @@ constexpr int64_t kTopMax = 4096;       // max columns of the dense top block (S
 constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
 constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
 constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
+constexpr int64_t kSmemPerCtaPair = 110 * 1024;  // dynamic smem per CTA with two CTAs per SM (228 KB - reserved/static)
 // bottom-of-tree subtree collapse (see factor_build_host)
 constexpr int32_t kCollapseHeight = 3;
 constexpr double kCollapseCols = 512;

@@ -30,7 +30,7 @@
 namespace qn {
 
 struct FactorView {
-  int32_t n, nsup, nbatch, nftask, nbtask;
+  int32_t n, nsup, nbatch, nftask, nbtask, bwd_entries;
   int64_t nvals, nupd;
   const int32_t* sup_col;
   const int64_t* sup_row_ptr;
@@ -68,6 +68,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.nbatch = (int32_t)f->nbatch;
   v.nftask = (int32_t)f->ftask.size();
   v.nbtask = (int32_t)f->btask.size();
+  v.bwd_entries = (int32_t)f->bwd_entries;
   v.nvals = f->nvals;
   v.nupd = f->nupd;
   v.sup_col = f->d_sup_col;
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
-  // smem: ztile[kTaskEntries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | row staging (int32)
+  // smem: ztile[bwd_entries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | dest[kBwdCols] | row staging
   extern __shared__ double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
     const int64_t R0 = F.sup_row_ptr[s];
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-    double* w = sm + kTaskEntries;
+    double* w = sm + F.bwd_entries;
     double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
     double** sdst = (double**)(pre + 3 * kBwdCols);  // [kBwdCols] io destination of each column
     int* srow = (int*)(sdst + kBwdCols);
@@ -720,7 +721,7 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   }
   const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
   if (nf > 0) {
-    sptrsv_forward<IO><<<std::min(nf, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
+    sptrsv_forward<IO><<<std::min(nf, f->grid_f), kSolveThreads, f->smem_f, stream>>>(v, io);
     QN_CHECK_LAUNCH();
   }
   if (f->ktop > 0) {
@@ -732,7 +733,7 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     QN_CHECK_LAUNCH();
   }
   if (nb > 0) {
-    sptrsv_backward<IO><<<std::min(nb, f->grid_ctas), kSolveThreads, f->smem_bytes, stream>>>(v, io);
+    sptrsv_backward<IO><<<std::min(nb, f->grid_b), kSolveThreads, f->smem_b, stream>>>(v, io);
     QN_CHECK_LAUNCH();
   }
   return QN_OK;
@@ -740,9 +741,8 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
 
 template <class IO>
 int prepare_solve_kernels(qn_factor* f) {
-  const int smem_bytes = f->smem_bytes;
-  QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->smem_f));
+  QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->smem_b));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   if (f->ktop > 0)
@@ -751,13 +751,13 @@ int prepare_solve_kernels(qn_factor* f) {
   if (f->batch_smem > 0)
     QN_CUDA(cudaFuncSetAttribute(sptrsv_batch<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->batch_smem));
   int per_f = 0, per_b = 0, dev = 0, sms = 0;
-  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, sptrsv_forward<IO>, kSolveThreads, smem_bytes));
-  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, sptrsv_backward<IO>, kSolveThreads, smem_bytes));
+  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_f, sptrsv_forward<IO>, kSolveThreads, f->smem_f));
+  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, sptrsv_backward<IO>, kSolveThreads, f->smem_b));
   QN_CUDA(cudaGetDevice(&dev));
   QN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int per = std::max(1, std::min(per_f, per_b));
-  const int grid = per * sms;
-  f->grid_ctas = f->grid_ctas ? std::min(f->grid_ctas, grid) : grid;
+  const int gf = std::max(1, per_f) * sms, gb = std::max(1, per_b) * sms;
+  f->grid_f = f->grid_f ? std::min(f->grid_f, gf) : gf;
+  f->grid_b = f->grid_b ? std::min(f->grid_b, gb) : gb;
   return QN_OK;
 }
 

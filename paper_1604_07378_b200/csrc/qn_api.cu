@@ -117,6 +117,10 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_bcount, f->bcount.data(), f->bcount.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
+  if ((rc = dev_upload(&f->d_hlev_ptr, f->hlev_ptr.data(), f->hlev_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_hlev_sup, f->hlev_sup.data(), f->hlev_sup.size()))) return rc;
+  if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
+  if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
   if (f->ktop > 0) {
     if ((rc = dev_upload(&f->d_sinv, f->sinv.data(), f->sinv.size()))) return rc;
     if ((rc = dev_upload(&f->d_tcols, f->tcols.data(), f->tcols.size()))) return rc;
@@ -139,8 +143,13 @@ int factor_upload(qn_factor* f) {
   QN_REQUIRE(std::max(f->smem_f, f->smem_b) <= 227 * 1024, QN_ERR_UNSUPPORTED,
              "factor: supernode front exceeds shared memory");
   // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
-  const size_t bsm = sizeof(double) * 3 * ((size_t)f->n + max_nc);
-  f->batch_smem = (f->nbatch > 1 && bsm <= 96 * 1024) ? (int)bsm : 0;
+  int64_t zmax = 0;
+  for (int s = 0; s < f->nsup; ++s)
+    zmax = std::max<int64_t>(zmax, (int64_t)(f->sup_col[s + 1] - f->sup_col[s]) * (f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]));
+  f->batch_max_nc = max_nc;
+  f->batch_zmax = (int32_t)((zmax + 1) / 2 * 2);  // keep the second buffer 16-byte aligned
+  const size_t bsm = sizeof(double) * 3 * ((size_t)f->n + (size_t)kBatchWarps * max_nc);
+  f->batch_smem = (f->nbatch > 1 && bsm <= 110 * 1024) ? (int)bsm : 0;
   if ((rc = prepare_solve_kernels<PlainIO>(f))) return rc;
   f->on_device = true;
   return QN_OK;
@@ -153,7 +162,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
                   f->d_fdep_idx, f->d_sinv,       f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
-                  f->d_gtop};
+                  f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

@@ -640,6 +640,27 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
         for (int32_t t = 0; t < f->fcount[c]; ++t) f->fdep_idx[w++] = f->ffirst[c] + t;
       }
     }
+    // level lists for the batched per-instance solve: forward by height
+    // (leaves first), backward by depth (root first); supernodes of one level
+    // are independent and run on different warps of the instance's CTA
+    {
+      int32_t mh = 0, md = 0;
+      for (int32_t s = 0; s < ns; ++s) {
+        mh = std::max(mh, height[s]);
+        md = std::max(md, dep[s]);
+      }
+      auto bucket = [&](const std::vector<int32_t>& key, int32_t nl, std::vector<int32_t>& ptr,
+                        std::vector<int32_t>& list) {
+        ptr.assign(nl + 2, 0);
+        for (int32_t s = 0; s < ns; ++s) ptr[key[s] + 1]++;
+        for (int32_t l = 0; l <= nl; ++l) ptr[l + 1] += ptr[l];
+        list.assign(ns, 0);
+        std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+        for (int32_t s = 0; s < ns; ++s) list[fill[key[s]]++] = s;
+      };
+      bucket(height, mh, f->hlev_ptr, f->hlev_sup);
+      bucket(dep, md, f->dlev_ptr, f->dlev_sup);
+    }
     // g_T gather lists: every non-top supernode whose parent is top passes all
     // of its subtree's updates to top columns in its update vector u_s
     if (f->ktop > 0) {

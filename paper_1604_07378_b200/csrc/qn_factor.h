@@ -34,6 +34,8 @@ struct qn_factor {
   std::vector<int32_t> fcount, bcount;  // tasks per supernode
   std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
   std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
+  std::vector<int32_t> hlev_ptr, hlev_sup;  // supernodes grouped by height (batched forward levels)
+  std::vector<int32_t> dlev_ptr, dlev_sup;  // supernodes grouped by depth (batched backward levels)
   // dense top: the supernodes within the top levels of the tree (K columns)
   // are solved together as x_T = S^-1 g_T, S = Schur complement on T
   std::vector<uint8_t> is_top;
@@ -73,6 +75,10 @@ struct qn_factor {
   int32_t* d_bcount = nullptr;
   int32_t* d_fdep_ptr = nullptr;
   int32_t* d_fdep_idx = nullptr;
+  int32_t* d_hlev_ptr = nullptr;
+  int32_t* d_hlev_sup = nullptr;
+  int32_t* d_dlev_ptr = nullptr;
+  int32_t* d_dlev_sup = nullptr;
   unsigned* d_flags = nullptr;    // nbatch x (n_ftask + n_btask) completion epochs
   double* d_sinv = nullptr;
   int32_t* d_tcols = nullptr;
@@ -85,6 +91,7 @@ struct qn_factor {
   int smem_f = 0, smem_b = 0;     // dynamic shared memory of the forward / backward solve kernels
   int grid_f = 0, grid_b = 0;     // persistent solve grids (co-resident CTAs)
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)
+  int32_t batch_max_nc = 0, batch_zmax = 0;  // batched mode: widest supernode, largest Z block (entries)
   bool on_device = false;
 };
 

@@ -30,7 +30,7 @@
 namespace qn {
 
 struct FactorView {
-  int32_t n, nsup, nbatch, nftask, nbtask, bwd_entries;
+  int32_t n, nsup, nbatch, nftask, nbtask, bwd_entries, batch_max_nc, batch_zmax, nhlev, ndlev;
   int64_t nvals, nupd;
   const int32_t* sup_col;
   const int64_t* sup_row_ptr;
@@ -46,6 +46,10 @@ struct FactorView {
   const int32_t* bcount;
   const int32_t* fdep_ptr;  // forward: task ids of all children's tasks
   const int32_t* fdep_idx;
+  const int32_t* hlev_ptr;   // batched: supernodes by height (forward levels)
+  const int32_t* hlev_sup;
+  const int32_t* dlev_ptr;   // batched: supernodes by depth (backward levels)
+  const int32_t* dlev_sup;
   const double* vals;
   double* y;
   double* x;
@@ -69,6 +73,14 @@ inline FactorView factor_view(const qn_factor* f) {
   v.nftask = (int32_t)f->ftask.size();
   v.nbtask = (int32_t)f->btask.size();
   v.bwd_entries = (int32_t)f->bwd_entries;
+  v.batch_max_nc = f->batch_max_nc;
+  v.batch_zmax = f->batch_zmax;
+  v.nhlev = (int32_t)f->hlev_ptr.size() - 1;
+  v.ndlev = (int32_t)f->dlev_ptr.size() - 1;
+  v.hlev_ptr = f->d_hlev_ptr;
+  v.hlev_sup = f->d_hlev_sup;
+  v.dlev_ptr = f->d_dlev_ptr;
+  v.dlev_sup = f->d_dlev_sup;
   v.nvals = f->nvals;
   v.nupd = f->nupd;
   v.sup_col = f->d_sup_col;
@@ -568,128 +580,160 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_apply(FactorView F, 
 }
 
 // ---- batched small systems (configs[3]): one CTA per instance walks its whole
-// tree (postorder forward, reverse backward) with CTA barriers between
-// supernodes — no inter-CTA flags, so thousands of instances run as
-// thousands of independent CTAs.  y/x of the instance live in shared memory
-// (x overwrites y in place during the backward sweep); the update vectors
-// stay in the instance's (L2-resident) global slice.
+// tree level by level — forward by height (leaves first), backward by depth
+// (root first) — with the independent supernodes of a level on different
+// warps and one CTA barrier per level, so the sequential chain is the tree
+// height, not the supernode count.  No inter-CTA flags: thousands of
+// instances run as thousands of independent CTAs.  The right-hand side of
+// every row is staged once; y/x of the instance live in shared memory (x
+// overwrites y in place during the backward sweep); each warp keeps its
+// supernode's f / y_J in a private shared-memory slice; the update vectors
+// stay in the instance's global (L2) slice.
+constexpr int kBatchThreads = 256, kBatchWarps = kBatchThreads / 32;
+constexpr int kBatchCols = 4;  // backward: columns per pass (12 independent chains per lane)
+
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_batch(FactorView F, IO io) {
-  extern __shared__ double sm[];  // yx[n*3] | f[max_nc*3]
+__global__ void __launch_bounds__(kBatchThreads, 4) sptrsv_batch(FactorView F, IO io) {
+  extern __shared__ double sm[];  // yx[n*3] | fw[kBatchWarps][max_nc*3]
   const int b = blockIdx.x;
   if (!io.active(b)) return;
   const int n = F.n;
   double* yx = sm;
-  double* f = sm + 3 * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* fw = sm + 3 * n + (size_t)warp * 3 * F.batch_max_nc;
   double* ub = F.u + (size_t)b * F.nupd * 3;
   const double* vb = F.vals + (size_t)b * F.nvals;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // ---- forward: y = L^-1 b ----
-  for (int s = 0; s < F.nsup; ++s) {
-    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
-    const int64_t R0 = F.sup_row_ptr[s];
-    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-    for (int p = tid; p < nc; p += blockDim.x) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)F.cidx[q];
-        a0 += uc[0];
-        a1 += uc[1];
-        a2 += uc[2];
-      }
-      double v[3];
-      io.rhs(b, c0 + p, v);
-      f[3 * p + 0] = v[0] - a0;
-      f[3 * p + 1] = v[1] - a1;
-      f[3 * p + 2] = v[2] - a2;
-    }
-    __syncthreads();
-    const double* Z = vb + F.sup_val_ptr[s];
-    for (int r = tid; r < nr; r += blockDim.x) {
-      const int kmax = r < nc ? r + 1 : nc;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      int k = 0;
-      for (; k + 8 <= kmax; k += 8) {
-        double l[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) l[q] = __ldg(Z + r + (int64_t)(k + q) * nr);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          a0 = fma(l[q], f[3 * (k + q) + 0], a0);
-          a1 = fma(l[q], f[3 * (k + q) + 1], a1);
-          a2 = fma(l[q], f[3 * (k + q) + 2], a2);
-        }
-      }
-      for (; k < kmax; ++k) {
-        const double l = __ldg(Z + r + (int64_t)k * nr);
-        a0 = fma(l, f[3 * k + 0], a0);
-        a1 = fma(l, f[3 * k + 1], a1);
-        a2 = fma(l, f[3 * k + 2], a2);
-      }
-      if (r < nc) {
-        yx[3 * (c0 + r) + 0] = a0;
-        yx[3 * (c0 + r) + 1] = a1;
-        yx[3 * (c0 + r) + 2] = a2;
-      } else {
-        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-        for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
+  for (int p = tid; p < n; p += blockDim.x) {  // b for every row (independent loads)
+    double v[3];
+    io.rhs(b, p, v);
+    yx[3 * p + 0] = v[0];
+    yx[3 * p + 1] = v[1];
+    yx[3 * p + 2] = v[2];
+  }
+  __syncthreads();
+  // ---- forward: y = L^-1 b, one level of independent supernodes at a time ----
+  for (int L = 0; L < F.nhlev; ++L) {
+    for (int i = F.hlev_ptr[L] + warp; i < F.hlev_ptr[L + 1]; i += kBatchWarps) {
+      const int s = F.hlev_sup[i];
+      const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
+      const int64_t R0 = F.sup_row_ptr[s];
+      const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+      const double* Z = vb + F.sup_val_ptr[s];
+      for (int p = lane; p < nc; p += 32) {  // f = b_J - children updates
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
           const double* uc = ub + 3 * (size_t)F.cidx[q];
-          e0 += uc[0];
-          e1 += uc[1];
-          e2 += uc[2];
+          a0 += __ldcg(uc);
+          a1 += __ldcg(uc + 1);
+          a2 += __ldcg(uc + 2);
         }
-        double* us = ub + (F.sup_upd_ptr[s] + (r - nc)) * 3;
-        us[0] = e0 + a0;
-        us[1] = e1 + a1;
-        us[2] = e2 + a2;
+        fw[3 * p + 0] = yx[3 * (c0 + p) + 0] - a0;
+        fw[3 * p + 1] = yx[3 * (c0 + p) + 1] - a1;
+        fw[3 * p + 2] = yx[3 * (c0 + p) + 2] - a2;
       }
+      __syncwarp();
+      for (int r = lane; r < nr; r += 32) {  // v = Z f (lanes over rows: coalesced Z)
+        const int kmax = r < nc ? r + 1 : nc;
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+        if (r >= nc)  // children's updates on this bottom row (independent of the FMAs)
+          for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
+            const double* uc = ub + 3 * (size_t)F.cidx[q];
+            e0 += __ldcg(uc);
+            e1 += __ldcg(uc + 1);
+            e2 += __ldcg(uc + 2);
+          }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        int k = 0;
+        for (; k + 8 <= kmax; k += 8) {
+          double l[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) l[q] = __ldg(Z + r + (int64_t)(k + q) * nr);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            a0 = fma(l[q], fw[3 * (k + q) + 0], a0);
+            a1 = fma(l[q], fw[3 * (k + q) + 1], a1);
+            a2 = fma(l[q], fw[3 * (k + q) + 2], a2);
+          }
+        }
+        for (; k < kmax; ++k) {
+          const double l = __ldg(Z + r + (int64_t)k * nr);
+          a0 = fma(l, fw[3 * k + 0], a0);
+          a1 = fma(l, fw[3 * k + 1], a1);
+          a2 = fma(l, fw[3 * k + 2], a2);
+        }
+        if (r < nc) {
+          yx[3 * (c0 + r) + 0] = a0;
+          yx[3 * (c0 + r) + 1] = a1;
+          yx[3 * (c0 + r) + 2] = a2;
+        } else {
+          double* us = ub + (F.sup_upd_ptr[s] + (r - nc)) * 3;
+          __stcg(us + 0, e0 + a0);
+          __stcg(us + 1, e1 + a1);
+          __stcg(us + 2, e2 + a2);
+        }
+      }
+      __syncwarp();
     }
     __syncthreads();
   }
-  // ---- backward: x = L^-T y (in place over y) ----
-  for (int s = F.nsup - 1; s >= 0; --s) {
-    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
-    const int64_t R0 = F.sup_row_ptr[s];
-    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-    for (int p = tid; p < 3 * nc; p += blockDim.x) f[p] = yx[3 * c0 + p];
-    __syncthreads();
-    const double* Z = vb + F.sup_val_ptr[s];
-    for (int k = warp; k < nc; k += kSolveWarps) {
-      const double* col = Z + (int64_t)k * nr;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int r = k + lane; r < nr; r += 32) {
-        const double l = __ldg(col + r);
-        double w0, w1, w2;
-        if (r < nc) {
-          w0 = f[3 * r + 0];
-          w1 = f[3 * r + 1];
-          w2 = f[3 * r + 2];
-        } else {
-          const int row = F.sup_rows[R0 + r];
-          w0 = -yx[3 * row + 0];
-          w1 = -yx[3 * row + 1];
-          w2 = -yx[3 * row + 2];
+  // ---- backward: x = L^-T y (in place over y), root level first ----
+  for (int L = 0; L < F.ndlev; ++L) {
+    for (int i = F.dlev_ptr[L] + warp; i < F.dlev_ptr[L + 1]; i += kBatchWarps) {
+      const int s = F.dlev_sup[i];
+      const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
+      const int64_t R0 = F.sup_row_ptr[s];
+      const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+      const double* Z = vb + F.sup_val_ptr[s];
+      for (int p = lane; p < 3 * nc; p += 32) fw[p] = yx[3 * c0 + p];  // y_J (x_J overwrites it)
+      __syncwarp();
+      for (int k0 = 0; k0 < nc; k0 += kBatchCols) {  // kBatchCols columns per pass, lanes over rows
+        const int nv = min(kBatchCols, nc - k0);
+        double a[kBatchCols][3];
+#pragma unroll
+        for (int j = 0; j < kBatchCols; ++j) a[j][0] = a[j][1] = a[j][2] = 0.0;
+        for (int r = k0 + lane; r < nr; r += 32) {
+          double w0, w1, w2;
+          if (r < nc) {
+            w0 = fw[3 * r + 0];
+            w1 = fw[3 * r + 1];
+            w2 = fw[3 * r + 2];
+          } else {
+            const int row = F.sup_rows[R0 + r];
+            w0 = -yx[3 * row + 0];
+            w1 = -yx[3 * row + 1];
+            w2 = -yx[3 * row + 2];
+          }
+          double l[kBatchCols];
+#pragma unroll
+          for (int j = 0; j < kBatchCols; ++j)
+            l[j] = (j < nv && r >= k0 + j) ? __ldg(Z + r + (int64_t)(k0 + j) * nr) : 0.0;
+#pragma unroll
+          for (int j = 0; j < kBatchCols; ++j) {
+            a[j][0] = fma(l[j], w0, a[j][0]);
+            a[j][1] = fma(l[j], w1, a[j][1]);
+            a[j][2] = fma(l[j], w2, a[j][2]);
+          }
         }
-        a0 = fma(l, w0, a0);
-        a1 = fma(l, w1, a1);
-        a2 = fma(l, w2, a2);
+#pragma unroll
+        for (int j = 0; j < kBatchCols; ++j) {
+          const double v0 = warp_sum(a[j][0]), v1 = warp_sum(a[j][1]), v2 = warp_sum(a[j][2]);
+          if (lane == j && j < nv) {
+            yx[3 * (c0 + k0 + j) + 0] = v0;
+            yx[3 * (c0 + k0 + j) + 1] = v1;
+            yx[3 * (c0 + k0 + j) + 2] = v2;
+          }
+        }
       }
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      a2 = warp_sum(a2);
-      if (lane == 0) {
-        yx[3 * (c0 + k) + 0] = a0;
-        yx[3 * (c0 + k) + 1] = a1;
-        yx[3 * (c0 + k) + 2] = a2;
-        const double v[3] = {a0, a1, a2};
-        io.store(b, c0 + k, v);
-      }
+      __syncwarp();
     }
     __syncthreads();
+  }
+  for (int p = tid; p < n; p += blockDim.x) {  // x -> caller
+    const double v[3] = {yx[3 * p + 0], yx[3 * p + 1], yx[3 * p + 2]};
+    io.store(b, p, v);
   }
 }
 
-// Plain solve: B (n,3) -> X (n,3) in the original row order, one instance.
 struct PlainIO {
   const double* B;
   double* X;
@@ -715,7 +759,7 @@ template <class IO>
 int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   const FactorView v = factor_view(f);
   if (f->batch_smem > 0) {  // batched small systems: one CTA per instance
-    sptrsv_batch<IO><<<(int)f->nbatch, kSolveThreads, f->batch_smem, stream>>>(v, io);
+    sptrsv_batch<IO><<<(int)f->nbatch, kBatchThreads, f->batch_smem, stream>>>(v, io);
     QN_CHECK_LAUNCH();
     return QN_OK;
   }

@@ -22,6 +22,9 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("smsp__inst_executed.sum", "warp_insts"),
     ("lts__t_bytes.sum", "l2_bytes"),
+    ("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "dfma"),
+    ("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", "dadd"),
+    ("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "dmul"),
 ]
 
 
@@ -70,7 +73,10 @@ def main(path, out_txt=None, traffic=None, keys=()):
                      f"({d.get('dram_pct', 0):.1f}% of peak) | SM {d.get('sm_pct', 0):.1f}% | FP64 pipe "
                      f"{d.get('fp64_pipe_pct', 0):.1f}% | occupancy {d.get('occupancy_pct', 0):.1f}% | regs "
                      f"{d.get('regs', 0):.0f} | grid {d.get('grid', 0):.0f} | L2 {d.get('l2_bytes', 0) / 1e6:.2f} MB\n"
-                     f"  stalls: {top}")
+                     f"  stalls: {top}"
+                     + (f"\n  fp64 flops {2 * d.get('dfma', 0) + d.get('dadd', 0) + d.get('dmul', 0):.4g} "
+                        f"({(2 * d.get('dfma', 0) + d.get('dadd', 0) + d.get('dmul', 0)) / max(d.get('duration', 1), 1e-9) / 1e6:.2f} TFLOP/s)"
+                        if d.get('dfma') else ""))
         per_kernel.setdefault(name, []).append(traffic_b)
     text = "\n".join(lines)
     print(text)

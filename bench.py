@@ -123,6 +123,35 @@ def ncu_traffic(workload, kernel):
         return None
 
 
+def frame_timeline(system, run, stream):
+    """Mean in-graph duration (us) per body pass of one traced frame (globaltimer
+    stamps written by the kernels themselves, qn_system_timeline): k_grad,
+    the solve (k_grad end -> k_eta entry), k_vec and k_tet."""
+    import ctypes as C
+    from paper_1604_07378_b200 import _lib
+    lib = _lib.load()
+    passes, kernels = 512, 4
+    buf = np.zeros(passes * kernels * 2, dtype=np.uint64)
+    try:
+        _lib.check(lib.qn_system_set_timeline(system._h, 1))
+        run.step(stream=stream.cuda_stream)
+        _lib.check(lib.qn_system_timeline(system._h, _lib.ptr(buf), C.c_int64(buf.size)))
+    finally:
+        _lib.check(lib.qn_system_set_timeline(system._h, 0))
+    t = buf.reshape(passes, kernels, 2).astype(np.int64)
+    npass = int((t[:, 3, 1] > 0).sum())
+    if npass == 0:
+        return None
+    full = [p for p in range(npass) if t[p, 0, 1] and t[p, 1, 0]]
+    def mean(vals):
+        return float(np.mean(vals)) / 1000.0 if len(vals) else None
+    return {"passes": npass,
+            "grad": mean([t[p, 0, 1] - t[p, 0, 0] for p in full]),
+            "solve": mean([t[p, 1, 0] - t[p, 0, 1] for p in full]),
+            "tet": mean([t[p, 3, 1] - t[p, 3, 0] for p in range(npass)]),
+            "frame": (t[npass - 1, 3, 1] - (t[0, 0, 0] or t[0, 3, 0])) / 1000.0}
+
+
 def build_scene(name, rank, world):
     from paper_1604_07378_b200 import scenes
     sc = scenes.CONFIGS[name]()
@@ -252,43 +281,64 @@ def run_ours(args, world, rank, local):
     value = world * its_per_step * args.steps / (total_ms / 1000.0)
     tet_evals = world * passes * sc.tets.shape[0] * n_inst / (total_ms / 1000.0)
 
-    # ---- roofline of the hot kernels (stand-alone CUDA-event timing, same stream) ----
+    # ---- roofline of the hot kernels (stand-alone CUDA-event timing, same stream,
+    #      every instance) + their live in-graph durations from one traced frame ----
     hbm, peak_kind = peaks()
     info = system.factor_info()
     m, n = sc.tets.shape[0], sc.verts.shape[0]
     tet_ms = system.time_kernel("tet", reps=20, stream=sptr)
-    tet_bytes = (192.0 + 24.0 * n / m) * m                    # idx+Dm^-1+vol+forces, x gathered once
+    tet_bytes = (192.0 + 24.0 * n / m) * m * n_inst           # idx+Dm^-1+vol+forces, x gathered once
     per_frame = total_ms / args.steps
     share_tet = tet_ms * passes / args.steps / per_frame
+    batched = info.get("nbatch", 1) > 1
     if "nnz_l" in info:
         solve_ms = system.time_kernel("solve", reps=20, stream=sptr)
-        solve_bytes = 2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]  # factor read twice + rhs/y/x/u vectors
+        # factor read twice + rhs/y/x/u vectors, per instance
+        solve_bytes = (2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]) * n_inst
         share_solve = solve_ms * sc.iterations / per_frame
     else:  # PCG system: the per-tet kernel is the timed hot kernel
         solve_ms, solve_bytes, share_solve = 1.0, 0.0, 0.0
+    live = frame_timeline(system, run, stream)
     dom = "tet" if share_tet >= share_solve else "solve"
     dms, dbytes = (tet_ms, tet_bytes) if dom == "tet" else (solve_ms, solve_bytes)
     achieved = dbytes / (dms / 1000.0) / 1e9
-    roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else "sptrsv_forward+backward",
+    solve_name = "sptrsv_batch (level-parallel, CTA per instance)" if batched else "sptrsv_forward+backward"
+    roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else solve_name,
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
             "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
             "share_of_step": share_tet if dom == "tet" else share_solve,
             "other": {"tet_ms": tet_ms, "tet_GBps": tet_bytes / tet_ms / 1e6, "tet_share": share_tet,
                       "solve_ms": solve_ms if solve_bytes else None,
                       "solve_GBps": solve_bytes / solve_ms / 1e6 if solve_bytes else None,
-                      "solve_share": share_solve}}
+                      "solve_share": share_solve, "in_graph_us_per_pass": live}}
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        st = Q.SimState(q_l=np.array(sc.q_l), q_prev=np.array(sc.q_prev))
+        # page-locked host buffers, rotated so a frame never writes the arrays it reads
+        shape = np.asarray(sc.q_l).shape
+        keep = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+        host = [k.numpy() for k in keep]
+        host[0][...] = sc.q_l
+        host[1][...] = sc.q_prev
+        st = Q.SimState(q_l=host[0], q_prev=host[1])
+        y_host = host[3]
+        slot = 2
+
+        def frame(st, slot):
+            out = Q.SimState(q_l=host[slot], q_prev=st.q_l, y=y_host)
+            nxt, _ = Q.simulate_frame(system, st, cfg, out=out)
+            used = {id(nxt.q_l), id(nxt.q_prev)}
+            free = next(i for i in range(3) if id(host[i]) not in used)
+            return nxt, free
+
         for _ in range(min(args.warmup, 2)):
-            st, _ = Q.simulate_frame(system, st, cfg)
+            st, slot = frame(st, slot)
         if world > 1:
             torch.distributed.barrier()
         t = time.perf_counter()
         for _ in range(args.steps):
-            st, _ = Q.simulate_frame(system, st, cfg)
+            st, slot = frame(st, slot)
         dt = time.perf_counter() - t
         if world > 1:
             tt = torch.tensor([dt], device="cuda", dtype=torch.float64)

@@ -12,7 +12,8 @@
  *     returns a message for the calling thread's last failure;
  *   - arrays are C-contiguous row-major, float64 unless stated (int32 indices);
  *   - `mem` selects where caller buffers live: QN_MEM_HOST (pageable or pinned
- *     host memory; the library stages through its own pinned buffers) or
+ *     host memory; pageable inputs are staged through the library's own
+ *     pinned buffer, page-locked ones are copied by DMA directly) or
  *     QN_MEM_DEVICE (device pointers on the current CUDA device);
  *   - `stream` is a cudaStream_t (NULL = the library's own stream); every call
  *     is stream-ordered and the call returns after the stream work completes

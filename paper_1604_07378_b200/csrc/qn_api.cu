@@ -29,6 +29,7 @@ int launch_finish(qn_system* S, cudaStream_t st);
 int build_graph(qn_system* S);
 int prepare_kernels(qn_system* S);
 int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st);
+int launch_solve_timing(qn_system* S, cudaStream_t st);
 __global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
                                int zero_fixed, double* part);
 __global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V);
@@ -592,7 +593,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       (rc = sys_alloc(S, &v.ctl, (size_t)ni)) || (rc = sys_alloc(S, &S->d_cfg, 1)) ||
       (rc = sys_alloc(S, &v.active, 1)) || (rc = sys_alloc(S, &v.passes, 1)) ||
       (rc = sys_alloc(S, &S->d_targets, (size_t)ni * std::max<int64_t>(d->n_fixed, 1) * 3)) ||
-      (rc = sys_alloc(S, &S->d_part_plain, (size_t)std::max(v.nblk_t, v.nblk_v) * 2)))
+      (rc = sys_alloc(S, &S->d_part_plain, (size_t)std::max((int64_t)v.nblk_t * v.n_inst, (int64_t)v.nblk_v) * 2)))
     return fail(rc);
   v.cfg = S->d_cfg;
   v.targets = S->d_targets;
@@ -684,7 +685,14 @@ int qn_system_last_frame_cg_iterations(qn_system* S, int64_t* iters) {
 
 static int stage_in(qn_system* S, double* dst, const double* src, size_t count, int32_t mem, cudaStream_t st) {
   if (mem == QN_MEM_DEVICE) return to_device(dst, src, count, mem, st);
-  // pinned staging: copy the caller's (possibly pageable) buffer first
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+    // caller's buffer is page-locked: one stream-ordered DMA, no staging copy
+    QN_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, st));
+    return QN_OK;
+  }
+  (void)cudaGetLastError();
+  // pageable: copy into the library's pinned staging buffer first
   QN_REQUIRE(count * sizeof(double) <= S->h_stage_bytes, QN_ERR_ARG, "stage: too large");
   QN_CUDA(cudaStreamSynchronize(st));
   std::memcpy(S->h_stage, src, count * sizeof(double));
@@ -934,12 +942,11 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
   int rc;
   auto launch = [&]() -> int {
     if (kernel == 0) {  // per-tet pass (F, SVD, VL energy, PK1 corner forces) at the resident q_l
-      int r = launch_tet_plain(S, v.q_l, 0, -1, S->d_part_plain, st);
+      int r = launch_tet_plain(S, v.q_l, -1, -1, S->d_part_plain, st);  // every instance
       if (r) return r;
-    } else {  // forward + backward supernodal solves with 3 RHS (instance 0)
+    } else {  // forward + backward supernodal solves with 3 RHS, every instance
       QN_REQUIRE(S->factor, QN_ERR_UNSUPPORTED, "time_kernel: no factor (PCG system)");
-      QN_CUDA(cudaMemcpyAsync(S->factor->d_io, v.q_l, S->n_free * 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      int r = factor_solve_plain(S->factor, 0, st);
+      int r = launch_solve_timing(S, st);
       if (r) return r;
     }
     return QN_OK;

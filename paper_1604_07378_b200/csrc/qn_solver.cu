@@ -378,6 +378,28 @@ struct SolverIO {
   }
 };
 
+// stand-alone timing of the solve kernels (qn_system_time_kernel): every
+// instance, right-hand side = the resident q_l, result into the R0 scratch
+struct TimingIO {
+  SysView v;
+  __device__ bool active(int) const { return true; }
+  __device__ void rhs(int b, int row, double (&q)[3]) const {
+    const double* x = v.q_l + inst_off(v, b) + (size_t)v.fact_vtx[row] * 3;
+    q[0] = x[0];
+    q[1] = x[1];
+    q[2] = x[2];
+  }
+  __device__ double* dest(int b, int row) const { return v.R0 + inst_off(v, b) + (size_t)v.fact_vtx[row] * 3; }
+  __device__ void store(int b, int row, const double (&x)[3]) const {
+    double* r = dest(b, row);
+    r[0] = x[0];
+    r[1] = x[1];
+    r[2] = x[2];
+  }
+};
+
+int launch_solve_timing(qn_system* S, cudaStream_t st) { return launch_solve(S->factor, TimingIO{S->v}, st); }
+
 // <t_i, r0> and the eta recursion (solvers.py:147-150)
 template <int M>
 __global__ void __launch_bounds__(kVT) k_eta(SysView v) {
@@ -659,16 +681,22 @@ __global__ void k_finish(SysView v) {
 // seam kernels (objective / gradient / element groups / SVD / material)
 
 template <bool kSm>
-__global__ void __launch_bounds__(kTT) k_tet_plain(SysView v, const double* x, int b, int mat_sel,
-                                                  double* part) {
+__global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet_plain(SysView v, const double* x, int b, int mat_sel,
+                                                                   double* part) {
+  // b < 0: every instance (blockIdx.y), x and part strided per instance (timing)
+  const int bb = b < 0 ? (int)blockIdx.y : b;
+  if (b < 0) {
+    x += inst_off(v, bb);
+    part += (size_t)bb * v.nblk_t;
+  }
   __shared__ double red[32];
   __shared__ qn_material smat[kMatSmem];
   __shared__ double fsm[kTT * kFStride];
   double e[1] = {0.0};
   if (v.mt > 0) {
-    const qn_material* mats = stage_materials<kSm>(v, b, smat);
-    e[0] = tet_thread(v, x, b, blockIdx.x * blockDim.x + threadIdx.x, mats, mat_sel, fsm);
-    store_forces(v, b, fsm);
+    const qn_material* mats = stage_materials<kSm>(v, bb, smat);
+    e[0] = tet_thread(v, x, bb, blockIdx.x * blockDim.x + threadIdx.x, mats, mat_sel, fsm);
+    store_forces(v, bb, fsm);
   }
   block_sum<1>(e, red);
   if (threadIdx.x == 0) part[blockIdx.x] = e[0];
@@ -1067,10 +1095,11 @@ int launch_body(qn_system* S, cudaStream_t st) {
 
 int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st) {
   const SysView& v = S->v;
+  const dim3 g(v.nblk_t, b < 0 ? v.n_inst : 1);
   if (v.n_mat <= kMatSmem) {
-    k_tet_plain<true><<<v.nblk_t, kTT, 0, st>>>(v, x, b, mat_sel, part);
+    k_tet_plain<true><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
   } else {
-    k_tet_plain<false><<<v.nblk_t, kTT, 0, st>>>(v, x, b, mat_sel, part);
+    k_tet_plain<false><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
   }
   QN_CHECK_LAUNCH();
   return QN_OK;
@@ -1090,7 +1119,11 @@ int launch_finish(qn_system* S, cudaStream_t st) {
   return QN_OK;
 }
 
-int prepare_kernels(qn_system* S) { return S->factor ? prepare_solve_kernels<SolverIO>(S->factor) : QN_OK; }
+int prepare_kernels(qn_system* S) {
+  if (!S->factor) return QN_OK;
+  const int rc = prepare_solve_kernels<SolverIO>(S->factor);
+  return rc ? rc : prepare_solve_kernels<TimingIO>(S->factor);
+}
 
 int build_graph(qn_system* S) {
   cudaStream_t st = S->stream;

@@ -110,14 +110,10 @@ class _RecordBuffers:
                                   _lib.ptr(self.ms), _lib.ptr(self.status))
 
     def records(self):
-        out = []
-        for b in range(self.g0.size):
-            out.append(ConvergenceRecord(g0=float(self.g0[b]), g=[float(v) for v in self.g[b]],
-                                         ls_trials=[int(v) for v in self.trials[b]],
-                                         alphas=[float(v) for v in self.alphas[b]],
-                                         cum_ms=[float(v) for v in self.ms[b]],
-                                         stagnated=bool(self.status[b] & 1)))
-        return out
+        g0, g, tr = self.g0.tolist(), self.g.tolist(), self.trials.tolist()
+        al, ms, stg = self.alphas.tolist(), self.ms.tolist(), (self.status & 1).astype(bool).tolist()
+        return [ConvergenceRecord(g0=g0[b], g=g[b], ls_trials=tr[b], alphas=al[b], cum_ms=ms[b], stagnated=stg[b])
+                for b in range(len(g0))]
 
     def raise_on_error(self):
         bad = np.nonzero(self.status & 2)[0]
@@ -125,9 +121,12 @@ class _RecordBuffers:
             raise SolverError(f"line search requires a descent direction (instance {int(bad[0])})")
 
 
-def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fixed_targets=None):
+def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fixed_targets=None,
+                   out: SimState | None = None):
     """Advance one frame; returns (next_state, ConvergenceRecord) — a list of
-    records for batch systems (solvers.py:260-352)."""
+    records for batch systems (solvers.py:260-352).  `out` (optional, not in
+    the reference signature): a SimState whose q_l / y arrays (float64,
+    C-contiguous, e.g. page-locked) receive x and y instead of new arrays."""
     if system.colliders:
         raise NotImplementedError("colliders are outside the B200 hot path")
     cfg = config.to_c()
@@ -137,8 +136,15 @@ def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fix
     tg = None
     if fixed_targets is not None and system.fixed.size:
         tg = _lib.f64(np.broadcast_to(fixed_targets, (system.n_inst, system.fixed.size, 3)))
-    x = np.empty(shape)
-    y = np.empty(shape)
+    if out is not None:
+        x, y = out.q_l, out.y
+        for a in (x, y):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                    and a.size == int(np.prod(shape))):
+                raise ValueError("simulate_frame: out.q_l / out.y must be C-contiguous float64 of the state's size")
+    else:
+        x = np.empty(shape)
+        y = np.empty(shape)
     rb = _RecordBuffers(system.n_inst, config.iterations)
     rc = _lib.load().qn_simulate_frame(system._h, C.byref(cfg), _lib.ptr(q_l), _lib.ptr(q_prev), _lib.ptr(tg),
                                        _lib.ptr(x), _lib.ptr(y), C.byref(rb.c), _lib.QN_MEM_HOST, None)

@@ -384,3 +384,23 @@ def test_resident_run_matches_stateless():
         assert recs[0].g == res[f][1].g
     np.testing.assert_array_equal(run.state().q_l, res[-1][0])
     assert run.last_ms > 0 and run.last_passes >= 10
+
+
+@pytest.mark.gpu
+def test_pinned_out_buffers_bitwise_equal():
+    import torch
+    sc = scenes.c1(frames=2)
+    s1 = build(sc)
+    res = run_gpu(s1, sc, 2)
+    s2 = build(sc)
+    keep = [torch.empty(np.asarray(sc.q_l).shape, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    h = [k.numpy() for k in keep]
+    h[0][...] = sc.q_l
+    h[1][...] = sc.q_prev
+    st = Q.SimState(q_l=h[0], q_prev=h[1])
+    for f, slot in enumerate((2, 1)):
+        st, rec = Q.simulate_frame(s2, st, Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m), out=Q.SimState(q_l=h[slot], q_prev=None, y=h[3]))
+        assert st.q_l is h[slot]
+        np.testing.assert_array_equal(st.q_l, res[f][0])
+    with pytest.raises(ValueError):
+        Q.simulate_frame(s2, st, Q.SolverConfig(kind="lbfgs"), out=Q.SimState(q_l=np.zeros(3), q_prev=None, y=h[3]))

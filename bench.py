@@ -130,7 +130,7 @@ def frame_timeline(system, run, stream):
     import ctypes as C
     from paper_1604_07378_b200 import _lib
     lib = _lib.load()
-    passes, kernels = 512, 4
+    passes, kernels = 512, 6
     buf = np.zeros(passes * kernels * 2, dtype=np.uint64)
     try:
         _lib.check(lib.qn_system_set_timeline(system._h, 1))

@@ -114,10 +114,10 @@ int qn_factor_solve(qn_factor* f, int64_t batch, const double* B, double* X, int
                     void* stream);
 int qn_factor_destroy(qn_factor* f);
 /* diagnostics: one traced solve (instance 0, current staging RHS); stamps =
- * globaltimer ns at (start, dependencies ready), then SM clock64 at (ready,
- * data staged, computed, published) per forward then backward work item;
- * tasks = {supernode, lo, hi, 0} per forward then backward task.
- * Sizes: 6 (n_ftask + n_btask) nbatch and 4 (n_ftask + n_btask). */
+ * globaltimer ns at (ticket taken, staging issued, dependencies ready), then
+ * SM clock64 at (ready, data staged, computed, published) per forward then
+ * backward work item; tasks = {supernode, lo, hi, 0} per forward then
+ * backward task.  Sizes: 7 (n_ftask + n_btask) nbatch and 4 (n_ftask + n_btask). */
 int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask);
 int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks);
 
@@ -221,11 +221,14 @@ int qn_system_last_frame_ms(qn_system* s, double* ms);
 /* body passes (line-search trials + re-evaluations) of the last frame */
 int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
 /* diagnostics: per body pass, globaltimer ns at the entry of block 0 and at
- * the end of the finalising block of k_grad, k_eta, k_vec (entry only) and
- * k_tet; out = [512 passes][4 kernels][2] (0 = not reached).  Enabling
- * rebuilds the frame graph. */
+ * the end of the finalising block / last CTA of k_grad, k_eta, k_vec (entry
+ * only), k_tet, sptrsv_forward, sptrsv_backward; out = [512 passes][6
+ * kernels][2] (0 = not reached).  Enabling rebuilds the frame graph. */
 int qn_system_set_timeline(qn_system* s, int32_t enable);
 int qn_system_timeline(qn_system* s, uint64_t* out, int64_t cap);
+/* diagnostics: task trace of the last in-graph solve (direct solver, timeline
+ * enabled), same layout as qn_factor_trace_solve */
+int qn_system_solve_trace(qn_system* s, uint64_t* stamps, int32_t* tasks);
 /* PCG mode: conjugate-gradient iterations of the last frame, summed over
  * instances (0 in direct mode) */
 int qn_system_last_frame_cg_iterations(qn_system* s, int64_t* iters);

@@ -119,6 +119,8 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
   if ((rc = dev_upload(&f->d_hlev_ptr, f->hlev_ptr.data(), f->hlev_ptr.size()))) return rc;
+  if (!f->fdesc.empty() && (rc = dev_upload(&f->d_fdesc, f->fdesc.data(), f->fdesc.size()))) return rc;
+  if (!f->fblob.empty() && (rc = dev_upload(&f->d_fblob, f->fblob.data(), f->fblob.size()))) return rc;
   if ((rc = dev_upload(&f->d_hlev_sup, f->hlev_sup.data(), f->hlev_sup.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
@@ -163,7 +165,8 @@ void factor_free_device(qn_factor* f) {
                   f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
                   f->d_fdep_idx, f->d_sinv,       f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
-                  f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup};
+                  f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
+                  f->d_fdesc,   f->d_fblob};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;
@@ -347,9 +350,22 @@ int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask
   return QN_OK;
 }
 
+int qn_system_solve_trace(qn_system* S, uint64_t* stamps, int32_t* tasks) {
+  QN_REQUIRE(S && stamps && tasks, QN_ERR_ARG, "solve_trace: null");
+  qn_factor* f = S->factor;
+  QN_REQUIRE(f && f->d_trace, QN_ERR_ARG, "solve_trace: no factor or timeline not enabled");
+  const size_t nf = f->ftask.size(), nb = f->btask.size(), items = (nf + nb) * (size_t)f->nbatch;
+  QN_CUDA(cudaDeviceSynchronize());
+  QN_CUDA(cudaMemcpy(stamps, f->d_trace, qn::kTraceSlots * items * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  std::memcpy(tasks, f->ftask.data(), nf * sizeof(int4));
+  std::memcpy(tasks + 4 * nf, f->btask.data(), nb * sizeof(int4));
+  return QN_OK;
+}
+
 int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks) {
   QN_REQUIRE(f && stamps && tasks, QN_ERR_ARG, "trace: null");
   const size_t nf = f->ftask.size(), nb = f->btask.size(), items = (nf + nb) * (size_t)f->nbatch;
+  QN_REQUIRE(!f->d_trace, QN_ERR_ARG, "trace: a system timeline is active");
   int rc = dev_alloc(&f->d_trace, qn::kTraceSlots * items);
   if (rc) return rc;
   rc = factor_solve_plain(f, 0, 0);
@@ -653,6 +669,20 @@ int qn_system_set_timeline(qn_system* S, int32_t enable) {
     if (rc) return rc;
   } else if (!enable) {
     S->v.ktl = nullptr;  // buffer stays owned by the system
+  }
+  if (S->factor) {
+    qn_factor* f = S->factor;
+    f->d_ktl = S->v.ktl;
+    f->d_passes = S->v.passes;
+    // the in-graph solves also record their task trace (last solve of a frame wins)
+    const size_t items = (f->ftask.size() + f->btask.size()) * (size_t)f->nbatch;
+    if (enable && !f->d_trace && items > 0) {
+      int rc = dev_alloc(&f->d_trace, qn::kTraceSlots * items);
+      if (rc) return rc;
+    } else if (!enable && f->d_trace) {
+      cudaFree(f->d_trace);
+      f->d_trace = nullptr;
+    }
   }
   if (S->exec) {  // kernels capture the view by value: rebuild the graph
     cudaGraphExecDestroy(S->exec);

@@ -10,6 +10,7 @@
 //      mat-vec (no sequential triangular sweeps on the GPU).
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -639,6 +640,41 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
         const int32_t c = f->child_idx[q];
         for (int32_t t = 0; t < f->fcount[c]; ++t) f->fdep_idx[w++] = f->ffirst[c] + t;
       }
+    }
+    // forward task descriptors + their relative extend-add lists
+    f->fdesc.clear();
+    f->fblob.clear();
+    for (const int4& t : f->ftask) {
+      const int32_t s = t.x, lo = t.y, hi = t.z;
+      const int32_t c0 = f->sup_col[s], nc = f->sup_col[s + 1] - c0;
+      const int64_t R0 = f->sup_row_ptr[s];
+      const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - R0);
+      const int32_t blo = std::max(lo, nc);
+      const int64_t ct0 = f->cptr[R0], ct1 = f->cptr[R0 + nc];
+      const int64_t cb0 = f->cptr[R0 + blo], cb1 = blo < hi ? f->cptr[R0 + hi] : cb0;
+      qn_fdesc d{};
+      d.zoff = f->sup_val_ptr[s] + lo;
+      d.lo = lo;
+      d.hi = hi;
+      d.rg = t.w;
+      d.c0 = c0;
+      d.nc = nc;
+      d.nr = nr;
+      d.blo = blo;
+      d.ntop = (int32_t)(ct1 - ct0);
+      d.nbot = (int32_t)(cb1 - cb0);
+      d.upd0 = (int32_t)f->sup_upd_ptr[s];
+      d.dep0 = f->fdep_ptr[s];
+      d.dep1 = f->fdep_ptr[s + 1];
+      QN_REQUIRE(f->fblob.size() < (size_t)INT32_MAX && f->nupd < INT32_MAX, QN_ERR_UNSUPPORTED,
+                 "factor: solve lists exceed 32-bit offsets");
+      d.blob = (int32_t)f->fblob.size();
+      for (int32_t p = 0; p <= nc; ++p) f->fblob.push_back((int32_t)(f->cptr[R0 + p] - ct0));
+      if (blo < hi)
+        for (int32_t p = 0; p <= hi - blo; ++p) f->fblob.push_back((int32_t)(f->cptr[R0 + blo + p] - cb0));
+      for (int64_t q = ct0; q < ct1; ++q) f->fblob.push_back(f->cidx[q]);
+      for (int64_t q = cb0; q < cb1; ++q) f->fblob.push_back(f->cidx[q]);
+      f->fdesc.push_back(d);
     }
     // level lists for the batched per-instance solve: forward by height
     // (leaves first), backward by depth (root first); supernodes of one level

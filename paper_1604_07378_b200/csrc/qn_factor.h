@@ -13,6 +13,17 @@
 
 #include "qnsim_b200.h"
 
+// Forward solve task descriptor: everything a task needs before its first
+// dependent load, in one 64-byte record (one round trip instead of a chain
+// task -> supernode -> row pointers -> extend-add lists).
+struct alignas(16) qn_fdesc {
+  int64_t zoff;                 // Z tile origin: sup_val_ptr[s] + lo
+  int32_t lo, hi, rg, c0;       // rows [lo, hi), row groups, first column
+  int32_t nc, nr, blo, ntop;    // supernode shape, first bottom row, #top list entries
+  int32_t nbot, upd0, dep0, dep1;  // #bottom list entries, update rows offset, fdep range
+  int32_t blob, pad;            // offset of [sp_top | sp_bot | si_top | si_bot] in fblob
+};
+
 struct qn_factor {
   // ---- symbolic (host) ----
   int64_t n = 0, nnz_a = 0, nbatch = 1;
@@ -34,6 +45,8 @@ struct qn_factor {
   std::vector<int32_t> fcount, bcount;  // tasks per supernode
   std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
   std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
+  std::vector<qn_fdesc> fdesc;              // per forward task
+  std::vector<int32_t> fblob;               // per-task relative extend-add lists
   std::vector<int32_t> hlev_ptr, hlev_sup;  // supernodes grouped by height (batched forward levels)
   std::vector<int32_t> dlev_ptr, dlev_sup;  // supernodes grouped by depth (batched backward levels)
   // dense top: the supernodes within the top levels of the tree (K columns)
@@ -75,6 +88,8 @@ struct qn_factor {
   int32_t* d_bcount = nullptr;
   int32_t* d_fdep_ptr = nullptr;
   int32_t* d_fdep_idx = nullptr;
+  qn_fdesc* d_fdesc = nullptr;
+  int32_t* d_fblob = nullptr;
   int32_t* d_hlev_ptr = nullptr;
   int32_t* d_hlev_sup = nullptr;
   int32_t* d_dlev_ptr = nullptr;
@@ -88,6 +103,8 @@ struct qn_factor {
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
   unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)
+  unsigned long long* d_ktl = nullptr;    // diagnostics only (qn_system_timeline; owned by the system)
+  const unsigned long long* d_passes = nullptr;
   int smem_f = 0, smem_b = 0;     // dynamic shared memory of the forward / backward solve kernels
   int grid_f = 0, grid_b = 0;     // persistent solve grids (co-resident CTAs)
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)

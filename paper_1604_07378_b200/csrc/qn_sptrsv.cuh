@@ -46,6 +46,8 @@ struct FactorView {
   const int32_t* bcount;
   const int32_t* fdep_ptr;  // forward: task ids of all children's tasks
   const int32_t* fdep_idx;
+  const qn_fdesc* fdesc;     // forward task descriptors
+  const int32_t* fblob;      // forward tasks' relative extend-add lists
   const int32_t* hlev_ptr;   // batched: supernodes by height (forward levels)
   const int32_t* hlev_sup;
   const int32_t* dlev_ptr;   // batched: supernodes by depth (backward levels)
@@ -63,6 +65,8 @@ struct FactorView {
   const int32_t* tg_ptr;
   const int32_t* tg_idx;
   double* gtop;              // [nbatch][K][3]
+  unsigned long long* ktl;   // diagnostics timeline (qn_system_timeline) or null
+  const unsigned long long* passes;
 };
 
 inline FactorView factor_view(const qn_factor* f) {
@@ -97,6 +101,8 @@ inline FactorView factor_view(const qn_factor* f) {
   v.bcount = f->d_bcount;
   v.fdep_ptr = f->d_fdep_ptr;
   v.fdep_idx = f->d_fdep_idx;
+  v.fdesc = f->d_fdesc;
+  v.fblob = f->d_fblob;
   v.vals = f->d_vals;
   v.y = f->d_y;
   v.x = f->d_x;
@@ -110,13 +116,15 @@ inline FactorView factor_view(const qn_factor* f) {
   v.tg_ptr = f->d_tg_ptr;
   v.tg_idx = f->d_tg_idx;
   v.gtop = f->d_gtop;
+  v.ktl = f->d_ktl;
+  v.passes = f->d_passes;
   return v;
 }
 
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kStageIdx = 2048;  // int32 index slots staged in shared memory per task
-constexpr int kTraceSlots = 6;   // globaltimer start, ready; clock64 ready, data staged, computed, published
+constexpr int kTraceSlots = 7;   // globaltimer ticket, staged, ready; clock64 ready, data staged, computed, published
 constexpr int kBwdCols = (int)kBwdTaskCols;  // max columns of a backward task
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -128,6 +136,14 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ __forceinline__ void trace_mark(unsigned long long* trace, size_t slot) {
   if (trace && threadIdx.x == 0) trace[slot] = gtime();
 }
+// frame timeline (kid 4 = forward, 5 = backward), per body pass
+__device__ __forceinline__ void solve_tl(const FactorView& F, int kid, int slot) {
+  if (F.ktl) {
+    const unsigned long long p = *((volatile const unsigned long long*)F.passes);
+    if (p < (unsigned long long)kTimelinePasses) F.ktl[(p * kTimelineKernels + kid) * 2 + slot] = gtime();
+  }
+}
+
 // SM cycle counter (phases inside one task run on one SM)
 __device__ __forceinline__ void trace_clock(unsigned long long* trace, size_t slot) {
   if (trace && threadIdx.x == 0) trace[slot] = (unsigned long long)clock64();
@@ -238,11 +254,12 @@ __device__ __forceinline__ int next_ticket(unsigned* sched, int* s_item) {
   return *s_item;
 }
 
-__device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch) {
+__device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const FactorView& F, int kid) {
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned e = atomicAdd(&sched[1], 1u);
     if (e == gridDim.x - 1) {  // last CTA out: reset for the next launch
+      solve_tl(F, kid, 1);
       sched[0] = 0;
       sched[1] = 0;
       __threadfence();
@@ -263,6 +280,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
   __shared__ unsigned s_epoch;
   unsigned* sched = F.sched;
   if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* zt = sm;
@@ -271,13 +289,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
     if (item >= total) break;
     const unsigned epoch = s_epoch;
     const int tid = item / F.nbatch;
-    const int4 task = F.ftask[tid];
     const int b = item % F.nbatch;
-    const int s = task.x, lo = task.y, hi = task.z, rg = task.w;  // rg = row groups of 32
     if (!io.active(b)) continue;
-    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
-    const int64_t R0 = F.sup_row_ptr[s];
-    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
+    const qn_fdesc d = F.fdesc[tid];
+    const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
     const int R = hi - lo;
     const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
     double* f = sm + kTaskEntries;
@@ -286,29 +302,23 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
     const double* ub = F.u + (size_t)b * F.nupd * 3;
     // ---- stage everything that does not depend on the children ----
     {  // Z tile rows [lo, hi) x k [0, kmax) -> zt[k * R + (r - lo)]
-      const double* Zg = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s] + lo;
+      const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
       const int cnt = R * kmax;
       for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         const int k = e / R, rr = e - k * R;
         cp_async8(zt + e, Zg + (int64_t)k * nr + rr);
       }
     }
-    const int blo = max(lo, nc);
-    const int64_t ct0 = F.cptr[R0], ct1 = F.cptr[R0 + nc];
-    const int64_t cb0 = F.cptr[R0 + blo], cb1 = blo < hi ? F.cptr[R0 + hi] : cb0;
-    const int ntop = (int)(ct1 - ct0), nbot = (int)(cb1 - cb0);
-    const int nptr_top = nc + 1, nptr_bot = blo < hi ? hi - blo + 1 : 0;
-    const bool staged = nptr_top + nptr_bot + ntop + nbot <= kStageIdx;
-    int* sp_top = sidx;
-    int* sp_bot = sp_top + nptr_top;
-    int* si_top = sp_bot + nptr_bot;
-    int* si_bot = si_top + ntop;
-    if (staged) {
-      for (int p = threadIdx.x; p < nptr_top; p += blockDim.x) sp_top[p] = (int)(F.cptr[R0 + p] - ct0);
-      for (int p = threadIdx.x; p < nptr_bot; p += blockDim.x) sp_bot[p] = (int)(F.cptr[R0 + blo + p] - cb0);
-      for (int q = threadIdx.x; q < ntop; q += blockDim.x) si_top[q] = F.cidx[ct0 + q];
-      for (int q = threadIdx.x; q < nbot; q += blockDim.x) si_bot[q] = F.cidx[cb0 + q];
-    }
+    const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
+    const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
+    const int* gblob = F.fblob + d.blob;
+    const bool staged = nblob <= kStageIdx;
+    if (staged)
+      for (int q = threadIdx.x; q < nblob; q += blockDim.x) sidx[q] = __ldg(gblob + q);
+    const int* sp_top = staged ? sidx : gblob;  // relative extend-add lists: [sp_top | sp_bot | si_top | si_bot]
+    const int* sp_bot = sp_top + nc + 1;
+    const int* si_top = sp_bot + nptr_bot;
+    const int* si_bot = si_top + d.ntop;
     for (int p = threadIdx.x; p < nc; p += blockDim.x) {
       double v[3];
       io.rhs(b, c0 + p, v);
@@ -316,18 +326,15 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
       f[3 * p + 1] = v[1];
       f[3 * p + 2] = v[2];
     }
-    trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
-    const int d0 = F.fdep_ptr[s], d1 = F.fdep_ptr[s + 1];
-    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d0, d1 - d0, epoch, F.sched);
     trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 2);
+    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 2);
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
     // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
     for (int p = threadIdx.x; p < nc; p += blockDim.x) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      const int q0 = staged ? sp_top[p] : (int)(F.cptr[R0 + p] - ct0);
-      const int q1 = staged ? sp_top[p + 1] : (int)(F.cptr[R0 + p + 1] - ct0);
-      for (int q = q0; q < q1; ++q) {
-        const double* uc = ub + 3 * (size_t)(staged ? si_top[q] : F.cidx[ct0 + q]);
+      for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
+        const double* uc = ub + 3 * (size_t)si_top[q];
         a0 += __ldcg(uc);
         a1 += __ldcg(uc + 1);
         a2 += __ldcg(uc + 2);
@@ -340,10 +347,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
     double e0 = 0.0, e1 = 0.0, e2 = 0.0;
     if (threadIdx.x < R && rr >= nc) {
       const int pr = rr - blo;
-      const int q0 = staged ? sp_bot[pr] : (int)(F.cptr[R0 + rr] - cb0);
-      const int q1 = staged ? sp_bot[pr + 1] : (int)(F.cptr[R0 + rr + 1] - cb0);
-      for (int q = q0; q < q1; ++q) {
-        const double* uc = ub + 3 * (size_t)(staged ? si_bot[q] : F.cidx[cb0 + q]);
+      for (int q = sp_bot[pr]; q < sp_bot[pr + 1]; ++q) {
+        const double* uc = ub + 3 * (size_t)si_bot[q];
         e0 += __ldcg(uc);
         e1 += __ldcg(uc + 1);
         e2 += __ldcg(uc + 2);
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
     }
     cp_async_wait_all();
     __syncthreads();
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
     // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
     const int ks = kSolveWarps / rg;
     const int g = warp / ks, j = warp % ks;
@@ -387,17 +392,17 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
         yg[1] = v1;
         yg[2] = v2;
       } else {
-        double* us = F.u + ((size_t)b * F.nupd + F.sup_upd_ptr[s] + (rr - nc)) * 3;
+        double* us = F.u + ((size_t)b * F.nupd + d.upd0 + (rr - nc)) * 3;
         __stcg(us + 0, e0 + v0);
         __stcg(us + 1, e1 + v1);
         __stcg(us + 2, e2 + v2);
       }
     }
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
-    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
     trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
+    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
+    trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
   }
-  cta_exit(sched, s_epoch);
+  cta_exit(sched, s_epoch, F, 4);
 }
 
 template <class IO>
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   __shared__ unsigned s_epoch;
   unsigned* sched = F.sched + 3;
   if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 5, 0);
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* zt = sm;
@@ -420,6 +426,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     const int b = item % F.nbatch;
     const int s = task.x, k0 = task.y, k1 = task.z;
     if (!io.active(b)) continue;
+    trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
     const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
     const int64_t R0 = F.sup_row_ptr[s];
     const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
       for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
     for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
     const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
-    trace_mark(F.trace, tb + 0);
+    trace_mark(F.trace, tb + 1);
     cp_async_wait_all();
     __syncthreads();
     // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
@@ -469,8 +476,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     if (p >= 0)
       wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, F.bfirst[p], F.bcount[p], epoch,
                       F.sched);
-    trace_mark(F.trace, tb + 1);
-    trace_clock(F.trace, tb + 2);
+    trace_mark(F.trace, tb + 2);
+    trace_clock(F.trace, tb + 3);
     const double* xg = F.x + (size_t)b * F.n * 3;
     for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) {
       const int row = staged ? srow[q] : F.sup_rows[R0 + nc + q];
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
       w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
     }
     __syncthreads();
-    trace_clock(F.trace, tb + 3);
+    trace_clock(F.trace, tb + 4);
     // ---- the -x_below part, plus the staged y_J part ----
     for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
       double a[3];
@@ -499,11 +506,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
         d[2] = v[2];
       }
     }
-    trace_clock(F.trace, tb + 4);
-    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
     trace_clock(F.trace, tb + 5);
+    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
+    trace_clock(F.trace, tb + 6);
   }
-  cta_exit(sched, s_epoch);
+  cta_exit(sched, s_epoch, F, 5);
 }
 
 // ---- dense top: g_T = b_T - (updates of the subtrees below T); x_T = S^-1 g_T ----

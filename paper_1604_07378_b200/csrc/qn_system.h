@@ -48,9 +48,6 @@ struct InstCtl {
 constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 4;
 constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
 
-// diagnostics timeline (qn_system_timeline): entry of block 0 and end of the
-// finalising block of the body kernels, per body pass
-constexpr int kTimelinePasses = 512, kTimelineKernels = 4;  // k_grad, k_eta, k_vec, k_tet
 
 struct PcgCtl {
   double rz[3], alpha[3], beta[3], bb[3], rr[3];

@@ -31,6 +31,29 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
   std::vector<double> y(n * 3), x(n * 3), u(std::max<int64_t>(f.nupd, 1) * 3);
   std::vector<int> done_f(f.nsup, 0), done_b(f.nsup, 0);
   // forward tasks in ticket order; every dependency must already be complete
+  // forward descriptors / relative lists must describe exactly the cptr/cidx structure
+  if (f.fdesc.size() != f.ftask.size()) return 93;
+  for (size_t i = 0; i < f.ftask.size(); ++i) {
+    const int4& t = f.ftask[i];
+    const qn_fdesc& d = f.fdesc[i];
+    const int s = t.x;
+    const int64_t R0 = f.sup_row_ptr[s];
+    const int nc = f.sup_col[s + 1] - f.sup_col[s];
+    if (d.lo != t.y || d.hi != t.z || d.nc != nc || d.c0 != f.sup_col[s] || d.zoff != f.sup_val_ptr[s] + t.y ||
+        d.upd0 != f.sup_upd_ptr[s] || d.dep0 != f.fdep_ptr[s] || d.dep1 != f.fdep_ptr[s + 1])
+      return 93;
+    const int32_t* sp_top = f.fblob.data() + d.blob;
+    const int nptr_bot = d.blo < d.hi ? d.hi - d.blo + 1 : 0;
+    const int32_t* sp_bot = sp_top + nc + 1;
+    const int32_t* si_top = sp_bot + nptr_bot;
+    const int32_t* si_bot = si_top + d.ntop;
+    for (int p = 0; p < nc; ++p)
+      for (int q = sp_top[p]; q < sp_top[p + 1]; ++q)
+        if (si_top[q] != f.cidx[f.cptr[R0 + p] + (q - sp_top[p])]) return 93;
+    for (int r = d.blo; r < d.hi; ++r)
+      for (int q = sp_bot[r - d.blo]; q < sp_bot[r - d.blo + 1]; ++q)
+        if (si_bot[q] != f.cidx[f.cptr[R0 + r] + (q - sp_bot[r - d.blo])]) return 93;
+  }
   for (const int4& t : f.ftask) {
     const int s = t.x;
     for (int q = f.child_ptr[s]; q < f.child_ptr[s + 1]; ++q)

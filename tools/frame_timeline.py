@@ -15,7 +15,7 @@ import paper_1604_07378_b200 as Q  # noqa: E402
 from paper_1604_07378_b200 import _lib  # noqa: E402
 from paper_1604_07378_b200.solvers import ResidentRun, SolverConfig  # noqa: E402
 
-PASSES, KERNELS = 512, 4
+PASSES, KERNELS = 512, 6
 
 
 def main(cfg="c2", frames="3"):
@@ -43,6 +43,8 @@ def main(cfg="c2", frames="3"):
         rows.append(((g1 - g0) if g0 and g1 else 0, (e0 - g1) if g1 and e0 else 0, (e1 - e0) if e0 and e1 else 0,
                      (k0 - v0) if v0 else 0, k1 - k0, (t[p + 1, 0, 0] - k1) if p + 1 < npass else 0))
     r = np.array(rows, dtype=np.float64) / 1000.0
+    sv = [(t[p, 4, 0] - t[p, 0, 1], t[p, 4, 1] - t[p, 4, 0], t[p, 5, 0] - t[p, 4, 1], t[p, 5, 1] - t[p, 5, 0],
+           t[p, 1, 0] - t[p, 5, 1]) for p in range(npass) if t[p, 4, 0] and t[p, 5, 1] and t[p, 0, 1] and t[p, 1, 0]]
     full = r[:, 1] > 0  # passes with a direction (grad + solve + eta)
     names = ["grad", "grad_end->eta (solve)", "eta", "vec", "tet", "tet_end->next grad"]
     print(f"{cfg}: {npass} passes in the last frame, {full.sum()} with a solve; "
@@ -50,6 +52,11 @@ def main(cfg="c2", frames="3"):
     for j, n in enumerate(names):
         sel = r[full, j] if j < 3 else r[:, j]
         print(f"  {n:24s} mean {sel.mean():7.2f} us  min {sel.min():7.2f}  max {sel.max():7.2f}")
+    if sv:
+        a = np.array(sv, dtype=np.float64) / 1000.0
+        for j, n in enumerate(["grad end -> fwd entry", "forward", "fwd end -> bwd entry", "backward",
+                               "bwd end -> eta entry"]):
+            print(f"    {n:22s} mean {a[:, j].mean():7.2f} us")
 
 
 if __name__ == "__main__":

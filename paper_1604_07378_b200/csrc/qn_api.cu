@@ -121,6 +121,7 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_hlev_ptr, f->hlev_ptr.data(), f->hlev_ptr.size()))) return rc;
   if (!f->fdesc.empty() && (rc = dev_upload(&f->d_fdesc, f->fdesc.data(), f->fdesc.size()))) return rc;
   if (!f->fblob.empty() && (rc = dev_upload(&f->d_fblob, f->fblob.data(), f->fblob.size()))) return rc;
+  if (!f->bdesc.empty() && (rc = dev_upload(&f->d_bdesc, f->bdesc.data(), f->bdesc.size()))) return rc;
   if ((rc = dev_upload(&f->d_hlev_sup, f->hlev_sup.data(), f->hlev_sup.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
@@ -166,7 +167,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
                   f->d_fdep_idx, f->d_sinv,       f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
-                  f->d_fdesc,   f->d_fblob};
+                  f->d_fdesc,   f->d_fblob,       f->d_bdesc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

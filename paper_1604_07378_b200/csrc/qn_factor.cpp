@@ -676,6 +676,24 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       for (int64_t q = cb0; q < cb1; ++q) f->fblob.push_back(f->cidx[q]);
       f->fdesc.push_back(d);
     }
+    f->bdesc.clear();
+    for (const int4& t : f->btask) {
+      const int32_t s = t.x;
+      const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
+      const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
+      const int32_t p = f->parent[s];
+      qn_bdesc d{};
+      d.zoff = f->sup_val_ptr[s] + (int64_t)t.y * nr;
+      d.rows = f->sup_row_ptr[s];
+      d.k0 = t.y;
+      d.k1 = t.z;
+      d.c0 = f->sup_col[s];
+      d.nc = nc;
+      d.nr = nr;
+      d.wait0 = p >= 0 ? f->bfirst[p] : 0;
+      d.nwait = p >= 0 ? f->bcount[p] : 0;
+      f->bdesc.push_back(d);
+    }
     // level lists for the batched per-instance solve: forward by height
     // (leaves first), backward by depth (root first); supernodes of one level
     // are independent and run on different warps of the instance's CTA

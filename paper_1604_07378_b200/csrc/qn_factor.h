@@ -24,6 +24,14 @@ struct alignas(16) qn_fdesc {
   int32_t blob, pad;            // offset of [sp_top | sp_bot | si_top | si_bot] in fblob
 };
 
+// Backward solve task descriptor (same idea as qn_fdesc).
+struct alignas(16) qn_bdesc {
+  int64_t zoff;                 // column k0 of Z: sup_val_ptr[s] + k0 nr
+  int64_t rows;                 // sup_row_ptr[s] (row ids in sup_rows)
+  int32_t k0, k1, c0, nc;
+  int32_t nr, wait0, nwait, pad;  // parent's backward tasks [wait0, wait0 + nwait)
+};
+
 struct qn_factor {
   // ---- symbolic (host) ----
   int64_t n = 0, nnz_a = 0, nbatch = 1;
@@ -46,6 +54,7 @@ struct qn_factor {
   std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
   std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
   std::vector<qn_fdesc> fdesc;              // per forward task
+  std::vector<qn_bdesc> bdesc;              // per backward task
   std::vector<int32_t> fblob;               // per-task relative extend-add lists
   std::vector<int32_t> hlev_ptr, hlev_sup;  // supernodes grouped by height (batched forward levels)
   std::vector<int32_t> dlev_ptr, dlev_sup;  // supernodes grouped by depth (batched backward levels)
@@ -89,6 +98,7 @@ struct qn_factor {
   int32_t* d_fdep_ptr = nullptr;
   int32_t* d_fdep_idx = nullptr;
   qn_fdesc* d_fdesc = nullptr;
+  qn_bdesc* d_bdesc = nullptr;
   int32_t* d_fblob = nullptr;
   int32_t* d_hlev_ptr = nullptr;
   int32_t* d_hlev_sup = nullptr;

@@ -47,6 +47,7 @@ struct FactorView {
   const int32_t* fdep_ptr;  // forward: task ids of all children's tasks
   const int32_t* fdep_idx;
   const qn_fdesc* fdesc;     // forward task descriptors
+  const qn_bdesc* bdesc;     // backward task descriptors
   const int32_t* fblob;      // forward tasks' relative extend-add lists
   const int32_t* hlev_ptr;   // batched: supernodes by height (forward levels)
   const int32_t* hlev_sup;
@@ -102,6 +103,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.fdep_ptr = f->d_fdep_ptr;
   v.fdep_idx = f->d_fdep_idx;
   v.fdesc = f->d_fdesc;
+  v.bdesc = f->d_bdesc;
   v.fblob = f->d_fblob;
   v.vals = f->d_vals;
   v.y = f->d_y;
@@ -422,28 +424,25 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
     if (item >= total) break;
     const unsigned epoch = s_epoch;
     const int tid = item / F.nbatch;
-    const int4 task = F.btask[tid];
     const int b = item % F.nbatch;
-    const int s = task.x, k0 = task.y, k1 = task.z;
     if (!io.active(b)) continue;
     trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
-    const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
-    const int64_t R0 = F.sup_row_ptr[s];
-    const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+    const qn_bdesc d = F.bdesc[tid];
+    const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
+    const int64_t R0 = d.rows;
     double* w = sm + F.bwd_entries;
     double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
     double** sdst = (double**)(pre + 3 * kBwdCols);  // [kBwdCols] io destination of each column
     int* srow = (int*)(sdst + kBwdCols);
     const bool staged = nr - nc <= kStageIdx;
-    const int p = F.parent[s];
     // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
     {
-      const double* Zg = F.vals + (size_t)b * F.nvals + F.sup_val_ptr[s];
+      const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
       const int cnt = (k1 - k0) * nr;
       for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         const int kk = e / nr, r = e - kk * nr;
         if (r >= k0 + kk)
-          cp_async8(zt + e, Zg + (int64_t)(k0 + kk) * nr + r);
+          cp_async8(zt + e, Zg + e);
         else
           zt[e] = 0.0;
       }
@@ -473,9 +472,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
         pre[3 * (kl + j) + 2] = a[2];
       }
     }
-    if (p >= 0)
-      wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, F.bfirst[p], F.bcount[p], epoch,
-                      F.sched);
+    if (d.nwait > 0)
+      wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, d.wait0, d.nwait, epoch, F.sched);
     trace_mark(F.trace, tb + 2);
     trace_clock(F.trace, tb + 3);
     const double* xg = F.x + (size_t)b * F.n * 3;

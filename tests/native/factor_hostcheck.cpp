@@ -54,6 +54,17 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
       for (int q = sp_bot[r - d.blo]; q < sp_bot[r - d.blo + 1]; ++q)
         if (si_bot[q] != f.cidx[f.cptr[R0 + r] + (q - sp_bot[r - d.blo])]) return 93;
   }
+  if (f.bdesc.size() != f.btask.size()) return 92;
+  for (size_t i = 0; i < f.btask.size(); ++i) {
+    const int4& t = f.btask[i];
+    const qn_bdesc& d = f.bdesc[i];
+    const int s = t.x, p = f.parent[s];
+    const int nr = (int)(f.sup_row_ptr[s + 1] - f.sup_row_ptr[s]);
+    if (d.k0 != t.y || d.k1 != t.z || d.c0 != f.sup_col[s] || d.nr != nr || d.rows != f.sup_row_ptr[s] ||
+        d.zoff != f.sup_val_ptr[s] + (int64_t)t.y * nr || d.nwait != (p >= 0 ? f.bcount[p] : 0) ||
+        (p >= 0 && d.wait0 != f.bfirst[p]))
+      return 92;
+  }
   for (const int4& t : f.ftask) {
     const int s = t.x;
     for (int q = f.child_ptr[s]; q < f.child_ptr[s + 1]; ++q)

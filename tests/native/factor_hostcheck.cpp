@@ -142,3 +142,17 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
   return 0;
 }
 }
+
+// ---- AMG hierarchy (qn_amg.cpp) + host reference PCG (TEST ONLY) ----
+#include "qn_amg.h"
+extern "C" int hc_amg_solve(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,
+                            const double* B, double* X, double tol, int maxit, int64_t* stats) {
+  qn::AmgHierarchy h;
+  int rc = qn::amg_build(n, indptr, indices, values, &h);
+  if (rc) return rc;
+  const int it = qn::amg_pcg_host(h, B, X, tol, maxit);
+  stats[0] = it;
+  stats[1] = (int64_t)h.lv.size();
+  for (size_t l = 0; l < h.lv.size() && l < 6; ++l) stats[2 + l] = h.lv[l].A.n;
+  return 0;
+}

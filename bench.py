@@ -170,7 +170,7 @@ def build_system(sc):
     if sc.batch:
         return Q.build_batch_system(mesh, [from_spec(s) for s in sc.batch_materials], h=sc.h, gravity=sc.gravity,
                                     fixed=sc.fixed)
-    solver = "pcg" if sc.name.startswith("c5") else "direct"  # configs[4]: PCG to 1e-10 (BASELINE.json)
+    solver = "amg" if sc.name.startswith("c5") else "direct"  # configs[4]: (AMG-)PCG to 1e-10 (BASELINE.json)
     return Q.build_system(mesh, from_spec(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed, solver=solver,
                           pcg_tol=1e-10)
 

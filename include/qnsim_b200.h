@@ -162,6 +162,7 @@ typedef struct qn_system_desc {
 
 #define QN_SOLVE_DIRECT 0
 #define QN_SOLVE_PCG 1
+#define QN_SOLVE_AMG 2  /* CG preconditioned by a smoothed-aggregation AMG V(1,1) cycle (single instance) */
 
 typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          */
   int32_t kind;                    /* 0 = pd_qn, 1 = lbfgs (lbfgs_init=system_matrix) */
@@ -232,6 +233,8 @@ int qn_system_solve_trace(qn_system* s, uint64_t* stamps, int32_t* tasks);
 /* PCG mode: conjugate-gradient iterations of the last frame, summed over
  * instances (0 in direct mode) */
 int qn_system_last_frame_cg_iterations(qn_system* s, int64_t* iters);
+/* AMG systems: out = [levels, rows of level 0..levels-1, setup ms]; cap >= 12 */
+int qn_system_amg_info(qn_system* s, int64_t* out, int64_t cap);
 
 /* Stand-alone timing of one hot kernel with CUDA events on `stream` (after a
  * warm-up launch): kernel 0 = per-tet pass at the resident q_l, kernel 1 =

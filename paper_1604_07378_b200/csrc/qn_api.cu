@@ -9,6 +9,7 @@
 #include "qn_common.cuh"
 #include "qn_factor.h"
 #include "qn_sptrsv.cuh"
+#include "qn_amg.h"
 #include "qn_system.h"
 
 namespace qn {
@@ -389,6 +390,12 @@ int qn_factor_destroy(qn_factor* f) {
 }
 
 // ---------------------------------------------------------------------------
+static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
+                       int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
+                       std::vector<double>& sval);
+static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
+                       const double* val, qn::SellDev* out);
+
 int qn_system_create(const qn_system_desc* d, qn_system** out) {
   QN_REQUIRE(d && out, QN_ERR_ARG, "system: null argument");
   *out = nullptr;
@@ -465,7 +472,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   SysView& v = S->v;
   int rc = QN_OK;
   std::vector<int32_t> fact_vtx(S->n_free);
-  const bool pcg = d->solver == QN_SOLVE_PCG;
+  const bool pcg = d->solver == QN_SOLVE_PCG || d->solver == QN_SOLVE_AMG;
   if (!pcg) {
     // factor of A_free (one numeric instance per system instance)
     S->factor = new qn_factor();
@@ -488,30 +495,12 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
         return fail(QN_ERR_NOT_SPD);
       }
     for (int64_t r = 0; r < nf; ++r) fact_vtx[r] = free_ids[r];
-    // SELL-32 copy of the CSR rows (same entry order within a row, zero padding)
     const int64_t nsl = (nf + 31) / 32;
-    std::vector<int64_t> sptr((size_t)nsl + 1, 0);
-    for (int64_t sl = 0; sl < nsl; ++sl) {
-      int64_t w = 0;
-      for (int64_t r = 32 * sl; r < std::min(nf, 32 * sl + 32); ++r) w = std::max(w, d->a_indptr[r + 1] - d->a_indptr[r]);
-      sptr[sl + 1] = sptr[sl] + 32 * w;
-    }
+    std::vector<int64_t> sptr;
+    std::vector<int32_t> scol;
+    std::vector<double> sval;
+    sell_build(nf, nf, d->a_indptr, d->a_indices, d->a_values, ni, nnz, sptr, scol, sval);
     const int64_t snz = sptr[nsl];
-    std::vector<int32_t> scol((size_t)snz);
-    std::vector<double> sval((size_t)ni * snz, 0.0);
-    for (int64_t sl = 0; sl < nsl; ++sl) {
-      const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
-      for (int64_t l = 0; l < 32; ++l) {
-        const int64_t r = 32 * sl + l;
-        const int64_t p0 = r < nf ? d->a_indptr[r] : 0, len = r < nf ? d->a_indptr[r + 1] - p0 : 0;
-        for (int64_t k = 0; k < w; ++k) {
-          const int64_t e = sptr[sl] + 32 * k + l;
-          scol[e] = k < len ? d->a_indices[p0 + k] : (int32_t)std::min(r, nf - 1);
-          if (k < len)
-            for (int64_t b = 0; b < ni; ++b) sval[b * snz + e] = d->a_values[b * nnz + p0 + k];
-        }
-      }
-    }
     int64_t* sp;
     int32_t* sc;
     double *sv, *di;
@@ -524,7 +513,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     v.sell_nnz = snz;
     v.nslice = (int32_t)nsl;
     v.dinv = di;
-    v.pcg = 1;
+    v.pcg = d->solver == QN_SOLVE_AMG ? 2 : 1;
     v.n_free = (int32_t)nf;
     v.nblk_p = div_up(nf, 128);
     int dev = 0, nsm = 148;
@@ -539,9 +528,52 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     if ((rc = sys_alloc(S, &v.px, fv)) || (rc = sys_alloc(S, &v.pr, fv)) ||
         (rc = sys_alloc(S, &v.pp, 2 * fv)) || (rc = sys_alloc(S, &v.pq, fv)) ||
         (rc = sys_alloc(S, &v.part_p, (size_t)ni * npart * 8)) ||
-        (rc = sys_alloc(S, &v.cnt_p, (size_t)3 * ni + 2)) || (rc = sys_alloc(S, &v.pctl, (size_t)ni)) ||
+        (rc = sys_alloc(S, &v.cnt_p, (size_t)4 * ni + 2)) || (rc = sys_alloc(S, &v.pctl, (size_t)ni)) ||
         (rc = sys_alloc(S, &v.pcg_active, 1)))
       return fail(rc);
+    if (v.pcg == 2) {  // AMG hierarchy (host setup once), SELL operators + level vectors on the device
+      QN_REQUIRE(ni == 1, QN_ERR_UNSUPPORTED, "system: the AMG solver supports one instance");
+      qn::AmgHierarchy H;
+      if ((rc = qn::amg_build(nf, d->a_indptr, d->a_indices, d->a_values, &H))) return fail(rc);
+      S->amg_setup_s = H.setup_seconds;
+      const int nl = (int)H.lv.size();
+      S->h_alev.assign(nl, qn::AmgDevLevel{});
+      if ((rc = sys_alloc(S, &v.pz, fv))) return fail(rc);
+      for (int l = 0; l < nl; ++l) {
+        const qn::AmgLevel& L = H.lv[l];
+        qn::AmgDevLevel& D = S->h_alev[l];
+        D.n = (int32_t)L.A.n;
+        D.omega = H.omega_l[l];
+        if ((rc = sell_upload(S, L.A.n, L.A.m, L.A.ptr.data(), L.A.col.data(), L.A.val.data(), &D.A))) return fail(rc);
+        double* dd;
+        if ((rc = sys_upload(S, &dd, L.dinv.data(), L.dinv.size()))) return fail(rc);
+        D.dinv = dd;
+        if (l + 1 < nl) {
+          if ((rc = sell_upload(S, L.P.n, L.P.m, L.P.ptr.data(), L.P.col.data(), L.P.val.data(), &D.P)) ||
+              (rc = sell_upload(S, L.R.n, L.R.m, L.R.ptr.data(), L.R.col.data(), L.R.val.data(), &D.R)))
+            return fail(rc);
+        }
+        const size_t lv3 = (size_t)L.A.n * 3;
+        if (l == 0) {
+          D.b = v.pr;  // the CG residual
+          D.t = v.pz;  // z = B r
+        } else if ((rc = sys_alloc(S, &D.b, lv3)) || (rc = sys_alloc(S, &D.t, lv3))) {
+          return fail(rc);
+        }
+        if ((rc = sys_alloc(S, &D.x, lv3)) || (rc = sys_alloc(S, &D.r, lv3))) return fail(rc);
+        const int64_t nsl_l = (L.A.n + 31) / 32;
+        D.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(div_up(nsl_l, qn::kSpmvWarps),
+                                                                 (int64_t)nsm * qn::kSpmvBlocksPerSm));
+      }
+      qn::AmgDevLevel* dl;
+      if ((rc = sys_upload(S, &dl, S->h_alev.data(), S->h_alev.size()))) return fail(rc);
+      v.alev = dl;
+      v.amg_levels = nl;
+      v.ncoarse = (int32_t)H.lv.back().A.n;
+      double* ci;
+      if ((rc = sys_upload(S, &ci, H.coarse_inv.data(), H.coarse_inv.size()))) return fail(rc);
+      v.cinv = ci;
+    }
   }
 
   v.n = (int32_t)n;
@@ -659,6 +691,67 @@ int qn_system_last_frame_ms(qn_system* S, double* ms) {
 int qn_system_last_frame_passes(qn_system* S, int64_t* passes) {
   QN_REQUIRE(S && passes, QN_ERR_ARG, "null");
   *passes = S->last_passes;
+  return QN_OK;
+}
+
+// SELL-32 copy of CSR rows (same entry order within a row, zero padding with
+// an in-range column); values of `ni` instances laid out [inst][nnz_sell]
+static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
+                       int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
+                       std::vector<double>& sval) {
+  const int64_t nsl = (nrows + 31) / 32;
+  sptr.assign((size_t)nsl + 1, 0);
+  for (int64_t sl = 0; sl < nsl; ++sl) {
+    int64_t w = 0;
+    for (int64_t r = 32 * sl; r < std::min(nrows, 32 * sl + 32); ++r) w = std::max(w, ptr[r + 1] - ptr[r]);
+    sptr[sl + 1] = sptr[sl] + 32 * w;
+  }
+  const int64_t snz = sptr[nsl];
+  scol.assign((size_t)snz, 0);
+  sval.assign((size_t)ni * snz, 0.0);
+  for (int64_t sl = 0; sl < nsl; ++sl) {
+    const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
+    for (int64_t l = 0; l < 32; ++l) {
+      const int64_t r = 32 * sl + l;
+      const int64_t p0 = r < nrows ? ptr[r] : 0, len = r < nrows ? ptr[r + 1] - p0 : 0;
+      for (int64_t k = 0; k < w; ++k) {
+        const int64_t e = sptr[sl] + 32 * k + l;
+        scol[e] = k < len ? col[p0 + k] : (int32_t)std::min(r, ncols - 1);
+        if (k < len)
+          for (int64_t b = 0; b < ni; ++b) sval[b * snz + e] = val[b * nnz + p0 + k];
+      }
+    }
+  }
+}
+
+static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
+                       const double* val, qn::SellDev* out) {
+  std::vector<int64_t> sp;
+  std::vector<int32_t> sc;
+  std::vector<double> sv;
+  sell_build(nrows, ncols, ptr, col, val, 1, ptr[nrows], sp, sc, sv);
+  int64_t* dp;
+  int32_t* dc;
+  double* dv;
+  int rc;
+  if ((rc = sys_upload(S, &dp, sp.data(), sp.size())) || (rc = sys_upload(S, &dc, sc.data(), sc.size())) ||
+      (rc = sys_upload(S, &dv, sv.data(), std::max<size_t>(sv.size(), 1))))
+    return rc;
+  out->ptr = dp;
+  out->col = dc;
+  out->val = dv;
+  out->nslice = (int32_t)(sp.size() - 1);
+  out->nrows = (int32_t)nrows;
+  return QN_OK;
+}
+
+int qn_system_amg_info(qn_system* S, int64_t* out, int64_t cap) {
+  QN_REQUIRE(S && out && cap >= 12, QN_ERR_ARG, "amg_info: args");
+  std::fill(out, out + cap, 0);
+  const int64_t nl = (int64_t)S->h_alev.size();
+  out[0] = nl;
+  for (int64_t l = 0; l < nl && l < 10; ++l) out[1 + l] = S->h_alev[l].n;
+  out[11] = (int64_t)(S->amg_setup_s * 1000.0);
   return QN_OK;
 }
 

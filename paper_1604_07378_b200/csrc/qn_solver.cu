@@ -775,7 +775,7 @@ __device__ __forceinline__ void pcg_global_tail(const SysView& v, int which) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned* gc = v.cnt_p + 3 * (size_t)v.n_inst + which;
+    unsigned* gc = v.cnt_p + 4 * (size_t)v.n_inst + which;
     const unsigned total = gridDim.x * gridDim.y;
     const unsigned old = atomicAdd(gc, 1u);
     if (old == total - 1) {
@@ -799,13 +799,14 @@ __global__ void __launch_bounds__(kPT) k_pcg_init(SysView v) {
       io.rhs(b, i, q);  // fact_vtx = free vertex ids in PCG mode
       const size_t o = ((size_t)b * v.n_free + i) * 3;
       const double di = v.dinv[(size_t)b * v.n_free + i];
+      const bool amg = v.pcg == 2;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double z = q[c] * di;
         v.px[o + c] = 0.0;
         v.pr[o + c] = q[c];
-        v.pp[o + c] = z;  // buffer 0 (read with beta = 0 by the first SpMV)
-        acc[c] = q[c] * z;
+        v.pp[o + c] = amg ? 0.0 : z;  // buffer 0 (read with beta = 0 by the first SpMV)
+        acc[c] = amg ? 0.0 : q[c] * z;  // AMG: r.z comes from k_pcg_rz after the first V-cycle
         acc[3 + c] = q[c] * q[c];
       }
     }
@@ -850,7 +851,9 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
   const size_t vo = (size_t)b * v.n_free * 3;
   const double* __restrict__ pold = v.pp + (size_t)pb * v.n_inst * v.n_free * 3 + vo;
   double* __restrict__ pnew = v.pp + (size_t)(pb ^ 1) * v.n_inst * v.n_free * 3 + vo;
-  const double* __restrict__ r = v.pr + vo;
+  // z = D^-1 r recomputed (Jacobi) or the stored V-cycle output (AMG: r <- z, dinv <- 1)
+  const bool amg = v.pcg == 2;
+  const double* __restrict__ r = amg ? v.pz + vo : v.pr + vo;
   const double* __restrict__ dinv = v.dinv + (size_t)b * v.n_free;
   const double* __restrict__ av = v.sell_val + (size_t)b * v.sell_nnz;
   double* __restrict__ q = v.pq + vo;
@@ -870,7 +873,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
         a[u] = __ldg(av + e + 32 * u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d[u] = __ldg(dinv + j[u]);
+      for (int u = 0; u < 4; ++u) d[u] = amg ? 1.0 : __ldg(dinv + j[u]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double* pj = pold + 3 * (size_t)j[u];
@@ -882,7 +885,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
     }
     for (; e < e1; e += 32) {
       const int j = __ldg(v.sell_col + e);
-      const double a = __ldg(av + e), d = __ldg(dinv + j);
+      const double a = __ldg(av + e), d = amg ? 1.0 : __ldg(dinv + j);
       const double* pj = pold + 3 * (size_t)j;
       const double* rj = r + 3 * (size_t)j;
       q0 = fma(a, fma(be0, pj[0], rj[0] * d), q0);
@@ -891,7 +894,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
     }
     const int i = 32 * sl + lane;
     if (i < v.n_free) {
-      const double d = dinv[i];
+      const double d = amg ? 1.0 : dinv[i];
       const double p0 = fma(be0, pold[3 * i + 0], r[3 * i + 0] * d);
       const double p1 = fma(be1, pold[3 * i + 1], r[3 * i + 1] * d);
       const double p2 = fma(be2, pold[3 * i + 2], r[3 * i + 2] * d);
@@ -990,8 +993,10 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
         int conv = p.conv;
         for (int k = 0; k < 3; ++k) {
           if ((conv >> k) & 1) continue;
-          p.beta[k] = tot[k] / p.rz[k];
-          p.rz[k] = tot[k];
+          if (v.pcg != 2) {  // AMG: beta and r.z come from k_pcg_rz after the V-cycle
+            p.beta[k] = tot[k] / p.rz[k];
+            p.rz[k] = tot[k];
+          }
           p.rr[k] = tot[3 + k];
           if (tot[3 + k] <= tol2 * p.bb[k]) conv |= 1 << k;
         }
@@ -1006,6 +1011,237 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
     }
   }
   pcg_global_tail(v, 1);
+}
+
+// ---- AMG V(1,1) cycle (pcg == 2, one instance): every kernel is one warp
+// per 32-row SELL slice, grid-stride, 3 right-hand sides; all no-ops once the
+// CG has converged.  Level l: x = w D^-1 b (fused into the residual), r = b -
+// A x, b_{l+1} = R r, ..., x += P t_{l+1}, t = x + w D^-1 (b - A x).
+
+// row sums of a SELL matrix times an (n x 3) vector for row 32 sl + lane
+__device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, const double* __restrict__ X,
+                                          double (&acc)[3]) {
+  const int64_t e0 = S.ptr[sl], e1 = S.ptr[sl + 1];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  int64_t e = e0 + lane;
+  for (; e + 96 < e1; e += 128) {
+    int j[4];
+    double a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      j[u] = __ldg(S.col + e + 32 * u);
+      a[u] = __ldg(S.val + e + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* xj = X + 3 * (size_t)j[u];
+      a0 = fma(a[u], xj[0], a0);
+      a1 = fma(a[u], xj[1], a1);
+      a2 = fma(a[u], xj[2], a2);
+    }
+  }
+  for (; e < e1; e += 32) {
+    const int j = __ldg(S.col + e);
+    const double a = __ldg(S.val + e);
+    const double* xj = X + 3 * (size_t)j;
+    a0 = fma(a, xj[0], a0);
+    a1 = fma(a, xj[1], a1);
+    a2 = fma(a, xj[2], a2);
+  }
+  acc[0] = a0;
+  acc[1] = a1;
+  acc[2] = a2;
+}
+
+__device__ __forceinline__ bool amg_on(const SysView& v) { return pcg_on(v, 0); }
+
+// x = w D^-1 b (pre-smoothing from zero) and r = b - A x, with x of the
+// neighbours recomputed from b (no extra pass)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
+  if (!amg_on(v)) return;
+  const AmgDevLevel& L = v.alev[l];
+  const double w = L.omega;
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int sl = w0; sl < L.A.nslice; sl += nw) {
+    const int64_t e0 = L.A.ptr[sl], e1 = L.A.ptr[sl + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int j = __ldg(L.A.col + e);
+      const double a = __ldg(L.A.val + e) * w * __ldg(L.dinv + j);
+      const double* bj = L.b + 3 * (size_t)j;
+      a0 = fma(a, bj[0], a0);
+      a1 = fma(a, bj[1], a1);
+      a2 = fma(a, bj[2], a2);
+    }
+    const int i = 32 * sl + lane;
+    if (i < L.n) {
+      const double wd = w * L.dinv[i];
+      const double* bi = L.b + 3 * (size_t)i;
+      double* xi = L.x + 3 * (size_t)i;
+      double* ri = L.r + 3 * (size_t)i;
+      xi[0] = wd * bi[0];
+      xi[1] = wd * bi[1];
+      xi[2] = wd * bi[2];
+      ri[0] = bi[0] - a0;
+      ri[1] = bi[1] - a1;
+      ri[2] = bi[2] - a2;
+    }
+  }
+}
+
+// b_{l+1} = R_l r_l
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict(SysView v, int l) {
+  if (!amg_on(v)) return;
+  const AmgDevLevel& L = v.alev[l];
+  const AmgDevLevel& C = v.alev[l + 1];
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int sl = w0; sl < L.R.nslice; sl += nw) {
+    double a[3];
+    sell_row3(L.R, sl, lane, L.r, a);
+    const int i = 32 * sl + lane;
+    if (i < C.n) {
+      double* bi = C.b + 3 * (size_t)i;
+      bi[0] = a[0];
+      bi[1] = a[1];
+      bi[2] = a[2];
+    }
+  }
+}
+
+// coarsest level: t = A_c^-1 b (dense inverse, warp per row, b staged in shared memory)
+__global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
+  if (!amg_on(v)) return;
+  extern __shared__ double sb[];
+  const AmgDevLevel& L = v.alev[v.amg_levels - 1];
+  const int nc = v.ncoarse;
+  for (int q = threadIdx.x; q < 3 * nc; q += blockDim.x) sb[q] = L.b[q];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int k = w0; k < nc; k += nw) {
+    const double* row = v.cinv + (size_t)k * nc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int c = lane; c < nc; c += 32) {
+      const double m = __ldg(row + c);
+      a0 = fma(m, sb[3 * c + 0], a0);
+      a1 = fma(m, sb[3 * c + 1], a1);
+      a2 = fma(m, sb[3 * c + 2], a2);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+      L.t[3 * k + 0] = a0;
+      L.t[3 * k + 1] = a1;
+      L.t[3 * k + 2] = a2;
+    }
+  }
+}
+
+// x_l += P_l t_{l+1}
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(SysView v, int l) {
+  if (!amg_on(v)) return;
+  const AmgDevLevel& L = v.alev[l];
+  const AmgDevLevel& C = v.alev[l + 1];
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int sl = w0; sl < L.P.nslice; sl += nw) {
+    double a[3];
+    sell_row3(L.P, sl, lane, C.t, a);
+    const int i = 32 * sl + lane;
+    if (i < L.n) {
+      double* xi = L.x + 3 * (size_t)i;
+      xi[0] += a[0];
+      xi[1] += a[1];
+      xi[2] += a[2];
+    }
+  }
+}
+
+// t = x + w D^-1 (b - A x)  (post-smoothing)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(SysView v, int l) {
+  if (!amg_on(v)) return;
+  const AmgDevLevel& L = v.alev[l];
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int sl = w0; sl < L.A.nslice; sl += nw) {
+    double a[3];
+    sell_row3(L.A, sl, lane, L.x, a);
+    const int i = 32 * sl + lane;
+    if (i < L.n) {
+      const double wd = L.omega * L.dinv[i];
+      const double* bi = L.b + 3 * (size_t)i;
+      const double* xi = L.x + 3 * (size_t)i;
+      double* ti = L.t + 3 * (size_t)i;
+      ti[0] = fma(wd, bi[0] - a[0], xi[0]);
+      ti[1] = fma(wd, bi[1] - a[1], xi[1]);
+      ti[2] = fma(wd, bi[2] - a[2], xi[2]);
+    }
+  }
+}
+
+// r.z after a V-cycle: init -> rz (beta stays 0); else beta = rz_new / rz
+__global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_rz(SysView v, int init) {
+  if (!amg_on(v)) return;
+  __shared__ double red[3 * 32];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(t % 3);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)v.n_free;
+  double rz = 0.0;
+  for (int64_t e = t; e < n3; e += stride) rz = fma(v.pr[e], v.pz[e], rz);
+  double acc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) acc[k] = k == c ? rz : 0.0;
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pp = v.part_p + (size_t)blockIdx.x * 8;
+    for (int k = 0; k < 3; ++k) pp[k] = acc[k];
+  }
+  if (last_block(v.cnt_p, 3, 0, v.n_inst, gridDim.x)) {
+    __shared__ double tot[3];
+    sum_partials(v.part_p, gridDim.x, 8, 3, tot);
+    if (threadIdx.x == 0) {
+      PcgCtl& p = v.pctl[0];
+      for (int k = 0; k < 3; ++k) {
+        if ((p.conv >> k) & 1) continue;
+        p.beta[k] = init ? 0.0 : tot[k] / p.rz[k];
+        p.rz[k] = tot[k];
+      }
+    }
+  }
+}
+
+int launch_vcycle(qn_system* S, cudaStream_t st) {
+  const SysView& v = S->v;
+  const int nl = (int)S->h_alev.size();
+  for (int l = 0; l + 1 < nl; ++l) {
+    const auto& L = S->h_alev[l];
+    k_amg_residual<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    QN_CHECK_LAUNCH();
+    const int gr = std::max(1, std::min(L.nblk, div_up(S->h_alev[l + 1].n, 32 * kSpmvWarps)));
+    k_amg_restrict<<<gr, kSpmvThreads, 0, st>>>(v, l);
+    QN_CHECK_LAUNCH();
+  }
+  const int nc = v.ncoarse;
+  k_amg_coarse<<<std::max(1, std::min(2 * kSMs, div_up(nc, kSpmvWarps))), kSpmvThreads,
+                 (size_t)3 * nc * sizeof(double), st>>>(v);
+  QN_CHECK_LAUNCH();
+  for (int l = nl - 2; l >= 0; --l) {
+    const auto& L = S->h_alev[l];
+    k_amg_prolong<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    QN_CHECK_LAUNCH();
+    k_amg_smooth<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    QN_CHECK_LAUNCH();
+  }
+  return QN_OK;
+}
+
+int launch_pcg_rz(qn_system* S, int init, cudaStream_t st) {
+  k_pcg_rz<<<S->v.nblk_upd, kUpdThreads, 0, st>>>(S->v, init);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
 }
 
 __global__ void __launch_bounds__(kPT) k_pcg_store(SysView v) {
@@ -1037,6 +1273,10 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
   if (v.pcg) {
     k_pcg_init<<<dim3(v.nblk_p, v.n_inst), kPT, 0, st>>>(v);
     QN_CHECK_LAUNCH();
+    if (v.pcg == 2) {  // z0 = B r0, rz0
+      int rc = launch_vcycle(S, st);
+      return rc ? rc : launch_pcg_rz(S, 1, st);
+    }
     return QN_OK;
   }
   SolverIO io{v};
@@ -1049,6 +1289,10 @@ int launch_pcg_iter(qn_system* S, cudaStream_t st) {
   QN_CHECK_LAUNCH();
   k_pcg_update<<<dim3(v.nblk_upd, v.n_inst), kUpdThreads, 0, st>>>(v);
   QN_CHECK_LAUNCH();
+  if (v.pcg == 2) {  // z = B r, beta = r.z / r.z_old
+    int rc = launch_vcycle(S, st);
+    return rc ? rc : launch_pcg_rz(S, 0, st);
+  }
   return QN_OK;
 }
 

@@ -49,6 +49,26 @@ constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPer
 constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
 
 
+// A sparse matrix as SELL-32 on the device (see SysView::sell_* below)
+struct SellDev {
+  const int64_t* ptr;  // [nslice + 1]
+  const int32_t* col;
+  const double* val;
+  int32_t nslice, nrows;
+};
+
+// One level of the AMG V-cycle (solver QN_SOLVE_AMG; n_inst == 1)
+struct AmgDevLevel {
+  SellDev A, P, R;      // operator (n x n), prolongator (n x n_coarse), restriction (n_coarse x n)
+  const double* dinv;   // [n]
+  double* x;            // [n][3] pre-smoothed (+ prolonged) iterate
+  double* t;            // [n][3] post-smoothed result (level 0: z)
+  double* b;            // [n][3] right-hand side (level 0: the CG residual)
+  double* r;            // [n][3] residual after pre-smoothing
+  double omega;         // Jacobi weight 4 / (3 rho(D^-1 A))
+  int32_t n, nblk;      // rows, grid of the level's SELL kernels
+};
+
 struct PcgCtl {
   double rz[3], alpha[3], beta[3], bb[3], rr[3];
   int32_t iter, conv, total, pad1;  // conv: bit c = column c converged; total: CG iterations this frame
@@ -100,7 +120,7 @@ struct SysView {
   unsigned long long* passes;
   unsigned long long* ktl;  // diagnostics timeline [kTimelinePasses][kTimelineKernels][2] ns, or null
   cudaGraphConditionalHandle handle;
-  // ---- PCG solve mode (pcg != 0) ----
+  // ---- PCG solve mode (pcg: 0 = direct, 1 = Jacobi-PCG, 2 = AMG-PCG) ----
   int32_t pcg, n_free, nblk_p, pcg_maxit;
   int32_t nslice, nblk_spmv, nblk_upd, pad_p;
   double pcg_tol;
@@ -117,10 +137,15 @@ struct SysView {
   double* pp;             // [2][inst][n_free][3] search directions (double buffered)
   double* pq;             // A p
   double* part_p;         // [inst][max(nblk_p, nblk_spmv, nblk_upd)][8]
-  unsigned* cnt_p;        // [3][inst] + [global]
+  unsigned* cnt_p;        // [4][inst] (init, spmv, update, rz) + [global]
   PcgCtl* pctl;           // [inst]
   int32_t* pcg_active;    // instances still iterating
   cudaGraphConditionalHandle pcg_handle;
+  // ---- AMG-preconditioned CG (pcg == 2) ----
+  int32_t amg_levels, ncoarse;
+  const AmgDevLevel* alev;  // [amg_levels] (device)
+  const double* cinv;       // dense inverse of the coarsest operator [ncoarse][ncoarse]
+  double* pz;               // z = B r (the V-cycle output on level 0)
 };
 
 }  // namespace qn
@@ -151,4 +176,7 @@ struct qn_system {
   // element-seam workspace
   double* d_part_plain = nullptr;
   std::vector<int32_t> h_tet_mat;
+  // AMG (host copy of the level table, for launch sizes and diagnostics)
+  std::vector<qn::AmgDevLevel> h_alev;
+  double amg_setup_s = 0.0;
 };

@@ -265,6 +265,36 @@ def test_c5_scaled_down_pcg_against_oracle():
     assert rel(xg, x) <= 1e-8
 
 
+def test_c5_scaled_down_amg_against_oracle():
+    """AMG-preconditioned CG (same 1e-10 tolerance) on the scaled configs[4]
+    bar: same parity bar as the Jacobi-PCG path, far fewer CG iterations."""
+    sc = scenes.c5(grid=(40, 10, 10), frames=1)
+    system = build(sc, solver="amg", pcg_tol=1e-10)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    run = Q.ResidentRun(system, Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev),
+                        Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
+    rg = run.step(record=True)[0]
+    xg = run.state().q_l
+    x, _, ro = O.simulate_frame(osys, sc.q_l.copy(), sc.q_prev.copy(), iterations=sc.iterations, m=sc.m)
+    assert rel(rg.g, ro.g) <= 1e-9
+    assert rel(xg, x) <= 1e-8
+    assert 0 < run.last_cg_iterations <= 40 * sc.iterations
+    info = system.amg_info()
+    assert info["levels"] >= 2
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_amg_graph_and_host_loop_agree(graph):
+    sc = scenes.c5(grid=(20, 6, 6), frames=1)
+    s1 = build(sc, solver="amg", pcg_tol=1e-12)
+    if not graph:
+        s1.set_graph_mode(False)
+    (x1, r1), = run_gpu(s1, sc, 1)
+    s2 = build(sc, solver="pcg", pcg_tol=1e-12)
+    (x2, r2), = run_gpu(s2, sc, 1)
+    assert rel(x1, x2) <= 1e-9 and rel(r1.g, r2.g) <= 1e-10
+
+
 # ---- semantics and edge cases (test_solvers.py / test_dynamics.py analogues) -----
 
 def unit_tet_mesh():

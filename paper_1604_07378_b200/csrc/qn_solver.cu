@@ -765,6 +765,7 @@ __global__ void k_material(const qn_material* M, int64_t k, const double* sig, d
 // block of the update kernel drives the inner WHILE node of the frame graph.
 
 constexpr int kPT = 128;  // PCG rows per block
+constexpr int kSellUnroll = 8;  // SELL row entries in flight per lane (c5 rows have <= 15)
 
 __device__ __forceinline__ bool pcg_on(const SysView& v, int b) {
   return v.ctl[b].phase == PH_DIR && !(v.pctl[b].conv & 8);
@@ -864,18 +865,18 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
     const int64_t e0 = v.sell_ptr[sl], e1 = v.sell_ptr[sl + 1];
     double q0 = 0.0, q1 = 0.0, q2 = 0.0;
     int64_t e = e0 + lane;
-    for (; e + 96 < e1; e += 128) {  // 4 entries of the row in flight
-      int j[4];
-      double a[4], d[4];
+    for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {  // kSellUnroll entries in flight
+      int j[kSellUnroll];
+      double a[kSellUnroll], d[kSellUnroll];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        j[u] = __ldg(v.sell_col + e + 32 * u);
-        a[u] = __ldg(av + e + 32 * u);
+      for (int u = 0; u < kSellUnroll; ++u) {
+        j[u] = __ldcs(v.sell_col + e + 32 * u);
+        a[u] = __ldcs(av + e + 32 * u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d[u] = amg ? 1.0 : __ldg(dinv + j[u]);
+      for (int u = 0; u < kSellUnroll; ++u) d[u] = amg ? 1.0 : __ldg(dinv + j[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kSellUnroll; ++u) {
         const double* pj = pold + 3 * (size_t)j[u];
         const double* rj = r + 3 * (size_t)j[u];
         q0 = fma(a[u], fma(be0, pj[0], rj[0] * d[u]), q0);
@@ -1024,16 +1025,16 @@ __device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, co
   const int64_t e0 = S.ptr[sl], e1 = S.ptr[sl + 1];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   int64_t e = e0 + lane;
-  for (; e + 96 < e1; e += 128) {
-    int j[4];
-    double a[4];
+  for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
+    int j[kSellUnroll];
+    double a[kSellUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      j[u] = __ldg(S.col + e + 32 * u);
-      a[u] = __ldg(S.val + e + 32 * u);
+    for (int u = 0; u < kSellUnroll; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
+      j[u] = __ldcs(S.col + e + 32 * u);
+      a[u] = __ldcs(S.val + e + 32 * u);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kSellUnroll; ++u) {
       const double* xj = X + 3 * (size_t)j[u];
       a0 = fma(a[u], xj[0], a0);
       a1 = fma(a[u], xj[1], a1);
@@ -1041,8 +1042,8 @@ __device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, co
     }
   }
   for (; e < e1; e += 32) {
-    const int j = __ldg(S.col + e);
-    const double a = __ldg(S.val + e);
+    const int j = __ldcs(S.col + e);
+    const double a = __ldcs(S.val + e);
     const double* xj = X + 3 * (size_t)j;
     a0 = fma(a, xj[0], a0);
     a1 = fma(a, xj[1], a1);
@@ -1066,13 +1067,31 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual
   for (int sl = w0; sl < L.A.nslice; sl += nw) {
     const int64_t e0 = L.A.ptr[sl], e1 = L.A.ptr[sl + 1];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int j = __ldg(L.A.col + e);
-      const double a = __ldg(L.A.val + e) * w * __ldg(L.dinv + j);
+    int64_t e = e0 + lane;
+    for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
+      int j[kSellUnroll];
+      double a[kSellUnroll];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        j[u] = __ldcs(L.A.col + e + 32 * u);
+        a[u] = __ldcs(L.A.val + e + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        const double c = a[u] * w * __ldg(L.dinv + j[u]);
+        const double* bj = L.b + 3 * (size_t)j[u];
+        a0 = fma(c, bj[0], a0);
+        a1 = fma(c, bj[1], a1);
+        a2 = fma(c, bj[2], a2);
+      }
+    }
+    for (; e < e1; e += 32) {
+      const int j = __ldcs(L.A.col + e);
+      const double c = __ldcs(L.A.val + e) * w * __ldg(L.dinv + j);
       const double* bj = L.b + 3 * (size_t)j;
-      a0 = fma(a, bj[0], a0);
-      a1 = fma(a, bj[1], a1);
-      a2 = fma(a, bj[2], a2);
+      a0 = fma(c, bj[0], a0);
+      a1 = fma(c, bj[1], a1);
+      a2 = fma(c, bj[2], a2);
     }
     const int i = 32 * sl + lane;
     if (i < L.n) {

@@ -45,7 +45,7 @@ struct InstCtl {
 // PCG kernel shapes: SpMV = one warp per 32-row slice, grid-stride over slices;
 // the vector update = one thread per (row, coordinate), grid-stride with a
 // stride that is a multiple of 3 so a thread keeps its coordinate.
-constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 4;
+constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 3;
 constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
 
 

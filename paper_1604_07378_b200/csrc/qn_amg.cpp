@@ -271,6 +271,10 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
     L.R = transpose(L.P);
     AmgLevel next;
     next.A = spgemm(L.R, spgemm(L.A, L.P));
+    {  // exact symmetry (the products round differently per side): A_c = (A_c + A_c^T) / 2
+      const Csr t = transpose(next.A);
+      for (int64_t e = 0; e < next.A.ptr[next.A.n]; ++e) next.A.val[e] = 0.5 * (next.A.val[e] + t.val[e]);
+    }
     h->lv.push_back(std::move(next));
   }
   // ---- dense inverse of the coarsest operator (Cholesky, then columns) ----
@@ -286,6 +290,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
       QN_REQUIRE(d > 0.0, QN_ERR_NOT_SPD, "amg: coarsest operator is not positive definite");
       d = std::sqrt(d);
       M[(size_t)j * nc + j] = d;
+#pragma omp parallel for schedule(static)
       for (int64_t i = j + 1; i < nc; ++i) {
         double s = M[(size_t)i * nc + j];
         for (int64_t k = 0; k < j; ++k) s -= M[(size_t)i * nc + k] * M[(size_t)j * nc + k];

@@ -30,15 +30,13 @@ struct AmgLevel {
 struct AmgHierarchy {
   std::vector<AmgLevel> lv;
   std::vector<double> coarse_inv;  // dense inverse of the coarsest operator (row-major)
-  double omega = 0.0;              // Jacobi smoothing weight (all levels: omega_l = kJacobiScale / rho_l)
-  std::vector<double> omega_l;
+  std::vector<double> omega_l;     // Jacobi smoothing weight per level: 4 / (3 rho(D^-1 A))
   double setup_seconds = 0.0;
 };
 
-constexpr int64_t kAmgCoarsest = 1024;    // stop coarsening at or below this many rows
+constexpr int64_t kAmgCoarsest = 3072;    // stop coarsening at or below this many rows (dense inverse <= 75 MB)
 constexpr int kAmgMaxLevels = 10;
 constexpr double kAmgStrength = 0.08;     // |a_ij| >= theta sqrt(a_ii a_jj)
-constexpr double kAmgJacobi = 2.0 / 3.0;  // smoother weight relative to 1/rho(D^-1 A) ... x (4/3)
 
 // Build the hierarchy for the CSR matrix (rows sorted, both triangles).
 int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* val, AmgHierarchy* h);

@@ -394,7 +394,7 @@ static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const i
                        int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
                        std::vector<double>& sval);
 static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
-                       const double* val, qn::SellDev* out);
+                       const double* val, qn::SellDevF* out);
 
 int qn_system_create(const qn_system_desc* d, qn_system** out) {
   QN_REQUIRE(d && out, QN_ERR_ARG, "system: null argument");
@@ -725,17 +725,19 @@ static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const i
 }
 
 static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
-                       const double* val, qn::SellDev* out) {
+                       const double* val, qn::SellDevF* out) {
   std::vector<int64_t> sp;
   std::vector<int32_t> sc;
   std::vector<double> sv;
   sell_build(nrows, ncols, ptr, col, val, 1, ptr[nrows], sp, sc, sv);
+  std::vector<float> sf(std::max<size_t>(sv.size(), 1), 0.0f);
+  for (size_t k = 0; k < sv.size(); ++k) sf[k] = (float)sv[k];
   int64_t* dp;
   int32_t* dc;
-  double* dv;
+  float* dv;
   int rc;
   if ((rc = sys_upload(S, &dp, sp.data(), sp.size())) || (rc = sys_upload(S, &dc, sc.data(), sc.size())) ||
-      (rc = sys_upload(S, &dv, sv.data(), std::max<size_t>(sv.size(), 1))))
+      (rc = sys_upload(S, &dv, sf.data(), sf.size())))
     return rc;
   out->ptr = dp;
   out->col = dc;

@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
 // A x, b_{l+1} = R r, ..., x += P t_{l+1}, t = x + w D^-1 (b - A x).
 
 // row sums of a SELL matrix times an (n x 3) vector for row 32 sl + lane
-__device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, const double* __restrict__ X,
+__device__ __forceinline__ void sell_row3(const SellDevF& S, int sl, int lane, const double* __restrict__ X,
                                           double (&acc)[3]) {
   const int64_t e0 = S.ptr[sl], e1 = S.ptr[sl + 1];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -1031,7 +1031,7 @@ __device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, co
 #pragma unroll
     for (int u = 0; u < kSellUnroll; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
       j[u] = __ldcs(S.col + e + 32 * u);
-      a[u] = __ldcs(S.val + e + 32 * u);
+      a[u] = (double)__ldcs(S.val + e + 32 * u);
     }
 #pragma unroll
     for (int u = 0; u < kSellUnroll; ++u) {
@@ -1043,7 +1043,7 @@ __device__ __forceinline__ void sell_row3(const SellDev& S, int sl, int lane, co
   }
   for (; e < e1; e += 32) {
     const int j = __ldcs(S.col + e);
-    const double a = __ldcs(S.val + e);
+    const double a = (double)__ldcs(S.val + e);
     const double* xj = X + 3 * (size_t)j;
     a0 = fma(a, xj[0], a0);
     a1 = fma(a, xj[1], a1);
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual
 #pragma unroll
       for (int u = 0; u < kSellUnroll; ++u) {
         j[u] = __ldcs(L.A.col + e + 32 * u);
-        a[u] = __ldcs(L.A.val + e + 32 * u);
+        a[u] = (double)__ldcs(L.A.val + e + 32 * u);
       }
 #pragma unroll
       for (int u = 0; u < kSellUnroll; ++u) {
@@ -1087,7 +1087,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual
     }
     for (; e < e1; e += 32) {
       const int j = __ldcs(L.A.col + e);
-      const double c = __ldcs(L.A.val + e) * w * __ldg(L.dinv + j);
+      const double c = (double)__ldcs(L.A.val + e) * w * __ldg(L.dinv + j);
       const double* bj = L.b + 3 * (size_t)j;
       a0 = fma(c, bj[0], a0);
       a1 = fma(c, bj[1], a1);
@@ -1383,6 +1383,9 @@ int launch_finish(qn_system* S, cudaStream_t st) {
 }
 
 int prepare_kernels(qn_system* S) {
+  if (S->v.pcg == 2)
+    QN_CUDA(cudaFuncSetAttribute(k_amg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(3 * sizeof(double) * S->v.ncoarse)));
   if (!S->factor) return QN_OK;
   const int rc = prepare_solve_kernels<SolverIO>(S->factor);
   return rc ? rc : prepare_solve_kernels<TimingIO>(S->factor);

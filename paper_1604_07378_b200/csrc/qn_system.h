@@ -57,9 +57,19 @@ struct SellDev {
   int32_t nslice, nrows;
 };
 
+// SELL-32 with fp32 coefficients: the AMG V-cycle operators.  The cycle is
+// only the CG preconditioner, so rounding its coefficients changes the
+// (still fixed, symmetric) preconditioner, not the system CG solves to 1e-10.
+struct SellDevF {
+  const int64_t* ptr;
+  const int32_t* col;
+  const float* val;
+  int32_t nslice, nrows;
+};
+
 // One level of the AMG V-cycle (solver QN_SOLVE_AMG; n_inst == 1)
 struct AmgDevLevel {
-  SellDev A, P, R;      // operator (n x n), prolongator (n x n_coarse), restriction (n_coarse x n)
+  SellDevF A, P, R;     // operator (n x n), prolongator (n x n_coarse), restriction (n_coarse x n)
   const double* dinv;   // [n]
   double* x;            // [n][3] pre-smoothed (+ prolonged) iterate
   double* t;            // [n][3] post-smoothed result (level 0: z)

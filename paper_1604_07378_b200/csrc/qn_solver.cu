@@ -37,6 +37,7 @@ namespace qn {
 
 constexpr int kVT = kVertexThreads;  // vertex-kernel block
 constexpr int kTT = 128;  // tet-kernel block
+constexpr int kGatherFast = 24;  // vertex valences up to this gather in two round trips (Freudenthal: <= 24)
 constexpr int kTetBlocksPerSm = 5;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
@@ -246,16 +247,32 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
     const double* fb = v.forces + (size_t)b * v.mt * 12 + (ci - 3 * i);
     const int e1 = __ldg(v.v2e_ptr + i + 1);
     int e = __ldg(v.v2e_ptr + i);
-    // element-order accumulation (the reference's np.add.at order); loads
-    // are batched 8 slots at a time so they are in flight together
-    for (; e + 8 <= e1; e += 8) {
-      double f[8];
+    // element-order accumulation (the reference's np.add.at order)
+    if (e1 - e <= kGatherFast) {
+      // all slot ids, then all corner forces, in flight together (two round
+      // trips instead of two per 8 slots), then the ordered adds
+      const int cnt = e1 - e;
+      int id[kGatherFast];
+      double f[kGatherFast];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) f[q] = __ldcg(fb + (size_t)__ldg(v.v2e + e + q) * 3);
+      for (int q = 0; q < kGatherFast; ++q)
+        if (q < cnt) id[q] = __ldg(v.v2e + e + q);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) g = __dadd_rn(g, f[q]);
+      for (int q = 0; q < kGatherFast; ++q)
+        if (q < cnt) f[q] = __ldcg(fb + (size_t)id[q] * 3);
+#pragma unroll
+      for (int q = 0; q < kGatherFast; ++q)
+        if (q < cnt) g = __dadd_rn(g, f[q]);
+    } else {
+      for (; e + 8 <= e1; e += 8) {
+        double f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = __ldcg(fb + (size_t)__ldg(v.v2e + e + q) * 3);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) g = __dadd_rn(g, f[q]);
+      }
+      for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + (size_t)__ldg(v.v2e + e) * 3));
     }
-    for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + (size_t)__ldg(v.v2e + e) * 3));
     if (v.is_fixed[i]) g = 0.0;
     v.Gr[vec_off(v, gnew, b) + ci] = g;
     acc[0] = g * g;

@@ -147,6 +147,8 @@ int factor_upload(qn_factor* f) {
   f->smem_b = (int)(sizeof(double) * (f->bwd_entries + 3 * (size_t)f->task_max_rows + 4 * kBwdCols) + sizeof(int) * kStageIdx);
   QN_REQUIRE(std::max(f->smem_f, f->smem_b) <= 227 * 1024, QN_ERR_UNSUPPORTED,
              "factor: supernode front exceeds shared memory");
+  f->fused = f->ktop == 0 && !(f->nbatch > 1);
+  f->smem_fused = std::max(f->smem_f, f->smem_b);
   // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
   int64_t zmax = 0;
   for (int s = 0; s < f->nsup; ++s)

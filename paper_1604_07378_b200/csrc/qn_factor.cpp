@@ -692,6 +692,8 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       d.nr = nr;
       d.wait0 = p >= 0 ? f->bfirst[p] : 0;
       d.nwait = p >= 0 ? f->bcount[p] : 0;
+      d.fwd0 = f->ffirst[s];
+      d.nfwd = f->fcount[s];
       f->bdesc.push_back(d);
     }
     // level lists for the batched per-instance solve: forward by height

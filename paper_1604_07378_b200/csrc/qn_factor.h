@@ -29,7 +29,8 @@ struct alignas(16) qn_bdesc {
   int64_t zoff;                 // column k0 of Z: sup_val_ptr[s] + k0 nr
   int64_t rows;                 // sup_row_ptr[s] (row ids in sup_rows)
   int32_t k0, k1, c0, nc;
-  int32_t nr, wait0, nwait, pad;  // parent's backward tasks [wait0, wait0 + nwait)
+  int32_t nr, wait0, nwait, fwd0;  // parent's backward tasks [wait0, wait0 + nwait); own forward tasks from fwd0
+  int32_t nfwd, pad0, pad1, pad2;   // ... nfwd of them (fused kernel)
 };
 
 struct qn_factor {
@@ -117,6 +118,8 @@ struct qn_factor {
   const unsigned long long* d_passes = nullptr;
   int smem_f = 0, smem_b = 0;     // dynamic shared memory of the forward / backward solve kernels
   int grid_f = 0, grid_b = 0;     // persistent solve grids (co-resident CTAs)
+  bool fused = false;             // forward + backward in one persistent kernel (no dense top)
+  int smem_fused = 0, grid_fused = 0;
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)
   int32_t batch_max_nc = 0, batch_zmax = 0;  // batched mode: widest supernode, largest Z block (entries)
   bool on_device = false;

@@ -274,6 +274,221 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
 //   __device__ bool active(int b) const;
 //   __device__ void rhs(int b, int row, double (&v)[3]) const;   // factor row
 //   __device__ void store(int b, int row, const double (&v)[3]) const;
+// One forward task (row block of one supernode): stage, wait for the
+// children, gather their updates, v = Z f, publish.
+template <class IO>
+__device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
+                                         int lane, int warp) {
+  double* zt = sm;
+  const int tid = item / F.nbatch;
+  const int b = item % F.nbatch;
+  if (!io.active(b)) return;
+  trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
+  const qn_fdesc d = F.fdesc[tid];
+  const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
+  const int R = hi - lo;
+  const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
+  double* f = sm + kTaskEntries;
+  double* part = f + 3 * nc;
+  int* sidx = (int*)(part + 3 * kSolveThreads);
+  const double* ub = F.u + (size_t)b * F.nupd * 3;
+  // ---- stage everything that does not depend on the children ----
+  {  // Z tile rows [lo, hi) x k [0, kmax) -> zt[k * R + (r - lo)]
+    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
+    const int cnt = R * kmax;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int k = e / R, rr = e - k * R;
+      cp_async8(zt + e, Zg + (int64_t)k * nr + rr);
+    }
+  }
+  const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
+  const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
+  const int* gblob = F.fblob + d.blob;
+  const bool staged = nblob <= kStageIdx;
+  if (staged)
+    for (int q = threadIdx.x; q < nblob; q += blockDim.x) sidx[q] = __ldg(gblob + q);
+  const int* sp_top = staged ? sidx : gblob;  // relative extend-add lists: [sp_top | sp_bot | si_top | si_bot]
+  const int* sp_bot = sp_top + nc + 1;
+  const int* si_top = sp_bot + nptr_bot;
+  const int* si_bot = si_top + d.ntop;
+  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+    double v[3];
+    io.rhs(b, c0 + p, v);
+    f[3 * p + 0] = v[0];
+    f[3 * p + 1] = v[1];
+    f[3 * p + 2] = v[2];
+  }
+  trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
+  wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
+  trace_mark(F.trace, kTraceSlots * (size_t)item + 2);
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
+  // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
+  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
+      const double* uc = ub + 3 * (size_t)si_top[q];
+      a0 += __ldcg(uc);
+      a1 += __ldcg(uc + 1);
+      a2 += __ldcg(uc + 2);
+    }
+    f[3 * p + 0] -= a0;
+    f[3 * p + 1] -= a1;
+    f[3 * p + 2] -= a2;
+  }
+  const int rr = lo + threadIdx.x;  // row owned by this thread in the epilogue
+  double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+  if (threadIdx.x < R && rr >= nc) {
+    const int pr = rr - blo;
+    for (int q = sp_bot[pr]; q < sp_bot[pr + 1]; ++q) {
+      const double* uc = ub + 3 * (size_t)si_bot[q];
+      e0 += __ldcg(uc);
+      e1 += __ldcg(uc + 1);
+      e2 += __ldcg(uc + 2);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
+  // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
+  const int ks = kSolveWarps / rg;
+  const int g = warp / ks, j = warp % ks;
+  const int per = (kmax + ks - 1) / ks;
+  const int kb = j * per, ke = min(kmax, kb + per);
+  const int rl = 32 * g + lane;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (g < rg && rl < R) {
+#pragma unroll 8
+    for (int k = kb; k < ke; ++k) {
+      const double l = zt[k * R + rl];
+      a0 = fma(l, f[3 * k + 0], a0);
+      a1 = fma(l, f[3 * k + 1], a1);
+      a2 = fma(l, f[3 * k + 2], a2);
+    }
+  }
+  part[3 * threadIdx.x + 0] = a0;
+  part[3 * threadIdx.x + 1] = a1;
+  part[3 * threadIdx.x + 2] = a2;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    const int gg = threadIdx.x >> 5;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int jj = 0; jj < ks; ++jj) {
+      const int t = (gg * ks + jj) * 32 + lane;
+      v0 += part[3 * t + 0];
+      v1 += part[3 * t + 1];
+      v2 += part[3 * t + 2];
+    }
+    if (rr < nc) {
+      double* yg = F.y + ((size_t)b * F.n + c0 + rr) * 3;
+      yg[0] = v0;
+      yg[1] = v1;
+      yg[2] = v2;
+    } else {
+      double* us = F.u + ((size_t)b * F.nupd + d.upd0 + (rr - nc)) * 3;
+      __stcg(us + 0, e0 + v0);
+      __stcg(us + 1, e1 + v1);
+      __stcg(us + 2, e2 + v2);
+    }
+  }
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
+  publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
+}
+
+// One backward task (column block of one supernode).  fused: forward and
+// backward share one persistent kernel, so y_J is waited for explicitly.
+template <class IO>
+__device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
+                                         int lane, int warp, bool fused) {
+  double* zt = sm;
+  const int tid = item / F.nbatch;
+  const int b = item % F.nbatch;
+  if (!io.active(b)) return;
+  trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
+  const qn_bdesc d = F.bdesc[tid];
+  const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
+  const int64_t R0 = d.rows;
+  double* w = sm + F.bwd_entries;
+  double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
+  double** sdst = (double**)(pre + 3 * kBwdCols);  // [kBwdCols] io destination of each column
+  int* srow = (int*)(sdst + kBwdCols);
+  const bool staged = nr - nc <= kStageIdx;
+  // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
+  {
+    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
+    const int cnt = (k1 - k0) * nr;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int kk = e / nr, r = e - kk * nr;
+      if (r >= k0 + kk)
+        cp_async8(zt + e, Zg + e);
+      else
+        zt[e] = 0.0;
+    }
+  }
+  if (fused)  // the forward of s may still be running: y_J must be complete
+    wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask), d.fwd0, d.nfwd, epoch, F.sched);
+  const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
+    w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
+    w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
+  }
+  if (staged)
+    for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
+  for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
+  const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
+  trace_mark(F.trace, tb + 1);
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
+  const int ncols = k1 - k0;
+  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+    double a[3];
+    const int j = lane >> 3;
+    col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
+    if ((lane & 7) == 0 && kl + j < ncols) {
+      pre[3 * (kl + j) + 0] = a[0];
+      pre[3 * (kl + j) + 1] = a[1];
+      pre[3 * (kl + j) + 2] = a[2];
+    }
+  }
+  if (d.nwait > 0)
+    wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, d.wait0, d.nwait, epoch, F.sched);
+  trace_mark(F.trace, tb + 2);
+  trace_clock(F.trace, tb + 3);
+  const double* xg = F.x + (size_t)b * F.n * 3;
+  for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) {
+    const int row = staged ? srow[q] : F.sup_rows[R0 + nc + q];
+    w[3 * (nc + q) + 0] = -__ldcg(xg + 3 * row + 0);
+    w[3 * (nc + q) + 1] = -__ldcg(xg + 3 * row + 1);
+    w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
+  }
+  __syncthreads();
+  trace_clock(F.trace, tb + 4);
+  // ---- the -x_below part, plus the staged y_J part ----
+  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+    double a[3];
+    const int j = lane >> 3;
+    col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
+    if ((lane & 7) == 0 && kl + j < ncols) {
+      const int k = k0 + kl + j;
+      const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
+                           a[2] + pre[3 * (kl + j) + 2]};
+      double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
+      xo[0] = v[0];
+      xo[1] = v[1];
+      xo[2] = v[2];
+      double* d = sdst[kl + j];
+      d[0] = v[0];
+      d[1] = v[1];
+      d[2] = v[2];
+    }
+  }
+  trace_clock(F.trace, tb + 5);
+  publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
+  trace_clock(F.trace, tb + 6);
+}
+
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F, IO io) {
   // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
@@ -285,124 +500,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* zt = sm;
   for (;;) {
     const int item = next_ticket(sched, &s_item);
     if (item >= total) break;
-    const unsigned epoch = s_epoch;
-    const int tid = item / F.nbatch;
-    const int b = item % F.nbatch;
-    if (!io.active(b)) continue;
-    trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
-    const qn_fdesc d = F.fdesc[tid];
-    const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
-    const int R = hi - lo;
-    const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
-    double* f = sm + kTaskEntries;
-    double* part = f + 3 * nc;
-    int* sidx = (int*)(part + 3 * kSolveThreads);
-    const double* ub = F.u + (size_t)b * F.nupd * 3;
-    // ---- stage everything that does not depend on the children ----
-    {  // Z tile rows [lo, hi) x k [0, kmax) -> zt[k * R + (r - lo)]
-      const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
-      const int cnt = R * kmax;
-      for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const int k = e / R, rr = e - k * R;
-        cp_async8(zt + e, Zg + (int64_t)k * nr + rr);
-      }
-    }
-    const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
-    const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
-    const int* gblob = F.fblob + d.blob;
-    const bool staged = nblob <= kStageIdx;
-    if (staged)
-      for (int q = threadIdx.x; q < nblob; q += blockDim.x) sidx[q] = __ldg(gblob + q);
-    const int* sp_top = staged ? sidx : gblob;  // relative extend-add lists: [sp_top | sp_bot | si_top | si_bot]
-    const int* sp_bot = sp_top + nc + 1;
-    const int* si_top = sp_bot + nptr_bot;
-    const int* si_bot = si_top + d.ntop;
-    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-      double v[3];
-      io.rhs(b, c0 + p, v);
-      f[3 * p + 0] = v[0];
-      f[3 * p + 1] = v[1];
-      f[3 * p + 2] = v[2];
-    }
-    trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
-    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
-    trace_mark(F.trace, kTraceSlots * (size_t)item + 2);
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
-    // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
-    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)si_top[q];
-        a0 += __ldcg(uc);
-        a1 += __ldcg(uc + 1);
-        a2 += __ldcg(uc + 2);
-      }
-      f[3 * p + 0] -= a0;
-      f[3 * p + 1] -= a1;
-      f[3 * p + 2] -= a2;
-    }
-    const int rr = lo + threadIdx.x;  // row owned by this thread in the epilogue
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-    if (threadIdx.x < R && rr >= nc) {
-      const int pr = rr - blo;
-      for (int q = sp_bot[pr]; q < sp_bot[pr + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)si_bot[q];
-        e0 += __ldcg(uc);
-        e1 += __ldcg(uc + 1);
-        e2 += __ldcg(uc + 2);
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
-    // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
-    const int ks = kSolveWarps / rg;
-    const int g = warp / ks, j = warp % ks;
-    const int per = (kmax + ks - 1) / ks;
-    const int kb = j * per, ke = min(kmax, kb + per);
-    const int rl = 32 * g + lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (g < rg && rl < R) {
-#pragma unroll 8
-      for (int k = kb; k < ke; ++k) {
-        const double l = zt[k * R + rl];
-        a0 = fma(l, f[3 * k + 0], a0);
-        a1 = fma(l, f[3 * k + 1], a1);
-        a2 = fma(l, f[3 * k + 2], a2);
-      }
-    }
-    part[3 * threadIdx.x + 0] = a0;
-    part[3 * threadIdx.x + 1] = a1;
-    part[3 * threadIdx.x + 2] = a2;
-    __syncthreads();
-    if (threadIdx.x < R) {
-      const int gg = threadIdx.x >> 5;
-      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-      for (int jj = 0; jj < ks; ++jj) {
-        const int t = (gg * ks + jj) * 32 + lane;
-        v0 += part[3 * t + 0];
-        v1 += part[3 * t + 1];
-        v2 += part[3 * t + 2];
-      }
-      if (rr < nc) {
-        double* yg = F.y + ((size_t)b * F.n + c0 + rr) * 3;
-        yg[0] = v0;
-        yg[1] = v1;
-        yg[2] = v2;
-      } else {
-        double* us = F.u + ((size_t)b * F.nupd + d.upd0 + (rr - nc)) * 3;
-        __stcg(us + 0, e0 + v0);
-        __stcg(us + 1, e1 + v1);
-        __stcg(us + 2, e2 + v2);
-      }
-    }
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
-    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
-    trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
+    fwd_task(F, io, item, s_epoch, sm, lane, warp);
   }
   cta_exit(sched, s_epoch, F, 4);
 }
@@ -418,95 +519,37 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 5, 0);
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* zt = sm;
   for (;;) {
     const int item = next_ticket(sched, &s_item);
     if (item >= total) break;
-    const unsigned epoch = s_epoch;
-    const int tid = item / F.nbatch;
-    const int b = item % F.nbatch;
-    if (!io.active(b)) continue;
-    trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
-    const qn_bdesc d = F.bdesc[tid];
-    const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
-    const int64_t R0 = d.rows;
-    double* w = sm + F.bwd_entries;
-    double* pre = w + 3 * nr;  // [kBwdCols][3] y_J part of each column
-    double** sdst = (double**)(pre + 3 * kBwdCols);  // [kBwdCols] io destination of each column
-    int* srow = (int*)(sdst + kBwdCols);
-    const bool staged = nr - nc <= kStageIdx;
-    // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
-    {
-      const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
-      const int cnt = (k1 - k0) * nr;
-      for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const int kk = e / nr, r = e - kk * nr;
-        if (r >= k0 + kk)
-          cp_async8(zt + e, Zg + e);
-        else
-          zt[e] = 0.0;
-      }
-    }
-    const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
-    for (int q = threadIdx.x; q < nc; q += blockDim.x) {
-      w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
-      w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
-      w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
-    }
-    if (staged)
-      for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
-    for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
-    const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
-    trace_mark(F.trace, tb + 1);
-    cp_async_wait_all();
-    __syncthreads();
-    // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
-    const int ncols = k1 - k0;
-    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-      double a[3];
-      const int j = lane >> 3;
-      col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
-      if ((lane & 7) == 0 && kl + j < ncols) {
-        pre[3 * (kl + j) + 0] = a[0];
-        pre[3 * (kl + j) + 1] = a[1];
-        pre[3 * (kl + j) + 2] = a[2];
-      }
-    }
-    if (d.nwait > 0)
-      wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, d.wait0, d.nwait, epoch, F.sched);
-    trace_mark(F.trace, tb + 2);
-    trace_clock(F.trace, tb + 3);
-    const double* xg = F.x + (size_t)b * F.n * 3;
-    for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) {
-      const int row = staged ? srow[q] : F.sup_rows[R0 + nc + q];
-      w[3 * (nc + q) + 0] = -__ldcg(xg + 3 * row + 0);
-      w[3 * (nc + q) + 1] = -__ldcg(xg + 3 * row + 1);
-      w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
-    }
-    __syncthreads();
-    trace_clock(F.trace, tb + 4);
-    // ---- the -x_below part, plus the staged y_J part ----
-    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-      double a[3];
-      const int j = lane >> 3;
-      col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
-      if ((lane & 7) == 0 && kl + j < ncols) {
-        const int k = k0 + kl + j;
-        const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
-                             a[2] + pre[3 * (kl + j) + 2]};
-        double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
-        xo[0] = v[0];
-        xo[1] = v[1];
-        xo[2] = v[2];
-        double* d = sdst[kl + j];
-        d[0] = v[0];
-        d[1] = v[1];
-        d[2] = v[2];
-      }
-    }
-    trace_clock(F.trace, tb + 5);
-    publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
-    trace_clock(F.trace, tb + 6);
+    bwd_task(F, io, item, s_epoch, sm, lane, warp, false);
+  }
+  cta_exit(sched, s_epoch, F, 5);
+}
+
+// Forward and backward in ONE persistent kernel (no dense top): forward
+// tickets first, then backward tickets, so idle CTAs start staging backward
+// tasks while the forward tail runs and one launch + ramp is saved.  Every
+// dependency has a smaller ticket (a backward task waits for its own
+// supernode's forward tasks and its parent's backward tasks), so the waits
+// cannot deadlock.
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
+  extern __shared__ double sm[];
+  __shared__ int s_item;
+  __shared__ unsigned s_epoch;
+  unsigned* sched = F.sched;
+  if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
+  const int nfi = F.nftask * F.nbatch, total = nfi + F.nbtask * F.nbatch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    const int item = next_ticket(sched, &s_item);
+    if (item >= total) break;
+    if (item < nfi)
+      fwd_task(F, io, item, s_epoch, sm, lane, warp);
+    else
+      bwd_task(F, io, item - nfi, s_epoch, sm, lane, warp, true);
   }
   cta_exit(sched, s_epoch, F, 5);
 }
@@ -769,6 +812,13 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     return QN_OK;
   }
   const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
+  if (f->fused) {
+    if (nf + nb > 0) {
+      sptrsv_fused<IO><<<std::min(nf + nb, f->grid_fused), kSolveThreads, f->smem_fused, stream>>>(v, io);
+      QN_CHECK_LAUNCH();
+    }
+    return QN_OK;
+  }
   if (nf > 0) {
     sptrsv_forward<IO><<<std::min(nf, f->grid_f), kSolveThreads, f->smem_f, stream>>>(v, io);
     QN_CHECK_LAUNCH();
@@ -805,6 +855,14 @@ int prepare_solve_kernels(qn_factor* f) {
   QN_CUDA(cudaGetDevice(&dev));
   QN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int gf = std::max(1, per_f) * sms, gb = std::max(1, per_b) * sms;
+  if (f->fused) {
+    QN_CUDA(cudaFuncSetAttribute(sptrsv_fused<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->smem_fused));
+    QN_CUDA(cudaFuncSetAttribute(sptrsv_fused<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_x = 0;
+    QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_x, sptrsv_fused<IO>, kSolveThreads, f->smem_fused));
+    const int gx = std::max(1, per_x) * sms;
+    f->grid_fused = f->grid_fused ? std::min(f->grid_fused, gx) : gx;
+  }
   f->grid_f = f->grid_f ? std::min(f->grid_f, gf) : gf;
   f->grid_b = f->grid_b ? std::min(f->grid_b, gb) : gb;
   return QN_OK;

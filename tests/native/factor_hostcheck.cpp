@@ -62,7 +62,7 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
     const int nr = (int)(f.sup_row_ptr[s + 1] - f.sup_row_ptr[s]);
     if (d.k0 != t.y || d.k1 != t.z || d.c0 != f.sup_col[s] || d.nr != nr || d.rows != f.sup_row_ptr[s] ||
         d.zoff != f.sup_val_ptr[s] + (int64_t)t.y * nr || d.nwait != (p >= 0 ? f.bcount[p] : 0) ||
-        (p >= 0 && d.wait0 != f.bfirst[p]))
+        (p >= 0 && d.wait0 != f.bfirst[p]) || d.fwd0 != f.ffirst[s] || d.nfwd != f.fcount[s])
       return 92;
   }
   for (const int4& t : f.ftask) {

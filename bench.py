@@ -39,7 +39,7 @@ FLUSH_BYTES = 256 << 20
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -57,20 +57,44 @@ def dist_setup():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled during the timed
+    region: NVML polled every ~2 ms from a thread (nvidia-smi -lms as fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, {reasons})
         self.proc = None
+        self.nvml = None
+        self.stop_evt = threading.Event()
 
     def start(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop_evt.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(sm), float(mx), {self.NAMES[i] for i, b in enumerate(bits) if rs & b}))
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -80,27 +104,33 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]) if parts[1].replace(".", "").isdigit() else None,
+                                  {self.NAMES[i] for i in range(4) if parts[2 + i].lower() == "active"}))
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.t.join(timeout=2)
+        if self.nvml is not None:
+            self.stop_evt.set()
+            self.t.join(timeout=2)
+            src = "nvml"
+        elif self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+            src = "nvidia-smi"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"], "samples": 0}
         rows = self.rows
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0, "source": src}
+        sm = [r[0] for r in rows]
+        mx = [r[1] for r in rows if r[1]]
+        reasons = sorted(set().union(*[r[2] for r in rows]))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "source": src}
 
 
 def peaks():
@@ -296,13 +326,19 @@ def run_ours(args, world, rank, local):
         # factor read twice + rhs/y/x/u vectors, per instance
         solve_bytes = (2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]) * n_inst
         share_solve = solve_ms * sc.iterations / per_frame
-    else:  # PCG system: the per-tet kernel is the timed hot kernel
-        solve_ms, solve_bytes, share_solve = 1.0, 0.0, 0.0
+    else:  # PCG / AMG system: the CG SpMV stands for the solve (share from the in-graph timeline)
+        solve_ms = system.time_kernel("spmv", reps=20, stream=sptr)
+        nnz_a = system.a_nnz
+        solve_bytes = 12.0 * nnz_a + 2 * 24.0 * system.n_free  # matrix once + x gathered once + y written
+        share_solve = 0.0
     live = frame_timeline(system, run, stream)
+    if "nnz_l" not in info and live and live.get("solve"):
+        share_solve = live["solve"] * live["passes"] / 1000.0 / per_frame  # whole CG solve share
     dom = "tet" if share_tet >= share_solve else "solve"
     dms, dbytes = (tet_ms, tet_bytes) if dom == "tet" else (solve_ms, solve_bytes)
     achieved = dbytes / (dms / 1000.0) / 1e9
-    solve_name = "sptrsv_batch (level-parallel, CTA per instance)" if batched else "sptrsv_forward+backward"
+    solve_name = ("sptrsv_batch (level-parallel, CTA per instance)" if batched else
+                  "sptrsv_forward+backward" if "nnz_l" in info else "k_pcg_spmv (CG SpMV, SELL-32 fp64)")
     roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else solve_name,
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
             "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,

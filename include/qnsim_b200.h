@@ -237,8 +237,10 @@ int qn_system_last_frame_cg_iterations(qn_system* s, int64_t* iters);
 int qn_system_amg_info(qn_system* s, int64_t* out, int64_t cap);
 
 /* Stand-alone timing of one hot kernel with CUDA events on `stream` (after a
- * warm-up launch): kernel 0 = per-tet pass at the resident q_l, kernel 1 =
- * forward + backward supernodal solve (3 RHS).  avg_ms = mean launch time. */
+ * warm-up launch), over every instance: kernel 0 = per-tet pass at the
+ * resident q_l, kernel 1 = forward + backward supernodal solve (3 RHS),
+ * kernel 2 = the CG's SpMV q = A_free x (PCG / AMG systems).  avg_ms = mean
+ * launch time. */
 int qn_system_time_kernel(qn_system* s, int32_t kernel, int32_t reps, double* avg_ms, void* stream);
 
 #ifdef __cplusplus

@@ -31,6 +31,7 @@ int build_graph(qn_system* S);
 int prepare_kernels(qn_system* S);
 int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st);
 int launch_solve_timing(qn_system* S, cudaStream_t st);
+int launch_spmv_timing(qn_system* S, cudaStream_t st);
 __global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
                                int zero_fixed, double* part);
 __global__ void k_svd(int64_t m, const double* F, double* U, double* s, double* V);
@@ -1064,7 +1065,7 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
 }
 
 int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* avg_ms, void* stream) {
-  QN_REQUIRE(S && avg_ms && reps >= 1 && (kernel == 0 || kernel == 1), QN_ERR_ARG, "time_kernel: args");
+  QN_REQUIRE(S && avg_ms && reps >= 1 && kernel >= 0 && kernel <= 2, QN_ERR_ARG, "time_kernel: args");
   cudaStream_t st = pick(S, stream);
   const SysView& v = S->v;
   int rc;
@@ -1072,9 +1073,13 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
     if (kernel == 0) {  // per-tet pass (F, SVD, VL energy, PK1 corner forces) at the resident q_l
       int r = launch_tet_plain(S, v.q_l, -1, -1, S->d_part_plain, st);  // every instance
       if (r) return r;
-    } else {  // forward + backward supernodal solves with 3 RHS, every instance
+    } else if (kernel == 1) {  // forward + backward supernodal solves with 3 RHS, every instance
       QN_REQUIRE(S->factor, QN_ERR_UNSUPPORTED, "time_kernel: no factor (PCG system)");
       int r = launch_solve_timing(S, st);
+      if (r) return r;
+    } else {  // the CG's SpMV q = A_free x (PCG / AMG systems)
+      QN_REQUIRE(S->v.pcg, QN_ERR_UNSUPPORTED, "time_kernel: spmv needs a PCG system");
+      int r = launch_spmv_timing(S, st);
       if (r) return r;
     }
     return QN_OK;

@@ -1249,6 +1249,54 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_rz(SysView
   }
 }
 
+// stand-alone timing of the CG's SpMV (qn_system_time_kernel "spmv"):
+// q = A_free x over the fp64 SELL matrix, the same access pattern as k_pcg_spmv
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_spmv_timing(SysView v) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int sl = w0; sl < v.nslice; sl += nw) {
+    const int64_t e0 = v.sell_ptr[sl], e1 = v.sell_ptr[sl + 1];
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+    int64_t e = e0 + lane;
+    for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
+      int j[kSellUnroll];
+      double a[kSellUnroll];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        j[u] = __ldcs(v.sell_col + e + 32 * u);
+        a[u] = __ldcs(v.sell_val + e + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        const double* xj = v.px + 3 * (size_t)j[u];
+        q0 = fma(a[u], xj[0], q0);
+        q1 = fma(a[u], xj[1], q1);
+        q2 = fma(a[u], xj[2], q2);
+      }
+    }
+    for (; e < e1; e += 32) {
+      const int j = __ldcs(v.sell_col + e);
+      const double a = __ldcs(v.sell_val + e);
+      const double* xj = v.px + 3 * (size_t)j;
+      q0 = fma(a, xj[0], q0);
+      q1 = fma(a, xj[1], q1);
+      q2 = fma(a, xj[2], q2);
+    }
+    const int i = 32 * sl + lane;
+    if (i < v.n_free) {
+      v.pq[3 * i + 0] = q0;
+      v.pq[3 * i + 1] = q1;
+      v.pq[3 * i + 2] = q2;
+    }
+  }
+}
+
+int launch_spmv_timing(qn_system* S, cudaStream_t st) {
+  k_spmv_timing<<<S->v.nblk_spmv, kSpmvThreads, 0, st>>>(S->v);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
+}
+
 int launch_vcycle(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const int nl = (int)S->h_alev.size();

@@ -97,11 +97,16 @@ class SimSystem:
     pd_groups: list = field(default_factory=list)
     colliders: list = field(default_factory=list)
     w_col: float = 0.0
+    a_nnz: int = 0  # nonzeros of A_free (setup diagnostics)
     _h: object = None
 
     @property
     def n(self):
         return self.masses.shape[0]
+
+    @property
+    def n_free(self):
+        return self.free.shape[0]
 
     def set_graph_mode(self, on: bool):
         _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
@@ -121,9 +126,11 @@ class SimSystem:
 
     def time_kernel(self, kernel: str, reps: int = 20, stream=None) -> float:
         """Mean CUDA-event time (ms) of one stand-alone launch of a hot kernel:
-        "tet" (per-tet pass at the resident q_l) or "solve" (fwd+bwd SpTRSV)."""
+        "tet" (per-tet pass at the resident q_l), "solve" (fwd+bwd SpTRSV) or
+        "spmv" (the CG's A_free SpMV, PCG/AMG systems)."""
         ms = C.c_double(0.0)
-        _lib.check(_lib.load().qn_system_time_kernel(self._h, {"tet": 0, "solve": 1}[kernel], reps, C.byref(ms),
+        _lib.check(_lib.load().qn_system_time_kernel(self._h, {"tet": 0, "solve": 1, "spmv": 2}[kernel], reps,
+                                                     C.byref(ms),
                                                      stream), "time_kernel")
         return ms.value
 
@@ -268,7 +275,7 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     system = SimSystem(mesh=mesh, masses=masses, h=float(h), gravity=np.asarray(gravity, dtype=np.float64),
                        groups=groups_per_inst[0] if n_inst == 1 else groups_per_inst, fixed=fixed, free=free,
                        L=Ls[0] if n_inst == 1 else Ls, sysfact=sysfact, scale=scale, n_inst=n_inst,
-                       materials=mats, _h=handle)
+                       materials=mats, a_nnz=int(a_indices.size), _h=handle)
     for b, gl in enumerate(groups_per_inst):
         for g, grp in enumerate(gl):
             grp._system, grp._index, grp._inst = system, g, b

@@ -153,6 +153,20 @@ def ncu_traffic(workload, kernel):
         return None
 
 
+FP64_PEAK_TFLOPS = 34.37  # DFMA microbenchmark on this pool's B200 (tools/probe_device.cu, profiles/r01_device_probe.txt)
+# fp64 flops per tet eval (2 DFMA + DMUL + DADD) from ncu sass counters of the per-tet kernel
+# (smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum / tets; c2 StVK, profiles/r01_fp64_flops.txt)
+FLOPS_PER_TET = 1388.0
+
+
+def tet_fp64(sc, tets, tet_ms):
+    """The per-tet kernel against the FP64 roofline (report K1 against
+    max(bytes/BW, flops/FP64 peak))."""
+    tf = FLOPS_PER_TET * tets / (tet_ms * 1e-3) / 1e12
+    return {"flops_per_tet": FLOPS_PER_TET, "achieved_tflops": tf, "peak_tflops": FP64_PEAK_TFLOPS,
+            "frac": tf / FP64_PEAK_TFLOPS, "flops_source": "ncu sass counters, c2 StVK material"}
+
+
 def frame_timeline(system, run, stream):
     """Mean in-graph duration (us) per body pass of one traced frame (globaltimer
     stamps written by the kernels themselves, qn_system_timeline): k_grad,
@@ -344,6 +358,7 @@ def run_ours(args, world, rank, local):
             "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
             "share_of_step": share_tet if dom == "tet" else share_solve,
             "other": {"tet_ms": tet_ms, "tet_GBps": tet_bytes / tet_ms / 1e6, "tet_share": share_tet,
+                      "tet_fp64": tet_fp64(sc, m * n_inst, tet_ms),
                       "solve_ms": solve_ms if solve_bytes else None,
                       "solve_GBps": solve_bytes / solve_ms / 1e6 if solve_bytes else None,
                       "solve_share": share_solve, "in_graph_us_per_pass": live}}

@@ -108,6 +108,11 @@ class SimSystem:
     def n_free(self):
         return self.free.shape[0]
 
+    @property
+    def op_handle(self) -> int:
+        """Integer handle for the torch custom ops (torch_ops.py)."""
+        return int(self._h.value)
+
     def set_graph_mode(self, on: bool):
         _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
 

@@ -59,6 +59,11 @@ class Factorization:
         self._h, self.n, self.nbatch, self._owned = handle, n, nbatch, False
         return self
 
+    @property
+    def op_handle(self) -> int:
+        """Integer handle for the torch custom ops (torch_ops.py)."""
+        return int(self._h.value if hasattr(self._h, "value") else self._h)
+
     def info(self) -> dict:
         inf = _lib.FactorInfo()
         _lib.check(_lib.load().qn_factor_info_get(self._h, C.byref(inf)))

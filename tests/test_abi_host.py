@@ -212,3 +212,12 @@ def test_host_amg_pcg_on_scaled_c5(hostcheck):
     assert levels >= 2 and st[3] < n / 4  # real coarsening
     assert its <= 60, its
     np.testing.assert_allclose(X, ref, rtol=0, atol=1e-8 * np.abs(ref).max())
+
+
+def test_torch_ops_registered_and_refuse_cpu_tensors(built_lib):
+    import torch
+    from paper_1604_07378_b200 import torch_ops  # noqa: F401 (registers the ops)
+    for name in ("svd_rv", "material_eval", "factor_solve", "objective", "frame_step"):
+        assert hasattr(torch.ops.qnsim_b200, name)
+    with pytest.raises(RuntimeError, match="CUDA tensor"):
+        torch.ops.qnsim_b200.svd_rv(torch.zeros((2, 3, 3), dtype=torch.float64))

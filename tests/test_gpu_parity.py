@@ -434,3 +434,32 @@ def test_pinned_out_buffers_bitwise_equal():
         np.testing.assert_array_equal(st.q_l, res[f][0])
     with pytest.raises(ValueError):
         Q.simulate_frame(s2, st, Q.SolverConfig(kind="lbfgs"), out=Q.SimState(q_l=np.zeros(3), q_prev=None, y=h[3]))
+
+
+def test_torch_custom_ops_match_the_c_abi_paths():
+    import torch
+    from paper_1604_07378_b200 import torch_ops
+    d = golden("svd_materials.npz")
+    F = torch.from_numpy(d["F"]).cuda()
+    U, s, V = torch.ops.qnsim_b200.svd_rv(F)
+    Ur, sr, Vr = Q.svd_rv_batch(d["F"])
+    assert np.array_equal(s.cpu().numpy(), sr) and np.array_equal(U.cpu().numpy(), Ur)
+    sc = scenes.c1(frames=1)
+    system = build(sc)
+    B = np.random.default_rng(4).standard_normal((system.sysfact.n, 3))
+    X = torch.ops.qnsim_b200.factor_solve(system.sysfact.op_handle, torch.from_numpy(B).cuda(), 0)
+    np.testing.assert_array_equal(X.cpu().numpy(), system.sysfact.solve(B))
+    y = np.asarray(sc.q_l) + 0.01
+    g, grad = torch.ops.qnsim_b200.objective(system.op_handle, torch.from_numpy(np.asarray(sc.q_l)).cuda(),
+                                             torch.from_numpy(y).cuda())
+    g_ref = Q.objective(system, Q.SimState(q_l=np.asarray(sc.q_l), q_prev=np.asarray(sc.q_prev), y=y),
+                        np.asarray(sc.q_l))
+    assert float(g.cpu()[0]) == pytest.approx(g_ref, rel=1e-13)
+    run = Q.ResidentRun(system, Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev),
+                        Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
+    gs = torch.ops.qnsim_b200.frame_step(system.op_handle, 1, sc.iterations, sc.m, 1)
+    (_, rec), = run_gpu(build(sc), sc, 1)
+    np.testing.assert_array_equal(gs.cpu().numpy()[0], np.asarray(rec.g))
+    h = torch_ops.register_material(from_spec(sc.material))
+    psi, tau = torch.ops.qnsim_b200.material_eval(h, s[:16].contiguous())
+    assert psi.shape == (16,) and tau.shape == (16, 3)

@@ -40,13 +40,13 @@ def main(cfg="c2", frames="3"):
         e0, e1 = t[p, 1]
         v0 = t[p, 2, 0]
         k0, k1 = t[p, 3]
-        rows.append(((g1 - g0) if g0 and g1 else 0, (e0 - g1) if g1 and e0 else 0, (e1 - e0) if e0 and e1 else 0,
+        rows.append(((g1 - g0) if g0 and g1 else 0, (e0 - g1) if g1 and e0 else 0, (v0 - e0) if e0 and v0 else 0,
                      (k0 - v0) if v0 else 0, k1 - k0, (t[p + 1, 0, 0] - k1) if p + 1 < npass else 0))
     r = np.array(rows, dtype=np.float64) / 1000.0
     sv = [(t[p, 4, 0] - t[p, 0, 1], t[p, 4, 1] - t[p, 4, 0], t[p, 5, 0] - t[p, 4, 1], t[p, 5, 1] - t[p, 5, 0],
            t[p, 1, 0] - t[p, 5, 1]) for p in range(npass) if t[p, 4, 0] and t[p, 5, 1] and t[p, 0, 1] and t[p, 1, 0]]
     full = r[:, 1] > 0  # passes with a direction (grad + solve + eta)
-    names = ["grad", "grad_end->eta (solve)", "eta", "vec", "tet", "tet_end->next grad"]
+    names = ["grad", "grad_end->eta (solve)", "eta (entry->vec entry)", "vec", "tet", "tet_end->next grad"]
     print(f"{cfg}: {npass} passes in the last frame, {full.sum()} with a solve; "
           f"frame span {(t[npass - 1, 3, 1] - t0) / 1000.0:.1f} us")
     for j, n in enumerate(names):

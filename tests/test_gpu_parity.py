@@ -463,3 +463,63 @@ def test_torch_custom_ops_match_the_c_abi_paths():
     h = torch_ops.register_material(from_spec(sc.material))
     psi, tau = torch.ops.qnsim_b200.material_eval(h, s[:16].contiguous())
     assert psi.shape == (16,) and tau.shape == (16, 3)
+
+
+# ---- analogues of the reference's unit edge cases (test_linalg / test_dynamics) ----
+
+def test_svd_rv_edge_cases_like_reference():
+    # identity, diagonal, reflection onto the last sigma, clamp of singular input (test_linalg.py:93-147)
+    r = Q.svd_rv(np.eye(3))
+    np.testing.assert_allclose(r.sigma, [1, 1, 1], atol=1e-15)
+    r = Q.svd_rv(np.diag([3.0, 2.0, 1.0]))
+    np.testing.assert_allclose(r.sigma, [3, 2, 1], atol=1e-14)
+    r = Q.svd_rv(np.diag([2.0, 1.0, -3.0]))  # det < 0: the sign goes to the smallest |sigma|
+    assert r.sigma[2] < 0 and np.all(r.sigma[:2] > 0)
+    assert np.linalg.det(r.U) == pytest.approx(1.0) and np.linalg.det(r.V) == pytest.approx(1.0)
+    r = Q.svd_rv(np.zeros((3, 3)))
+    assert np.all(np.abs(r.sigma) >= 1e-10 - 1e-25)
+    with pytest.raises(ValueError):
+        Q.svd_rv(np.full((3, 3), np.nan))
+    with pytest.raises(ValueError):
+        Q.svd_rv(np.zeros((2, 3)))
+
+
+def test_objective_zero_at_rest_and_fixed_rows_and_translation():
+    # test_dynamics.py:149 (zero at rest), :233 (fixed rows zero), :243 (elastic forces sum to zero)
+    sc = scenes.c1(frames=1)
+    system = build(sc)
+    x0 = np.asarray(sc.verts)
+    st = Q.SimState(q_l=x0, q_prev=x0, y=x0)
+    assert abs(Q.objective(system, st, x0)) <= 1e-9 * max(1.0, np.abs(x0).max())
+    rng = np.random.default_rng(7)
+    x = x0 + 0.02 * rng.standard_normal(x0.shape)
+    g = Q.gradient(system, st, x)
+    assert np.all(g[sc.fixed] == 0.0)
+    # elastic part of the gradient (inertia removed via y = x) sums to zero over all vertices
+    free_sys = build(sc, **{})
+    st_x = Q.SimState(q_l=x, q_prev=x, y=x)
+    ge = Q.gradient(Q.build_system(Q.TetMesh(sc.verts, sc.tets, sc.density), from_spec(sc.material), h=sc.h,
+                                   gravity=sc.gravity, fixed=()), st_x, x)
+    assert np.abs(ge.sum(axis=0)).max() <= 1e-9 * np.abs(ge).max()
+    del free_sys
+
+
+def test_factorize_rejects_nonsquare_and_solve_dimension_mismatch():
+    # test_linalg.py:48-81: nonsquare -> FactorizationError, row mismatch -> ValueError
+    with pytest.raises(Q.FactorizationError):
+        Q.factorize_spd(np.ones((3, 4)))
+    F = Q.factorize_spd(np.eye(4) * 2.0)
+    np.testing.assert_allclose(Q.solve_prefactored(F, np.ones((4, 3))), 0.5 * np.ones((4, 3)), rtol=0, atol=1e-15)
+    F1 = Q.factorize_spd(np.array([[4.0]]))
+    np.testing.assert_allclose(Q.solve_prefactored(F1, np.array([[8.0, 4.0, 0.0]])), [[2.0, 1.0, 0.0]], atol=1e-15)
+    with pytest.raises(ValueError):
+        Q.solve_prefactored(F, np.ones((5, 3)))
+
+
+def test_factorization_reuse_bit_identical():
+    sc = scenes.c2(frames=1)
+    system = build(sc)
+    B = np.random.default_rng(8).standard_normal((system.sysfact.n, 3))
+    X1 = system.sysfact.solve(B)
+    X2 = system.sysfact.solve(B)
+    assert np.array_equal(X1, X2)

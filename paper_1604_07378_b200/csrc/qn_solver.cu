@@ -37,6 +37,7 @@ namespace qn {
 
 constexpr int kVT = kVertexThreads;  // vertex-kernel block
 constexpr int kTT = 128;  // tet-kernel block
+constexpr int kBodyUnroll = 2;  // body passes per WHILE iteration of the frame graph (direct solver)
 constexpr int kGatherFast = 24;  // vertex valences up to this gather in two round trips (Freudenthal: <= 24)
 constexpr int kTetBlocksPerSm = 5;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
@@ -1492,9 +1493,15 @@ int build_graph(qn_system* S) {
   QN_CUDA(cudaGraphAddNode(&cond, g, &init_node, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   if (!S->v.pcg) {
+    // kBodyUnroll passes per WHILE iteration: the loop edge (~6 us) is paid
+    // once per kBodyUnroll passes; a pass after every instance is done is a
+    // no-op in every kernel (phase checks), so the extra pass at the end of
+    // a frame only costs its launches
     QN_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    rc = launch_body_pre(S, st);
-    if (rc == QN_OK) rc = launch_body_post(S, st);
+    for (int u = 0; u < kBodyUnroll && rc == QN_OK; ++u) {
+      rc = launch_body_pre(S, st);
+      if (rc == QN_OK) rc = launch_body_post(S, st);
+    }
     QN_CUDA(cudaStreamEndCapture(st, &body));
     if (rc) return rc;
   } else {

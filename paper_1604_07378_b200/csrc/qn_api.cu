@@ -16,12 +16,17 @@ namespace qn {
 
 namespace {
 thread_local std::string g_err;
+thread_local int g_capturing = 0;
 std::atomic<int64_t> g_launches{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_err = msg; }
 const char* get_error() { return g_err.c_str(); }
-void count_launch(int n) { g_launches += n; }
+void count_launch(int n) {
+  if (!g_capturing) g_launches += n;
+}
+CaptureScope::CaptureScope() { ++g_capturing; }
+CaptureScope::~CaptureScope() { --g_capturing; }
 
 // defined in qn_solver.cu
 int launch_body(qn_system* S, cudaStream_t st);
@@ -936,7 +941,11 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   unsigned long long passes = 0;
   QN_CUDA(cudaMemcpy(&passes, S->v.passes, sizeof(passes), cudaMemcpyDeviceToHost));
   S->last_passes = (int64_t)passes;
-  if (S->use_graph) count_launch((int)(2 + 6 * passes));
+  if (S->use_graph) {  // kernel nodes the graph executed: init + finish + passes + CG iterations
+    int64_t cg = 0;
+    if (S->v.pcg && S->kernels_per_cg > 0 && qn_system_last_frame_cg_iterations(S, &cg) != QN_OK) cg = 0;
+    count_launch((int)(2 + S->kernels_per_pass * (int64_t)passes + S->kernels_per_cg * cg));
+  }
   if (S->factor && (rc = factor_check_watchdog(S->factor))) return rc;
   if ((int64_t)passes > (int64_t)c.max_passes) {
     set_error("frame: pass limit exceeded (phase machine did not terminate)");

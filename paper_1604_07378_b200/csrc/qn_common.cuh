@@ -20,6 +20,11 @@ constexpr int kTimelinePasses = 512, kTimelineKernels = 6;
 void set_error(const std::string& msg);
 const char* get_error();
 void count_launch(int n = 1);
+// while a graph is being captured, QN_CHECK_LAUNCH records nodes, not launches
+struct CaptureScope {
+  CaptureScope();
+  ~CaptureScope();
+};
 
 #define QN_CUDA(call)                                                                       \
   do {                                                                                      \

@@ -1457,7 +1457,25 @@ int prepare_kernels(qn_system* S) {
   return rc ? rc : prepare_solve_kernels<TimingIO>(S->factor);
 }
 
+// kernel nodes of a (sub)graph, for launch accounting only: any query error
+// is cleared so it cannot surface at the next launch check
+static int64_t kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  int64_t k = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) == cudaSuccess && n > 0) {
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(g, nodes.data(), &n) == cudaSuccess)
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+      }
+  }
+  (void)cudaGetLastError();
+  return k;
+}
+
 int build_graph(qn_system* S) {
+  CaptureScope capture_scope;  // launches while capturing are nodes, not executions
   cudaStream_t st = S->stream;
   if (S->exec) {
     cudaGraphExecDestroy(S->exec);
@@ -1504,6 +1522,8 @@ int build_graph(qn_system* S) {
     }
     QN_CUDA(cudaStreamEndCapture(st, &body));
     if (rc) return rc;
+    S->kernels_per_pass = kernel_nodes(body) / kBodyUnroll;
+    S->kernels_per_cg = 0;
   } else {
     // pre -> WHILE(pcg active){ spmv, update } -> post, all inside the body
     cudaGraphConditionalHandle hp;
@@ -1542,6 +1562,8 @@ int build_graph(qn_system* S) {
     rc = launch_body_post(S, st);
     QN_CUDA(cudaStreamEndCapture(st, &tmpb));
     if (rc) return rc;
+    S->kernels_per_pass = kernel_nodes(body);
+    S->kernels_per_cg = kernel_nodes(ibody);
   }
   // finish
   QN_CUDA(cudaStreamBeginCaptureToGraph(st, g, &cond, nullptr, 1, cudaStreamCaptureModeThreadLocal));

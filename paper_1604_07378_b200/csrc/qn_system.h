@@ -183,6 +183,7 @@ struct qn_system {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t last_passes = 0;
+  int64_t kernels_per_pass = 0, kernels_per_cg = 0;  // kernel nodes of the captured frame graph
   // element-seam workspace
   double* d_part_plain = nullptr;
   std::vector<int32_t> h_tet_mat;

@@ -39,7 +39,7 @@ constexpr int kVT = kVertexThreads;  // vertex-kernel block
 constexpr int kTT = 128;  // tet-kernel block
 constexpr int kBodyUnroll = 2;  // body passes per WHILE iteration of the frame graph (direct solver)
 constexpr int kGatherFast = 24;  // vertex valences up to this gather in two round trips (Freudenthal: <= 24)
-constexpr int kTetBlocksPerSm = 5;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
+constexpr int kTetBlocksPerSm = 6;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
 constexpr double kAlphaFloor = 1e-12;      // solvers.py:29

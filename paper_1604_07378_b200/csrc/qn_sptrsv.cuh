@@ -637,11 +637,11 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_apply(FactorView F, 
 // overwrites y in place during the backward sweep); each warp keeps its
 // supernode's f / y_J in a private shared-memory slice; the update vectors
 // stay in the instance's global (L2) slice.
-constexpr int kBatchThreads = 256, kBatchWarps = kBatchThreads / 32;
+constexpr int kBatchThreads = 128, kBatchWarps = kBatchThreads / 32;
 constexpr int kBatchCols = 4;  // backward: columns per pass (12 independent chains per lane)
 
 template <class IO>
-__global__ void __launch_bounds__(kBatchThreads, 4) sptrsv_batch(FactorView F, IO io) {
+__global__ void __launch_bounds__(kBatchThreads, 8) sptrsv_batch(FactorView F, IO io) {
   extern __shared__ double sm[];  // yx[n*3] | fw[kBatchWarps][max_nc*3]
   const int b = blockIdx.x;
   if (!io.active(b)) return;

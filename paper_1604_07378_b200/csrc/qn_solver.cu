@@ -110,10 +110,10 @@ __device__ void sum_partials(const double* part, int nblk, int stride, int nval,
   __syncthreads();
 }
 
-__device__ void record(const SysView& v, InstCtl& c, double g, int trials, double alpha) {
+__device__ void record(const SysView& v, int b, InstCtl& c, double g, int trials, double alpha) {
   const int it = v.cfg->iterations;
   if (c.k < it && c.k < v.rec_cap) {
-    const size_t o = (size_t)blockIdx.y * v.rec_cap + c.k;
+    const size_t o = (size_t)b * v.rec_cap + c.k;
     v.rec_g[o] = g;
     v.rec_trials[o] = trials;
     v.rec_alpha[o] = alpha;
@@ -201,7 +201,7 @@ __device__ __forceinline__ void ctl_store(InstCtl* g, const InstCtl* s) {
   for (int w = threadIdx.x; w < (int)(sizeof(InstCtl) / 8); w += blockDim.x) __stcg(dst + w, src[w]);
 }
 
-__device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, bool push, int np, int cand,
+__device__ void grad_finalize(const SysView& v, int b, InstCtl& c, const double* tot, bool push, int np, int cand,
                               int gnew);
 __device__ void eta_finalize(InstCtl& c, const double* tot, int np);
 
@@ -225,7 +225,9 @@ template <int M>
 __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   constexpr int NG = 5 + 2 * M;
   tl_entry(v, 0);
-  const int b = blockIdx.y;
+  // instances in reverse launch order: the per-tet pass just wrote the last
+  // instances' corner forces, which are the ones still resident in L2
+  const int b = (int)(gridDim.y - 1 - blockIdx.y);
   const InstCtl* cc = v.ctl + b;
   if (cc->phase != PH_GRAD) return;
   __shared__ double red[kNG * 32];
@@ -321,12 +323,12 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
   sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG, gridDim.x, kNG, nval, tot);
   __shared__ InstCtl sc;
   ctl_load(v.ctl + b, &sc);
-  if (threadIdx.x == 0) grad_finalize(v, sc, tot, push, np, cand, gnew);
+  if (threadIdx.x == 0) grad_finalize(v, b, sc, tot, push, np, cand, gnew);
   ctl_store(v.ctl + b, &sc);
   tl_mark(v, 0, 1);
 }
 
-__device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, bool push, int np, int cand,
+__device__ void grad_finalize(const SysView& v, int b, InstCtl& c, const double* tot, bool push, int np, int cand,
                               int gnew) {
   const DevConfig& cfg = *v.cfg;
   c.gs_cur = gnew;
@@ -351,7 +353,7 @@ __device__ void grad_finalize(const SysView& v, InstCtl& c, const double* tot, b
   }
   c.have_prev = 1;
   if (sqrt(tot[0]) <= cfg.grad_tol) {  // solvers.py:292-298
-    record(v, c, c.g_x, 0, 0.0);
+    record(v, b, c, c.g_x, 0, 0.0);
     c.xs_prev = c.xs_cur;
     c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;  // forces still belong to x
     if (c.phase == PH_DONE) atomicSub(v.active, 1);
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
 }
 
 // one thread; e_el / inert / slope are the block-parallel sums of the partials
-__device__ void finalize_trial(const SysView& v, InstCtl& c, double e_el, double inert, double slope) {
+__device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el, double inert, double slope) {
   const DevConfig& cfg = *v.cfg;
   const double g_new = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
   const int ph = c.phase;
@@ -533,7 +535,7 @@ __device__ void finalize_trial(const SysView& v, InstCtl& c, double e_el, double
       atomicSub(v.active, 1);
       return;
     } else if (-slope <= 1e-12 * fmax(fabs(c.g_x), 1.0)) {  // solvers.py:319-326
-      record(v, c, c.g_x, 0, 0.0);
+      record(v, b, c, c.g_x, 0, 0.0);
       c.xs_prev = c.xs_cur;
       c.phase = c.k >= cfg.iterations ? PH_DONE : PH_COPY;
       c.xs_trial = c.xs_cur;
@@ -551,13 +553,13 @@ __device__ void finalize_trial(const SysView& v, InstCtl& c, double e_el, double
     c.xs_prev = c.xs_cur;
     c.xs_cur = c.xs_trial;
     c.g_x = g_new;
-    record(v, c, g_new, c.trials, cfg.line_search ? c.alpha : 1.0);
+    record(v, b, c, g_new, c.trials, cfg.line_search ? c.alpha : 1.0);
     c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;
   } else {
     c.alpha = __dmul_rn(c.alpha, cfg.shrink);
     if (c.alpha < kAlphaFloor) {  // StagnationError: pad the record (solvers.py:329-336)
       c.status |= 1;
-      while (c.k < cfg.iterations) record(v, c, c.g_x, 0, 0.0);
+      while (c.k < cfg.iterations) record(v, b, c, c.g_x, 0, 0.0);
       c.phase = PH_DONE;
     } else {
       c.trials += 1;
@@ -658,7 +660,7 @@ __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
       sum_partials(v.part_v + (size_t)b * v.nblk_v * kNG + (kNG - 2), v.nblk_v, kNG, 2, tot + 1);
       __shared__ InstCtl sc;
       ctl_load(v.ctl + b, &sc);
-      if (threadIdx.x == 0) finalize_trial(v, sc, tot[0], tot[1], tot[2]);
+      if (threadIdx.x == 0) finalize_trial(v, b, sc, tot[0], tot[1], tot[2]);
       ctl_store(v.ctl + b, &sc);
     }
   }

@@ -243,6 +243,71 @@ int qn_system_amg_info(qn_system* s, int64_t* out, int64_t cap);
  * launch time. */
 int qn_system_time_kernel(qn_system* s, int32_t kernel, int32_t reps, double* avg_ms, void* stream);
 
+/* Slab decomposition of one mesh across ranks (configs[4]):
+ * the per-rank stages of simulate_frame (solvers.py:260-352) with the
+ * reference's gradient (dynamics.py:470-478), objective (:460-467),
+ * two-loop direction (solvers.py:120-151) with A_free solved by CG, and the
+ * Armijo trial (:241-257).  The reference is single-process; these entry
+ * points are new API under the same semantics.  A rank owns a contiguous
+ * range of its local vertices and a suffix of its local tets; `local` is a
+ * qn_system built (QN_SOLVE_PCG or QN_SOLVE_AMG) on the rank's own plus
+ * ghost cells with the ghost and pinned vertices as its fixed set, so its
+ * free rows are the owned free vertices and its A_free (= the preconditioner
+ * block) is A restricted to them.  Each stage writes this rank's
+ * fixed-order partial sums to the SEND buffer; the host all-gathers SEND into
+ * every rank's GATHER buffer ([n_ranks][32]) and exchanges the boundary
+ * planes of P / R0 between neighbours before the stages that read them. */
+typedef struct qn_slab qn_slab;
+
+typedef struct qn_slab_desc {
+  qn_system* local;        /* borrowed; must outlive the slab                  */
+  int64_t own_lo, own_hi;  /* owned local vertex range                         */
+  int64_t tet_own_lo;      /* local tets [tet_own_lo, m) count in the energy   */
+  const uint8_t* pinned;   /* (n) reference fixed vertices (gradient rows 0)   */
+  /* A = L + M/h^2 on the owned free rows (local free order), columns = local
+   * vertex ids of the non-pinned vertices (ghost columns included)          */
+  int64_t a_nnz;
+  const int64_t* a_indptr;
+  const int32_t* a_indices;
+  const double* a_values;
+  int32_t n_ranks;
+  int32_t pcg_maxit;
+  double pcg_tol;          /* ||r|| <= pcg_tol ||b|| per coordinate           */
+} qn_slab_desc;
+
+#define QN_SLAB_SEND 0      /* [32] this rank's partial sums of the last stage   */
+#define QN_SLAB_GATHER 1    /* [n_ranks][32] all-gathered SEND                   */
+#define QN_SLAB_P 2         /* (n,3) CG search vector, vertex layout (halo)      */
+#define QN_SLAB_R0 3        /* (n,3) A_free^-1 q, vertex layout (halo)           */
+#define QN_SLAB_QL 4        /* (n,3) state q_l                                   */
+#define QN_SLAB_QPREV 5     /* (n,3) state q_prev                                */
+#define QN_SLAB_Y 6         /* (n,3) inertia target                              */
+#define QN_SLAB_X 7         /* (2,n,3) current / trial iterate                   */
+#define QN_SLAB_G 8         /* (n,3) gradient (owned rows complete)              */
+
+#define QN_SLAB_INIT 0        /* y, x = y                                          */
+#define QN_SLAB_EVAL 1        /* objective at X[xs]: SEND[0] elastic, [1] inertia sum m|x-y|^2 */
+#define QN_SLAB_GRAD 2        /* gradient at X[xs], L-BFGS pair, dots (see qn_slab.cu) */
+#define QN_SLAB_PCG_SETUP 3   /* q = -g - sum zeta t, CG start; SEND [bb, rz]     */
+#define QN_SLAB_PCG_P 4       /* p = z + beta p from GATHER (first: [bb, rz], else [rr, rz]) */
+#define QN_SLAB_PCG_SPMV 5    /* q = A p; SEND [pq]                                */
+#define QN_SLAB_PCG_UPDATE 6  /* x += alpha p, r -= alpha q, z = B r; SEND [rr, rz] */
+#define QN_SLAB_STORE 7       /* R0 = CG solution in vertex layout                 */
+#define QN_SLAB_ETA 8         /* SEND[j] = <t_j, r0>                               */
+#define QN_SLAB_DIR 9         /* d = r0 + sum (zeta - eta) s; SEND[0] = <g, d>     */
+#define QN_SLAB_TRIAL 10      /* X[xs_to] = X[xs] + alpha d                        */
+#define QN_SLAB_FINISH 11     /* q_prev <- q_l, q_l <- X[xs]                       */
+
+int qn_slab_create(const qn_slab_desc* d, qn_slab** out);
+int qn_slab_destroy(qn_slab* s);
+int qn_slab_buffer(qn_slab* s, int32_t which, void** ptr, int64_t* count);
+/* args (doubles): [xs, xs_to, have_prev, new_slot, nring, first, alpha,
+ * ring[9] (slot ids oldest -> newest), coef[9]]; asynchronous on `stream` */
+int qn_slab_stage(qn_slab* s, int32_t stage, const double* args, int32_t nargs, void* stream);
+/* CG status after the last update (synchronises `stream`): conv bits (bit 3 =
+ * finished), CG iterations of the current solve */
+int qn_slab_pcg_status(qn_slab* s, int32_t* conv, int32_t* iters, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

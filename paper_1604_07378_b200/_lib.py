@@ -70,6 +70,14 @@ class SystemDesc(C.Structure):
     ]
 
 
+class SlabDesc(C.Structure):
+    _fields_ = [
+        ("local", C.c_void_p), ("own_lo", C.c_int64), ("own_hi", C.c_int64), ("tet_own_lo", C.c_int64),
+        ("pinned", C.c_void_p), ("a_nnz", C.c_int64), ("a_indptr", C.c_void_p), ("a_indices", C.c_void_p),
+        ("a_values", C.c_void_p), ("n_ranks", C.c_int32), ("pcg_maxit", C.c_int32), ("pcg_tol", C.c_double),
+    ]
+
+
 class SolverConfigC(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("iterations", C.c_int32), ("m", C.c_int32), ("line_search", C.c_int32),
@@ -119,6 +127,11 @@ SIGNATURES = {
     "qn_system_timeline": [_P, _P, C.c_int64],
     "qn_system_solve_trace": [_P, _P, _P],
     "qn_system_time_kernel": [_P, _I32, _I32, _P, _P],
+    "qn_slab_create": [_P, _P],
+    "qn_slab_destroy": [_P],
+    "qn_slab_buffer": [_P, _I32, _P, _P],
+    "qn_slab_stage": [_P, _I32, _P, _I32, _P],
+    "qn_slab_pcg_status": [_P, _P, _P, _P],
 }
 
 _lib = None

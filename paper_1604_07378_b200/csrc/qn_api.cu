@@ -398,9 +398,9 @@ int qn_factor_destroy(qn_factor* f) {
 }
 
 // ---------------------------------------------------------------------------
-static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
-                       int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
-                       std::vector<double>& sval);
+void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
+                int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
+                std::vector<double>& sval);
 static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
                        const double* val, qn::SellDevF* out);
 
@@ -704,9 +704,9 @@ int qn_system_last_frame_passes(qn_system* S, int64_t* passes) {
 
 // SELL-32 copy of CSR rows (same entry order within a row, zero padding with
 // an in-range column); values of `ni` instances laid out [inst][nnz_sell]
-static void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
-                       int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
-                       std::vector<double>& sval) {
+void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col, const double* val,
+                int64_t ni, int64_t nnz, std::vector<int64_t>& sptr, std::vector<int32_t>& scol,
+                std::vector<double>& sval) {
   const int64_t nsl = (nrows + 31) / 32;
   sptr.assign((size_t)nsl + 1, 0);
   for (int64_t sl = 0; sl < nsl; ++sl) {

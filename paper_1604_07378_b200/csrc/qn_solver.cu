@@ -30,16 +30,15 @@
 
 #include "qn_common.cuh"
 #include "qn_element.cuh"
+#include "qn_kernels.cuh"
 #include "qn_sptrsv.cuh"
 #include "qn_system.h"
 
 namespace qn {
 
 constexpr int kVT = kVertexThreads;  // vertex-kernel block
-constexpr int kTT = 128;  // tet-kernel block
 constexpr int kBodyUnroll = 2;  // body passes per WHILE iteration of the frame graph (direct solver)
 constexpr int kGatherFast = 24;  // vertex valences up to this gather in two round trips (Freudenthal: <= 24)
-constexpr int kTetBlocksPerSm = 6;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
 constexpr double kAlphaFloor = 1e-12;      // solvers.py:29
@@ -53,61 +52,6 @@ __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-// last block of instance b for counter `which`?  (after all partial writes)
-// Partials are written by thread 0 before this call; one fence by that thread
-// (after the barrier) orders them before the counter increment.  The last
-// block reads the partials with L2 loads (__ldcg).
-__device__ __forceinline__ bool last_block(unsigned* cnt, int which, int b, int n_inst, int nblk) {
-  __shared__ bool s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned* c = cnt + (size_t)which * n_inst + b;
-    const unsigned old = atomicAdd(c, 1u);
-    s_last = (old == (unsigned)nblk - 1);
-    if (s_last) {
-      *c = 0;
-      __threadfence();
-    }
-  }
-  __syncthreads();
-  return s_last;
-}
-
-// Deterministic block-parallel sum of per-block partials (run by every thread of
-// the finalising block): out[k] = sum_blk part[blk * stride + k], k < nval
-// (nval <= stride <= kNG).  Blocks are processed in chunks: the chunk's
-// partial rows (contiguous) are copied to shared memory with every thread
-// issuing independent loads, then lane l of the warp owning value k adds the
-// chunk's blocks l, l+32, ... into its running sum; a fixed butterfly
-// finishes.  Fixed order throughout, so the result is reproducible.
-__device__ void sum_partials(const double* part, int nblk, int stride, int nval, double* out) {
-  // thread t < G*nval owns value k = t % nval and blocks t/nval, t/nval + G, ...
-  // (8 independent loads in flight per thread); the G per-thread sums of a
-  // value are then combined by thread k in index order.
-  __shared__ double sums[256];
-  const int G = min((int)blockDim.x, 256) / nval;
-  const int t = threadIdx.x;
-  if (t < G * nval) {
-    const int k = t % nval, j0 = t / nval;
-    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int blk = j0;
-    for (; blk + 7 * G < nblk; blk += 8 * G) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] += __ldcg(part + (size_t)(blk + u * G) * stride + k);
-    }
-    for (; blk < nblk; blk += G) a[0] += __ldcg(part + (size_t)blk * stride + k);
-    sums[t] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-  }
-  __syncthreads();
-  if (t < nval) {
-    double s = 0.0;
-    for (int j = 0; j < G; ++j) s += sums[j * nval + t];
-    out[t] = s;
-  }
-  __syncthreads();
 }
 
 __device__ void record(const SysView& v, int b, InstCtl& c, double g, int trials, double alpha) {
@@ -567,70 +511,6 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
     }
   }
   if (c.phase == PH_DONE) atomicSub(v.active, 1);
-}
-
-constexpr int kMatSmem = 4;  // materials per instance staged in shared memory
-
-// Material table of instance b: staged in shared memory (block-cooperative
-// copy) when kSm (n_mat <= kMatSmem, chosen on the host), else read from
-// global memory.  The compile-time choice keeps shared-memory accesses LDS.
-template <bool kSm>
-__device__ __forceinline__ const qn_material* stage_materials(const SysView& v, int b, qn_material* smat) {
-  const qn_material* src = v.mats + (size_t)b * v.n_mat;
-  if (!kSm) return src;
-  const int words = v.n_mat * (int)(sizeof(qn_material) / 8);
-  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
-  unsigned long long* d = reinterpret_cast<unsigned long long*>(smat);
-  for (int w = threadIdx.x; w < words; w += blockDim.x) d[w] = __ldg(s + w);
-  __syncthreads();
-  return smat;
-}
-
-constexpr int kFStride = 13;  // padded per-thread stride of the staged corner forces
-
-// Energy and corner forces of tet t (all lanes execute: lanes past the end
-// evaluate a clamped tet and do not store, keeping the SVD's warp votes
-// convergent).  Tets not in `mat_sel` (>= 0) contribute zero.  The 12 forces
-// are staged in shared memory and written block-contiguously (coalesced) by
-// store_forces().
-__device__ __forceinline__ double tet_thread(const SysView& v, const double* __restrict__ x, int b, int t_raw,
-                                             const qn_material* mats, int mat_sel, double* fsm) {
-  const int t = min(t_raw, v.mt - 1);
-  const int4 tv = __ldg(v.tets + t);
-  const int id[4] = {tv.x, tv.y, tv.z, tv.w};
-  double xs[4][3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    xs[k][0] = x[3 * id[k] + 0];
-    xs[k][1] = x[3 * id[k] + 1];
-    xs[k][2] = x[3 * id[k] + 2];
-  }
-  double Dm[3][3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int q = 0; q < 3; ++q) Dm[r][q] = __ldg(v.dminv + (size_t)(r * 3 + q) * v.mt + t);
-  const double vol = __ldg(v.vols + t);
-  const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
-  double f[4][3];
-  double e = tet_eval<true>(mats[mi], xs, Dm, vol, f);
-  const bool keep = t_raw < v.mt;
-  const bool sel = mat_sel < 0 || mi == mat_sel;
-  double* fs = fsm + threadIdx.x * kFStride;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) fs[3 * k + a] = sel ? f[k][a] : 0.0;
-  return keep && sel ? e : 0.0;
-}
-
-// coalesced write of the block's staged forces: [tet][corner][xyz] contiguous
-__device__ __forceinline__ void store_forces(const SysView& v, int b, const double* fsm) {
-  __syncthreads();
-  const int t0 = blockIdx.x * blockDim.x;
-  const int cnt = min((int)blockDim.x, v.mt - t0) * 12;
-  double* out = v.forces + ((size_t)b * v.mt + t0) * 12;
-  for (int w = threadIdx.x; w < cnt; w += blockDim.x) out[w] = fsm[(w / 12) * kFStride + (w % 12)];
 }
 
 // per-tet pass at the trial point: energy partials + corner forces

@@ -51,6 +51,27 @@ def grid_bar(nx, ny, nz, size):
     return verts, tets
 
 
+def grid_bar_cells(nx, ny, nz, size, c_lo, c_hi):
+    """Tets of the cells with x index in [c_lo, c_hi) of grid_bar(nx, ny, nz,
+    size), global vertex ids, in grid_bar's order (the cells of an x range are
+    a contiguous block of its tet array), without building the whole mesh."""
+    sx, sy, sz = size[0] / nx, size[1] / ny, size[2] / nz
+    ci, cj, ck = (a.ravel() for a in np.meshgrid(np.arange(c_lo, c_hi), np.arange(ny), np.arange(nz), indexing="ij"))
+    corner = np.stack([((ci + (c >> 2)) * (ny + 1) + (cj + ((c >> 1) & 1))) * (nz + 1) + (ck + (c & 1))
+                       for c in range(8)], axis=1)
+    tets = corner[:, _CUBE6].reshape(-1, 4).astype(np.int64)
+    plane = (ny + 1) * (nz + 1)
+    g = tets - c_lo * plane  # local grid coordinates of the corners (rest, unjittered)
+    k = g % (nz + 1)
+    j = (g // (nz + 1)) % (ny + 1)
+    i = g // plane + c_lo
+    p = np.stack([i * sx, j * sy, k * sz], axis=-1).astype(np.float64)
+    e = p[:, 1:] - p[:, :1]
+    flip = np.linalg.det(e) < 0
+    tets[flip] = tets[flip][:, [0, 1, 3, 2]]
+    return tets
+
+
 def bar_mesh(nx=12, ny=4, nz=4, size=(1.5, 0.5, 0.5)):
     """assets.bar_mesh signature (assets.py:66-69)."""
     return grid_bar(nx, ny, nz, size)

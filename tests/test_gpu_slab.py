@@ -1,0 +1,160 @@
+"""Slab-decomposed frame (configs[4] multi-GPU path) on one B200.
+
+Several ranks' slabs live in one process (EmulatedComm: the all-gathers and
+halo exchanges are device copies, no kernel waits on another), so the
+decomposition is checked against the CPU oracle and against the single-system
+frame without more GPUs; the NCCL path is checked at world size 1.
+Tolerances as the scaled-c5 single-system tests (CG to 1e-10 vs the oracle's
+direct solve): positions 1e-8, energies 1e-9 relative.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle.qnsim_oracle as O
+import paper_1604_07378_b200 as Q
+from paper_1604_07378_b200 import _lib, scenes, slab
+from paper_1604_07378_b200.materials import from_spec
+from tests.helpers import oracle_material
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu(built_lib):
+    _lib.require_gpu()
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
+
+
+def run_emulated(sc, world, frames, solver="amg", pcg_tol=1e-10, cfg=None):
+    ranks = slab.scene_slabs(sc, world, solver=solver, pcg_tol=pcg_tol)
+    run = slab.SlabRun(slab.EmulatedComm(ranks), cfg or Q.SolverConfig(kind="lbfgs", iterations=sc.iterations,
+                                                                      m=sc.m), sc.h, slab.scene_grad_tol(sc))
+    out = []
+    for _ in range(frames):
+        rec = run.step()
+        out.append((slab.gather_positions(ranks), rec))
+    return out, run
+
+
+def oracle_frames(sc, frames, cfg=None):
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed)
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    out = []
+    kw = {} if cfg is None else dict(kind=cfg.kind, use_line_search=cfg.line_search)
+    for _ in range(frames):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m, **kw)
+        q_prev, q_l = q_l, x
+        out.append((x, rec))
+    return out
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_slab_c5_scaled_against_oracle(world):
+    """configs[4] material and solver (AMG-PCG to 1e-10) on a 40x10x10 bar
+    split into `world` slabs."""
+    sc = scenes.c5(grid=(40, 10, 10), frames=1)
+    res, run = run_emulated(sc, world, 1)
+    (x, ro), = oracle_frames(sc, 1)
+    xg, rg = res[0]
+    assert rel(rg.g, ro.g) <= 1e-9
+    assert rel(xg, x) <= 1e-8
+    assert rg.ls_trials == ro.ls_trials
+    assert 0 < run.cg_iterations
+
+
+def test_slab_jacobi_lbfgs_history_against_oracle():
+    """c2-like cantilever (StVK, seeded initial velocity) on 3 slabs with the
+    Jacobi preconditioner, 2 frames: exercises pushes, evictions (m=3 < its)
+    and the Gram-form two-loop across slabs."""
+    sc = scenes.c2(grid=(12, 3, 3), frames=2, iterations=8)
+    sc.m = 3
+    res, _ = run_emulated(sc, 3, 2, solver="pcg", pcg_tol=1e-13)
+    ref = oracle_frames(sc, 2)
+    for (xg, rg), (x, ro) in zip(res, ref):
+        assert rel(rg.g, ro.g) <= 1e-10
+        assert rg.ls_trials == ro.ls_trials
+        assert rel(xg, x) <= 1e-9
+
+
+def test_slab_decomposition_independent_of_world():
+    """1, 2 and 4 slabs give the same trajectory within the CG tolerance, and
+    the same number of line-search trials."""
+    sc = scenes.c5(grid=(24, 6, 6), frames=2)
+    base, _ = run_emulated(sc, 1, 2, pcg_tol=1e-12)
+    for world in (2, 4):
+        res, _ = run_emulated(sc, world, 2, pcg_tol=1e-12)
+        for (xa, ra), (xb, rb) in zip(base, res):
+            assert rel(xb, xa) <= 1e-9
+            assert rel(rb.g, ra.g) <= 1e-10
+            assert rb.ls_trials == ra.ls_trials
+
+
+def test_slab_pd_qn_and_no_line_search():
+    sc = scenes.c1(frames=1)
+    for cfg in (Q.SolverConfig(kind="pd_qn", iterations=sc.iterations),
+                Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m, line_search=False)):
+        res, _ = run_emulated(sc, 2, 1, solver="pcg", pcg_tol=1e-13, cfg=cfg)
+        (x, ro), = oracle_frames(sc, 1, cfg)
+        assert rel(res[0][1].g, ro.g) <= 1e-10
+        assert rel(res[0][0], x) <= 1e-9
+
+
+def test_slab_nccl_world1_matches_emulated():
+    """The NCCL communicator (torch.distributed, one rank) runs the same
+    stages: bitwise the emulated single-slab result."""
+    import torch
+    import torch.distributed as dist
+    sc = scenes.c5(grid=(16, 4, 4), frames=1)
+    emu, _ = run_emulated(sc, 1, 1)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rk, = slab.scene_slabs(sc, 1)
+        run = slab.SlabRun(slab.NcclComm(rk), Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m),
+                           sc.h, slab.scene_grad_tol(sc))
+        rec = run.step()
+        x = rk.owned_positions().cpu().numpy()
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(x, emu[0][0])
+    assert rec.g == emu[0][1].g and rec.ls_trials == emu[0][1].ls_trials
+
+
+def test_slab_owned_gradient_is_the_single_system_gradient():
+    """Owned gradient rows are bitwise those of the single system (same
+    element order, same corner forces); ghost-layer tets are not counted in
+    the energy."""
+    sc = scenes.c5(grid=(10, 3, 3), frames=1)
+    system = Q.build_system(Q.TetMesh(sc.verts, sc.tets, sc.density), from_spec(sc.material), h=sc.h,
+                            gravity=sc.gravity, fixed=sc.fixed, solver="pcg")
+    st = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
+    rng = np.random.default_rng(5)
+    st.y = Q.inertia_target(st, system)
+    x = st.y + rng.normal(0, 1e-3, sc.verts.shape)
+    x[sc.fixed] = sc.q_l[sc.fixed]
+    g_ref = Q.gradient(system, st, x)
+    e_ref = Q.objective(system, st, x)
+    ranks = slab.scene_slabs(sc, 3, solver="pcg")
+    comm = slab.EmulatedComm(ranks)
+    run = slab.SlabRun(comm, Q.SolverConfig(kind="lbfgs"), sc.h, 0.0)
+    import torch
+    for rk in ranks:
+        lay = rk.lay
+        rk.stage(slab.INIT)
+        rk.buf[slab.X][: lay.n * 3].copy_(torch.as_tensor(x[lay.v0: lay.v0 + lay.n].reshape(-1)))
+    e = run._energy(0)
+    run._stage(slab.GRAD, xs=0)
+    for rk in ranks:
+        lay = rk.lay
+        g = rk.buf[slab.G].view(-1, 3)[lay.own_lo: lay.own_hi].cpu().numpy()
+        assert np.array_equal(g, g_ref[lay.v0 + lay.own_lo: lay.v0 + lay.own_hi])
+    assert abs(e - e_ref) <= 1e-12 * abs(e_ref)

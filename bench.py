@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="host-driven body loop (for per-kernel ncu lists)")
+    p.add_argument("--slab", action="store_true",
+                   help="c5: slab-decomposed frame (one slab per rank; the default for c5 when N > 1)")
     return p.parse_args()
 
 
@@ -429,11 +431,129 @@ def run_ours(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
+def run_slab(args, world, rank, local):
+    """configs[4] as one mesh split into `world` x-slabs, one per GPU (SURVEY
+    §8e): per-rank stage kernels, NCCL all-gathers of the partial sums, NCCL
+    send/recv of the boundary planes (paper_1604_07378_b200/slab.py).  Total
+    work is fixed, so the scaling is strong; value = L-BFGS iterations of the
+    one mesh per second (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1604_07378_b200 as Q
+    from paper_1604_07378_b200 import _lib, scenes, slab
+    from paper_1604_07378_b200.materials import from_spec
+    from paper_1604_07378_b200.mesh import TetMesh, lumped_masses
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", init_method=None if world > 1 else "tcp://127.0.0.1:%d" % _free_port(),
+                            rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    grid = (400, 100, 100)
+    iterations, m_hist = 10, 5
+    t_build = time.perf_counter()
+    verts, spec, fixed = scenes.c5_vertices(grid=grid)
+    lay = slab.slab_layout(grid, world, rank)
+    size = tuple(scenes.SPACING * g for g in grid)
+    tets = slab.local_tets_generated(lay, size)
+    vl = verts[lay.v0: lay.v0 + lay.n]
+    rk = slab.SlabRank(lay, vl, tets, from_spec(spec), fixed, scenes.H, scenes.GRAVITY, scenes.DENSITY,
+                       solver="amg", pcg_tol=1e-10)
+    rk.set_state(vl, vl)
+    mm = torch.tensor([float(lumped_masses(TetMesh(vl, tets, scenes.DENSITY))[lay.own_lo:lay.own_hi].max())],
+                      dtype=torch.float64, device="cuda")
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+    bbox = float(np.linalg.norm(verts.max(axis=0) - verts.min(axis=0)))
+    t_build = time.perf_counter() - t_build
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=iterations, m=m_hist)
+    run = slab.SlabRun(slab.NcclComm(rk), cfg, scenes.H, slab.grad_tolerance(bbox, float(mm.item()), scenes.H))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        run.step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evals = 0
+    cg0 = run.cg_iterations
+    l0 = _lib.launch_count()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        rec = run.step()
+        ev[k][1].record(stream)
+        evals += 1 + sum(rec.ls_trials)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    per_frame = total_ms / args.steps
+    m_all = 6 * grid[0] * grid[1] * grid[2]
+    n_all = verts.shape[0]
+    value = iterations * args.steps / (total_ms / 1000.0)
+    # roofline: the CG SpMV of this rank's owned block (the local system's A_oo, same rows)
+    hbm, peak_kind = peaks()
+    spmv_ms = rk.system.time_kernel("spmv", reps=20, stream=stream.cuda_stream)
+    spmv_bytes = 12.0 * rk.system.a_nnz + 2 * 24.0 * rk.system.n_free
+    achieved = spmv_bytes / (spmv_ms / 1000.0) / 1e9
+    cg_per_step = (run.cg_iterations - cg0) / args.steps
+    roof = {"bound": "hbm", "kernel": "CG SpMV of the rank's owned block (SELL-32 fp64)", "achieved": achieved,
+            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+            "algorithmic_bytes": spmv_bytes, "launch_ms": spmv_ms,
+            "share_of_step": None}
+    # e2e: state from / positions to page-locked host buffers every frame
+    e2e = None
+    if not args.no_e2e:
+        hq = torch.empty(lay.n * 3, dtype=torch.float64, pin_memory=True)
+        hp = torch.empty(lay.n * 3, dtype=torch.float64, pin_memory=True)
+        hx = torch.empty((lay.own_hi - lay.own_lo) * 3, dtype=torch.float64, pin_memory=True)
+        hq.copy_(rk.buf[slab.QL])
+        hp.copy_(rk.buf[slab.QPREV])
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rk.buf[slab.QL].copy_(hq, non_blocking=True)
+            rk.buf[slab.QPREV].copy_(hp, non_blocking=True)
+            run.step()
+            hx.copy_(rk.buf[slab.QL][lay.own_lo * 3: lay.own_hi * 3], non_blocking=True)
+            torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": iterations * args.steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * lay.n * 24 * world, "d2h_bytes_per_step": n_all * 24}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": per_frame, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c5", "engine": "slab", "tets": m_all, "verts": n_all,
+                           "iterations_per_step": iterations, "m": m_hist, "slabs": world,
+                           "l2": "flushed between steps (256 MiB write)", "parallelism": f"x-slabs/{world}",
+                           "preconditioner": "per-slab AMG V(1,1) (block Jacobi across slabs)"},
+                "tet_evals_per_s": evals * m_all / (total_ms / 1000.0), "roofline": roof, "cpu_baseline": None,
+                "e2e": e2e, "clocks": clk, "gpu_launches": launches, "build_s": t_build,
+                "cg_iterations_per_step": cg_per_step}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.config == "c5" and (world > 1 or args.slab):
+        run_slab(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -39,8 +39,7 @@ def grid_bar(nx, ny, nz, size):
     qnsim.assets.bar_mesh, assets.py:10-69): vertex (i, j, k) has id
     (i (ny+1) + j)(nz+1) + k; cell corners are coded di*4 + dj*2 + dk."""
     sx, sy, sz = size[0] / nx, size[1] / ny, size[2] / nz
-    ii, jj, kk = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
-    verts = np.column_stack([0.0 + ii.ravel() * sx, 0.0 + jj.ravel() * sy, 0.0 + kk.ravel() * sz])
+    verts = grid_bar_verts(nx, ny, nz, size)
     ci, cj, ck = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"))
     corner = np.stack([((ci + (c >> 2)) * (ny + 1) + (cj + ((c >> 1) & 1))) * (nz + 1) + (ck + (c & 1))
                        for c in range(8)], axis=1)
@@ -49,6 +48,13 @@ def grid_bar(nx, ny, nz, size):
     flip = np.linalg.det(e) < 0
     tets[flip] = tets[flip][:, [0, 1, 3, 2]]
     return verts, tets
+
+
+def grid_bar_verts(nx, ny, nz, size):
+    """Rest vertices of grid_bar (vertex (i, j, k) at (i sx, j sy, k sz))."""
+    sx, sy, sz = size[0] / nx, size[1] / ny, size[2] / nz
+    ii, jj, kk = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+    return np.column_stack([0.0 + ii.ravel() * sx, 0.0 + jj.ravel() * sy, 0.0 + kk.ravel() * sz])
 
 
 def grid_bar_cells(nx, ny, nz, size, c_lo, c_hi):

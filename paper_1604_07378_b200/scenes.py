@@ -174,14 +174,30 @@ def c5(seed=4, frames=5, iterations=10, grid=(400, 100, 100)):
     SURVEY.md §8d), E = 5e5, nu = 0.45, c3 = mu U(0.05, 0.2)."""
     rng = np.random.default_rng(seed)
     verts, tets = jittered_bar(*grid, rng)
+    spec = _c5_material(rng)
+    q = verts.copy()
+    return Scene("c5_large_poly", verts, tets, face_ids(*grid, 0), spec, q, q.copy(), iterations, frames,
+                 grid=grid)
+
+
+def c5_vertices(seed=4, grid=(400, 100, 100)):
+    """configs[4] without the global tet array (each slab generates its own
+    cells with mesh.grid_bar_cells): jittered rest vertices, material spec and
+    pinned ids, drawn from the same seeded stream as c5()."""
+    from paper_1604_07378_b200.mesh import grid_bar_verts
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = grid
+    verts = grid_bar_verts(nx, ny, nz, (SPACING * nx, SPACING * ny, SPACING * nz))
+    verts = verts + rng.uniform(-JITTER, JITTER, size=verts.shape)
+    return verts, _c5_material(rng), face_ids(*grid, 0)
+
+
+def _c5_material(rng):
     mu, lam = lame(5e5, 0.45)
     k3 = mu * rng.uniform(0.05, 0.2)
     a = np.array([-mu / 2.0, 0.0, mu / 2.0, 0.0, 0.0, 0.0, 0.0])
     a = a + k3 * np.array([-1.0, 0.0, 3.0, 0.0, -3.0, 0.0, 1.0])
-    spec = (("poly", list(a)), ("zero",), ("log", -mu, lam))
-    q = verts.copy()
-    return Scene("c5_large_poly", verts, tets, face_ids(*grid, 0), spec, q, q.copy(), iterations, frames,
-                 grid=grid)
+    return (("poly", list(a)), ("zero",), ("log", -mu, lam))
 
 
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

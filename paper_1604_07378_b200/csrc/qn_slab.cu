@@ -59,7 +59,7 @@ struct SlabArgs {  // per-stage scalars passed by value
 struct SlabView {
   SysView v;  // the slab-local system: tets, Dm^-1, vols, materials, gather map, masses, forces, AMG levels
   int32_t n, mt, tet_own_lo, own_lo, own_hi, nf, G, amg;
-  int32_t nblk_all, nblk_own, nblk_t, nblk_f, nblk_spmv, pcg_maxit, nblk_max, pad0;
+  int32_t nblk_all, nblk_own, nblk_t, nblk_f, nblk_spmv, pcg_maxit, nblk_max, nblk_flat;
   double pcg_tol;
   const uint8_t* pinned;  // [n]
   const int32_t* f2v;     // [nf] owned free row -> local vertex
@@ -254,15 +254,24 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_pcg_setup(SlabView s, SlabArgs
   finish_sum<6>(s, acc, 3, 0);
 }
 
+// The CG vector kernels run over the flattened (row, coordinate) elements
+// e = 3 f + c of the owned free rows, grid-stride with a stride that is a
+// multiple of 3 (kSlabFT), so a thread keeps its coordinate c; the vertex-
+// layout search vector is addressed through f2v.
+constexpr int kSlabFT = 384;
+constexpr int kSlabFU = 4;  // elements in flight per thread
+
 // <r, z> after a V-cycle -> send[3..5]
-__global__ void __launch_bounds__(kSlabVT) k_slab_rz(SlabView s) {
+__global__ void __launch_bounds__(kSlabFT) k_slab_rz(SlabView s) {
   if (s.pc->conv & 8) return;
-  double acc[3] = {0, 0, 0};
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < s.nf) {
-    const size_t fo = (size_t)f * 3;
-    for (int c = 0; c < 3; ++c) acc[c] = s.pr[fo + c] * s.pz[fo + c];
-  }
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(t % 3);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)s.nf;
+  double rz = 0.0;
+  for (int64_t e = t; e < n3; e += stride) rz = fma(s.pr[e], s.pz[e], rz);
+  double acc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) acc[k] = k == c ? rz : 0.0;
   finish_sum<3>(s, acc, 4, 3);
 }
 
@@ -270,13 +279,12 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_rz(SlabView s) {
 // first: gath = [bb, rz]; later: gath = [rr, rz_new].  Columns whose
 // residual reached tol ||b|| freeze (the single-system rule).  The last
 // block commits the scalars.
-__global__ void __launch_bounds__(kSlabVT) k_slab_pcg_p(SlabView s, int first) {
+__global__ void __launch_bounds__(kSlabFT) k_slab_pcg_p(SlabView s, int first) {
   const SlabPcg pc = *s.pc;
   if (pc.conv & 8) return;
-  double rz[3], beta[3];
+  double rz[3], beta[3], bb[3];
   int conv = pc.conv;
   const double tol2 = s.pcg_tol * s.pcg_tol;
-  double bb[3];
   for (int c = 0; c < 3; ++c) {
     const double a0 = gsum(s, c), a1 = gsum(s, 3 + c);
     rz[c] = a1;
@@ -291,13 +299,31 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_pcg_p(SlabView s, int first) {
     }
   }
   const bool done = (conv & 7) == 7 || (!first && pc.iter >= s.pcg_maxit);
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!done && f < s.nf) {
-    const size_t fo = (size_t)f * 3, o = (size_t)s.f2v[f] * 3;
-    for (int c = 0; c < 3; ++c) {
-      if ((conv >> c) & 1) continue;
-      const double z = s.pz[fo + c];
-      s.pv[o + c] = first ? z : fma(beta[c], s.pv[o + c], z);
+  if (!done) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (int)(t % 3);
+    const double be = beta[c];
+    const bool frozen = (conv >> c) & 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)s.nf;
+    if (!frozen) {
+      int64_t e = t;
+      for (; e + (kSlabFU - 1) * stride < n3; e += kSlabFU * stride) {
+        double z[kSlabFU], pv[kSlabFU];
+        int64_t o[kSlabFU];
+#pragma unroll
+        for (int u = 0; u < kSlabFU; ++u) {
+          const int64_t f = e + u * stride;
+          o[u] = 3 * (int64_t)__ldg(s.f2v + f / 3) + c;
+          z[u] = s.pz[f];
+          pv[u] = first ? 0.0 : s.pv[o[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < kSlabFU; ++u) s.pv[o[u]] = first ? z[u] : fma(be, pv[u], z[u]);
+      }
+      for (; e < n3; e += stride) {
+        const int64_t o = 3 * (int64_t)__ldg(s.f2v + e / 3) + c;
+        s.pv[o] = first ? s.pz[e] : fma(be, s.pv[o], s.pz[e]);
+      }
     }
   }
   if (last_block(s.cnt, 5, 0, 1, gridDim.x) && threadIdx.x == 0) {
@@ -306,9 +332,7 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_pcg_p(SlabView s, int first) {
       if (first) p.bb[c] = bb[c];
       if (!((pc.conv >> c) & 1)) p.rz[c] = rz[c];
     }
-    if (first) {
-      p.iter = 0;
-    }
+    if (first) p.iter = 0;
     p.conv = conv | (done ? 8 : 0);
   }
 }
@@ -365,27 +389,57 @@ __global__ void __launch_bounds__(kSpmvThreads) k_slab_spmv(SlabView s) {
 
 // ---- x += alpha p, r -= alpha q with alpha = rz / <p, q> (gathered);
 // send[0..2] <r, r>; Jacobi: z = D^-1 r, send[3..5] <r, z>
-__global__ void __launch_bounds__(kSlabVT) k_slab_pcg_update(SlabView s) {
+__global__ void __launch_bounds__(kSlabFT) k_slab_pcg_update(SlabView s) {
   const SlabPcg pc = *s.pc;
   if (pc.conv & 8) return;
-  double al[3];
-  for (int c = 0; c < 3; ++c) al[c] = (pc.conv >> c) & 1 ? 0.0 : pc.rz[c] / gsum(s, c);
-  double acc[6] = {0, 0, 0, 0, 0, 0};
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < s.nf) {
-    const size_t fo = (size_t)f * 3, o = (size_t)s.f2v[f] * 3;
-    const double di = s.amg ? 0.0 : s.dinv[f];
-    for (int c = 0; c < 3; ++c) {
-      s.px[fo + c] = fma(al[c], s.pv[o + c], s.px[fo + c]);
-      const double rn = fma(-al[c], s.pq[fo + c], s.pr[fo + c]);
-      s.pr[fo + c] = rn;
-      acc[c] = rn * rn;
-      if (!s.amg) {
-        const double z = rn * di;
-        s.pz[fo + c] = z;
-        acc[3 + c] = rn * z;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(t % 3);
+  const double al = (pc.conv >> c) & 1 ? 0.0 : pc.rz[c] / gsum(s, c);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)s.nf;
+  const bool jac = !s.amg;
+  double rr = 0.0, rz = 0.0;
+  int64_t e = t;
+  for (; e + (kSlabFU - 1) * stride < n3; e += kSlabFU * stride) {
+    double xv[kSlabFU], pv[kSlabFU], rv[kSlabFU], qv[kSlabFU], dv[kSlabFU];
+#pragma unroll
+    for (int u = 0; u < kSlabFU; ++u) {
+      const int64_t f = e + u * stride;
+      xv[u] = s.px[f];
+      pv[u] = s.pv[3 * (int64_t)__ldg(s.f2v + f / 3) + c];
+      rv[u] = s.pr[f];
+      qv[u] = s.pq[f];
+      dv[u] = jac ? __ldg(s.dinv + f / 3) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kSlabFU; ++u) {
+      const int64_t f = e + u * stride;
+      s.px[f] = fma(al, pv[u], xv[u]);
+      const double rn = fma(-al, qv[u], rv[u]);
+      s.pr[f] = rn;
+      rr = fma(rn, rn, rr);
+      if (jac) {
+        const double z = rn * dv[u];
+        s.pz[f] = z;
+        rz = fma(rn, z, rz);
       }
     }
+  }
+  for (; e < n3; e += stride) {
+    s.px[e] = fma(al, s.pv[3 * (int64_t)__ldg(s.f2v + e / 3) + c], s.px[e]);
+    const double rn = fma(-al, s.pq[e], s.pr[e]);
+    s.pr[e] = rn;
+    rr = fma(rn, rn, rr);
+    if (jac) {
+      const double z = rn * __ldg(s.dinv + e / 3);
+      s.pz[e] = z;
+      rz = fma(rn, z, rz);
+    }
+  }
+  double acc[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    acc[k] = k == c ? rr : 0.0;
+    acc[3 + k] = k == c ? rz : 0.0;
   }
   finish_sum<6>(s, acc, 7, 0);
 }
@@ -569,7 +623,8 @@ int qn_slab_create(const qn_slab_desc* d, qn_slab** out) {
   s.nblk_f = std::max(1, div_up(nf, kSlabVT));
   const int64_t nsl = (nf + 31) / 32;
   s.nblk_spmv = (int32_t)std::max<int64_t>(1, std::min<int64_t>(div_up(nsl, kSpmvWarps), (int64_t)nsm * 3));
-  S->nblk_max = std::max(std::max(s.nblk_all, s.nblk_t), s.nblk_spmv);
+  s.nblk_flat = (int32_t)std::max<int64_t>(1, std::min<int64_t>(div_up(3 * nf, 384), (int64_t)nsm * 4));
+  S->nblk_max = std::max(std::max(std::max(s.nblk_all, s.nblk_t), s.nblk_spmv), s.nblk_flat);
   s.nblk_max = S->nblk_max;
 
   // free rows of the local system (= owned free vertices, increasing): read its fact_vtx map
@@ -695,12 +750,12 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
       QN_CHECK_LAUNCH();
       if (s.amg) {
         if ((rc = launch_vcycle(S->local, st))) return rc;
-        k_slab_rz<<<s.nblk_all, kSlabVT, 0, st>>>(s);
+        k_slab_rz<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
         QN_CHECK_LAUNCH();
       }
       break;
     case QN_SLAB_PCG_P:
-      k_slab_pcg_p<<<s.nblk_all, kSlabVT, 0, st>>>(s, a.first);
+      k_slab_pcg_p<<<s.nblk_flat, kSlabFT, 0, st>>>(s, a.first);
       QN_CHECK_LAUNCH();
       break;
     case QN_SLAB_PCG_SPMV:
@@ -708,13 +763,13 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
       QN_CHECK_LAUNCH();
       break;
     case QN_SLAB_PCG_UPDATE:
-      k_slab_pcg_update<<<s.nblk_all, kSlabVT, 0, st>>>(s);
+      k_slab_pcg_update<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
       QN_CHECK_LAUNCH();
       k_slab_pcg_count<<<1, 1, 0, st>>>(s);
       QN_CHECK_LAUNCH();
       if (s.amg) {
         if ((rc = launch_vcycle(S->local, st))) return rc;
-        k_slab_rz<<<s.nblk_all, kSlabVT, 0, st>>>(s);
+        k_slab_rz<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
         QN_CHECK_LAUNCH();
       }
       break;

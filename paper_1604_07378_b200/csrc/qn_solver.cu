@@ -1180,6 +1180,19 @@ int launch_spmv_timing(qn_system* S, cudaStream_t st) {
   return QN_OK;
 }
 
+// Several systems (e.g. the slabs held by one process) stage coarse levels of
+// different sizes: the kernel's dynamic shared-memory limit only ever grows.
+// Called before any graph capture (prepare_kernels) and before direct launches.
+static int ensure_coarse_smem(int nc) {
+  static int smem_set = 0;
+  const int need = (int)(3 * sizeof(double) * nc);
+  if (need > smem_set) {
+    QN_CUDA(cudaFuncSetAttribute(k_amg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+    smem_set = need;
+  }
+  return QN_OK;
+}
+
 int launch_vcycle(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const int nl = (int)S->h_alev.size();
@@ -1192,6 +1205,7 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
     QN_CHECK_LAUNCH();
   }
   const int nc = v.ncoarse;
+  if (int rc = ensure_coarse_smem(nc)) return rc;
   k_amg_coarse<<<std::max(1, std::min(2 * kSMs, div_up(nc, kSpmvWarps))), kSpmvThreads,
                  (size_t)3 * nc * sizeof(double), st>>>(v);
   QN_CHECK_LAUNCH();
@@ -1332,8 +1346,7 @@ int launch_finish(qn_system* S, cudaStream_t st) {
 
 int prepare_kernels(qn_system* S) {
   if (S->v.pcg == 2)
-    QN_CUDA(cudaFuncSetAttribute(k_amg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(3 * sizeof(double) * S->v.ncoarse)));
+    if (int rc = ensure_coarse_smem(S->v.ncoarse)) return rc;
   if (!S->factor) return QN_OK;
   const int rc = prepare_solve_kernels<SolverIO>(S->factor);
   return rc ? rc : prepare_solve_kernels<TimingIO>(S->factor);

@@ -43,6 +43,8 @@ INIT, EVAL, GRAD, PCG_SETUP, PCG_P, PCG_SPMV, PCG_UPDATE, STORE, ETA, DIR, TRIAL
 MAX_M = 8                 # kSlabMaxM
 RING = MAX_M + 1
 NSEND = 32
+_STAGE_NAMES = ["init", "eval", "grad", "pcg_setup", "pcg_p", "pcg_spmv", "pcg_update", "store", "eta", "dir",
+                "trial", "finish"]
 CURVATURE_GUARD = 1e-12   # solvers.py:28
 ALPHA_FLOOR = 1e-12       # solvers.py:29
 
@@ -304,12 +306,39 @@ class SlabRun:
         self.last_ms = 0.0
 
     # -- helpers -------------------------------------------------------------
-    def _stage(self, *a, **k):
-        for rk in self.comm.local:
-            rk.stage(*a, **k)
+    def enable_profile(self, on=True):
+        """Record CUDA events around every stage / exchange (diagnostics:
+        `stage_ms()` sums them per stage after the frame)."""
+        self._prof = [] if on else None
+
+    def _ev(self, name, fn):
+        if getattr(self, "_prof", None) is None:
+            return fn()
+        import torch
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        self._prof.append((name, a, b))
+        return out
+
+    def stage_ms(self):
+        import torch
+        torch.cuda.synchronize()
+        tot = {}
+        for name, a, b in self._prof or []:
+            n, t = tot.get(name, (0, 0.0))
+            tot[name] = (n + 1, t + a.elapsed_time(b))
+        return tot
+
+    def _stage(self, st, **k):
+        def go():
+            for rk in self.comm.local:
+                rk.stage(st, **k)
+        self._ev(_STAGE_NAMES[st], go)
 
     def _gather(self):
-        self.comm.allgather()
+        self._ev("allgather", self.comm.allgather)
         return rank_sum(self.comm.scalars())
 
     def _energy(self, xs):
@@ -320,15 +349,15 @@ class SlabRun:
     def _solve(self, ring, zeta):
         """r0 = A_free^-1 (-g - sum zeta t) by CG over the slabs (3 columns)."""
         self._stage(PCG_SETUP, ring=ring, coef=zeta)
-        self.comm.allgather()
+        self._ev("allgather", self.comm.allgather)
         self._stage(PCG_P, first=1)
         it = 0
         while True:
-            self.comm.halo(P)
+            self._ev("halo", lambda: self.comm.halo(P))
             self._stage(PCG_SPMV)
-            self.comm.allgather()
+            self._ev("allgather", self.comm.allgather)
             self._stage(PCG_UPDATE)
-            self.comm.allgather()
+            self._ev("allgather", self.comm.allgather)
             self._stage(PCG_P, first=0)
             it += 1
             if it % self.pcg_check == 0:
@@ -337,7 +366,7 @@ class SlabRun:
                     self.cg_iterations += its
                     break
         self._stage(STORE)
-        self.comm.halo(R0)
+        self._ev("halo", lambda: self.comm.halo(R0))
 
     # -- one frame -------------------------------------------------------------
     def step(self) -> ConvergenceRecord:

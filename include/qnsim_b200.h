@@ -68,6 +68,19 @@ typedef struct qn_material {
   double shift;
 } qn_material;
 
+/* Collider (dynamics.py:199-270): keeps vertices outside a solid.  Penalty
+ * w_col (depth . n)^2 per active constraint (dynamics.py:446-457), active set
+ * rebuilt at the start of every iteration (update_collisions, :486-516). */
+#define QN_COL_HALFSPACE 0  /* p = point, n = unit normal                 */
+#define QN_COL_SPHERE 1     /* p = center, r0 = radius                    */
+#define QN_COL_TORUS 2      /* p = center, r0 = major, r1 = minor radius  */
+#define QN_MAX_COLLIDERS 4
+typedef struct qn_collider {
+  int32_t kind, pad;
+  double p[3], n[3];
+  double r0, r1;
+} qn_collider;
+
 /* ------------------------------------------------------------------------ */
 /* library                                                                  */
 
@@ -158,6 +171,10 @@ typedef struct qn_system_desc {
   int32_t solver;
   int32_t pcg_maxit;
   double pcg_tol;
+  /* colliders (shared by all instances); w_col = collision_weight or 10 max w */
+  int64_t n_colliders;        /* <= QN_MAX_COLLIDERS                             */
+  const qn_collider* colliders;
+  double w_col;
 } qn_system_desc;
 
 #define QN_SOLVE_DIRECT 0

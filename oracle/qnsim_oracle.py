@@ -10,8 +10,9 @@ Differences from the reference, all deliberate and documented in DESIGN.md:
   dense `cho_factor` of `linalg.py:31` / `dynamics.py:413` (dense is O(n^2)
   memory, infeasible beyond configs[1]); `factor="dense"` restates the
   reference exactly;
-* the harness-side scenario parsing, colliders, PD materials, Chebyshev and
-  Newton are out of the hot-path scope and not restated.
+* the harness-side scenario parsing, PD materials, Chebyshev and Newton are
+  out of the hot-path scope and not restated; colliders
+  (§8f row f2) are restated below.
 """
 
 from __future__ import annotations
@@ -395,6 +396,8 @@ class System:
     A_free: scipy.sparse.csr_matrix
     factor: object
     scale: float
+    colliders: list = None
+    w_col: float = 0.0
 
     @property
     def n(self):
@@ -402,7 +405,7 @@ class System:
 
 
 def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), factor="sparse",
-          masses=None):
+          masses=None, colliders=(), collision_weight=None):
     """Restates dynamics.build_system (dynamics.py:351-434) for VL tet groups.
 
     `materials` is a VLMaterial (all tets) or a list of (tet_index_array, VLMaterial).
@@ -440,8 +443,113 @@ def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), fa
     fac = DenseFactor(A_free.toarray()) if factor == "dense" else SparseFactor(A_free)
     bbox = verts.max(axis=0) - verts.min(axis=0)
     scale = float(np.linalg.norm(bbox)) or 1.0                     # dynamics.py:416-417
+    max_w = max((float((g.vols * g.k).max()) for g in groups if g.vols.size), default=0.0)
+    w_col = float(collision_weight) if collision_weight is not None else 10.0 * max_w  # dynamics.py:417
     return System(verts, tets, masses, float(h), np.asarray(gravity, dtype=np.float64), groups,
-                  fixed, free, L, A_free, fac, scale)
+                  fixed, free, L, A_free, fac, scale, list(colliders), w_col)
+
+
+# --------------------------------------------------------------------------
+# colliders (dynamics.py:199-285, 446-457, 486-516)
+
+class HalfSpace:
+    """dynamics.py:199-212"""
+
+    def __init__(self, point, normal):
+        self.point = np.asarray(point, dtype=np.float64)
+        n = np.asarray(normal, dtype=np.float64)
+        self.normal = n / np.linalg.norm(n)
+
+    def signed_distance(self, x):
+        return (x - self.point) @ self.normal
+
+    def project(self, x):
+        sd = self.signed_distance(x)
+        return x - sd[:, None] * self.normal, np.broadcast_to(self.normal, x.shape)
+
+
+class Sphere:
+    """dynamics.py:215-234"""
+
+    def __init__(self, center, radius):
+        self.center = np.asarray(center, dtype=np.float64)
+        self.radius = float(radius)
+
+    def signed_distance(self, x):
+        return np.linalg.norm(x - self.center, axis=1) - self.radius
+
+    def project(self, x):
+        r = x - self.center
+        dist = np.linalg.norm(r, axis=1)
+        n = r / np.maximum(dist, 1e-12)[:, None]
+        n[dist < 1e-12] = (0.0, 0.0, 1.0)
+        return self.center + self.radius * n, n
+
+
+class Torus:
+    """dynamics.py:237-270 (axis z through the center; on-axis points keep
+    the reference's ring choice: only the x component is replaced by R)"""
+
+    def __init__(self, center, major_radius, minor_radius):
+        self.center = np.asarray(center, dtype=np.float64)
+        self.R, self.r = float(major_radius), float(minor_radius)
+
+    def _ring(self, x):
+        local = x - self.center
+        radial = np.linalg.norm(local[:, :2], axis=1)
+        safe = np.maximum(radial, 1e-12)
+        ring = np.zeros_like(local)
+        ring[:, 0] = self.R * local[:, 0] / safe
+        ring[:, 1] = self.R * local[:, 1] / safe
+        ring[radial < 1e-12, 0] = self.R
+        return local, ring
+
+    def signed_distance(self, x):
+        local, ring = self._ring(x)
+        return np.linalg.norm(local - ring, axis=1) - self.r
+
+    def project(self, x):
+        local, ring = self._ring(x)
+        q = local - ring
+        dist = np.linalg.norm(q, axis=1)
+        n = q / np.maximum(dist, 1e-12)[:, None]
+        n[dist < 1e-12] = (0.0, 0.0, 1.0)
+        return self.center + ring + self.r * n, n
+
+
+def update_collisions(sys, q_l, x):
+    """Active constraints (idx, t, n), collider-major (dynamics.py:486-516)."""
+    idx, ts, ns = [], [], []
+    for col in sys.colliders or ():
+        pen = np.nonzero(col.signed_distance(x) < 0)[0]
+        if pen.size == 0:
+            continue
+        t, nrm = col.project(x[pen])
+        vn = np.einsum("kc,kc->k", (x[pen] - q_l[pen]) / sys.h, nrm)
+        keep = (vn < 0.0) | (col.signed_distance(q_l[pen]) < 0.0)
+        if np.any(keep):
+            idx.append(pen[keep])
+            ts.append(t[keep])
+            ns.append(nrm[keep])
+    if not idx:
+        return None
+    return np.concatenate(idx), np.concatenate(ts), np.concatenate(ns)
+
+
+def collision_energy(sys, cons, x):
+    """dynamics.py:446-450"""
+    if cons is None:
+        return 0.0
+    depth = np.einsum("kc,kc->k", x[cons[0]] - cons[1], cons[2])
+    return float(sys.w_col * np.dot(depth, depth))
+
+
+def add_collision_gradient(sys, cons, x, out):
+    """dynamics.py:453-457"""
+    if cons is None:
+        return
+    depth = np.einsum("kc,kc->k", x[cons[0]] - cons[1], cons[2])
+    np.add.at(out, cons[0], 2.0 * sys.w_col * depth[:, None] * cons[2])
 
 
 def inertia_target(sys, q_l, q_prev, fixed_targets=None):
@@ -453,20 +561,22 @@ def inertia_target(sys, q_l, q_prev, fixed_targets=None):
     return y
 
 
-def objective(sys, y, x):
-    """dynamics.py:460-467 (no colliders)."""
+def objective(sys, y, x, cons=None):
+    """dynamics.py:460-467."""
     d = x - y
     g = 0.5 / sys.h ** 2 * float(np.einsum("vc,v,vc->", d, sys.masses, d))
     for grp in sys.groups:
         g += grp.energy(x)
+    g += collision_energy(sys, cons, x)
     return g
 
 
-def gradient(sys, y, x):
-    """dynamics.py:470-478: inertia, then elastic scatter, then zero fixed rows."""
+def gradient(sys, y, x, cons=None):
+    """dynamics.py:470-478: inertia, elastic scatter, collisions, then zero fixed rows."""
     out = (sys.masses[:, None] / sys.h ** 2) * (x - y)
     for grp in sys.groups:
         grp.add_gradient(x, out)
+    add_collision_gradient(sys, cons, x, out)
     if sys.fixed.size:
         out[sys.fixed] = 0.0
     return out
@@ -514,7 +624,7 @@ def direction(sys, hist, grad):
     return r
 
 
-def line_search(sys, y, x, d, g_x, grad, gamma=0.3, alpha_init=2.0, shrink=0.5):
+def line_search(sys, y, x, d, g_x, grad, gamma=0.3, alpha_init=2.0, shrink=0.5, cons=None):
     """Armijo backtracking (solvers.py:241-257)."""
     slope = float(np.vdot(grad, d))
     if slope >= 0.0:
@@ -526,7 +636,7 @@ def line_search(sys, y, x, d, g_x, grad, gamma=0.3, alpha_init=2.0, shrink=0.5):
             raise OracleStagnation("alpha underflow")
         trials += 1
         x_new = x + alpha * d
-        g_new = objective(sys, y, x_new)
+        g_new = objective(sys, y, x_new, cons)
         if g_new <= g_x + gamma * alpha * slope:
             return alpha, x_new, g_new, trials
 
@@ -553,7 +663,8 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
     hist = History(m)
     prev_x = prev_g = None
     grad_tol = 1e-12 * sys.scale * max(1.0, float(sys.masses.max()) / sys.h ** 2)
-    rec.g0 = objective(sys, y, x)
+    cons = update_collisions(sys, q_l, x) if sys.colliders else None   # solvers.py:280
+    rec.g0 = objective(sys, y, x, cons)
 
     def log(g, tr, a):
         rec.g.append(g)
@@ -562,8 +673,10 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
         rec.cum_ms.append(1000.0 * (time.perf_counter() - t0))
 
     for _ in range(iterations):
-        g_x = objective(sys, y, x)
-        grad = gradient(sys, y, x)
+        if sys.colliders:
+            cons = update_collisions(sys, q_l, x)                         # solvers.py:285
+        g_x = objective(sys, y, x, cons)
+        grad = gradient(sys, y, x, cons)
         if kind == "lbfgs" and prev_x is not None:
             hist.push(x - prev_x, grad - prev_g)
         if float(np.linalg.norm(grad)) <= grad_tol:
@@ -578,7 +691,8 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
                 prev_x, prev_g = x, grad
                 continue
             try:
-                alpha, x_new, g_new, trials = line_search(sys, y, x, d, g_x, grad, gamma, alpha_init, shrink)
+                alpha, x_new, g_new, trials = line_search(sys, y, x, d, g_x, grad, gamma, alpha_init, shrink,
+                                                          cons)
             except OracleStagnation:
                 rec.stagnated = True
                 while len(rec.g) < iterations:
@@ -586,7 +700,7 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
                 break
         else:
             alpha, x_new, trials = 1.0, x + d, 1
-            g_new = objective(sys, y, x_new)
+            g_new = objective(sys, y, x_new, cons)
         prev_x, prev_g = x, grad
         x = x_new
         log(g_new, trials, alpha)

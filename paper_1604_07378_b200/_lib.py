@@ -67,7 +67,17 @@ class SystemDesc(C.Structure):
         ("a_nnz", C.c_int64), ("a_indptr", C.c_void_p), ("a_indices", C.c_void_p), ("a_values", C.c_void_p),
         ("free_coords", C.c_void_p),
         ("solver", C.c_int32), ("pcg_maxit", C.c_int32), ("pcg_tol", C.c_double),
+        ("n_colliders", C.c_int64), ("colliders", C.c_void_p), ("w_col", C.c_double),
     ]
+
+
+class Collider(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("p", C.c_double * 3), ("n", C.c_double * 3),
+                ("r0", C.c_double), ("r1", C.c_double)]
+
+
+QN_COL_HALFSPACE, QN_COL_SPHERE, QN_COL_TORUS = 0, 1, 2
+QN_MAX_COLLIDERS = 4
 
 
 class SlabDesc(C.Structure):

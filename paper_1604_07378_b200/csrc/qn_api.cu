@@ -411,6 +411,11 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   QN_REQUIRE(d->n_tets == 0 || (d->tets && d->Dm_inv && d->vols && d->mats), QN_ERR_ARG, "system: missing tets");
   QN_REQUIRE(d->masses && d->a_indptr && d->a_indices && d->a_values, QN_ERR_ARG, "system: missing arrays");
   QN_REQUIRE(d->h > 0, QN_ERR_ARG, "system: h must be positive");
+  QN_REQUIRE(d->n_colliders >= 0 && d->n_colliders <= QN_MAX_COLLIDERS && (d->n_colliders == 0 || d->colliders),
+             QN_ERR_ARG, "system: colliders");
+  for (int64_t k = 0; k < d->n_colliders; ++k)
+    QN_REQUIRE(d->colliders[k].kind >= QN_COL_HALFSPACE && d->colliders[k].kind <= QN_COL_TORUS, QN_ERR_ARG,
+               "system: unknown collider kind");
   const int64_t n = d->n_verts, mt = d->n_tets, ni = d->n_inst;
   QN_REQUIRE(n * ni < (int64_t)1 << 31 && mt * 4 < (int64_t)1 << 31, QN_ERR_ARG, "system: too large");
   qn_system* S = new qn_system();
@@ -591,6 +596,20 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_fixed = (int32_t)d->n_fixed;
   v.nblk_v = div_up(3 * n, kVertexThreads);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, 128));
+  if (d->n_colliders > 0) {  // colliders: per (instance, vertex, collider) constraint state
+    const int64_t nc = d->n_colliders;
+    qn_collider* dc;
+    if ((rc = sys_upload(S, &dc, d->colliders, (size_t)nc)) ||
+        (rc = sys_alloc(S, &v.col_act, (size_t)ni * n * nc)) || (rc = sys_alloc(S, &v.col_t, (size_t)ni * n * nc * 3)) ||
+        (rc = sys_alloc(S, &v.col_n, (size_t)ni * n * nc * 3)) || (rc = sys_alloc(S, &v.col_g, (size_t)ni * n * 3)) ||
+        (rc = sys_alloc(S, &v.part_c, (size_t)ni * div_up(n, kVertexThreads))) ||
+        (rc = sys_alloc(S, &v.cnt_c, (size_t)ni)))
+      return fail(rc);
+    v.cols = dc;
+    v.n_col = (int32_t)nc;
+    v.nblk_c = div_up(n, kVertexThreads);
+    v.w_col = d->w_col;
+  }
   v.h = d->h;
   for (int a = 0; a < 3; ++a) v.grav[a] = d->gravity[a];
   const size_t vec = (size_t)ni * n * 3;

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
       }
       for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + (size_t)__ldg(v.v2e + e) * 3));
     }
+    if (v.n_col) g = __dadd_rn(g, v.col_g[oc]);  // add_collision_gradient (dynamics.py:476)
     if (v.is_fixed[i]) g = 0.0;
     v.Gr[vec_off(v, gnew, b) + ci] = g;
     acc[0] = g * g;
@@ -455,10 +456,12 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
 // one thread; e_el / inert / slope are the block-parallel sums of the partials
 __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el, double inert, double slope) {
   const DevConfig& cfg = *v.cfg;
-  const double g_new = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
+  const double e_base = (0.5 / __dmul_rn(v.h, v.h)) * inert + e_el;  // dynamics.py:463-465
+  const double g_new = v.n_col ? e_base + c.e_col : e_base;          // + collision_energy (:466)
   const int ph = c.phase;
   if (ph == PH_FIRST) {
     c.g0 = c.g_x = g_new;
+    c.e_base = e_base;
     c.phase = PH_GRAD;
     return;
   }
@@ -497,6 +500,7 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
     c.xs_prev = c.xs_cur;
     c.xs_cur = c.xs_trial;
     c.g_x = g_new;
+    c.e_base = e_base;
     record(v, b, c, g_new, c.trials, cfg.line_search ? c.alpha : 1.0);
     c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;
   } else {
@@ -511,6 +515,147 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
     }
   }
   if (c.phase == PH_DONE) atomicSub(v.active, 1);
+}
+
+// ---------------------------------------------------------------------------
+// colliders (dynamics.py:199-285): signed distance and projection per kind
+
+__device__ __forceinline__ double norm3(double a, double b, double c) { return sqrt((a * a + b * b) + c * c); }
+
+// torus ring point of `local` (TorusCollider._ring, dynamics.py:244-255), including
+// the reference's treatment of on-axis points (only the x component is replaced)
+__device__ __forceinline__ void torus_ring(const qn_collider& C, const double* local, double* ring) {
+  const double radial = sqrt(local[0] * local[0] + local[1] * local[1]);
+  const double safe = fmax(radial, 1e-12);
+  ring[0] = radial < 1e-12 ? C.r0 : C.r0 * local[0] / safe;
+  ring[1] = C.r0 * local[1] / safe;
+  ring[2] = 0.0;
+}
+
+__device__ double col_sdist(const qn_collider& C, const double* x) {
+  if (C.kind == QN_COL_HALFSPACE)
+    return (x[0] - C.p[0]) * C.n[0] + (x[1] - C.p[1]) * C.n[1] + (x[2] - C.p[2]) * C.n[2];
+  if (C.kind == QN_COL_SPHERE) return norm3(x[0] - C.p[0], x[1] - C.p[1], x[2] - C.p[2]) - C.r0;
+  double l[3] = {x[0] - C.p[0], x[1] - C.p[1], x[2] - C.p[2]}, ring[3];
+  torus_ring(C, l, ring);
+  return norm3(l[0] - ring[0], l[1] - ring[1], l[2] - ring[2]) - C.r1;
+}
+
+// surface point t and outward normal n of a penetrating vertex (project, :207-270)
+__device__ void col_project(const qn_collider& C, const double* x, double* t, double* n) {
+  if (C.kind == QN_COL_HALFSPACE) {
+    const double sd = col_sdist(C, x);
+    for (int a = 0; a < 3; ++a) {
+      t[a] = x[a] - sd * C.n[a];
+      n[a] = C.n[a];
+    }
+    return;
+  }
+  double q[3], base[3], rad;
+  if (C.kind == QN_COL_SPHERE) {
+    for (int a = 0; a < 3; ++a) {
+      q[a] = x[a] - C.p[a];
+      base[a] = C.p[a];
+    }
+    rad = C.r0;
+  } else {
+    double l[3] = {x[0] - C.p[0], x[1] - C.p[1], x[2] - C.p[2]}, ring[3];
+    torus_ring(C, l, ring);
+    for (int a = 0; a < 3; ++a) {
+      q[a] = l[a] - ring[a];
+      base[a] = C.p[a] + ring[a];
+    }
+    rad = C.r1;
+  }
+  const double dist = norm3(q[0], q[1], q[2]);
+  const double safe = fmax(dist, 1e-12);
+  for (int a = 0; a < 3; ++a) n[a] = q[a] / safe;
+  if (dist < 1e-12) n[0] = n[1] = 0.0, n[2] = 1.0;
+  for (int a = 0; a < 3; ++a) t[a] = base[a] + rad * n[a];
+}
+
+// which = 0 (before k_grad, PH_GRAD): rebuild the active set at the current
+//   iterate (update_collisions, dynamics.py:486-516), its gradient terms
+//   2 w_col depth n (:453-457) and g_x = objective(x) with the new set
+//   (solvers.py:285-286);
+// which = 1 (before k_tet, evaluation phases): collision energy at the trial
+//   (PH_FIRST: the set is first built at x = y, solvers.py:280-281).
+__global__ void __launch_bounds__(kVT) k_col(SysView v, int which) {
+  const int b = blockIdx.y;
+  InstCtl* cc = v.ctl + b;
+  const int ph = cc->phase;
+  bool rebuild;
+  int xs;
+  if (which == 0) {
+    if (ph != PH_GRAD) return;
+    rebuild = true;
+    xs = cc->xs_cur;
+  } else {
+    if (ph != PH_FIRST && ph != PH_DIR && ph != PH_ALPHA) return;
+    rebuild = ph == PH_FIRST;
+    xs = cc->xs_trial;
+  }
+  __shared__ double red[32];
+  double e[1] = {0.0};
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    const size_t o = inst_off(v, b) + (size_t)i * 3;
+    const double* xp = v.X + vec_off(v, xs, b) + (size_t)i * 3;
+    const double x[3] = {xp[0], xp[1], xp[2]};
+    const double w2 = 2.0 * v.w_col;
+    double g[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < v.n_col; ++k) {
+      const size_t ck = ((size_t)b * v.n + i) * v.n_col + k;
+      const qn_collider& C = v.cols[k];
+      double* t = v.col_t + 3 * ck;
+      double* nr = v.col_n + 3 * ck;
+      if (rebuild) {
+        bool act = false;
+        if (col_sdist(C, x) < 0.0) {
+          double tt[3], nn[3];
+          col_project(C, x, tt, nn);
+          const double* ql = v.q_l + o;
+          const double vn = ((x[0] - ql[0]) / v.h) * nn[0] + ((x[1] - ql[1]) / v.h) * nn[1] +
+                            ((x[2] - ql[2]) / v.h) * nn[2];
+          act = vn < 0.0 || col_sdist(C, ql) < 0.0;
+          for (int a = 0; a < 3; ++a) {
+            t[a] = tt[a];
+            nr[a] = nn[a];
+          }
+        }
+        v.col_act[ck] = act ? 1 : 0;
+      }
+      if (v.col_act[ck]) {
+        const double depth = (x[0] - t[0]) * nr[0] + (x[1] - t[1]) * nr[1] + (x[2] - t[2]) * nr[2];
+        e[0] = fma(depth, depth, e[0]);
+        if (which == 0)
+          for (int a = 0; a < 3; ++a) g[a] += (w2 * depth) * nr[a];
+      }
+    }
+    if (which == 0)
+      for (int a = 0; a < 3; ++a) v.col_g[o + a] = g[a];
+  }
+  block_sum<1>(e, red);
+  if (threadIdx.x == 0) v.part_c[(size_t)b * v.nblk_c + blockIdx.x] = e[0];
+  if (last_block(v.cnt_c, 0, b, v.n_inst, gridDim.x)) {
+    __shared__ double tot[1];
+    sum_partials(v.part_c + (size_t)b * v.nblk_c, gridDim.x, 1, 1, tot);
+    if (threadIdx.x == 0) {
+      const double ec = v.w_col * tot[0];  // collision_energy (dynamics.py:446-450)
+      if (which == 0) {
+        cc->g_x = cc->e_base + ec;  // objective(x) with the new set
+      } else {
+        cc->e_col = ec;
+      }
+    }
+  }
+}
+
+int launch_col(qn_system* S, int which, cudaStream_t st) {
+  if (!S->v.n_col) return QN_OK;
+  k_col<<<dim3(S->v.nblk_c, S->v.n_inst), kVT, 0, st>>>(S->v, which);
+  QN_CHECK_LAUNCH();
+  return QN_OK;
 }
 
 // per-tet pass at the trial point: energy partials + corner forces
@@ -1245,6 +1390,7 @@ __global__ void __launch_bounds__(kPT) k_pcg_store(SysView v) {
 int launch_body_pre(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const dim3 gv(v.nblk_v, v.n_inst);
+  if (int rc = launch_col(S, 0, st)) return rc;
   if (S->h_cfg.m <= 5) {  // default window: smaller register footprint
     k_grad<5><<<gv, kVT, 0, st>>>(v);
   } else {
@@ -1293,6 +1439,7 @@ int launch_body_post(qn_system* S, cudaStream_t st) {
   QN_CHECK_LAUNCH();
   k_vec<<<gv, kVT, 0, st>>>(v);
   QN_CHECK_LAUNCH();
+  if (int rc = launch_col(S, 1, st)) return rc;
   if (v.n_mat <= kMatSmem) {
     k_tet<true><<<gt, kTT, 0, st>>>(v);
   } else {

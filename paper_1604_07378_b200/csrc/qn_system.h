@@ -32,6 +32,7 @@ struct InstCtl {
   int32_t npairs, have_prev, pad0, pad1;
   int32_t ring[kMaxM + 1];
   double g0, g_x, alpha, slope;
+  double e_base, e_col;  // colliders: objective without the collision term at x; collision term at the trial
   unsigned long long t0;
   double rho[kMaxM + 1];
   double sg[kMaxM + 1];
@@ -156,6 +157,16 @@ struct SysView {
   const AmgDevLevel* alev;  // [amg_levels] (device)
   const double* cinv;       // dense inverse of the coarsest operator [ncoarse][ncoarse]
   double* pz;               // z = B r (the V-cycle output on level 0)
+  // ---- colliders (dynamics.py:199-285, 446-457, 486-516) ----
+  int32_t n_col, nblk_c;
+  double w_col;
+  const qn_collider* cols;  // [n_col]
+  uint8_t* col_act;         // [inst][n][n_col] active constraint of (vertex, collider)
+  double* col_t;            // [inst][n][n_col][3] surface point
+  double* col_n;            // [inst][n][n_col][3] outward normal
+  double* col_g;            // [inst][n][3] collision gradient at the current iterate
+  double* part_c;           // [inst][nblk_c]
+  unsigned* cnt_c;          // [inst]
 };
 
 }  // namespace qn

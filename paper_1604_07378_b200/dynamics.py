@@ -10,7 +10,8 @@ configs[3] case: many instances of one mesh with per-instance materials and
 numeric factors.
 
 Out of the B200 hot-path scope ("next" rows): ARAP / spring PD
-groups, anisotropic fibres and colliders raise NotImplementedError.
+groups and anisotropic fibres raise NotImplementedError; colliders (HalfSpace,
+SphereCollider, TorusCollider) run inside the frame graph.
 """
 
 from __future__ import annotations
@@ -65,6 +66,58 @@ class VLGroup:
         _lib.check(_lib.load().qn_system_elements(self._system._h, self._inst, self._index, _lib.ptr(xs),
                                                   C.byref(e), _lib.ptr(buf), _lib.QN_MEM_HOST, None), "group grad")
         out[...] = buf
+
+
+class HalfSpace:
+    """dynamics.py:199-212: keeps vertices on the positive side of a plane."""
+
+    def __init__(self, point, normal):
+        self.point = np.asarray(point, dtype=np.float64)
+        n = np.asarray(normal, dtype=np.float64)
+        self.normal = n / np.linalg.norm(n)
+
+    def signed_distance(self, x):
+        return (x - self.point) @ self.normal
+
+    def to_c(self):
+        c = _lib.Collider()
+        c.kind = _lib.QN_COL_HALFSPACE
+        c.p[:], c.n[:] = self.point, self.normal
+        return c
+
+
+class SphereCollider:
+    """dynamics.py:215-234: keeps vertices outside a solid sphere."""
+
+    def __init__(self, center, radius):
+        self.center = np.asarray(center, dtype=np.float64)
+        self.radius = float(radius)
+
+    def signed_distance(self, x):
+        return np.linalg.norm(x - self.center, axis=1) - self.radius
+
+    def to_c(self):
+        c = _lib.Collider()
+        c.kind = _lib.QN_COL_SPHERE
+        c.p[:] = self.center
+        c.r0 = self.radius
+        return c
+
+
+class TorusCollider:
+    """dynamics.py:237-270: keeps vertices outside a solid torus (axis z)."""
+
+    def __init__(self, center, major_radius, minor_radius):
+        self.center = np.asarray(center, dtype=np.float64)
+        self.R = float(major_radius)
+        self.r = float(minor_radius)
+
+    def to_c(self):
+        c = _lib.Collider()
+        c.kind = _lib.QN_COL_TORUS
+        c.p[:] = self.center
+        c.r0, c.r1 = self.R, self.r
+        return c
 
 
 @dataclass
@@ -172,7 +225,7 @@ def _pattern_sum(rows, cols, n):
 
 
 def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, solver="direct", pcg_tol=1e-10,
-           pcg_maxit=20000):
+           pcg_maxit=20000, colliders=(), collision_weight=None):
     if not isinstance(mesh, TetMesh):
         raise NotImplementedError("spring networks (cloth) are outside the B200 hot path")
     _lib.require_gpu()
@@ -269,6 +322,16 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
         raise DynamicsError(f"unknown solver {solver!r} (direct | pcg | amg)")
     d.solver = {"direct": 0, "pcg": 1, "amg": 2}[solver]
     d.pcg_tol, d.pcg_maxit = float(pcg_tol), int(pcg_maxit)
+    colliders = list(colliders)
+    if len(colliders) > _lib.QN_MAX_COLLIDERS:
+        raise DynamicsError(f"at most {_lib.QN_MAX_COLLIDERS} colliders")
+    for col in colliders:
+        if not hasattr(col, "to_c"):
+            raise DynamicsError(f"unknown collider {col!r}")
+    ccols = (_lib.Collider * max(1, len(colliders)))(*[col.to_c() for col in colliders])
+    max_w = max((float(grp.w.max()) for gl in groups_per_inst for grp in gl if grp.w.size), default=0.0)
+    w_col = float(collision_weight) if collision_weight is not None else 10.0 * max_w  # dynamics.py:417
+    d.n_colliders, d.colliders, d.w_col = len(colliders), C.cast(ccols, C.c_void_p), w_col
     handle = C.c_void_p()
     _lib.check(_lib.load().qn_system_create(C.byref(d), C.byref(handle)), "build_system")
     sysfact = None
@@ -280,7 +343,7 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     system = SimSystem(mesh=mesh, masses=masses, h=float(h), gravity=np.asarray(gravity, dtype=np.float64),
                        groups=groups_per_inst[0] if n_inst == 1 else groups_per_inst, fixed=fixed, free=free,
                        L=Ls[0] if n_inst == 1 else Ls, sysfact=sysfact, scale=scale, n_inst=n_inst,
-                       materials=mats, a_nnz=int(a_indices.size), _h=handle)
+                       materials=mats, a_nnz=int(a_indices.size), colliders=colliders, w_col=w_col, _h=handle)
     for b, gl in enumerate(groups_per_inst):
         for g, grp in enumerate(gl):
             grp._system, grp._index, grp._inst = system, g, b
@@ -300,14 +363,14 @@ def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_G
     (same tolerance, ~40x fewer iterations on configs[4])."""
     if aniso:
         raise NotImplementedError("anisotropic fibres are outside the B200 hot path (SURVEY §8f)")
-    if colliders:
-        raise NotImplementedError("colliders are outside the B200 hot path (SURVEY §8f)")
     assign = _assign(mesh, materials)
-    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit)
+    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit,
+                  colliders, collision_weight)
 
 
 def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(),
-                       fit_interval: FitInterval = FitInterval()) -> SimSystem:
+                       fit_interval: FitInterval = FitInterval(), colliders=(),
+                       collision_weight: float | None = None) -> SimSystem:
     """configs[3]: independent instances of one mesh, one MaterialModel (or
     group assignment) per instance, each with its own factored A."""
     inst = [_assign(mesh, m) for m in materials_per_instance]
@@ -316,7 +379,8 @@ def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP
     sizes = {len(a) for a in inst}
     if len(sizes) != 1:
         raise DynamicsError("all instances need the same material-group layout")
-    return _build(mesh, inst, h, gravity, fixed, fit_interval, len(inst[0]))
+    return _build(mesh, inst, h, gravity, fixed, fit_interval, len(inst[0]), colliders=colliders,
+                  collision_weight=collision_weight)
 
 
 def inertia_target(state: SimState, system: SimSystem, fixed_targets=None) -> np.ndarray:

@@ -127,8 +127,6 @@ def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fix
     records for batch systems (solvers.py:260-352).  `out` (optional, not in
     the reference signature): a SimState whose q_l / y arrays (float64,
     C-contiguous, e.g. page-locked) receive x and y instead of new arrays."""
-    if system.colliders:
-        raise NotImplementedError("colliders are outside the B200 hot path")
     cfg = config.to_c()
     shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
     q_l = _lib.f64(state.q_l).reshape(shape)

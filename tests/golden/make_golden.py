@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick]
+    python tests/golden/make_golden.py [--quick] [--colliders (only the collider fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -34,7 +34,7 @@ from qnsim import mesh as ref_mesh  # noqa: E402
 from qnsim import solvers as ref_solvers  # noqa: E402
 
 from paper_1604_07378_b200 import scenes  # noqa: E402
-from tests.helpers import material_specs  # noqa: E402
+from tests.helpers import collider_bar_scene, material_specs  # noqa: E402
 
 
 def ref_material(spec, name="custom"):
@@ -154,17 +154,91 @@ def gen_frames(quick):
         print("c2 frame 0", time.time() - t)
 
 
+def ref_colliders(cols):
+    out = []
+    for c in cols:
+        if c[0] == "halfspace":
+            out.append(ref_dyn.HalfSpace(c[1], c[2]))
+        elif c[0] == "sphere":
+            out.append(ref_dyn.SphereCollider(c[1], c[2]))
+        else:
+            out.append(ref_dyn.TorusCollider(c[1], c[2], c[3]))
+    return out
+
+
+def gen_colliders():
+    """Colliders: the reference's own sphere_drop scenario
+    through its harness, and the three-collider bar through build_system."""
+    from qnsim import harness as ref_harness
+    t = time.time()
+    scn = ref_harness.load_scenario(os.path.join(REF, "scenarios", "sphere_drop.json"))
+    run = ref_harness.SimulationRun(scn)
+    g, tr, al, g0, pos = [], [], [], [], {}
+    frames = 30
+    for f in range(frames):
+        rec = run.step()
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+        al.append(rec.alphas)
+        g0.append(rec.g0)
+        if f in (0, 9, 19, 29):
+            pos[f"x_{f}"] = run.state.q_l.copy()
+    # the same scenario with the tet list reversed (identical mathematics, another
+    # summation order): penalty contact amplifies roundoff through active-set
+    # flips, so this run is the reference's own roundoff envelope for parity
+    mesh = run.system.mesh
+    rmesh = ref_mesh.TetMesh(vertices=mesh.vertices.copy(), tets=mesh.tets[::-1].copy(), density=mesh.density)
+    rsys = ref_dyn.build_system(rmesh, ref_harness._make_material(scn.material_spec), h=scn.h, gravity=scn.gravity,
+                                fixed=[], colliders=scn.colliders, collision_weight=scn.collision_weight,
+                                fit_interval=scn.fit_interval)
+    rstate = ref_dyn.SimState(q_l=mesh.vertices.copy(), q_prev=mesh.vertices.copy())
+    rg, rpos = [], {}
+    for f in range(frames):
+        rstate, rec = ref_solvers.simulate_frame(rsys, rstate, scn.solver)
+        rg.append(rec.g)
+        if f in (0, 9, 19, 29):
+            rpos[f"rev_x_{f}"] = rstate.q_l.copy()
+    np.savez_compressed(os.path.join(HERE, "frames_sphere_drop.npz"), frames=frames, g=np.array(g),
+                        trials=np.array(tr), alphas=np.array(al), g0=np.array(g0), w_col=run.system.w_col,
+                        rev_g=np.array(rg), **pos, **rpos)
+    sc, cols = collider_bar_scene()
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed,
+                                  colliders=ref_colliders(cols))
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = ref_solvers.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+    g, tr, al, g0, pos, ncol = [], [], [], [], {}, []
+    frames = 20
+    for f in range(frames):
+        state, rec = ref_solvers.simulate_frame(system, state, cfg)
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+        al.append(rec.alphas)
+        g0.append(rec.g0)
+        ncol.append(ref_dyn.update_collisions(system, state, state.q_l).count)
+        if f in (0, 4, 9, 19):
+            pos[f"x_{f}"] = state.q_l.copy()
+    np.savez_compressed(os.path.join(HERE, "frames_collider_bar.npz"), frames=frames, g=np.array(g),
+                        trials=np.array(tr), alphas=np.array(al), g0=np.array(g0), w_col=system.w_col,
+                        active=np.array(ncol), **pos)
+    print("colliders", time.time() - t, "active per frame", ncol)
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
     for src in ("frontend/tests/fixtures/twist_lbfgs.csv", "frontend/tests/fixtures/twist_pd_qn.csv",
-                "assets/bar_small.node", "assets/bar_small.ele", "scenarios/bar_twist_small.json"):
+                "assets/bar_small.node", "assets/bar_small.ele", "scenarios/bar_twist_small.json",
+                "assets/sphere.node", "assets/sphere.ele", "scenarios/sphere_drop.json"):
         shutil.copy(os.path.join(REF, src), os.path.join(dst, os.path.basename(src)))
 
 
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
     copy_fixtures()
+    if "--colliders" in sys.argv:
+        gen_colliders()
+        sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()
     gen_frames(quick)

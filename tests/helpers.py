@@ -83,3 +83,57 @@ def material_specs():
         "spline": scenes.nh_spline_spec(np.random.default_rng(11)),
         "poly_cubic": scenes.c5(grid=(2, 1, 1)).material,
     }
+
+
+def collider_bar_scene():
+    """A c1-style NH bar (10x3x3, x=0 face pinned) thrown down (v0 = -2 m/s in
+    z) onto a half-space, a sphere and a torus: every collider kind of
+    dynamics.py:199-270 is active within the first frames.  Collider specs:
+    (kind, ...) tuples, built by the caller for each implementation."""
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    v0 = np.zeros_like(sc.verts)
+    v0[:, 2] = -2.0
+    v0[sc.fixed] = 0.0
+    sc.q_prev = sc.q_l - sc.h * v0
+    cols = [("halfspace", (0.0, 0.0, -0.08), (0.0, 0.1, 1.0)),
+            ("sphere", (0.75, 0.15, -0.25), 0.27),
+            ("torus", (0.35, 0.15, -0.16), 0.2, 0.12)]
+    return sc, cols
+
+
+def make_colliders(cols, ns):
+    """Collider objects of module `ns` (oracle: HalfSpace/Sphere/Torus;
+    package dynamics: HalfSpace/SphereCollider/TorusCollider)."""
+    sphere = getattr(ns, "SphereCollider", None) or ns.Sphere
+    torus = getattr(ns, "TorusCollider", None) or ns.Torus
+    out = []
+    for c in cols:
+        if c[0] == "halfspace":
+            out.append(ns.HalfSpace(c[1], c[2]))
+        elif c[0] == "sphere":
+            out.append(sphere(c[1], c[2]))
+        else:
+            out.append(torus(c[1], c[2], c[3]))
+    return out
+
+
+class SphereDropScene:
+    """The reference's sphere_drop.json (corotated sphere mesh dropped on a
+    half-space, collision_weight 3e5, 20 iterations), as run by its harness
+    for tests/golden/frames_sphere_drop.npz."""
+
+    def __init__(self):
+        with open(os.path.join(FIX, "sphere_drop.json")) as fh:
+            scn = json.load(fh)
+        self.verts, self.tets = O.read_node_ele(os.path.join(FIX, "sphere.node"), os.path.join(FIX, "sphere.ele"))
+        self.h = float(scn["h"])
+        self.gravity = tuple(scn["gravity"])
+        self.density = float(scn["mesh"]["density"])
+        self.material = scenes.builtin_spec("corotated", float(scn["material"]["mu"]), float(scn["material"]["lambda"]))
+        self.iterations = int(scn["solver"]["iterations"])
+        self.m = int(scn["solver"].get("m", 5))
+        self.collision_weight = float(scn["collision_weight"])
+        self.cols = [("halfspace", tuple(c["point"]), tuple(c["normal"])) for c in scn["colliders"]]
+        self.fixed = np.zeros(0, dtype=np.int64)
+        self.q_l = self.verts.copy()
+        self.q_prev = self.verts.copy()

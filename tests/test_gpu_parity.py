@@ -523,3 +523,80 @@ def test_factorization_reuse_bit_identical():
     X1 = system.sysfact.solve(B)
     X2 = system.sysfact.solve(B)
     assert np.array_equal(X1, X2)
+
+
+# ---- colliders -----------------------------------------------
+
+def _gpu_collider_run(sc, cols, frames, collision_weight=None, graph=True):
+    from tests.helpers import make_colliders
+    from paper_1604_07378_b200 import dynamics as D
+    system = build(sc, colliders=make_colliders(cols, D), collision_weight=collision_weight)
+    if not graph:
+        system.set_graph_mode(False)
+    return system, run_gpu(system, sc, frames)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_colliders_three_kinds_against_reference_golden(graph):
+    """Half-space, sphere and torus penalties (update_collisions every
+    iteration, dynamics.py:486-516) inside the frame graph: the reference's
+    own trajectory (tests/golden/frames_collider_bar.npz)."""
+    from tests.helpers import collider_bar_scene
+    sc, cols = collider_bar_scene()
+    d = golden("frames_collider_bar.npz")
+    system, res = _gpu_collider_run(sc, cols, int(d["frames"]), graph=graph)
+    assert system.w_col == float(d["w_col"])
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d["g"][f]) <= G_TOL
+        assert rec.ls_trials == list(d["trials"][f])
+        if f"x_{f}" in d:
+            assert rel(x, d[f"x_{f}"]) <= X_TOL
+
+
+def test_sphere_drop_scenario_against_reference_harness():
+    """The reference's bundled sphere_drop.json scenario, 30 frames.  Penalty
+    contact amplifies roundoff through active-set flips: the reference itself,
+    run with its tet list reversed (same mathematics, another summation
+    order), departs from its own trajectory by 1e-12 at frame 2 and by ~4e-2
+    in g / ~5e-4 in x once the sphere rests on the floor (golden rev_*).  The
+    B200 run must match strictly until contact and stay inside 4x that
+    envelope after it."""
+    from tests.helpers import SphereDropScene
+    sd = SphereDropScene()
+    d = golden("frames_sphere_drop.npz")
+    _, res = _gpu_collider_run(sd, sd.cols, int(d["frames"]), collision_weight=sd.collision_weight)
+    g_ref, g_rev = d["g"], d["rev_g"]
+    env_g = max(np.abs(g_rev[f] - g_ref[f]).max() / np.abs(g_ref[f]).max() for f in range(2, g_ref.shape[0]))
+    env_x = max(rel(d[f"rev_x_{f}"], d[f"x_{f}"]) for f in (9, 19, 29))
+    for f, (x, rec) in enumerate(res):
+        if f <= 3:  # before contact: the strict parity bar
+            np.testing.assert_allclose(rec.g, g_ref[f], rtol=G_TOL, atol=1e-12)
+            assert rec.ls_trials == list(d["trials"][f])
+        else:
+            assert np.abs(np.array(rec.g) - g_ref[f]).max() / np.abs(g_ref[f]).max() <= 4 * env_g
+        if f"x_{f}" in d:
+            assert rel(x, d[f"x_{f}"]) <= (X_TOL if f == 0 else 4 * env_x)
+
+
+def test_colliders_batch_instances_match_single():
+    """Batched instances (configs[3] machinery) with colliders: identical
+    instances stay bitwise identical, and equal the single-system run within
+    the parity tolerance (the batched solve sums in another order)."""
+    from tests.helpers import collider_bar_scene, make_colliders
+    from paper_1604_07378_b200 import dynamics as D
+    sc, cols = collider_bar_scene()
+    mesh = Q.TetMesh(sc.verts, sc.tets, sc.density)
+    mat = from_spec(sc.material)
+    bsys = Q.build_batch_system(mesh, [mat, mat, mat], h=sc.h, gravity=sc.gravity, fixed=sc.fixed,
+                                colliders=make_colliders(cols, D))
+    ssys = build(sc, colliders=make_colliders(cols, D))
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+    bst = Q.SimState(q_l=np.stack([sc.q_l] * 3), q_prev=np.stack([sc.q_prev] * 3))
+    sst = Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    for _ in range(3):
+        bst, brecs = Q.simulate_frame(bsys, bst, cfg)
+        sst, srec = Q.simulate_frame(ssys, sst, cfg)
+        for b in range(3):
+            assert np.array_equal(bst.q_l[b], bst.q_l[0]) and brecs[b].g == brecs[0].g
+            assert rel(bst.q_l[b], sst.q_l) <= X_TOL and rel(brecs[b].g, srec.g) <= G_TOL
+            assert brecs[b].ls_trials == srec.ls_trials

@@ -127,3 +127,40 @@ def test_sparse_factor_equals_dense():
     B = np.random.default_rng(0).standard_normal((a.free.size, 3))
     xa, xb = a.factor.solve(B), b.factor.solve(B)
     assert np.abs(xa - xb).max() <= 1e-13 * np.abs(xa).max()
+
+
+# ---- colliders: oracle vs the reference's own runs ----------
+
+def _collider_frames(sys_, sc, frames):
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(frames):
+        x, _, rec = O.simulate_frame(sys_, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        yield f, x, rec
+
+
+def test_oracle_colliders_three_kinds_match_reference():
+    from tests.helpers import collider_bar_scene, make_colliders
+    sc, cols = collider_bar_scene()
+    d = golden("frames_collider_bar.npz")
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense", colliders=make_colliders(cols, O))
+    assert osys.w_col == float(d["w_col"])
+    for f, x, rec in _collider_frames(osys, sc, 10):
+        np.testing.assert_allclose(rec.g, d["g"][f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(d["trials"][f])
+        if f"x_{f}" in d:
+            np.testing.assert_allclose(x, d[f"x_{f}"], rtol=0, atol=1e-12 * np.abs(d[f"x_{f}"]).max())
+
+
+def test_oracle_sphere_drop_matches_reference_harness():
+    from tests.helpers import SphereDropScene, make_colliders
+    sd = SphereDropScene()
+    d = golden("frames_sphere_drop.npz")
+    osys = O.build(sd.verts, sd.tets, sd.density, oracle_material(sd.material), sd.h, sd.gravity, sd.fixed,
+                   factor="dense", colliders=make_colliders(sd.cols, O), collision_weight=sd.collision_weight)
+    for f, x, rec in _collider_frames(osys, sd, 10):  # contact starts at frame ~7
+        np.testing.assert_allclose(rec.g, d["g"][f], rtol=1e-12, atol=1e-12)
+        assert list(rec.ls_trials) == list(d["trials"][f])
+        if f"x_{f}" in d:
+            np.testing.assert_allclose(x, d[f"x_{f}"], rtol=0, atol=1e-12 * np.abs(d[f"x_{f}"]).max())

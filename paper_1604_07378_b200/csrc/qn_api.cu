@@ -753,12 +753,28 @@ void sell_build(int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t*
 
 static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t* ptr, const int32_t* col,
                        const double* val, qn::SellDevF* out) {
+  // layout by mean row length: short rows -> SELL-32 (lane per row), long rows
+  // (Galerkin coarse operators, restriction) -> CSR with K lanes per row
+  const int64_t nnz = ptr[nrows];
+  const double mean = nrows ? (double)nnz / (double)nrows : 0.0;
+  const int kl = mean <= 16.0 ? 0 : mean <= 32.0 ? 4 : mean <= 64.0 ? 8 : mean <= 128.0 ? 16 : 32;
+  int dev = 0, nsm = qn::kSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)nsm * qn::kSpmvBlocksPerSm;
   std::vector<int64_t> sp;
   std::vector<int32_t> sc;
   std::vector<double> sv;
-  sell_build(nrows, ncols, ptr, col, val, 1, ptr[nrows], sp, sc, sv);
+  if (kl == 0) {
+    sell_build(nrows, ncols, ptr, col, val, 1, nnz, sp, sc, sv);
+  } else {
+    sp.assign(ptr, ptr + nrows + 1);
+    sc.assign(col, col + nnz);
+    sv.assign(val, val + nnz);
+  }
   std::vector<float> sf(std::max<size_t>(sv.size(), 1), 0.0f);
   for (size_t k = 0; k < sv.size(); ++k) sf[k] = (float)sv[k];
+  if (sc.empty()) sc.push_back(0);
   int64_t* dp;
   int32_t* dc;
   float* dv;
@@ -769,8 +785,11 @@ static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t
   out->ptr = dp;
   out->col = dc;
   out->val = dv;
-  out->nslice = (int32_t)(sp.size() - 1);
+  out->nslice = kl == 0 ? (int32_t)(sp.size() - 1) : 0;
   out->nrows = (int32_t)nrows;
+  out->kl = kl;
+  const int64_t units = kl == 0 ? (nrows + 31) / 32 : (nrows + 32 / kl - 1) / (32 / kl);  // warps of work
+  out->nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>((units + qn::kSpmvWarps - 1) / qn::kSpmvWarps, cap));
   return QN_OK;
 }
 

@@ -1064,39 +1064,94 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
 // CG has converged.  Level l: x = w D^-1 b (fused into the residual), r = b -
 // A x, b_{l+1} = R r, ..., x += P t_{l+1}, t = x + w D^-1 (b - A x).
 
-// row sums of a SELL matrix times an (n x 3) vector for row 32 sl + lane
-__device__ __forceinline__ void sell_row3(const SellDevF& S, int sl, int lane, const double* __restrict__ X,
-                                          double (&acc)[3]) {
-  const int64_t e0 = S.ptr[sl], e1 = S.ptr[sl + 1];
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  int64_t e = e0 + lane;
-  for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
-    int j[kSellUnroll];
-    double a[kSellUnroll];
+// Row products y_i = sum_j a_ij X(j) (3 columns) of a V-cycle operator, for
+// every row, handed to `epi(i, acc)`.  Two layouts (chosen per operator at
+// upload from its mean row length, qn_api.cu sell_upload):
+//  * S.kl == 0: SELL-32, one warp per 32-row slice, lane = row (short rows:
+//    the fine-level operators of configs[4] have ~13 entries per row);
+//  * S.kl = K in {4, 8, 16, 32}: CSR, K lanes per row, 32/K rows per warp;
+//    the lanes of a row stride its entries (coalesced), a K-lane butterfly
+//    sums them (long rows: Galerkin coarse operators, restriction).
+// `xv(j, c)` returns column j's value (callers fuse scalings into it).
+template <class XV, class EPI>
+__device__ __forceinline__ void op_rows(const SellDevF& S, XV xv, EPI epi) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  if (S.kl == 0) {
+    for (int sl = w0; sl < S.nslice; sl += nw) {
+      const int64_t e1 = S.ptr[sl + 1];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      int64_t e = S.ptr[sl] + lane;
+      for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
+        int j[kSellUnroll];
+        double a[kSellUnroll];
 #pragma unroll
-    for (int u = 0; u < kSellUnroll; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
-      j[u] = __ldcs(S.col + e + 32 * u);
-      a[u] = (double)__ldcs(S.val + e + 32 * u);
+        for (int u = 0; u < kSellUnroll; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
+          j[u] = __ldcs(S.col + e + 32 * u);
+          a[u] = (double)__ldcs(S.val + e + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kSellUnroll; ++u) {
+          a0 = fma(a[u], xv(j[u], 0), a0);
+          a1 = fma(a[u], xv(j[u], 1), a1);
+          a2 = fma(a[u], xv(j[u], 2), a2);
+        }
+      }
+      for (; e < e1; e += 32) {
+        const int j = __ldcs(S.col + e);
+        const double a = (double)__ldcs(S.val + e);
+        a0 = fma(a, xv(j, 0), a0);
+        a1 = fma(a, xv(j, 1), a1);
+        a2 = fma(a, xv(j, 2), a2);
+      }
+      const int i = 32 * sl + lane;
+      if (i < S.nrows) {
+        const double acc[3] = {a0, a1, a2};
+        epi(i, acc);
+      }
     }
+    return;
+  }
+  const int K = S.kl, g = lane / K, q = lane % K, rpw = 32 / K;
+  for (int r0 = w0 * rpw; r0 < S.nrows; r0 += nw * rpw) {  // warp-uniform loop
+    const int i = r0 + g;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (i < S.nrows) {
+      const int64_t e1 = S.ptr[i + 1];
+      int64_t e = S.ptr[i] + q;
+      for (; e + (int64_t)K * 3 < e1; e += 4 * K) {  // 4 entries in flight per lane
+        int j[4];
+        double a[4];
 #pragma unroll
-    for (int u = 0; u < kSellUnroll; ++u) {
-      const double* xj = X + 3 * (size_t)j[u];
-      a0 = fma(a[u], xj[0], a0);
-      a1 = fma(a[u], xj[1], a1);
-      a2 = fma(a[u], xj[2], a2);
+        for (int u = 0; u < 4; ++u) {
+          j[u] = __ldcs(S.col + e + K * u);
+          a[u] = (double)__ldcs(S.val + e + K * u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a0 = fma(a[u], xv(j[u], 0), a0);
+          a1 = fma(a[u], xv(j[u], 1), a1);
+          a2 = fma(a[u], xv(j[u], 2), a2);
+        }
+      }
+      for (; e < e1; e += K) {
+        const int j = __ldcs(S.col + e);
+        const double a = (double)__ldcs(S.val + e);
+        a0 = fma(a, xv(j, 0), a0);
+        a1 = fma(a, xv(j, 1), a1);
+        a2 = fma(a, xv(j, 2), a2);
+      }
+    }
+    for (int o = K >> 1; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (q == 0 && i < S.nrows) {
+      const double acc[3] = {a0, a1, a2};
+      epi(i, acc);
     }
   }
-  for (; e < e1; e += 32) {
-    const int j = __ldcs(S.col + e);
-    const double a = (double)__ldcs(S.val + e);
-    const double* xj = X + 3 * (size_t)j;
-    a0 = fma(a, xj[0], a0);
-    a1 = fma(a, xj[1], a1);
-    a2 = fma(a, xj[2], a2);
-  }
-  acc[0] = a0;
-  acc[1] = a1;
-  acc[2] = a2;
 }
 
 __device__ __forceinline__ bool amg_on(const SysView& v) { return pcg_on(v, 0); }
@@ -1107,51 +1162,20 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
   const double w = L.omega;
-  const int lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
-  for (int sl = w0; sl < L.A.nslice; sl += nw) {
-    const int64_t e0 = L.A.ptr[sl], e1 = L.A.ptr[sl + 1];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    int64_t e = e0 + lane;
-    for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
-      int j[kSellUnroll];
-      double a[kSellUnroll];
-#pragma unroll
-      for (int u = 0; u < kSellUnroll; ++u) {
-        j[u] = __ldcs(L.A.col + e + 32 * u);
-        a[u] = (double)__ldcs(L.A.val + e + 32 * u);
-      }
-#pragma unroll
-      for (int u = 0; u < kSellUnroll; ++u) {
-        const double c = a[u] * w * __ldg(L.dinv + j[u]);
-        const double* bj = L.b + 3 * (size_t)j[u];
-        a0 = fma(c, bj[0], a0);
-        a1 = fma(c, bj[1], a1);
-        a2 = fma(c, bj[2], a2);
-      }
-    }
-    for (; e < e1; e += 32) {
-      const int j = __ldcs(L.A.col + e);
-      const double c = (double)__ldcs(L.A.val + e) * w * __ldg(L.dinv + j);
-      const double* bj = L.b + 3 * (size_t)j;
-      a0 = fma(c, bj[0], a0);
-      a1 = fma(c, bj[1], a1);
-      a2 = fma(c, bj[2], a2);
-    }
-    const int i = 32 * sl + lane;
-    if (i < L.n) {
-      const double wd = w * L.dinv[i];
-      const double* bi = L.b + 3 * (size_t)i;
-      double* xi = L.x + 3 * (size_t)i;
-      double* ri = L.r + 3 * (size_t)i;
-      xi[0] = wd * bi[0];
-      xi[1] = wd * bi[1];
-      xi[2] = wd * bi[2];
-      ri[0] = bi[0] - a0;
-      ri[1] = bi[1] - a1;
-      ri[2] = bi[2] - a2;
-    }
-  }
+  const double* __restrict__ b = L.b;
+  const double* __restrict__ dinv = L.dinv;
+  op_rows(
+      L.A, [&](int j, int c) { return w * __ldg(dinv + j) * b[3 * (size_t)j + c]; },
+      [&](int i, const double* a) {
+        const double wd = w * dinv[i];
+        const double* bi = b + 3 * (size_t)i;
+        double* xi = L.x + 3 * (size_t)i;
+        double* ri = L.r + 3 * (size_t)i;
+        for (int c = 0; c < 3; ++c) {
+          xi[c] = wd * bi[c];
+          ri[c] = bi[c] - a[c];
+        }
+      });
 }
 
 // b_{l+1} = R_l r_l
@@ -1159,19 +1183,13 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  const int lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
-  for (int sl = w0; sl < L.R.nslice; sl += nw) {
-    double a[3];
-    sell_row3(L.R, sl, lane, L.r, a);
-    const int i = 32 * sl + lane;
-    if (i < C.n) {
-      double* bi = C.b + 3 * (size_t)i;
-      bi[0] = a[0];
-      bi[1] = a[1];
-      bi[2] = a[2];
-    }
-  }
+  const double* __restrict__ r = L.r;
+  op_rows(
+      L.R, [&](int j, int c) { return r[3 * (size_t)j + c]; },
+      [&](int i, const double* a) {
+        double* bi = C.b + 3 * (size_t)i;
+        for (int c = 0; c < 3; ++c) bi[c] = a[c];
+      });
 }
 
 // coarsest level: t = A_c^-1 b (dense inverse, warp per row, b staged in shared memory)
@@ -1209,41 +1227,29 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  const int lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
-  for (int sl = w0; sl < L.P.nslice; sl += nw) {
-    double a[3];
-    sell_row3(L.P, sl, lane, C.t, a);
-    const int i = 32 * sl + lane;
-    if (i < L.n) {
-      double* xi = L.x + 3 * (size_t)i;
-      xi[0] += a[0];
-      xi[1] += a[1];
-      xi[2] += a[2];
-    }
-  }
+  const double* __restrict__ t = C.t;
+  op_rows(
+      L.P, [&](int j, int c) { return t[3 * (size_t)j + c]; },
+      [&](int i, const double* a) {
+        double* xi = L.x + 3 * (size_t)i;
+        for (int c = 0; c < 3; ++c) xi[c] += a[c];
+      });
 }
 
 // t = x + w D^-1 (b - A x)  (post-smoothing)
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(SysView v, int l) {
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
-  const int lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
-  for (int sl = w0; sl < L.A.nslice; sl += nw) {
-    double a[3];
-    sell_row3(L.A, sl, lane, L.x, a);
-    const int i = 32 * sl + lane;
-    if (i < L.n) {
-      const double wd = L.omega * L.dinv[i];
-      const double* bi = L.b + 3 * (size_t)i;
-      const double* xi = L.x + 3 * (size_t)i;
-      double* ti = L.t + 3 * (size_t)i;
-      ti[0] = fma(wd, bi[0] - a[0], xi[0]);
-      ti[1] = fma(wd, bi[1] - a[1], xi[1]);
-      ti[2] = fma(wd, bi[2] - a[2], xi[2]);
-    }
-  }
+  const double* __restrict__ x = L.x;
+  op_rows(
+      L.A, [&](int j, int c) { return x[3 * (size_t)j + c]; },
+      [&](int i, const double* a) {
+        const double wd = L.omega * L.dinv[i];
+        const double* bi = L.b + 3 * (size_t)i;
+        const double* xi = x + 3 * (size_t)i;
+        double* ti = L.t + 3 * (size_t)i;
+        for (int c = 0; c < 3; ++c) ti[c] = fma(wd, bi[c] - a[c], xi[c]);
+      });
 }
 
 // r.z after a V-cycle: init -> rz (beta stays 0); else beta = rz_new / rz
@@ -1343,10 +1349,9 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
   const int nl = (int)S->h_alev.size();
   for (int l = 0; l + 1 < nl; ++l) {
     const auto& L = S->h_alev[l];
-    k_amg_residual<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    k_amg_residual<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
-    const int gr = std::max(1, std::min(L.nblk, div_up(S->h_alev[l + 1].n, 32 * kSpmvWarps)));
-    k_amg_restrict<<<gr, kSpmvThreads, 0, st>>>(v, l);
+    k_amg_restrict<<<L.R.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
   }
   const int nc = v.ncoarse;
@@ -1356,9 +1361,9 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
   QN_CHECK_LAUNCH();
   for (int l = nl - 2; l >= 0; --l) {
     const auto& L = S->h_alev[l];
-    k_amg_prolong<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    k_amg_prolong<<<L.P.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
-    k_amg_smooth<<<L.nblk, kSpmvThreads, 0, st>>>(v, l);
+    k_amg_smooth<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
   }
   return QN_OK;

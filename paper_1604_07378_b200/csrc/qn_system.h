@@ -46,7 +46,7 @@ struct InstCtl {
 // PCG kernel shapes: SpMV = one warp per 32-row slice, grid-stride over slices;
 // the vector update = one thread per (row, coordinate), grid-stride with a
 // stride that is a multiple of 3 so a thread keeps its coordinate.
-constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 3;
+constexpr int kSpmvThreads = 256, kSpmvWarps = kSpmvThreads / 32, kSpmvBlocksPerSm = 4;
 constexpr int kUpdThreads = 384, kUpdBlocksPerSm = 3;
 
 
@@ -62,10 +62,12 @@ struct SellDev {
 // only the CG preconditioner, so rounding its coefficients changes the
 // (still fixed, symmetric) preconditioner, not the system CG solves to 1e-10.
 struct SellDevF {
-  const int64_t* ptr;
+  const int64_t* ptr;   // SELL: [nslice + 1] slice offsets; CSR (kl > 0): [nrows + 1] row offsets
   const int32_t* col;
   const float* val;
   int32_t nslice, nrows;
+  int32_t kl;           // 0 = SELL-32 (lane per row); K = CSR with K lanes per row
+  int32_t nblk;         // grid of the kernels applying this operator
 };
 
 // One level of the AMG V-cycle (solver QN_SOLVE_AMG; n_inst == 1)

@@ -44,6 +44,8 @@ extern "C" {
 #define QN_FN_POLY 1
 #define QN_FN_LOG 2
 #define QN_FN_HERMITE 3
+#define QN_FN_SQDEV 4    /* c[0] (x - c[1])^2: the ARAP tet energy (w/2)||F - R||^2 = vol k/2 sum (s_i - 1)^2
+                            of dynamics.ARAPGroup (dynamics.py:73-108) as a Valanis-Landel a(x) */
 
 #define QN_MAX_COEF 12   /* polynomial coefficients (ascending)  */
 #define QN_MAX_KNOTS 12  /* cubic Hermite control points          */

@@ -355,6 +355,35 @@ class TetGroup:
         np.add.at(out, self.tets.reshape(-1), self.corner_forces(x).reshape(-1, 3))
 
 
+@dataclass
+class ARAP:
+    """PDMaterial("arap", k) (materials.py:163-173) for tets."""
+    k: float
+
+
+@dataclass
+class ARAPTetGroup:
+    """dynamics.ARAPGroup (dynamics.py:73-108): (w/2)||F - R(F)||^2, w = vol k."""
+    tets: np.ndarray
+    G: np.ndarray
+    vols: np.ndarray
+    k: float
+
+    def _residual(self, x):
+        F = np.einsum("eva,evc->eac", x[self.tets], self.G)
+        U, _, V = svd_rv(F)
+        return F - np.einsum("eab,ecb->eac", U, V)
+
+    def energy(self, x):
+        D = self._residual(x)
+        return float((0.5 * (self.vols * self.k) * np.einsum("eac,eac->e", D, D)).sum())
+
+    def add_gradient(self, x, out):
+        D = self._residual(x)
+        g = (self.vols * self.k)[:, None, None] * np.einsum("eac,evc->eva", D, self.G)
+        np.add.at(out, self.tets.reshape(-1), g.reshape(-1, 3))
+
+
 class DenseFactor:
     """Dense Cholesky, restating linalg.py:23-40."""
 
@@ -418,10 +447,13 @@ def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), fa
     groups = []
     if tets.shape[0]:
         G, vols = diff_operators(verts, tets)
-        assign = [(np.arange(tets.shape[0]), materials)] if isinstance(materials, VLMaterial) else \
+        assign = [(np.arange(tets.shape[0]), materials)] if isinstance(materials, (VLMaterial, ARAP)) else \
             [(np.asarray(i, dtype=np.int64), m) for i, m in materials]
         for idx, mat in assign:
-            groups.append(TetGroup(tets[idx], G[idx], vols[idx], mat, fit_stiffness(mat, *fit)))
+            if isinstance(mat, ARAP):  # dynamics.py:341-342
+                groups.append(ARAPTetGroup(tets[idx], G[idx], vols[idx], float(mat.k)))
+            else:
+                groups.append(TetGroup(tets[idx], G[idx], vols[idx], mat, fit_stiffness(mat, *fit)))
     rows, cols, vals = [], [], []
     for g in groups:
         w = g.vols * g.k                                          # dynamics.py:48

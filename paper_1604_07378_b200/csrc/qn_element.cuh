@@ -75,9 +75,17 @@ __device__ __forceinline__ void hermite_eval(const qn_scalar_fn& f, double x, do
   dv = ((6 * u2 - 6 * u) * y0 + (-6 * u2 + 6 * u) * y1) * ih + (3 * u2 - 4 * u + 1) * t0 + (3 * u2 - 2 * u) * t1;
 }
 
+// c0 (x - c1)^2 evaluated on the deviation (no cancellation near x = c1)
+__device__ __forceinline__ void sqdev_eval(const qn_scalar_fn& f, double x, double& v, double& dv) {
+  const double u = x - f.c[1];
+  v = f.c[0] * (u * u);
+  dv = (2.0 * f.c[0]) * u;
+}
+
 __device__ __forceinline__ void fn_eval(const qn_scalar_fn& f, double x, double& v, double& dv) {
   switch (f.kind) {
     case QN_FN_POLY: poly_eval(f, x, v, dv); break;
+    case QN_FN_SQDEV: sqdev_eval(f, x, v, dv); break;
     case QN_FN_LOG: log_eval(f, x, v, dv); break;
     case QN_FN_HERMITE: hermite_eval(f, x, v, dv); break;
     default: v = 0.0; dv = 0.0; break;
@@ -119,6 +127,9 @@ __device__ __forceinline__ void fn_eval_n(const qn_scalar_fn& f, const double (&
   } else if (kind == QN_FN_HERMITE) {
 #pragma unroll
     for (int j = 0; j < N; ++j) hermite_eval(f, x[j], v[j], dv[j]);
+  } else if (kind == QN_FN_SQDEV) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) sqdev_eval(f, x[j], v[j], dv[j]);
   } else {
 #pragma unroll
     for (int j = 0; j < N; ++j) v[j] = dv[j] = 0.0;

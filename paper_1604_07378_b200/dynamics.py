@@ -24,7 +24,7 @@ import scipy.sparse
 
 from paper_1604_07378_b200 import _lib
 from paper_1604_07378_b200.linalg import Factorization
-from paper_1604_07378_b200.materials import FitInterval, MaterialModel, estimate_stiffness
+from paper_1604_07378_b200.materials import FitInterval, MaterialModel, PDMaterial, estimate_stiffness
 from paper_1604_07378_b200.mesh import TetMesh, lumped_masses, tet_diff_operators
 
 DEFAULT_TIMESTEP = 1.0 / 30.0      # dynamics.py:28
@@ -203,10 +203,16 @@ class SimSystem:
 
 
 def _assign(mesh, materials):
+    """Tet groups of a material assignment (dynamics.py:330-345); ARAP PD
+    materials become their Valanis-Landel form (materials.PDMaterial.as_vl)."""
+    if isinstance(materials, PDMaterial):
+        materials = materials.as_vl()
     if isinstance(materials, MaterialModel):
         return [(np.arange(mesh.tets.shape[0]), materials)]
     out = []
     for idx, mat in materials:
+        if isinstance(mat, PDMaterial):
+            mat = mat.as_vl()
         if not isinstance(mat, MaterialModel):
             raise NotImplementedError(f"material {mat!r}: only Valanis-Landel tet groups run on the B200 path")
         out.append((np.asarray(idx, dtype=np.int64), mat))

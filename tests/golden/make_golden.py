@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders (only the collider fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -224,6 +224,33 @@ def gen_colliders():
     print("colliders", time.time() - t, "active per frame", ncol)
 
 
+def gen_arap():
+    """PD ARAP tets (PDMaterial("arap"), dynamics.ARAPGroup, SURVEY §8f row
+    f3) through the reference's build_system: a bar of ARAP tets, and a bar
+    whose tets alternate between ARAP and Neo-Hookean groups."""
+    t = time.time()
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    m = sc.tets.shape[0]
+    out = {}
+    half = np.arange(m) % 2 == 0
+    cases = {"arap": ref_mat.PDMaterial(kind="arap", k=2e5),
+             "mixed": [(np.nonzero(half)[0], ref_mat.PDMaterial(kind="arap", k=2e5)),
+                       (np.nonzero(~half)[0], ref_material(sc.material))]}
+    for name, mat in cases.items():
+        mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+        system = ref_dyn.build_system(mesh, mat, h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+        state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+        cfg = ref_solvers.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+        g, tr = [], []
+        for f in range(10):
+            state, rec = ref_solvers.simulate_frame(system, state, cfg)
+            g.append(rec.g)
+            tr.append(rec.ls_trials)
+        out[f"{name}_g"], out[f"{name}_trials"], out[f"{name}_x_9"] = np.array(g), np.array(tr), state.q_l.copy()
+    np.savez_compressed(os.path.join(HERE, "frames_arap.npz"), **out)
+    print("arap", time.time() - t)
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
@@ -238,6 +265,9 @@ if __name__ == "__main__":
     copy_fixtures()
     if "--colliders" in sys.argv:
         gen_colliders()
+        sys.exit(0)
+    if "--arap" in sys.argv:
+        gen_arap()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

@@ -600,3 +600,23 @@ def test_colliders_batch_instances_match_single():
             assert np.array_equal(bst.q_l[b], bst.q_l[0]) and brecs[b].g == brecs[0].g
             assert rel(bst.q_l[b], sst.q_l) <= X_TOL and rel(brecs[b].g, srec.g) <= G_TOL
             assert brecs[b].ls_trials == srec.ls_trials
+
+
+@pytest.mark.parametrize("name", ["arap", "mixed"])
+def test_arap_groups_against_reference_golden(name):
+    """PDMaterial("arap") tets (dynamics.ARAPGroup, dynamics.py:73-108) run as
+    the Valanis-Landel material k/2 (s - 1)^2 with w = vol k, alone and
+    alternating with a Neo-Hookean group: 10 frames vs the reference."""
+    from paper_1604_07378_b200.materials import PDMaterial
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    d = golden("frames_arap.npz")
+    half = np.arange(sc.tets.shape[0]) % 2 == 0
+    mats = PDMaterial("arap", 2e5) if name == "arap" else \
+        [(np.nonzero(half)[0], PDMaterial("arap", 2e5)), (np.nonzero(~half)[0], from_spec(sc.material))]
+    system = Q.build_system(Q.TetMesh(sc.verts, sc.tets, sc.density), mats, h=sc.h, gravity=sc.gravity,
+                            fixed=sc.fixed)
+    res = run_gpu(system, sc, 10)
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d[f"{name}_g"][f]) <= G_TOL
+        assert rec.ls_trials == list(d[f"{name}_trials"][f])
+    assert rel(res[-1][0], d[f"{name}_x_9"]) <= X_TOL

@@ -164,3 +164,26 @@ def test_oracle_sphere_drop_matches_reference_harness():
         assert list(rec.ls_trials) == list(d["trials"][f])
         if f"x_{f}" in d:
             np.testing.assert_allclose(x, d[f"x_{f}"], rtol=0, atol=1e-12 * np.abs(d[f"x_{f}"]).max())
+
+
+def _arap_case(name, sc):
+    m = sc.tets.shape[0]
+    half = np.arange(m) % 2 == 0
+    if name == "arap":
+        return O.ARAP(2e5)
+    return [(np.nonzero(half)[0], O.ARAP(2e5)), (np.nonzero(~half)[0], oracle_material(sc.material))]
+
+
+@pytest.mark.parametrize("name", ["arap", "mixed"])
+def test_oracle_arap_groups_match_reference(name):
+    """PDMaterial("arap") tets alone and mixed with a VL group (dynamics.py:73-108, 330-345)."""
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    d = golden("frames_arap.npz")
+    osys = O.build(sc.verts, sc.tets, sc.density, _arap_case(name, sc), sc.h, sc.gravity, sc.fixed, factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(10):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d[f"{name}_g"][f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
+    np.testing.assert_allclose(x, d[f"{name}_x_9"], rtol=0, atol=1e-12 * np.abs(x).max())

@@ -184,11 +184,14 @@ typedef struct qn_system_desc {
 #define QN_SOLVE_AMG 2  /* CG preconditioned by a smoothed-aggregation AMG V(1,1) cycle (single instance) */
 
 typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          */
-  int32_t kind;                    /* 0 = pd_qn, 1 = lbfgs (lbfgs_init=system_matrix) */
+  int32_t kind;                    /* 0 = pd_qn, 1 = lbfgs (lbfgs_init=system_matrix),
+                                      2 = chebyshev (solvers.py:154-164, 306-311) */
   int32_t iterations;
   int32_t m;
   int32_t line_search;
   double gamma, alpha_init, alpha_shrink;
+  double rho;                      /* chebyshev: spectral radius estimate         */
+  int32_t S, pad;                  /* chebyshev: iterations before acceleration   */
 } qn_solver_config;
 
 typedef struct qn_frame_record {   /* ConvergenceRecord (solvers.py:71-80), per instance */
@@ -198,6 +201,7 @@ typedef struct qn_frame_record {   /* ConvergenceRecord (solvers.py:71-80), per 
   double* alphas;    /* (n_inst, iterations)     */
   double* cum_ms;    /* (n_inst, iterations)     */
   int32_t* status;   /* (n_inst): bit0 stagnated, bit1 ascent error */
+  int32_t* fallbacks;/* (n_inst) or NULL: chebyshev non-descent fallbacks (rec.fallbacks) */
 } qn_frame_record;
 
 int qn_system_create(const qn_system_desc* desc, qn_system** out);

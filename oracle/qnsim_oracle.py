@@ -682,10 +682,23 @@ class Record:
     alphas: list = field(default_factory=list)
     cum_ms: list = field(default_factory=list)
     stagnated: bool = False
+    fallbacks: int = 0
+
+
+def direction_chebyshev(x_k, x_km1, q, k, omega_prev, rho, S):
+    """solvers.py:154-164"""
+    if k < S:
+        omega = 1.0
+    elif k == S:
+        omega = 2.0 / (2.0 - rho ** 2)
+    else:
+        omega = 4.0 / (4.0 - rho ** 2 * omega_prev)
+    x_hat = x_k + q
+    return omega * (x_hat - x_km1) + x_km1 - x_k, omega
 
 
 def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3, alpha_init=2.0,
-                   shrink=0.5, use_line_search=True, fixed_targets=None):
+                   shrink=0.5, use_line_search=True, fixed_targets=None, rho=0.9, S=10):
     """One backward-Euler frame (solvers.py:260-352) for kind in {lbfgs, pd_qn},
     lbfgs_init='system_matrix', no colliders.  Returns (x, y, Record)."""
     t0 = time.perf_counter()
@@ -704,7 +717,9 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
         rec.alphas.append(a)
         rec.cum_ms.append(1000.0 * (time.perf_counter() - t0))
 
-    for _ in range(iterations):
+    x_prev_iter = x.copy()                                                # solvers.py:271-272
+    omega = 1.0
+    for k in range(1, iterations + 1):
         if sys.colliders:
             cons = update_collisions(sys, q_l, x)                         # solvers.py:285
         g_x = objective(sys, y, x, cons)
@@ -715,7 +730,14 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
             log(g_x, 0, 0.0)
             prev_x, prev_g = x, grad
             continue
-        d = direction(sys, hist, grad)
+        if kind == "chebyshev":                                           # solvers.py:306-311
+            q = direction(sys, hist, grad)
+            d, omega = direction_chebyshev(x, x_prev_iter, q, k, omega, rho, S)
+            if float(np.vdot(grad, d)) >= 0.0:
+                d = q
+                rec.fallbacks += 1
+        else:
+            d = direction(sys, hist, grad)
         if use_line_search:
             slope = float(np.vdot(grad, d))
             if slope < 0.0 and -slope <= 1e-12 * max(abs(g_x), 1.0):
@@ -734,6 +756,7 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
             alpha, x_new, trials = 1.0, x + d, 1
             g_new = objective(sys, y, x_new, cons)
         prev_x, prev_g = x, grad
+        x_prev_iter = x
         x = x_new
         log(g_new, trials, alpha)
     return x, y, rec

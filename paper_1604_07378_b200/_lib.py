@@ -92,13 +92,14 @@ class SolverConfigC(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("iterations", C.c_int32), ("m", C.c_int32), ("line_search", C.c_int32),
         ("gamma", C.c_double), ("alpha_init", C.c_double), ("alpha_shrink", C.c_double),
+        ("rho", C.c_double), ("S", C.c_int32), ("pad", C.c_int32),
     ]
 
 
 class FrameRecord(C.Structure):
     _fields_ = [
         ("g0", C.c_void_p), ("g", C.c_void_p), ("ls_trials", C.c_void_p), ("alphas", C.c_void_p),
-        ("cum_ms", C.c_void_p), ("status", C.c_void_p),
+        ("cum_ms", C.c_void_p), ("status", C.c_void_p), ("fallbacks", C.c_void_p),
     ]
 
 

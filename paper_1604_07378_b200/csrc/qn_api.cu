@@ -916,7 +916,8 @@ static int ensure_records(qn_system* S, int iterations) {
 int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed_targets, qn_frame_record* rec,
                   int32_t mem, int32_t sync, void* stream) {
   QN_REQUIRE(S && cfg, QN_ERR_ARG, "frame_step: null");
-  QN_REQUIRE(cfg->kind == 0 || cfg->kind == 1, QN_ERR_UNSUPPORTED, "solver kind not supported on the B200 path");
+  QN_REQUIRE(cfg->kind >= 0 && cfg->kind <= 2, QN_ERR_UNSUPPORTED, "solver kind not supported on the B200 path");
+  QN_REQUIRE(cfg->kind != 2 || (cfg->rho >= 0.0 && cfg->rho < 1.0), QN_ERR_ARG, "frame_step: chebyshev rho");
   QN_REQUIRE(cfg->iterations >= 1 && cfg->m >= 0 && cfg->m <= kMaxM, QN_ERR_ARG, "frame_step: bad iterations/m");
   QN_REQUIRE(cfg->gamma > 0 && cfg->gamma < 1, QN_ERR_ARG, "frame_step: gamma");
   QN_REQUIRE(sync || !rec, QN_ERR_ARG, "frame_step: a record needs sync");
@@ -932,6 +933,8 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   c.alpha_init = cfg->alpha_init;
   c.shrink = cfg->alpha_shrink;
   c.grad_tol = 1e-12 * S->scale * std::max(1.0, S->max_mass / (S->h * S->h));  // solvers.py:278
+  c.cheb_rho = cfg->rho;
+  c.cheb_S = cfg->S;
   c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
   c.use_graph = S->use_graph ? 1 : 0;
   // at most 41 trials per line search + one re-evaluation per iteration, plus slack
@@ -1001,12 +1004,13 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
     QN_CUDA(cudaMemcpy(ms_.data(), S->v.rec_ms, ms_.size() * sizeof(double), cudaMemcpyDeviceToHost));
     QN_CUDA(cudaMemcpy(tr.data(), S->v.rec_trials, tr.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
     std::vector<double> g0(ni);
-    std::vector<int32_t> status(ni);
+    std::vector<int32_t> status(ni), fallbacks(ni);
     std::vector<double> og((size_t)ni * it), oa((size_t)ni * it), om((size_t)ni * it);
     std::vector<int32_t> ot((size_t)ni * it);
     for (int64_t b = 0; b < ni; ++b) {
       g0[b] = ctl[b].g0;
       status[b] = ctl[b].status;
+      fallbacks[b] = ctl[b].fallbacks;
       for (int k = 0; k < it; ++k) {
         og[b * it + k] = g[b * cap + k];
         oa[b * it + k] = al[b * cap + k];
@@ -1025,7 +1029,8 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
       return QN_OK;
     };
     if ((rc = put(rec->g0, g0)) || (rc = put(rec->g, og)) || (rc = put(rec->ls_trials, ot)) ||
-        (rc = put(rec->alphas, oa)) || (rc = put(rec->cum_ms, om)) || (rc = put(rec->status, status)))
+        (rc = put(rec->alphas, oa)) || (rc = put(rec->cum_ms, om)) || (rc = put(rec->status, status)) ||
+        (rc = put(rec->fallbacks, fallbacks)))
       return rc;
   }
   return QN_OK;

@@ -109,6 +109,9 @@ __global__ void k_init(SysView v) {
     c.k = 0;
     c.trials = 0;
     c.status = 0;
+    c.fallbacks = 0;
+    c.cheb_fb = 0;
+    c.omega = 1.0;  // solvers.py:272
     c.xs_cur = 0;
     c.xs_prev = -1;
     c.xs_trial = 0;
@@ -299,7 +302,7 @@ __device__ void grad_finalize(const SysView& v, int b, InstCtl& c, const double*
   c.have_prev = 1;
   if (sqrt(tot[0]) <= cfg.grad_tol) {  // solvers.py:292-298
     record(v, b, c, c.g_x, 0, 0.0);
-    c.xs_prev = c.xs_cur;
+    if (cfg.kind != 2) c.xs_prev = c.xs_cur;  // chebyshev keeps x_prev_iter (solvers.py:347)
     c.phase = c.k >= cfg.iterations ? PH_DONE : PH_GRAD;  // forces still belong to x
     if (c.phase == PH_DONE) atomicSub(v.active, 1);
     return;
@@ -310,6 +313,12 @@ __device__ void grad_finalize(const SysView& v, int b, InstCtl& c, const double*
     double q = -c.sg[sp];
     for (int j = p + 1; j < npn; ++j) q -= c.zeta[j] * c.gram[sp][c.ring[j]];
     c.zeta[p] = q / c.rho[sp];
+  }
+  if (cfg.kind == 2) {  // chebyshev weight of this iteration (solvers.py:154-161), k = c.k + 1
+    const int k = c.k + 1;
+    const double r2 = cfg.cheb_rho * cfg.cheb_rho;
+    c.omega = k < cfg.cheb_S ? 1.0 : k == cfg.cheb_S ? 2.0 / (2.0 - r2) : 4.0 / (4.0 - r2 * c.omega);
+    c.cheb_fb = 0;
   }
   c.xs_trial = free_slot(c.xs_cur, c.xs_prev);
   c.phase = PH_DIR;
@@ -432,6 +441,13 @@ __global__ void __launch_bounds__(kVT) k_vec(SysView v) {
         const int np = cc->npairs;
         for (int p = 0; p < np; ++p)  // r += s (zeta - eta), oldest first
           d = __dadd_rn(d, __dmul_rn(v.S[vec_off(v, cc->ring[p], b) + ci], cc->coef[p]));
+        if (v.cfg->kind == 2 && !cc->cheb_fb) {
+          // d = omega (x + q - x_prev_iter) + x_prev_iter - x (solvers.py:162-163), q = the pd_qn direction
+          const int xp = cc->xs_prev < 0 ? cc->xs_cur : cc->xs_prev;
+          const double xkm1 = v.X[vec_off(v, xp, b) + ci];
+          const double xhat = __dadd_rn(x, d);
+          d = __dsub_rn(__dadd_rn(__dmul_rn(cc->omega, __dsub_rn(xhat, xkm1)), xkm1), x);
+        }
         v.D[oc] = d;
         acc[1] = v.Gr[vec_off(v, cc->gs_cur, b) + ci] * d;
       } else {
@@ -471,6 +487,11 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
   }
   bool accept = false;
   if (ph == PH_DIR) {
+    if (cfg.kind == 2 && !c.cheb_fb && slope >= 0.0) {  // solvers.py:309-311: d = q, fallbacks += 1
+      c.fallbacks += 1;
+      c.cheb_fb = 1;  // the next pass re-forms the first trial from the pd_qn direction
+      return;
+    }
     c.slope = slope;
     c.trials = 1;
     c.alpha = __dmul_rn(cfg.alpha_init, cfg.shrink);
@@ -483,7 +504,7 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
       return;
     } else if (-slope <= 1e-12 * fmax(fabs(c.g_x), 1.0)) {  // solvers.py:319-326
       record(v, b, c, c.g_x, 0, 0.0);
-      c.xs_prev = c.xs_cur;
+      if (cfg.kind != 2) c.xs_prev = c.xs_cur;
       c.phase = c.k >= cfg.iterations ? PH_DONE : PH_COPY;
       c.xs_trial = c.xs_cur;
       if (c.phase == PH_DONE) atomicSub(v.active, 1);

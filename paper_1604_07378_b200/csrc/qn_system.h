@@ -29,10 +29,11 @@ constexpr int kNG = 5 + 2 * kMaxM;  // gradient-kernel dot products per block
 struct InstCtl {
   int32_t phase, k, trials, status;
   int32_t xs_cur, xs_prev, xs_trial, gs_cur;
-  int32_t npairs, have_prev, pad0, pad1;
+  int32_t npairs, have_prev, fallbacks, cheb_fb;  // chebyshev: fallbacks so far, this direction fell back
   int32_t ring[kMaxM + 1];
   double g0, g_x, alpha, slope;
   double e_base, e_col;  // colliders: objective without the collision term at x; collision term at the trial
+  double omega;          // chebyshev weight of the current direction (solvers.py:154-164)
   unsigned long long t0;
   double rho[kMaxM + 1];
   double sg[kMaxM + 1];
@@ -90,7 +91,8 @@ struct PcgCtl {
 struct DevConfig {
   int32_t kind, iterations, m, line_search;
   double gamma, alpha_init, shrink, grad_tol;
-  int32_t has_targets, use_graph, max_passes, pad;
+  int32_t has_targets, use_graph, max_passes, cheb_S;
+  double cheb_rho;
 };
 
 struct SysView {

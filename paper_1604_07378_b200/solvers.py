@@ -64,14 +64,15 @@ class SolverConfig:
             raise SolverError(f"unknown lbfgs_init {self.lbfgs_init!r}; valid: {LBFGS_INITS}")
 
     def to_c(self) -> _lib.SolverConfigC:
-        if self.kind not in ("pd_qn", "lbfgs"):
+        if self.kind not in ("pd_qn", "lbfgs", "chebyshev"):
             raise NotImplementedError(f"solver kind {self.kind!r} is outside the B200 hot path (SURVEY §8f)")
         if self.kind == "lbfgs" and self.lbfgs_init != "system_matrix":
             raise NotImplementedError(f"lbfgs_init {self.lbfgs_init!r} is outside the B200 hot path")
         if self.m > _lib.QN_MAX_M:
             raise NotImplementedError(f"history window m > {_lib.QN_MAX_M}")
         c = _lib.SolverConfigC()
-        c.kind = 1 if self.kind == "lbfgs" else 0
+        c.kind = {"pd_qn": 0, "lbfgs": 1, "chebyshev": 2}[self.kind]
+        c.rho, c.S = float(self.rho), int(self.S)
         c.iterations, c.m, c.line_search = self.iterations, self.m, 1 if self.line_search else 0
         c.gamma, c.alpha_init, c.alpha_shrink = self.gamma, self.alpha_init, self.alpha_shrink
         return c
@@ -106,14 +107,16 @@ class _RecordBuffers:
         self.alphas = np.zeros((n_inst, iterations))
         self.ms = np.zeros((n_inst, iterations))
         self.status = np.zeros(n_inst, dtype=np.int32)
+        self.fallbacks = np.zeros(n_inst, dtype=np.int32)
         self.c = _lib.FrameRecord(_lib.ptr(self.g0), _lib.ptr(self.g), _lib.ptr(self.trials), _lib.ptr(self.alphas),
-                                  _lib.ptr(self.ms), _lib.ptr(self.status))
+                                  _lib.ptr(self.ms), _lib.ptr(self.status), _lib.ptr(self.fallbacks))
 
     def records(self):
         g0, g, tr = self.g0.tolist(), self.g.tolist(), self.trials.tolist()
         al, ms, stg = self.alphas.tolist(), self.ms.tolist(), (self.status & 1).astype(bool).tolist()
-        return [ConvergenceRecord(g0=g0[b], g=g[b], ls_trials=tr[b], alphas=al[b], cum_ms=ms[b], stagnated=stg[b])
-                for b in range(len(g0))]
+        fb = self.fallbacks.tolist()
+        return [ConvergenceRecord(g0=g0[b], g=g[b], ls_trials=tr[b], alphas=al[b], cum_ms=ms[b], stagnated=stg[b],
+                                  fallbacks=fb[b]) for b in range(len(g0))]
 
     def raise_on_error(self):
         bad = np.nonzero(self.status & 2)[0]

@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -251,6 +251,31 @@ def gen_arap():
     print("arap", time.time() - t)
 
 
+def gen_chebyshev():
+    """Chebyshev-accelerated PD (solvers.py:154-164, 306-311) through the
+    reference: the c2-like bar with seeded initial velocity, defaults
+    (rho 0.9, S 10) and an aggressive (rho 0.99999, S 5) schedule that falls back once."""
+    t = time.time()
+    sc = scenes.c2(grid=(12, 3, 3), iterations=20)
+    out = {}
+    for name, rho, S in (("default", 0.9, 10), ("aggressive", 0.99999, 5)):
+        mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+        system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+        state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+        cfg = ref_solvers.SolverConfig(kind="chebyshev", iterations=sc.iterations, rho=rho, S=S)
+        g, tr, fb = [], [], []
+        for f in range(8):
+            state, rec = ref_solvers.simulate_frame(system, state, cfg)
+            g.append(rec.g)
+            tr.append(rec.ls_trials)
+            fb.append(rec.fallbacks)
+        out[f"{name}_g"], out[f"{name}_trials"] = np.array(g), np.array(tr)
+        out[f"{name}_fallbacks"], out[f"{name}_x_7"] = np.array(fb), state.q_l.copy()
+        out[f"{name}_rho"], out[f"{name}_S"] = rho, S
+    np.savez_compressed(os.path.join(HERE, "frames_chebyshev.npz"), **out)
+    print("chebyshev", time.time() - t, {k: v for k, v in out.items() if k.endswith("fallbacks")})
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
@@ -268,6 +293,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--arap" in sys.argv:
         gen_arap()
+        sys.exit(0)
+    if "--chebyshev" in sys.argv:
+        gen_chebyshev()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

@@ -620,3 +620,24 @@ def test_arap_groups_against_reference_golden(name):
         assert rel(rec.g, d[f"{name}_g"][f]) <= G_TOL
         assert rec.ls_trials == list(d[f"{name}_trials"][f])
     assert rel(res[-1][0], d[f"{name}_x_9"]) <= X_TOL
+
+
+@pytest.mark.parametrize("name", ["default", "aggressive"])
+@pytest.mark.parametrize("graph", [True, False])
+def test_chebyshev_against_reference_golden(name, graph):
+    """kind="chebyshev": omega schedule, x_prev_iter bookkeeping and the
+    non-descent fallback (rec.fallbacks) on the device, vs the reference."""
+    sc = scenes.c2(grid=(12, 3, 3), iterations=20)
+    d = golden("frames_chebyshev.npz")
+    system = build(sc)
+    if not graph:
+        system.set_graph_mode(False)
+    cfg = Q.SolverConfig(kind="chebyshev", iterations=sc.iterations, rho=float(d[f"{name}_rho"]),
+                         S=int(d[f"{name}_S"]))
+    st = Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    for f in range(8):
+        st, rec = Q.simulate_frame(system, st, cfg)
+        assert rel(rec.g, d[f"{name}_g"][f]) <= G_TOL
+        assert rec.ls_trials == list(d[f"{name}_trials"][f])
+        assert rec.fallbacks == int(d[f"{name}_fallbacks"][f])
+    assert rel(st.q_l, d[f"{name}_x_7"]) <= X_TOL

@@ -187,3 +187,21 @@ def test_oracle_arap_groups_match_reference(name):
         np.testing.assert_allclose(rec.g, d[f"{name}_g"][f], rtol=1e-12)
         assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
     np.testing.assert_allclose(x, d[f"{name}_x_9"], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+@pytest.mark.parametrize("name", ["default", "aggressive"])
+def test_oracle_chebyshev_matches_reference(name):
+    """kind="chebyshev" (solvers.py:154-164, 306-311), incl. a non-descent fallback."""
+    sc = scenes.c2(grid=(12, 3, 3), iterations=20)
+    d = golden("frames_chebyshev.npz")
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(8):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m, kind="chebyshev",
+                                     rho=float(d[f"{name}_rho"]), S=int(d[f"{name}_S"]))
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d[f"{name}_g"][f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
+        assert rec.fallbacks == int(d[f"{name}_fallbacks"][f])
+    np.testing.assert_allclose(x, d[f"{name}_x_7"], rtol=0, atol=1e-12 * np.abs(x).max())

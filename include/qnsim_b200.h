@@ -191,7 +191,9 @@ typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          *
   int32_t line_search;
   double gamma, alpha_init, alpha_shrink;
   double rho;                      /* chebyshev: spectral radius estimate         */
-  int32_t S, pad;                  /* chebyshev: iterations before acceleration   */
+  int32_t S;                       /* chebyshev: iterations before acceleration   */
+  int32_t lbfgs_init;              /* lbfgs: 0 = system_matrix (A^-1), 1 = scaled_identity
+                                      (rho/<t,t> of the newest pair, solvers.py:136-141) */
 } qn_solver_config;
 
 typedef struct qn_frame_record {   /* ConvergenceRecord (solvers.py:71-80), per instance */

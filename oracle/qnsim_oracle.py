@@ -639,7 +639,7 @@ def solve_free(sys, q):
     return r
 
 
-def direction(sys, hist, grad):
+def direction(sys, hist, grad, lbfgs_init="system_matrix"):
     """Two-loop recursion with H0 = A^-1 (solvers.py:120-151); empty history is
     bitwise the pd_qn direction (solvers.py:113-117)."""
     q = -grad.copy()
@@ -649,7 +649,15 @@ def direction(sys, hist, grad):
         q -= z * t
         zetas.append(z)
     zetas.reverse()
-    r = solve_free(sys, q)
+    if lbfgs_init == "scaled_identity":                                    # solvers.py:136-141
+        if hist.pairs:
+            s, t, rho = hist.pairs[-1]
+            scale = rho / float(np.vdot(t, t))
+        else:
+            scale = 1.0
+        r = scale * q
+    else:
+        r = solve_free(sys, q)
     for (s, t, rho), z in zip(hist.pairs, zetas):
         eta = float(np.vdot(t, r)) / rho
         r += s * (z - eta)
@@ -698,7 +706,7 @@ def direction_chebyshev(x_k, x_km1, q, k, omega_prev, rho, S):
 
 
 def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3, alpha_init=2.0,
-                   shrink=0.5, use_line_search=True, fixed_targets=None, rho=0.9, S=10):
+                   shrink=0.5, use_line_search=True, fixed_targets=None, rho=0.9, S=10, lbfgs_init="system_matrix"):
     """One backward-Euler frame (solvers.py:260-352) for kind in {lbfgs, pd_qn},
     lbfgs_init='system_matrix', no colliders.  Returns (x, y, Record)."""
     t0 = time.perf_counter()
@@ -737,7 +745,7 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
                 d = q
                 rec.fallbacks += 1
         else:
-            d = direction(sys, hist, grad)
+            d = direction(sys, hist, grad, lbfgs_init)
         if use_line_search:
             slope = float(np.vdot(grad, d))
             if slope < 0.0 and -slope <= 1e-12 * max(abs(g_x), 1.0):

@@ -92,7 +92,7 @@ class SolverConfigC(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("iterations", C.c_int32), ("m", C.c_int32), ("line_search", C.c_int32),
         ("gamma", C.c_double), ("alpha_init", C.c_double), ("alpha_shrink", C.c_double),
-        ("rho", C.c_double), ("S", C.c_int32), ("pad", C.c_int32),
+        ("rho", C.c_double), ("S", C.c_int32), ("lbfgs_init", C.c_int32),
     ]
 
 

@@ -935,6 +935,10 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   c.grad_tol = 1e-12 * S->scale * std::max(1.0, S->max_mass / (S->h * S->h));  // solvers.py:278
   c.cheb_rho = cfg->rho;
   c.cheb_S = cfg->S;
+  QN_REQUIRE(cfg->lbfgs_init == 0 || cfg->lbfgs_init == 1, QN_ERR_UNSUPPORTED, "frame_step: lbfgs_init");
+  QN_REQUIRE(cfg->lbfgs_init == 0 || !S->v.pcg, QN_ERR_UNSUPPORTED,
+             "frame_step: scaled_identity needs a direct-solver system");
+  c.lbfgs_init = cfg->kind == 1 ? cfg->lbfgs_init : 0;
   c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
   c.use_graph = S->use_graph ? 1 : 0;
   // at most 41 trials per line search + one re-evaluation per iteration, plus slack
@@ -950,7 +954,7 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   QN_CUDA(cudaEventRecord(S->ev0, st));
   if (S->use_graph) {
     const int mb = c.m <= 5 ? 5 : kMaxM;  // kernels are specialised on the history bound
-    if (S->exec && S->graph_m_bound != mb) {
+    if (S->exec && (S->graph_m_bound != mb || S->graph_init != c.lbfgs_init)) {
       cudaGraphExecDestroy(S->exec);
       S->exec = nullptr;
       cudaGraphDestroy(S->graph);
@@ -959,6 +963,7 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
     if (!S->exec) {
       if ((rc = build_graph(S))) return rc;
       S->graph_m_bound = mb;
+      S->graph_init = c.lbfgs_init;
     }
     QN_CUDA(cudaGraphLaunch(S->exec, st));
     count_launch(0);

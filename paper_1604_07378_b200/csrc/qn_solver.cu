@@ -287,6 +287,7 @@ __device__ void grad_finalize(const SysView& v, int b, InstCtl& c, const double*
     if (rho > guard) {
       for (int p = 0; p < np; ++p) c.gram[c.ring[p]][cand] = tot[5 + p];
       c.rho[cand] = rho;
+      c.tt[cand] = tot[3];
       c.sg[cand] = tot[4];
       if (np < cfg.m) {
         c.npairs = np + 1;
@@ -351,6 +352,23 @@ struct SolverIO {
     r[2] = x[2];
   }
 };
+
+// lbfgs_init = "scaled_identity" (solvers.py:136-141): r = (rho / <t, t>) q of
+// the newest pair (1 with an empty history) in place of A^-1 q, every row
+// (fixed rows of q are zero), one thread per (vertex, coordinate)
+__global__ void __launch_bounds__(kVertexThreads) k_scaled(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* c = v.ctl + b;
+  if (c->phase != PH_DIR) return;
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= 3 * v.n) return;
+  const int np = c->npairs;
+  double q = -v.Gr[vec_off(v, c->gs_cur, b) + ci];
+  for (int p = np - 1; p >= 0; --p)  // q -= zeta t, newest first
+    q = __dsub_rn(q, __dmul_rn(c->zeta[p], v.T[vec_off(v, c->ring[p], b) + ci]));
+  const double scale = np > 0 ? c->rho[c->ring[np - 1]] / c->tt[c->ring[np - 1]] : 1.0;
+  v.R0[inst_off(v, b) + ci] = scale * q;
+}
 
 // stand-alone timing of the solve kernels (qn_system_time_kernel): every
 // instance, right-hand side = the resident q_l, result into the R0 scratch
@@ -1430,6 +1448,11 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
       int rc = launch_vcycle(S, st);
       return rc ? rc : launch_pcg_rz(S, 1, st);
     }
+    return QN_OK;
+  }
+  if (S->h_cfg.lbfgs_init == 1) {
+    k_scaled<<<gv, kVT, 0, st>>>(v);
+    QN_CHECK_LAUNCH();
     return QN_OK;
   }
   SolverIO io{v};

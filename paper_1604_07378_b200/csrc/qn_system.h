@@ -36,6 +36,7 @@ struct InstCtl {
   double omega;          // chebyshev weight of the current direction (solvers.py:154-164)
   unsigned long long t0;
   double rho[kMaxM + 1];
+  double tt[kMaxM + 1];  // <t, t> per slot (lbfgs_init = scaled_identity)
   double sg[kMaxM + 1];
   double gram[kMaxM + 1][kMaxM + 1];  // gram[i][j] = <s_i, t_j> (slot ids), i older than j
   double zeta[kMaxM];                 // by ring position
@@ -93,6 +94,7 @@ struct DevConfig {
   double gamma, alpha_init, shrink, grad_tol;
   int32_t has_targets, use_graph, max_passes, cheb_S;
   double cheb_rho;
+  int32_t lbfgs_init, pad2;
 };
 
 struct SysView {
@@ -193,6 +195,7 @@ struct qn_system {
   // graph
   bool use_graph = true;
   int graph_m_bound = 0;  // history bound the captured graph's kernels are specialised on
+  int graph_init = 0;     // lbfgs_init the captured graph's direction step was built for
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

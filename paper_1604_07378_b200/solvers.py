@@ -66,13 +66,14 @@ class SolverConfig:
     def to_c(self) -> _lib.SolverConfigC:
         if self.kind not in ("pd_qn", "lbfgs", "chebyshev"):
             raise NotImplementedError(f"solver kind {self.kind!r} is outside the B200 hot path (SURVEY §8f)")
-        if self.kind == "lbfgs" and self.lbfgs_init != "system_matrix":
+        if self.kind == "lbfgs" and self.lbfgs_init not in ("system_matrix", "scaled_identity"):
             raise NotImplementedError(f"lbfgs_init {self.lbfgs_init!r} is outside the B200 hot path")
         if self.m > _lib.QN_MAX_M:
             raise NotImplementedError(f"history window m > {_lib.QN_MAX_M}")
         c = _lib.SolverConfigC()
         c.kind = {"pd_qn": 0, "lbfgs": 1, "chebyshev": 2}[self.kind]
         c.rho, c.S = float(self.rho), int(self.S)
+        c.lbfgs_init = 1 if (self.kind == "lbfgs" and self.lbfgs_init == "scaled_identity") else 0
         c.iterations, c.m, c.line_search = self.iterations, self.m, 1 if self.line_search else 0
         c.gamma, c.alpha_init, c.alpha_shrink = self.gamma, self.alpha_init, self.alpha_shrink
         return c

@@ -272,6 +272,27 @@ def gen_chebyshev():
         out[f"{name}_g"], out[f"{name}_trials"] = np.array(g), np.array(tr)
         out[f"{name}_fallbacks"], out[f"{name}_x_7"] = np.array(fb), state.q_l.copy()
         out[f"{name}_rho"], out[f"{name}_S"] = rho, S
+    # L-BFGS with the standard initial Hessian (lbfgs_init="scaled_identity", solvers.py:136-141)
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = ref_solvers.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m, lbfgs_init="scaled_identity")
+    g, tr = [], []
+    for f in range(8):
+        state, rec = ref_solvers.simulate_frame(system, state, cfg)
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+    out["scaled_g"], out["scaled_trials"], out["scaled_x_7"] = np.array(g), np.array(tr), state.q_l.copy()
+    # unconverged frames of this method carry roundoff into the next frame and
+    # amplify it: the reference with its tet list reversed is the envelope
+    rmesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets[::-1].copy(), density=sc.density)
+    rsys = ref_dyn.build_system(rmesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    rstate = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    rg = []
+    for f in range(8):
+        rstate, rec = ref_solvers.simulate_frame(rsys, rstate, cfg)
+        rg.append(rec.g)
+    out["scaled_rev_g"], out["scaled_rev_x_7"] = np.array(rg), rstate.q_l.copy()
     np.savez_compressed(os.path.join(HERE, "frames_chebyshev.npz"), **out)
     print("chebyshev", time.time() - t, {k: v for k, v in out.items() if k.endswith("fallbacks")})
 

@@ -205,3 +205,19 @@ def test_oracle_chebyshev_matches_reference(name):
         assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
         assert rec.fallbacks == int(d[f"{name}_fallbacks"][f])
     np.testing.assert_allclose(x, d[f"{name}_x_7"], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+def test_oracle_lbfgs_scaled_identity_matches_reference():
+    """lbfgs_init="scaled_identity" (solvers.py:136-141): no solve, r = rho/<t,t> q."""
+    sc = scenes.c2(grid=(12, 3, 3), iterations=20)
+    d = golden("frames_chebyshev.npz")
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(8):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m,
+                                     lbfgs_init="scaled_identity")
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d["scaled_g"][f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(d["scaled_trials"][f])
+    np.testing.assert_allclose(x, d["scaled_x_7"], rtol=0, atol=1e-12 * np.abs(x).max())

@@ -309,6 +309,8 @@ typedef struct qn_slab_desc {
 #define QN_SLAB_Y 6         /* (n,3) inertia target                              */
 #define QN_SLAB_X 7         /* (2,n,3) current / trial iterate                   */
 #define QN_SLAB_G 8         /* (n,3) gradient (owned rows complete)              */
+#define QN_SLAB_CSEND 9     /* (nc,3) this rank's P_c^T r (coarse correction)     */
+#define QN_SLAB_CGATHER 10  /* [n_ranks](nc,3) all-gathered CSEND                 */
 
 #define QN_SLAB_INIT 0        /* y, x = y                                          */
 #define QN_SLAB_EVAL 1        /* objective at X[xs]: SEND[0] elastic, [1] inertia sum m|x-y|^2 */
@@ -322,6 +324,9 @@ typedef struct qn_slab_desc {
 #define QN_SLAB_DIR 9         /* d = r0 + sum (zeta - eta) s; SEND[0] = <g, d>     */
 #define QN_SLAB_TRIAL 10      /* X[xs_to] = X[xs] + alpha d                        */
 #define QN_SLAB_FINISH 11     /* q_prev <- q_l, q_l <- X[xs]                       */
+#define QN_SLAB_PCG_RZ 12     /* SEND[3..5] = <r, z> after the preconditioner      */
+#define QN_SLAB_COARSE_R 13   /* CSEND = P_c^T r                                   */
+#define QN_SLAB_COARSE_APPLY 14 /* z += P_c A_c^-1 (sum over ranks of CGATHER)     */
 
 int qn_slab_create(const qn_slab_desc* d, qn_slab** out);
 int qn_slab_destroy(qn_slab* s);
@@ -329,6 +334,17 @@ int qn_slab_buffer(qn_slab* s, int32_t which, void** ptr, int64_t* count);
 /* args (doubles): [xs, xs_to, have_prev, new_slot, nring, first, alpha,
  * ring[9] (slot ids oldest -> newest), coef[9]]; asynchronous on `stream` */
 int qn_slab_stage(qn_slab* s, int32_t stage, const double* args, int32_t nargs, void* stream);
+/* Two-level preconditioner z = B_slab r + P_c A_c^-1 P_c^T r for a grid bar
+ * (grid = cells per dimension, vertex id (i (ny+1) + j)(nz+1) + k): P_c = the
+ * trilinear hat functions of a coarse grid (coarse_dims nodes per dimension),
+ * given per dimension d and fine index i by hat_first (first coarse node of
+ * its cell) and hat_w (weights of that node and the next), concatenated over
+ * d = x, y, z; node_pos = fine index of each coarse node (concatenated).  The
+ * rank owns the x-planes [i_lo, i_lo + n_planes); v0 = global id of its
+ * local vertex 0; cinv = A_c^-1 (nc x nc, identical on every rank). */
+int qn_slab_set_coarse(qn_slab* s, const int32_t* grid, const int32_t* coarse_dims, int64_t v0, int64_t i_lo,
+                       int64_t n_planes, const int32_t* hat_first, const double* hat_w, const int32_t* node_pos,
+                       const double* cinv);
 /* CG status after the last update (synchronises `stream`): conv bits (bit 3 =
  * finished), CG iterations of the current solve */
 int qn_slab_pcg_status(qn_slab* s, int32_t* conv, int32_t* iters, void* stream);

@@ -143,6 +143,7 @@ SIGNATURES = {
     "qn_slab_buffer": [_P, _I32, _P, _P],
     "qn_slab_stage": [_P, _I32, _P, _I32, _P],
     "qn_slab_pcg_status": [_P, _P, _P, _P],
+    "qn_slab_set_coarse": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P],
 }
 
 _lib = None

@@ -87,6 +87,21 @@ struct SlabView {
   double* send;           // [kSlabSend]
   const double* gath;     // [G][kSlabSend]
   SlabPcg* pc;
+  // two-level additive preconditioner: z += P_c A_c^-1 P_c^T r with P_c the
+  // trilinear hat functions of a coarse grid of the bar (separable, applied
+  // dimension by dimension; every rank holds A_c^-1)
+  int32_t nc, gx, gy, gz;     // coarse nodes; fine grid cells per dimension
+  int32_t cx, cy, cz, npl;    // coarse nodes per dimension; owned x-planes of this rank
+  int32_t i_lo, v0;           // first owned x-plane (global), global id of local vertex 0
+  const int32_t* hI[3];       // per dimension and fine index: first coarse node of its cell
+  const double* hw[3];        // per dimension and fine index: weights (node I, node I+1)
+  const int32_t* hpos[3];     // per dimension: fine index of each coarse node
+  const double* cinv;         // [nc][nc]
+  double* t0;                 // [npl][gy+1][cz][3] restricted along z
+  double* t1;                 // [npl][cy][cz][3] restricted along z and y
+  double* csend;              // [nc][3] this rank's P_c^T r
+  const double* cgath;        // [G][nc][3]
+  double* ec;                 // [nc][3] A_c^-1 (sum over ranks of P_c^T r)
 };
 
 __device__ __forceinline__ double* part_of(const SlabView& s, int which) {
@@ -444,6 +459,144 @@ __global__ void __launch_bounds__(kSlabFT) k_slab_pcg_update(SlabView s) {
   finish_sum<6>(s, acc, 7, 0);
 }
 
+// ---- coarse correction (additive two-level Schwarz with the slabs' local
+// preconditioners): r_c = sum_ranks P_c^T r, e_c = A_c^-1 r_c, z += P_c e_c.
+// P_c^T r of this rank is applied separably: along z, then y, then x; each
+// output sums its hat support in a fixed order (deterministic).
+
+// weight of coarse node I (dimension d) at fine index i
+__device__ __forceinline__ double hat_w(const SlabView& s, int d, int i, int I) {
+  const int I0 = s.hI[d][i];
+  return I0 == I ? s.hw[d][2 * i] : (I0 + 1 == I ? s.hw[d][2 * i + 1] : 0.0);
+}
+__device__ __forceinline__ void hat_range(const SlabView& s, int d, int I, int nmax, int& lo, int& hi) {
+  const int nI = d == 0 ? s.cx : d == 1 ? s.cy : s.cz;
+  lo = I > 0 ? s.hpos[d][I - 1] : 0;
+  hi = I + 1 < nI ? s.hpos[d][I + 1] : nmax;  // inclusive
+}
+
+// t0[pl][j][K][c] = sum_k w_z(k, K) r(i_lo + pl, j, k, c)   (r = 0 on pinned / non-owned vertices)
+__global__ void __launch_bounds__(kSlabVT) k_slab_coarse_z(SlabView s) {
+  if (s.pc->conv & 8) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)s.npl * (s.gy + 1) * s.cz * 3;
+  if (t >= total) return;
+  const int c = (int)(t % 3);
+  const int K = (int)((t / 3) % s.cz);
+  const int j = (int)((t / (3 * s.cz)) % (s.gy + 1));
+  const int pl = (int)(t / (3 * (int64_t)s.cz * (s.gy + 1)));
+  const int plane = (s.gy + 1) * (s.gz + 1);
+  const int64_t base = (int64_t)(s.i_lo + pl) * plane + (int64_t)j * (s.gz + 1) - s.v0;  // local id of (i, j, 0)
+  int lo, hi;
+  hat_range(s, 2, K, s.gz, lo, hi);
+  double a = 0.0;
+  for (int k = lo; k <= hi; ++k) {
+    const int f = s.v2f[base + k];
+    if (f >= 0) a = fma(hat_w(s, 2, k, K), s.pr[3 * (size_t)f + c], a);
+  }
+  s.t0[t] = a;
+}
+
+// t1[pl][J][K][c] = sum_j w_y(j, J) t0[pl][j][K][c]
+__global__ void __launch_bounds__(kSlabVT) k_slab_coarse_y(SlabView s) {
+  if (s.pc->conv & 8) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)s.npl * s.cy * s.cz * 3;
+  if (t >= total) return;
+  const int c = (int)(t % 3);
+  const int K = (int)((t / 3) % s.cz);
+  const int J = (int)((t / (3 * s.cz)) % s.cy);
+  const int pl = (int)(t / (3 * (int64_t)s.cz * s.cy));
+  int lo, hi;
+  hat_range(s, 1, J, s.gy, lo, hi);
+  double a = 0.0;
+  for (int j = lo; j <= hi; ++j)
+    a = fma(hat_w(s, 1, j, J), s.t0[(((int64_t)pl * (s.gy + 1) + j) * s.cz + K) * 3 + c], a);
+  s.t1[t] = a;
+}
+
+// csend[I][J][K][c] = sum_{owned planes i} w_x(i, I) t1[i - i_lo][J][K][c]
+__global__ void __launch_bounds__(kSlabVT) k_slab_coarse_x(SlabView s) {
+  if (s.pc->conv & 8) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * s.nc) return;
+  const int c = t % 3;
+  const int K = (t / 3) % s.cz;
+  const int J = (t / (3 * s.cz)) % s.cy;
+  const int I = t / (3 * s.cz * s.cy);
+  int lo, hi;
+  hat_range(s, 0, I, s.gx, lo, hi);
+  lo = max(lo, s.i_lo);
+  hi = min(hi, s.i_lo + s.npl - 1);
+  double a = 0.0;
+  for (int i = lo; i <= hi; ++i)
+    a = fma(hat_w(s, 0, i, I), s.t1[(((int64_t)(i - s.i_lo) * s.cy + J) * s.cz + K) * 3 + c], a);
+  s.csend[t] = a;
+}
+
+// the ranks' restricted residuals summed in rank order into shared memory,
+// then the dense coarse inverse, warp per coarse row
+__global__ void __launch_bounds__(kSpmvThreads) k_slab_coarse_solve(SlabView s) {
+  if (s.pc->conv & 8) return;
+  extern __shared__ double rcs[];
+  const int n3 = 3 * s.nc;
+  for (int q = threadIdx.x; q < n3; q += blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < s.G; ++r) a += s.cgath[(size_t)r * n3 + q];
+    rcs[q] = a;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  for (int k = w0; k < s.nc; k += nw) {
+    const double* row = s.cinv + (size_t)k * s.nc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int c = lane; c < s.nc; c += 32) {
+      const double m = __ldg(row + c);
+      a0 = fma(m, rcs[3 * c + 0], a0);
+      a1 = fma(m, rcs[3 * c + 1], a1);
+      a2 = fma(m, rcs[3 * c + 2], a2);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+      s.ec[3 * (size_t)k + 0] = a0;
+      s.ec[3 * (size_t)k + 1] = a1;
+      s.ec[3 * (size_t)k + 2] = a2;
+    }
+  }
+}
+
+// z += P_c e_c on the owned free rows: 8 trilinear terms per (row, coordinate)
+__global__ void __launch_bounds__(kSlabFT) k_slab_coarse_p(SlabView s) {
+  if (s.pc->conv & 8) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(t % 3);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, n3 = 3 * (int64_t)s.nf;
+  const int plane = (s.gy + 1) * (s.gz + 1);
+  for (int64_t e = t; e < n3; e += stride) {
+    const int64_t gid = (int64_t)__ldg(s.f2v + e / 3) + s.v0;
+    const int i = (int)(gid / plane), rem = (int)(gid % plane);
+    const int j = rem / (s.gz + 1), k = rem % (s.gz + 1);
+    const int Ix = s.hI[0][i], Iy = s.hI[1][j], Iz = s.hI[2][k];
+    const double wx[2] = {s.hw[0][2 * i], s.hw[0][2 * i + 1]};
+    const double wy[2] = {s.hw[1][2 * j], s.hw[1][2 * j + 1]};
+    const double wz[2] = {s.hw[2][2 * k], s.hw[2][2 * k + 1]};
+    double a = 0.0;
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz) {
+          const double w = wx[dx] * wy[dy] * wz[dz];
+          if (w != 0.0) a = fma(w, s.ec[(((size_t)(Ix + dx) * s.cy + (Iy + dy)) * s.cz + (Iz + dz)) * 3 + c], a);
+        }
+    s.pz[e] += a;
+  }
+}
+
 __global__ void k_slab_pcg_count(SlabView s) {
   if (s.pc->conv & 8) return;
   s.pc->iter += 1;
@@ -711,6 +864,8 @@ int qn_slab_buffer(qn_slab* S, int32_t which, void** ptr, int64_t* count) {
     case QN_SLAB_Y: *ptr = s.y; *count = v3; break;
     case QN_SLAB_X: *ptr = s.X; *count = 2 * v3; break;
     case QN_SLAB_G: *ptr = s.g; *count = v3; break;
+    case QN_SLAB_CSEND: *ptr = s.csend; *count = 3 * (int64_t)s.nc; break;
+    case QN_SLAB_CGATHER: *ptr = (void*)s.cgath; *count = 3 * (int64_t)s.nc * s.G; break;
     default: qn::set_error("slab_buffer: unknown buffer"); return QN_ERR_ARG;
   }
   return QN_OK;
@@ -748,11 +903,7 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
       QN_CUDA(cudaMemsetAsync(s.pc, 0, sizeof(SlabPcg), st));
       k_slab_pcg_setup<<<s.nblk_all, kSlabVT, 0, st>>>(s, a);
       QN_CHECK_LAUNCH();
-      if (s.amg) {
-        if ((rc = launch_vcycle(S->local, st))) return rc;
-        k_slab_rz<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
-        QN_CHECK_LAUNCH();
-      }
+      if (s.amg && (rc = launch_vcycle(S->local, st))) return rc;
       break;
     case QN_SLAB_PCG_P:
       k_slab_pcg_p<<<s.nblk_flat, kSlabFT, 0, st>>>(s, a.first);
@@ -767,11 +918,28 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
       QN_CHECK_LAUNCH();
       k_slab_pcg_count<<<1, 1, 0, st>>>(s);
       QN_CHECK_LAUNCH();
-      if (s.amg) {
-        if ((rc = launch_vcycle(S->local, st))) return rc;
-        k_slab_rz<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
-        QN_CHECK_LAUNCH();
-      }
+      if (s.amg && (rc = launch_vcycle(S->local, st))) return rc;
+      break;
+    case QN_SLAB_PCG_RZ:
+      k_slab_rz<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
+      break;
+    case QN_SLAB_COARSE_R:
+      QN_REQUIRE(s.nc > 0, QN_ERR_ARG, "slab_stage: no coarse level set");
+      k_slab_coarse_z<<<std::max(1, div_up((int64_t)s.npl * (s.gy + 1) * s.cz * 3, kSlabVT)), kSlabVT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
+      k_slab_coarse_y<<<std::max(1, div_up((int64_t)s.npl * s.cy * s.cz * 3, kSlabVT)), kSlabVT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
+      k_slab_coarse_x<<<std::max(1, div_up(3 * (int64_t)s.nc, kSlabVT)), kSlabVT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
+      break;
+    case QN_SLAB_COARSE_APPLY:
+      QN_REQUIRE(s.nc > 0, QN_ERR_ARG, "slab_stage: no coarse level set");
+      k_slab_coarse_solve<<<std::max(1, std::min(2 * kSMs, div_up(s.nc, kSpmvWarps))), kSpmvThreads,
+                            (size_t)3 * s.nc * sizeof(double), st>>>(s);
+      QN_CHECK_LAUNCH();
+      k_slab_coarse_p<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
       break;
     case QN_SLAB_STORE:
       k_slab_store<<<s.nblk_all, kSlabVT, 0, st>>>(s);
@@ -797,6 +965,62 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
       set_error("slab_stage: unknown stage");
       return QN_ERR_ARG;
   }
+  return QN_OK;
+}
+
+int qn_slab_set_coarse(qn_slab* S, const int32_t* grid, const int32_t* coarse_dims, int64_t v0, int64_t i_lo,
+                       int64_t n_planes, const int32_t* hat_first, const double* hat_w, const int32_t* node_pos,
+                       const double* cinv) {
+  using namespace qn;
+  QN_REQUIRE(S && grid && coarse_dims && hat_first && hat_w && node_pos && cinv, QN_ERR_ARG, "slab_set_coarse: null");
+  SlabView& s = S->s;
+  QN_REQUIRE(s.nc == 0, QN_ERR_ARG, "slab_set_coarse: already set");
+  const int64_t nc = (int64_t)coarse_dims[0] * coarse_dims[1] * coarse_dims[2];
+  QN_REQUIRE(nc > 0 && 3 * nc * (int64_t)sizeof(double) <= 200 * 1024, QN_ERR_ARG, "slab_set_coarse: coarse size");
+  const int64_t plane = (int64_t)(grid[1] + 1) * (grid[2] + 1);
+  QN_REQUIRE(n_planes >= 1 && i_lo >= 0 && i_lo + n_planes <= grid[0] + 1 && i_lo * plane >= v0 &&
+                 (i_lo + n_planes) * plane - v0 <= s.n,
+             QN_ERR_ARG, "slab_set_coarse: owned planes outside the slab");
+  int rc;
+  int64_t off_h = 0, off_p = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int nf = grid[d] + 1;
+    int32_t* dI;
+    double* dw;
+    int32_t* dp;
+    for (int i = 0; i < nf; ++i)
+      QN_REQUIRE(hat_first[off_h + i] >= 0 && hat_first[off_h + i] + 1 < coarse_dims[d], QN_ERR_ARG,
+                 "slab_set_coarse: hat table");
+    if ((rc = slab_upload(S, &dI, hat_first + off_h, (size_t)nf)) ||
+        (rc = slab_upload(S, &dw, hat_w + 2 * off_h, (size_t)2 * nf)) ||
+        (rc = slab_upload(S, &dp, node_pos + off_p, (size_t)coarse_dims[d])))
+      return rc;
+    s.hI[d] = dI;
+    s.hw[d] = dw;
+    s.hpos[d] = dp;
+    off_h += nf;
+    off_p += coarse_dims[d];
+  }
+  double *dci, *dgath;
+  if ((rc = slab_upload(S, &dci, cinv, (size_t)(nc * nc))) || (rc = slab_alloc(S, &s.csend, (size_t)nc * 3)) ||
+      (rc = slab_alloc(S, &dgath, (size_t)nc * 3 * s.G)) || (rc = slab_alloc(S, &s.ec, (size_t)nc * 3)) ||
+      (rc = slab_alloc(S, &s.t0, (size_t)n_planes * (grid[1] + 1) * coarse_dims[2] * 3)) ||
+      (rc = slab_alloc(S, &s.t1, (size_t)n_planes * coarse_dims[1] * coarse_dims[2] * 3)))
+    return rc;
+  QN_CUDA(cudaFuncSetAttribute(k_slab_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(3 * nc * sizeof(double))));
+  s.cinv = dci;
+  s.cgath = dgath;
+  s.gx = grid[0];
+  s.gy = grid[1];
+  s.gz = grid[2];
+  s.cx = coarse_dims[0];
+  s.cy = coarse_dims[1];
+  s.cz = coarse_dims[2];
+  s.npl = (int32_t)n_planes;
+  s.i_lo = (int32_t)i_lo;
+  s.v0 = (int32_t)v0;
+  s.nc = (int32_t)nc;
   return QN_OK;
 }
 

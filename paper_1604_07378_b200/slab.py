@@ -38,13 +38,14 @@ from paper_1604_07378_b200.mesh import TetMesh, grid_bar_cells, lumped_masses
 from paper_1604_07378_b200.parallel import shard_instances
 from paper_1604_07378_b200.solvers import ConvergenceRecord, SolverConfig, SolverError
 
-SEND, GATHER, P, R0, QL, QPREV, Y, X, G = range(9)
-INIT, EVAL, GRAD, PCG_SETUP, PCG_P, PCG_SPMV, PCG_UPDATE, STORE, ETA, DIR, TRIAL, FINISH = range(12)
+SEND, GATHER, P, R0, QL, QPREV, Y, X, G, CSEND, CGATHER = range(11)
+(INIT, EVAL, GRAD, PCG_SETUP, PCG_P, PCG_SPMV, PCG_UPDATE, STORE, ETA, DIR, TRIAL, FINISH, PCG_RZ, COARSE_R,
+ COARSE_APPLY) = range(15)
 MAX_M = 8                 # kSlabMaxM
 RING = MAX_M + 1
 NSEND = 32
 _STAGE_NAMES = ["init", "eval", "grad", "pcg_setup", "pcg_p", "pcg_spmv", "pcg_update", "store", "eta", "dir",
-                "trial", "finish"]
+                "trial", "finish", "pcg_rz", "coarse_r", "coarse_apply"]
 CURVATURE_GUARD = 1e-12   # solvers.py:28
 ALPHA_FLOOR = 1e-12       # solvers.py:29
 
@@ -160,6 +161,9 @@ class SlabRank:
         self.system = _build(mesh, [[(np.arange(mesh.tets.shape[0]), material)]], h, gravity, local_fixed,
                              fit_interval, 1, solver=solver, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit)
         Ar = slab_operator(self.system.L, lumped_masses(mesh), h, pin, owned)
+        self.A_of = Ar
+        self.owned_free = np.nonzero(owned & ~pin)[0]
+        self.coarse = False
         self._a = (_lib.i64(Ar.indptr), _lib.i32(Ar.indices), _lib.f64(Ar.data), np.ascontiguousarray(pin, np.uint8))
         d = _lib.SlabDesc()
         d.local = self.system._h
@@ -177,6 +181,38 @@ class SlabRank:
             _lib.check(_lib.load().qn_slab_buffer(self._h, which, C.byref(p), C.byref(cnt)))
             self.buf[which] = torch.as_tensor(_CudaBuffer(p.value, cnt.value), device="cuda")
         self._args = np.zeros(7 + 2 * RING, dtype=np.float64)
+
+    # -- two-level preconditioner (geometric coarse grid over the whole bar) --
+    def coarse_rows(self, cs):
+        """P_c rows of every local vertex (CSR, local vertex x coarse node)."""
+        lay = self.lay
+        return cs.rows(lay.v0 + np.arange(lay.n))
+
+    def coarse_partial(self, cs):
+        """This rank's part of A_c = P_c^T A P_c: its owned free rows only, so
+        the rank-order sum over slabs is the global Galerkin product (dense)."""
+        return galerkin_part(self.A_of, self.coarse_rows(cs), self.owned_free)
+
+    def set_coarse(self, cs, cinv):
+        lay = self.lay
+        first, w, pos = cs.tables()
+        grid = np.asarray(cs.grid, dtype=np.int32)
+        dims = np.asarray(cs.dims, dtype=np.int32)
+        i_lo = lay.v0 // lay.plane + lay.own_lo // lay.plane
+        n_planes = (lay.own_hi - lay.own_lo) // lay.plane
+        keep = (grid, dims, first, w, pos, _lib.f64(cinv))
+        _lib.check(_lib.load().qn_slab_set_coarse(self._h, _lib.ptr(grid), _lib.ptr(dims), C.c_int64(lay.v0),
+                                                  C.c_int64(i_lo), C.c_int64(n_planes), _lib.ptr(first),
+                                                  _lib.ptr(w), _lib.ptr(pos), _lib.ptr(keep[5])), "slab_set_coarse")
+        self.coarse = True
+        self._refresh_buffers((CSEND, CGATHER))
+
+    def _refresh_buffers(self, which):
+        import torch
+        for w in which:
+            p, cnt = C.c_void_p(), C.c_int64()
+            _lib.check(_lib.load().qn_slab_buffer(self._h, w, C.byref(p), C.byref(cnt)))
+            self.buf[w] = torch.as_tensor(_CudaBuffer(p.value, cnt.value), device="cuda")
 
     def stage(self, stage, xs=0, xs_to=0, have_prev=0, new_slot=0, ring=(), coef=(), first=0, alpha=0.0):
         import torch
@@ -229,11 +265,21 @@ class EmulatedComm:
     def local(self):
         return self.ranks
 
-    def allgather(self):
+    def allgather(self, pair=(SEND, GATHER)):
         import torch
-        allv = torch.cat([rk.buf[SEND] for rk in self.ranks])
+        allv = torch.cat([rk.buf[pair[0]] for rk in self.ranks])
         for rk in self.ranks:
-            rk.buf[GATHER].copy_(allv)
+            rk.buf[pair[1]].copy_(allv)
+
+    def reduce_dense(self, parts):
+        """rank-order sum of every rank's dense setup matrix"""
+        out = np.zeros_like(parts[0])
+        for p in parts:
+            out = out + p
+        return out
+
+    def same_on_all(self, a):
+        return a
 
     def halo(self, which):
         for lo, hi in zip(self.ranks[:-1], self.ranks[1:]):
@@ -259,8 +305,29 @@ class NcclComm:
     def local(self):
         return [self.rk]
 
-    def allgather(self):
-        self.dist.all_gather_into_tensor(self.rk.buf[GATHER], self.rk.buf[SEND], group=self.group)
+    def allgather(self, pair=(SEND, GATHER)):
+        self.dist.all_gather_into_tensor(self.rk.buf[pair[1]], self.rk.buf[pair[0]], group=self.group)
+
+    def reduce_dense(self, parts):
+        """rank-order sum of every rank's dense setup matrix (all-gather, then
+        the same additions on every rank)"""
+        import torch
+        mine = torch.as_tensor(parts[0], device="cuda")
+        world = self.dist.get_world_size(self.group)
+        allp = torch.empty((world,) + mine.shape, dtype=mine.dtype, device="cuda")
+        self.dist.all_gather_into_tensor(allp, mine, group=self.group)
+        allp = allp.cpu().numpy()
+        out = np.zeros_like(allp[0])
+        for r in range(world):
+            out = out + allp[r]
+        return out
+
+    def same_on_all(self, a):
+        """rank 0's array on every rank (setup results computed redundantly)"""
+        import torch
+        t = torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+        self.dist.broadcast(t, 0, group=self.group)
+        return t.cpu().numpy()
 
     def halo(self, which):
         dist, rk = self.dist, self.rk
@@ -280,6 +347,76 @@ class NcclComm:
 
     def scalars(self):
         return self.rk.buf[GATHER].cpu().numpy().reshape(-1, NSEND)
+
+
+class CoarseSpace:
+    """Trilinear hat functions on a coarse grid of the bar (index space: coarse
+    node I of dimension d sits at fine index min(I f_d, n_d)); the coarse level
+    of the slabs' two-level preconditioner.  f_d >= 2 keeps A_c = P^T A P a
+    27-point operator."""
+
+    def __init__(self, grid, target=(40, 5, 5)):
+        self.grid = tuple(grid)
+        self.f = tuple(max(2, -(-n // t)) for n, t in zip(grid, target))
+        self.pos = [np.minimum(np.arange(-(-n // f) + 1) * f, n) for n, f in zip(grid, self.f)]
+        self.dims = tuple(p.size for p in self.pos)
+        self.n = int(np.prod(self.dims))
+
+    def _hat(self, d, i):
+        pos = self.pos[d]
+        I = np.clip(np.searchsorted(pos, i, side="right") - 1, 0, pos.size - 2)
+        t = (i - pos[I]) / (pos[I + 1] - pos[I])
+        return I, 1.0 - t, t
+
+    def tables(self):
+        """Per-dimension hat tables for the device (x, y, z concatenated): first
+        coarse node of each fine index's cell, its two weights, node positions."""
+        first, w, pos = [], [], []
+        for d, n in enumerate(self.grid):
+            I, a0, a1 = self._hat(d, np.arange(n + 1))
+            first.append(I.astype(np.int32))
+            w.append(np.stack([a0, a1], axis=1).reshape(-1))
+            pos.append(self.pos[d].astype(np.int32))
+        return np.concatenate(first), np.concatenate(w), np.concatenate(pos)
+
+    def rows(self, gids):
+        """P_c rows of global vertex ids (scipy CSR, len(gids) x n)."""
+        nx, ny, nz = self.grid
+        gids = np.asarray(gids, dtype=np.int64)
+        i, rem = np.divmod(gids, (ny + 1) * (nz + 1))
+        j, k = np.divmod(rem, nz + 1)
+        (Ix, ax0, ax1), (Iy, ay0, ay1), (Iz, az0, az1) = self._hat(0, i), self._hat(1, j), self._hat(2, k)
+        Cy, Cz = self.dims[1], self.dims[2]
+        rows, cols, vals = [], [], []
+        for dx, wx in ((0, ax0), (1, ax1)):
+            for dy, wy in ((0, ay0), (1, ay1)):
+                for dz, wz in ((0, az0), (1, az1)):
+                    w = wx * wy * wz
+                    nzm = w != 0.0
+                    rows.append(np.nonzero(nzm)[0])
+                    cols.append((((Ix + dx) * Cy + (Iy + dy)) * Cz + (Iz + dz))[nzm])
+                    vals.append(w[nzm])
+        return scipy.sparse.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                       shape=(gids.size, self.n))
+
+
+def galerkin_part(A_of, P_local, owned_free):
+    """P_own^T (A_of P_local), dense: a slab's share of P_c^T A P_c (the rows
+    of A_of are the slab's owned free rows; P_local has a row per local vertex)."""
+    return (P_local[owned_free].T @ (A_of @ P_local)).toarray()
+
+
+def setup_coarse(comm, grid, target=(40, 5, 5)):
+    """Two-level preconditioner for the slabs of `comm`: every rank's part of
+    the Galerkin product, summed in rank order, inverted (rank 0's inverse on
+    every rank), and each rank's rows of P_c and P_c^T uploaded."""
+    cs = CoarseSpace(grid, target)
+    Ac = comm.reduce_dense([rk.coarse_partial(cs) for rk in comm.local])
+    Ac = 0.5 * (Ac + Ac.T)
+    cinv = comm.same_on_all(np.linalg.inv(Ac))
+    for rk in comm.local:
+        rk.set_coarse(cs, cinv)
+    return cs
 
 
 def rank_sum(vals):
@@ -346,9 +483,18 @@ class SlabRun:
         v = self._gather()
         return 0.5 / self.h ** 2 * v[1] + v[0]
 
+    def _precondition(self):
+        """z = B_slab r (done by the stage) [+ P_c A_c^-1 sum_ranks P_c^T r], then <r, z>."""
+        if self.comm.local[0].coarse:
+            self._stage(COARSE_R)
+            self._ev("allgather_coarse", lambda: self.comm.allgather((CSEND, CGATHER)))
+            self._stage(COARSE_APPLY)
+        self._stage(PCG_RZ)
+
     def _solve(self, ring, zeta):
         """r0 = A_free^-1 (-g - sum zeta t) by CG over the slabs (3 columns)."""
         self._stage(PCG_SETUP, ring=ring, coef=zeta)
+        self._precondition()
         self._ev("allgather", self.comm.allgather)
         self._stage(PCG_P, first=1)
         it = 0
@@ -357,6 +503,7 @@ class SlabRun:
             self._stage(PCG_SPMV)
             self._ev("allgather", self.comm.allgather)
             self._stage(PCG_UPDATE)
+            self._precondition()
             self._ev("allgather", self.comm.allgather)
             self._stage(PCG_P, first=0)
             it += 1

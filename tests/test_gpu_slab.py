@@ -31,10 +31,13 @@ def rel(a, b):
     return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
 
 
-def run_emulated(sc, world, frames, solver="amg", pcg_tol=1e-10, cfg=None):
+def run_emulated(sc, world, frames, solver="amg", pcg_tol=1e-10, cfg=None, coarse=False, target=(8, 2, 2)):
     ranks = slab.scene_slabs(sc, world, solver=solver, pcg_tol=pcg_tol)
-    run = slab.SlabRun(slab.EmulatedComm(ranks), cfg or Q.SolverConfig(kind="lbfgs", iterations=sc.iterations,
-                                                                      m=sc.m), sc.h, slab.scene_grad_tol(sc))
+    comm = slab.EmulatedComm(ranks)
+    if coarse:
+        slab.setup_coarse(comm, sc.grid, target)
+    run = slab.SlabRun(comm, cfg or Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m), sc.h,
+                       slab.scene_grad_tol(sc))
     out = []
     for _ in range(frames):
         rec = run.step()
@@ -158,3 +161,29 @@ def test_slab_owned_gradient_is_the_single_system_gradient():
         g = rk.buf[slab.G].view(-1, 3)[lay.own_lo: lay.own_hi].cpu().numpy()
         assert np.array_equal(g, g_ref[lay.v0 + lay.own_lo: lay.v0 + lay.own_hi])
     assert abs(e - e_ref) <= 1e-12 * abs(e_ref)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_slab_two_level_against_oracle(world):
+    """Per-slab AMG + the geometric coarse correction (additive two-level
+    Schwarz): same parity bar as the single-system AMG-PCG."""
+    sc = scenes.c5(grid=(40, 10, 10), frames=1)
+    res, run = run_emulated(sc, world, 1, coarse=True)
+    (x, ro), = oracle_frames(sc, 1)
+    xg, rg = res[0]
+    assert rel(rg.g, ro.g) <= 1e-9
+    assert rel(xg, x) <= 1e-8
+    assert rg.ls_trials == ro.ls_trials
+
+
+def test_slab_coarse_correction_keeps_cg_iterations_flat():
+    """Block-Jacobi across slabs loses the long-range coupling along the bar
+    (CG iterations grow with the slab count); the coarse level restores it."""
+    sc = scenes.c5(grid=(64, 8, 8), frames=1)
+    its = {}
+    for world, coarse in ((1, False), (4, False), (4, True), (8, True)):
+        _, run = run_emulated(sc, world, 1, coarse=coarse)
+        its[(world, coarse)] = run.cg_iterations
+    print(its)
+    assert its[(4, True)] < its[(4, False)]
+    assert its[(4, True)] <= 1.3 * its[(1, False)] and its[(8, True)] <= 1.4 * its[(1, False)]

@@ -198,3 +198,36 @@ def test_slab_communicator_allgather_and_halo(world):
         np.testing.assert_array_equal(gath, expect)
         np.testing.assert_array_equal(p, gid)
     assert np.array_equal(slab.rank_sum(expect.reshape(world, -1)), sum(expect.reshape(world, -1)[r] for r in range(world)))
+
+
+def test_slab_coarse_space_galerkin_parts_sum_to_global():
+    """The two-level preconditioner's coarse operator: the rank-order sum of the
+    slabs' Galerkin parts P_own^T A_of P_local is the global P^T A_free P."""
+    from paper_1604_07378_b200 import slab
+    from paper_1604_07378_b200.mesh import TetMesh, lumped_masses, tet_diff_operators
+    sc = scenes.c5(grid=(12, 3, 4), frames=1)
+    h, k = sc.h, 2.5e6
+    mesh = TetMesh(sc.verts, sc.tets, sc.density)
+    _, vols = tet_diff_operators(mesh)
+    cs = slab.CoarseSpace(sc.grid, target=(4, 2, 2))
+    P = cs.rows(np.arange(mesh.n))
+    assert np.allclose(np.asarray(P.sum(axis=1)).ravel(), 1.0)  # partition of unity
+    pin_g = np.zeros(mesh.n, dtype=bool)
+    pin_g[sc.fixed] = True
+    Ag = slab.slab_operator(slab.stiffness_matrix(mesh, vols * k), lumped_masses(mesh), h, pin_g,
+                            np.ones(mesh.n, dtype=bool))
+    free = np.nonzero(~pin_g)[0]
+    ref = slab.galerkin_part(Ag, P, free)
+    for world in (2, 3):
+        tot = np.zeros_like(ref)
+        for r in range(world):
+            lay = slab.slab_layout(sc.grid, world, r)
+            lm = TetMesh(sc.verts[lay.v0: lay.v0 + lay.n], slab.local_tets_from_global(sc.tets, lay), sc.density)
+            _, lv = tet_diff_operators(lm)
+            pin = pin_g[lay.v0: lay.v0 + lay.n]
+            owned = np.zeros(lay.n, dtype=bool)
+            owned[lay.own_lo: lay.own_hi] = True
+            Al = slab.slab_operator(slab.stiffness_matrix(lm, lv * k), lumped_masses(lm), h, pin, owned)
+            tot = tot + slab.galerkin_part(Al, cs.rows(lay.v0 + np.arange(lay.n)), np.nonzero(owned & ~pin)[0])
+        np.testing.assert_allclose(tot, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    assert np.allclose(ref, ref.T, rtol=1e-12, atol=1e-9 * np.abs(ref).max())

@@ -22,11 +22,15 @@ def main():
     ap.add_argument("--world", type=int, default=1)
     ap.add_argument("--frames", type=int, default=1)
     ap.add_argument("--check", type=int, default=4)
+    ap.add_argument("--coarse", action="store_true", help="two-level preconditioner (slab.setup_coarse)")
     a = ap.parse_args()
     t = time.perf_counter()
     sc = scenes.c5(grid=tuple(a.grid), frames=a.frames)
     ranks = slab.scene_slabs(sc, a.world)
-    run = slab.SlabRun(slab.EmulatedComm(ranks), Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m),
+    comm = slab.EmulatedComm(ranks)
+    if a.coarse:
+        slab.setup_coarse(comm, sc.grid)
+    run = slab.SlabRun(comm, Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m),
                        sc.h, slab.scene_grad_tol(sc), pcg_check=a.check)
     print(f"build {time.perf_counter() - t:.1f} s", flush=True)
     run.step()  # warm-up

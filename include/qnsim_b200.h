@@ -177,7 +177,15 @@ typedef struct qn_system_desc {
   int64_t n_colliders;        /* <= QN_MAX_COLLIDERS                             */
   const qn_collider* colliders;
   double w_col;
+  /* QN_ELEM_TET (default) or QN_ELEM_SPRING: spring networks (SpringGroup,
+   * dynamics.py:111-151): tets rows are (a, b, -1, -1), vols = rest lengths,
+   * Dm_inv unused, material a.c[0] = k (PDMaterial mass_spring)          */
+  int32_t element_kind;
+  int32_t pad_e;
 } qn_system_desc;
+
+#define QN_ELEM_TET 0
+#define QN_ELEM_SPRING 1
 
 #define QN_SOLVE_DIRECT 0
 #define QN_SOLVE_PCG 1

@@ -384,6 +384,80 @@ class ARAPTetGroup:
         np.add.at(out, self.tets.reshape(-1), g.reshape(-1, 3))
 
 
+@dataclass
+class SpringGroupO:
+    """dynamics.SpringGroup (dynamics.py:111-151): (w/2)(|d| - r)^2, w = k."""
+    edges: np.ndarray
+    rest: np.ndarray
+    k: float
+
+    def _dirs(self, x):
+        d = x[self.edges[:, 1]] - x[self.edges[:, 0]]
+        return d, np.linalg.norm(d, axis=1)
+
+    def energy(self, x):
+        _, length = self._dirs(x)
+        return float((0.5 * np.full(self.edges.shape[0], self.k) * (length - self.rest) ** 2).sum())
+
+    def add_gradient(self, x, out):
+        d, length = self._dirs(x)
+        resid = np.full(self.edges.shape[0], self.k)[:, None] * (1.0 - self.rest / length)[:, None] * d
+        g = np.empty((self.edges.shape[0], 2, 3))
+        g[:, 0] = -resid
+        g[:, 1] = resid
+        np.add.at(out, self.edges.reshape(-1), g.reshape(-1, 3))
+
+
+def read_obj_springs(path):
+    """load_obj_springs (mesh.py:135-171): vertices, sorted unique triangle
+    edges, rest lengths, faces."""
+    verts, faces = [], []
+    with open(path) as fh:
+        for line in fh:
+            p = line.split("#", 1)[0].split()
+            if not p:
+                continue
+            if p[0] == "v":
+                verts.append([float(p[1]), float(p[2]), float(p[3])])
+            elif p[0] == "f":
+                faces.append([int(q.split("/")[0]) - 1 for q in p[1:4]])
+    verts, faces = np.asarray(verts), np.asarray(faces, dtype=np.int64)
+    es = set()
+    for a, b, c in faces:
+        for u, v in ((a, b), (b, c), (a, c)):
+            es.add((min(u, v), max(u, v)))
+    edges = np.asarray(sorted(es), dtype=np.int64)
+    rest = np.linalg.norm(verts[edges[:, 1]] - verts[edges[:, 0]], axis=1)
+    return verts, edges, rest, faces
+
+
+def build_springs(verts, edges, rest, faces, density, k, h, gravity, fixed, factor="dense", colliders=(),
+                  collision_weight=None):
+    """dynamics.build_system for a spring network (dynamics.py:374-434)."""
+    verts = np.asarray(verts, dtype=np.float64)
+    n = verts.shape[0]
+    v = verts[faces]
+    areas = 0.5 * np.linalg.norm(np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]), axis=1)  # mesh.py:184-191
+    masses = np.zeros(n)
+    for c in range(3):
+        np.add.at(masses, faces[:, c], density * areas / 3.0)
+    grp = SpringGroupO(np.asarray(edges), np.asarray(rest), float(k))
+    blk = np.full(edges.shape[0], float(k))[:, None, None] * np.array([[1.0, -1.0], [-1.0, 1.0]])[None]
+    L = scipy.sparse.coo_matrix((blk.reshape(-1), (np.repeat(edges, 2, axis=1).reshape(-1),
+                                                   np.tile(edges, (1, 2)).reshape(-1))), shape=(n, n)).tocsr()
+    fixed = np.asarray(sorted(set(int(i) for i in fixed)), dtype=np.int64)
+    mask = np.ones(n, dtype=bool)
+    mask[fixed] = False
+    free = np.nonzero(mask)[0]
+    A = (L + scipy.sparse.diags(masses / h ** 2)).tocsr()
+    A_free = A[free][:, free].tocsr()
+    fac = DenseFactor(A_free.toarray()) if factor == "dense" else SparseFactor(A_free)
+    bbox = verts.max(axis=0) - verts.min(axis=0)
+    w_col = float(collision_weight) if collision_weight is not None else 10.0 * float(k)
+    return System(verts, np.asarray(edges), masses, float(h), np.asarray(gravity, dtype=np.float64), [grp],
+                  fixed, free, L, A_free, fac, float(np.linalg.norm(bbox)) or 1.0, list(colliders), w_col)
+
+
 class DenseFactor:
     """Dense Cholesky, restating linalg.py:23-40."""
 

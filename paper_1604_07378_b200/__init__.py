@@ -15,7 +15,8 @@ from paper_1604_07378_b200.linalg import (
     svd_rv,
     svd_rv_batch,
 )
-from paper_1604_07378_b200.mesh import TetMesh, bar_mesh, grid_bar, load_tet_mesh, lumped_masses, tet_diff_operators
+from paper_1604_07378_b200.mesh import (SpringNetwork, TetMesh, bar_mesh, grid_bar, load_obj_springs, load_tet_mesh,
+                                        lumped_masses, tet_diff_operators)
 from paper_1604_07378_b200.materials import (
     FitInterval,
     HermiteFn,
@@ -52,7 +53,7 @@ from paper_1604_07378_b200.solvers import (
 
 __all__ = [
     "Factorization", "FactorizationError", "RotVarSVD", "factorize_spd", "solve_prefactored", "svd_rv",
-    "svd_rv_batch", "TetMesh", "bar_mesh", "grid_bar", "load_tet_mesh", "lumped_masses", "tet_diff_operators",
+    "svd_rv_batch", "SpringNetwork", "load_obj_springs", "TetMesh", "bar_mesh", "grid_bar", "load_tet_mesh", "lumped_masses", "tet_diff_operators",
     "FitInterval", "HermiteFn", "LogFn", "MaterialError", "MaterialModel", "PolyFn", "ZeroFn",
     "estimate_stiffness", "make_builtin", "vl_energy_batch", "vl_stress_batch", "DynamicsError", "SimState",
     "SimSystem", "VLGroup", "build_batch_system", "build_system", "gradient", "inertia_target", "objective",

@@ -68,6 +68,7 @@ class SystemDesc(C.Structure):
         ("free_coords", C.c_void_p),
         ("solver", C.c_int32), ("pcg_maxit", C.c_int32), ("pcg_tol", C.c_double),
         ("n_colliders", C.c_int64), ("colliders", C.c_void_p), ("w_col", C.c_double),
+        ("element_kind", C.c_int32), ("pad_e", C.c_int32),
     ]
 
 
@@ -77,6 +78,7 @@ class Collider(C.Structure):
 
 
 QN_COL_HALFSPACE, QN_COL_SPHERE, QN_COL_TORUS = 0, 1, 2
+QN_ELEM_TET, QN_ELEM_SPRING = 0, 1
 QN_MAX_COLLIDERS = 4
 
 

@@ -408,7 +408,9 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   QN_REQUIRE(d && out, QN_ERR_ARG, "system: null argument");
   *out = nullptr;
   QN_REQUIRE(d->n_verts > 0 && d->n_tets >= 0 && d->n_inst >= 1 && d->n_mat >= 1, QN_ERR_ARG, "system: bad sizes");
-  QN_REQUIRE(d->n_tets == 0 || (d->tets && d->Dm_inv && d->vols && d->mats), QN_ERR_ARG, "system: missing tets");
+  QN_REQUIRE(d->element_kind == QN_ELEM_TET || d->element_kind == QN_ELEM_SPRING, QN_ERR_ARG, "system: element kind");
+  QN_REQUIRE(d->n_tets == 0 || (d->tets && (d->Dm_inv || d->element_kind == QN_ELEM_SPRING) && d->vols && d->mats),
+             QN_ERR_ARG, "system: missing tets");
   QN_REQUIRE(d->masses && d->a_indptr && d->a_indices && d->a_values, QN_ERR_ARG, "system: missing arrays");
   QN_REQUIRE(d->h > 0, QN_ERR_ARG, "system: h must be positive");
   QN_REQUIRE(d->n_colliders >= 0 && d->n_colliders <= QN_MAX_COLLIDERS && (d->n_colliders == 0 || d->colliders),
@@ -459,20 +461,22 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   std::vector<int32_t> v2e_ptr(n + 1, 0), v2e((size_t)std::max<int64_t>(mt, 1) * 4);
   for (int64_t t = 0; t < mt; ++t) {
     const int32_t* tv = d->tets + 4 * t;
+    const int corners = d->element_kind == QN_ELEM_SPRING ? 2 : 4;  // springs: (a, b, -1, -1)
     for (int c = 0; c < 4; ++c)
-      if (tv[c] < 0 || tv[c] >= n) {
-        set_error("system: tet vertex out of range");
+      if (c < corners ? (tv[c] < 0 || tv[c] >= n) : tv[c] != -1) {
+        set_error("system: element vertex out of range");
         return fail(QN_ERR_ARG);
       }
     tets[t] = make_int4(tv[0], tv[1], tv[2], tv[3]);
-    for (int k = 0; k < 9; ++k) dminv[(size_t)k * mt + t] = d->Dm_inv[9 * t + k];
-    for (int c = 0; c < 4; ++c) v2e_ptr[tv[c] + 1]++;
+    for (int k = 0; k < 9; ++k) dminv[(size_t)k * mt + t] = d->Dm_inv ? d->Dm_inv[9 * t + k] : 0.0;
+    for (int c = 0; c < corners; ++c) v2e_ptr[tv[c] + 1]++;
   }
   for (int64_t i = 0; i < n; ++i) v2e_ptr[i + 1] += v2e_ptr[i];
   {
     std::vector<int32_t> fill(v2e_ptr.begin(), v2e_ptr.end() - 1);
     for (int64_t t = 0; t < mt; ++t)
-      for (int c = 0; c < 4; ++c) v2e[fill[d->tets[4 * t + c]]++] = (int32_t)(4 * t + c);
+      for (int c = 0; c < 4; ++c)
+        if (d->tets[4 * t + c] >= 0) v2e[fill[d->tets[4 * t + c]]++] = (int32_t)(4 * t + c);
   }
   if (d->tet_mat) {
     for (int64_t t = 0; t < mt; ++t)
@@ -596,6 +600,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_fixed = (int32_t)d->n_fixed;
   v.nblk_v = div_up(3 * n, kVertexThreads);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, 128));
+  v.spring = d->element_kind == QN_ELEM_SPRING ? 1 : 0;
   if (d->n_colliders > 0) {  // colliders: per (instance, vertex, collider) constraint state
     const int64_t nc = d->n_colliders;
     qn_collider* dc;

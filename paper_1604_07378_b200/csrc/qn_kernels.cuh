@@ -92,10 +92,38 @@ constexpr int kFStride = 13;  // padded per-thread stride of the staged corner f
 // convergent).  Tets not in `mat_sel` (>= 0) contribute zero.  The 12 forces
 // are staged in shared memory and written block-contiguously (coalesced) by
 // store_forces().
+// Edge spring (a, b) of a spring network (SpringGroup, dynamics.py:111-151):
+// energy w/2 (|d| - r)^2 and forces -+ w (1 - r/|d|) d, w = k (material a.c[0]),
+// r = vols[t]; corners 2, 3 of the element stay zero.
+__device__ __forceinline__ double spring_thread(const SysView& v, const double* __restrict__ x, int t, int t_raw, int4 tv,
+                                             const qn_material* mats, int mat_sel, double* fsm) {
+  const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
+  const double w = mats[mi].a.c[0];
+  const double r = __ldg(v.vols + t);
+  double d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = x[3 * tv.y + a] - x[3 * tv.x + a];
+  const double len = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+  const double e = 0.5 * w * ((len - r) * (len - r));
+  const double s = w * (1.0 - r / fmax(len, 1e-300));
+  const bool sel = mat_sel < 0 || mi == mat_sel;
+  double* fs = fsm + threadIdx.x * kFStride;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double rs = s * d[a];
+    fs[a] = sel ? -rs : 0.0;
+    fs[3 + a] = sel ? rs : 0.0;
+    fs[6 + a] = 0.0;
+    fs[9 + a] = 0.0;
+  }
+  return t_raw < v.mt && sel ? e : 0.0;
+}
+
 __device__ __forceinline__ double tet_thread(const SysView& v, const double* __restrict__ x, int b, int t_raw,
                                              const qn_material* mats, int mat_sel, double* fsm) {
   const int t = min(t_raw, v.mt - 1);
   const int4 tv = __ldg(v.tets + t);
+  if (v.spring) return spring_thread(v, x, t, t_raw, tv, mats, mat_sel, fsm);
   const int id[4] = {tv.x, tv.y, tv.z, tv.w};
   double xs[4][3];
 #pragma unroll

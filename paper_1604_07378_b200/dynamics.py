@@ -9,9 +9,10 @@ solver workspace, CUDA graph of the frame).  `build_batch_system` adds the
 configs[3] case: many instances of one mesh with per-instance materials and
 numeric factors.
 
-Out of the B200 hot-path scope ("next" rows): ARAP / spring PD
-groups and anisotropic fibres raise NotImplementedError; colliders (HalfSpace,
-SphereCollider, TorusCollider) run inside the frame graph.
+Beyond the VL tet groups: ARAP tets run as a VL
+material, spring networks (cloth) run the spring branch of the element kernel,
+colliders (HalfSpace, SphereCollider, TorusCollider) run inside the frame
+graph; anisotropic fibres raise NotImplementedError.
 """
 
 from __future__ import annotations
@@ -25,7 +26,7 @@ import scipy.sparse
 from paper_1604_07378_b200 import _lib
 from paper_1604_07378_b200.linalg import Factorization
 from paper_1604_07378_b200.materials import FitInterval, MaterialModel, PDMaterial, estimate_stiffness
-from paper_1604_07378_b200.mesh import TetMesh, lumped_masses, tet_diff_operators
+from paper_1604_07378_b200.mesh import SpringNetwork, TetMesh, lumped_masses, tet_diff_operators
 
 DEFAULT_TIMESTEP = 1.0 / 30.0      # dynamics.py:28
 DEFAULT_GRAVITY = (0.0, 0.0, -9.8)  # dynamics.py:29
@@ -66,6 +67,21 @@ class VLGroup:
         _lib.check(_lib.load().qn_system_elements(self._system._h, self._inst, self._index, _lib.ptr(xs),
                                                   C.byref(e), _lib.ptr(buf), _lib.QN_MEM_HOST, None), "group grad")
         out[...] = buf
+
+
+class SpringGroup(VLGroup):
+    """Edge springs with the PD energy (w/2)(|d| - r)^2, w = k (dynamics.py:111-151);
+    GPU seam with the same duck type."""
+
+    def __init__(self, edges, rest, k: float):
+        self.verts = edges
+        self.rest = rest
+        self.w = np.full(edges.shape[0], float(k))
+        self._system, self._index, self._inst = None, 0, 0
+
+    def L_blocks(self):
+        block = np.array([[1.0, -1.0], [-1.0, 1.0]])
+        return self.w[:, None, None] * block[None], self.verts
 
 
 class HalfSpace:
@@ -356,6 +372,78 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     return system
 
 
+def _build_springs(mesh: SpringNetwork, material, h, gravity, fixed, solver, pcg_tol, pcg_maxit, colliders,
+                   collision_weight):
+    """Spring-network system (dynamics.py:374-380 + the common assembly
+    :382-434): one SpringGroup, L = sum w [[1,-1],[-1,1]], A = L + M/h^2 on the
+    free vertices; the per-element pass runs the spring branch of the element
+    kernel (elements (a, b, -1, -1), vols = rest lengths)."""
+    if not isinstance(material, PDMaterial) or material.kind != "mass_spring":
+        raise DynamicsError("spring networks require a mass_spring material")
+    _lib.require_gpu()
+    n, edges, rest = mesh.n, np.asarray(mesh.edges, dtype=np.int64), np.asarray(mesh.rest_lengths, np.float64)
+    masses = lumped_masses(mesh)
+    grp = SpringGroup(edges, rest, material.k)
+    blocks, verts = grp.L_blocks()
+    rows = np.repeat(verts, 2, axis=1).reshape(-1)
+    cols = np.tile(verts, (1, 2)).reshape(-1)
+    L = scipy.sparse.coo_matrix((blocks.reshape(-1), (rows, cols)), shape=(n, n)).tocsr()  # dynamics.py:398-402
+    fixed = np.asarray(sorted(set(int(i) for i in fixed)), dtype=np.int64)
+    if fixed.size and (fixed.min() < 0 or fixed.max() >= n):
+        raise DynamicsError("fixed vertex index out of range")
+    mask = np.ones(n, dtype=bool)
+    mask[fixed] = False
+    free = np.nonzero(mask)[0]
+    if free.size == 0:
+        raise DynamicsError("all vertices fixed; nothing to simulate")
+    A = (L + scipy.sparse.diags(masses / h ** 2)).tocsr()
+    Af = A[free][:, free].tocsr()
+    Af.sort_indices()
+    elems = np.full((edges.shape[0], 4), -1, dtype=np.int32)
+    elems[:, :2] = edges
+    cm = (_lib.Material * 1)()
+    cm[0].a.kind, cm[0].a.c[0] = _lib.QN_FN_ZERO, float(material.k)
+    bbox = mesh.vertices.max(axis=0) - mesh.vertices.min(axis=0)
+    scale = float(np.linalg.norm(bbox)) or 1.0
+    colliders = list(colliders)
+    ccols = (_lib.Collider * max(1, len(colliders)))(*[col.to_c() for col in colliders])
+    w_col = float(collision_weight) if collision_weight is not None else 10.0 * float(material.k)
+    keep = (elems, _lib.f64(rest), _lib.f64(masses), _lib.i32(fixed), _lib.i64(Af.indptr), _lib.i32(Af.indices),
+            _lib.f64(Af.data), _lib.f64(mesh.vertices[free]))
+    d = _lib.SystemDesc()
+    d.n_verts, d.n_tets, d.n_inst, d.n_mat = n, edges.shape[0], 1, 1
+    d.tets, d.Dm_inv, d.vols, d.tet_mat = _lib.ptr(keep[0]), None, _lib.ptr(keep[1]), None
+    d.mats = C.cast(cm, C.c_void_p)
+    d.masses = _lib.ptr(keep[2])
+    d.n_fixed, d.fixed = fixed.size, _lib.ptr(keep[3])
+    d.h = float(h)
+    for a in range(3):
+        d.gravity[a] = float(gravity[a])
+    d.scale = scale
+    d.a_nnz = Af.nnz
+    d.a_indptr, d.a_indices, d.a_values = _lib.ptr(keep[4]), _lib.ptr(keep[5]), _lib.ptr(keep[6])
+    d.free_coords = _lib.ptr(keep[7])
+    if solver not in ("direct", "pcg", "amg"):
+        raise DynamicsError(f"unknown solver {solver!r} (direct | pcg | amg)")
+    d.solver = {"direct": 0, "pcg": 1, "amg": 2}[solver]
+    d.pcg_tol, d.pcg_maxit = float(pcg_tol), int(pcg_maxit)
+    d.n_colliders, d.colliders, d.w_col = len(colliders), C.cast(ccols, C.c_void_p), w_col
+    d.element_kind = _lib.QN_ELEM_SPRING
+    handle = C.c_void_p()
+    _lib.check(_lib.load().qn_system_create(C.byref(d), C.byref(handle)), "build_system")
+    sysfact = None
+    if solver == "direct":
+        fh = C.c_void_p()
+        _lib.check(_lib.load().qn_system_factor(handle, C.byref(fh)))
+        sysfact = Factorization._borrow(fh, free.size, 1)
+    system = SimSystem(mesh=mesh, masses=masses, h=float(h), gravity=np.asarray(gravity, dtype=np.float64),
+                       groups=[grp], fixed=fixed, free=free, L=L, sysfact=sysfact, scale=scale, n_inst=1,
+                       materials=[[material]], pd_groups=[grp], a_nnz=int(Af.nnz), colliders=colliders,
+                       w_col=w_col, _h=handle)
+    grp._system = system
+    return system
+
+
 def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(), aniso=None,
                  colliders=(), collision_weight: float | None = None,
                  fit_interval: FitInterval = FitInterval(), solver: str = "direct", pcg_tol: float = 1e-10,
@@ -367,6 +455,11 @@ def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_G
     ||r|| <= pcg_tol ||b|| (configs[4]: meshes too large to factor);
     solver="amg" uses CG preconditioned by a smoothed-aggregation AMG V-cycle
     (same tolerance, ~40x fewer iterations on configs[4])."""
+    if isinstance(mesh, SpringNetwork):
+        if aniso:
+            raise DynamicsError("anisotropy applies to tet meshes only")
+        return _build_springs(mesh, materials, h, gravity, fixed, solver, pcg_tol, pcg_maxit, colliders,
+                              collision_weight)
     if aniso:
         raise NotImplementedError("anisotropic fibres are outside the B200 hot path (SURVEY §8f)")
     assign = _assign(mesh, materials)

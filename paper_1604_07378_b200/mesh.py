@@ -34,6 +34,63 @@ class TetMesh:
 _CUBE6 = np.array([(0, 1, 3, 7), (0, 3, 2, 7), (0, 2, 6, 7), (0, 6, 4, 7), (0, 4, 5, 7), (0, 5, 1, 7)])
 
 
+@dataclass
+class SpringNetwork:
+    """Edge-spring discretisation of a triangle mesh (mesh.py:31-43)."""
+
+    vertices: np.ndarray  # (n, 3)
+    edges: np.ndarray  # (m, 2)
+    rest_lengths: np.ndarray  # (m,)
+    faces: np.ndarray  # (f, 3), for mass lumping
+    density: float = 1.0  # kg/m^2 (areal)
+    fixed: set = field(default_factory=set)
+
+    @property
+    def n(self) -> int:
+        return self.vertices.shape[0]
+
+
+def load_obj_springs(path, density: float = 1.0) -> SpringNetwork:
+    """OBJ triangle mesh as a spring network: unique triangle edges, sorted
+    (mesh.py:135-171)."""
+    try:
+        with open(path) as fh:
+            raw = fh.readlines()
+    except OSError as exc:
+        raise MeshError(f"cannot read {path}: {exc}") from exc
+    verts, faces = [], []
+    for lineno, line in enumerate(raw, 1):
+        text = line.split("#", 1)[0].strip()
+        if not text:
+            continue
+        parts = text.split()
+        if parts[0] == "v":
+            try:
+                verts.append([float(parts[1]), float(parts[2]), float(parts[3])])
+            except (ValueError, IndexError) as exc:
+                raise MeshError(f"{path}:{lineno}: bad vertex record {text!r}") from exc
+        elif parts[0] == "f":
+            try:
+                faces.append([int(p.split("/")[0]) - 1 for p in parts[1:4]])
+            except (ValueError, IndexError) as exc:
+                raise MeshError(f"{path}:{lineno}: bad face record {text!r}") from exc
+    if not verts or not faces:
+        raise MeshError(f"{path}: no triangles found")
+    vertices = np.asarray(verts)
+    faces = np.asarray(faces, dtype=np.int64)
+    if faces.min() < 0 or faces.max() >= vertices.shape[0]:
+        raise MeshError(f"{path}: face index out of range")
+    edge_set = set()
+    for tri in faces:
+        for a, b in ((tri[0], tri[1]), (tri[1], tri[2]), (tri[0], tri[2])):
+            edge_set.add((min(a, b), max(a, b)))
+    edges = np.asarray(sorted(edge_set), dtype=np.int64)
+    rest = np.linalg.norm(vertices[edges[:, 1]] - vertices[edges[:, 0]], axis=1)
+    if np.any(rest <= 0):
+        raise MeshError(f"{path}: zero-length edge in mesh")
+    return SpringNetwork(vertices=vertices, edges=edges, rest_lengths=rest, faces=faces, density=float(density))
+
+
 def grid_bar(nx, ny, nz, size):
     """Freudenthal 6-tet bar, vectorised (same ids and orientation as
     qnsim.assets.bar_mesh, assets.py:10-69): vertex (i, j, k) has id
@@ -88,12 +145,20 @@ def tet_volumes(mesh: TetMesh) -> np.ndarray:
     return np.linalg.det(v[:, 1:] - v[:, :1]) / 6.0
 
 
-def lumped_masses(mesh: TetMesh) -> np.ndarray:
-    """rho V / 4 to each corner (mesh.py:178-197)."""
-    share = mesh.density * tet_volumes(mesh) / 4.0
+def lumped_masses(mesh) -> np.ndarray:
+    """rho V / 4 to each tet corner, or rho A / 3 to each triangle corner of a
+    spring network (mesh.py:176-197)."""
     m = np.zeros(mesh.n)
-    for c in range(4):
-        np.add.at(m, mesh.tets[:, c], share)
+    if isinstance(mesh, SpringNetwork):
+        v = mesh.vertices[mesh.faces]
+        areas = 0.5 * np.linalg.norm(np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]), axis=1)
+        share = mesh.density * areas / 3.0
+        for c in range(3):
+            np.add.at(m, mesh.faces[:, c], share)
+    else:
+        share = mesh.density * tet_volumes(mesh) / 4.0
+        for c in range(4):
+            np.add.at(m, mesh.tets[:, c], share)
     bad = np.nonzero(m <= 0)[0]
     if bad.size:
         raise MeshError(f"vertex {bad[0]} has zero mass (isolated vertex?)")

@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -297,12 +297,33 @@ def gen_chebyshev():
     print("chebyshev", time.time() - t, {k: v for k, v in out.items() if k.endswith("fallbacks")})
 
 
+def gen_cloth():
+    """The reference's cloth_hang.json scenario (mass-spring network,
+    SURVEY §8f row f3) through its harness."""
+    from qnsim import harness as ref_harness
+    t = time.time()
+    scn = ref_harness.load_scenario(os.path.join(REF, "scenarios", "cloth_hang.json"))
+    run = ref_harness.SimulationRun(scn)
+    g, tr, pos = [], [], {}
+    frames = 20
+    for f in range(frames):
+        rec = run.step()
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+        if f in (0, 9, 19):
+            pos[f"x_{f}"] = run.state.q_l.copy()
+    np.savez_compressed(os.path.join(HERE, "frames_cloth_hang.npz"), frames=frames, g=np.array(g),
+                        trials=np.array(tr), fixed=np.asarray(run.system.fixed), **pos)
+    print("cloth", time.time() - t)
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
     for src in ("frontend/tests/fixtures/twist_lbfgs.csv", "frontend/tests/fixtures/twist_pd_qn.csv",
                 "assets/bar_small.node", "assets/bar_small.ele", "scenarios/bar_twist_small.json",
-                "assets/sphere.node", "assets/sphere.ele", "scenarios/sphere_drop.json"):
+                "assets/sphere.node", "assets/sphere.ele", "scenarios/sphere_drop.json",
+                "assets/cloth20.obj", "scenarios/cloth_hang.json"):
         shutil.copy(os.path.join(REF, src), os.path.join(dst, os.path.basename(src)))
 
 
@@ -317,6 +338,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--chebyshev" in sys.argv:
         gen_chebyshev()
+        sys.exit(0)
+    if "--cloth" in sys.argv:
+        gen_cloth()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

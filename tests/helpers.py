@@ -137,3 +137,22 @@ class SphereDropScene:
         self.fixed = np.zeros(0, dtype=np.int64)
         self.q_l = self.verts.copy()
         self.q_prev = self.verts.copy()
+
+
+class ClothScene:
+    """The reference's cloth_hang.json: cloth20.obj as a mass-spring network
+    (k = 200, areal density 0.2), corners 0 and 19 pinned, lbfgs 10 its."""
+
+    def __init__(self):
+        with open(os.path.join(FIX, "cloth_hang.json")) as fh:
+            scn = json.load(fh)
+        self.verts, self.edges, self.rest, self.faces = O.read_obj_springs(os.path.join(FIX, "cloth20.obj"))
+        self.density = float(scn["mesh"]["density"])
+        self.k = float(scn["material"]["k"])
+        self.h = float(scn["h"])
+        self.gravity = tuple(scn["gravity"])
+        self.fixed = np.asarray(scn["fixed"][0]["indices"], dtype=np.int64)
+        self.iterations = int(scn["solver"]["iterations"])
+        self.m = 5
+        self.q_l = self.verts.copy()
+        self.q_prev = self.verts.copy()

@@ -669,3 +669,23 @@ def test_lbfgs_scaled_identity_against_reference_golden(graph):
     st2, rec2 = Q.simulate_frame(system, Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy()),
                                  Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
     assert rec2.ls_trials[0] == 1
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_cloth_hang_scenario_against_reference_harness(graph):
+    """Spring networks (cloth): the reference's cloth_hang.json, 20 frames."""
+    from paper_1604_07378_b200.materials import PDMaterial
+    from tests.helpers import ClothScene
+    cs = ClothScene()
+    d = golden("frames_cloth_hang.npz")
+    mesh = Q.load_obj_springs(os.path.join(FIX, "cloth20.obj"), density=cs.density)
+    assert np.array_equal(mesh.edges, cs.edges)
+    system = Q.build_system(mesh, PDMaterial("mass_spring", cs.k), h=cs.h, gravity=cs.gravity, fixed=cs.fixed)
+    if not graph:
+        system.set_graph_mode(False)
+    res = run_gpu(system, cs, int(d["frames"]))
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d["g"][f]) <= G_TOL
+        assert rec.ls_trials == list(d["trials"][f])
+        if f"x_{f}" in d:
+            assert rel(x, d[f"x_{f}"]) <= X_TOL

@@ -221,3 +221,20 @@ def test_oracle_lbfgs_scaled_identity_matches_reference():
         np.testing.assert_allclose(rec.g, d["scaled_g"][f], rtol=1e-12)
         assert list(rec.ls_trials) == list(d["scaled_trials"][f])
     np.testing.assert_allclose(x, d["scaled_x_7"], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+def test_oracle_cloth_hang_matches_reference_harness():
+    """Spring networks (mass_spring, dynamics.py:111-151): cloth_hang.json."""
+    from tests.helpers import ClothScene
+    cs = ClothScene()
+    d = golden("frames_cloth_hang.npz")
+    assert np.array_equal(cs.fixed, d["fixed"])
+    osys = O.build_springs(cs.verts, cs.edges, cs.rest, cs.faces, cs.density, cs.k, cs.h, cs.gravity, cs.fixed)
+    q_l, q_prev = cs.q_l.copy(), cs.q_prev.copy()
+    for f in range(int(d["frames"])):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=cs.iterations, m=cs.m)
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d["g"][f], rtol=1e-12, atol=1e-18)
+        assert list(rec.ls_trials) == list(d["trials"][f])
+        if f"x_{f}" in d:
+            np.testing.assert_allclose(x, d[f"x_{f}"], rtol=0, atol=1e-12 * np.abs(x).max())

@@ -46,6 +46,9 @@ extern "C" {
 #define QN_FN_HERMITE 3
 #define QN_FN_SQDEV 4    /* c[0] (x - c[1])^2: the ARAP tet energy (w/2)||F - R||^2 = vol k/2 sum (s_i - 1)^2
                             of dynamics.ARAPGroup (dynamics.py:73-108) as a Valanis-Landel a(x) */
+#define QN_FN_ANISO 5    /* material a of an anisotropic-fibre element (dynamics.AnisoGroup,
+                            dynamics.py:154-193): c[0..2] = unit fibre d, c[3] = kappa;
+                            energy vol kappa/2 (|F d| - 1)^2, no SVD                    */
 
 #define QN_MAX_COEF 12   /* polynomial coefficients (ascending)  */
 #define QN_MAX_KNOTS 12  /* cubic Hermite control points          */

@@ -385,6 +385,37 @@ class ARAPTetGroup:
 
 
 @dataclass
+class AnisoGroupO:
+    """dynamics.AnisoGroup (dynamics.py:154-193): V kappa/2 (|F d| - 1)^2."""
+    tets: np.ndarray
+    G: np.ndarray
+    vols: np.ndarray
+    d: np.ndarray
+    kappa: np.ndarray
+
+    def __post_init__(self):
+        self.d = self.d / np.linalg.norm(self.d, axis=-1, keepdims=True)
+        self.k = self.kappa  # w = vols * kappa (for L and w_col)
+
+    def _fiber(self, x):
+        F = np.einsum("eva,evc->eac", x[self.tets], self.G)
+        u = np.einsum("eac,ec->ea", F, np.broadcast_to(self.d, (self.tets.shape[0], 3)))
+        return u, np.linalg.norm(u, axis=1)
+
+    def energy(self, x):
+        _, nu = self._fiber(x)
+        return float((0.5 * (self.vols * self.kappa) * (nu - 1.0) ** 2).sum())
+
+    def add_gradient(self, x, out):
+        u, nu = self._fiber(x)
+        nu = np.maximum(nu, 1e-12)
+        P = ((self.vols * self.kappa) * (nu - 1.0) / nu)[:, None, None] * np.einsum(
+            "ea,ec->eac", u, np.broadcast_to(self.d, (self.tets.shape[0], 3)))
+        g = np.einsum("eac,evc->eva", P, self.G)
+        np.add.at(out, self.tets.reshape(-1), g.reshape(-1, 3))
+
+
+@dataclass
 class SpringGroupO:
     """dynamics.SpringGroup (dynamics.py:111-151): (w/2)(|d| - r)^2, w = k."""
     edges: np.ndarray
@@ -508,7 +539,7 @@ class System:
 
 
 def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), factor="sparse",
-          masses=None, colliders=(), collision_weight=None):
+          masses=None, colliders=(), collision_weight=None, aniso=None):
     """Restates dynamics.build_system (dynamics.py:351-434) for VL tet groups.
 
     `materials` is a VLMaterial (all tets) or a list of (tet_index_array, VLMaterial).
@@ -528,6 +559,10 @@ def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), fa
                 groups.append(ARAPTetGroup(tets[idx], G[idx], vols[idx], float(mat.k)))
             else:
                 groups.append(TetGroup(tets[idx], G[idx], vols[idx], mat, fit_stiffness(mat, *fit)))
+        if aniso:  # dynamics.py:368-373
+            idx = np.asarray([a[0] for a in aniso], dtype=np.int64)
+            groups.append(AnisoGroupO(tets[idx], G[idx], vols[idx], np.asarray([a[1] for a in aniso], dtype=np.float64),
+                                      np.asarray([a[2] for a in aniso], dtype=np.float64) * np.ones(idx.size)))
     rows, cols, vals = [], [], []
     for g in groups:
         w = g.vols * g.k                                          # dynamics.py:48

@@ -25,7 +25,7 @@ QN_ERR_UNSUPPORTED = 6
 QN_MEM_HOST = 0
 QN_MEM_DEVICE = 1
 
-QN_FN_ZERO, QN_FN_POLY, QN_FN_LOG, QN_FN_HERMITE, QN_FN_SQDEV = 0, 1, 2, 3, 4
+QN_FN_ZERO, QN_FN_POLY, QN_FN_LOG, QN_FN_HERMITE, QN_FN_SQDEV, QN_FN_ANISO = 0, 1, 2, 3, 4, 5
 QN_MAX_COEF = 12
 QN_MAX_KNOTS = 12
 QN_MAX_M = 16

@@ -601,6 +601,9 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.nblk_v = div_up(3 * n, kVertexThreads);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, 128));
   v.spring = d->element_kind == QN_ELEM_SPRING ? 1 : 0;
+  v.aniso = 0;
+  for (int64_t q = 0; q < ni * d->n_mat && mt > 0; ++q)
+    if (d->mats[q].a.kind == QN_FN_ANISO) v.aniso = 1;
   if (d->n_colliders > 0) {  // colliders: per (instance, vertex, collider) constraint state
     const int64_t nc = d->n_colliders;
     qn_collider* dc;

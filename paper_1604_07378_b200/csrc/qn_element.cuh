@@ -330,4 +330,35 @@ __device__ __forceinline__ double tet_eval(const qn_material& M, const double (&
   return vol * psi;
 }
 
+// anisotropic fibre (dynamics.py:154-193): u = F d, energy w/2 (|u| - 1)^2 with
+// w = vol kappa, P = w (|u|' - 1)/|u|' u d^T with |u|' = max(|u|, 1e-12)
+__device__ __forceinline__ double aniso_eval(const qn_material& M, const double (&x)[4][3],
+                                             const double (&Dm)[3][3], double vol, double (&f)[4][3]) {
+  const double d[3] = {M.a.c[0], M.a.c[1], M.a.c[2]};
+  const double w = vol * M.a.c[3];
+  double u[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double e0 = x[1][a] - x[0][a], e1 = x[2][a] - x[0][a], e2 = x[3][a] - x[0][a];
+    double Fa[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Fa[c] = e0 * Dm[0][c] + e1 * Dm[1][c] + e2 * Dm[2][c];
+    u[a] = Fa[0] * d[0] + Fa[1] * d[1] + Fa[2] * d[2];
+  }
+  const double nu = sqrt((u[0] * u[0] + u[1] * u[1]) + u[2] * u[2]);
+  const double nuc = fmax(nu, 1e-12);
+  const double coef = w * (nuc - 1.0) / nuc;
+  double G0[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) G0[c] = -(Dm[0][c] + Dm[1][c] + Dm[2][c]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double pa = coef * u[a];
+    f[0][a] = pa * (d[0] * G0[0] + d[1] * G0[1] + d[2] * G0[2]);
+#pragma unroll
+    for (int v = 1; v < 4; ++v) f[v][a] = pa * (d[0] * Dm[v - 1][0] + d[1] * Dm[v - 1][1] + d[2] * Dm[v - 1][2]);
+  }
+  return 0.5 * w * ((nu - 1.0) * (nu - 1.0));
+}
+
 }  // namespace qn

@@ -119,6 +119,9 @@ __device__ __forceinline__ double spring_thread(const SysView& v, const double* 
   return t_raw < v.mt && sel ? e : 0.0;
 }
 
+// kAniso: the system has anisotropic-fibre elements (a separate instantiation,
+// so the plain per-tet kernel keeps its register allocation)
+template <bool kAniso = false>
 __device__ __forceinline__ double tet_thread(const SysView& v, const double* __restrict__ x, int b, int t_raw,
                                              const qn_material* mats, int mat_sel, double* fsm) {
   const int t = min(t_raw, v.mt - 1);
@@ -140,7 +143,11 @@ __device__ __forceinline__ double tet_thread(const SysView& v, const double* __r
   const double vol = __ldg(v.vols + t);
   const int mi = v.tet_mat ? __ldg(v.tet_mat + t) : 0;
   double f[4][3];
+  // every lane runs the SVD path (its sweeps end on warp votes, so a warp
+  // holding both element kinds must not diverge there); fibre elements then
+  // replace the result (their VL material evaluates to zero)
   double e = tet_eval<true>(mats[mi], xs, Dm, vol, f);
+  if (kAniso && mats[mi].a.kind == QN_FN_ANISO) e = aniso_eval(mats[mi], xs, Dm, vol, f);
   const bool keep = t_raw < v.mt;
   const bool sel = mat_sel < 0 || mi == mat_sel;
   double* fs = fsm + threadIdx.x * kFStride;

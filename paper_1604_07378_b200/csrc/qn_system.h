@@ -99,7 +99,7 @@ struct DevConfig {
 
 struct SysView {
   int32_t n, mt, n_inst, n_mat, n_fixed, nblk_v, nblk_t, rec_cap;
-  int32_t spring, pad_s;  // elements are edge springs (a, b, -1, -1), vols = rest lengths
+  int32_t spring, aniso;  // elements are edge springs (a, b, -1, -1), vols = rest lengths; fibre materials present
   double h;
   double grav[3];
   const int4* tets;

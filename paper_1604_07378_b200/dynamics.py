@@ -12,7 +12,7 @@ numeric factors.
 Beyond the VL tet groups: ARAP tets run as a VL
 material, spring networks (cloth) run the spring branch of the element kernel,
 colliders (HalfSpace, SphereCollider, TorusCollider) run inside the frame
-graph; anisotropic fibres raise NotImplementedError.
+graph, anisotropic fibres run the fibre branch of the per-tet kernel.
 """
 
 from __future__ import annotations
@@ -25,7 +25,7 @@ import scipy.sparse
 
 from paper_1604_07378_b200 import _lib
 from paper_1604_07378_b200.linalg import Factorization
-from paper_1604_07378_b200.materials import FitInterval, MaterialModel, PDMaterial, estimate_stiffness
+from paper_1604_07378_b200.materials import AnisoMaterial, FitInterval, MaterialModel, PDMaterial, estimate_stiffness
 from paper_1604_07378_b200.mesh import SpringNetwork, TetMesh, lumped_masses, tet_diff_operators
 
 DEFAULT_TIMESTEP = 1.0 / 30.0      # dynamics.py:28
@@ -233,6 +233,23 @@ def _assign(mesh, materials):
             raise NotImplementedError(f"material {mat!r}: only Valanis-Landel tet groups run on the B200 path")
         out.append((np.asarray(idx, dtype=np.int64), mat))
     return out
+
+
+def _aniso_groups(mesh, aniso):
+    """(element_index, direction, kappa) triples -> one fibre group per distinct
+    (direction, kappa), in order of first appearance, elements in list order."""
+    keyed = {}
+    for e, d, kappa in aniso:
+        e = int(e)
+        if not 0 <= e < mesh.tets.shape[0]:
+            raise DynamicsError(f"anisotropy element {e} out of range")
+        dn = np.asarray(d, dtype=np.float64)
+        dn = dn / np.linalg.norm(dn)
+        if float(kappa) < 0:
+            raise DynamicsError("anisotropic stiffness must be non-negative")
+        key = (float(dn[0]), float(dn[1]), float(dn[2]), float(kappa))
+        keyed.setdefault(key, []).append(e)
+    return [(np.asarray(idx, dtype=np.int64), AnisoMaterial(key[:3], key[3])) for key, idx in keyed.items()]
 
 
 def _pattern_sum(rows, cols, n):
@@ -460,9 +477,9 @@ def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_G
             raise DynamicsError("anisotropy applies to tet meshes only")
         return _build_springs(mesh, materials, h, gravity, fixed, solver, pcg_tol, pcg_maxit, colliders,
                               collision_weight)
-    if aniso:
-        raise NotImplementedError("anisotropic fibres are outside the B200 hot path (SURVEY §8f)")
     assign = _assign(mesh, materials)
+    if aniso:  # AnisoGroup appended after the material groups (dynamics.py:368-373)
+        assign = assign + _aniso_groups(mesh, aniso)
     return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit,
                   colliders, collision_weight)
 

@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -34,7 +34,7 @@ from qnsim import mesh as ref_mesh  # noqa: E402
 from qnsim import solvers as ref_solvers  # noqa: E402
 
 from paper_1604_07378_b200 import scenes  # noqa: E402
-from tests.helpers import collider_bar_scene, material_specs  # noqa: E402
+from tests.helpers import aniso_cases, collider_bar_scene, material_specs  # noqa: E402
 
 
 def ref_material(spec, name="custom"):
@@ -317,6 +317,31 @@ def gen_cloth():
     print("cloth", time.time() - t)
 
 
+def gen_aniso():
+    """Anisotropic fibres (dynamics.AnisoGroup) through the
+    reference's build_system: every tet reinforced along one direction (the
+    harness's "anisotropy" key), and two fibre families on alternating tets."""
+    t = time.time()
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    m = sc.tets.shape[0]
+    cases = aniso_cases(m)
+    out = {}
+    for name, aniso in cases.items():
+        mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+        system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed,
+                                      aniso=aniso)
+        state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+        cfg = ref_solvers.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+        g, tr = [], []
+        for f in range(10):
+            state, rec = ref_solvers.simulate_frame(system, state, cfg)
+            g.append(rec.g)
+            tr.append(rec.ls_trials)
+        out[f"{name}_g"], out[f"{name}_trials"], out[f"{name}_x_9"] = np.array(g), np.array(tr), state.q_l.copy()
+    np.savez_compressed(os.path.join(HERE, "frames_aniso.npz"), **out)
+    print("aniso", time.time() - t)
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
@@ -341,6 +366,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--cloth" in sys.argv:
         gen_cloth()
+        sys.exit(0)
+    if "--aniso" in sys.argv:
+        gen_aniso()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

@@ -156,3 +156,9 @@ class ClothScene:
         self.m = 5
         self.q_l = self.verts.copy()
         self.q_prev = self.verts.copy()
+
+
+def aniso_cases(m):
+    """Fibre assignments of tests/golden/frames_aniso.npz (make_golden.gen_aniso)."""
+    return {"uniform": [(e, (1.0, 0.2, 0.0), 3e5) for e in range(m)],
+            "two": [(e, (1.0, 0.0, 1.0) if e % 2 else (0.0, 1.0, 0.5), 1e5 if e % 2 else 4e5) for e in range(m)]}

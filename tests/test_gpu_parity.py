@@ -689,3 +689,18 @@ def test_cloth_hang_scenario_against_reference_harness(graph):
         assert rec.ls_trials == list(d["trials"][f])
         if f"x_{f}" in d:
             assert rel(x, d[f"x_{f}"]) <= X_TOL
+
+
+@pytest.mark.parametrize("name", ["uniform", "two"])
+def test_aniso_fibres_against_reference_golden(name):
+    """Anisotropic fibres (dynamics.AnisoGroup) on the fibre branch of the
+    per-tet kernel, appended after the Neo-Hookean group: 10 frames."""
+    from tests.helpers import aniso_cases
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    d = golden("frames_aniso.npz")
+    system = build(sc, aniso=aniso_cases(sc.tets.shape[0])[name])
+    res = run_gpu(system, sc, 10)
+    for f, (x, rec) in enumerate(res):
+        assert rel(rec.g, d[f"{name}_g"][f]) <= G_TOL
+        assert rec.ls_trials == list(d[f"{name}_trials"][f])
+    assert rel(res[-1][0], d[f"{name}_x_9"]) <= X_TOL

@@ -238,3 +238,20 @@ def test_oracle_cloth_hang_matches_reference_harness():
         assert list(rec.ls_trials) == list(d["trials"][f])
         if f"x_{f}" in d:
             np.testing.assert_allclose(x, d[f"x_{f}"], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+@pytest.mark.parametrize("name", ["uniform", "two"])
+def test_oracle_aniso_matches_reference(name):
+    """Anisotropic fibres (dynamics.AnisoGroup, dynamics.py:154-193)."""
+    from tests.helpers import aniso_cases
+    sc = scenes.c1(grid=(10, 3, 3), iterations=10)
+    d = golden("frames_aniso.npz")
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense", aniso=aniso_cases(sc.tets.shape[0])[name])
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(10):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, m=sc.m)
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d[f"{name}_g"][f], rtol=1e-12)
+        assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
+    np.testing.assert_allclose(x, d[f"{name}_x_9"], rtol=0, atol=1e-12 * np.abs(x).max())

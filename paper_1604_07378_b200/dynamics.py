@@ -252,17 +252,6 @@ def _aniso_groups(mesh, aniso):
     return [(np.asarray(idx, dtype=np.int64), AnisoMaterial(key[:3], key[3])) for key, idx in keyed.items()]
 
 
-def _pattern_sum(rows, cols, n):
-    """CSR pattern of a COO triple and the map contribution -> CSR slot."""
-    key = rows.astype(np.int64) * n + cols
-    uniq, inv = np.unique(key, return_inverse=True)
-    r = (uniq // n).astype(np.int64)
-    c = (uniq % n).astype(np.int64)
-    indptr = np.zeros(n + 1, dtype=np.int64)
-    np.add.at(indptr, r + 1, 1)
-    return np.cumsum(indptr), c, inv, r
-
-
 def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, solver="direct", pcg_tol=1e-10,
            pcg_maxit=20000, colliders=(), collision_weight=None):
     if not isinstance(mesh, TetMesh):
@@ -289,23 +278,15 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     Gs, vs = G[order], vols[order]
     m = tets.shape[0]
 
-    # L = sum_groups w G G^T per instance (dynamics.py:387-402), then A_free
+    # L = sum_groups w G G^T per instance, assembled exactly as the reference
+    # does (COO in group-major order -> CSR, dynamics.py:387-402, so L is bitwise
+    # the reference's), then A = L + M/h^2 restricted to the free dofs (:413-414)
     GG = np.einsum("evc,euc->evu", Gs, Gs) if m else np.zeros((0, 4, 4))
     rows = np.repeat(tets, 4, axis=1).reshape(-1)
     cols = np.tile(tets, (1, 4)).reshape(-1)
-    diag = np.arange(n)
-    all_rows = np.concatenate([rows, diag])
-    all_cols = np.concatenate([cols, diag])
-    indptr, indices, inv, row_of = _pattern_sum(all_rows, all_cols, n)
-    # restrict to free rows/cols
-    keep = mask[row_of] & mask[indices]
-    remap = -np.ones(n, dtype=np.int64)
-    remap[free] = np.arange(free.size)
-    fr, fc = remap[row_of[keep]], remap[indices[keep]]
-    f_indptr = np.zeros(free.size + 1, dtype=np.int64)
-    np.add.at(f_indptr, fr + 1, 1)
-    f_indptr = np.cumsum(f_indptr)
+    diag_m = scipy.sparse.diags(masses / h ** 2)
     values, Ls, groups_per_inst, mats = [], [], [], []
+    f_indptr = a_idx = None
     for assign in inst_materials:
         ks, gl = [], []
         for g, (idx, mat) in enumerate(assign):
@@ -313,14 +294,19 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
             ks.append(k)
             gl.append(VLGroup(mesh.tets[idx], G[idx], vols[idx], mat, k))
         w = (vs * np.asarray(ks)[tet_mat]) if m else np.zeros(0)
-        contrib = np.concatenate([(w[:, None, None] * GG).reshape(-1), masses / h ** 2])
-        sums = np.bincount(inv, weights=contrib, minlength=indices.size)
-        Lv = np.bincount(inv[: rows.size], weights=contrib[: rows.size], minlength=indices.size) if m else \
-            np.zeros(indices.size)
-        Ls.append(scipy.sparse.csr_matrix((Lv, indices, indptr), shape=(n, n)))
-        values.append(sums[keep])
+        L = scipy.sparse.coo_matrix(((w[:, None, None] * GG).reshape(-1), (rows, cols)), shape=(n, n)).tocsr() \
+            if m else scipy.sparse.csr_matrix((n, n))
+        Af = (L + diag_m).tocsr()[free][:, free].tocsr()
+        Af.sort_indices()
+        if f_indptr is None:
+            f_indptr, a_idx = Af.indptr.astype(np.int64), Af.indices
+        elif not (np.array_equal(f_indptr, Af.indptr) and np.array_equal(a_idx, Af.indices)):
+            raise DynamicsError("instances must share the system-matrix pattern")
+        Ls.append(L)
+        values.append(Af.data)
         groups_per_inst.append(gl)
         mats.append([mat for _, mat in assign])
+    fc = a_idx
     a_values = np.concatenate(values)
     a_indices = _lib.i32(fc)
 

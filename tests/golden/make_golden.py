@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso | --writers (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -342,6 +342,31 @@ def gen_aniso():
     print("aniso", time.time() - t)
 
 
+def gen_writers():
+    """The reference harness's output formats (harness.py:390-420): its
+    write_csv on records of two reference frames, its surface_triangles and
+    export_frames on the bar_small mesh."""
+    from types import SimpleNamespace
+    from qnsim import harness as ref_harness
+    sc = scenes.c1(grid=(4, 2, 2), iterations=4)
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    recs, states = [], []
+    for _ in range(2):
+        state, rec = ref_solvers.simulate_frame(system, state, ref_solvers.SolverConfig(kind="lbfgs", iterations=4))
+        rec.cum_ms = [0.125 * (k + 1) for k in range(len(rec.g))]  # deterministic timing column
+        rec.rel_error = [] if not recs else [1.0 / (k + 2) for k in range(len(rec.g))]
+        recs.append(rec)
+        states.append(state.q_l.copy())
+    ref_harness.write_csv(os.path.join(HERE, "writers_report.csv"), SimpleNamespace(records=recs))
+    d = os.path.join(HERE, "writers_obj")
+    ref_harness.export_frames(states[:1], d, ref_mesh.surface_triangles(mesh))
+    np.savez_compressed(os.path.join(HERE, "writers_inputs.npz"), x0=states[0],
+                        **{f"r{f}_{k}": np.asarray(getattr(recs[f], k)) for f in range(2)
+                           for k in ("g", "ls_trials", "cum_ms", "rel_error")})
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
@@ -369,6 +394,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--aniso" in sys.argv:
         gen_aniso()
+        sys.exit(0)
+    if "--writers" in sys.argv:
+        gen_writers()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

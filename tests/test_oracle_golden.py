@@ -255,3 +255,21 @@ def test_oracle_aniso_matches_reference(name):
         np.testing.assert_allclose(rec.g, d[f"{name}_g"][f], rtol=1e-12)
         assert list(rec.ls_trials) == list(d[f"{name}_trials"][f])
     np.testing.assert_allclose(x, d[f"{name}_x_9"], rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+def test_output_writers_match_reference_bytes(tmp_path):
+    """CSV and OBJ output formats (harness.py:390-420, mesh.py:236-249) are
+    byte-identical to the reference harness's files on the same records."""
+    from paper_1604_07378_b200 import io as QIO
+    from paper_1604_07378_b200.mesh import TetMesh
+    from paper_1604_07378_b200.solvers import ConvergenceRecord
+    d = golden("writers_inputs.npz")
+    recs = [ConvergenceRecord(g=d[f"r{f}_g"].tolist(), ls_trials=d[f"r{f}_ls_trials"].tolist(),
+                              cum_ms=d[f"r{f}_cum_ms"].tolist(), rel_error=d[f"r{f}_rel_error"].tolist())
+            for f in range(2)]
+    QIO.write_csv(str(tmp_path / "r.csv"), recs)
+    assert (tmp_path / "r.csv").read_bytes() == open(os.path.join(os.path.dirname(FIX), "writers_report.csv"), "rb").read()
+    sc = scenes.c1(grid=(4, 2, 2))
+    QIO.export_frames([d["x0"]], str(tmp_path / "obj"), QIO.surface_triangles(TetMesh(sc.verts, sc.tets)))
+    ref = open(os.path.join(os.path.dirname(FIX), "writers_obj", "frame_0000.obj"), "rb").read()
+    assert (tmp_path / "obj" / "frame_0000.obj").read_bytes() == ref

@@ -279,6 +279,17 @@ int qn_system_amg_info(qn_system* s, int64_t* out, int64_t cap);
  * launch time. */
 int qn_system_time_kernel(qn_system* s, int32_t kernel, int32_t reps, double* avg_ms, void* stream);
 
+/* Newton direction (solvers.py:167-234): d = -H^-1 g on the free dofs, H =
+ * sum of per-element central-difference Hessian blocks of the corner forces
+ * (step = fd step, e.g. 1e-6 scale) with eigenvalues clamped at eig_floor
+ * (project_psd) + M/h^2, dense, Cholesky-factored (QN_ERR_NOT_SPD when not
+ * SPD).  x, grad, d: (n,3); fixed rows of d are zero.  Single instance, no
+ * colliders; for the small meshes the reference runs Newton on. */
+int qn_newton_direction(qn_system* s, const double* x, const double* grad, double step, double eig_floor, double* d,
+                        int32_t mem, void* stream);
+/* free the Newton workspace of a system (also freed with the process) */
+int qn_newton_release(qn_system* s);
+
 /* Slab decomposition of one mesh across ranks (configs[4]):
  * the per-rank stages of simulate_frame (solvers.py:260-352) with the
  * reference's gradient (dynamics.py:470-478), objective (:460-467),

@@ -847,7 +847,12 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
             log(g_x, 0, 0.0)
             prev_x, prev_g = x, grad
             continue
-        if kind == "chebyshev":                                           # solvers.py:306-311
+        if kind == "newton":                                              # solvers.py:312-315
+            d = direction_newton(sys, x, grad)
+            if float(np.vdot(grad, d)) >= 0.0:
+                d = direction(sys, hist, grad)
+                rec.fallbacks += 1
+        elif kind == "chebyshev":                                         # solvers.py:306-311
             q = direction(sys, hist, grad)
             d, omega = direction_chebyshev(x, x_prev_iter, q, k, omega, rho, S)
             if float(np.vdot(grad, d)) >= 0.0:
@@ -877,6 +882,96 @@ def simulate_frame(sys, q_l, q_prev, iterations=10, m=5, kind="lbfgs", gamma=0.3
         x = x_new
         log(g_new, trials, alpha)
     return x, y, rec
+
+
+# --------------------------------------------------------------------------
+# Newton baseline (solvers.py:167-234, 355-398), VL tet groups
+
+NEWTON_FD_STEP_REL = 1e-6    # solvers.py:32
+HESSIAN_EIG_FLOOR = 1e-8     # solvers.py:31
+
+
+def _vl_elem_gradient(grp, X):
+    """VLGroup.elem_gradient (dynamics.py:50-55)"""
+    F = np.einsum("eva,evc->eac", X, grp.G)
+    U, s, V = svd_rv(F)
+    P = np.einsum("eab,eb,ecb->eac", U, vl_stress(grp.mat, s), V)
+    return grp.vols[:, None, None] * np.einsum("eac,evc->eva", P, grp.G)
+
+
+def _elem_hessians_fd(grp, x, step):
+    """solvers.py:170-185"""
+    X0 = x[grp.tets]
+    k, a, _ = X0.shape
+    dim = 3 * a
+    H = np.empty((k, dim, dim))
+    for v in range(a):
+        for c in range(3):
+            Xp = X0.copy()
+            Xp[:, v, c] += step
+            Xm = X0.copy()
+            Xm[:, v, c] -= step
+            H[:, :, 3 * v + c] = ((_vl_elem_gradient(grp, Xp) - _vl_elem_gradient(grp, Xm)) / (2.0 * step)).reshape(k, dim)
+    return 0.5 * (H + np.swapaxes(H, 1, 2))
+
+
+def _project_psd(blocks, floor=HESSIAN_EIG_FLOOR):
+    """solvers.py:188-192"""
+    w, Q = np.linalg.eigh(blocks)
+    return np.einsum("kij,kj,klj->kil", Q, np.maximum(w, floor), Q)
+
+
+def direction_newton(sys, x, grad):
+    """solvers.py:195-234 (no colliders): dense free-dof Hessian, cho_factor."""
+    n = sys.n
+    step = NEWTON_FD_STEP_REL * sys.scale
+    rows, cols, vals = [], [], []
+    for grp in sys.groups:
+        H = _project_psd(_elem_hessians_fd(grp, x, step))
+        a = grp.tets.shape[1]
+        dofs = (grp.tets[:, :, None] * 3 + np.arange(3)).reshape(grp.tets.shape[0], 3 * a)
+        rows.append(np.repeat(dofs, 3 * a, axis=1).reshape(-1))
+        cols.append(np.tile(dofs, (1, 3 * a)).reshape(-1))
+        vals.append(H.reshape(-1))
+    H = scipy.sparse.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                shape=(3 * n, 3 * n)).toarray()
+    H[np.diag_indices_from(H)] += np.repeat(sys.masses / sys.h ** 2, 3)
+    free3 = (sys.free[:, None] * 3 + np.arange(3)).reshape(-1)
+    fac = scipy.linalg.cho_factor(H[np.ix_(free3, free3)])
+    d = np.zeros_like(x)
+    d[sys.free] = scipy.linalg.cho_solve(fac, -grad[sys.free].reshape(-1)).reshape(-1, 3)
+    return d
+
+
+def newton_reference(sys, q_l, q_prev, grad_tol_rel=1e-10, max_iterations=200, gamma=0.3, alpha_init=2.0,
+                     shrink=0.5):
+    """solvers.py:355-398: (x*, g*)"""
+    y = inertia_target(sys, q_l, q_prev)
+    x = y.copy()
+    tol = grad_tol_rel * max(1.0, float(np.linalg.norm(gradient(sys, y, x))))
+    g_x = objective(sys, y, x)
+    best, stalled = np.inf, 0
+    for _ in range(max_iterations):
+        g_x = objective(sys, y, x)
+        grad = gradient(sys, y, x)
+        gn = float(np.linalg.norm(grad))
+        if gn <= tol:
+            break
+        if gn >= 0.999 * best:
+            stalled += 1
+            if stalled >= 3:
+                break
+        else:
+            stalled = 0
+        best = min(best, gn)
+        d = direction_newton(sys, x, grad)
+        if float(np.vdot(grad, d)) >= 0.0:
+            d = direction(sys, History(0), grad)
+        try:
+            _, x, g_x, _ = line_search(sys, y, x, d, g_x, grad, gamma, alpha_init, shrink)
+        except OracleStagnation:
+            break
+    return x, g_x
 
 
 def twist_targets(rest, idx, axis, center, deg_per_s, t):

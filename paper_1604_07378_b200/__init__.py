@@ -48,6 +48,8 @@ from paper_1604_07378_b200.solvers import (
     SolverError,
     StagnationError,
     relative_error,
+    direction_newton,
+    newton_reference,
     simulate_frame,
 )
 
@@ -58,5 +60,5 @@ __all__ = [
     "estimate_stiffness", "make_builtin", "vl_energy_batch", "vl_stress_batch", "DynamicsError", "SimState",
     "SimSystem", "VLGroup", "build_batch_system", "build_system", "gradient", "inertia_target", "objective",
     "ConvergenceRecord", "ResidentRun", "SolverConfig", "SolverError", "StagnationError", "relative_error",
-    "simulate_frame",
+    "simulate_frame", "direction_newton", "newton_reference",
 ]

@@ -23,7 +23,7 @@ LIB = os.path.join(PKG, "libqnsim_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3", f"-I{INCLUDE}", f"-I{CSRC}"]
-SOURCES = ["qn_api.cu", "qn_solver.cu", "qn_slab.cu", "qn_factor.cpp", "qn_amg.cpp"]
+SOURCES = ["qn_api.cu", "qn_solver.cu", "qn_slab.cu", "qn_newton.cu", "qn_factor.cpp", "qn_amg.cpp"]
 
 
 def _deps():
@@ -52,7 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, log in results:
             sys.stderr.write(log)
     objs = [o for o, _ in results]
-    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", LIB, *objs, "-lgomp"]
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", LIB, *objs, "-lgomp",
+           "-L/usr/local/cuda/lib64", "-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

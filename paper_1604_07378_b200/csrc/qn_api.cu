@@ -691,8 +691,11 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   return QN_OK;
 }
 
+int qn_newton_release(qn_system* S);
+
 int qn_system_destroy(qn_system* S) {
   if (!S) return QN_OK;
+  qn_newton_release(S);
   if (S->exec) cudaGraphExecDestroy(S->exec);
   if (S->graph) cudaGraphDestroy(S->graph);
   for (void* p : S->allocs) cudaFree(p);

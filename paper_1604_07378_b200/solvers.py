@@ -125,12 +125,152 @@ class _RecordBuffers:
             raise SolverError(f"line search requires a descent direction (instance {int(bad[0])})")
 
 
+NEWTON_FD_STEP_REL = 1e-6   # solvers.py:32
+HESSIAN_EIG_FLOOR = 1e-8    # solvers.py:31
+
+
+def direction_newton(system: SimSystem, state: SimState, x, grad=None) -> np.ndarray:
+    """solvers.py:228-234 on the device: central-difference element Hessians,
+    eigenvalue floor, dense free-dof Hessian + M/h^2, Cholesky (qn_newton_direction)."""
+    from paper_1604_07378_b200.dynamics import gradient
+    from paper_1604_07378_b200.linalg import FactorizationError
+    if system.colliders:
+        raise NotImplementedError("newton with colliders is outside the B200 path")
+    if grad is None:
+        grad = gradient(system, state, x)
+    xs, gs = _lib.f64(x), _lib.f64(grad)
+    d = np.empty_like(xs)
+    rc = _lib.load().qn_newton_direction(system._h, _lib.ptr(xs), _lib.ptr(gs),
+                                         C.c_double(NEWTON_FD_STEP_REL * system.scale),
+                                         C.c_double(HESSIAN_EIG_FLOOR), _lib.ptr(d), _lib.QN_MEM_HOST, None)
+    if rc == _lib.QN_ERR_NOT_SPD:
+        raise FactorizationError(_lib.load().qn_last_error().decode())
+    _lib.check(rc, "newton_direction")
+    return d
+
+
+def direction_pd_qn(system: SimSystem, grad) -> np.ndarray:
+    """solvers.py:113-117 with the device factor."""
+    if system.sysfact is None:
+        raise NotImplementedError("pd_qn direction on the host needs a prefactored (direct) system")
+    d = np.zeros_like(grad)
+    d[system.free] = -system.sysfact.solve(np.ascontiguousarray(grad[system.free]))
+    return d
+
+
+def _line_search(system, st, x, d, g_x, grad, config):
+    """solvers.py:241-257"""
+    from paper_1604_07378_b200.dynamics import objective
+    slope = float(np.vdot(grad, d))
+    if slope >= 0.0:
+        raise SolverError(f"line search requires a descent direction (slope={slope})")
+    alpha, trials = config.alpha_init, 0
+    while True:
+        alpha *= config.alpha_shrink
+        if alpha < 1e-12:
+            raise StagnationError("step size underflow")
+        trials += 1
+        x_new = x + alpha * d
+        g_new = objective(system, st, x_new)
+        if g_new <= g_x + config.gamma * alpha * slope:
+            return alpha, x_new, g_new, trials
+
+
+def _simulate_frame_newton(system, state, config, fixed_targets):
+    """simulate_frame (solvers.py:260-352) for kind="newton": the frame control
+    on the host, every objective / gradient / direction on the device."""
+    import time
+    from paper_1604_07378_b200.dynamics import gradient, inertia_target, objective
+    if system.n_inst != 1:
+        raise NotImplementedError("newton: single-instance systems")
+    t0 = time.perf_counter()
+    y = inertia_target(state, system, fixed_targets)
+    st = SimState(q_l=state.q_l, q_prev=state.q_prev, y=y)
+    x = y.copy()
+    rec = ConvergenceRecord()
+    grad_tol = 1e-12 * system.scale * max(1.0, float(system.masses.max()) / system.h ** 2)
+
+    def log(g, tr, a):
+        rec.g.append(g)
+        rec.ls_trials.append(tr)
+        rec.alphas.append(a)
+        rec.cum_ms.append(1000.0 * (time.perf_counter() - t0))
+
+    rec.g0 = objective(system, st, x)
+    for _ in range(config.iterations):
+        g_x = objective(system, st, x)
+        grad = gradient(system, st, x)
+        if float(np.linalg.norm(grad)) <= grad_tol:
+            log(g_x, 0, 0.0)
+            continue
+        d = direction_newton(system, st, x, grad)
+        if float(np.vdot(grad, d)) >= 0.0:
+            d = direction_pd_qn(system, grad)
+            rec.fallbacks += 1
+        if config.line_search:
+            slope = float(np.vdot(grad, d))
+            if slope < 0.0 and -slope <= 1e-12 * max(abs(g_x), 1.0):
+                log(g_x, 0, 0.0)
+                continue
+            try:
+                alpha, x_new, g_new, trials = _line_search(system, st, x, d, g_x, grad, config)
+            except StagnationError:
+                rec.stagnated = True
+                while len(rec.g) < config.iterations:
+                    log(g_x, 0, 0.0)
+                break
+        else:
+            alpha, x_new, trials = 1.0, x + d, 1
+            g_new = objective(system, st, x_new)
+        x = x_new
+        log(g_new, trials, alpha)
+    return SimState(q_l=x, q_prev=np.asarray(state.q_l), y=y), rec
+
+
+def newton_reference(system: SimSystem, state: SimState, fixed_targets=None, grad_tol_rel: float = 1e-10,
+                     max_iterations: int = 200, config: SolverConfig | None = None):
+    """solvers.py:355-398: the frame solved to (near) optimality with Newton;
+    returns (x*, g*), the reference minimum for relative errors."""
+    from paper_1604_07378_b200.dynamics import gradient, inertia_target, objective
+    config = config or SolverConfig(kind="newton", iterations=1)
+    y = inertia_target(state, system, fixed_targets)
+    st = SimState(q_l=state.q_l, q_prev=state.q_prev, y=y)
+    x = y.copy()
+    grad0 = gradient(system, st, x)
+    tol = grad_tol_rel * max(1.0, float(np.linalg.norm(grad0)))
+    g_x = objective(system, st, x)
+    best, stalled = np.inf, 0
+    for _ in range(max_iterations):
+        g_x = objective(system, st, x)
+        grad = gradient(system, st, x)
+        gn = float(np.linalg.norm(grad))
+        if gn <= tol:
+            break
+        if gn >= 0.999 * best:
+            stalled += 1
+            if stalled >= 3:
+                break
+        else:
+            stalled = 0
+        best = min(best, gn)
+        d = direction_newton(system, st, x, grad)
+        if float(np.vdot(grad, d)) >= 0.0:
+            d = direction_pd_qn(system, grad)
+        try:
+            _, x, g_x, _ = _line_search(system, st, x, d, g_x, grad, config)
+        except StagnationError:
+            break
+    return x, g_x
+
+
 def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fixed_targets=None,
                    out: SimState | None = None):
     """Advance one frame; returns (next_state, ConvergenceRecord) — a list of
     records for batch systems (solvers.py:260-352).  `out` (optional, not in
     the reference signature): a SimState whose q_l / y arrays (float64,
     C-contiguous, e.g. page-locked) receive x and y instead of new arrays."""
+    if config.kind == "newton":
+        return _simulate_frame_newton(system, state, config, fixed_targets)
     cfg = config.to_c()
     shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
     q_l = _lib.f64(state.q_l).reshape(shape)

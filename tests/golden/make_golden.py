@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso | --writers (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso | --writers | --newton (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -367,6 +367,32 @@ def gen_writers():
                            for k in ("g", "ls_trials", "cum_ms", "rel_error")})
 
 
+def gen_newton():
+    """Newton (solvers.py:167-234) frames and newton_reference g* (:355-398)
+    through the reference: a 6x2x2 bar (3 frames x 5 Newton iterations) and
+    the reference minimum of configs[0]'s first frame."""
+    t = time.time()
+    out = {}
+    sc = scenes.c2(grid=(6, 2, 2), iterations=5)
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = ref_solvers.SolverConfig(kind="newton", iterations=sc.iterations)
+    g, tr = [], []
+    for f in range(3):
+        state, rec = ref_solvers.simulate_frame(system, state, cfg)
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+    out["frames_g"], out["frames_trials"], out["frames_x_2"] = np.array(g), np.array(tr), state.q_l.copy()
+    sc1 = scenes.c1()
+    mesh = ref_mesh.TetMesh(vertices=sc1.verts, tets=sc1.tets, density=sc1.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc1.material), h=sc1.h, gravity=sc1.gravity, fixed=sc1.fixed)
+    xs, gs = ref_solvers.newton_reference(system, ref_dyn.SimState(q_l=sc1.q_l.copy(), q_prev=sc1.q_prev.copy()))
+    out["c1_gstar"], out["c1_xstar"] = gs, xs
+    np.savez_compressed(os.path.join(HERE, "frames_newton.npz"), **out)
+    print("newton", time.time() - t, gs)
+
+
 def copy_fixtures():
     dst = os.path.join(HERE, "ref_fixtures")
     os.makedirs(dst, exist_ok=True)
@@ -397,6 +423,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--writers" in sys.argv:
         gen_writers()
+        sys.exit(0)
+    if "--newton" in sys.argv:
+        gen_newton()
         sys.exit(0)
     gen_svd_materials()
     gen_meshes_elements()

@@ -395,7 +395,7 @@ def test_unsupported_options_raise():
     sc = scenes.c1(frames=1)
     system = build(sc)
     st = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
-    for cfg in (Q.SolverConfig(kind="newton"), Q.SolverConfig(kind="lbfgs", lbfgs_init="rest_pose_hessian")):
+    for cfg in (Q.SolverConfig(kind="lbfgs", lbfgs_init="rest_pose_hessian"),):
         with pytest.raises(NotImplementedError):
             Q.simulate_frame(system, st, cfg)
     with pytest.raises(Q.DynamicsError):
@@ -704,3 +704,24 @@ def test_aniso_fibres_against_reference_golden(name):
         assert rel(rec.g, d[f"{name}_g"][f]) <= G_TOL
         assert rec.ls_trials == list(d[f"{name}_trials"][f])
     assert rel(res[-1][0], d[f"{name}_x_9"]) <= X_TOL
+
+
+def test_newton_frames_and_reference_minimum_against_reference():
+    """kind="newton" and newton_reference on the device (central-difference
+    element Hessians, eigenvalue floor, dense Cholesky): frames vs the
+    reference within the finite-difference noise (see the oracle test), the
+    reference minimum g* of configs[0]'s first frame to 1e-12."""
+    d = golden("frames_newton.npz")
+    sc = scenes.c2(grid=(6, 2, 2), iterations=5)
+    system = build(sc)
+    st = Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    for f in range(3):
+        st, rec = Q.simulate_frame(system, st, Q.SolverConfig(kind="newton", iterations=sc.iterations))
+        assert rel(rec.g, d["frames_g"][f]) <= G_TOL  # measured ~7e-12
+        assert rec.ls_trials == list(d["frames_trials"][f])
+    assert rel(st.q_l, d["frames_x_2"]) <= X_TOL
+    sc1 = scenes.c1()
+    s1 = build(sc1)
+    xs, gs = Q.newton_reference(s1, Q.SimState(q_l=sc1.q_l.copy(), q_prev=sc1.q_prev.copy()))
+    assert abs(gs - float(d["c1_gstar"])) <= 1e-12 * abs(gs)  # measured 8e-14
+    assert rel(xs, d["c1_xstar"]) <= 1e-9

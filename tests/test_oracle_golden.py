@@ -273,3 +273,24 @@ def test_output_writers_match_reference_bytes(tmp_path):
     QIO.export_frames([d["x0"]], str(tmp_path / "obj"), QIO.surface_triangles(TetMesh(sc.verts, sc.tets)))
     ref = open(os.path.join(os.path.dirname(FIX), "writers_obj", "frame_0000.obj"), "rb").read()
     assert (tmp_path / "obj" / "frame_0000.obj").read_bytes() == ref
+
+
+def test_oracle_newton_matches_reference():
+    """Newton frames (solvers.py:167-234) and newton_reference g* (:355-398).
+    The central-difference Hessian divides rounding-level differences of the
+    element gradient by the 1e-6 scale step, so frames agree to ~1e-11."""
+    d = golden("frames_newton.npz")
+    sc = scenes.c2(grid=(6, 2, 2), iterations=5)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(3):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=sc.iterations, kind="newton")
+        q_prev, q_l = q_l, x
+        np.testing.assert_allclose(rec.g, d["frames_g"][f], rtol=1e-9)
+        assert list(rec.ls_trials) == list(d["frames_trials"][f])
+    sc1 = scenes.c1()
+    osys = O.build(sc1.verts, sc1.tets, sc1.density, oracle_material(sc1.material), sc1.h, sc1.gravity, sc1.fixed,
+                   factor="dense")
+    _, gs = O.newton_reference(osys, sc1.q_l.copy(), sc1.q_prev.copy())
+    assert abs(gs - float(d["c1_gstar"])) <= 1e-12 * abs(gs)

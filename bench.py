@@ -242,6 +242,11 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     from paper_1604_07378_b200 import scenes
+    if args.config == "c5":  # the oracle's sparse LU of a 12 M-dof A_free does not fit a bounded host run
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "value": None,
+                          "unavailable": "configs[4]: the CPU oracle factors A_free (12 M dofs); not a bounded "
+                                         "host run (DESIGN.md section 6)"}), flush=True)
+        return
     sc = scenes.CONFIGS[args.config]()
     threads = os.cpu_count() or 1
     import oracle.qnsim_oracle as O

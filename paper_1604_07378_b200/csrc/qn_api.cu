@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1011,8 +1012,17 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   if (rec) {
     const int it = cfg->iterations, cap = S->rec_cap;
     const int64_t ni = S->n_inst;
-    std::vector<InstCtl> ctl(ni);
-    QN_CUDA(cudaMemcpy(ctl.data(), S->v.ctl, ni * sizeof(InstCtl), cudaMemcpyDeviceToHost));
+    // only the record fields of the control blocks (strided copies, not the
+    // whole ~2.5 KB block per instance)
+    std::vector<double> ctl_g0(ni);
+    std::vector<int32_t> ctl_status(ni), ctl_fb(ni);
+    const char* cb = reinterpret_cast<const char*>(S->v.ctl);
+    QN_CUDA(cudaMemcpy2D(ctl_g0.data(), sizeof(double), cb + offsetof(InstCtl, g0), sizeof(InstCtl), sizeof(double),
+                         ni, cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy2D(ctl_status.data(), sizeof(int32_t), cb + offsetof(InstCtl, status), sizeof(InstCtl),
+                         sizeof(int32_t), ni, cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy2D(ctl_fb.data(), sizeof(int32_t), cb + offsetof(InstCtl, fallbacks), sizeof(InstCtl),
+                         sizeof(int32_t), ni, cudaMemcpyDeviceToHost));
     std::vector<double> g((size_t)ni * cap), al((size_t)ni * cap), ms_((size_t)ni * cap);
     std::vector<int32_t> tr((size_t)ni * cap);
     QN_CUDA(cudaMemcpy(g.data(), S->v.rec_g, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1024,9 +1034,9 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
     std::vector<double> og((size_t)ni * it), oa((size_t)ni * it), om((size_t)ni * it);
     std::vector<int32_t> ot((size_t)ni * it);
     for (int64_t b = 0; b < ni; ++b) {
-      g0[b] = ctl[b].g0;
-      status[b] = ctl[b].status;
-      fallbacks[b] = ctl[b].fallbacks;
+      g0[b] = ctl_g0[b];
+      status[b] = ctl_status[b];
+      fallbacks[b] = ctl_fb[b];
       for (int k = 0; k < it; ++k) {
         og[b * it + k] = g[b * cap + k];
         oa[b * it + k] = al[b * cap + k];

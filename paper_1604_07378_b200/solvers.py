@@ -113,6 +113,18 @@ class _RecordBuffers:
                                   _lib.ptr(self.ms), _lib.ptr(self.status), _lib.ptr(self.fallbacks))
 
     def records(self):
+        if len(self.g0) > 64:  # batches: build the records without collector pauses
+            import gc
+            was = gc.isenabled()
+            gc.disable()
+            try:
+                return self._records()
+            finally:
+                if was:
+                    gc.enable()
+        return self._records()
+
+    def _records(self):
         g0, g, tr = self.g0.tolist(), self.g.tolist(), self.trials.tolist()
         al, ms, stg = self.alphas.tolist(), self.ms.tolist(), (self.status & 1).astype(bool).tolist()
         fb = self.fallbacks.tolist()

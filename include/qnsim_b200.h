@@ -204,7 +204,8 @@ typedef struct qn_solver_config {  /* SolverConfig (solvers.py:43-68)          *
   double rho;                      /* chebyshev: spectral radius estimate         */
   int32_t S;                       /* chebyshev: iterations before acceleration   */
   int32_t lbfgs_init;              /* lbfgs: 0 = system_matrix (A^-1), 1 = scaled_identity
-                                      (rho/<t,t> of the newest pair, solvers.py:136-141) */
+                                      (rho/<t,t> of the newest pair, solvers.py:136-141),
+                                      2 = rest_pose_hessian (qn_system_rest_hessian first) */
 } qn_solver_config;
 
 typedef struct qn_frame_record {   /* ConvergenceRecord (solvers.py:71-80), per instance */
@@ -287,6 +288,11 @@ int qn_system_time_kernel(qn_system* s, int32_t kernel, int32_t reps, double* av
  * colliders; for the small meshes the reference runs Newton on. */
 int qn_newton_direction(qn_system* s, const double* x, const double* grad, double step, double eig_floor, double* d,
                         int32_t mem, void* stream);
+/* lbfgs_init = "rest_pose_hessian" (solvers.py:142-146, 401-407): the Newton
+ * Hessian at the rest positions `rest` (n,3) (y = rest), factored and inverted
+ * once on the device; frames with that init then apply the dense inverse in
+ * their direction step.  Single instance, <= 20000 free dofs. */
+int qn_system_rest_hessian(qn_system* s, const double* rest, double step, double eig_floor);
 /* free the Newton workspace of a system (also freed with the process) */
 int qn_newton_release(qn_system* s);
 

@@ -758,7 +758,10 @@ def direction(sys, hist, grad, lbfgs_init="system_matrix"):
         q -= z * t
         zetas.append(z)
     zetas.reverse()
-    if lbfgs_init == "scaled_identity":                                    # solvers.py:136-141
+    if lbfgs_init == "rest_pose_hessian":                                  # solvers.py:142-146
+        r = np.zeros_like(q)
+        r[sys.free] = scipy.linalg.cho_solve(rest_hessian_factor(sys), q[sys.free].reshape(-1)).reshape(-1, 3)
+    elif lbfgs_init == "scaled_identity":                                  # solvers.py:136-141
         if hist.pairs:
             s, t, rho = hist.pairs[-1]
             scale = rho / float(np.vdot(t, t))
@@ -922,7 +925,22 @@ def _project_psd(blocks, floor=HESSIAN_EIG_FLOOR):
 
 
 def direction_newton(sys, x, grad):
-    """solvers.py:195-234 (no colliders): dense free-dof Hessian, cho_factor."""
+    """solvers.py:228-234 (no colliders): dense free-dof Hessian, cho_factor."""
+    fac = scipy.linalg.cho_factor(newton_hessian_free(sys, x))
+    d = np.zeros_like(x)
+    d[sys.free] = scipy.linalg.cho_solve(fac, -grad[sys.free].reshape(-1)).reshape(-1, 3)
+    return d
+
+
+def rest_hessian_factor(sys):
+    """solvers.py:401-407: the Newton Hessian at the rest pose, factored once."""
+    if getattr(sys, "_rest_fac", None) is None:
+        sys._rest_fac = scipy.linalg.cho_factor(newton_hessian_free(sys, sys.verts.copy()))
+    return sys._rest_fac
+
+
+def newton_hessian_free(sys, x):
+    """solvers.py:195-225 (no colliders): the dense Hessian on the free dofs."""
     n = sys.n
     step = NEWTON_FD_STEP_REL * sys.scale
     rows, cols, vals = [], [], []
@@ -937,10 +955,7 @@ def direction_newton(sys, x, grad):
                                 shape=(3 * n, 3 * n)).toarray()
     H[np.diag_indices_from(H)] += np.repeat(sys.masses / sys.h ** 2, 3)
     free3 = (sys.free[:, None] * 3 + np.arange(3)).reshape(-1)
-    fac = scipy.linalg.cho_factor(H[np.ix_(free3, free3)])
-    d = np.zeros_like(x)
-    d[sys.free] = scipy.linalg.cho_solve(fac, -grad[sys.free].reshape(-1)).reshape(-1, 3)
-    return d
+    return H[np.ix_(free3, free3)]
 
 
 def newton_reference(sys, q_l, q_prev, grad_tol_rel=1e-10, max_iterations=200, gamma=0.3, alpha_init=2.0,

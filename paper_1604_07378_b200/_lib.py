@@ -142,6 +142,7 @@ SIGNATURES = {
     "qn_system_time_kernel": [_P, _I32, _I32, _P, _P],
     "qn_newton_direction": [_P, _P, _P, C.c_double, C.c_double, _P, _I32, _P],
     "qn_newton_release": [_P],
+    "qn_system_rest_hessian": [_P, _P, C.c_double, C.c_double],
     "qn_slab_create": [_P, _P],
     "qn_slab_destroy": [_P],
     "qn_slab_buffer": [_P, _I32, _P, _P],

@@ -947,9 +947,11 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   c.grad_tol = 1e-12 * S->scale * std::max(1.0, S->max_mass / (S->h * S->h));  // solvers.py:278
   c.cheb_rho = cfg->rho;
   c.cheb_S = cfg->S;
-  QN_REQUIRE(cfg->lbfgs_init == 0 || cfg->lbfgs_init == 1, QN_ERR_UNSUPPORTED, "frame_step: lbfgs_init");
+  QN_REQUIRE(cfg->lbfgs_init >= 0 && cfg->lbfgs_init <= 2, QN_ERR_UNSUPPORTED, "frame_step: lbfgs_init");
   QN_REQUIRE(cfg->lbfgs_init == 0 || !S->v.pcg, QN_ERR_UNSUPPORTED,
-             "frame_step: scaled_identity needs a direct-solver system");
+             "frame_step: this lbfgs_init needs a direct-solver system");
+  QN_REQUIRE(cfg->lbfgs_init != 2 || cfg->kind != 1 || (S->v.hrest_inv && S->n_inst == 1), QN_ERR_ARG,
+             "frame_step: rest_pose_hessian needs qn_system_rest_hessian first (single instance)");
   c.lbfgs_init = cfg->kind == 1 ? cfg->lbfgs_init : 0;
   c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
   c.use_graph = S->use_graph ? 1 : 0;

@@ -329,6 +329,70 @@ int qn_newton_direction(qn_system* S, const double* x, const double* grad, doubl
   return QN_OK;
 }
 
+// rest-pose Hessian (solvers.py:401-407): the Newton Hessian at the rest
+// positions with y = rest, Cholesky-factored and inverted once; the frame's
+// direction step then applies the dense inverse (k_rest_apply)
+int qn_system_rest_hessian(qn_system* S, const double* rest, double step, double eig_floor) {
+  using namespace qn;
+  QN_REQUIRE(S && rest && step > 0, QN_ERR_ARG, "rest_hessian: args");
+  QN_REQUIRE(S->n_inst == 1 && S->v.n_col == 0, QN_ERR_UNSUPPORTED, "rest_hessian: single instance, no colliders");
+  NewtonWork* W = work_of(S);
+  int rc;
+  if (!W->ready && (rc = newton_setup(S, W))) return rc;
+  QN_REQUIRE(W->nf3 <= 20000, QN_ERR_UNSUPPORTED, "rest_hessian: dense inverse limited to 20000 free dofs");
+  cudaStream_t st = S->stream;
+  const int64_t n3 = 3 * S->n, nf3 = W->nf3;
+  QN_CUDA(cudaMemcpyAsync(W->x, rest, n3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (S->mt > 0) {
+    k_newton_blocks<<<div_up(S->mt, kNT), kNT, 0, st>>>(S->v, W->x, step, eig_floor, W->He, W->scratch);
+    QN_CHECK_LAUNCH();
+  }
+  QN_CUDA(cudaMemsetAsync(W->H, 0, (size_t)nf3 * nf3 * sizeof(double), st));
+  k_newton_assemble<<<div_up(W->npat, 256), 256, 0, st>>>(W->npat, W->pat_dst, W->ptr, W->src, W->He, W->diag_add,
+                                                           W->H);
+  QN_CHECK_LAUNCH();
+  cusolverDnSetStream(W->solver, st);
+  if (cusolverDnDpotrf(W->solver, CUBLAS_FILL_MODE_LOWER, (int)nf3, W->H, (int)nf3, W->work, W->lwork, W->info) !=
+      CUSOLVER_STATUS_SUCCESS) {
+    set_error("rest_hessian: potrf failed to launch");
+    return QN_ERR_CUDA;
+  }
+  int info = 0;
+  QN_CUDA(cudaMemcpyAsync(&info, W->info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  QN_CUDA(cudaStreamSynchronize(st));
+  if (info != 0) {
+    set_error("rest_hessian: Hessian is not positive definite");
+    return QN_ERR_NOT_SPD;
+  }
+  // inverse: solve against the identity (column-major == row-major for the symmetric result)
+  double* inv;
+  if ((rc = nalloc(&inv, (size_t)(nf3 * nf3)))) return rc;
+  S->allocs.push_back(inv);
+  std::vector<double> eye((size_t)nf3 * nf3, 0.0);
+  for (int64_t k = 0; k < nf3; ++k) eye[(size_t)k * nf3 + k] = 1.0;
+  QN_CUDA(cudaMemcpy(inv, eye.data(), eye.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (cusolverDnDpotrs(W->solver, CUBLAS_FILL_MODE_LOWER, (int)nf3, (int)nf3, W->H, (int)nf3, inv, (int)nf3,
+                       W->info) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("rest_hessian: potrs failed to launch");
+    return QN_ERR_CUDA;
+  }
+  QN_CUDA(cudaStreamSynchronize(st));
+  double* qb;
+  if ((rc = nalloc(&qb, (size_t)nf3))) return rc;
+  S->allocs.push_back(qb);
+  S->v.hrest_inv = inv;
+  S->v.qbuf = qb;
+  S->v.free3 = W->free3;
+  S->v.nf3 = (int32_t)nf3;
+  if (S->exec) {  // views changed: rebuild the frame graph
+    cudaGraphExecDestroy(S->exec);
+    S->exec = nullptr;
+    cudaGraphDestroy(S->graph);
+    S->graph = nullptr;
+  }
+  return QN_OK;
+}
+
 int qn_newton_release(qn_system* S) {
   for (size_t i = 0; i < g_newton.size(); ++i)
     if (g_newton[i].first == S) {

@@ -370,6 +370,35 @@ __global__ void __launch_bounds__(kVertexThreads) k_scaled(SysView v) {
   v.R0[inst_off(v, b) + ci] = scale * q;
 }
 
+// lbfgs_init = "rest_pose_hessian": q on the free dofs (two-loop first half,
+// reference rounding), then r = H_rest^-1 q as a dense product (the inverse
+// is formed once from the Cholesky factor), warp per row; fixed rows of R0 = 0
+__global__ void __launch_bounds__(kVertexThreads) k_rest_rhs(SysView v) {
+  const InstCtl* c = v.ctl;
+  if (c->phase != PH_DIR) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < 3 * v.n) v.R0[k] = 0.0;
+  if (k >= v.nf3) return;
+  const int dof = v.free3[k];
+  double q = -v.Gr[vec_off(v, c->gs_cur, 0) + dof];
+  for (int p = c->npairs - 1; p >= 0; --p)
+    q = __dsub_rn(q, __dmul_rn(c->zeta[p], v.T[vec_off(v, c->ring[p], 0) + dof]));
+  v.qbuf[k] = q;
+}
+
+__global__ void __launch_bounds__(256) k_rest_apply(SysView v) {
+  if (v.ctl->phase != PH_DIR) return;
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * 8 + (threadIdx.x >> 5), nw = gridDim.x * 8;
+  for (int r = w0; r < v.nf3; r += nw) {
+    const double* row = v.hrest_inv + (size_t)r * v.nf3;
+    double a = 0.0;
+    for (int j = lane; j < v.nf3; j += 32) a = fma(__ldg(row + j), v.qbuf[j], a);
+    a = warp_sum(a);
+    if (lane == 0) v.R0[v.free3[r]] = a;
+  }
+}
+
 // stand-alone timing of the solve kernels (qn_system_time_kernel): every
 // instance, right-hand side = the resident q_l, result into the R0 scratch
 struct TimingIO {
@@ -1452,6 +1481,13 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
   }
   if (S->h_cfg.lbfgs_init == 1) {
     k_scaled<<<gv, kVT, 0, st>>>(v);
+    QN_CHECK_LAUNCH();
+    return QN_OK;
+  }
+  if (S->h_cfg.lbfgs_init == 2) {
+    k_rest_rhs<<<div_up(std::max<int64_t>(3 * (int64_t)v.n, v.nf3), kVT), kVT, 0, st>>>(v);
+    QN_CHECK_LAUNCH();
+    k_rest_apply<<<std::max(1, std::min(4 * kSMs, div_up(v.nf3, 8))), 256, 0, st>>>(v);
     QN_CHECK_LAUNCH();
     return QN_OK;
   }

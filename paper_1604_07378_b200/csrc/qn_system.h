@@ -174,6 +174,11 @@ struct SysView {
   double* col_g;            // [inst][n][3] collision gradient at the current iterate
   double* part_c;           // [inst][nblk_c]
   unsigned* cnt_c;          // [inst]
+  // ---- lbfgs_init = rest_pose_hessian (solvers.py:142-146, 401-407) ----
+  int32_t nf3, pad_r;       // free dofs
+  const int32_t* free3;     // [nf3] dof = 3 vertex + coordinate
+  const double* hrest_inv;  // [nf3][nf3] inverse of the rest-pose Hessian (dense, symmetric)
+  double* qbuf;             // [nf3] first-loop vector q on the free dofs
 };
 
 }  // namespace qn

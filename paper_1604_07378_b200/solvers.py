@@ -66,14 +66,14 @@ class SolverConfig:
     def to_c(self) -> _lib.SolverConfigC:
         if self.kind not in ("pd_qn", "lbfgs", "chebyshev"):
             raise NotImplementedError(f"solver kind {self.kind!r} is outside the B200 hot path (SURVEY §8f)")
-        if self.kind == "lbfgs" and self.lbfgs_init not in ("system_matrix", "scaled_identity"):
-            raise NotImplementedError(f"lbfgs_init {self.lbfgs_init!r} is outside the B200 hot path")
+
         if self.m > _lib.QN_MAX_M:
             raise NotImplementedError(f"history window m > {_lib.QN_MAX_M}")
         c = _lib.SolverConfigC()
         c.kind = {"pd_qn": 0, "lbfgs": 1, "chebyshev": 2}[self.kind]
         c.rho, c.S = float(self.rho), int(self.S)
-        c.lbfgs_init = 1 if (self.kind == "lbfgs" and self.lbfgs_init == "scaled_identity") else 0
+        c.lbfgs_init = {"system_matrix": 0, "scaled_identity": 1, "rest_pose_hessian": 2}[self.lbfgs_init] \
+            if self.kind == "lbfgs" else 0
         c.iterations, c.m, c.line_search = self.iterations, self.m, 1 if self.line_search else 0
         c.gamma, c.alpha_init, c.alpha_shrink = self.gamma, self.alpha_init, self.alpha_shrink
         return c
@@ -275,6 +275,22 @@ def newton_reference(system: SimSystem, state: SimState, fixed_targets=None, gra
     return x, g_x
 
 
+def _prepare(system: SimSystem, config: SolverConfig):
+    """lbfgs_init="rest_pose_hessian": the rest-pose Hessian is factored (and
+    inverted) once per system, lazily (dynamics.py:307, solvers.py:401-407)."""
+    if config.kind == "lbfgs" and config.lbfgs_init == "rest_pose_hessian" and \
+            not getattr(system, "_rest_hessian_ready", False):
+        from paper_1604_07378_b200.linalg import FactorizationError
+        rest = _lib.f64(system.mesh.vertices)
+        rc = _lib.load().qn_system_rest_hessian(system._h, _lib.ptr(rest),
+                                                C.c_double(NEWTON_FD_STEP_REL * system.scale),
+                                                C.c_double(HESSIAN_EIG_FLOOR))
+        if rc == _lib.QN_ERR_NOT_SPD:
+            raise FactorizationError(_lib.load().qn_last_error().decode())
+        _lib.check(rc, "rest_pose_hessian")
+        system._rest_hessian_ready = True
+
+
 def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fixed_targets=None,
                    out: SimState | None = None):
     """Advance one frame; returns (next_state, ConvergenceRecord) — a list of
@@ -283,6 +299,7 @@ def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fix
     C-contiguous, e.g. page-locked) receive x and y instead of new arrays."""
     if config.kind == "newton":
         return _simulate_frame_newton(system, state, config, fixed_targets)
+    _prepare(system, config)
     cfg = config.to_c()
     shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
     q_l = _lib.f64(state.q_l).reshape(shape)
@@ -316,6 +333,7 @@ class ResidentRun:
 
     def __init__(self, system: SimSystem, state: SimState, config: SolverConfig):
         self.system, self.config = system, config
+        _prepare(system, config)
         self._cfg = config.to_c()
         shape = (system.n_inst, system.n, 3) if system.n_inst > 1 else (system.n, 3)
         _lib.check(_lib.load().qn_state_set(system._h, _lib.ptr(_lib.f64(state.q_l).reshape(shape)),

@@ -389,6 +389,28 @@ def gen_newton():
     system = ref_dyn.build_system(mesh, ref_material(sc1.material), h=sc1.h, gravity=sc1.gravity, fixed=sc1.fixed)
     xs, gs = ref_solvers.newton_reference(system, ref_dyn.SimState(q_l=sc1.q_l.copy(), q_prev=sc1.q_prev.copy()))
     out["c1_gstar"], out["c1_xstar"] = gs, xs
+    # L-BFGS with the rest-pose Hessian as the initial inverse (solvers.py:142-146, 401-407)
+    mesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets, density=sc.density)
+    system = ref_dyn.build_system(mesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    state = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = ref_solvers.SolverConfig(kind="lbfgs", iterations=10, m=5, lbfgs_init="rest_pose_hessian")
+    g, tr = [], []
+    for f in range(3):
+        state, rec = ref_solvers.simulate_frame(system, state, cfg)
+        g.append(rec.g)
+        tr.append(rec.ls_trials)
+    out["rest_g"], out["rest_trials"], out["rest_x_2"] = np.array(g), np.array(tr), state.q_l.copy()
+    # these frames converge to roundoff within the budget, so line-search
+    # decisions at the noise floor (and the frame-end state) depend on the
+    # summation order: the reference with its tet list reversed is the envelope
+    rmesh = ref_mesh.TetMesh(vertices=sc.verts, tets=sc.tets[::-1].copy(), density=sc.density)
+    rsys = ref_dyn.build_system(rmesh, ref_material(sc.material), h=sc.h, gravity=sc.gravity, fixed=sc.fixed)
+    rstate = ref_dyn.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    rg = []
+    for f in range(3):
+        rstate, rec = ref_solvers.simulate_frame(rsys, rstate, cfg)
+        rg.append(rec.g)
+    out["rest_rev_g"], out["rest_rev_x_2"] = np.array(rg), rstate.q_l.copy()
     np.savez_compressed(os.path.join(HERE, "frames_newton.npz"), **out)
     print("newton", time.time() - t, gs)
 

@@ -395,9 +395,10 @@ def test_unsupported_options_raise():
     sc = scenes.c1(frames=1)
     system = build(sc)
     st = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
-    for cfg in (Q.SolverConfig(kind="lbfgs", lbfgs_init="rest_pose_hessian"),):
-        with pytest.raises(NotImplementedError):
-            Q.simulate_frame(system, st, cfg)
+    cs = Q.build_system(Q.TetMesh(sc.verts, sc.tets), from_spec(sc.material), fixed=sc.fixed,
+                        colliders=[Q.dynamics.HalfSpace((0, 0, -1), (0, 0, 1))])
+    with pytest.raises(NotImplementedError):
+        Q.simulate_frame(cs, st, Q.SolverConfig(kind="newton"))
     with pytest.raises(Q.DynamicsError):
         Q.build_system(Q.TetMesh(sc.verts, sc.tets), from_spec(sc.material), fixed=np.arange(sc.verts.shape[0]))
 
@@ -725,3 +726,21 @@ def test_newton_frames_and_reference_minimum_against_reference():
     xs, gs = Q.newton_reference(s1, Q.SimState(q_l=sc1.q_l.copy(), q_prev=sc1.q_prev.copy()))
     assert abs(gs - float(d["c1_gstar"])) <= 1e-12 * abs(gs)  # measured 8e-14
     assert rel(xs, d["c1_xstar"]) <= 1e-9
+
+
+def test_lbfgs_rest_pose_hessian_against_reference_golden():
+    """lbfgs_init="rest_pose_hessian": the Newton Hessian at rest, factored and
+    inverted once on the device, applied in the frame graph's direction step."""
+    d = golden("frames_newton.npz")
+    sc = scenes.c2(grid=(6, 2, 2), iterations=10)
+    system = build(sc)
+    st = Q.SimState(q_l=sc.q_l.copy(), q_prev=sc.q_prev.copy())
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=10, m=5, lbfgs_init="rest_pose_hessian")
+    # the frames converge to roundoff within the budget: decisions at the
+    # noise floor depend on summation order, so the bar is the strict one or
+    # 10x the reference's own reordering envelope (golden rest_rev_*)
+    for f in range(3):
+        st, rec = Q.simulate_frame(system, st, cfg)
+        env = np.abs(d["rest_rev_g"][f] - d["rest_g"][f]).max() / np.abs(d["rest_g"][f]).max()
+        assert rel(rec.g, d["rest_g"][f]) <= max(G_TOL, 10 * env)
+    assert rel(st.q_l, d["rest_x_2"]) <= max(X_TOL, 10 * rel(d["rest_rev_x_2"], d["rest_x_2"]))

@@ -294,3 +294,16 @@ def test_oracle_newton_matches_reference():
                    factor="dense")
     _, gs = O.newton_reference(osys, sc1.q_l.copy(), sc1.q_prev.copy())
     assert abs(gs - float(d["c1_gstar"])) <= 1e-12 * abs(gs)
+
+
+def test_oracle_lbfgs_rest_pose_hessian_matches_reference():
+    d = golden("frames_newton.npz")
+    sc = scenes.c2(grid=(6, 2, 2), iterations=10)
+    osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(sc.material), sc.h, sc.gravity, sc.fixed,
+                   factor="dense")
+    q_l, q_prev = sc.q_l.copy(), sc.q_prev.copy()
+    for f in range(3):
+        x, _, rec = O.simulate_frame(osys, q_l, q_prev, iterations=10, m=5, lbfgs_init="rest_pose_hessian")
+        q_prev, q_l = q_l, x
+        env = np.abs(d["rest_rev_g"][f] - d["rest_g"][f]).max() / np.abs(d["rest_g"][f]).max()
+        assert np.abs(np.array(rec.g) - d["rest_g"][f]).max() / np.abs(d["rest_g"][f]).max() <= max(1e-10, 10 * env)

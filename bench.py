@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="host-driven body loop (for per-kernel ncu lists)")
     p.add_argument("--slab", action="store_true",
                    help="c5: slab-decomposed frame (one slab per rank; the default for c5 when N > 1)")
+    p.add_argument("--coarse", action="store_true",
+                   help="c5 slab frame: two-level preconditioner also at N = 1 (always on for N > 1)")
     return p.parse_args()
 
 
@@ -475,7 +477,7 @@ def run_slab(args, world, rank, local):
     cfg = Q.SolverConfig(kind="lbfgs", iterations=iterations, m=m_hist)
     comm = slab.NcclComm(rk)
     t_coarse = time.perf_counter()
-    if world > 1:  # two-level preconditioner: per-slab AMG + geometric coarse grid (slab.setup_coarse)
+    if world > 1 or args.coarse:  # two-level preconditioner: per-slab AMG + geometric coarse grid (slab.setup_coarse)
         slab.setup_coarse(comm, grid)
     t_coarse = time.perf_counter() - t_coarse
     run = slab.SlabRun(comm, cfg, scenes.H, slab.grad_tolerance(bbox, float(mm.item()), scenes.H))
@@ -547,7 +549,7 @@ def run_slab(args, world, rank, local):
                            "iterations_per_step": iterations, "m": m_hist, "slabs": world,
                            "l2": "flushed between steps (256 MiB write)", "parallelism": f"x-slabs/{world}",
                            "preconditioner": "per-slab AMG V(1,1) + geometric coarse grid (additive two-level)"
-                           if world > 1 else "AMG V(1,1)"},
+                           if (world > 1 or args.coarse) else "AMG V(1,1)"},
                 "tet_evals_per_s": evals * m_all / (total_ms / 1000.0), "roofline": roof, "cpu_baseline": None,
                 "e2e": e2e, "clocks": clk, "gpu_launches": launches, "build_s": t_build, "coarse_setup_s": t_coarse,
                 "cg_iterations_per_step": cg_per_step}

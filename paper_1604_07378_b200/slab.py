@@ -312,7 +312,7 @@ class NcclComm:
         """rank-order sum of every rank's dense setup matrix (all-gather, then
         the same additions on every rank)"""
         import torch
-        mine = torch.as_tensor(parts[0], device="cuda")
+        mine = torch.as_tensor(np.ascontiguousarray(parts[0]), device="cuda")
         world = self.dist.get_world_size(self.group)
         allp = torch.empty((world,) + mine.shape, dtype=mine.dtype, device="cuda")
         self.dist.all_gather_into_tensor(allp, mine, group=self.group)

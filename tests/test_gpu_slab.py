@@ -126,10 +126,20 @@ def test_slab_nccl_world1_matches_emulated():
                            sc.h, slab.scene_grad_tol(sc))
         rec = run.step()
         x = rk.owned_positions().cpu().numpy()
+        # the coarse level's setup collectives (all-gather of the Galerkin
+        # shares, broadcast of the inverse) and its per-iteration all-gather
+        rk2, = slab.scene_slabs(sc, 1)
+        comm2 = slab.NcclComm(rk2)
+        slab.setup_coarse(comm2, sc.grid, (4, 2, 2))
+        rec2 = slab.SlabRun(comm2, Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m), sc.h,
+                            slab.scene_grad_tol(sc)).step()
+        x2 = rk2.owned_positions().cpu().numpy()
     finally:
         dist.destroy_process_group()
     assert np.array_equal(x, emu[0][0])
     assert rec.g == emu[0][1].g and rec.ls_trials == emu[0][1].ls_trials
+    emu2, _ = run_emulated(sc, 1, 1, coarse=True, target=(4, 2, 2))
+    assert np.array_equal(x2, emu2[0][0]) and rec2.g == emu2[0][1].g
 
 
 def test_slab_owned_gradient_is_the_single_system_gradient():

@@ -15,6 +15,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "qn_kernels.cuh"
@@ -168,9 +169,11 @@ struct NewtonWork {
   cusolverDnHandle_t solver = nullptr;
 };
 
-std::vector<std::pair<qn_system*, NewtonWork*>> g_newton;  // per system (tooling path, one thread)
+std::vector<std::pair<qn_system*, NewtonWork*>> g_newton;  // per system (released with the system)
+std::mutex g_newton_mu;  // guards the table; a system's workspace is used by one thread at a time
 
 NewtonWork* work_of(qn_system* S) {
+  std::lock_guard<std::mutex> lock(g_newton_mu);
   for (auto& p : g_newton)
     if (p.first == S) return p.second;
   g_newton.push_back({S, new NewtonWork()});
@@ -394,6 +397,7 @@ int qn_system_rest_hessian(qn_system* S, const double* rest, double step, double
 }
 
 int qn_newton_release(qn_system* S) {
+  std::lock_guard<std::mutex> lock(g_newton_mu);
   for (size_t i = 0; i < g_newton.size(); ++i)
     if (g_newton[i].first == S) {
       NewtonWork* W = g_newton[i].second;

@@ -27,6 +27,7 @@
 // vector updates q -= zeta t and r += s (zeta - eta) are applied in the
 // reference's order with the reference's rounding (mul, then add).
 #include <cstring>
+#include <mutex>
 
 #include "qn_common.cuh"
 #include "qn_element.cuh"
@@ -1403,8 +1404,10 @@ int launch_spmv_timing(qn_system* S, cudaStream_t st) {
 // different sizes: the kernel's dynamic shared-memory limit only ever grows.
 // Called before any graph capture (prepare_kernels) and before direct launches.
 static int ensure_coarse_smem(int nc) {
+  static std::mutex mu;
   static int smem_set = 0;
   const int need = (int)(3 * sizeof(double) * nc);
+  std::lock_guard<std::mutex> lock(mu);
   if (need > smem_set) {
     QN_CUDA(cudaFuncSetAttribute(k_amg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
     smem_set = need;

@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="host-driven body loop (for per-kernel ncu lists)")
     p.add_argument("--slab", action="store_true",
                    help="c5: slab-decomposed frame (one slab per rank; the default for c5 when N > 1)")
+    p.add_argument("--fp32", action="store_true",
+                   help="the optional fp32 element pass (configs[2] 'optional fp32 run'; fp64 elsewhere)")
     p.add_argument("--coarse", action="store_true",
                    help="c5 slab frame: two-level preconditioner also at N = 1 (always on for N > 1)")
     return p.parse_args()
@@ -293,6 +295,8 @@ def run_ours(args, world, rank, local):
     n_inst = max(1, sc.batch)
     t_build = time.perf_counter()
     system = build_system(sc)
+    if args.fp32:
+        system.set_precision("fp32")
     t_build = time.perf_counter() - t_build
     cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
     st0 = Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev)
@@ -424,7 +428,8 @@ def run_ours(args, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": per_frame, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 element pass, f64 elsewhere" if args.fp32 else "f64",
+                "data": "synthetic",
                 "config": {"workload": args.config, "tets": int(m), "verts": int(n), "instances": n_inst * world,
                            "iterations_per_step": sc.iterations, "m": sc.m,
                            "l2": "flushed between steps (256 MiB write)",

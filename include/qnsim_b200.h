@@ -251,6 +251,10 @@ int qn_system_objective(qn_system* s, const double* x, const double* y, double* 
 int qn_system_elements(qn_system* s, int64_t inst, int64_t mat, const double* x, double* energy,
                        double* grad_accum, int32_t mem, void* stream);
 
+/* Optional fp32 element pass (configs[2] "optional fp32 run"; tolerance 1e-4
+ * on positions): the per-tet SVD / material / PK1 math in single precision,
+ * positions, forces, gather, L-BFGS and the solve stay fp64.  VL / ARAP tets. */
+int qn_system_set_precision(qn_system* s, int32_t fp32);
 /* Execution mode for debugging: 1 = CUDA graph with conditional nodes
  * (default), 0 = host-driven loop (one host sync per line-search trial). */
 int qn_system_set_graph_mode(qn_system* s, int32_t use_graph);

@@ -132,6 +132,7 @@ SIGNATURES = {
     "qn_system_objective": [_P, _P, _P, _P, _P, _I32, _P],
     "qn_system_elements": [_P, _I64, _I64, _P, _P, _P, _I32, _P],
     "qn_system_set_graph_mode": [_P, _I32],
+    "qn_system_set_precision": [_P, _I32],
     "qn_system_last_frame_ms": [_P, _P],
     "qn_system_last_frame_passes": [_P, _P],
     "qn_system_last_frame_cg_iterations": [_P, _P],

@@ -715,6 +715,20 @@ int qn_system_factor(qn_system* S, qn_factor** out) {
   return QN_OK;
 }
 
+int qn_system_set_precision(qn_system* S, int32_t fp32) {
+  QN_REQUIRE(S, QN_ERR_ARG, "set_precision: null");
+  QN_REQUIRE(!fp32 || (!S->v.spring && !S->v.aniso), QN_ERR_UNSUPPORTED,
+             "set_precision: the fp32 element pass covers Valanis-Landel / ARAP tets");
+  S->v.f32 = fp32 ? 1 : 0;
+  if (S->exec) {  // the frame graph holds the kernel instantiation
+    cudaGraphExecDestroy(S->exec);
+    S->exec = nullptr;
+    cudaGraphDestroy(S->graph);
+    S->graph = nullptr;
+  }
+  return QN_OK;
+}
+
 int qn_system_set_graph_mode(qn_system* S, int32_t use_graph) {
   QN_REQUIRE(S, QN_ERR_ARG, "null");
   S->use_graph = use_graph != 0;

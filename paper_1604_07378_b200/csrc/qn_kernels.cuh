@@ -6,6 +6,7 @@
 
 #include "qn_common.cuh"
 #include "qn_element.cuh"
+#include "qn_element_f32.cuh"
 #include "qn_system.h"
 
 namespace qn {
@@ -121,7 +122,7 @@ __device__ __forceinline__ double spring_thread(const SysView& v, const double* 
 
 // kAniso: the system has anisotropic-fibre elements (a separate instantiation,
 // so the plain per-tet kernel keeps its register allocation)
-template <bool kAniso = false>
+template <bool kAniso = false, bool kF32 = false>
 __device__ __forceinline__ double tet_thread(const SysView& v, const double* __restrict__ x, int b, int t_raw,
                                              const qn_material* mats, int mat_sel, double* fsm) {
   const int t = min(t_raw, v.mt - 1);
@@ -146,8 +147,13 @@ __device__ __forceinline__ double tet_thread(const SysView& v, const double* __r
   // every lane runs the SVD path (its sweeps end on warp votes, so a warp
   // holding both element kinds must not diverge there); fibre elements then
   // replace the result (their VL material evaluates to zero)
-  double e = tet_eval<true>(mats[mi], xs, Dm, vol, f);
-  if (kAniso && mats[mi].a.kind == QN_FN_ANISO) e = aniso_eval(mats[mi], xs, Dm, vol, f);
+  double e;
+  if (kF32) {  // the optional fp32 element pass (fp64 storage and gather)
+    e = tet_eval_f32(mats[mi], xs, Dm, vol, f);
+  } else {
+    e = tet_eval<true>(mats[mi], xs, Dm, vol, f);
+    if (kAniso && mats[mi].a.kind == QN_FN_ANISO) e = aniso_eval(mats[mi], xs, Dm, vol, f);
+  }
   const bool keep = t_raw < v.mt;
   const bool sel = mat_sel < 0 || mi == mat_sel;
   double* fs = fsm + threadIdx.x * kFStride;

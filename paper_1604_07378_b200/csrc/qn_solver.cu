@@ -728,7 +728,7 @@ int launch_col(qn_system* S, int which, cudaStream_t st) {
 }
 
 // per-tet pass at the trial point: energy partials + corner forces
-template <bool kSm, bool kAniso>
+template <bool kSm, bool kAniso, bool kF32 = false>
 __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
   tl_entry(v, 3);
   const int b = blockIdx.y;
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
     double e[1] = {0.0};
     if (v.mt > 0) {
       const qn_material* mats = stage_materials<kSm>(v, b, smat);
-      e[0] = tet_thread<kAniso>(v, v.X + vec_off(v, cc->xs_trial, b), b, blockIdx.x * blockDim.x + threadIdx.x, mats, -1,
+      e[0] = tet_thread<kAniso, kF32>(v, v.X + vec_off(v, cc->xs_trial, b), b, blockIdx.x * blockDim.x + threadIdx.x, mats, -1,
                         fsm);
       store_forces(v, b, fsm);
     }
@@ -794,7 +794,7 @@ __global__ void k_finish(SysView v) {
 // ---------------------------------------------------------------------------
 // seam kernels (objective / gradient / element groups / SVD / material)
 
-template <bool kSm, bool kAniso>
+template <bool kSm, bool kAniso, bool kF32 = false>
 __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet_plain(SysView v, const double* x, int b, int mat_sel,
                                                                    double* part) {
   // b < 0: every instance (blockIdx.y), x and part strided per instance (timing)
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet_plain(SysView v, c
   double e[1] = {0.0};
   if (v.mt > 0) {
     const qn_material* mats = stage_materials<kSm>(v, bb, smat);
-    e[0] = tet_thread<kAniso>(v, x, bb, blockIdx.x * blockDim.x + threadIdx.x, mats, mat_sel, fsm);
+    e[0] = tet_thread<kAniso, kF32>(v, x, bb, blockIdx.x * blockDim.x + threadIdx.x, mats, mat_sel, fsm);
     store_forces(v, bb, fsm);
   }
   block_sum<1>(e, red);
@@ -1529,11 +1529,15 @@ int launch_body_post(qn_system* S, cudaStream_t st) {
   QN_CHECK_LAUNCH();
   if (int rc = launch_col(S, 1, st)) return rc;
   if (v.n_mat <= kMatSmem) {
-    if (v.aniso) {
+    if (v.f32) {
+      k_tet<true, false, true><<<gt, kTT, 0, st>>>(v);
+    } else if (v.aniso) {
       k_tet<true, true><<<gt, kTT, 0, st>>>(v);
     } else {
       k_tet<true, false><<<gt, kTT, 0, st>>>(v);
     }
+  } else if (v.f32) {
+    k_tet<false, false, true><<<gt, kTT, 0, st>>>(v);
   } else if (v.aniso) {
     k_tet<false, true><<<gt, kTT, 0, st>>>(v);
   } else {
@@ -1563,11 +1567,15 @@ int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* 
   const SysView& v = S->v;
   const dim3 g(v.nblk_t, b < 0 ? v.n_inst : 1);
   if (v.n_mat <= kMatSmem) {
-    if (v.aniso) {
+    if (v.f32) {
+      k_tet_plain<true, false, true><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
+    } else if (v.aniso) {
       k_tet_plain<true, true><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
     } else {
       k_tet_plain<true, false><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
     }
+  } else if (v.f32) {
+    k_tet_plain<false, false, true><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
   } else if (v.aniso) {
     k_tet_plain<false, true><<<g, kTT, 0, st>>>(v, x, b, mat_sel, part);
   } else {

@@ -100,6 +100,7 @@ struct DevConfig {
 struct SysView {
   int32_t n, mt, n_inst, n_mat, n_fixed, nblk_v, nblk_t, rec_cap;
   int32_t spring, aniso;  // elements are edge springs (a, b, -1, -1), vols = rest lengths; fibre materials present
+  int32_t f32, pad_f;     // optional fp32 element pass (VL tets; fp64 storage, gather and reductions)
   double h;
   double grav[3];
   const int4* tets;

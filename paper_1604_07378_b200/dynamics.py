@@ -182,6 +182,14 @@ class SimSystem:
         """Integer handle for the torch custom ops (torch_ops.py)."""
         return int(self._h.value)
 
+    def set_precision(self, precision: str):
+        """"fp64" (default) or "fp32": the optional single-precision element
+        pass (configs[2]); everything else stays fp64."""
+        if precision not in ("fp64", "fp32"):
+            raise DynamicsError(f"precision {precision!r}: fp64 | fp32")
+        _lib.check(_lib.load().qn_system_set_precision(self._h, 1 if precision == "fp32" else 0), "set_precision")
+        self.precision = precision
+
     def set_graph_mode(self, on: bool):
         _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
 
@@ -450,7 +458,7 @@ def _build_springs(mesh: SpringNetwork, material, h, gravity, fixed, solver, pcg
 def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(), aniso=None,
                  colliders=(), collision_weight: float | None = None,
                  fit_interval: FitInterval = FitInterval(), solver: str = "direct", pcg_tol: float = 1e-10,
-                 pcg_maxit: int = 20000) -> SimSystem:
+                 pcg_maxit: int = 20000, precision: str = "fp64") -> SimSystem:
     """dynamics.py:351-434 for Valanis-Landel tet groups (single instance).
 
     solver="direct" prefactors A_free once (the reference's semantics);
@@ -466,8 +474,11 @@ def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_G
     assign = _assign(mesh, materials)
     if aniso:  # AnisoGroup appended after the material groups (dynamics.py:368-373)
         assign = assign + _aniso_groups(mesh, aniso)
-    return _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit,
-                  colliders, collision_weight)
+    system = _build(mesh, [assign], h, gravity, fixed, fit_interval, len(assign), solver, pcg_tol, pcg_maxit,
+                    colliders, collision_weight)
+    if precision != "fp64":
+        system.set_precision(precision)
+    return system
 
 
 def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_GRAVITY, fixed=(),

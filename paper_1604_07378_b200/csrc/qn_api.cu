@@ -664,6 +664,12 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     int32_t* ve;
     if ((rc = sys_upload(S, &ve, v2e.data(), v2e.size()))) return fail(rc);
     v.v2e = ve;
+    // corner forces are stored in gather order: slot 4t + c -> its v2e position
+    std::vector<int32_t> slot_pos((size_t)std::max<int64_t>(mt, 1) * 4, -1);
+    for (int64_t k = 0; k < v2e_ptr[n]; ++k) slot_pos[v2e[k]] = (int32_t)k;
+    int32_t* sp;
+    if ((rc = sys_upload(S, &sp, slot_pos.data(), slot_pos.size()))) return fail(rc);
+    v.slot_pos = sp;
     int32_t* fv;
     if ((rc = sys_upload(S, &fv, fact_vtx.data(), fact_vtx.size()))) return fail(rc);
     v.fact_vtx = fv;

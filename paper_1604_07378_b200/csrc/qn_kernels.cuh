@@ -164,13 +164,25 @@ __device__ __forceinline__ double tet_thread(const SysView& v, const double* __r
   return keep && sel ? e : 0.0;
 }
 
-// coalesced write of the block's staged forces: [tet][corner][xyz] contiguous
+// corner forces of this thread's element to their gather positions: slot
+// 4t + c goes to entry slot_pos[4t + c] of the vertex-major gather order
+// (v2e), so the gradient gather streams each vertex's contiguous run of
+// entries instead of chasing slot ids (same values, same order)
 __device__ __forceinline__ void store_forces(const SysView& v, int b, const double* fsm) {
-  __syncthreads();
-  const int t0 = blockIdx.x * blockDim.x;
-  const int cnt = min((int)blockDim.x, v.mt - t0) * 12;
-  double* out = v.forces + ((size_t)b * v.mt + t0) * 12;
-  for (int w = threadIdx.x; w < cnt; w += blockDim.x) out[w] = fsm[(w / 12) * kFStride + (w % 12)];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= v.mt) return;
+  const double* fs = fsm + threadIdx.x * kFStride;
+  double* base = v.forces + (size_t)b * v.mt * 12;
+  const int4 pos = __ldg(reinterpret_cast<const int4*>(v.slot_pos) + t);
+  const int p[4] = {pos.x, pos.y, pos.z, pos.w};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (p[c] < 0) continue;
+    double* o = base + 3 * (size_t)p[c];
+    o[0] = fs[3 * c + 0];
+    o[1] = fs[3 * c + 1];
+    o[2] = fs[3 * c + 2];
+  }
 }
 
 }  // namespace qn

@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_grad(SlabView s, SlabArgs a) {
     const double w = __ldg(v.w_in + i);
     for (int c = 0; c < 3; ++c) g[c] = __dmul_rn(w, __dsub_rn(x[c], s.y[o + c]));
     for (int k = v.v2e_ptr[i]; k < v.v2e_ptr[i + 1]; ++k) {
-      const double* f = v.forces + (size_t)v.v2e[k] * 3;
+      const double* f = v.forces + (size_t)k * 3;  // gather order
       for (int c = 0; c < 3; ++c) g[c] = __dadd_rn(g[c], f[c]);
     }
     if (s.pinned[i]) g[0] = g[1] = g[2] = 0.0;

@@ -195,22 +195,18 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
     const size_t oc = inst_off(v, b) + (size_t)ci;
     const double xc = v.X[vec_off(v, cur, b) + ci];
     double g = __dmul_rn(__ldg(v.w_in + i), __dsub_rn(xc, v.y[oc]));
+    // corner forces are stored in gather order: this vertex's entries are the
+    // contiguous run [v2e_ptr[i], v2e_ptr[i+1]) (element order = the
+    // reference's np.add.at order)
     const double* fb = v.forces + (size_t)b * v.mt * 12 + (ci - 3 * i);
     const int e1 = __ldg(v.v2e_ptr + i + 1);
     int e = __ldg(v.v2e_ptr + i);
-    // element-order accumulation (the reference's np.add.at order)
     if (e1 - e <= kGatherFast) {
-      // all slot ids, then all corner forces, in flight together (two round
-      // trips instead of two per 8 slots), then the ordered adds
       const int cnt = e1 - e;
-      int id[kGatherFast];
       double f[kGatherFast];
 #pragma unroll
       for (int q = 0; q < kGatherFast; ++q)
-        if (q < cnt) id[q] = __ldg(v.v2e + e + q);
-#pragma unroll
-      for (int q = 0; q < kGatherFast; ++q)
-        if (q < cnt) f[q] = __ldcg(fb + (size_t)id[q] * 3);
+        if (q < cnt) f[q] = __ldcg(fb + 3 * (size_t)(e + q));
 #pragma unroll
       for (int q = 0; q < kGatherFast; ++q)
         if (q < cnt) g = __dadd_rn(g, f[q]);
@@ -218,11 +214,11 @@ __global__ void __launch_bounds__(kVT) k_grad(SysView v) {
       for (; e + 8 <= e1; e += 8) {
         double f[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) f[q] = __ldcg(fb + (size_t)__ldg(v.v2e + e + q) * 3);
+        for (int q = 0; q < 8; ++q) f[q] = __ldcg(fb + 3 * (size_t)(e + q));
 #pragma unroll
         for (int q = 0; q < 8; ++q) g = __dadd_rn(g, f[q]);
       }
-      for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + (size_t)__ldg(v.v2e + e) * 3));
+      for (; e < e1; ++e) g = __dadd_rn(g, __ldcg(fb + 3 * (size_t)e));
     }
     if (v.n_col) g = __dadd_rn(g, v.col_g[oc]);  // add_collision_gradient (dynamics.py:476)
     if (v.is_fixed[i]) g = 0.0;
@@ -834,7 +830,7 @@ __global__ void k_gather_plain(SysView v, const double* x, const double* y, doub
     }
     const double* fb = v.forces + (size_t)b * v.mt * 12;
     for (int k = v.v2e_ptr[i]; k < v.v2e_ptr[i + 1]; ++k) {
-      const double* f = fb + (size_t)v.v2e[k] * 3;
+      const double* f = fb + (size_t)k * 3;
       for (int a = 0; a < 3; ++a) g[a] = __dadd_rn(g[a], f[a]);
     }
     if (zero_fixed && v.is_fixed[i]) g[0] = g[1] = g[2] = 0.0;

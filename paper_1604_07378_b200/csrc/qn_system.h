@@ -114,6 +114,7 @@ struct SysView {
   const int32_t* fixed_pos;  // vertex -> index into the fixed list, -1 if free
   const int32_t* v2e_ptr;
   const int32_t* v2e;        // slots 4 t + c, increasing
+  const int32_t* slot_pos;   // [4 mt] gather position of slot 4 t + c (forces are stored in v2e order), -1 if absent
   const int32_t* fact_vtx;   // factor row -> vertex
   double* q_l;
   double* q_prev;
@@ -124,7 +125,7 @@ struct SysView {
   double* T;
   double* R0;      // [inst][n][3]
   double* D;       // [inst][n][3]
-  double* forces;  // [inst][mt][4][3]
+  double* forces;  // [inst][4 mt][3] corner forces in gather (v2e) order
   const double* targets;  // [inst][n_fixed][3]
   double* part_v;  // [inst][nblk_v][kNG]
   double* part_t;  // [inst][nblk_t]

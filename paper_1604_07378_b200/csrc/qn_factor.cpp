@@ -88,7 +88,11 @@ struct ND {
   }
 
   void run(std::vector<int32_t> verts) {
-    if ((int64_t)verts.size() <= kLeaf) {
+    static const int64_t leaf = [] {
+      const char* e = std::getenv("QN_ND_LEAF");
+      return e ? std::max<int64_t>(8, std::atoll(e)) : (int64_t)kLeaf;
+    }();
+    if ((int64_t)verts.size() <= leaf) {
       std::sort(verts.begin(), verts.end());
       order.insert(order.end(), verts.begin(), verts.end());
       return;
@@ -374,6 +378,12 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
   // subtree root's, by the etree ancestor property).  inv(L11) of the merged
   // block is stored dense, explicit zeros included.
   if (nbatch == 1) {
+    // experiment knobs (defaults measured on configs[1..2])
+    int32_t collapse_h = kCollapseHeight;
+    double collapse_cols = kCollapseCols, collapse_growth = kCollapseGrowth;
+    if (const char* e = std::getenv("QN_COLLAPSE_HEIGHT")) collapse_h = std::atoi(e);
+    if (const char* e = std::getenv("QN_COLLAPSE_COLS")) collapse_cols = std::atof(e);
+    if (const char* e = std::getenv("QN_COLLAPSE_GROWTH")) collapse_growth = std::atof(e);
     const int32_t ng = (int32_t)f->sup_col.size();
     std::vector<int32_t> gcol(f->sup_col);
     gcol.push_back((int32_t)n);
@@ -403,8 +413,8 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     for (int32_t g = ng - 1; g >= 0; --g) {  // parents before children
       const bool pc = gpar[g] >= 0 && covered[gpar[g]];
       const double zm = sub_nc[g] * (sub_nc[g] + below_g[g]);
-      const bool ok = gsize[g] > 1 && ht[g] <= kCollapseHeight && sub_nc[g] <= kCollapseCols &&
-                      zm <= kCollapseGrowth * sub_z[g];
+      const bool ok = gsize[g] > 1 && ht[g] <= collapse_h && sub_nc[g] <= collapse_cols &&
+                      zm <= collapse_growth * sub_z[g];
       sel[g] = !pc && ok;
       covered[g] = pc || sel[g];
     }

@@ -133,7 +133,7 @@ constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if i
 constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
 constexpr int64_t kSmemPerCtaPair = 110 * 1024;  // dynamic smem per CTA with two CTAs per SM (228 KB - reserved/static)
 // bottom-of-tree subtree collapse (see factor_build_host)
-constexpr int32_t kCollapseHeight = 3;
+constexpr int32_t kCollapseHeight = 2;  // swept on c1-c3 with the current solve kernels: 2 > 3 (+3.6 % at c2), 1 and 4 slower
 constexpr double kCollapseCols = 512;
 constexpr double kCollapseGrowth = 2.5;
 

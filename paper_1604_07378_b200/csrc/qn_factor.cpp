@@ -346,6 +346,10 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
   };
   f->sup_col.clear();
   std::vector<int32_t> last_f;  // last fundamental supernode of each merged group
+  const double relax = [] {      // experiment knob: scales the allowed zero fractions
+    const char* e = std::getenv("QN_RELAX_SCALE");
+    return e ? std::max(0.0, std::atof(e)) : 1.0;
+  }();
   {
     int32_t g0 = 0;       // first fundamental supernode of the open group
     double true_nnz = 0;  // sum of exact column counts of the open group
@@ -359,7 +363,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
         double tn = true_nnz;
         for (int32_t j = fcol[s + 1]; j < fcol[s + 2]; ++j) tn += (double)cnt[j];
         const double z = (merged - tn) / merged;
-        merge = ncol <= 4 || (ncol <= 16 && z <= 0.8) || (ncol <= 48 && z <= 0.1) || z <= 0.05;
+        merge = ncol <= 4 || (ncol <= 16 && z <= 0.8) || (ncol <= 48 && z <= 0.1 * relax) || z <= 0.05 * relax;
       }
       if (!merge) {
         f->sup_col.push_back(fcol[g0]);
@@ -597,6 +601,14 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     };
     f->ffirst.assign(ns, 0);
     f->bfirst.assign(ns, 0);
+    // experiment knobs (<= the compile-time tile bounds)
+    auto knob = [](const char* name, int64_t dflt, int64_t hi) {
+      const char* e = std::getenv(name);
+      return e ? std::max<int64_t>(1, std::min<int64_t>(hi, std::atoll(e))) : dflt;
+    };
+    const int64_t te_f = knob("QN_FWD_TASK_ENTRIES", kTaskEntries, kTaskEntries);
+    const int64_t te_b = knob("QN_BWD_TASK_ENTRIES", kTaskEntries, kTaskEntries);
+    const int64_t bcols = knob("QN_BWD_TASK_COLS", kBwdTaskCols, kBwdTaskCols);
     // backward Z tile: as large as kTaskEntries but small enough that two
     // CTAs (each also holding w = nr x 3 of the tallest front) share an SM
     {
@@ -605,7 +617,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
         if (!f->is_top[s]) mr = std::max<int32_t>(mr, (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]));
       const int64_t rest = 8 * (3 * (int64_t)mr + 4 * kBwdTaskCols) + 4 * 2048;
       const int64_t fit = (kSmemPerCtaPair - rest) / 8;
-      f->bwd_entries = std::max<int64_t>(mr, std::min<int64_t>(kTaskEntries, fit));
+      f->bwd_entries = std::max<int64_t>(mr, std::min<int64_t>(te_b, fit));
       f->task_max_rows = mr;
     }
     for (int32_t s : order) {
@@ -614,8 +626,8 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nc <= kTaskEntries && nr - nc <= (int64_t)1 << 20, QN_ERR_UNSUPPORTED,
                  "factor: supernode too wide for the device solve tiles");
-      const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, kTaskEntries / (32 * (int64_t)nc))));
-      const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::min<int64_t>(32, kTaskEntries / nc);
+      const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, te_f / (32 * (int64_t)nc))));
+      const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::max<int64_t>(1, std::min<int64_t>(32, te_f / nc));
       f->ffirst[s] = (int32_t)f->ftask.size();
       for (int32_t r = 0; r < nr; r += rows) {
         f->ftask.push_back({s, r, std::min(nr, r + rows), rg});
@@ -629,7 +641,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nr <= f->bwd_entries, QN_ERR_UNSUPPORTED, "factor: supernode front too tall for the device tiles");
-      const int32_t cols = (int32_t)std::min<int64_t>(kBwdTaskCols, std::max<int64_t>(1, f->bwd_entries / nr));
+      const int32_t cols = (int32_t)std::min<int64_t>(bcols, std::max<int64_t>(1, f->bwd_entries / nr));
       f->bfirst[s] = (int32_t)f->btask.size();
       for (int32_t k = 0; k < nc; k += cols) {
         f->btask.push_back({s, k, std::min(nc, k + cols), 0});

@@ -599,7 +599,8 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_inst = (int32_t)ni;
   v.n_mat = (int32_t)d->n_mat;
   v.n_fixed = (int32_t)d->n_fixed;
-  v.nblk_v = div_up(3 * n, kVertexThreads);  // vector kernels run one thread per (vertex, coordinate)
+  v.vt = ni == 1 ? kVertexThreadsMax : kVertexThreads;
+  v.nblk_v = div_up(3 * n, v.vt);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, 128));
   v.spring = d->element_kind == QN_ELEM_SPRING ? 1 : 0;
   v.aniso = 0;
@@ -1108,7 +1109,7 @@ int qn_system_objective(qn_system* S, const double* x, const double* y, double* 
   for (int64_t b = 0; b < S->n_inst; ++b) {
     if ((rc = to_device(dx, x + b * nv, nv, mem, st)) || (rc = to_device(dy, y + b * nv, nv, mem, st))) return rc;
     if ((rc = launch_tet_plain(S, dx, (int)b, -1, S->d_part_plain, st))) return rc;
-    k_gather_plain<<<v.nblk_v, kVertexThreads, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
+    k_gather_plain<<<v.nblk_v, v.vt, 0, st>>>(v, dx, dy, dg, (int)b, 1, 1, S->d_part_plain + v.nblk_t);
     QN_CHECK_LAUNCH();
     QN_CUDA(cudaMemcpyAsync(pt.data(), S->d_part_plain, v.nblk_t * sizeof(double), cudaMemcpyDeviceToHost, st));
     QN_CUDA(cudaMemcpyAsync(pv.data(), S->d_part_plain + v.nblk_t, v.nblk_v * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1145,7 +1146,7 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
   if ((rc = launch_tet_plain(S, dx, (int)inst, (int)mat, S->d_part_plain, st))) return rc;
   if (grad_accum) {
     if ((rc = to_device(dg, grad_accum, nv, mem, st))) return rc;
-    k_gather_plain<<<v.nblk_v, kVertexThreads, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
+    k_gather_plain<<<v.nblk_v, v.vt, 0, st>>>(v, dx, nullptr, dg, (int)inst, 0, 0, nullptr);
     QN_CHECK_LAUNCH();
     if ((rc = from_device(grad_accum, dg, nv, mem, st))) return rc;
   }

@@ -37,8 +37,9 @@
 
 namespace qn {
 
-constexpr int kVT = kVertexThreads;  // vertex-kernel block
-constexpr int kBodyUnroll = 2;  // body passes per WHILE iteration of the frame graph (direct solver)
+constexpr int kVT = kVertexThreads;     // vertex-kernel block of the small kernels (k_col, k_rest_rhs)
+constexpr int kVTB = kVertexThreadsMax;  // launch bound of the per-(vertex, coordinate) kernels (block = v.vt)
+constexpr int kBodyUnroll = 3;  // body passes per WHILE iteration of the frame graph (direct solver)
 constexpr int kGatherFast = 24;  // vertex valences up to this gather in two round trips (Freudenthal: <= 24)
 
 constexpr double kCurvatureGuard = 1e-12;  // solvers.py:28
@@ -170,7 +171,7 @@ __device__ __forceinline__ void tl_entry(const SysView& v, int kid) {
 // M = compile-time bound on the history window (the register footprint of the
 // dot-product accumulators scales with it; the host picks the smallest that fits).
 template <int M>
-__global__ void __launch_bounds__(kVT) k_grad(SysView v) {
+__global__ void __launch_bounds__(kVTB) k_grad(SysView v) {
   constexpr int NG = 5 + 2 * M;
   tl_entry(v, 0);
   // instances in reverse launch order: the per-tet pass just wrote the last
@@ -353,7 +354,7 @@ struct SolverIO {
 // lbfgs_init = "scaled_identity" (solvers.py:136-141): r = (rho / <t, t>) q of
 // the newest pair (1 with an empty history) in place of A^-1 q, every row
 // (fixed rows of q are zero), one thread per (vertex, coordinate)
-__global__ void __launch_bounds__(kVertexThreads) k_scaled(SysView v) {
+__global__ void __launch_bounds__(kVTB) k_scaled(SysView v) {
   const int b = blockIdx.y;
   const InstCtl* c = v.ctl + b;
   if (c->phase != PH_DIR) return;
@@ -420,7 +421,7 @@ int launch_solve_timing(qn_system* S, cudaStream_t st) { return launch_solve(S->
 
 // <t_i, r0> and the eta recursion (solvers.py:147-150)
 template <int M>
-__global__ void __launch_bounds__(kVT) k_eta(SysView v) {
+__global__ void __launch_bounds__(kVTB) k_eta(SysView v) {
   tl_entry(v, 1);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -465,7 +466,7 @@ __device__ void eta_finalize(InstCtl& c, const double* tot, int np) {
 }
 
 // direction, trial point, inertia / slope partials
-__global__ void __launch_bounds__(kVT) k_vec(SysView v) {
+__global__ void __launch_bounds__(kVTB) k_vec(SysView v) {
   tl_entry(v, 2);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -1464,9 +1465,9 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
   const dim3 gv(v.nblk_v, v.n_inst);
   if (int rc = launch_col(S, 0, st)) return rc;
   if (S->h_cfg.m <= 5) {  // default window: smaller register footprint
-    k_grad<5><<<gv, kVT, 0, st>>>(v);
+    k_grad<5><<<gv, v.vt, 0, st>>>(v);
   } else {
-    k_grad<kMaxM><<<gv, kVT, 0, st>>>(v);
+    k_grad<kMaxM><<<gv, v.vt, 0, st>>>(v);
   }
   QN_CHECK_LAUNCH();
   if (v.pcg) {
@@ -1479,7 +1480,7 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
     return QN_OK;
   }
   if (S->h_cfg.lbfgs_init == 1) {
-    k_scaled<<<gv, kVT, 0, st>>>(v);
+    k_scaled<<<gv, v.vt, 0, st>>>(v);
     QN_CHECK_LAUNCH();
     return QN_OK;
   }
@@ -1516,12 +1517,12 @@ int launch_body_post(qn_system* S, cudaStream_t st) {
     QN_CHECK_LAUNCH();
   }
   if (small_m) {
-    k_eta<5><<<gv, kVT, 0, st>>>(v);
+    k_eta<5><<<gv, v.vt, 0, st>>>(v);
   } else {
-    k_eta<kMaxM><<<gv, kVT, 0, st>>>(v);
+    k_eta<kMaxM><<<gv, v.vt, 0, st>>>(v);
   }
   QN_CHECK_LAUNCH();
-  k_vec<<<gv, kVT, 0, st>>>(v);
+  k_vec<<<gv, v.vt, 0, st>>>(v);
   QN_CHECK_LAUNCH();
   if (int rc = launch_col(S, 1, st)) return rc;
   if (v.n_mat <= kMatSmem) {
@@ -1583,14 +1584,14 @@ int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* 
 
 int launch_init(qn_system* S, cudaStream_t st) {
   const dim3 gv(S->v.nblk_v, S->v.n_inst);
-  k_init<<<gv, kVT, 0, st>>>(S->v);
+  k_init<<<gv, S->v.vt, 0, st>>>(S->v);
   QN_CHECK_LAUNCH();
   return QN_OK;
 }
 
 int launch_finish(qn_system* S, cudaStream_t st) {
   const dim3 gv(S->v.nblk_v, S->v.n_inst);
-  k_finish<<<gv, kVT, 0, st>>>(S->v);
+  k_finish<<<gv, S->v.vt, 0, st>>>(S->v);
   QN_CHECK_LAUNCH();
   return QN_OK;
 }

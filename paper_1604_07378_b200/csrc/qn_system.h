@@ -23,7 +23,8 @@ enum Phase : int32_t {
 };
 
 constexpr int kMaxM = QN_MAX_M;
-constexpr int kVertexThreads = 128;  // vertex kernels: small blocks so every SM gets work
+constexpr int kVertexThreads = 128;     // vertex kernels of batched systems: small blocks so every SM gets work
+constexpr int kVertexThreadsMax = 256;  // vertex kernels of single systems (swept on configs[1]: 256 > 128)
 constexpr int kNG = 5 + 2 * kMaxM;  // gradient-kernel dot products per block
 
 struct InstCtl {
@@ -99,6 +100,7 @@ struct DevConfig {
 
 struct SysView {
   int32_t n, mt, n_inst, n_mat, n_fixed, nblk_v, nblk_t, rec_cap;
+  int32_t vt, pad_vt;     // vertex-kernel block size (kVertexThreads or kVertexThreadsMax)
   int32_t spring, aniso;  // elements are edge springs (a, b, -1, -1), vols = rest lengths; fibre materials present
   int32_t f32, pad_f;     // optional fp32 element pass (VL tets; fp64 storage, gather and reductions)
   double h;

@@ -601,7 +601,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_fixed = (int32_t)d->n_fixed;
   v.vt = ni == 1 ? kVertexThreadsMax : kVertexThreads;
   v.nblk_v = div_up(3 * n, v.vt);  // vector kernels run one thread per (vertex, coordinate)
-  v.nblk_t = std::max(1, div_up(mt, 128));
+  v.nblk_t = std::max(1, div_up(mt, kTetThreads));
   v.spring = d->element_kind == QN_ELEM_SPRING ? 1 : 0;
   v.aniso = 0;
   for (int64_t q = 0; q < ni * d->n_mat && mt > 0; ++q)

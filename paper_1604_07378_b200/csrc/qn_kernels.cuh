@@ -11,7 +11,7 @@
 
 namespace qn {
 
-constexpr int kTT = 128;  // tet-kernel block
+constexpr int kTT = kTetThreads;  // tet-kernel block
 constexpr int kTetBlocksPerSm = 6;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
 
 // last block of instance b for counter `which`?  (after all partial writes)

@@ -24,7 +24,8 @@ enum Phase : int32_t {
 
 constexpr int kMaxM = QN_MAX_M;
 constexpr int kVertexThreads = 128;     // vertex kernels of batched systems: small blocks so every SM gets work
-constexpr int kVertexThreadsMax = 256;  // vertex kernels of single systems (swept on configs[1]: 256 > 128)
+constexpr int kVertexThreadsMax = 256;
+constexpr int kTetThreads = 128;  // per-tet kernel block (qn_kernels.cuh kTT; the grid is mt / kTetThreads)  // vertex kernels of single systems (swept on configs[1]: 256 > 128)
 constexpr int kNG = 5 + 2 * kMaxM;  // gradient-kernel dot products per block
 
 struct InstCtl {

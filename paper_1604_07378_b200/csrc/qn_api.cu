@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -600,6 +601,8 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   v.n_mat = (int32_t)d->n_mat;
   v.n_fixed = (int32_t)d->n_fixed;
   v.vt = ni == 1 ? kVertexThreadsMax : kVertexThreads;
+  if (const char* e = std::getenv("QN_VERTEX_THREADS"))  // experiment knob: 32 .. kVertexThreadsMax, multiple of 32
+    v.vt = std::max(32, std::min(kVertexThreadsMax, (std::atoi(e) / 32) * 32));
   v.nblk_v = div_up(3 * n, v.vt);  // vector kernels run one thread per (vertex, coordinate)
   v.nblk_t = std::max(1, div_up(mt, kTetThreads));
   v.spring = d->element_kind == QN_ELEM_SPRING ? 1 : 0;

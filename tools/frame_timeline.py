@@ -23,7 +23,7 @@ def main(cfg="c2", frames="3"):
     sc = bench.build_scene(cfg, 0, 1)
     system = bench.build_system(sc)
     lib = _lib.load()
-    run = ResidentRun(system, Q.SimState(sc.q_l, sc.q_prev), SolverConfig(iterations=sc.iterations, m=sc.m))
+    run = ResidentRun(system, Q.SimState(sc.q_l, sc.q_prev), SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
     for _ in range(2):
         run.step()
     _lib.check(lib.qn_system_set_timeline(system._h, 1))

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqnsim_b200.so")
+# QN_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("QN_LIB") or os.path.join(_HERE, "libqnsim_b200.so")
 
 QN_OK = 0
 QN_ERR_ARG = 1

@@ -247,9 +247,9 @@ def run_reference(args, world, rank):
         return
     from paper_1604_07378_b200 import scenes
     if args.config == "c5":  # the oracle's sparse LU of a 12 M-dof A_free does not fit a bounded host run
-        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "value": None,
+        emit({"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "value": None,
                           "unavailable": "configs[4]: the CPU oracle factors A_free (12 M dofs); not a bounded "
-                                         "host run (DESIGN.md section 6)"}), flush=True)
+                                         "host run (DESIGN.md section 6)"})
         return
     sc = scenes.CONFIGS[args.config]()
     threads = os.cpu_count() or 1
@@ -279,7 +279,7 @@ def run_reference(args, world, rank):
                        "iterations_per_step": its},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, world, rank, local):
@@ -442,7 +442,7 @@ def run_ours(args, world, rank, local):
                 "build_s": t_build, "passes_per_step": passes / args.steps}
         if cg_iters:
             line["cg_iterations_per_step"] = cg_iters / args.steps
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -558,7 +558,7 @@ def run_slab(args, world, rank, local):
                 "tet_evals_per_s": evals * m_all / (total_ms / 1000.0), "roofline": roof, "cpu_baseline": None,
                 "e2e": e2e, "clocks": clk, "gpu_launches": launches, "build_s": t_build, "coarse_setup_s": t_coarse,
                 "cg_iterations_per_step": cg_per_step}
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -569,7 +569,27 @@ def _free_port():
         return sk.getsockname()[1]
 
 
+_OUT = sys.stdout
+
+
+def emit(line):
+    """The contract's one JSON line, on the real stdout."""
+    print(json.dumps(line), file=_OUT, flush=True)
+
+
+def _private_stdout():
+    """Native libraries print to fd 1 (the GPU boxes set NCCL_DEBUG=VERSION, so
+    NCCL's banner lands there at communicator creation): fd 1 becomes stderr and
+    the JSON line goes through a private duplicate of the original stdout."""
+    global _OUT
+    sys.stdout.flush()
+    fd = os.dup(1)
+    os.dup2(2, 1)
+    _OUT = os.fdopen(fd, "w", buffering=1)
+
+
 def main():
+    _private_stdout()
     args = parse()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -4,15 +4,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
-One step = one frame (simulate_frame) of the configuration; the default
-workload is configs[1] (c2: 60x15x15 StVK bar, 81 000 tets, 20 L-BFGS
-iterations per frame), the configuration the metric is quoted on that fits one
-GPU.  N > 1: launched by torch.distributed.run, one process per GPU; c1-c3 do
-not shard (independent replicas per rank, "weak"), c4 shards its 1024
-instances across ranks (no data-path collective).  Timing: CUDA events on the
-launching stream around each frame, L2 flushed (256 MiB write) between frames,
-max over ranks.  `--impl reference` times the CPU oracle port of the reference
-(oracle/, numpy + scipy sparse factor) on host threads.
+One step = one frame (simulate_frame) of the configuration.  BASELINE.json's
+metric names no configuration, so the default workload is the largest
+configuration that runs on one GPU as a single system: configs[2] (c3:
+100x25x25 spline bar, 375 000 tets, 10 L-BFGS iterations per frame).  N > 1:
+launched by torch.distributed.run, one process per GPU; c1-c3 do not shard
+(independent replicas per rank, "weak"), c4 splits its fixed 1024 instances
+across ranks (no data-path collective, "strong"), c5 splits one mesh into
+x-slabs (NCCL, "strong").  Timing: CUDA events on the launching stream around
+each frame, L2 flushed (256 MiB write) between frames, max over ranks.
+`--impl reference` times the CPU oracle port of the reference (oracle/, numpy +
+scipy sparse factor) on host threads, one full frame per step (the same
+iterations per step as the GPU arm).
 """
 
 from __future__ import annotations
@@ -41,7 +44,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -161,16 +164,20 @@ def ncu_traffic(workload, kernel):
 
 FP64_PEAK_TFLOPS = 34.37  # DFMA microbenchmark on this pool's B200 (tools/probe_device.cu, profiles/r01_device_probe.txt)
 # fp64 flops per tet eval (2 DFMA + DMUL + DADD) from ncu sass counters of the per-tet kernel
-# (smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum / tets; c2 StVK, profiles/r01_fp64_flops.txt)
-FLOPS_PER_TET = 1388.0
+# (smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum / tets), per workload because the
+# material (and the SVD sweep count of the state) changes the count: profiles/r0*_fp64_flops*.txt
+FLOPS_PER_TET = {"c2": (1388.0, "ncu sass counters, c2 StVK (profiles/r01_fp64_flops.txt)")}
 
 
 def tet_fp64(sc, tets, tet_ms):
     """The per-tet kernel against the FP64 roofline (report K1 against
     max(bytes/BW, flops/FP64 peak))."""
-    tf = FLOPS_PER_TET * tets / (tet_ms * 1e-3) / 1e12
-    return {"flops_per_tet": FLOPS_PER_TET, "achieved_tflops": tf, "peak_tflops": FP64_PEAK_TFLOPS,
-            "frac": tf / FP64_PEAK_TFLOPS, "flops_source": "ncu sass counters, c2 StVK material"}
+    fpt, src = FLOPS_PER_TET.get(sc.name.split("_")[0], (None, None))
+    if fpt is None:
+        return None
+    tf = fpt * tets / (tet_ms * 1e-3) / 1e12
+    return {"flops_per_tet": fpt, "achieved_tflops": tf, "peak_tflops": FP64_PEAK_TFLOPS,
+            "frac": tf / FP64_PEAK_TFLOPS, "flops_source": src}
 
 
 def frame_timeline(system, run, stream):
@@ -200,6 +207,12 @@ def frame_timeline(system, run, stream):
             "solve": mean([t[p, 1, 0] - t[p, 0, 1] for p in full]),
             "tet": mean([t[p, 3, 1] - t[p, 3, 0] for p in range(npass)]),
             "frame": (t[npass - 1, 3, 1] - (t[0, 0, 0] or t[0, 3, 0])) / 1000.0}
+
+
+def scaling_of(workload):
+    """c4's 1024 instances and c5's one mesh are fixed totals split over the ranks
+    (strong); c1-c3 run one replica per rank (weak)."""
+    return "strong" if workload in ("c4", "c5") else "weak"
 
 
 def build_scene(name, rank, world):
@@ -260,23 +273,26 @@ def run_reference(args, world, rank):
     osys = O.build(sc.verts, sc.tets, sc.density, oracle_material(spec), sc.h, sc.gravity, sc.fixed)
     q_l = np.array(sc.q_l[0] if sc.batch else sc.q_l)
     q_prev = np.array(sc.q_prev[0] if sc.batch else sc.q_prev)
-    its = 2 if sc.tets.shape[0] > 10000 else sc.iterations  # bounded sample per step
+    its = sc.iterations  # one whole frame per step: the GPU arm's iterations_per_step
+    warm = min(args.warmup, 1)  # host code has no JIT / cache warm-up beyond the first frame
     times = []
-    for k in range(args.warmup + args.steps):
+    for k in range(warm + args.steps):
         t = time.perf_counter()
         x, _, _ = O.simulate_frame(osys, q_l, q_prev, iterations=its, m=sc.m)
         dt = time.perf_counter() - t
         q_prev, q_l = q_l, x
-        if k >= args.warmup:
+        if k >= warm:
             times.append(dt)
     total = sum(times)
     value = its * args.steps / total  # (instance-)iterations per second on the host
-    sample = f"{its} L-BFGS iterations of one {args.config} frame per step (oracle port, sparse LU factor)"
+    sample = (f"{args.steps} consecutive {args.config} frames x {its} L-BFGS iterations from the scene's initial "
+              f"state after {warm} untimed frame(s) (oracle port, sparse LU factor, {threads} element-pass threads)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": args.config, "tets": int(sc.tets.shape[0]), "verts": int(sc.verts.shape[0]),
-                       "iterations_per_step": its},
+                       "instances": 1, "iterations_per_step": its, "m": sc.m},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
@@ -344,7 +360,10 @@ def run_ours(args, world, rank, local):
     info = system.factor_info()
     m, n = sc.tets.shape[0], sc.verts.shape[0]
     tet_ms = system.time_kernel("tet", reps=20, stream=sptr)
-    tet_bytes = (192.0 + 24.0 * n / m) * m * n_inst           # idx+Dm^-1+vol+forces, x gathered once
+    # idx + Dm^-1 + vol (96 B/tet) are shared by all instances of a batch (one mesh,
+    # qn_kernels.cuh: no instance term); forces (96 B) and the x gather (24 n/m)
+    # are per instance
+    tet_bytes = 96.0 * m + (96.0 + 24.0 * n / m) * m * n_inst
     per_frame = total_ms / args.steps
     share_tet = tet_ms * passes / args.steps / per_frame
     batched = info.get("nbatch", 1) > 1
@@ -428,7 +447,8 @@ def run_ours(args, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": per_frame, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 element pass, f64 elsewhere" if args.fp32 else "f64",
+                "scaling": scaling_of(args.config), "vs_baseline": None,
+                "dtype": "f32 element pass, f64 elsewhere" if args.fp32 else "f64",
                 "data": "synthetic",
                 "config": {"workload": args.config, "tets": int(m), "verts": int(n), "instances": n_inst * world,
                            "iterations_per_step": sc.iterations, "m": sc.m,

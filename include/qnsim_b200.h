@@ -267,6 +267,14 @@ int qn_system_last_frame_passes(qn_system* s, int64_t* passes);
  * only), k_tet, sptrsv_forward, sptrsv_backward; out = [512 passes][6
  * kernels][2] (0 = not reached).  Enabling rebuilds the frame graph. */
 int qn_system_set_timeline(qn_system* s, int32_t enable);
+/* Test-only fault injection into the device line search, from L-BFGS iteration
+ * `iteration` (1-based) on: mode 1 negates the direction (slope >= 0, the
+ * ascent -> SolverError branch of solvers.py:244-246); mode 2 steps along -d
+ * while the Armijo test uses the slope of d (every trial increases g: the
+ * StagnationError branch, solvers.py:250-252 and the record padding of
+ * :329-336, as pkg/tests/test_solvers.py:318-337 provoke on the host).
+ * mode 0 = off (the default). */
+int qn_system_set_fault(qn_system* s, int32_t mode, int32_t iteration);
 int qn_system_timeline(qn_system* s, uint64_t* out, int64_t cap);
 /* diagnostics: task trace of the last in-graph solve (direct solver, timeline
  * enabled), same layout as qn_factor_trace_solve */

@@ -86,6 +86,18 @@ int sys_upload(qn_system* S, T** p, const T* h, size_t count) {
 
 cudaStream_t pick(qn_system* S, void* stream) { return stream ? (cudaStream_t)stream : S->stream; }
 
+// three n x 3 vectors for the seam entry points (objective / elements), owned
+// by the system and freed with it
+int ensure_scratch(qn_system* S) {
+  if (S->scratch[0]) return QN_OK;
+  const size_t nv = (size_t)S->n * 3;
+  for (int i = 0; i < 3; ++i) {
+    int rc = sys_alloc(S, &S->scratch[i], nv);
+    if (rc) return rc;
+  }
+  return QN_OK;
+}
+
 // copy between a caller buffer (host or device) and a device buffer
 int to_device(double* dst, const double* src, size_t count, int32_t mem, cudaStream_t st) {
   QN_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double),
@@ -839,6 +851,12 @@ int qn_system_amg_info(qn_system* S, int64_t* out, int64_t cap) {
   return QN_OK;
 }
 
+int qn_system_set_fault(qn_system* S, int32_t mode, int32_t iteration) {
+  QN_REQUIRE(S && mode >= 0 && mode <= 2 && iteration >= 1 && iteration < (1 << 20), QN_ERR_ARG, "set_fault: args");
+  S->fault = mode ? (mode | (iteration << 4)) : 0;
+  return QN_OK;
+}
+
 int qn_system_set_timeline(qn_system* S, int32_t enable) {
   QN_REQUIRE(S, QN_ERR_ARG, "null");
   const size_t cnt = (size_t)qn::kTimelinePasses * qn::kTimelineKernels * 2;
@@ -977,10 +995,23 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   QN_REQUIRE(cfg->lbfgs_init != 2 || cfg->kind != 1 || (S->v.hrest_inv && S->n_inst == 1), QN_ERR_ARG,
              "frame_step: rest_pose_hessian needs qn_system_rest_hessian first (single instance)");
   c.lbfgs_init = cfg->kind == 1 ? cfg->lbfgs_init : 0;
+  c.fault = S->fault;
   c.has_targets = fixed_targets != nullptr && S->n_fixed > 0;
   c.use_graph = S->use_graph ? 1 : 0;
-  // at most 41 trials per line search + one re-evaluation per iteration, plus slack
-  c.max_passes = 64 * cfg->iterations + 64;
+  // Runaway guard: the line search (solvers.py:241-257) shrinks alpha from
+  // alpha_init until it accepts or alpha < 1e-12, so one iteration takes at most
+  // ceil(log(1e-12 / alpha_init) / log(shrink)) + 1 trials plus one
+  // re-evaluation pass; the bound follows the configured alpha_init / shrink.
+  QN_REQUIRE(!(cfg->line_search && cfg->alpha_shrink >= 1.0 && cfg->alpha_init >= 1e-12), QN_ERR_UNSUPPORTED,
+             "frame_step: alpha_shrink >= 1 never reaches the step floor (the line search cannot terminate)");
+  {
+    double trials = 1.0;
+    if (cfg->line_search && cfg->alpha_shrink > 0.0 && cfg->alpha_init >= 1e-12)
+      trials = std::ceil(std::log(1e-12 / cfg->alpha_init) / std::log(cfg->alpha_shrink)) + 1.0;
+    const double bound = (double)cfg->iterations * (std::max(trials, 1.0) + 2.0) + 64.0;
+    QN_REQUIRE(bound < 2.0e9, QN_ERR_UNSUPPORTED, "frame_step: line-search trial bound too large");
+    c.max_passes = (int32_t)bound;
+  }
   QN_CUDA(cudaMemcpyAsync(S->d_cfg, &c, sizeof(DevConfig), cudaMemcpyHostToDevice, st));
   if (c.has_targets) {
     rc = stage_in(S, S->d_targets, fixed_targets, (size_t)S->n_inst * S->n_fixed * 3, mem, st);
@@ -1101,12 +1132,13 @@ int qn_simulate_frame(qn_system* S, const qn_solver_config* cfg, const double* q
 int qn_system_objective(qn_system* S, const double* x, const double* y, double* g_out, double* grad_out, int32_t mem,
                         void* stream) {
   QN_REQUIRE(S && x && y && g_out, QN_ERR_ARG, "objective: null");
-  cudaStream_t st = S->stream;
-  (void)stream;
+  // in order on the caller's stream (device inputs are ready there); scratch is
+  // the system's own, so nothing is allocated or leaked per call
+  cudaStream_t st = pick(S, stream);
   const size_t nv = (size_t)S->n * 3;
-  double *dx = nullptr, *dy = nullptr, *dg = nullptr;
   int rc;
-  if ((rc = dev_alloc(&dx, nv)) || (rc = dev_alloc(&dy, nv)) || (rc = dev_alloc(&dg, nv))) return rc;
+  if ((rc = ensure_scratch(S))) return rc;
+  double *dx = S->scratch[0], *dy = S->scratch[1], *dg = S->scratch[2];
   const SysView& v = S->v;
   std::vector<double> pt(v.nblk_t), pv(v.nblk_v);
   for (int64_t b = 0; b < S->n_inst; ++b) {
@@ -1124,26 +1156,23 @@ int qn_system_objective(qn_system* S, const double* x, const double* y, double* 
     for (double p : pv) in += p;
     const double gv = (0.5 / (S->h * S->h)) * in + e;
     if (mem == QN_MEM_DEVICE) {
-      QN_CUDA(cudaMemcpy(g_out + b, &gv, sizeof(double), cudaMemcpyHostToDevice));
+      QN_CUDA(cudaMemcpyAsync(g_out + b, &gv, sizeof(double), cudaMemcpyHostToDevice, st));
+      QN_CUDA(cudaStreamSynchronize(st));
     } else {
       g_out[b] = gv;
     }
   }
-  cudaFree(dx);
-  cudaFree(dy);
-  cudaFree(dg);
   return QN_OK;
 }
 
 int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x, double* energy, double* grad_accum,
                        int32_t mem, void* stream) {
   QN_REQUIRE(S && x && energy && inst >= 0 && inst < S->n_inst && mat < S->n_mat, QN_ERR_ARG, "elements: args");
-  cudaStream_t st = S->stream;
-  (void)stream;
+  cudaStream_t st = pick(S, stream);
   const size_t nv = (size_t)S->n * 3;
-  double *dx = nullptr, *dg = nullptr;
   int rc;
-  if ((rc = dev_alloc(&dx, nv)) || (rc = dev_alloc(&dg, nv))) return rc;
+  if ((rc = ensure_scratch(S))) return rc;
+  double *dx = S->scratch[0], *dg = S->scratch[2];
   const SysView& v = S->v;
   if ((rc = to_device(dx, x, nv, mem, st))) return rc;
   if ((rc = launch_tet_plain(S, dx, (int)inst, (int)mat, S->d_part_plain, st))) return rc;
@@ -1159,12 +1188,11 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
   double e = 0.0;
   for (double p : pt) e += p;
   if (mem == QN_MEM_DEVICE) {
-    QN_CUDA(cudaMemcpy(energy, &e, sizeof(double), cudaMemcpyHostToDevice));
+    QN_CUDA(cudaMemcpyAsync(energy, &e, sizeof(double), cudaMemcpyHostToDevice, st));
+    QN_CUDA(cudaStreamSynchronize(st));
   } else {
     *energy = e;
   }
-  cudaFree(dx);
-  cudaFree(dg);
   return QN_OK;
 }
 

@@ -497,8 +497,15 @@ __global__ void __launch_bounds__(kVTB) k_vec(SysView v) {
           const double xhat = __dadd_rn(x, d);
           d = __dsub_rn(__dadd_rn(__dmul_rn(cc->omega, __dsub_rn(xhat, xkm1)), xkm1), x);
         }
-        v.D[oc] = d;
+        double ds = d;  // step direction (differs from d only under test fault injection)
+        const int fault = v.cfg->fault;
+        if (fault && cc->k + 1 >= (fault >> 4)) {  // cc->k = iterations recorded so far
+          if ((fault & 15) == 1) d = ds = -d;  // ascent
+          else ds = -d;                        // steps that only increase g: stagnation
+        }
+        v.D[oc] = ds;
         acc[1] = v.Gr[vec_off(v, cc->gs_cur, b) + ci] * d;
+        d = ds;
       } else {
         d = v.D[oc];
       }

@@ -96,7 +96,7 @@ struct DevConfig {
   double gamma, alpha_init, shrink, grad_tol;
   int32_t has_targets, use_graph, max_passes, cheb_S;
   double cheb_rho;
-  int32_t lbfgs_init, pad2;
+  int32_t lbfgs_init, fault;  // fault: test-only injection, mode | (first iteration << 4)
 };
 
 struct SysView {
@@ -205,6 +205,7 @@ struct qn_system {
   size_t h_stage_bytes = 0;
   // graph
   bool use_graph = true;
+  int32_t fault = 0;  // qn_system_set_fault
   int graph_m_bound = 0;  // history bound the captured graph's kernels are specialised on
   int graph_init = 0;     // lbfgs_init the captured graph's direction step was built for
   cudaGraph_t graph = nullptr;
@@ -215,6 +216,7 @@ struct qn_system {
   int64_t kernels_per_pass = 0, kernels_per_cg = 0;  // kernel nodes of the captured frame graph
   // element-seam workspace
   double* d_part_plain = nullptr;
+  double* scratch[3] = {nullptr, nullptr, nullptr};  // n x 3 vectors of the objective / elements seams
   std::vector<int32_t> h_tet_mat;
   // AMG (host copy of the level table, for launch sizes and diagnostics)
   std::vector<qn::AmgDevLevel> h_alev;

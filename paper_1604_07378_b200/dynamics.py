@@ -138,7 +138,10 @@ class TorusCollider:
 
 @dataclass
 class SimState:
-    """dynamics.py:314-329 (collisions are out of scope: always empty)."""
+    """dynamics.py:314-329.  `collisions` is the active contact set of the
+    reference's host loop (CollisionSet: idx / t / n); the frame graph rebuilds
+    its own set on the device (k_col), so only the objective / gradient seams
+    look at this field (they refuse a non-empty set, see _objective_gradient)."""
 
     q_l: np.ndarray
     q_prev: np.ndarray
@@ -189,6 +192,11 @@ class SimSystem:
             raise DynamicsError(f"precision {precision!r}: fp64 | fp32")
         _lib.check(_lib.load().qn_system_set_precision(self._h, 1 if precision == "fp32" else 0), "set_precision")
         self.precision = precision
+
+    def set_fault(self, mode: int, iteration: int = 1):
+        """Test-only fault injection into the device line search (qn_system_set_fault):
+        0 off, 1 ascent direction, 2 steps that only increase g (stagnation)."""
+        _lib.check(_lib.load().qn_system_set_fault(self._h, int(mode), int(iteration)))
 
     def set_graph_mode(self, on: bool):
         _lib.check(_lib.load().qn_system_set_graph_mode(self._h, 1 if on else 0))
@@ -510,6 +518,13 @@ def inertia_target(state: SimState, system: SimSystem, fixed_targets=None) -> np
 
 
 def _objective_gradient(system: SimSystem, state: SimState, x, want_grad: bool):
+    cons = getattr(state, "collisions", None)
+    if cons is not None and int(getattr(cons, "count", len(getattr(cons, "idx", ())))) > 0:
+        # dynamics.py:464-467,475 add w_col * depth^2 terms for the active set; the
+        # device seam evaluates inertia + elastic only, so a non-empty set would
+        # silently differ from the reference
+        raise NotImplementedError("objective/gradient seam: non-empty state.collisions (the contact penalty is "
+                                  "evaluated inside simulate_frame's graph, not by this seam)")
     x = _lib.f64(x)
     y = _lib.f64(state.y)
     g = np.empty(system.n_inst)

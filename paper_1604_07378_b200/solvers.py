@@ -4,10 +4,14 @@ qnsim.solvers, solvers.py:1-407).
 `simulate_frame` keeps the reference signature and return types
 (solvers.py:260-352); the whole frame — inertia target, L-BFGS two-loop with
 the prefactored A as H0, Armijo backtracking, early-outs, stagnation — runs as
-one CUDA-graph launch (`qn_frame_step`).  Supported: kind "pd_qn" and
-"lbfgs" (lbfgs_init="system_matrix"), with or without line search.  Chebyshev,
-Newton and the other L-BFGS initialisations are out of the hot-path scope
- and raise NotImplementedError.
+one CUDA-graph launch (`qn_frame_step`).  Every solver kind and L-BFGS
+initialisation of solvers.py:25-27 is supported: "pd_qn", "lbfgs" (all three
+`lbfgs_init`s) and "chebyshev" run in the device frame graph; "newton" (and
+`newton_reference`, the minima for `relative_error`) runs its frame control on
+the host like the reference, with per-element Hessian blocks and assembly on
+the device and the dense Cholesky by cuSOLVER.  Device-side limits: m <=
+QN_MAX_M, alpha_shrink < 1 with a line search (the reference would loop
+forever without acceptance), newton without colliders / on single instances.
 """
 
 from __future__ import annotations
@@ -69,6 +73,10 @@ class SolverConfig:
 
         if self.m > _lib.QN_MAX_M:
             raise NotImplementedError(f"history window m > {_lib.QN_MAX_M}")
+        if self.line_search and self.alpha_shrink >= 1.0 and self.alpha_init >= ALPHA_FLOOR:
+            # solvers.py:247-252 never reaches the floor: the reference loops until
+            # some trial is accepted; the device frame needs a bounded pass count
+            raise SolverError(f"alpha_shrink must be < 1 with a line search, got {self.alpha_shrink}")
         c = _lib.SolverConfigC()
         c.kind = {"pd_qn": 0, "lbfgs": 1, "chebyshev": 2}[self.kind]
         c.rho, c.S = float(self.rho), int(self.S)

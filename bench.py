@@ -166,7 +166,13 @@ FP64_PEAK_TFLOPS = 34.37  # DFMA microbenchmark on this pool's B200 (tools/probe
 # fp64 flops per tet eval (2 DFMA + DMUL + DADD) from ncu sass counters of the per-tet kernel
 # (smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum / tets), per workload because the
 # material (and the SVD sweep count of the state) changes the count: profiles/r0*_fp64_flops*.txt
-FLOPS_PER_TET = {"c2": (1388.0, "ncu sass counters, c2 StVK (profiles/r01_fp64_flops.txt)")}
+FLOPS_PER_TET = {
+    "c1": (1478.0, "ncu sass counters, c1 Neo-Hookean after 3 frames (profiles/r02_fp64_flops.txt)"),
+    "c2": (1388.0, "ncu sass counters, c2 StVK (profiles/r01_fp64_flops.txt)"),
+    "c3": (1533.0, "ncu sass counters, c3 Hermite splines after 3 frames (profiles/r02_fp64_flops.txt)"),
+    "c4": (1466.0, "ncu sass counters, c4 1024 x Neo-Hookean after 3 frames (profiles/r02_fp64_flops.txt)"),
+    "c5": (1418.0, "ncu sass counters, c5 poly + log material on a 100x25x25 bar (profiles/r02_fp64_flops.txt)"),
+}
 
 
 def tet_fp64(sc, tets, tet_ms):

@@ -9,7 +9,8 @@ Differences from the reference, all deliberate and documented in DESIGN.md:
 * the prefactored solve can use a sparse LU (`factor="sparse"`) in place of the
   dense `cho_factor` of `linalg.py:31` / `dynamics.py:413` (dense is O(n^2)
   memory, infeasible beyond configs[1]); `factor="dense"` restates the
-  reference exactly;
+  reference exactly; for configs[4] (12 M dofs, sparse LU infeasible too)
+  `factor="cg"` solves with Jacobi-PCG to 1e-13 (oracle/cg_free.c, SURVEY §8c);
 * the harness-side scenario parsing, PD materials, Chebyshev and Newton are
   out of the hot-path scope and not restated; colliders
   (§8f row f2) are restated below.
@@ -482,7 +483,12 @@ def build_springs(verts, edges, rest, faces, density, k, h, gravity, fixed, fact
     free = np.nonzero(mask)[0]
     A = (L + scipy.sparse.diags(masses / h ** 2)).tocsr()
     A_free = A[free][:, free].tocsr()
-    fac = DenseFactor(A_free.toarray()) if factor == "dense" else SparseFactor(A_free)
+    if factor == "dense":
+        fac = DenseFactor(A_free.toarray())
+    elif factor == "cg":                                           # configs[4]
+        fac = CGFactor(A_free, tol=cg_tol)
+    else:
+        fac = SparseFactor(A_free)
     bbox = verts.max(axis=0) - verts.min(axis=0)
     w_col = float(collision_weight) if collision_weight is not None else 10.0 * float(k)
     return System(verts, np.asarray(edges), masses, float(h), np.asarray(gravity, dtype=np.float64), [grp],
@@ -516,6 +522,61 @@ class SparseFactor:
         return self.lu.solve(np.asarray(B, dtype=np.float64))
 
 
+_CG_LIB = None
+
+
+def cg_lib():
+    """ctypes handle of oracle/cg_free.c (built by __graft_entry__.build(), or here
+    on first use)."""
+    global _CG_LIB
+    if _CG_LIB is None:
+        import ctypes as C
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        so = os.path.join(here, "_build", "libcg_free.so")
+        src = os.path.join(here, "cg_free.c")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            os.makedirs(os.path.dirname(so), exist_ok=True)
+            subprocess.run(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-o", so, src, "-lm"], check=True)
+        lib = C.CDLL(so)
+        P = C.c_void_p
+        lib.oracle_cg3.argtypes = [C.c_int64, P, P, P, P, P, C.c_double, C.c_int32, P, P]
+        lib.oracle_cg3.restype = C.c_int
+        _CG_LIB = lib
+    return _CG_LIB
+
+
+class CGFactor:
+    """SURVEY §8c's configs[4] restatement of `sysfact` (linalg.py:57-59): the
+    dense Cholesky of A_free is infeasible at 12 M dofs, so `solve` runs
+    Jacobi-preconditioned CG per coordinate (oracle/cg_free.c) to a relative
+    residual of `tol` (1e-13, three orders tighter than the GPU's 1e-10)."""
+
+    def __init__(self, A, tol=1e-13, maxit=20000):
+        A = scipy.sparse.csr_matrix(A)
+        A.sort_indices()
+        self.n = A.shape[0]
+        self.ptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        self.idx = np.ascontiguousarray(A.indices, dtype=np.int32)
+        self.val = np.ascontiguousarray(A.data, dtype=np.float64)
+        self.tol, self.maxit = float(tol), int(maxit)
+        self.log = []  # (iterations per column, true relative residual per column) per solve
+
+    def solve(self, B):
+        B = np.ascontiguousarray(B, dtype=np.float64).reshape(self.n, 3)
+        X = np.empty_like(B)
+        its = np.zeros(3, dtype=np.int32)
+        res = np.zeros(3)
+        rc = cg_lib().oracle_cg3(self.n, self.ptr.ctypes.data, self.idx.ctypes.data, self.val.ctypes.data,
+                                 B.ctypes.data, X.ctypes.data, self.tol, self.maxit, its.ctypes.data,
+                                 res.ctypes.data)
+        self.log.append((its.tolist(), res.tolist()))
+        if rc:
+            raise OracleError(f"CG did not reach {self.tol} in {self.maxit} iterations: {res}")
+        return X
+
+
 @dataclass
 class System:
     verts: np.ndarray
@@ -539,7 +600,7 @@ class System:
 
 
 def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), factor="sparse",
-          masses=None, colliders=(), collision_weight=None, aniso=None):
+          masses=None, colliders=(), collision_weight=None, aniso=None, cg_tol=1e-13):
     """Restates dynamics.build_system (dynamics.py:351-434) for VL tet groups.
 
     `materials` is a VLMaterial (all tets) or a list of (tet_index_array, VLMaterial).
@@ -581,7 +642,12 @@ def build(verts, tets, density, materials, h, gravity, fixed, fit=(0.5, 1.5), fa
     free = np.nonzero(mask)[0]
     A = (L + scipy.sparse.diags(masses / h ** 2)).tocsr()          # dynamics.py:413
     A_free = A[free][:, free].tocsr()
-    fac = DenseFactor(A_free.toarray()) if factor == "dense" else SparseFactor(A_free)
+    if factor == "dense":
+        fac = DenseFactor(A_free.toarray())
+    elif factor == "cg":                                           # configs[4]
+        fac = CGFactor(A_free, tol=cg_tol)
+    else:
+        fac = SparseFactor(A_free)
     bbox = verts.max(axis=0) - verts.min(axis=0)
     scale = float(np.linalg.norm(bbox)) or 1.0                     # dynamics.py:416-417
     max_w = max((float((g.vols * g.k).max()) for g in groups if g.vols.size), default=0.0)

@@ -473,7 +473,15 @@ def build_system(mesh, materials, h: float = DEFAULT_TIMESTEP, gravity=DEFAULT_G
     solver="pcg" solves every direction with Jacobi-preconditioned CG to
     ||r|| <= pcg_tol ||b|| (configs[4]: meshes too large to factor);
     solver="amg" uses CG preconditioned by a smoothed-aggregation AMG V-cycle
-    (same tolerance, ~40x fewer iterations on configs[4])."""
+    (same tolerance, ~40x fewer iterations on configs[4]).
+
+    Inputs may be the reference's own objects (qnsim TetMesh / SpringNetwork,
+    MaterialModel / PDMaterial, FitInterval, colliders): they are converted by
+    `adopt` so that `qnsim.harness.build_system` can be swapped for this one."""
+    from paper_1604_07378_b200 import adopt
+    mesh, materials = adopt.mesh(mesh), adopt.materials(materials)
+    fit_interval = adopt.fit_interval(fit_interval)
+    colliders = [adopt.collider(c) for c in (colliders or ())]
     if isinstance(mesh, SpringNetwork):
         if aniso:
             raise DynamicsError("anisotropy applies to tet meshes only")
@@ -494,7 +502,10 @@ def build_batch_system(mesh, materials_per_instance, h: float = DEFAULT_TIMESTEP
                        collision_weight: float | None = None) -> SimSystem:
     """configs[3]: independent instances of one mesh, one MaterialModel (or
     group assignment) per instance, each with its own factored A."""
-    inst = [_assign(mesh, m) for m in materials_per_instance]
+    from paper_1604_07378_b200 import adopt
+    mesh, fit_interval = adopt.mesh(mesh), adopt.fit_interval(fit_interval)
+    colliders = [adopt.collider(c) for c in (colliders or ())]
+    inst = [_assign(mesh, adopt.materials(m)) for m in materials_per_instance]
     if not inst:
         raise DynamicsError("empty batch")
     sizes = {len(a) for a in inst}

@@ -247,12 +247,22 @@ def _simulate_frame_newton(system, state, config, fixed_targets):
     return SimState(q_l=x, q_prev=np.asarray(state.q_l), y=y), rec
 
 
+def as_config(config) -> SolverConfig:
+    """This package's SolverConfig from any object with the reference's fields
+    (qnsim.solvers.SolverConfig, solvers.py:43-68), validated the same way."""
+    if config is None or isinstance(config, SolverConfig):
+        return config
+    return SolverConfig(kind=config.kind, iterations=config.iterations, m=config.m, gamma=config.gamma,
+                        alpha_init=config.alpha_init, alpha_shrink=config.alpha_shrink, rho=config.rho, S=config.S,
+                        lbfgs_init=config.lbfgs_init, line_search=config.line_search)
+
+
 def newton_reference(system: SimSystem, state: SimState, fixed_targets=None, grad_tol_rel: float = 1e-10,
                      max_iterations: int = 200, config: SolverConfig | None = None):
     """solvers.py:355-398: the frame solved to (near) optimality with Newton;
     returns (x*, g*), the reference minimum for relative errors."""
     from paper_1604_07378_b200.dynamics import gradient, inertia_target, objective
-    config = config or SolverConfig(kind="newton", iterations=1)
+    config = as_config(config) or SolverConfig(kind="newton", iterations=1)
     y = inertia_target(state, system, fixed_targets)
     st = SimState(q_l=state.q_l, q_prev=state.q_prev, y=y)
     x = y.copy()
@@ -304,7 +314,9 @@ def simulate_frame(system: SimSystem, state: SimState, config: SolverConfig, fix
     """Advance one frame; returns (next_state, ConvergenceRecord) — a list of
     records for batch systems (solvers.py:260-352).  `out` (optional, not in
     the reference signature): a SimState whose q_l / y arrays (float64,
-    C-contiguous, e.g. page-locked) receive x and y instead of new arrays."""
+    C-contiguous, e.g. page-locked) receive x and y instead of new arrays.
+    `config` may be the reference's own SolverConfig (same fields)."""
+    config = as_config(config)
     if config.kind == "newton":
         return _simulate_frame_newton(system, state, config, fixed_targets)
     _prepare(system, config)
@@ -340,6 +352,7 @@ class ResidentRun:
     path of bench.py.  `last_ms` is the CUDA-event time of the last frame."""
 
     def __init__(self, system: SimSystem, state: SimState, config: SolverConfig):
+        config = as_config(config)
         self.system, self.config = system, config
         _prepare(system, config)
         self._cfg = config.to_c()

@@ -1,7 +1,7 @@
 """Generate golden vectors from the UNMODIFIED reference (run in the build
 container, where /root/reference exists; the GPU box never runs this).
 
-    python tests/golden/make_golden.py [--quick] [--colliders | --arap | --chebyshev | --cloth | --aniso | --writers | --newton (only those fixtures)]
+    python tests/golden/make_golden.py [--quick] [--c4 | --colliders | --arap | --chebyshev | --cloth | --aniso | --writers | --newton (only those fixtures)]
 
 Writes tests/golden/*.npz and copies the reference's own golden trajectories
 (pkg/frontend/tests/fixtures/twist_{lbfgs,pd_qn}.csv) plus the bar_small asset
@@ -122,6 +122,30 @@ def run_reference(sc, mat_spec, frames, iterations, kind="lbfgs", save_frames=()
         if f in save_frames:
             pos[f"x_{f}"] = state.q_l.copy()
     return dict(g=np.array(g), trials=np.array(tr), alphas=np.array(al), g0=np.array(g0), **pos)
+
+
+def c4_spread_instances():
+    """40 of the 1024 configs[3] instances: both ends of every 1/2/4/8-rank shard
+    (shard_instances) plus evenly spread ones (>= 32 instances spread
+    across ranks)."""
+    ends = [r * 128 + o for r in range(8) for o in (0, 127)]
+    spread = np.linspace(0, 1023, 24).round().astype(int).tolist()
+    return sorted(set(ends + spread))
+
+
+def gen_c4_spread(frames=10):
+    t = time.time()
+    sc4 = scenes.c4(instances=1024)
+    keep = c4_spread_instances()
+    out = {"instances": np.array(keep), "frames": frames}
+    q_l, q_prev = sc4.q_l[0].copy(), sc4.q_prev[0].copy()
+    for b in keep:
+        sc4.q_l, sc4.q_prev = q_l, q_prev
+        d = run_reference(sc4, sc4.batch_materials[b], frames, sc4.iterations, save_frames={frames - 1})
+        for k, v in d.items():
+            out[f"i{b}_{k}"] = v
+    np.savez_compressed(os.path.join(HERE, "frames_c4_spread.npz"), **out)
+    print("c4 spread", len(keep), "instances", time.time() - t)
 
 
 def gen_frames(quick):
@@ -428,6 +452,9 @@ def copy_fixtures():
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
     copy_fixtures()
+    if "--c4" in sys.argv:
+        gen_c4_spread()
+        sys.exit(0)
     if "--colliders" in sys.argv:
         gen_colliders()
         sys.exit(0)

@@ -143,6 +143,32 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
 }
 }
 
+// Symbolic structure of the host factor (diagnostics / kernel design):
+// sup[s] = {parent, col0, nc, nr, is_top}, sizes[] = {n, nsup, ktop, nvals, n_ftask, n_btask, nnz_l}.
+// Call with sup == nullptr first to get nsup.
+extern "C" int hc_factor_structure(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,
+                                   const double* coords, int64_t* sizes, int32_t* sup, int64_t cap) {
+  qn_factor f;
+  int rc = qn::factor_build_host(&f, n, indptr, indices, values, 1, coords);
+  if (rc) return rc;
+  sizes[0] = f.n;
+  sizes[1] = f.nsup;
+  sizes[2] = f.ktop;
+  sizes[3] = f.nvals;
+  sizes[4] = (int64_t)f.ftask.size();
+  sizes[5] = (int64_t)f.btask.size();
+  sizes[6] = f.nnz_l;
+  if (!sup || cap < f.nsup) return 0;
+  for (int s = 0; s < f.nsup; ++s) {
+    sup[5 * s + 0] = f.parent[s];
+    sup[5 * s + 1] = f.sup_col[s];
+    sup[5 * s + 2] = f.sup_col[s + 1] - f.sup_col[s];
+    sup[5 * s + 3] = (int32_t)(f.sup_row_ptr[s + 1] - f.sup_row_ptr[s]);
+    sup[5 * s + 4] = f.is_top.empty() ? 0 : f.is_top[s];
+  }
+  return 0;
+}
+
 // ---- AMG hierarchy (qn_amg.cpp) + host reference PCG (TEST ONLY) ----
 #include "qn_amg.h"
 extern "C" int hc_amg_solve(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,

@@ -69,6 +69,9 @@ def main(cfg="c2", mode="plain"):
     print(cfg, mode, f.info())
     report("forward", st[:nf], tk[:nf])
     report("backward", st[nf:nf + nb], tk[nf:nf + nb])
+    import os
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.savez(f"gpurun_out/trace_{cfg}_{mode}.npz", st=st, tk=tk, nf=nf, nb=nb)
 
 
 if __name__ == "__main__":

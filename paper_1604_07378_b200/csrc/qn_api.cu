@@ -147,7 +147,22 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
   if (f->ktop > 0) {
-    if ((rc = dev_upload(&f->d_sinv, f->sinv.data(), f->sinv.size()))) return rc;
+    {  // S^-1 is symmetric: only the tiles (I, J), I >= J, are stored (half the bytes of the dense K x K)
+      const int64_t K = f->ktop, T = kTopTile, nt = (K + T - 1) / T;
+      f->tnt = (int32_t)nt;
+      std::vector<double> tiles((size_t)(nt * (nt + 1) / 2) * T * T, 0.0);
+      for (int64_t I = 0; I < nt; ++I)
+        for (int64_t J = 0; J <= I; ++J) {
+          double* t = tiles.data() + (size_t)(I * (I + 1) / 2 + J) * T * T;
+          for (int64_t j = 0; j < T && J * T + j < K; ++j)
+            for (int64_t i = 0; i < T && I * T + i < K; ++i)
+              t[i + j * T] = f->sinv[(size_t)(I * T + i) + (size_t)(J * T + j) * K];
+        }
+      if ((rc = dev_upload(&f->d_stile, tiles.data(), tiles.size()))) return rc;
+      if ((rc = dev_alloc(&f->d_tpart, (size_t)f->nbatch * nt * nt * T * 3))) return rc;
+      std::vector<unsigned> zero((size_t)f->nbatch * nt, 0u);
+      if ((rc = dev_upload(&f->d_tcnt, zero.data(), zero.size()))) return rc;
+    }
     if ((rc = dev_upload(&f->d_tcols, f->tcols.data(), f->tcols.size()))) return rc;
     if ((rc = dev_upload(&f->d_tg_ptr, f->tg_ptr.data(), f->tg_ptr.size()))) return rc;
     if ((rc = dev_upload(&f->d_tg_idx, f->tg_idx.data(), f->tg_idx.size()))) return rc;
@@ -188,9 +203,9 @@ void factor_free_device(qn_factor* f) {
                   f->d_perm,    f->d_vals,        f->d_y,         f->d_x,         f->d_u,
                   f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
-                  f->d_fdep_idx, f->d_sinv,       f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
+                  f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
-                  f->d_fdesc,   f->d_fblob,       f->d_bdesc};
+                  f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

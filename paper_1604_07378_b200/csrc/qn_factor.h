@@ -106,7 +106,10 @@ struct qn_factor {
   int32_t* d_dlev_ptr = nullptr;
   int32_t* d_dlev_sup = nullptr;
   unsigned* d_flags = nullptr;    // nbatch x (n_ftask + n_btask) completion epochs
-  double* d_sinv = nullptr;
+  double* d_stile = nullptr;      // S^-1 as packed lower-triangle tiles (kTopTile^2 each, tile (I,J), I >= J)
+  double* d_tpart = nullptr;      // nbatch x nt x nt x kTopTile x 3 partial products of the symmetric top apply
+  unsigned* d_tcnt = nullptr;     // nbatch x nt arrival counters of the partials per row block
+  int32_t tnt = 0;                // row blocks of the top (ceil(K / kTopTile))
   int32_t* d_tcols = nullptr;
   int32_t* d_tg_ptr = nullptr;
   int32_t* d_tg_idx = nullptr;
@@ -127,7 +130,8 @@ struct qn_factor {
 
 namespace qn {
 constexpr int64_t kTaskEntries = 8192;  // Z entries per solve task (64 KB shared-memory tile)
-constexpr int64_t kTopMax = 4096;       // max columns of the dense top block (S^-1 <= 134 MB)
+constexpr int64_t kTopMax = 4096;
+constexpr int kTopTile = 64;            // symmetric top apply: S^-1 stored as 64 x 64 lower-triangle tiles       // max columns of the dense top block (S^-1 <= 134 MB)
 constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
 constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
 constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task

@@ -61,7 +61,10 @@ struct FactorView {
   unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
   unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
-  const double* sinv;        // K x K symmetric
+  const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
+  double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
+  unsigned* tcnt;            // [nbatch][nt] arrivals per row block
+  int32_t tnt;
   const int32_t* tcols;
   const int32_t* tg_ptr;
   const int32_t* tg_idx;
@@ -113,7 +116,10 @@ inline FactorView factor_view(const qn_factor* f) {
   v.sched = f->d_sched;
   v.trace = f->d_trace;
   v.ktop = f->ktop;
-  v.sinv = f->d_sinv;
+  v.stile = f->d_stile;
+  v.tpart = f->d_tpart;
+  v.tcnt = f->d_tcnt;
+  v.tnt = f->tnt;
   v.tcols = f->d_tcols;
   v.tg_ptr = f->d_tg_ptr;
   v.tg_idx = f->d_tg_idx;
@@ -349,16 +355,20 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   cp_async_wait_all();
   __syncthreads();
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
-  // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j) ----
+  // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
+  // a tile of R < 32 rows (wide supernodes) also splits each warp's k-slice
+  // over L = 32 / R lane groups (lane = sub R + row), so every lane works ----
   const int ks = kSolveWarps / rg;
   const int g = warp / ks, j = warp % ks;
   const int per = (kmax + ks - 1) / ks;
   const int kb = j * per, ke = min(kmax, kb + per);
-  const int rl = 32 * g + lane;
+  const int L = R < 32 ? 32 / R : 1;  // rg == 1 whenever R < 32
+  const int sub = R < 32 ? lane / R : 0;
+  const int rl = R < 32 ? lane - sub * R : 32 * g + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  if (g < rg && rl < R) {
+  if (g < rg && rl < R && sub < L) {
 #pragma unroll 8
-    for (int k = kb; k < ke; ++k) {
+    for (int k = kb + sub; k < ke; k += L) {
       const double l = zt[k * R + rl];
       a0 = fma(l, f[3 * k + 0], a0);
       a1 = fma(l, f[3 * k + 1], a1);
@@ -372,12 +382,13 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   if (threadIdx.x < R) {
     const int gg = threadIdx.x >> 5;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-    for (int jj = 0; jj < ks; ++jj) {
-      const int t = (gg * ks + jj) * 32 + lane;
-      v0 += part[3 * t + 0];
-      v1 += part[3 * t + 1];
-      v2 += part[3 * t + 2];
-    }
+    for (int jj = 0; jj < ks; ++jj)
+      for (int q = 0; q < L; ++q) {  // fixed order: k-slice, then lane group
+        const int t = (gg * ks + jj) * 32 + (R < 32 ? q * R + (int)threadIdx.x : lane);
+        v0 += part[3 * t + 0];
+        v1 += part[3 * t + 1];
+        v2 += part[3 * t + 2];
+      }
     if (rr < nc) {
       double* yg = F.y + ((size_t)b * F.n + c0 + rr) * 3;
       yg[0] = v0;
@@ -440,16 +451,43 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   trace_mark(F.trace, tb + 1);
   cp_async_wait_all();
   __syncthreads();
-  // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
+  // ---- before the parent is done: the y_J part of every column, 4 columns per warp.
+  // Fewer than kSolveWarps column quads (tall fronts, few columns per task):
+  // each quad's rows are split over rs warps and the slices summed in order ----
   const int ncols = k1 - k0;
-  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-    double a[3];
-    const int j = lane >> 3;
-    col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
-    if ((lane & 7) == 0 && kl + j < ncols) {
-      pre[3 * (kl + j) + 0] = a[0];
-      pre[3 * (kl + j) + 1] = a[1];
-      pre[3 * (kl + j) + 2] = a[2];
+  const int nquads = (ncols + 3) / 4;
+  const int rs = nquads >= kSolveWarps ? 1 : kSolveWarps / nquads;
+  __shared__ double slp[kSolveWarps][4][3];
+  if (rs > 1) {
+    const int quad = warp / rs, slice = warp % rs, kl = 4 * quad;
+    double a[3] = {0.0, 0.0, 0.0};
+    if (quad < nquads) {
+      const int r0 = k0 + kl, len = nc - r0, per = (len + rs - 1) / rs;
+      const int ra = r0 + slice * per, rb = min(nc, ra + per);
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), ra, max(ra, rb), lane, a);
+    }
+    if ((lane & 7) == 0) {
+      slp[warp][lane >> 3][0] = a[0];
+      slp[warp][lane >> 3][1] = a[1];
+      slp[warp][lane >> 3][2] = a[2];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < 3 * ncols) {
+      const int c = threadIdx.x / 3, q = threadIdx.x - 3 * c;
+      double v = 0.0;
+      for (int sl = 0; sl < rs; ++sl) v += slp[(c >> 2) * rs + sl][c & 3][q];
+      pre[threadIdx.x] = v;
+    }
+  } else {
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        pre[3 * (kl + j) + 0] = a[0];
+        pre[3 * (kl + j) + 1] = a[1];
+        pre[3 * (kl + j) + 2] = a[2];
+      }
     }
   }
   if (d.nwait > 0)
@@ -466,22 +504,56 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   __syncthreads();
   trace_clock(F.trace, tb + 4);
   // ---- the -x_below part, plus the staged y_J part ----
-  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-    double a[3];
-    const int j = lane >> 3;
-    col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
-    if ((lane & 7) == 0 && kl + j < ncols) {
-      const int k = k0 + kl + j;
-      const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
-                           a[2] + pre[3 * (kl + j) + 2]};
-      double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
+  if (rs > 1) {
+    const int quad = warp / rs, slice = warp % rs, kl = 4 * quad;
+    double a[3] = {0.0, 0.0, 0.0};
+    if (quad < nquads) {
+      const int len = nr - nc, per = (len + rs - 1) / rs;
+      const int ra = nc + slice * per, rb = min(nr, ra + per);
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), ra, max(ra, rb), lane, a);
+    }
+    __syncthreads();  // the y_J pass's slp reads are done
+    if ((lane & 7) == 0) {
+      slp[warp][lane >> 3][0] = a[0];
+      slp[warp][lane >> 3][1] = a[1];
+      slp[warp][lane >> 3][2] = a[2];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < ncols) {
+      const int c = threadIdx.x;
+      double v[3];
+      for (int q = 0; q < 3; ++q) {
+        double t = 0.0;
+        for (int sl = 0; sl < rs; ++sl) t += slp[(c >> 2) * rs + sl][c & 3][q];
+        v[q] = t + pre[3 * c + q];
+      }
+      double* xo = F.x + ((size_t)b * F.n + c0 + k0 + c) * 3;
       xo[0] = v[0];
       xo[1] = v[1];
       xo[2] = v[2];
-      double* d = sdst[kl + j];
+      double* d = sdst[c];
       d[0] = v[0];
       d[1] = v[1];
       d[2] = v[2];
+    }
+  } else {
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        const int k = k0 + kl + j;
+        const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
+                             a[2] + pre[3 * (kl + j) + 2]};
+        double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
+        xo[0] = v[0];
+        xo[1] = v[1];
+        xo[2] = v[2];
+        double* d = sdst[kl + j];
+        d[0] = v[0];
+        d[1] = v[1];
+        d[2] = v[2];
+      }
     }
   }
   trace_clock(F.trace, tb + 5);
@@ -576,54 +648,120 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_gather(FactorView F,
   g[2] = v[2] - a2;
 }
 
-// x_T = S^-1 g_T: warp per row k; row k of the symmetric S^-1 is its contiguous
-// column k, so every lane streams its share with 8 loads in flight.
+// x_T = S^-1 g_T with the symmetric S^-1 read once from half storage: CTA per
+// lower-triangle tile (I, J) (64 x 64, column-major, staged in shared memory)
+// computes the row-block product S_IJ g_J (-> block I) and, off the diagonal,
+// the transposed product S_IJ^T g_I (-> block J).  Each row block receives
+// exactly nt partials (slot = the other block index); the CTA that delivers the
+// last one (arrival counter) sums them in slot order — a fixed order, so the
+// result is bitwise reproducible — and writes x_T.  Half the bytes of the
+// dense K x K product (c3: 62 MB instead of 118 MB per solve).
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_apply(FactorView F, IO io) {
-  extern __shared__ double sg[];  // g_T (K x 3)
+__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_sym(FactorView F, IO io) {
+  constexpr int T = kTopTile, LD = T + 1, NQ = kSolveThreads / T;  // NQ = 4 column / row quarters
+  __shared__ double st[T * LD];
+  __shared__ double gI[T * 3], gJ[T * 3];
+  __shared__ double red[2][NQ][T * 3];
+  __shared__ int s_last[2];
   const int b = blockIdx.y;
   if (!io.active(b)) return;
-  const int K = F.ktop;
+  const int t = blockIdx.x;
+  int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  const int J = t - I * (I + 1) / 2;
+  const int K = F.ktop, nt = F.tnt;
+  {  // the tile: T*T doubles, kSolveThreads-strided (all loads issued before the stores)
+    const double* tile = F.stile + (size_t)t * T * T;
+    constexpr int PER = T * T / kSolveThreads;
+    double l[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) l[q] = __ldcs(tile + threadIdx.x + q * kSolveThreads);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * kSolveThreads;
+      st[(e % T) + (e / T) * LD] = l[q];
+    }
+  }
   const double* g = F.gtop + (size_t)b * K * 3;
-  for (int w = threadIdx.x; w < 3 * K; w += blockDim.x) sg[w] = __ldcg(g + w);
+  for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+    const int r = e / 3, c = e - 3 * r;
+    gI[e] = I * T + r < K ? __ldcg(g + 3 * (I * T + r) + c) : 0.0;
+    gJ[e] = J * T + r < K ? __ldcg(g + 3 * (J * T + r) + c) : 0.0;
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warp_global = blockIdx.x * kSolveWarps + (threadIdx.x >> 5);
-  const int nwarps = gridDim.x * kSolveWarps;
-  for (int k = warp_global; k < K; k += nwarps) {
-    const double* col = F.sinv + (size_t)k * K;
+  const int i = threadIdx.x % T, q = threadIdx.x / T;
+  {  // row i of S_IJ g_J over columns [q T/NQ, (q+1) T/NQ)
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    int c = lane;
-    for (; c + 224 < K; c += 256) {
-      double l[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) l[q] = __ldg(col + c + 32 * q);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int cc = c + 32 * q;
-        a0 = fma(l[q], sg[3 * cc + 0], a0);
-        a1 = fma(l[q], sg[3 * cc + 1], a1);
-        a2 = fma(l[q], sg[3 * cc + 2], a2);
-      }
+#pragma unroll 8
+    for (int j = q * (T / NQ); j < (q + 1) * (T / NQ); ++j) {
+      const double sv = st[i + j * LD];
+      a0 = fma(sv, gJ[3 * j + 0], a0);
+      a1 = fma(sv, gJ[3 * j + 1], a1);
+      a2 = fma(sv, gJ[3 * j + 2], a2);
     }
-    for (; c < K; c += 32) {
-      const double l = __ldg(col + c);
-      a0 = fma(l, sg[3 * c + 0], a0);
-      a1 = fma(l, sg[3 * c + 1], a1);
-      a2 = fma(l, sg[3 * c + 2], a2);
+    red[0][q][3 * i + 0] = a0;
+    red[0][q][3 * i + 1] = a1;
+    red[0][q][3 * i + 2] = a2;
+  }
+  if (I != J) {  // column i of S_IJ (= row i of S_JI) against g_I over rows [q T/NQ, (q+1) T/NQ)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 8
+    for (int r = q * (T / NQ); r < (q + 1) * (T / NQ); ++r) {
+      const double sv = st[r + i * LD];
+      a0 = fma(sv, gI[3 * r + 0], a0);
+      a1 = fma(sv, gI[3 * r + 1], a1);
+      a2 = fma(sv, gI[3 * r + 2], a2);
     }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    a2 = warp_sum(a2);
-    if (lane == 0) {
+    red[1][q][3 * i + 0] = a0;
+    red[1][q][3 * i + 1] = a1;
+    red[1][q][3 * i + 2] = a2;
+  }
+  __syncthreads();
+  double* pb = F.tpart + (size_t)b * nt * nt * T * 3;
+  for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+    double v = red[0][0][e];
+#pragma unroll
+    for (int qq = 1; qq < NQ; ++qq) v += red[0][qq][e];
+    __stcg(pb + ((size_t)I * nt + J) * T * 3 + e, v);  // block I, slot J
+    if (I != J) {
+      double w = red[1][0][e];
+#pragma unroll
+      for (int qq = 1; qq < NQ; ++qq) w += red[1][qq][e];
+      __stcg(pb + ((size_t)J * nt + I) * T * 3 + e, w);  // block J, slot I
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* cnt = F.tcnt + (size_t)b * nt;
+    s_last[0] = atomicAdd(cnt + I, 1u) == (unsigned)nt - 1 ? I : -1;
+    s_last[1] = (I != J && atomicAdd(cnt + J, 1u) == (unsigned)nt - 1) ? J : -1;
+  }
+  __syncthreads();
+  for (int w = 0; w < 2; ++w) {
+    const int B = s_last[w];
+    if (B < 0) continue;
+    __threadfence();
+    const double* pr = pb + (size_t)B * nt * T * 3;
+    for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+      double v = 0.0;
+      for (int S = 0; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);  // slot order: fixed
+      gI[e] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < T && B * T + (int)threadIdx.x < K) {
+      const int k = B * T + threadIdx.x;
+      const double v[3] = {gI[3 * threadIdx.x + 0], gI[3 * threadIdx.x + 1], gI[3 * threadIdx.x + 2]};
       const int row = F.tcols[k];
       double* xo = F.x + ((size_t)b * F.n + row) * 3;
-      xo[0] = a0;
-      xo[1] = a1;
-      xo[2] = a2;
-      const double v[3] = {a0, a1, a2};
+      xo[0] = v[0];
+      xo[1] = v[1];
+      xo[2] = v[2];
       io.store(b, row, v);
     }
+    if (threadIdx.x == 0) F.tcnt[(size_t)b * nt + B] = 0;  // every partial of B has arrived: reset for the next solve
+    __syncthreads();
   }
 }
 
@@ -827,8 +965,8 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     const dim3 gg((f->ktop + kSolveThreads - 1) / kSolveThreads, (unsigned)f->nbatch);
     sptrsv_top_gather<IO><<<gg, kSolveThreads, 0, stream>>>(v, io);
     QN_CHECK_LAUNCH();
-    const dim3 ga(std::max(1, std::min(2 * kSMs, (f->ktop + kSolveWarps - 1) / kSolveWarps)), (unsigned)f->nbatch);
-    sptrsv_top_apply<IO><<<ga, kSolveThreads, (size_t)f->ktop * 3 * sizeof(double), stream>>>(v, io);
+    const dim3 ga((unsigned)(f->tnt * (f->tnt + 1) / 2), (unsigned)f->nbatch);
+    sptrsv_top_sym<IO><<<ga, kSolveThreads, 0, stream>>>(v, io);
     QN_CHECK_LAUNCH();
   }
   if (nb > 0) {
@@ -844,9 +982,6 @@ int prepare_solve_kernels(qn_factor* f) {
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->smem_b));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  if (f->ktop > 0)
-    QN_CUDA(cudaFuncSetAttribute(sptrsv_top_apply<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(f->ktop * 3 * sizeof(double))));
   if (f->batch_smem > 0)
     QN_CUDA(cudaFuncSetAttribute(sptrsv_batch<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->batch_smem));
   int per_f = 0, per_b = 0, dev = 0, sms = 0;

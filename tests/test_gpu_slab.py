@@ -4,8 +4,9 @@ Several ranks' slabs live in one process (EmulatedComm: the all-gathers and
 halo exchanges are device copies, no kernel waits on another), so the
 decomposition is checked against the CPU oracle and against the single-system
 frame without more GPUs; the NCCL path is checked at world size 1.
-Tolerances as the scaled-c5 single-system tests (CG to 1e-10 vs the oracle's
-direct solve): positions 1e-8, energies 1e-9 relative.
+Tolerances: the north_star bar (positions 1e-9, per-iteration g 1e-10
+relative, identical line-search trials) with CG at the BASELINE's 1e-10
+against the oracle's direct solve (measured ~1e-14 / ~1e-12).
 """
 import os
 import socket
@@ -65,8 +66,8 @@ def test_slab_c5_scaled_against_oracle(world):
     res, run = run_emulated(sc, world, 1)
     (x, ro), = oracle_frames(sc, 1)
     xg, rg = res[0]
-    assert rel(rg.g, ro.g) <= 1e-9
-    assert rel(xg, x) <= 1e-8
+    assert rel(rg.g, ro.g) <= 1e-10
+    assert rel(xg, x) <= 1e-9
     assert rg.ls_trials == ro.ls_trials
     assert 0 < run.cg_iterations
 
@@ -181,8 +182,8 @@ def test_slab_two_level_against_oracle(world):
     res, run = run_emulated(sc, world, 1, coarse=True)
     (x, ro), = oracle_frames(sc, 1)
     xg, rg = res[0]
-    assert rel(rg.g, ro.g) <= 1e-9
-    assert rel(xg, x) <= 1e-8
+    assert rel(rg.g, ro.g) <= 1e-10
+    assert rel(xg, x) <= 1e-9
     assert rg.ls_trials == ro.ls_trials
 
 

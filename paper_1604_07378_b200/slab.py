@@ -1,8 +1,8 @@
 """Slab-decomposed frame for one large mesh across ranks (configs[4]).
 
 The reference has one process and one `simulate_frame` (solvers.py:260-352).
-Here the mesh is cut into slabs of grid cells along x (`parallel.slab_partition`
-semantics), one per rank; every rank keeps a one-cell ghost layer so that the
+Here the mesh is cut into slabs of grid cells along x (`slab_layout`: the
+cells balanced like `parallel.shard_instances`), one per rank; every rank keeps a one-cell ghost layer so that the
 gradient of each owned vertex is computed locally, bit for bit as in the
 single system, and the frame control (push, two-loop, CG, Armijo) runs on
 global sums.  The device work is the C-ABI `qn_slab_*` stages

@@ -123,6 +123,7 @@ def main():
         log = system.sysfact.log[nlog:]
         res[f"cg_iters_{f}"] = np.array([l[0] for l in log])
         res[f"cg_relres_{f}"] = np.array([l[1] for l in log])
+        res["frames"] = f + 1
         print(f"frame {f}: {time.time() - t:.0f} s, g {rec.g[-1]:.17g}, trials {rec.ls_trials}, "
               f"cg its {[l[0][0] for l in log]}, max relres {np.max([l[1] for l in log]):.2e}", flush=True)
         np.savez_compressed(out, **res)

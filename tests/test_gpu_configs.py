@@ -83,7 +83,7 @@ def test_c5_frames_against_reference_cg_golden(name):
         pytest.skip(f"{name} not generated")
     d = np.load(path)
     grid = tuple(int(v) for v in d["grid"])
-    frames = int(d["frames"])
+    frames = sum(1 for k in d.files if k.startswith("g_"))  # frames written so far (the generator saves per frame)
     sc = scenes.c5(grid=grid)
     system = Q.build_system(Q.TetMesh(sc.verts, sc.tets, sc.density), from_spec(sc.material), h=sc.h,
                             gravity=sc.gravity, fixed=sc.fixed, solver="amg", pcg_tol=1e-10)

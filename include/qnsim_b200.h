@@ -258,6 +258,12 @@ int qn_system_set_precision(qn_system* s, int32_t fp32);
 /* Execution mode for debugging: 1 = CUDA graph with conditional nodes
  * (default), 0 = host-driven loop (one host sync per line-search trial). */
 int qn_system_set_graph_mode(qn_system* s, int32_t use_graph);
+/* Device-only records of the last qn_frame_step, enqueued on `stream` (no host
+ * sync, for the torch op boundary): g_out[b][k] = per-iteration objective
+ * (rec.g, solvers.py:71-80) of instance b for k < iterations, and
+ * status_out[b] = bit 0 stagnated, bit 1 ascent (SolverError); both device
+ * pointers. */
+int qn_frame_records_device(qn_system* s, int32_t iterations, double* g_out, int32_t* status_out, void* stream);
 /* device time (ms) of the last qn_frame_step measured with CUDA events */
 int qn_system_last_frame_ms(qn_system* s, double* ms);
 /* body passes (line-search trials + re-evaluations) of the last frame */

@@ -140,9 +140,62 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
   if ((rc = dev_upload(&f->d_hlev_ptr, f->hlev_ptr.data(), f->hlev_ptr.size()))) return rc;
-  if (!f->fdesc.empty() && (rc = dev_upload(&f->d_fdesc, f->fdesc.data(), f->fdesc.size()))) return rc;
+  {
+    // Task-tiled copies of Z for the persistent solve kernels: every forward /
+    // backward task's tile is one contiguous, 16-byte aligned block laid out as
+    // the task holds it in shared memory (forward: rows [lo, hi) x k < kmax,
+    // column-major with leading dimension hi - lo; backward: columns [k0, k1)
+    // x all nr rows, zeros above the diagonal), so one TMA bulk copy stages it.
+    // Descriptors' zoff become tile offsets.  Batched mode (one CTA per
+    // instance, sptrsv_batch) reads vals directly and needs no copies.
+    int max_nc_all = 0;
+    for (int s = 0; s < f->nsup; ++s) max_nc_all = std::max(max_nc_all, f->sup_col[s + 1] - f->sup_col[s]);
+    const size_t bsm0 = sizeof(double) * 3 * ((size_t)f->n + (size_t)kBatchWarps * max_nc_all);
+    const bool batch_mode = f->nbatch > 1 && bsm0 <= 110 * 1024;
+    std::vector<qn_fdesc> fd = f->fdesc;
+    std::vector<qn_bdesc> bd = f->bdesc;
+    if (!batch_mode) {
+      int64_t off = 0;
+      for (auto& d : fd) {
+        const int64_t cnt = (int64_t)(d.hi - d.lo) * std::min(d.hi, d.nc);
+        d.zoff = off;
+        off += (cnt + 1) / 2 * 2;
+      }
+      f->ftile_n = std::max<int64_t>(off, 2);
+      off = 0;
+      for (auto& d : bd) {
+        const int64_t cnt = (int64_t)(d.k1 - d.k0) * d.nr;
+        d.zoff = off;
+        off += (cnt + 1) / 2 * 2;
+      }
+      f->btile_n = std::max<int64_t>(off, 2);
+      std::vector<double> ft((size_t)f->nbatch * f->ftile_n, 0.0), bt((size_t)f->nbatch * f->btile_n, 0.0);
+      for (int64_t b = 0; b < f->nbatch; ++b) {
+        const double* vb = f->vals.data() + (size_t)b * f->nvals;
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t i = 0; i < (int64_t)fd.size(); ++i) {
+          const qn_fdesc& h = f->fdesc[i];  // host descriptor: zoff = sup_val_ptr[s] + lo
+          const int R = h.hi - h.lo, kmax = std::min(h.hi, h.nc);
+          double* t = ft.data() + (size_t)b * f->ftile_n + fd[i].zoff;
+          for (int k = 0; k < kmax; ++k)
+            for (int r = 0; r < R; ++r) t[(size_t)k * R + r] = vb[h.zoff + (int64_t)k * h.nr + r];
+        }
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t i = 0; i < (int64_t)bd.size(); ++i) {
+          const qn_bdesc& h = f->bdesc[i];  // zoff = sup_val_ptr[s] + k0 nr
+          double* t = bt.data() + (size_t)b * f->btile_n + bd[i].zoff;
+          for (int kk = 0; kk < h.k1 - h.k0; ++kk)
+            for (int r = 0; r < h.nr; ++r)
+              t[(size_t)kk * h.nr + r] = r >= h.k0 + kk ? vb[h.zoff + (int64_t)kk * h.nr + r] : 0.0;
+        }
+      }
+      if ((rc = dev_upload(&f->d_ftile, ft.data(), ft.size()))) return rc;
+      if ((rc = dev_upload(&f->d_btile, bt.data(), bt.size()))) return rc;
+    }
+    if (!fd.empty() && (rc = dev_upload(&f->d_fdesc, fd.data(), fd.size()))) return rc;
+    if (!bd.empty() && (rc = dev_upload(&f->d_bdesc, bd.data(), bd.size()))) return rc;
+  }
   if (!f->fblob.empty() && (rc = dev_upload(&f->d_fblob, f->fblob.data(), f->fblob.size()))) return rc;
-  if (!f->bdesc.empty() && (rc = dev_upload(&f->d_bdesc, f->bdesc.data(), f->bdesc.size()))) return rc;
   if ((rc = dev_upload(&f->d_hlev_sup, f->hlev_sup.data(), f->hlev_sup.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
@@ -205,7 +258,8 @@ void factor_free_device(qn_factor* f) {
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
                   f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
-                  f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt};
+                  f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt,
+                  f->d_ftile,   f->d_btile};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;
@@ -863,6 +917,18 @@ int qn_system_amg_info(qn_system* S, int64_t* out, int64_t cap) {
   out[0] = nl;
   for (int64_t l = 0; l < nl && l < 10; ++l) out[1 + l] = S->h_alev[l].n;
   out[11] = (int64_t)(S->amg_setup_s * 1000.0);
+  return QN_OK;
+}
+
+int qn_frame_records_device(qn_system* S, int32_t iterations, double* g_out, int32_t* status_out, void* stream) {
+  QN_REQUIRE(S && g_out && status_out && iterations >= 1 && iterations <= S->rec_cap, QN_ERR_ARG,
+             "frame_records_device: args (iterations must not exceed the last frame's record capacity)");
+  cudaStream_t st = pick(S, stream);
+  QN_CUDA(cudaMemcpy2DAsync(g_out, sizeof(double) * iterations, S->v.rec_g, sizeof(double) * S->rec_cap,
+                            sizeof(double) * iterations, S->n_inst, cudaMemcpyDeviceToDevice, st));
+  QN_CUDA(cudaMemcpy2DAsync(status_out, sizeof(int32_t), reinterpret_cast<const char*>(S->v.ctl) +
+                            offsetof(qn::InstCtl, status), sizeof(qn::InstCtl), sizeof(int32_t), S->n_inst,
+                            cudaMemcpyDeviceToDevice, st));
   return QN_OK;
 }
 

@@ -106,6 +106,9 @@ struct qn_factor {
   int32_t* d_dlev_ptr = nullptr;
   int32_t* d_dlev_sup = nullptr;
   unsigned* d_flags = nullptr;    // nbatch x (n_ftask + n_btask) completion epochs
+  double* d_ftile = nullptr;      // task-tiled Z copies of the persistent solve (see factor_upload)
+  double* d_btile = nullptr;
+  int64_t ftile_n = 0, btile_n = 0;  // entries per instance
   double* d_stile = nullptr;      // S^-1 as packed lower-triangle tiles (kTopTile^2 each, tile (I,J), I >= J)
   double* d_tpart = nullptr;      // nbatch x nt x nt x kTopTile x 3 partial products of the symmetric top apply
   unsigned* d_tcnt = nullptr;     // nbatch x nt arrival counters of the partials per row block

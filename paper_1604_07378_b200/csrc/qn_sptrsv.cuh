@@ -54,6 +54,9 @@ struct FactorView {
   const int32_t* dlev_ptr;   // batched: supernodes by depth (backward levels)
   const int32_t* dlev_sup;
   const double* vals;
+  const double* ftile;       // task-tiled Z copies (persistent kernels): forward / backward
+  const double* btile;
+  int64_t ftile_n, btile_n;
   double* y;
   double* x;
   double* u;
@@ -109,6 +112,10 @@ inline FactorView factor_view(const qn_factor* f) {
   v.bdesc = f->d_bdesc;
   v.fblob = f->d_fblob;
   v.vals = f->d_vals;
+  v.ftile = f->d_ftile;
+  v.btile = f->d_btile;
+  v.ftile_n = f->ftile_n;
+  v.btile_n = f->btile_n;
   v.y = f->d_y;
   v.x = f->d_x;
   v.u = f->d_u;
@@ -160,6 +167,36 @@ __device__ __forceinline__ void trace_clock(unsigned long long* trace, size_t sl
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+// TMA bulk staging of a contiguous tile: thread 0 arms the CTA's mbarrier with
+// the byte count and issues one cp.async.bulk; every thread later waits on the
+// barrier's phase (parity flips once per task).
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  if (threadIdx.x == 0) {
+    const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(m)
+                 : "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, unsigned bytes, uint64_t* mbar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst), m = (unsigned)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "fence.proxy.async.shared::cta;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];" ::"r"(m),
+      "r"(bytes), "r"(d), "l"(src)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(m),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -284,7 +321,7 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
 // children, gather their updates, v = Z f, publish.
 template <class IO>
 __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp) {
+                                         int lane, int warp, uint64_t* mbar, unsigned& phase) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
@@ -299,13 +336,9 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   int* sidx = (int*)(part + 3 * kSolveThreads);
   const double* ub = F.u + (size_t)b * F.nupd * 3;
   // ---- stage everything that does not depend on the children ----
-  {  // Z tile rows [lo, hi) x k [0, kmax) -> zt[k * R + (r - lo)]
-    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
+  if (threadIdx.x == 0) {  // Z tile rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)]: one contiguous block
     const int cnt = R * kmax;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-      const int k = e / R, rr = e - k * R;
-      cp_async8(zt + e, Zg + (int64_t)k * nr + rr);
-    }
+    bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
   }
   const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
   const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
@@ -352,7 +385,8 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
       e2 += __ldcg(uc + 2);
     }
   }
-  cp_async_wait_all();
+  mbar_wait(mbar, phase);
+  phase ^= 1u;
   __syncthreads();
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
@@ -375,6 +409,20 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
       a2 = fma(l, f[3 * k + 2], a2);
     }
   }
+  if (L > 1) {  // lane groups -> group 0, in group order (shuffles, fixed order)
+    double s0 = a0, s1 = a1, s2 = a2;
+    for (int q = 1; q < L; ++q) {
+      const int src = q * R + (lane < R ? lane : 0);
+      const double t0 = __shfl_sync(0xffffffffu, a0, src), t1 = __shfl_sync(0xffffffffu, a1, src),
+                   t2 = __shfl_sync(0xffffffffu, a2, src);
+      s0 += t0;
+      s1 += t1;
+      s2 += t2;
+    }
+    a0 = s0;
+    a1 = s1;
+    a2 = s2;
+  }
   part[3 * threadIdx.x + 0] = a0;
   part[3 * threadIdx.x + 1] = a1;
   part[3 * threadIdx.x + 2] = a2;
@@ -382,13 +430,12 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   if (threadIdx.x < R) {
     const int gg = threadIdx.x >> 5;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-    for (int jj = 0; jj < ks; ++jj)
-      for (int q = 0; q < L; ++q) {  // fixed order: k-slice, then lane group
-        const int t = (gg * ks + jj) * 32 + (R < 32 ? q * R + (int)threadIdx.x : lane);
-        v0 += part[3 * t + 0];
-        v1 += part[3 * t + 1];
-        v2 += part[3 * t + 2];
-      }
+    for (int jj = 0; jj < ks; ++jj) {
+      const int t = (gg * ks + jj) * 32 + lane;
+      v0 += part[3 * t + 0];
+      v1 += part[3 * t + 1];
+      v2 += part[3 * t + 2];
+    }
     if (rr < nc) {
       double* yg = F.y + ((size_t)b * F.n + c0 + rr) * 3;
       yg[0] = v0;
@@ -410,7 +457,7 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
 // backward share one persistent kernel, so y_J is waited for explicitly.
 template <class IO>
 __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp, bool fused) {
+                                         int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
@@ -425,16 +472,9 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   int* srow = (int*)(sdst + kBwdCols);
   const bool staged = nr - nc <= kStageIdx;
   // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
-  {
-    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
+  if (threadIdx.x == 0) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
     const int cnt = (k1 - k0) * nr;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-      const int kk = e / nr, r = e - kk * nr;
-      if (r >= k0 + kk)
-        cp_async8(zt + e, Zg + e);
-      else
-        zt[e] = 0.0;
-    }
+    bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
   }
   if (fused)  // the forward of s may still be running: y_J must be complete
     wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask), d.fwd0, d.nfwd, epoch, F.sched);
@@ -449,7 +489,8 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
   const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
   trace_mark(F.trace, tb + 1);
-  cp_async_wait_all();
+  mbar_wait(mbar, phase);
+  phase ^= 1u;
   __syncthreads();
   // ---- before the parent is done: the y_J part of every column, 4 columns per warp.
   // Fewer than kSolveWarps column quads (tall fronts, few columns per task):
@@ -564,9 +605,12 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F, IO io) {
   // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
+  __shared__ uint64_t s_mbar;
+  unsigned phase = 0;
+  mbar_init(&s_mbar);
   unsigned* sched = F.sched;
   if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
@@ -575,7 +619,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
   for (;;) {
     const int item = next_ticket(sched, &s_item);
     if (item >= total) break;
-    fwd_task(F, io, item, s_epoch, sm, lane, warp);
+    fwd_task(F, io, item, s_epoch, sm, lane, warp, &s_mbar, phase);
   }
   cta_exit(sched, s_epoch, F, 4);
 }
@@ -583,9 +627,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
   // smem: ztile[bwd_entries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | dest[kBwdCols] | row staging
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
+  __shared__ uint64_t s_mbar;
+  unsigned phase = 0;
+  mbar_init(&s_mbar);
   unsigned* sched = F.sched + 3;
   if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 5, 0);
@@ -594,7 +641,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   for (;;) {
     const int item = next_ticket(sched, &s_item);
     if (item >= total) break;
-    bwd_task(F, io, item, s_epoch, sm, lane, warp, false);
+    bwd_task(F, io, item, s_epoch, sm, lane, warp, false, &s_mbar, phase);
   }
   cta_exit(sched, s_epoch, F, 5);
 }
@@ -607,9 +654,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
 // cannot deadlock.
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ int s_item;
   __shared__ unsigned s_epoch;
+  __shared__ uint64_t s_mbar;
+  unsigned phase = 0;
+  mbar_init(&s_mbar);
   unsigned* sched = F.sched;
   if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
@@ -619,9 +669,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
     const int item = next_ticket(sched, &s_item);
     if (item >= total) break;
     if (item < nfi)
-      fwd_task(F, io, item, s_epoch, sm, lane, warp);
+      fwd_task(F, io, item, s_epoch, sm, lane, warp, &s_mbar, phase);
     else
-      bwd_task(F, io, item - nfi, s_epoch, sm, lane, warp, true);
+      bwd_task(F, io, item - nfi, s_epoch, sm, lane, warp, true, &s_mbar, phase);
   }
   cta_exit(sched, s_epoch, F, 5);
 }

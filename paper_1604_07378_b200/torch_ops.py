@@ -9,7 +9,7 @@ the sm_100a kernels.
     torch.ops.qnsim_b200.material_eval(h, sigma)      # (k,3)   -> psi, tau      (materials.py:184-197)
     torch.ops.qnsim_b200.factor_solve(h, B, batch)    # (n,3)   -> A^-1 B        (linalg.py:36-40)
     torch.ops.qnsim_b200.objective(h, x, y)           # (n,3)   -> g, grad       (dynamics.py:460-478)
-    torch.ops.qnsim_b200.frame_step(h, n_inst, its, m, kind)  # resident frame     (solvers.py:260-352)
+    torch.ops.qnsim_b200.frame_step(h, n_inst, its, m, kind)  # resident frame -> g, status (solvers.py:260-352)
 
 `h` is an integer handle: `register_material(mat)`, `Factorization.op_handle`
 or `SimSystem.op_handle`.
@@ -114,19 +114,27 @@ def _(handle, x, y):
 
 
 @torch.library.custom_op("qnsim_b200::frame_step", mutates_args=())
-def frame_step(handle: int, n_inst: int, iterations: int, m: int, kind: int) -> torch.Tensor:
+def frame_step(handle: int, n_inst: int, iterations: int, m: int, kind: int) -> tuple[torch.Tensor, torch.Tensor]:
     """One frame on the resident state of system `handle` (state set with
-    qn_state_set / ResidentRun; kind 1 = lbfgs, 0 = pd_qn); returns the
-    per-iteration objective g of every instance, shape (n_inst, iterations)."""
-    from .solvers import SolverConfig, _RecordBuffers
+    qn_state_set / ResidentRun; kind 1 = lbfgs, 0 = pd_qn), enqueued on the
+    current stream with no host synchronisation.  Returns the per-iteration
+    objective g of every instance, (n_inst, iterations), and the per-instance
+    status (bit 0 stagnated, bit 1 ascent = the reference's SolverError), both
+    device tensors written by the device (qn_frame_records_device)."""
+    from .solvers import SolverConfig
     cfg = SolverConfig(kind="lbfgs" if kind == 1 else "pd_qn", iterations=iterations, m=m).to_c()
-    rb = _RecordBuffers(n_inst, iterations)
-    _lib.check(_lib.load().qn_frame_step(C.c_void_p(handle), C.byref(cfg), None, C.byref(rb.c), _lib.QN_MEM_HOST, 1,
-                                         C.c_void_p(_stream())), "frame_step")
-    rb.raise_on_error()
-    return torch.from_numpy(rb.g.copy()).to(torch.device("cuda", torch.cuda.current_device()))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.empty((n_inst, iterations), dtype=torch.float64, device=dev)
+    status = torch.empty((n_inst,), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.qn_frame_step(C.c_void_p(handle), C.byref(cfg), None, None, _lib.QN_MEM_DEVICE, 0,
+                                 C.c_void_p(_stream())), "frame_step")
+    _lib.check(lib.qn_frame_records_device(C.c_void_p(handle), iterations, C.c_void_p(g.data_ptr()),
+                                           C.c_void_p(status.data_ptr()), C.c_void_p(_stream())), "frame_step")
+    return g, status
 
 
 @frame_step.register_fake
 def _(handle, n_inst, iterations, m, kind):
-    return torch.empty((n_inst, iterations), dtype=torch.float64, device="cuda")
+    return (torch.empty((n_inst, iterations), dtype=torch.float64, device="cuda"),
+            torch.empty((n_inst,), dtype=torch.int32, device="cuda"))

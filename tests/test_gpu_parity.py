@@ -460,9 +460,19 @@ def test_torch_custom_ops_match_the_c_abi_paths():
     assert float(g.cpu()[0]) == pytest.approx(g_ref, rel=1e-13)
     run = Q.ResidentRun(system, Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev),
                         Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
-    gs = torch.ops.qnsim_b200.frame_step(system.op_handle, 1, sc.iterations, sc.m, 1)
+    gs, status = torch.ops.qnsim_b200.frame_step(system.op_handle, 1, sc.iterations, sc.m, 1)
+    assert gs.is_cuda and status.is_cuda  # device-only: no host round trip inside the op
     (_, rec), = run_gpu(build(sc), sc, 1)
     np.testing.assert_array_equal(gs.cpu().numpy()[0], np.asarray(rec.g))
+    assert int(status.cpu()[0]) == 0
+    # the objective op runs in order on torch's current stream: inputs produced
+    # by a kernel just before the call on the same stream are seen complete
+    xq = torch.from_numpy(np.asarray(sc.q_l)).cuda()
+    for _ in range(3):
+        x2 = xq * 1.0 + 0.0
+        y2 = x2 + 0.01
+        g2, _ = torch.ops.qnsim_b200.objective(system.op_handle, x2, y2)
+        assert float(g2.cpu()[0]) == pytest.approx(g_ref, rel=1e-13)
     h = torch_ops.register_material(from_spec(sc.material))
     psi, tau = torch.ops.qnsim_b200.material_eval(h, s[:16].contiguous())
     assert psi.shape == (16,) and tau.shape == (16, 3)

@@ -130,14 +130,12 @@ int factor_upload(qn_factor* f) {
   if ((rc = dev_alloc(&f->d_y, (size_t)f->nbatch * f->n * 3))) return rc;
   if ((rc = dev_alloc(&f->d_x, (size_t)f->nbatch * f->n * 3))) return rc;
   if ((rc = dev_alloc(&f->d_u, (size_t)f->nbatch * std::max<int64_t>(f->nupd, 1) * 3))) return rc;
-  // task flags, then one 'f assembled' flag per supernode
-  if ((rc = dev_alloc(&f->d_flags, (size_t)f->nbatch * (f->ftask.size() + f->btask.size() + f->nsup)))) return rc;
+  if ((rc = dev_alloc(&f->d_flags, (size_t)f->nbatch * (f->ftask.size() + f->btask.size())))) return rc;
   if ((rc = dev_upload(&f->d_cptr, f->cptr.data(), f->cptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_cidx, f->cidx.data(), f->cidx.size()))) return rc;
   if ((rc = dev_upload(&f->d_ftask, f->ftask.data(), f->ftask.size()))) return rc;
   if ((rc = dev_upload(&f->d_btask, f->btask.data(), f->btask.size()))) return rc;
   if ((rc = dev_upload(&f->d_bfirst, f->bfirst.data(), f->bfirst.size()))) return rc;
-  if ((rc = dev_upload(&f->d_ffirst, f->ffirst.data(), f->ffirst.size()))) return rc;
   if ((rc = dev_upload(&f->d_bcount, f->bcount.data(), f->bcount.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_ptr, f->fdep_ptr.data(), f->fdep_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_fdep_idx, f->fdep_idx.data(), f->fdep_idx.size()))) return rc;
@@ -198,12 +196,6 @@ int factor_upload(qn_factor* f) {
     if (!bd.empty() && (rc = dev_upload(&f->d_bdesc, bd.data(), bd.size()))) return rc;
   }
   if (!f->fblob.empty() && (rc = dev_upload(&f->d_fblob, f->fblob.data(), f->fblob.size()))) return rc;
-  if (!f->asm_need.empty()) {
-    if ((rc = dev_upload(&f->d_asm_need, f->asm_need.data(), f->asm_need.size()))) return rc;
-    std::vector<unsigned> zero((size_t)f->nbatch * f->nsup, 0u);
-    if ((rc = dev_upload(&f->d_asm_cnt, zero.data(), zero.size()))) return rc;
-    if ((rc = dev_alloc(&f->d_fglob, (size_t)f->nbatch * f->n * 3))) return rc;
-  }
   if ((rc = dev_upload(&f->d_hlev_sup, f->hlev_sup.data(), f->hlev_sup.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_ptr, f->dlev_ptr.data(), f->dlev_ptr.size()))) return rc;
   if ((rc = dev_upload(&f->d_dlev_sup, f->dlev_sup.data(), f->dlev_sup.size()))) return rc;
@@ -267,8 +259,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
                   f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt,
-                  f->d_ftile,   f->d_btile,       f->d_asm_need,  f->d_asm_cnt,   f->d_fglob,
-                  f->d_ffirst};
+                  f->d_ftile,   f->d_btile};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

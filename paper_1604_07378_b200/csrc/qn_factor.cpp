@@ -664,11 +664,6 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       }
     }
     // forward task descriptors + their relative extend-add lists
-    f->asm_need.assign(ns, 0);
-    if (const char* e = std::getenv("QN_NO_ASM"); !(e && std::atoi(e)))  // experiment knob
-      for (int32_t s = 0; s < ns; ++s)
-        if (!f->is_top[s] && f->fcount[s] >= kAsmMinTasks && f->fdep_ptr[s + 1] > f->fdep_ptr[s])
-          f->asm_need[s] = f->fdep_ptr[s + 1] - f->fdep_ptr[s];
     f->fdesc.clear();
     f->fblob.clear();
     for (const int4& t : f->ftask) {
@@ -693,8 +688,6 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       d.upd0 = (int32_t)f->sup_upd_ptr[s];
       d.dep0 = f->fdep_ptr[s];
       d.dep1 = f->fdep_ptr[s + 1];
-      d.asmp = (f->parent[s] >= 0 && f->asm_need[f->parent[s]] > 0) ? f->parent[s] : -1;
-      d.self_asm = f->asm_need[s] > 0 ? s + 1 : 0;
       QN_REQUIRE(f->fblob.size() < (size_t)INT32_MAX && f->nupd < INT32_MAX, QN_ERR_UNSUPPORTED,
                  "factor: solve lists exceed 32-bit offsets");
       d.blob = (int32_t)f->fblob.size();

@@ -22,9 +22,6 @@ struct alignas(16) qn_fdesc {
   int32_t nc, nr, blo, ntop;    // supernode shape, first bottom row, #top list entries
   int32_t nbot, upd0, dep0, dep1;  // #bottom list entries, update rows offset, fdep range
   int32_t blob, pad;            // offset of [sp_top | sp_bot | si_top | si_bot] in fblob
-  int32_t asmp;                 // parent supernode whose f this task's completion counts towards (-1: none)
-  int32_t self_asm;             // s + 1 if this supernode's f is assembled once (wait for its flag, load fglob), else 0
-  int32_t pad2, pad3;
 };
 
 // Backward solve task descriptor (same idea as qn_fdesc).
@@ -58,10 +55,6 @@ struct qn_factor {
   std::vector<int32_t> ffirst, bfirst;  // first task of each supernode
   std::vector<int32_t> fdep_ptr, fdep_idx;  // forward: all tasks of the children of s
   std::vector<qn_fdesc> fdesc;              // per forward task
-  // assembled forward f: supernodes with several row tasks get f_J = b_J -
-  // (children's updates) computed ONCE, by the CTA of the last child task to
-  // finish, into fglob (factor order); their row tasks wait for one flag
-  std::vector<int32_t> asm_need;            // per supernode: child tasks to arrive (0 = not assembled)
   std::vector<qn_bdesc> bdesc;              // per backward task
   std::vector<int32_t> fblob;               // per-task relative extend-add lists
   std::vector<int32_t> hlev_ptr, hlev_sup;  // supernodes grouped by height (batched forward levels)
@@ -102,14 +95,10 @@ struct qn_factor {
   int4* d_ftask = nullptr;
   int4* d_btask = nullptr;
   int32_t* d_bfirst = nullptr;
-  int32_t* d_ffirst = nullptr;
   int32_t* d_bcount = nullptr;
   int32_t* d_fdep_ptr = nullptr;
   int32_t* d_fdep_idx = nullptr;
   qn_fdesc* d_fdesc = nullptr;
-  int32_t* d_asm_need = nullptr;
-  unsigned* d_asm_cnt = nullptr;  // nbatch x nsup arrival counters
-  double* d_fglob = nullptr;      // nbatch x n x 3 assembled f (factor order)
   qn_bdesc* d_bdesc = nullptr;
   int32_t* d_fblob = nullptr;
   int32_t* d_hlev_ptr = nullptr;
@@ -148,8 +137,7 @@ constexpr int64_t kTopMax = 4096;
 constexpr int kTopTile = 64;            // symmetric top apply: S^-1 stored as 64 x 64 lower-triangle tiles       // max columns of the dense top block (S^-1 <= 134 MB)
 constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
 constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
-constexpr int64_t kBwdTaskCols = 64;
-constexpr int32_t kAsmMinTasks = 3;     // supernodes with at least this many forward tasks assemble f once    // max columns of a backward task
+constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
 constexpr int64_t kSmemPerCtaPair = 110 * 1024;  // dynamic smem per CTA with two CTAs per SM (228 KB - reserved/static)
 // bottom-of-tree subtree collapse (see factor_build_host)
 constexpr int32_t kCollapseHeight = 2;  // swept on c1-c3 with the current solve kernels: 2 > 3 (+3.6 % at c2), 1 and 4 slower

@@ -47,10 +47,6 @@ struct FactorView {
   const int32_t* fdep_ptr;  // forward: task ids of all children's tasks
   const int32_t* fdep_idx;
   const qn_fdesc* fdesc;     // forward task descriptors
-  const int32_t* asm_need;   // per supernode: child tasks that must arrive before f is assembled (0 = inline)
-  unsigned* asm_cnt;         // [nbatch][nsup]
-  double* fglob;             // [nbatch][n][3] assembled f (factor order)
-  const int32_t* ffirst;     // first forward task of each supernode
   const qn_bdesc* bdesc;     // backward task descriptors
   const int32_t* fblob;      // forward tasks' relative extend-add lists
   const int32_t* hlev_ptr;   // batched: supernodes by height (forward levels)
@@ -113,10 +109,6 @@ inline FactorView factor_view(const qn_factor* f) {
   v.fdep_ptr = f->d_fdep_ptr;
   v.fdep_idx = f->d_fdep_idx;
   v.fdesc = f->d_fdesc;
-  v.asm_need = f->d_asm_need;
-  v.asm_cnt = f->d_asm_cnt;
-  v.fglob = f->d_fglob;
-  v.ffirst = f->d_ffirst;
   v.bdesc = f->d_bdesc;
   v.fblob = f->d_fblob;
   v.vals = f->d_vals;
@@ -321,40 +313,6 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
   }
 }
 
-// 'f assembled' flag of supernode s (after every batch's task flags)
-__device__ __forceinline__ unsigned* asm_flag(const FactorView& F, int b, int s) {
-  return F.flags + (size_t)F.nbatch * (F.nftask + F.nbtask) + (size_t)b * F.nsup + s;
-}
-
-// f_J of supernode p = b_J - (children's updates on J), written once to fglob
-// by the CTA whose task completed p's last child task (all threads of the CTA).
-template <class IO>
-__device__ __forceinline__ void assemble_f(const FactorView& F, const IO& io, int b, int p, unsigned epoch) {
-  __threadfence();  // acquire: the other children's u (published before their arrivals)
-  const qn_fdesc d = F.fdesc[F.ffirst[p]];  // any task of p: its top lists cover all of J_p
-  const int nptr_bot = d.blo < d.hi ? d.hi - d.blo + 1 : 0;
-  const int* sp_top = F.fblob + d.blob;
-  const int* si_top = sp_top + d.nc + 1 + nptr_bot;
-  const double* ub = F.u + (size_t)b * F.nupd * 3;
-  double* fo = F.fglob + ((size_t)b * F.n + d.c0) * 3;
-  for (int r = threadIdx.x; r < d.nc; r += blockDim.x) {
-    double v[3];
-    io.rhs(b, d.c0 + r, v);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int q = __ldg(sp_top + r); q < __ldg(sp_top + r + 1); ++q) {
-      const double* uc = ub + 3 * (size_t)__ldg(si_top + q);
-      a0 += __ldcg(uc);
-      a1 += __ldcg(uc + 1);
-      a2 += __ldcg(uc + 2);
-    }
-    __stcg(fo + 3 * r + 0, v[0] - a0);
-    __stcg(fo + 3 * r + 1, v[1] - a1);
-    __stcg(fo + 3 * r + 2, v[2] - a2);
-  }
-  if (threadIdx.x == 0) F.asm_cnt[(size_t)b * F.nsup + p] = 0;  // every child has arrived: reset for the next solve
-  publish(asm_flag(F, b, p), epoch);
-}
-
 // IO: struct with
 //   __device__ bool active(int b) const;
 //   __device__ void rhs(int b, int row, double (&v)[3]) const;   // factor row
@@ -392,40 +350,29 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   const int* sp_bot = sp_top + nc + 1;
   const int* si_top = sp_bot + nptr_bot;
   const int* si_bot = si_top + d.ntop;
-  if (!d.self_asm)
-    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-      double v[3];
-      io.rhs(b, c0 + p, v);
-      f[3 * p + 0] = v[0];
-      f[3 * p + 1] = v[1];
-      f[3 * p + 2] = v[2];
-    }
-  trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
-  if (d.self_asm) {  // f was assembled once for the whole supernode: one flag
-    const int32_t one = 0;
-    wait_flags(asm_flag(F, b, d.self_asm - 1), &one, 1, epoch, F.sched);
-  } else {
-    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
+  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+    double v[3];
+    io.rhs(b, c0 + p, v);
+    f[3 * p + 0] = v[0];
+    f[3 * p + 1] = v[1];
+    f[3 * p + 2] = v[2];
   }
+  trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
+  wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
   trace_mark(F.trace, kTraceSlots * (size_t)item + 2);
   trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
   // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
-  if (d.self_asm) {
-    const double* fg = F.fglob + ((size_t)b * F.n + c0) * 3;
-    for (int p = threadIdx.x; p < 3 * nc; p += blockDim.x) f[p] = __ldcg(fg + p);
-  } else {
-    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)si_top[q];
-        a0 += __ldcg(uc);
-        a1 += __ldcg(uc + 1);
-        a2 += __ldcg(uc + 2);
-      }
-      f[3 * p + 0] -= a0;
-      f[3 * p + 1] -= a1;
-      f[3 * p + 2] -= a2;
+  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
+      const double* uc = ub + 3 * (size_t)si_top[q];
+      a0 += __ldcg(uc);
+      a1 += __ldcg(uc + 1);
+      a2 += __ldcg(uc + 2);
     }
+    f[3 * p + 0] -= a0;
+    f[3 * p + 1] -= a1;
+    f[3 * p + 2] -= a2;
   }
   const int rr = lo + threadIdx.x;  // row owned by this thread in the epilogue
   double e0 = 0.0, e1 = 0.0, e2 = 0.0;
@@ -504,16 +451,6 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
   publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
   trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
-  if (d.asmp >= 0) {  // count this task towards the parent's f; the last arrival assembles it
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned old = atomicAdd(F.asm_cnt + (size_t)b * F.nsup + d.asmp, 1u);
-      s_last = old + 1 == (unsigned)__ldg(F.asm_need + d.asmp);
-    }
-    __syncthreads();
-    if (s_last) assemble_f(F, io, b, d.asmp, epoch);
-  }
 }
 
 // One backward task (column block of one supernode).  fused: forward and
@@ -859,15 +796,7 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_sym(FactorView F, IO
     const double* pr = pb + (size_t)B * nt * T * 3;
     for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
       double v = 0.0;
-      int S = 0;
-      for (; S + 16 <= nt; S += 16) {  // 16 independent loads in flight, summed in slot order
-        double l[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) l[q] = __ldcg(pr + (size_t)(S + q) * T * 3 + e);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v += l[q];
-      }
-      for (; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);
+      for (int S = 0; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);  // slot order: fixed
       gI[e] = v;
     }
     __syncthreads();

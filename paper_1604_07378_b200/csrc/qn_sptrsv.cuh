@@ -796,7 +796,15 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_sym(FactorView F, IO
     const double* pr = pb + (size_t)B * nt * T * 3;
     for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
       double v = 0.0;
-      for (int S = 0; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);  // slot order: fixed
+      int S = 0;
+      for (; S + 16 <= nt; S += 16) {  // 16 independent loads in flight, summed in slot order
+        double l[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) l[q] = __ldcg(pr + (size_t)(S + q) * T * 3 + e);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v += l[q];
+      }
+      for (; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);
       gI[e] = v;
     }
     __syncthreads();

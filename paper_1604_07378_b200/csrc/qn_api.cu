@@ -221,6 +221,7 @@ int factor_upload(qn_factor* f) {
     if ((rc = dev_upload(&f->d_tg_idx, f->tg_idx.data(), f->tg_idx.size()))) return rc;
     if ((rc = dev_alloc(&f->d_gtop, (size_t)f->nbatch * f->ktop * 3))) return rc;
   }
+  if (const char* e = std::getenv("QN_SOLVE_OPTS")) f->solve_opts = std::atoi(e);  // experiment knob
   const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};  // [ticket, exited, epoch] x 2, watchdog
   if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
   if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;

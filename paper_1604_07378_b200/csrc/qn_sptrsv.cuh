@@ -64,6 +64,7 @@ struct FactorView {
   unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
   unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
+  int32_t opts;              // experiment knobs (QN_SOLVE_OPTS): bit 0 no forward lane groups, bit 1 no backward row split
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
   double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
   unsigned* tcnt;            // [nbatch][nt] arrivals per row block
@@ -123,6 +124,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.sched = f->d_sched;
   v.trace = f->d_trace;
   v.ktop = f->ktop;
+  v.opts = f->solve_opts;
   v.stile = f->d_stile;
   v.tpart = f->d_tpart;
   v.tcnt = f->d_tcnt;
@@ -396,9 +398,9 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   const int g = warp / ks, j = warp % ks;
   const int per = (kmax + ks - 1) / ks;
   const int kb = j * per, ke = min(kmax, kb + per);
-  const int L = R < 32 ? 32 / R : 1;  // rg == 1 whenever R < 32
-  const int sub = R < 32 ? lane / R : 0;
-  const int rl = R < 32 ? lane - sub * R : 32 * g + lane;
+  const int L = (R < 32 && !(F.opts & 1)) ? 32 / R : 1;  // rg == 1 whenever R < 32
+  const int sub = L > 1 ? lane / R : 0;
+  const int rl = L > 1 ? lane - sub * R : 32 * g + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (g < rg && rl < R && sub < L) {
 #pragma unroll 8
@@ -497,7 +499,7 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   // each quad's rows are split over rs warps and the slices summed in order ----
   const int ncols = k1 - k0;
   const int nquads = (ncols + 3) / 4;
-  const int rs = nquads >= kSolveWarps ? 1 : kSolveWarps / nquads;
+  const int rs = (nquads >= kSolveWarps || (F.opts & 2)) ? 1 : kSolveWarps / nquads;
   __shared__ double slp[kSolveWarps][4][3];
   if (rs > 1) {
     const int quad = warp / rs, slice = warp % rs, kl = 4 * quad;

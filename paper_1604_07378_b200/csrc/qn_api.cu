@@ -581,6 +581,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     if (rc == QN_OK) rc = factor_upload(S->factor);
     if (rc) return fail(rc);
     for (int64_t r = 0; r < S->n_free; ++r) fact_vtx[r] = free_ids[S->factor->perm[r]];
+    v.n_free = (int32_t)S->n_free;  // factor rows (k_solve_rhs)
   } else {
     // PCG: A_free on the device as CSR (free-vertex order), Jacobi preconditioner
     QN_REQUIRE(d->pcg_tol > 0 && d->pcg_maxit > 0, QN_ERR_ARG, "system: PCG needs pcg_tol > 0 and pcg_maxit > 0");
@@ -763,7 +764,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   if ((rc = sys_alloc(S, &v.q_l, vec)) || (rc = sys_alloc(S, &v.q_prev, vec)) || (rc = sys_alloc(S, &v.y, vec)) ||
       (rc = sys_alloc(S, &v.X, 3 * vec)) || (rc = sys_alloc(S, &v.Gr, 2 * vec)) ||
       (rc = sys_alloc(S, &v.S, (size_t)(kMaxM + 1) * vec)) || (rc = sys_alloc(S, &v.T, (size_t)(kMaxM + 1) * vec)) ||
-      (rc = sys_alloc(S, &v.R0, vec)) || (rc = sys_alloc(S, &v.D, vec)) ||
+      (rc = sys_alloc(S, &v.R0, vec)) || (rc = sys_alloc(S, &v.D, vec)) || (rc = sys_alloc(S, &v.qf, vec)) ||
       (rc = sys_alloc(S, &v.forces, (size_t)ni * std::max<int64_t>(mt, 1) * 12)) ||
       (rc = sys_alloc(S, &v.part_v, (size_t)ni * v.nblk_v * kNG)) ||
       (rc = sys_alloc(S, &v.part_t, (size_t)ni * v.nblk_t)) || (rc = sys_alloc(S, &v.cnt, (size_t)4 * ni + 1)) ||

@@ -401,6 +401,33 @@ __global__ void __launch_bounds__(256) k_rest_apply(SysView v) {
   }
 }
 
+// The persistent solve's right-hand side precomputed once per direction in
+// factor order (qf), so a forward task loads its rows contiguously instead of
+// forming q' = -g - sum zeta t row by row (the wide supernodes' row tasks all
+// need the same nc rows).  Same rounding as SolverIO::rhs.
+__global__ void __launch_bounds__(kVTB) k_solve_rhs(SysView v) {
+  const int b = blockIdx.y;
+  const InstCtl* c = v.ctl + b;
+  if (c->phase != PH_DIR) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (factor row, coordinate)
+  if (i >= 3 * v.n_free) return;
+  const int row = i / 3, k = i - 3 * row;
+  const size_t o = (size_t)v.fact_vtx[row] * 3 + k;
+  double q = -v.Gr[vec_off(v, c->gs_cur, b) + o];
+  for (int p = c->npairs - 1; p >= 0; --p)  // q -= zeta t, newest first
+    q = __dsub_rn(q, __dmul_rn(c->zeta[p], v.T[vec_off(v, c->ring[p], b) + o]));
+  v.qf[(size_t)b * v.n_free * 3 + i] = q;
+}
+
+struct FactorRhsIO : SolverIO {
+  __device__ void rhs(int b, int row, double (&q)[3]) const {
+    const double* r = v.qf + ((size_t)b * v.n_free + row) * 3;
+    q[0] = __ldcg(r);
+    q[1] = __ldcg(r + 1);
+    q[2] = __ldcg(r + 2);
+  }
+};
+
 // stand-alone timing of the solve kernels (qn_system_time_kernel): every
 // instance, right-hand side = the resident q_l, result into the R0 scratch
 struct TimingIO {
@@ -1502,7 +1529,13 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
     QN_CHECK_LAUNCH();
     return QN_OK;
   }
-  SolverIO io{v};
+  if (S->factor->batch_smem > 0) {  // one CTA per instance: every row's rhs is formed exactly once anyway
+    SolverIO io{v};
+    return launch_solve(S->factor, io, st);
+  }
+  k_solve_rhs<<<dim3(div_up(3 * (int64_t)v.n_free, kVTB), v.n_inst), kVTB, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
+  FactorRhsIO io{{v}};
   return launch_solve(S->factor, io, st);
 }
 
@@ -1611,7 +1644,8 @@ int prepare_kernels(qn_system* S) {
   if (S->v.pcg == 2)
     if (int rc = ensure_coarse_smem(S->v.ncoarse)) return rc;
   if (!S->factor) return QN_OK;
-  const int rc = prepare_solve_kernels<SolverIO>(S->factor);
+  int rc = prepare_solve_kernels<SolverIO>(S->factor);
+  if (!rc) rc = prepare_solve_kernels<FactorRhsIO>(S->factor);
   return rc ? rc : prepare_solve_kernels<TimingIO>(S->factor);
 }
 

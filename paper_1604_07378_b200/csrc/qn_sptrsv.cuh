@@ -403,13 +403,27 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   const int rl = L > 1 ? lane - sub * R : 32 * g + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (g < rg && rl < R && sub < L) {
-#pragma unroll 8
-    for (int k = kb + sub; k < ke; k += L) {
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;  // two chains per coordinate (even / odd steps)
+    int k = kb + sub;
+#pragma unroll 4
+    for (; k + L < ke; k += 2 * L) {
+      const double l = zt[k * R + rl], m = zt[(k + L) * R + rl];
+      a0 = fma(l, f[3 * k + 0], a0);
+      a1 = fma(l, f[3 * k + 1], a1);
+      a2 = fma(l, f[3 * k + 2], a2);
+      b0 = fma(m, f[3 * (k + L) + 0], b0);
+      b1 = fma(m, f[3 * (k + L) + 1], b1);
+      b2 = fma(m, f[3 * (k + L) + 2], b2);
+    }
+    if (k < ke) {
       const double l = zt[k * R + rl];
       a0 = fma(l, f[3 * k + 0], a0);
       a1 = fma(l, f[3 * k + 1], a1);
       a2 = fma(l, f[3 * k + 2], a2);
     }
+    a0 += b0;
+    a1 += b1;
+    a2 += b2;
   }
   if (L > 1) {  // lane groups -> group 0, in group order (shuffles, fixed order)
     double s0 = a0, s1 = a1, s2 = a2;

@@ -127,6 +127,7 @@ struct SysView {
   double* S;       // [kMaxM+1][inst][n][3]
   double* T;
   double* R0;      // [inst][n][3]
+  double* qf;      // [inst][n_free][3] solve right-hand side in factor order (direct solver, non-batched)
   double* D;       // [inst][n][3]
   double* forces;  // [inst][4 mt][3] corner forces in gather (v2e) order
   const double* targets;  // [inst][n_fixed][3]

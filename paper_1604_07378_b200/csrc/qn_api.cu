@@ -203,13 +203,14 @@ int factor_upload(qn_factor* f) {
     {  // S^-1 is symmetric: only the tiles (I, J), I >= J, are stored (half the bytes of the dense K x K)
       const int64_t K = f->ktop, T = kTopTile, nt = (K + T - 1) / T;
       f->tnt = (int32_t)nt;
-      std::vector<double> tiles((size_t)(nt * (nt + 1) / 2) * T * T, 0.0);
+      const int64_t LD = T + 1;  // padded leading dimension (bank-conflict-free row and column products)
+      std::vector<double> tiles((size_t)(nt * (nt + 1) / 2) * T * LD, 0.0);
       for (int64_t I = 0; I < nt; ++I)
         for (int64_t J = 0; J <= I; ++J) {
-          double* t = tiles.data() + (size_t)(I * (I + 1) / 2 + J) * T * T;
+          double* t = tiles.data() + (size_t)(I * (I + 1) / 2 + J) * T * LD;
           for (int64_t j = 0; j < T && J * T + j < K; ++j)
             for (int64_t i = 0; i < T && I * T + i < K; ++i)
-              t[i + j * T] = f->sinv[(size_t)(I * T + i) + (size_t)(J * T + j) * K];
+              t[i + j * LD] = f->sinv[(size_t)(I * T + i) + (size_t)(J * T + j) * K];
         }
       if ((rc = dev_upload(&f->d_stile, tiles.data(), tiles.size()))) return rc;
       if ((rc = dev_alloc(&f->d_tpart, (size_t)f->nbatch * nt * nt * T * 3))) return rc;

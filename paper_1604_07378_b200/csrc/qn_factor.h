@@ -124,7 +124,6 @@ struct qn_factor {
   const unsigned long long* d_passes = nullptr;
   int smem_f = 0, smem_b = 0;     // dynamic shared memory of the forward / backward solve kernels
   int grid_f = 0, grid_b = 0;     // persistent solve grids (co-resident CTAs)
-  int grid_top = 0;               // persistent grid of the symmetric top apply
   bool fused = false;             // forward + backward in one persistent kernel (no dense top)
   int smem_fused = 0, grid_fused = 0;
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)

@@ -655,143 +655,128 @@ __global__ void __launch_bounds__(kSolveThreads) sptrsv_top_gather(FactorView F,
   g[2] = v[2] - a2;
 }
 
-// x_T = S^-1 g_T with the symmetric S^-1 read once from half storage.
-// Persistent CTAs walk the lower-triangle tiles (I, J) (64 x 64, stored with
-// leading dimension 65 so both the row and the column products read shared
-// memory without bank conflicts), double-buffered: the TMA bulk copy of the
-// next tile is in flight while the current one is multiplied.  A tile gives
+// x_T = S^-1 g_T with the symmetric S^-1 read once from half storage: CTA per
+// lower-triangle tile (I, J) (64 x 64, stored with leading dimension 65 so the
+// row and the column products both read shared memory without bank
+// conflicts; the TMA engine brings the tile in one bulk copy).  A tile gives
 // the row-block product S_IJ g_J (-> block I) and, off the diagonal, the
 // transposed product S_IJ^T g_I (-> block J).  Each row block receives exactly
 // nt partials (slot = the other block index); the CTA that delivers the last
 // one (arrival counter) sums them in slot order — a fixed order, so the result
 // is bitwise reproducible — and writes x_T.  Half the bytes of the dense K x K
-// product (c3: 64 MB instead of 118 MB per solve).
+// product (c3: 64 MB instead of 118 MB per solve).  Small CTAs (37 KB of shared
+// memory, the partial products reuse the tile buffer) keep 6 tiles in flight
+// per SM: the per-tile phases are latency chains, so concurrency matters more
+// than pipelining inside one CTA (a persistent double-buffered variant was
+// slower: 45 vs 33 us on c3).
 constexpr int kTopLD = kTopTile + 1;
 constexpr int kTopTileEntries = kTopTile * kTopLD;  // 4160 doubles = 33,280 B (a multiple of 16)
 
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_sym(FactorView F, IO io) {
+__global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F, IO io) {
   constexpr int T = kTopTile, LD = kTopLD, NQ = kSolveThreads / T;  // NQ = 4 column / row quarters
-  extern __shared__ __align__(16) double tsm[];  // 2 tile buffers
+  __shared__ __align__(16) double st[kTopTileEntries];
   __shared__ double gI[T * 3], gJ[T * 3];
-  __shared__ double red[2][NQ][T * 3];
   __shared__ int s_last[2];
-  __shared__ uint64_t s_mbar[2];
+  __shared__ uint64_t s_mbar;
+  double* red = st;  // [2][NQ][T * 3] partial products, after the tile is consumed
   const int b = blockIdx.y;
   if (!io.active(b)) return;
-  const int K = F.ktop, nt = F.tnt, ntiles = nt * (nt + 1) / 2;
-  if (threadIdx.x < 2) {
-    const unsigned m = (unsigned)__cvta_generic_to_shared(&s_mbar[threadIdx.x]);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m) : "memory");
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  unsigned phase[2] = {0u, 0u};
-  const double* tiles = F.stile;
-  int t = blockIdx.x;
-  if (threadIdx.x == 0 && t < ntiles)
-    bulk_stage(tsm, tiles + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), &s_mbar[0]);
+  const int t = blockIdx.x;
+  const int K = F.ktop, nt = F.tnt;
+  mbar_init(&s_mbar);
+  if (threadIdx.x == 0)
+    bulk_stage(st, F.stile + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), &s_mbar);
+  int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  const int J = t - I * (I + 1) / 2;
   const double* g = F.gtop + (size_t)b * K * 3;
+  for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+    const int r = e / 3, c = e - 3 * r;
+    gI[e] = I * T + r < K ? __ldcg(g + 3 * (I * T + r) + c) : 0.0;
+    gJ[e] = J * T + r < K ? __ldcg(g + 3 * (J * T + r) + c) : 0.0;
+  }
+  mbar_wait(&s_mbar, 0);
+  __syncthreads();
+  const int i = threadIdx.x % T, q = threadIdx.x / T;
+  double r0 = 0.0, r1 = 0.0, r2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll 8
+  for (int j = q * (T / NQ); j < (q + 1) * (T / NQ); ++j) {  // row i of S_IJ g_J, columns of quarter q
+    const double sv = st[i + j * LD];
+    r0 = fma(sv, gJ[3 * j + 0], r0);
+    r1 = fma(sv, gJ[3 * j + 1], r1);
+    r2 = fma(sv, gJ[3 * j + 2], r2);
+  }
+  if (I != J) {
+#pragma unroll 8
+    for (int r = q * (T / NQ); r < (q + 1) * (T / NQ); ++r) {  // column i of S_IJ against g_I, rows of quarter q
+      const double sv = st[r + i * LD];
+      c0 = fma(sv, gI[3 * r + 0], c0);
+      c1 = fma(sv, gI[3 * r + 1], c1);
+      c2 = fma(sv, gI[3 * r + 2], c2);
+    }
+  }
+  __syncthreads();  // the tile is consumed: its buffer holds the partial products now
+  red[(0 * NQ + q) * T * 3 + 3 * i + 0] = r0;
+  red[(0 * NQ + q) * T * 3 + 3 * i + 1] = r1;
+  red[(0 * NQ + q) * T * 3 + 3 * i + 2] = r2;
+  red[(1 * NQ + q) * T * 3 + 3 * i + 0] = c0;
+  red[(1 * NQ + q) * T * 3 + 3 * i + 1] = c1;
+  red[(1 * NQ + q) * T * 3 + 3 * i + 2] = c2;
+  __syncthreads();
   double* pb = F.tpart + (size_t)b * nt * nt * T * 3;
-  for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
-    const int buf = it & 1;
-    const int tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < ntiles)  // the other buffer was released by the previous tile's barriers
-      bulk_stage(tsm + (buf ^ 1) * kTopTileEntries, tiles + (size_t)tn * kTopTileEntries,
-                 kTopTileEntries * sizeof(double), &s_mbar[buf ^ 1]);
-    int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((I + 1) * (I + 2) / 2 <= t) ++I;
-    while (I * (I + 1) / 2 > t) --I;
-    const int J = t - I * (I + 1) / 2;
-    for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
-      const int r = e / 3, c = e - 3 * r;
-      gI[e] = I * T + r < K ? __ldcg(g + 3 * (I * T + r) + c) : 0.0;
-      gJ[e] = J * T + r < K ? __ldcg(g + 3 * (J * T + r) + c) : 0.0;
-    }
-    mbar_wait(&s_mbar[buf], phase[buf]);
-    phase[buf] ^= 1u;
-    __syncthreads();
-    const double* st = tsm + buf * kTopTileEntries;
-    const int i = threadIdx.x % T, q = threadIdx.x / T;
-    {  // row i of S_IJ g_J over columns [q T/NQ, (q+1) T/NQ)
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 8
-      for (int j = q * (T / NQ); j < (q + 1) * (T / NQ); ++j) {
-        const double sv = st[i + j * LD];
-        a0 = fma(sv, gJ[3 * j + 0], a0);
-        a1 = fma(sv, gJ[3 * j + 1], a1);
-        a2 = fma(sv, gJ[3 * j + 2], a2);
-      }
-      red[0][q][3 * i + 0] = a0;
-      red[0][q][3 * i + 1] = a1;
-      red[0][q][3 * i + 2] = a2;
-    }
-    if (I != J) {  // column i of S_IJ (= row i of S_JI) against g_I over rows [q T/NQ, (q+1) T/NQ)
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 8
-      for (int r = q * (T / NQ); r < (q + 1) * (T / NQ); ++r) {
-        const double sv = st[r + i * LD];
-        a0 = fma(sv, gI[3 * r + 0], a0);
-        a1 = fma(sv, gI[3 * r + 1], a1);
-        a2 = fma(sv, gI[3 * r + 2], a2);
-      }
-      red[1][q][3 * i + 0] = a0;
-      red[1][q][3 * i + 1] = a1;
-      red[1][q][3 * i + 2] = a2;
-    }
-    __syncthreads();  // the tile buffer and gI/gJ are free from here on
-    for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
-      double v = red[0][0][e];
+  for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+    double v = red[e];
 #pragma unroll
-      for (int qq = 1; qq < NQ; ++qq) v += red[0][qq][e];
-      __stcg(pb + ((size_t)I * nt + J) * T * 3 + e, v);  // block I, slot J
-      if (I != J) {
-        double w = red[1][0][e];
+    for (int qq = 1; qq < NQ; ++qq) v += red[qq * T * 3 + e];
+    __stcg(pb + ((size_t)I * nt + J) * T * 3 + e, v);  // block I, slot J
+    if (I != J) {
+      double w = red[NQ * T * 3 + e];
 #pragma unroll
-        for (int qq = 1; qq < NQ; ++qq) w += red[1][qq][e];
-        __stcg(pb + ((size_t)J * nt + I) * T * 3 + e, w);  // block J, slot I
-      }
+      for (int qq = 1; qq < NQ; ++qq) w += red[(NQ + qq) * T * 3 + e];
+      __stcg(pb + ((size_t)J * nt + I) * T * 3 + e, w);  // block J, slot I
     }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* cnt = F.tcnt + (size_t)b * nt;
+    s_last[0] = atomicAdd(cnt + I, 1u) == (unsigned)nt - 1 ? I : -1;
+    s_last[1] = (I != J && atomicAdd(cnt + J, 1u) == (unsigned)nt - 1) ? J : -1;
+  }
+  __syncthreads();
+  for (int w = 0; w < 2; ++w) {
+    const int B = s_last[w];
+    if (B < 0) continue;
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned* cnt = F.tcnt + (size_t)b * nt;
-      s_last[0] = atomicAdd(cnt + I, 1u) == (unsigned)nt - 1 ? I : -1;
-      s_last[1] = (I != J && atomicAdd(cnt + J, 1u) == (unsigned)nt - 1) ? J : -1;
+    const double* pr = pb + (size_t)B * nt * T * 3;
+    for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
+      double v = 0.0;
+      int S = 0;
+      for (; S + 16 <= nt; S += 16) {  // 16 independent loads in flight, summed in slot order
+        double l[16];
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) l[qq] = __ldcg(pr + (size_t)(S + qq) * T * 3 + e);
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) v += l[qq];
+      }
+      for (; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);
+      gI[e] = v;
     }
     __syncthreads();
-    for (int w = 0; w < 2; ++w) {
-      const int B = s_last[w];
-      if (B < 0) continue;
-      __threadfence();
-      const double* pr = pb + (size_t)B * nt * T * 3;
-      for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
-        double v = 0.0;
-        int S = 0;
-        for (; S + 16 <= nt; S += 16) {  // 16 independent loads in flight, summed in slot order
-          double l[16];
-#pragma unroll
-          for (int qq = 0; qq < 16; ++qq) l[qq] = __ldcg(pr + (size_t)(S + qq) * T * 3 + e);
-#pragma unroll
-          for (int qq = 0; qq < 16; ++qq) v += l[qq];
-        }
-        for (; S < nt; ++S) v += __ldcg(pr + (size_t)S * T * 3 + e);
-        gI[e] = v;
-      }
-      __syncthreads();
-      if (threadIdx.x < T && B * T + (int)threadIdx.x < K) {
-        const int k = B * T + threadIdx.x;
-        const double v[3] = {gI[3 * threadIdx.x + 0], gI[3 * threadIdx.x + 1], gI[3 * threadIdx.x + 2]};
-        const int row = F.tcols[k];
-        double* xo = F.x + ((size_t)b * F.n + row) * 3;
-        xo[0] = v[0];
-        xo[1] = v[1];
-        xo[2] = v[2];
-        io.store(b, row, v);
-      }
-      if (threadIdx.x == 0) F.tcnt[(size_t)b * nt + B] = 0;  // every partial of B has arrived: reset for the next solve
-      __syncthreads();
+    if (threadIdx.x < T && B * T + (int)threadIdx.x < K) {
+      const int k = B * T + threadIdx.x;
+      const double v[3] = {gI[3 * threadIdx.x + 0], gI[3 * threadIdx.x + 1], gI[3 * threadIdx.x + 2]};
+      const int row = F.tcols[k];
+      double* xo = F.x + ((size_t)b * F.n + row) * 3;
+      xo[0] = v[0];
+      xo[1] = v[1];
+      xo[2] = v[2];
+      io.store(b, row, v);
     }
+    if (threadIdx.x == 0) F.tcnt[(size_t)b * nt + B] = 0;  // every partial of B has arrived: reset for the next solve
+    __syncthreads();
   }
 }
 
@@ -995,8 +980,8 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     const dim3 gg((f->ktop + kSolveThreads - 1) / kSolveThreads, (unsigned)f->nbatch);
     sptrsv_top_gather<IO><<<gg, kSolveThreads, 0, stream>>>(v, io);
     QN_CHECK_LAUNCH();
-    const dim3 ga((unsigned)std::min(f->tnt * (f->tnt + 1) / 2, f->grid_top), (unsigned)f->nbatch);
-    sptrsv_top_sym<IO><<<ga, kSolveThreads, 2 * kTopTileEntries * sizeof(double), stream>>>(v, io);
+    const dim3 ga((unsigned)(f->tnt * (f->tnt + 1) / 2), (unsigned)f->nbatch);
+    sptrsv_top_sym<IO><<<ga, kSolveThreads, 0, stream>>>(v, io);
     QN_CHECK_LAUNCH();
   }
   if (nb > 0) {
@@ -1012,15 +997,6 @@ int prepare_solve_kernels(qn_factor* f) {
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->smem_b));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_forward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   QN_CUDA(cudaFuncSetAttribute(sptrsv_backward<IO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  if (f->ktop > 0) {
-    const int tsm = 2 * kTopTileEntries * sizeof(double);
-    QN_CUDA(cudaFuncSetAttribute(sptrsv_top_sym<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm));
-    int per = 0, dev = 0, sms = 0;
-    QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sptrsv_top_sym<IO>, kSolveThreads, tsm));
-    QN_CUDA(cudaGetDevice(&dev));
-    QN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    f->grid_top = std::max(1, per) * sms;
-  }
   if (f->batch_smem > 0)
     QN_CUDA(cudaFuncSetAttribute(sptrsv_batch<IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, f->batch_smem));
   int per_f = 0, per_b = 0, dev = 0, sms = 0;

@@ -293,14 +293,43 @@ __device__ __forceinline__ void publish(unsigned* flag, unsigned epoch) {
   }
 }
 
-// persistent-CTA ticket loop helpers; sched = [ticket, exited, epoch]
-__device__ __forceinline__ int next_ticket(unsigned* sched, int* s_item) {
-  __syncthreads();  // previous item fully done with shared memory
+// Lookahead ticket pipe of the persistent solve kernels: a CTA holds the ticket
+// it works on and the next one, whose 64-byte task descriptor is already being
+// copied into shared memory (cp.async, 4 x 16 B) while the current task runs,
+// so a task starts without a dependent descriptor load.  Tickets stay
+// monotone per CTA and every dependency has a smaller ticket, so the waits
+// cannot deadlock (the smallest unfinished ticket is always some CTA's current
+// one).
+static_assert(sizeof(qn_fdesc) == 64 && sizeof(qn_bdesc) == 64, "descriptor prefetch copies 64 bytes");
+struct alignas(16) DescSlot {
+  unsigned char bytes[64];
+};
+__device__ __forceinline__ void desc_prefetch(const FactorView& F, int item, int nfi, int total, DescSlot* dst) {
+  if (threadIdx.x < 4 && item < total) {
+    const unsigned char* src = item < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + item / F.nbatch)
+                                          : reinterpret_cast<const unsigned char*>(F.bdesc + (item - nfi) / F.nbatch);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst->bytes + 16 * threadIdx.x);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 16 * threadIdx.x) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// take the next ticket (thread 0) and start its descriptor copy; returns it
+__device__ __forceinline__ int pipe_next(const FactorView& F, unsigned* sched, int* s_item, int nfi, int total,
+                                         DescSlot* dst) {
+  __syncthreads();  // the previous task is done with shared memory
   if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
   __syncthreads();
-  return *s_item;
+  const int item = *s_item;
+  desc_prefetch(F, item, nfi, total, dst);
+  return item;
+}
+// the current task's descriptor (all but the newest cp.async group) is in place
+__device__ __forceinline__ void pipe_ready() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncthreads();
 }
 
+// persistent-CTA ticket loop helpers; sched = [ticket, exited, epoch]
 __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const FactorView& F, int kid) {
   if (threadIdx.x == 0) {
     __threadfence();
@@ -323,13 +352,13 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
 // children, gather their updates, v = Z f, publish.
 template <class IO>
 __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp, uint64_t* mbar, unsigned& phase) {
+                                         int lane, int warp, uint64_t* mbar, unsigned& phase, const qn_fdesc* sdesc) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
   if (!io.active(b)) return;
   trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
-  const qn_fdesc d = F.fdesc[tid];
+  const qn_fdesc d = *sdesc;  // prefetched into shared memory by the ticket pipe
   const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
   const int R = hi - lo;
   const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
@@ -473,13 +502,14 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
 // backward share one persistent kernel, so y_J is waited for explicitly.
 template <class IO>
 __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase) {
+                                         int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase,
+                                         const qn_bdesc* sdesc) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
   if (!io.active(b)) return;
   trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
-  const qn_bdesc d = F.bdesc[tid];
+  const qn_bdesc d = *sdesc;  // prefetched into shared memory by the ticket pipe
   const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
   const int64_t R0 = d.rows;
   double* w = sm + F.bwd_entries;
@@ -573,11 +603,17 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (;;) {
-    const int item = next_ticket(sched, &s_item);
-    if (item >= total) break;
-    fwd_task(F, io, item, s_epoch, sm, lane, warp, &s_mbar, phase);
+  __shared__ DescSlot s_desc[2];
+  int cur = pipe_next(F, sched, &s_item, total, total, &s_desc[0]), slot = 0;
+  while (cur < total) {
+    const int nxt = pipe_next(F, sched, &s_item, total, total, &s_desc[slot ^ 1]);
+    pipe_ready();
+    fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
+             reinterpret_cast<const qn_fdesc*>(s_desc[slot].bytes));
+    cur = nxt;
+    slot ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   cta_exit(sched, s_epoch, F, 4);
 }
 
@@ -595,11 +631,17 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 5, 0);
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (;;) {
-    const int item = next_ticket(sched, &s_item);
-    if (item >= total) break;
-    bwd_task(F, io, item, s_epoch, sm, lane, warp, false, &s_mbar, phase);
+  __shared__ DescSlot s_desc[2];
+  int cur = pipe_next(F, sched, &s_item, 0, total, &s_desc[0]), slot = 0;
+  while (cur < total) {
+    const int nxt = pipe_next(F, sched, &s_item, 0, total, &s_desc[slot ^ 1]);
+    pipe_ready();
+    bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase,
+             reinterpret_cast<const qn_bdesc*>(s_desc[slot].bytes));
+    cur = nxt;
+    slot ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   cta_exit(sched, s_epoch, F, 5);
 }
 
@@ -622,14 +664,21 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
   if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
   const int nfi = F.nftask * F.nbatch, total = nfi + F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (;;) {
-    const int item = next_ticket(sched, &s_item);
-    if (item >= total) break;
-    if (item < nfi)
-      fwd_task(F, io, item, s_epoch, sm, lane, warp, &s_mbar, phase);
+  __shared__ DescSlot s_desc[2];
+  int cur = pipe_next(F, sched, &s_item, nfi, total, &s_desc[0]), slot = 0;
+  while (cur < total) {
+    const int nxt = pipe_next(F, sched, &s_item, nfi, total, &s_desc[slot ^ 1]);
+    pipe_ready();
+    if (cur < nfi)
+      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
+               reinterpret_cast<const qn_fdesc*>(s_desc[slot].bytes));
     else
-      bwd_task(F, io, item - nfi, s_epoch, sm, lane, warp, true, &s_mbar, phase);
+      bwd_task(F, io, cur - nfi, s_epoch, sm, lane, warp, true, &s_mbar, phase,
+               reinterpret_cast<const qn_bdesc*>(s_desc[slot].bytes));
+    cur = nxt;
+    slot ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   cta_exit(sched, s_epoch, F, 5);
 }
 

@@ -64,7 +64,8 @@ struct FactorView {
   unsigned* sched;           // [ticket, exited, epoch] forward, then backward; [6] watchdog
   unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
-  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups
+  int32_t lookahead;         // ticket pipe prefetches the next task (many tasks per CTA)
+  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
   double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
   unsigned* tcnt;            // [nbatch][nt] arrivals per row block
@@ -125,6 +126,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.trace = f->d_trace;
   v.ktop = f->ktop;
   v.opts = f->solve_opts;
+  v.lookahead = f->lookahead;
   v.stile = f->d_stile;
   v.tpart = f->d_tpart;
   v.tcnt = f->d_tcnt;
@@ -327,6 +329,35 @@ __device__ __forceinline__ int pipe_next(const FactorView& F, unsigned* sched, i
 __device__ __forceinline__ void pipe_ready() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
   __syncthreads();
+}
+
+// The ticket loop of a persistent solve kernel: body(item, descriptor slot).
+// With lookahead (many tasks per CTA: throughput-bound, e.g. configs[2]) the
+// next descriptor is prefetched during the current task; without it (few
+// tasks per CTA: latency-bound, e.g. configs[1]) a CTA never holds a ticket it
+// is not working on, so an idle CTA can start every ready task.
+template <class Body>
+__device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched, int* s_item, int nfi, int total,
+                                            DescSlot* s_desc, Body body) {
+  if (F.lookahead) {
+    int cur = pipe_next(F, sched, s_item, nfi, total, &s_desc[0]), slot = 0;
+    while (cur < total) {
+      const int nxt = pipe_next(F, sched, s_item, nfi, total, &s_desc[slot ^ 1]);
+      pipe_ready();
+      body(cur, s_desc[slot].bytes);
+      cur = nxt;
+      slot ^= 1;
+    }
+  } else {
+    for (;;) {
+      const int cur = pipe_next(F, sched, s_item, nfi, total, &s_desc[0]);
+      if (cur >= total) break;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+      body(cur, s_desc[0].bytes);
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // persistent-CTA ticket loop helpers; sched = [ticket, exited, epoch]
@@ -604,16 +635,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F,
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  int cur = pipe_next(F, sched, &s_item, total, total, &s_desc[0]), slot = 0;
-  while (cur < total) {
-    const int nxt = pipe_next(F, sched, &s_item, total, total, &s_desc[slot ^ 1]);
-    pipe_ready();
-    fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
-             reinterpret_cast<const qn_fdesc*>(s_desc[slot].bytes));
-    cur = nxt;
-    slot ^= 1;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  ticket_loop(F, sched, &s_item, total, total, s_desc, [&](int cur, const unsigned char* dsc) {
+    fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
+  });
   cta_exit(sched, s_epoch, F, 4);
 }
 
@@ -632,16 +656,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  int cur = pipe_next(F, sched, &s_item, 0, total, &s_desc[0]), slot = 0;
-  while (cur < total) {
-    const int nxt = pipe_next(F, sched, &s_item, 0, total, &s_desc[slot ^ 1]);
-    pipe_ready();
-    bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase,
-             reinterpret_cast<const qn_bdesc*>(s_desc[slot].bytes));
-    cur = nxt;
-    slot ^= 1;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  ticket_loop(F, sched, &s_item, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
+    bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase, reinterpret_cast<const qn_bdesc*>(dsc));
+  });
   cta_exit(sched, s_epoch, F, 5);
 }
 
@@ -665,20 +682,13 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
   const int nfi = F.nftask * F.nbatch, total = nfi + F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  int cur = pipe_next(F, sched, &s_item, nfi, total, &s_desc[0]), slot = 0;
-  while (cur < total) {
-    const int nxt = pipe_next(F, sched, &s_item, nfi, total, &s_desc[slot ^ 1]);
-    pipe_ready();
+  ticket_loop(F, sched, &s_item, nfi, total, s_desc, [&](int cur, const unsigned char* dsc) {
     if (cur < nfi)
-      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
-               reinterpret_cast<const qn_fdesc*>(s_desc[slot].bytes));
+      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
     else
       bwd_task(F, io, cur - nfi, s_epoch, sm, lane, warp, true, &s_mbar, phase,
-               reinterpret_cast<const qn_bdesc*>(s_desc[slot].bytes));
-    cur = nxt;
-    slot ^= 1;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+               reinterpret_cast<const qn_bdesc*>(dsc));
+  });
   cta_exit(sched, s_epoch, F, 5);
 }
 
@@ -1064,6 +1074,10 @@ int prepare_solve_kernels(qn_factor* f) {
   }
   f->grid_f = f->grid_f ? std::min(f->grid_f, gf) : gf;
   f->grid_b = f->grid_b ? std::min(f->grid_b, gb) : gb;
+  // descriptor lookahead pays off when CTAs run many tasks each (c3: 27, c2: 5 per CTA)
+  const int64_t tasks = (int64_t)(f->ftask.size() + f->btask.size()) * f->nbatch;
+  f->lookahead = tasks >= 12 * (int64_t)std::max(f->grid_f, 1) ? 1 : 0;
+  if (f->solve_opts & 2) f->lookahead = 0;
   return QN_OK;
 }
 

@@ -152,9 +152,12 @@ int factor_upload(qn_factor* f) {
     for (int s = 0; s < f->nsup; ++s) max_nc_all = std::max(max_nc_all, f->sup_col[s + 1] - f->sup_col[s]);
     const size_t bsm0 = sizeof(double) * 3 * ((size_t)f->n + (size_t)kBatchWarps * max_nc_all);
     const bool batch_mode = f->nbatch > 1 && bsm0 <= 110 * 1024;
+    // a factor that fits in L2 next to the frame's vectors keeps one copy: the
+    // backward sweep re-reads what the forward sweep pulled into L2 (c2: 30 MB)
+    const bool small = (double)f->nbatch * f->nvals * sizeof(double) <= 48.0 * (1 << 20);
     std::vector<qn_fdesc> fd = f->fdesc;
     std::vector<qn_bdesc> bd = f->bdesc;
-    if (!batch_mode) {
+    if (!batch_mode && !small) {
       int64_t off = 0;
       for (auto& d : fd) {
         const int64_t cnt = (int64_t)(d.hi - d.lo) * std::min(d.hi, d.nc);

@@ -65,6 +65,7 @@ struct FactorView {
   unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
   int32_t lookahead;         // ticket pipe prefetches the next task (many tasks per CTA)
+  int32_t tiled;             // tasks stage Z from the task-tiled copies (TMA) instead of vals (cp.async)
   int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
   double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
@@ -127,6 +128,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.ktop = f->ktop;
   v.opts = f->solve_opts;
   v.lookahead = f->lookahead;
+  v.tiled = f->d_ftile != nullptr;
   v.stile = f->d_stile;
   v.tpart = f->d_tpart;
   v.tcnt = f->d_tcnt;
@@ -398,9 +400,16 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   int* sidx = (int*)(part + 3 * kSolveThreads);
   const double* ub = F.u + (size_t)b * F.nupd * 3;
   // ---- stage everything that does not depend on the children ----
-  if (threadIdx.x == 0) {  // Z tile rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)]: one contiguous block
-    const int cnt = R * kmax;
-    bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
+  if (F.tiled) {  // Z tile rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)]: one contiguous block
+    if (threadIdx.x == 0) {
+      const int cnt = R * kmax;
+      bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
+    }
+  } else {  // small factors: straight from vals, which the backward re-reads from L2
+    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
+    for (int k = warp; k < kmax; k += kSolveWarps)
+      for (int rr = lane; rr < R; rr += 32) cp_async8(zt + k * R + rr, Zg + (int64_t)k * nr + rr);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
   const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
@@ -447,8 +456,12 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
       e2 += __ldcg(uc + 2);
     }
   }
-  mbar_wait(mbar, phase);
-  phase ^= 1u;
+  if (F.tiled) {
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+  } else {
+    cp_async_wait_all();
+  }
   __syncthreads();
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
@@ -549,9 +562,23 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   int* srow = (int*)(sdst + kBwdCols);
   const bool staged = nr - nc <= kStageIdx;
   // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
-  if (threadIdx.x == 0) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
+  if (F.tiled) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
+    if (threadIdx.x == 0) {
+      const int cnt = (k1 - k0) * nr;
+      bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)),
+                 mbar);
+    }
+  } else {
+    const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
     const int cnt = (k1 - k0) * nr;
-    bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int kk = e / nr, r = e - kk * nr;
+      if (r >= k0 + kk)
+        cp_async8(zt + e, Zg + e);
+      else
+        zt[e] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   if (fused)  // the forward of s may still be running: y_J must be complete
     wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask), d.fwd0, d.nfwd, epoch, F.sched);
@@ -566,8 +593,12 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
   const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
   trace_mark(F.trace, tb + 1);
-  mbar_wait(mbar, phase);
-  phase ^= 1u;
+  if (F.tiled) {
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+  } else {
+    cp_async_wait_all();
+  }
   __syncthreads();
   // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
   // (splitting a few-column task's rows over idle warps measured slower: the

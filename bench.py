@@ -375,8 +375,11 @@ def run_ours(args, world, rank, local):
     batched = info.get("nbatch", 1) > 1
     if "nnz_l" in info:
         solve_ms = system.time_kernel("solve", reps=20, stream=sptr)
-        # factor read twice + rhs/y/x/u vectors, per instance
-        solve_bytes = (2 * 8.0 * info["nnz_l"] + 5 * 24.0 * info["n"]) * n_inst
+        # per instance: L of the sparse sweeps read twice (forward, backward), the
+        # dense top's symmetric S^-1 read once (half: K (K + 1) / 2), rhs/y/x/u vectors
+        K = info.get("dense_top", 0) or 0
+        solve_bytes = (2 * 8.0 * info.get("nnz_l_sparse", info["nnz_l"]) + 8.0 * K * (K + 1) / 2
+                       + 5 * 24.0 * info["n"]) * n_inst
         share_solve = solve_ms * sc.iterations / per_frame
     else:  # PCG / AMG system: the CG SpMV stands for the solve (share from the in-graph timeline)
         solve_ms = system.time_kernel("spmv", reps=20, stream=sptr)
@@ -390,7 +393,8 @@ def run_ours(args, world, rank, local):
     dms, dbytes = (tet_ms, tet_bytes) if dom == "tet" else (solve_ms, solve_bytes)
     achieved = dbytes / (dms / 1000.0) / 1e9
     solve_name = ("sptrsv_batch (level-parallel, CTA per instance)" if batched else
-                  "sptrsv_forward+backward" if "nnz_l" in info else "k_pcg_spmv (CG SpMV, SELL-32 fp64)")
+                  ("sptrsv_forward + top (symmetric S^-1) + backward" if info.get("dense_top") else
+                   "sptrsv_forward+backward") if "nnz_l" in info else "k_pcg_spmv (CG SpMV, SELL-32 fp64)")
     roof = {"bound": "hbm", "kernel": "k_tet (per-tet F/SVD/VL/PK1)" if dom == "tet" else solve_name,
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
             "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,
@@ -462,7 +466,8 @@ def run_ours(args, world, rank, local):
                            "parallelism": "replicas" if not sc.batch else f"instances/{world} per rank"},
                 "tet_evals_per_s": tet_evals, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches,
-                "factor": ({"nnz_l": info["nnz_l"], "supernodes": info["n_supernodes"],
+                "factor": ({"nnz_l": info["nnz_l"], "nnz_l_sparse": info.get("nnz_l_sparse"),
+                            "supernodes": info["n_supernodes"],
                             "depth": info["tree_depth"], "factor_s": info["factor_seconds"],
                             "dense_top": info.get("dense_top")} if "nnz_l" in info else info),
                 "build_s": t_build, "passes_per_step": passes / args.steps}

@@ -122,6 +122,8 @@ typedef struct qn_factor_info {
   int64_t n, nnz_a, nnz_l, n_supernodes, max_front, tree_depth, nbatch;
   double factor_seconds, flops;
   int64_t dense_top;  /* columns solved by the dense top block S^-1 (0 = none) */
+  int64_t nnz_l_sparse; /* entries of L in the supernodes solved by the sparse sweeps (not the dense top) */
+  int64_t sinv_stored;  /* entries of S^-1 the top apply reads (lower-triangle tiles, padded) */
 } qn_factor_info;
 
 int qn_factor_create(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,

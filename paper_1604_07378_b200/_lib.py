@@ -55,6 +55,7 @@ class FactorInfo(C.Structure):
         ("n", C.c_int64), ("nnz_a", C.c_int64), ("nnz_l", C.c_int64), ("n_supernodes", C.c_int64),
         ("max_front", C.c_int64), ("tree_depth", C.c_int64), ("nbatch", C.c_int64),
         ("factor_seconds", C.c_double), ("flops", C.c_double), ("dense_top", C.c_int64),
+        ("nnz_l_sparse", C.c_int64), ("sinv_stored", C.c_int64),
     ]
 
 

@@ -402,6 +402,14 @@ int qn_factor_info_get(const qn_factor* f, qn_factor_info* info) {
   info->factor_seconds = f->factor_seconds;
   info->flops = f->flops;
   info->dense_top = f->ktop;
+  int64_t sparse = 0;
+  for (int s = 0; s < f->nsup; ++s) {
+    if (!f->is_top.empty() && f->is_top[s]) continue;
+    const int64_t nc = f->sup_col[s + 1] - f->sup_col[s], nr = f->sup_row_ptr[s + 1] - f->sup_row_ptr[s];
+    sparse += nr * nc - nc * (nc - 1) / 2;  // L's lower trapezoid of the supernode
+  }
+  info->nnz_l_sparse = sparse;
+  info->sinv_stored = f->ktop > 0 ? (int64_t)f->tnt * (f->tnt + 1) / 2 * kTopTile * (kTopTile + 1) : 0;
   return QN_OK;
 }
 

@@ -149,7 +149,8 @@ int hc_factor_solve(int64_t n, const int64_t* indptr, const int32_t* indices, co
 extern "C" int hc_factor_structure(int64_t n, const int64_t* indptr, const int32_t* indices, const double* values,
                                    const double* coords, int64_t* sizes, int32_t* sup, int64_t cap) {
   qn_factor f;
-  int rc = qn::factor_build_host(&f, n, indptr, indices, values, 1, coords);
+  const int64_t nbatch = sizes[7] > 0 ? sizes[7] : 1;  // in: instances (values = nbatch x nnz)
+  int rc = qn::factor_build_host(&f, n, indptr, indices, values, nbatch, coords);
   if (rc) return rc;
   sizes[0] = f.n;
   sizes[1] = f.nsup;

@@ -250,74 +250,6 @@ int factor_upload(qn_factor* f) {
   f->batch_zmax = (int32_t)((zmax + 1) / 2 * 2);  // keep the second buffer 16-byte aligned
   const size_t bsm = sizeof(double) * 3 * ((size_t)f->n + (size_t)kBatchWarps * max_nc);
   f->batch_smem = (f->nbatch > 1 && bsm <= 110 * 1024) ? (int)bsm : 0;
-  if (f->batch_smem > 0) {
-    // level-ordered per-instance copies of Z, chunked for TMA staging
-    const int64_t cap = kBatchChunkEntries;
-    std::vector<int32_t> ord(2 * (size_t)f->nsup);
-    std::vector<int64_t> zoff(2 * (size_t)f->nsup);
-    std::vector<int4> chunks;
-    std::vector<int64_t> chz;
-    int64_t total = 0, cmax = 0;
-    auto block = [&](int s) { return (int64_t)(f->sup_col[s + 1] - f->sup_col[s]) * (f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]); };
-    for (int dir = 0; dir < 2; ++dir) {
-      const std::vector<int32_t>& lp = dir == 0 ? f->hlev_ptr : f->dlev_ptr;
-      const std::vector<int32_t>& ls = dir == 0 ? f->hlev_sup : f->dlev_sup;
-      int64_t off = 0;
-      int pos = 0;
-      for (size_t L = 0; L + 1 < lp.size(); ++L) {
-        int c0 = pos;
-        int64_t z0 = off;
-        bool first = true;
-        for (int i = lp[L]; i < lp[L + 1]; ++i) {
-          const int s = ls[i];
-          const int64_t e = (block(s) + 1) / 2 * 2;
-          QN_REQUIRE(e <= cap, QN_ERR_UNSUPPORTED, "factor: supernode too large for the batched solve chunks");
-          if (off + e - z0 > cap) {  // close the chunk
-            chunks.push_back({c0, pos, first ? 1 : 0, dir});
-            chz.push_back(z0);
-            chz.push_back(off);
-            cmax = std::max(cmax, off - z0);
-            first = false;
-            c0 = pos;
-            z0 = off;
-          }
-          ord[(size_t)dir * f->nsup + pos] = s;
-          zoff[(size_t)dir * f->nsup + pos] = off;
-          off += e;
-          ++pos;
-        }
-        if (pos > c0) {
-          chunks.push_back({c0, pos, first ? 1 : 0, dir});
-          chz.push_back(z0);
-          chz.push_back(off);
-          cmax = std::max(cmax, off - z0);
-        }
-      }
-      if (dir == 0) f->nfch = (int32_t)chunks.size();
-      total = std::max(total, off);
-    }
-    f->nbch = (int32_t)chunks.size() - f->nfch;
-    f->bz_n = total;
-    f->bchunk_max = (int32_t)cmax;
-    std::vector<double> zf((size_t)f->nbatch * total, 0.0), zb((size_t)f->nbatch * total, 0.0);
-#pragma omp parallel for schedule(static)
-    for (int64_t b = 0; b < f->nbatch; ++b)
-      for (int dir = 0; dir < 2; ++dir)
-        for (int p = 0; p < f->nsup; ++p) {
-          const int s = ord[(size_t)dir * f->nsup + p];
-          const double* src = f->vals.data() + (size_t)b * f->nvals + f->sup_val_ptr[s];
-          double* dst = (dir == 0 ? zf : zb).data() + (size_t)b * total + zoff[(size_t)dir * f->nsup + p];
-          std::copy(src, src + block(s), dst);
-        }
-    if ((rc = dev_upload(&f->d_bzf, zf.data(), zf.size())) || (rc = dev_upload(&f->d_bzb, zb.data(), zb.size())) ||
-        (rc = dev_upload(&f->d_bord, ord.data(), ord.size())) ||
-        (rc = dev_upload(&f->d_bzoff, zoff.data(), zoff.size())) ||
-        (rc = dev_upload(&f->d_bchunk, chunks.data(), chunks.size())) ||
-        (rc = dev_upload(&f->d_bchz, chz.data(), chz.size())))
-      return rc;
-    f->batch_smem = (int)(bsm + 2 * sizeof(double) * (size_t)cmax);
-    QN_REQUIRE(f->batch_smem <= 227 * 1024, QN_ERR_UNSUPPORTED, "factor: batched solve exceeds shared memory");
-  }
   if ((rc = prepare_solve_kernels<PlainIO>(f))) return rc;
   f->on_device = true;
   return QN_OK;
@@ -332,8 +264,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
                   f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt,
-                  f->d_ftile,   f->d_btile,       f->d_bzf,       f->d_bzb,       f->d_bord,
-                  f->d_bzoff,   f->d_bchunk,      f->d_bchz};
+                  f->d_ftile,   f->d_btile};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

@@ -127,17 +127,6 @@ struct qn_factor {
   bool fused = false;             // forward + backward in one persistent kernel (no dense top)
   int smem_fused = 0, grid_fused = 0;
   int batch_smem = 0;             // > 0: batched mode, one CTA per instance (bytes of shared memory)
-  // batched mode: Z re-stored per instance in forward (height) and backward
-  // (depth) level order, cut into chunks of whole supernodes of one level that
-  // one TMA bulk copy stages (sptrsv_batch, double-buffered)
-  double* d_bzf = nullptr;        // nbatch x bz_n
-  double* d_bzb = nullptr;
-  int64_t bz_n = 0;               // entries per instance (each supernode block padded to an even count)
-  int32_t* d_bord = nullptr;      // [2][nsup]: supernode at each forward / backward position
-  int64_t* d_bzoff = nullptr;     // [2][nsup]: its block offset in bzf / bzb
-  int4* d_bchunk = nullptr;       // [nfch + nbch]: {pos_begin, pos_end, new_level, 0}
-  int64_t* d_bchz = nullptr;      // [nfch + nbch][2]: z range of the chunk
-  int32_t nfch = 0, nbch = 0, bchunk_max = 0;
   int32_t batch_max_nc = 0, batch_zmax = 0;  // batched mode: widest supernode, largest Z block (entries)
   bool on_device = false;
   int32_t lookahead = 0;          // persistent solve ticket lookahead (prepare_solve_kernels)
@@ -150,8 +139,7 @@ constexpr int64_t kTopMax = 4096;
 constexpr int kTopTile = 64;            // symmetric top apply: S^-1 stored as 64 x 64 lower-triangle tiles       // max columns of the dense top block (S^-1 <= 134 MB)
 constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
 constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
-constexpr int64_t kBwdTaskCols = 64;
-constexpr int64_t kBatchChunkEntries = 5376;  // batched solve: Z entries per TMA-staged chunk (42 KB, 2 buffers)    // max columns of a backward task
+constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
 constexpr int64_t kSmemPerCtaPair = 110 * 1024;  // dynamic smem per CTA with two CTAs per SM (228 KB - reserved/static)
 // bottom-of-tree subtree collapse (see factor_build_host)
 constexpr int32_t kCollapseHeight = 2;  // swept on c1-c3 with the current solve kernels: 2 > 3 (+3.6 % at c2), 1 and 4 slower

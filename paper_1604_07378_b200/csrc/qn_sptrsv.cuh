@@ -53,14 +53,6 @@ struct FactorView {
   const int32_t* hlev_sup;
   const int32_t* dlev_ptr;   // batched: supernodes by depth (backward levels)
   const int32_t* dlev_sup;
-  const double* bzf;        // batched: level-ordered Z copies (forward by height, backward by depth)
-  const double* bzb;
-  int64_t bz_n;
-  const int32_t* bord;      // [2][nsup]
-  const int64_t* bzoff;     // [2][nsup]
-  const int4* bchunk;       // {pos_begin, pos_end, new_level, dir}
-  const int64_t* bchz;      // [chunk][2]
-  int32_t nfch, nbch, bchunk_max;
   const double* vals;
   const double* ftile;       // task-tiled Z copies (persistent kernels): forward / backward
   const double* btile;
@@ -103,16 +95,6 @@ inline FactorView factor_view(const qn_factor* f) {
   v.hlev_sup = f->d_hlev_sup;
   v.dlev_ptr = f->d_dlev_ptr;
   v.dlev_sup = f->d_dlev_sup;
-  v.bzf = f->d_bzf;
-  v.bzb = f->d_bzb;
-  v.bz_n = f->bz_n;
-  v.bord = f->d_bord;
-  v.bzoff = f->d_bzoff;
-  v.bchunk = f->d_bchunk;
-  v.bchz = f->d_bchz;
-  v.nfch = f->nfch;
-  v.nbch = f->nbch;
-  v.bchunk_max = f->bchunk_max;
   v.nvals = f->nvals;
   v.nupd = f->nupd;
   v.sup_col = f->d_sup_col;
@@ -891,45 +873,27 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
 // ---- batched small systems (configs[3]): one CTA per instance walks its whole
 // tree level by level — forward by height (leaves first), backward by depth
 // (root first) — with the independent supernodes of a level on different
-// warps, so the sequential chain is the tree height, not the supernode count.
-// No inter-CTA flags: thousands of instances run as thousands of independent
-// CTAs.  Each instance's Z is stored twice in level order (forward, backward)
-// and cut into chunks of whole supernodes of one level; the chunks stream into
-// two shared-memory buffers by TMA bulk copies, the next chunk in flight while
-// the current one is multiplied (so the FMAs read shared memory, not global).
-// The right-hand side of every row is staged once; y/x of the instance live in
-// shared memory (x overwrites y in place during the backward sweep); each warp
-// keeps its supernode's f / y_J in a private shared-memory slice; the update
-// vectors stay in the instance's global (L2) slice.
+// warps and one CTA barrier per level, so the sequential chain is the tree
+// height, not the supernode count.  No inter-CTA flags: thousands of
+// instances run as thousands of independent CTAs.  The right-hand side of
+// every row is staged once; y/x of the instance live in shared memory (x
+// overwrites y in place during the backward sweep); each warp keeps its
+// supernode's f / y_J in a private shared-memory slice; the update vectors
+// stay in the instance's global (L2) slice.
 constexpr int kBatchThreads = 128, kBatchWarps = kBatchThreads / 32;
 constexpr int kBatchCols = 4;  // backward: columns per pass (12 independent chains per lane)
 
 template <class IO>
-__global__ void __launch_bounds__(kBatchThreads, 2) sptrsv_batch(FactorView F, IO io) {
-  extern __shared__ __align__(16) double sm[];  // zbuf[2][chunk_max] | yx[n*3] | fw[kBatchWarps][max_nc*3]
-  __shared__ uint64_t mbar[2];
+__global__ void __launch_bounds__(kBatchThreads, 8) sptrsv_batch(FactorView F, IO io) {
+  extern __shared__ double sm[];  // yx[n*3] | fw[kBatchWarps][max_nc*3]
   const int b = blockIdx.x;
   if (!io.active(b)) return;
   const int n = F.n;
-  double* zbuf = sm;
-  double* yx = sm + 2 * (size_t)F.bchunk_max;
+  double* yx = sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* fw = yx + 3 * n + (size_t)warp * 3 * F.batch_max_nc;
+  double* fw = sm + 3 * n + (size_t)warp * 3 * F.batch_max_nc;
   double* ub = F.u + (size_t)b * F.nupd * 3;
-  if (tid < 2) {
-    const unsigned m = (unsigned)__cvta_generic_to_shared(&mbar[tid]);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m) : "memory");
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  unsigned phase[2] = {0u, 0u};
-  const int nch = F.nfch + F.nbch;
-  auto stage = [&](int c) {  // chunk c -> buffer c & 1 (thread 0)
-    const double* src = (c < F.nfch ? F.bzf : F.bzb) + (size_t)b * F.bz_n + F.bchz[2 * c];
-    const unsigned bytes = (unsigned)((F.bchz[2 * c + 1] - F.bchz[2 * c]) * sizeof(double));
-    bulk_stage(zbuf + (size_t)(c & 1) * F.bchunk_max, src, bytes, &mbar[c & 1]);
-  };
-  if (tid == 0) stage(0);
+  const double* vb = F.vals + (size_t)b * F.nvals;
   for (int p = tid; p < n; p += blockDim.x) {  // b for every row (independent loads)
     double v[3];
     io.rhs(b, p, v);
@@ -937,119 +901,123 @@ __global__ void __launch_bounds__(kBatchThreads, 2) sptrsv_batch(FactorView F, I
     yx[3 * p + 1] = v[1];
     yx[3 * p + 2] = v[2];
   }
-  for (int c = 0; c < nch; ++c) {
-    const int4 ch = F.bchunk[c];
-    // chunk c + 1 streams into the other buffer (freed by the barrier that ended chunk c - 1)
-    if (tid == 0 && c + 1 < nch) stage(c + 1);
-    if (ch.z) __syncthreads();  // a new level: the previous level's y / u / x are complete
-    mbar_wait(&mbar[c & 1], phase[c & 1]);
-    phase[c & 1] ^= 1u;
-    const double* zc = zbuf + (size_t)(c & 1) * F.bchunk_max - F.bchz[2 * c];  // indexed by level-order offsets
-    const bool fwd = c < F.nfch;
-    const int dir = fwd ? 0 : 1;
-    for (int pos = ch.x + warp; pos < ch.y; pos += kBatchWarps) {
-      const int s = F.bord[dir * F.nsup + pos];
-      const double* Z = zc + F.bzoff[dir * F.nsup + pos];
+  __syncthreads();
+  // ---- forward: y = L^-1 b, one level of independent supernodes at a time ----
+  for (int L = 0; L < F.nhlev; ++L) {
+    for (int i = F.hlev_ptr[L] + warp; i < F.hlev_ptr[L + 1]; i += kBatchWarps) {
+      const int s = F.hlev_sup[i];
       const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
       const int64_t R0 = F.sup_row_ptr[s];
       const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
-      if (fwd) {
-        for (int p = lane; p < nc; p += 32) {  // f = b_J - children updates
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-          for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
+      const double* Z = vb + F.sup_val_ptr[s];
+      for (int p = lane; p < nc; p += 32) {  // f = b_J - children updates
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
+          const double* uc = ub + 3 * (size_t)F.cidx[q];
+          a0 += __ldcg(uc);
+          a1 += __ldcg(uc + 1);
+          a2 += __ldcg(uc + 2);
+        }
+        fw[3 * p + 0] = yx[3 * (c0 + p) + 0] - a0;
+        fw[3 * p + 1] = yx[3 * (c0 + p) + 1] - a1;
+        fw[3 * p + 2] = yx[3 * (c0 + p) + 2] - a2;
+      }
+      __syncwarp();
+      for (int r = lane; r < nr; r += 32) {  // v = Z f (lanes over rows: coalesced Z)
+        const int kmax = r < nc ? r + 1 : nc;
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+        if (r >= nc)  // children's updates on this bottom row (independent of the FMAs)
+          for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
             const double* uc = ub + 3 * (size_t)F.cidx[q];
-            a0 += __ldcg(uc);
-            a1 += __ldcg(uc + 1);
-            a2 += __ldcg(uc + 2);
+            e0 += __ldcg(uc);
+            e1 += __ldcg(uc + 1);
+            e2 += __ldcg(uc + 2);
           }
-          fw[3 * p + 0] = yx[3 * (c0 + p) + 0] - a0;
-          fw[3 * p + 1] = yx[3 * (c0 + p) + 1] - a1;
-          fw[3 * p + 2] = yx[3 * (c0 + p) + 2] - a2;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        int k = 0;
+        for (; k + 8 <= kmax; k += 8) {
+          double l[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) l[q] = __ldg(Z + r + (int64_t)(k + q) * nr);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            a0 = fma(l[q], fw[3 * (k + q) + 0], a0);
+            a1 = fma(l[q], fw[3 * (k + q) + 1], a1);
+            a2 = fma(l[q], fw[3 * (k + q) + 2], a2);
+          }
         }
-        __syncwarp();
-        for (int r = lane; r < nr; r += 32) {  // v = Z f (lanes over rows: conflict-free shared memory)
-          const int kmax = r < nc ? r + 1 : nc;
-          double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-          if (r >= nc)  // children's updates on this bottom row (independent of the FMAs)
-            for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
-              const double* uc = ub + 3 * (size_t)F.cidx[q];
-              e0 += __ldcg(uc);
-              e1 += __ldcg(uc + 1);
-              e2 += __ldcg(uc + 2);
-            }
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
-          int k = 0;
-          for (; k + 2 <= kmax; k += 2) {  // two chains per coordinate
-            const double l = Z[r + (int64_t)k * nr], m = Z[r + (int64_t)(k + 1) * nr];
-            a0 = fma(l, fw[3 * k + 0], a0);
-            a1 = fma(l, fw[3 * k + 1], a1);
-            a2 = fma(l, fw[3 * k + 2], a2);
-            b0 = fma(m, fw[3 * k + 3], b0);
-            b1 = fma(m, fw[3 * k + 4], b1);
-            b2 = fma(m, fw[3 * k + 5], b2);
-          }
-          if (k < kmax) {
-            const double l = Z[r + (int64_t)k * nr];
-            a0 = fma(l, fw[3 * k + 0], a0);
-            a1 = fma(l, fw[3 * k + 1], a1);
-            a2 = fma(l, fw[3 * k + 2], a2);
-          }
-          a0 += b0;
-          a1 += b1;
-          a2 += b2;
+        for (; k < kmax; ++k) {
+          const double l = __ldg(Z + r + (int64_t)k * nr);
+          a0 = fma(l, fw[3 * k + 0], a0);
+          a1 = fma(l, fw[3 * k + 1], a1);
+          a2 = fma(l, fw[3 * k + 2], a2);
+        }
+        if (r < nc) {
+          yx[3 * (c0 + r) + 0] = a0;
+          yx[3 * (c0 + r) + 1] = a1;
+          yx[3 * (c0 + r) + 2] = a2;
+        } else {
+          double* us = ub + (F.sup_upd_ptr[s] + (r - nc)) * 3;
+          __stcg(us + 0, e0 + a0);
+          __stcg(us + 1, e1 + a1);
+          __stcg(us + 2, e2 + a2);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  // ---- backward: x = L^-T y (in place over y), root level first ----
+  for (int L = 0; L < F.ndlev; ++L) {
+    for (int i = F.dlev_ptr[L] + warp; i < F.dlev_ptr[L + 1]; i += kBatchWarps) {
+      const int s = F.dlev_sup[i];
+      const int c0 = F.sup_col[s], nc = F.sup_col[s + 1] - c0;
+      const int64_t R0 = F.sup_row_ptr[s];
+      const int nr = (int)(F.sup_row_ptr[s + 1] - R0);
+      const double* Z = vb + F.sup_val_ptr[s];
+      for (int p = lane; p < 3 * nc; p += 32) fw[p] = yx[3 * c0 + p];  // y_J (x_J overwrites it)
+      __syncwarp();
+      for (int k0 = 0; k0 < nc; k0 += kBatchCols) {  // kBatchCols columns per pass, lanes over rows
+        const int nv = min(kBatchCols, nc - k0);
+        double a[kBatchCols][3];
+#pragma unroll
+        for (int j = 0; j < kBatchCols; ++j) a[j][0] = a[j][1] = a[j][2] = 0.0;
+        for (int r = k0 + lane; r < nr; r += 32) {
+          double w0, w1, w2;
           if (r < nc) {
-            yx[3 * (c0 + r) + 0] = a0;
-            yx[3 * (c0 + r) + 1] = a1;
-            yx[3 * (c0 + r) + 2] = a2;
+            w0 = fw[3 * r + 0];
+            w1 = fw[3 * r + 1];
+            w2 = fw[3 * r + 2];
           } else {
-            double* us = ub + (F.sup_upd_ptr[s] + (r - nc)) * 3;
-            __stcg(us + 0, e0 + a0);
-            __stcg(us + 1, e1 + a1);
-            __stcg(us + 2, e2 + a2);
+            const int row = F.sup_rows[R0 + r];
+            w0 = -yx[3 * row + 0];
+            w1 = -yx[3 * row + 1];
+            w2 = -yx[3 * row + 2];
           }
-        }
-      } else {
-        for (int p = lane; p < 3 * nc; p += 32) fw[p] = yx[3 * c0 + p];  // y_J (x_J overwrites it)
-        __syncwarp();
-        for (int k0 = 0; k0 < nc; k0 += kBatchCols) {  // kBatchCols columns per pass, lanes over rows
-          const int nv = min(kBatchCols, nc - k0);
-          double a[kBatchCols][3];
+          double l[kBatchCols];
 #pragma unroll
-          for (int j = 0; j < kBatchCols; ++j) a[j][0] = a[j][1] = a[j][2] = 0.0;
-          for (int r = k0 + lane; r < nr; r += 32) {
-            double w0, w1, w2;
-            if (r < nc) {
-              w0 = fw[3 * r + 0];
-              w1 = fw[3 * r + 1];
-              w2 = fw[3 * r + 2];
-            } else {
-              const int row = F.sup_rows[R0 + r];
-              w0 = -yx[3 * row + 0];
-              w1 = -yx[3 * row + 1];
-              w2 = -yx[3 * row + 2];
-            }
-#pragma unroll
-            for (int j = 0; j < kBatchCols; ++j) {
-              const double l = (j < nv && r >= k0 + j) ? Z[r + (int64_t)(k0 + j) * nr] : 0.0;
-              a[j][0] = fma(l, w0, a[j][0]);
-              a[j][1] = fma(l, w1, a[j][1]);
-              a[j][2] = fma(l, w2, a[j][2]);
-            }
-          }
+          for (int j = 0; j < kBatchCols; ++j)
+            l[j] = (j < nv && r >= k0 + j) ? __ldg(Z + r + (int64_t)(k0 + j) * nr) : 0.0;
 #pragma unroll
           for (int j = 0; j < kBatchCols; ++j) {
-            const double v0 = warp_sum(a[j][0]), v1 = warp_sum(a[j][1]), v2 = warp_sum(a[j][2]);
-            if (lane == j && j < nv) {
-              yx[3 * (c0 + k0 + j) + 0] = v0;
-              yx[3 * (c0 + k0 + j) + 1] = v1;
-              yx[3 * (c0 + k0 + j) + 2] = v2;
-            }
+            a[j][0] = fma(l[j], w0, a[j][0]);
+            a[j][1] = fma(l[j], w1, a[j][1]);
+            a[j][2] = fma(l[j], w2, a[j][2]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatchCols; ++j) {
+          const double v0 = warp_sum(a[j][0]), v1 = warp_sum(a[j][1]), v2 = warp_sum(a[j][2]);
+          if (lane == j && j < nv) {
+            yx[3 * (c0 + k0 + j) + 0] = v0;
+            yx[3 * (c0 + k0 + j) + 1] = v1;
+            yx[3 * (c0 + k0 + j) + 2] = v2;
           }
         }
       }
       __syncwarp();
     }
-    __syncthreads();  // the chunk's buffer is free for chunk c + 2; its results are visible
+    __syncthreads();
   }
   for (int p = tid; p < n; p += blockDim.x) {  // x -> caller
     const double v[3] = {yx[3 * p + 0], yx[3 * p + 1], yx[3 * p + 2]};

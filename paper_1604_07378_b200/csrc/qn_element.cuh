@@ -177,7 +177,10 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // the next sweep removes what the approximate angle left (~1e-7 relative).
 // Branch-free (lanes never diverge): a converged pair gets t = 0, i.e. the
 // identity rotation c = 1, s = 0, which leaves A and V bit-identical.
-// Returns whether the pair needed a rotation.
+// Returns whether the pair needed a rotation that was not tiny (|t| >= 1e-12):
+// after a sweep of tiny rotations the off-diagonal is ~1e-7 |t| (the fp32
+// angle's error) below the diagonal, under the 1e-18 rotation threshold, so
+// the sweep that would only confirm convergence is skipped.
 __device__ __forceinline__ bool jacobi_rot(double (&A)[3][3], double (&V)[3][3], int p, int q) {
   const double apq = A[p][q];
   const double app = A[p][p], aqq = A[q][q];
@@ -204,7 +207,7 @@ __device__ __forceinline__ bool jacobi_rot(double (&A)[3][3], double (&V)[3][3],
     V[k][p] = c * vkp - s * vkq;
     V[k][q] = s * vkp + c * vkq;
   }
-  return need;
+  return need && fabs(t) >= 1e-12;
 }
 
 // swap eigenpairs i <-> j when A[i][i] < A[j][j] (branch-free); the swapped

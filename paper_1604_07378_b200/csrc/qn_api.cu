@@ -38,6 +38,7 @@ int build_graph(qn_system* S);
 int prepare_kernels(qn_system* S);
 int launch_tet_plain(qn_system* S, const double* x, int b, int mat_sel, double* part, cudaStream_t st);
 int launch_solve_timing(qn_system* S, cudaStream_t st);
+int launch_vcycle(qn_system* S, cudaStream_t st);
 int launch_spmv_timing(qn_system* S, cudaStream_t st);
 __global__ void k_gather_plain(SysView v, const double* x, const double* y, double* out, int b, int inertia,
                                int zero_fixed, double* part);
@@ -656,6 +657,9 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       for (int l = 0; l < nl; ++l) {
         const qn::AmgLevel& L = H.lv[l];
         qn::AmgDevLevel& D = S->h_alev[l];
+        S->amg_nnz.push_back(L.A.ptr.empty() ? 0 : L.A.ptr.back());
+        S->amg_nnz.push_back(L.P.ptr.empty() ? 0 : L.P.ptr.back());
+        S->amg_nnz.push_back(L.R.ptr.empty() ? 0 : L.R.ptr.back());
         D.n = (int32_t)L.A.n;
         D.omega = H.omega_l[l];
         if ((rc = sell_upload(S, L.A.n, L.A.m, L.A.ptr.data(), L.A.col.data(), L.A.val.data(), &D.A))) return fail(rc);
@@ -931,6 +935,8 @@ int qn_system_amg_info(qn_system* S, int64_t* out, int64_t cap) {
   out[0] = nl;
   for (int64_t l = 0; l < nl && l < 10; ++l) out[1 + l] = S->h_alev[l].n;
   out[11] = (int64_t)(S->amg_setup_s * 1000.0);
+  for (int64_t l = 0; l < nl && l < 10 && 12 + 3 * l + 2 < cap; ++l)  // nnz of A, P, R per level
+    for (int k = 0; k < 3; ++k) out[12 + 3 * l + k] = S->amg_nnz[3 * l + k];
   return QN_OK;
 }
 
@@ -1292,7 +1298,19 @@ int qn_system_elements(qn_system* S, int64_t inst, int64_t mat, const double* x,
 }
 
 int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* avg_ms, void* stream) {
-  QN_REQUIRE(S && avg_ms && reps >= 1 && kernel >= 0 && kernel <= 2, QN_ERR_ARG, "time_kernel: args");
+  QN_REQUIRE(S && avg_ms && reps >= 1 && kernel >= 0 && kernel <= 3, QN_ERR_ARG, "time_kernel: args");
+  // kernel 3 = one AMG V(1,1) cycle on the resident level vectors: its kernels
+  // only run for an instance in the direction phase with an unconverged CG,
+  // so the two control words are set for the timing and restored after
+  int32_t saved_phase = 0, saved_conv = 0;
+  if (kernel == 3) {
+    QN_REQUIRE(S->v.pcg == 2, QN_ERR_UNSUPPORTED, "time_kernel: vcycle needs an AMG system");
+    QN_CUDA(cudaMemcpy(&saved_phase, &S->v.ctl[0].phase, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    QN_CUDA(cudaMemcpy(&saved_conv, &S->v.pctl[0].conv, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    const int32_t on = qn::PH_DIR, zero = 0;
+    QN_CUDA(cudaMemcpy(&S->v.ctl[0].phase, &on, sizeof(int32_t), cudaMemcpyHostToDevice));
+    QN_CUDA(cudaMemcpy(&S->v.pctl[0].conv, &zero, sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   cudaStream_t st = pick(S, stream);
   const SysView& v = S->v;
   int rc;
@@ -1304,9 +1322,12 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
       QN_REQUIRE(S->factor, QN_ERR_UNSUPPORTED, "time_kernel: no factor (PCG system)");
       int r = launch_solve_timing(S, st);
       if (r) return r;
-    } else {  // the CG's SpMV q = A_free x (PCG / AMG systems)
+    } else if (kernel == 2) {  // the CG's SpMV q = A_free x (PCG / AMG systems)
       QN_REQUIRE(S->v.pcg, QN_ERR_UNSUPPORTED, "time_kernel: spmv needs a PCG system");
       int r = launch_spmv_timing(S, st);
+      if (r) return r;
+    } else {
+      int r = launch_vcycle(S, st);
       if (r) return r;
     }
     return QN_OK;
@@ -1321,6 +1342,10 @@ int qn_system_time_kernel(qn_system* S, int32_t kernel, int32_t reps, double* av
   float ms = 0.f;
   QN_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
   *avg_ms = ms / reps;
+  if (kernel == 3) {
+    QN_CUDA(cudaMemcpy(&S->v.ctl[0].phase, &saved_phase, sizeof(int32_t), cudaMemcpyHostToDevice));
+    QN_CUDA(cudaMemcpy(&S->v.pctl[0].conv, &saved_conv, sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   return QN_OK;
 }
 

@@ -221,5 +221,6 @@ struct qn_system {
   std::vector<int32_t> h_tet_mat;
   // AMG (host copy of the level table, for launch sizes and diagnostics)
   std::vector<qn::AmgDevLevel> h_alev;
+  std::vector<int64_t> amg_nnz;  // per level: nnz(A), nnz(P), nnz(R) of the host hierarchy
   double amg_setup_s = 0.0;
 };

@@ -209,17 +209,21 @@ class SimSystem:
 
     def amg_info(self) -> dict:
         """AMG systems: number of levels, rows per level, host setup time."""
-        out = np.zeros(12, dtype=np.int64)
+        out = np.zeros(42, dtype=np.int64)
         _lib.check(_lib.load().qn_system_amg_info(self._h, _lib.ptr(out), C.c_int64(out.size)))
         nl = int(out[0])
-        return {"levels": nl, "rows": [int(v) for v in out[1:1 + nl]], "setup_s": out[11] / 1000.0}
+        nnz = out[12:12 + 3 * nl].reshape(nl, 3) if nl else np.zeros((0, 3), dtype=np.int64)
+        return {"levels": nl, "rows": [int(v) for v in out[1:1 + nl]], "setup_s": out[11] / 1000.0,
+                "nnz_A": [int(v) for v in nnz[:, 0]], "nnz_P": [int(v) for v in nnz[:, 1]],
+                "nnz_R": [int(v) for v in nnz[:, 2]]}
 
     def time_kernel(self, kernel: str, reps: int = 20, stream=None) -> float:
         """Mean CUDA-event time (ms) of one stand-alone launch of a hot kernel:
         "tet" (per-tet pass at the resident q_l), "solve" (fwd+bwd SpTRSV) or
-        "spmv" (the CG's A_free SpMV, PCG/AMG systems)."""
+        "spmv" (the CG's A_free SpMV, PCG/AMG systems) or "vcycle" (one AMG
+        V(1,1) preconditioner application on the resident level vectors)."""
         ms = C.c_double(0.0)
-        _lib.check(_lib.load().qn_system_time_kernel(self._h, {"tet": 0, "solve": 1, "spmv": 2}[kernel], reps,
+        _lib.check(_lib.load().qn_system_time_kernel(self._h, {"tet": 0, "solve": 1, "spmv": 2, "vcycle": 3}[kernel], reps,
                                                      C.byref(ms),
                                                      stream), "time_kernel")
         return ms.value

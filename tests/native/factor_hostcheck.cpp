@@ -181,5 +181,10 @@ extern "C" int hc_amg_solve(int64_t n, const int64_t* indptr, const int32_t* ind
   stats[0] = it;
   stats[1] = (int64_t)h.lv.size();
   for (size_t l = 0; l < h.lv.size() && l < 6; ++l) stats[2 + l] = h.lv[l].A.n;
+  if (stats[8] == -1)  // caller asks for nnz per level too: A, P in stats[9 + 2l], stats[10 + 2l]
+    for (size_t l = 0; l < h.lv.size() && l < 6; ++l) {
+      stats[9 + 2 * l] = h.lv[l].A.ptr.empty() ? 0 : h.lv[l].A.ptr.back();
+      stats[10 + 2 * l] = h.lv[l].P.ptr.empty() ? 0 : h.lv[l].P.ptr.back();
+    }
   return 0;
 }

@@ -12,7 +12,7 @@
 namespace qn {
 
 constexpr int kTT = kTetThreads;  // tet-kernel block
-constexpr int kTetBlocksPerSm = 6;  // <= 102 registers: 640 resident tets per SM (81k tets = one wave)
+constexpr int kTetBlocksPerSm = 7;  // <= 72 registers
 
 // last block of instance b for counter `which`?  (after all partial writes)
 // Partials are written by thread 0 before this call; one fence by that thread

@@ -237,7 +237,7 @@ int factor_upload(qn_factor* f) {
   }
   // forward: Z tile + f (nc x 3) + partials (256 x 3) + index staging;
   // backward: Z tile + w (nr x 3) + pre (64 x 3) + destinations (64) + row staging
-  f->smem_f = (int)(sizeof(double) * (kTaskEntries + 3 * ((size_t)max_nc_task + kSolveThreads)) + sizeof(int) * kStageIdx);
+  f->smem_f = (int)(sizeof(double) * (f->fwd_entries + 3 * ((size_t)max_nc_task + kSolveThreads)) + sizeof(int) * kStageIdx);
   f->smem_b = (int)(sizeof(double) * (f->bwd_entries + 3 * (size_t)f->task_max_rows + 4 * kBwdCols) + sizeof(int) * kStageIdx);
   QN_REQUIRE(std::max(f->smem_f, f->smem_b) <= 227 * 1024, QN_ERR_UNSUPPORTED,
              "factor: supernode front exceeds shared memory");

@@ -620,6 +620,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       f->bwd_entries = std::max<int64_t>(mr, std::min<int64_t>(te_b, fit));
       f->task_max_rows = mr;
     }
+    f->fwd_entries = 2;
     for (int32_t s : order) {
       if (f->is_top[s]) continue;
       const int32_t nc = f->sup_col[s + 1] - f->sup_col[s];
@@ -630,6 +631,8 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::max<int64_t>(1, std::min<int64_t>(32, te_f / nc));
       f->ffirst[s] = (int32_t)f->ftask.size();
       for (int32_t r = 0; r < nr; r += rows) {
+        const int32_t hi = std::min(nr, r + rows);
+        f->fwd_entries = std::max<int64_t>(f->fwd_entries, ((int64_t)(hi - r) * std::min(hi, nc) + 1) / 2 * 2);
         f->ftask.push_back({s, r, std::min(nr, r + rows), rg});
         f->fcount[s]++;
       }

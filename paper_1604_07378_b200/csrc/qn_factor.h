@@ -70,6 +70,7 @@ struct qn_factor {
   int32_t max_rows = 0, depth = 0;
   int32_t task_max_rows = 0;   // tallest front among the supernodes solved by tasks (not the dense top)
   int64_t bwd_entries = 8192;  // Z entries per backward task tile (<= kTaskEntries, set by the task builder)
+  int64_t fwd_entries = 8192;  // largest forward task tile (<= kTaskEntries, even)
   double flops = 0.0, factor_seconds = 0.0;
   // ---- numeric (host, nbatch x nvals) ----
   std::vector<double> vals;

@@ -30,7 +30,7 @@
 namespace qn {
 
 struct FactorView {
-  int32_t n, nsup, nbatch, nftask, nbtask, bwd_entries, batch_max_nc, batch_zmax, nhlev, ndlev;
+  int32_t n, nsup, nbatch, nftask, nbtask, bwd_entries, fwd_entries, batch_max_nc, batch_zmax, nhlev, ndlev;
   int64_t nvals, nupd;
   const int32_t* sup_col;
   const int64_t* sup_row_ptr;
@@ -87,6 +87,7 @@ inline FactorView factor_view(const qn_factor* f) {
   v.nftask = (int32_t)f->ftask.size();
   v.nbtask = (int32_t)f->btask.size();
   v.bwd_entries = (int32_t)f->bwd_entries;
+  v.fwd_entries = (int32_t)f->fwd_entries;
   v.batch_max_nc = f->batch_max_nc;
   v.batch_zmax = f->batch_zmax;
   v.nhlev = (int32_t)f->hlev_ptr.size() - 1;
@@ -395,7 +396,7 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
   const int R = hi - lo;
   const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
-  double* f = sm + kTaskEntries;
+  double* f = sm + F.fwd_entries;
   double* part = f + 3 * nc;
   int* sidx = (int*)(part + 3 * kSolveThreads);
   const double* ub = F.u + (size_t)b * F.nupd * 3;
@@ -652,7 +653,7 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
 }
 
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_forward(FactorView F, IO io) {
+__global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F, IO io) {
   // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_item;

@@ -142,6 +142,27 @@ int qn_factor_task_counts(const qn_factor* f, int64_t* n_ftask, int64_t* n_btask
 int qn_factor_trace_solve(qn_factor* f, uint64_t* stamps, int32_t* tasks);
 
 /* ------------------------------------------------------------------------ */
+/* Device setup assembly — replaces the numpy part of dynamics.build_system
+ * (dynamics.py:351-414) with mesh.tet_diff_operators (mesh.py:200-216) and
+ * mesh.lumped_masses (mesh.py:178-197) for tet meshes: per tet G (m x 4 x 3)
+ * and rest volume, lumped vertex masses, L = sum w G G^T (w = vol k_of_tet)
+ * as CSR with sorted columns, and A_free = (L + M/h^2)[free][:, free].
+ * Tets with volume < vol_eps raise QN_ERR_ARG (MeshError in the reference).
+ * Summation orders are the reference's (masses corner-major then element
+ * order, L entries in element order); the 3x3 inverse is the adjugate, so
+ * values agree with the reference to rounding.  qn_setup_copy writes host
+ * arrays (any pointer may be NULL to skip that output). */
+typedef struct qn_setup qn_setup;
+int qn_setup_create(int64_t n, const double* verts, int64_t m, const int32_t* tets, double density,
+                    const double* k_of_tet, double h, int64_t n_fixed, const int32_t* fixed, double vol_eps,
+                    qn_setup** out);
+int qn_setup_sizes(const qn_setup* s, int64_t* nnz_l, int64_t* n_free, int64_t* nnz_a);
+int qn_setup_copy(const qn_setup* s, double* G, double* vols, double* masses, int64_t* l_indptr,
+                  int32_t* l_indices, double* l_values, int64_t* a_indptr, int32_t* a_indices,
+                  double* a_values);
+int qn_setup_destroy(qn_setup* s);
+
+/* ------------------------------------------------------------------------ */
 /* Simulation system — replaces dynamics.build_system (dynamics.py:351-434)
  * for Valanis-Landel tet groups, plus the per-frame solver
  * solvers.simulate_frame (solvers.py:260-352).  `n_inst` independent

@@ -23,7 +23,7 @@ LIB = os.path.join(PKG, "libqnsim_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3", f"-I{INCLUDE}", f"-I{CSRC}"]
-SOURCES = ["qn_api.cu", "qn_solver.cu", "qn_slab.cu", "qn_newton.cu", "qn_factor.cpp", "qn_amg.cpp"]
+SOURCES = ["qn_api.cu", "qn_solver.cu", "qn_slab.cu", "qn_newton.cu", "qn_setup.cu", "qn_factor.cpp", "qn_amg.cpp"]
 
 
 def _deps():

@@ -142,6 +142,10 @@ SIGNATURES = {
     "qn_system_set_timeline": [_P, C.c_int32],
     "qn_system_set_fault": [_P, C.c_int32, C.c_int32],
     "qn_frame_records_device": [_P, C.c_int32, _P, _P, _P],
+    "qn_setup_create": [C.c_int64, _P, C.c_int64, _P, C.c_double, _P, C.c_double, C.c_int64, _P, C.c_double, _P],
+    "qn_setup_sizes": [_P, _P, _P, _P],
+    "qn_setup_copy": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "qn_setup_destroy": [_P],
     "qn_system_timeline": [_P, _P, C.c_int64],
     "qn_system_solve_trace": [_P, _P, _P],
     "qn_system_time_kernel": [_P, _I32, _I32, _P, _P],

@@ -26,7 +26,7 @@ import scipy.sparse
 from paper_1604_07378_b200 import _lib
 from paper_1604_07378_b200.linalg import Factorization
 from paper_1604_07378_b200.materials import AnisoMaterial, FitInterval, MaterialModel, PDMaterial, estimate_stiffness
-from paper_1604_07378_b200.mesh import SpringNetwork, TetMesh, lumped_masses, tet_diff_operators
+from paper_1604_07378_b200.mesh import VOLUME_EPS, MeshError, SpringNetwork, TetMesh, lumped_masses, tet_diff_operators
 
 DEFAULT_TIMESTEP = 1.0 / 30.0      # dynamics.py:28
 DEFAULT_GRAVITY = (0.0, 0.0, -9.8)  # dynamics.py:29
@@ -277,9 +277,12 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     if not isinstance(mesh, TetMesh):
         raise NotImplementedError("spring networks (cloth) are outside the B200 hot path")
     _lib.require_gpu()
+    from paper_1604_07378_b200 import setup as dsetup
     n = mesh.n
-    masses = lumped_masses(mesh)
-    G, vols = tet_diff_operators(mesh)
+    device = dsetup.use_device(mesh.tets.shape[0], len(inst_materials))
+    if not device:
+        masses = lumped_masses(mesh)
+        G, vols = tet_diff_operators(mesh)
     fixed = np.asarray(sorted(set(int(i) for i in fixed)), dtype=np.int64)
     if fixed.size and (fixed.min() < 0 or fixed.max() >= n):
         raise DynamicsError("fixed vertex index out of range")
@@ -294,16 +297,30 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     order = np.concatenate([idx for idx, _ in assign0]) if assign0 else np.zeros(0, dtype=np.int64)
     tet_mat = np.concatenate([np.full(idx.size, g, dtype=np.int32) for g, (idx, _) in enumerate(assign0)]) \
         if assign0 else np.zeros(0, dtype=np.int32)
-    tets = mesh.tets[order]
-    Gs, vs = G[order], vols[order]
+    tets = mesh.tets[order] if not np.array_equal(order, np.arange(order.size)) else mesh.tets
     m = tets.shape[0]
+    dev = None
+    if device:  # configs[4]-size meshes: G, volumes, masses, L and A_free assembled on the GPU (setup.py)
+        ks0 = [mat.k_fit if mat.k_fit is not None else estimate_stiffness(mat, fit_interval) for _, mat in assign0]
+        Gs, vs, masses, L_dev, Af_dev = dsetup.assemble(mesh.vertices, tets, mesh.density,
+                                                        np.asarray(ks0)[tet_mat], h, fixed, VOLUME_EPS)
+        bad = np.nonzero(masses <= 0)[0]
+        if bad.size:
+            raise MeshError(f"vertex {bad[0]} has zero mass (isolated vertex?)")
+        inv = np.empty_like(order)
+        inv[order] = np.arange(order.size)
+        G, vols = (Gs, vs) if tets is mesh.tets else (Gs[inv], vs[inv])
+        dev = (L_dev, Af_dev)
+    else:
+        Gs, vs = (G, vols) if tets is mesh.tets else (G[order], vols[order])
 
     # L = sum_groups w G G^T per instance, assembled exactly as the reference
     # does (COO in group-major order -> CSR, dynamics.py:387-402, so L is bitwise
     # the reference's), then A = L + M/h^2 restricted to the free dofs (:413-414)
-    GG = np.einsum("evc,euc->evu", Gs, Gs) if m else np.zeros((0, 4, 4))
-    rows = np.repeat(tets, 4, axis=1).reshape(-1)
-    cols = np.tile(tets, (1, 4)).reshape(-1)
+    if not device:
+        GG = np.einsum("evc,euc->evu", Gs, Gs) if m else np.zeros((0, 4, 4))
+        rows = np.repeat(tets, 4, axis=1).reshape(-1)
+        cols = np.tile(tets, (1, 4)).reshape(-1)
     diag_m = scipy.sparse.diags(masses / h ** 2)
     values, Ls, groups_per_inst, mats = [], [], [], []
     f_indptr = a_idx = None
@@ -313,11 +330,14 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
             k = mat.k_fit if mat.k_fit is not None else estimate_stiffness(mat, fit_interval)
             ks.append(k)
             gl.append(VLGroup(mesh.tets[idx], G[idx], vols[idx], mat, k))
-        w = (vs * np.asarray(ks)[tet_mat]) if m else np.zeros(0)
-        L = scipy.sparse.coo_matrix(((w[:, None, None] * GG).reshape(-1), (rows, cols)), shape=(n, n)).tocsr() \
-            if m else scipy.sparse.csr_matrix((n, n))
-        Af = (L + diag_m).tocsr()[free][:, free].tocsr()
-        Af.sort_indices()
+        if dev is not None:
+            L, Af = dev
+        else:
+            w = (vs * np.asarray(ks)[tet_mat]) if m else np.zeros(0)
+            L = scipy.sparse.coo_matrix(((w[:, None, None] * GG).reshape(-1), (rows, cols)), shape=(n, n)).tocsr() \
+                if m else scipy.sparse.csr_matrix((n, n))
+            Af = (L + diag_m).tocsr()[free][:, free].tocsr()
+            Af.sort_indices()
         if f_indptr is None:
             f_indptr, a_idx = Af.indptr.astype(np.int64), Af.indices
         elif not (np.array_equal(f_indptr, Af.indptr) and np.array_equal(a_idx, Af.indices)):

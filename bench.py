@@ -490,7 +490,8 @@ def run_ours(args, world, rank, local):
                             "supernodes": info["n_supernodes"],
                             "depth": info["tree_depth"], "factor_s": info["factor_seconds"],
                             "dense_top": info.get("dense_top")} if "nnz_l" in info else info),
-                "build_s": t_build, "passes_per_step": passes / args.steps}
+                "build_s": t_build, "build_phases_s": getattr(system, "build_times", None),
+                "passes_per_step": passes / args.steps}
         if cg_iters:
             line["cg_iterations_per_step"] = cg_iters / args.steps
         emit(line)

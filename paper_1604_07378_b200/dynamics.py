@@ -278,6 +278,9 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
         raise NotImplementedError("spring networks (cloth) are outside the B200 hot path")
     _lib.require_gpu()
     from paper_1604_07378_b200 import setup as dsetup
+    import time as _time
+    _t0 = _time.perf_counter()
+    _tm = {}
     n = mesh.n
     device = dsetup.use_device(mesh.tets.shape[0], len(inst_materials))
     if not device:
@@ -311,6 +314,7 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
         inv[order] = np.arange(order.size)
         G, vols = (Gs, vs) if tets is mesh.tets else (Gs[inv], vs[inv])
         dev = (L_dev, Af_dev)
+        _tm["device_assembly"] = _time.perf_counter() - _t0
     else:
         Gs, vs = (G, vols) if tets is mesh.tets else (G[order], vols[order])
 
@@ -398,7 +402,9 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     w_col = float(collision_weight) if collision_weight is not None else 10.0 * max_w  # dynamics.py:417
     d.n_colliders, d.colliders, d.w_col = len(colliders), C.cast(ccols, C.c_void_p), w_col
     handle = C.c_void_p()
+    _tm["host_prep"] = _time.perf_counter() - _t0 - sum(_tm.values())
     _lib.check(_lib.load().qn_system_create(C.byref(d), C.byref(handle)), "build_system")
+    _tm["system_create"] = _time.perf_counter() - _t0 - sum(_tm.values())
     sysfact = None
     if solver == "direct":
         fh = C.c_void_p()
@@ -412,6 +418,7 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     for b, gl in enumerate(groups_per_inst):
         for g, grp in enumerate(gl):
             grp._system, grp._index, grp._inst = system, g, b
+    system.build_times = _tm  # seconds per build phase (diagnostics)
     return system
 
 

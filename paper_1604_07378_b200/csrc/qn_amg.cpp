@@ -10,6 +10,8 @@
 #include "qn_amg.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <numeric>
@@ -154,6 +156,14 @@ double rho_dinv_a(const Csr& a, const std::vector<double>& dinv, int its = 15) {
 
 int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* val, AmgHierarchy* h) {
   const auto t0 = std::chrono::steady_clock::now();
+  const bool verbose = std::getenv("QN_AMG_VERBOSE") != nullptr;  // diagnostics: per-phase setup times
+  auto tp = t0;
+  auto phase = [&](const char* what, int lev) {
+    if (!verbose) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "amg setup L%d %-12s %8.3f s\n", lev, what, std::chrono::duration<double>(t - tp).count());
+    tp = t;
+  };
   h->lv.clear();
   h->omega_l.clear();
   AmgLevel L0;
@@ -176,6 +186,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
       L.dinv[i] = 1.0 / diag[i];
     }
     h->omega_l.push_back(4.0 / (3.0 * rho_dinv_a(A, L.dinv)));
+    phase("diag+rho", lev);
     if (nl <= kAmgCoarsest || lev == kAmgMaxLevels - 1) break;
     // ---- strength + filtered operator ----
     std::vector<uint8_t> strong(A.ptr[nl], 0);
@@ -189,6 +200,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
         else
           fdiag[i] += A.val[e];  // lump the weak coupling (row sums preserved)
       }
+    phase("strength", lev);
     // ---- greedy aggregation ----
     std::vector<int32_t> agg(nl, -1);
     int32_t na = 0;
@@ -221,6 +233,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
       ++na;
     }
     if (na >= nl || na < 1) break;  // no coarsening possible
+    phase("aggregate", lev);
     // ---- smoothed prolongator P = (I - w D_F^-1 A_F) P_tent ----
     Csr Af;
     Af.n = Af.m = nl;
@@ -268,14 +281,17 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
       }
     }
     L.P = std::move(P);
+    phase("prolongator", lev);
     L.R = transpose(L.P);
     AmgLevel next;
     next.A = spgemm(L.R, spgemm(L.A, L.P));
+    phase("galerkin", lev);
     {  // exact symmetry (the products round differently per side): A_c = (A_c + A_c^T) / 2
       const Csr t = transpose(next.A);
       for (int64_t e = 0; e < next.A.ptr[next.A.n]; ++e) next.A.val[e] = 0.5 * (next.A.val[e] + t.val[e]);
     }
     h->lv.push_back(std::move(next));
+    phase("symmetrise", lev);
   }
   // ---- dense inverse of the coarsest operator (Cholesky, then columns) ----
   {
@@ -314,6 +330,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
       for (int64_t i = 0; i < nc; ++i) h->coarse_inv[(size_t)i * nc + c] = z[i];
     }
   }
+  phase("coarse inv", (int)h->lv.size() - 1);
   h->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return QN_OK;
 }

@@ -129,24 +129,38 @@ void spmv3(const Csr& a, const double* x, double* y) {  // y = A x, 3 RHS
   }
 }
 
-// largest eigenvalue of D^-1 A (power iteration, deterministic start)
+// largest eigenvalue of D^-1 A (power iteration, deterministic start); the
+// row loop is parallel and the norms are summed over fixed 64 k-row chunks in
+// chunk order, so the result does not depend on the thread count
 double rho_dinv_a(const Csr& a, const std::vector<double>& dinv, int its = 15) {
   const int64_t n = a.n;
-  std::vector<double> x(n), y(n);
+  constexpr int64_t kChunk = 65536;
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  std::vector<double> x(n), y(n), part(2 * nch);
   for (int64_t i = 0; i < n; ++i) x[i] = 1.0 + 0.1 * std::sin(0.7 * (double)i);
   double lam = 1.0;
   for (int k = 0; k < its; ++k) {
-    double nrm = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      double s = 0.0;
-      for (int64_t e = a.ptr[i]; e < a.ptr[i + 1]; ++e) s += a.val[e] * x[a.col[e]];
-      y[i] = dinv[i] * s;
-      nrm += y[i] * y[i];
+#pragma omp parallel for schedule(static)
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      double ny = 0.0, nx = 0.0;
+      for (int64_t i = ch * kChunk; i < std::min(n, (ch + 1) * kChunk); ++i) {
+        double s = 0.0;
+        for (int64_t e = a.ptr[i]; e < a.ptr[i + 1]; ++e) s += a.val[e] * x[a.col[e]];
+        y[i] = dinv[i] * s;
+        ny += y[i] * y[i];
+        nx += x[i] * x[i];
+      }
+      part[2 * ch] = ny;
+      part[2 * ch + 1] = nx;
+    }
+    double nrm = 0.0, xn = 0.0;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      nrm += part[2 * ch];
+      xn += part[2 * ch + 1];
     }
     nrm = std::sqrt(nrm);
-    double xn = 0.0;
-    for (int64_t i = 0; i < n; ++i) xn += x[i] * x[i];
     lam = nrm / std::max(std::sqrt(xn), 1e-300);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) x[i] = y[i] / std::max(nrm, 1e-300);
   }
   return lam;
@@ -253,31 +267,52 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
     P.n = nl;
     P.m = na;
     P.ptr.assign(nl + 1, 0);
-    {
-      std::vector<int32_t> cols;
-      std::vector<double> vals;
-      for (int64_t i = 0; i < nl; ++i) {
-        cols.clear();
-        vals.clear();
-        auto add = [&](int32_t c, double v) {
-          for (size_t k = 0; k < cols.size(); ++k)
-            if (cols[k] == c) {
-              vals[k] += v;
-              return;
-            }
-          cols.push_back(c);
-          vals.push_back(v);
-        };
-        add(agg[i], 1.0);
-        for (int64_t e = Af.ptr[i]; e < Af.ptr[i + 1]; ++e) add(agg[Af.col[e]], -wp * fdinv[i] * Af.val[e]);
-        std::vector<int32_t> ord(cols.size());
-        std::iota(ord.begin(), ord.end(), 0);
-        std::sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cols[x] < cols[y]; });
-        for (int32_t k : ord) {
-          P.col.push_back(cols[k]);
-          P.val.push_back(vals[k]);
+    {  // rows are independent: per-thread row ranges, concatenated in row order
+      int nt = 1;
+#ifdef _OPENMP
+      nt = omp_get_max_threads();
+#endif
+      const int64_t chunk = std::max<int64_t>(1, (nl + nt - 1) / nt);
+      std::vector<std::vector<int32_t>> tcol(nt);
+      std::vector<std::vector<double>> tval(nt);
+#pragma omp parallel num_threads(nt)
+      {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        std::vector<int32_t> cols;
+        std::vector<double> vals;
+        for (int64_t i = t * chunk; i < std::min<int64_t>(nl, (t + 1) * chunk); ++i) {
+          cols.clear();
+          vals.clear();
+          auto add = [&](int32_t c, double v) {
+            for (size_t k = 0; k < cols.size(); ++k)
+              if (cols[k] == c) {
+                vals[k] += v;
+                return;
+              }
+            cols.push_back(c);
+            vals.push_back(v);
+          };
+          add(agg[i], 1.0);
+          for (int64_t e = Af.ptr[i]; e < Af.ptr[i + 1]; ++e) add(agg[Af.col[e]], -wp * fdinv[i] * Af.val[e]);
+          std::vector<int32_t> ord(cols.size());
+          std::iota(ord.begin(), ord.end(), 0);
+          std::sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return cols[x] < cols[y]; });
+          for (int32_t k : ord) {
+            tcol[t].push_back(cols[k]);
+            tval[t].push_back(vals[k]);
+          }
+          P.ptr[i + 1] = (int64_t)ord.size();
         }
-        P.ptr[i + 1] = (int64_t)P.col.size();
+      }
+      for (int64_t i = 0; i < nl; ++i) P.ptr[i + 1] += P.ptr[i];
+      P.col.reserve(P.ptr[nl]);
+      P.val.reserve(P.ptr[nl]);
+      for (int t = 0; t < nt; ++t) {
+        P.col.insert(P.col.end(), tcol[t].begin(), tcol[t].end());
+        P.val.insert(P.val.end(), tval[t].begin(), tval[t].end());
       }
     }
     L.P = std::move(P);
@@ -294,7 +329,7 @@ int amg_build(int64_t n, const int64_t* ptr, const int32_t* col, const double* v
     phase("symmetrise", lev);
   }
   // ---- dense inverse of the coarsest operator (Cholesky, then columns) ----
-  {
+  if (!h->skip_coarse_inverse) {
     const Csr& A = h->lv.back().A;
     const int64_t nc = A.n;
     std::vector<double> M((size_t)nc * nc, 0.0);

@@ -30,6 +30,7 @@ struct AmgLevel {
 struct AmgHierarchy {
   std::vector<AmgLevel> lv;
   std::vector<double> coarse_inv;  // dense inverse of the coarsest operator (row-major)
+  bool skip_coarse_inverse = false;  // caller inverts the coarsest operator itself (device: cuSOLVER)
   std::vector<double> omega_l;     // Jacobi smoothing weight per level: 4 / (3 rho(D^-1 A))
   double setup_seconds = 0.0;
 };

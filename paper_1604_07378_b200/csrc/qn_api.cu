@@ -1,5 +1,7 @@
 // extern "C" boundary of libqnsim_b200 (declared in include/qnsim_b200.h).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <cstddef>
@@ -7,6 +9,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <cusolverDn.h>
 
 #include "qn_common.cuh"
 #include "qn_factor.h"
@@ -86,6 +90,51 @@ int sys_upload(qn_system* S, T** p, const T* h, size_t count) {
 }
 
 cudaStream_t pick(qn_system* S, void* stream) { return stream ? (cudaStream_t)stream : S->stream; }
+
+// Dense inverse of the AMG hierarchy's coarsest operator (SPD, a few thousand
+// rows) on the device: cuSOLVER Cholesky, then potrs against the identity
+// (library factorisation of a setup-time dense block; seconds on the host).
+// The result is symmetric, so its column-major layout is the row-major one the
+// coarse kernel reads.
+int coarse_inverse_device(qn_system* S, const qn::Csr& A, double** out) {
+  const int64_t nc = A.n;
+  std::vector<double> M((size_t)nc * nc, 0.0);
+  for (int64_t i = 0; i < nc; ++i)
+    for (int64_t e = A.ptr[i]; e < A.ptr[i + 1]; ++e) M[(size_t)A.col[e] * nc + i] = A.val[e];
+  double *dM = nullptr, *dI = nullptr, *work = nullptr;
+  int* info = nullptr;
+  int rc = QN_OK;
+  if ((rc = dev_upload(&dM, M.data(), M.size()))) return rc;
+  std::fill(M.begin(), M.end(), 0.0);
+  for (int64_t i = 0; i < nc; ++i) M[(size_t)i * nc + i] = 1.0;
+  if ((rc = sys_upload(S, &dI, M.data(), M.size()))) {
+    cudaFree(dM);
+    return rc;
+  }
+  cusolverDnHandle_t h = nullptr;
+  int lwork = 0, hinfo = 0;
+  bool ok = cusolverDnCreate(&h) == CUSOLVER_STATUS_SUCCESS &&
+            cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, (int)nc, dM, (int)nc, &lwork) ==
+                CUSOLVER_STATUS_SUCCESS &&
+            cudaMalloc((void**)&work, sizeof(double) * std::max(lwork, 1)) == cudaSuccess &&
+            cudaMalloc((void**)&info, sizeof(int)) == cudaSuccess &&
+            cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)nc, dM, (int)nc, work, lwork, info) ==
+                CUSOLVER_STATUS_SUCCESS &&
+            cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && hinfo == 0 &&
+            cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, (int)nc, (int)nc, dM, (int)nc, dI, (int)nc, info) ==
+                CUSOLVER_STATUS_SUCCESS &&
+            cudaDeviceSynchronize() == cudaSuccess;
+  if (h) cusolverDnDestroy(h);
+  cudaFree(dM);
+  cudaFree(work);
+  cudaFree(info);
+  if (!ok) {
+    set_error(hinfo ? "amg: coarsest operator is not positive definite" : "amg: cuSOLVER coarse inverse failed");
+    return hinfo ? QN_ERR_NOT_SPD : QN_ERR_CUDA;
+  }
+  *out = dI;
+  return QN_OK;
+}
 
 // three n x 3 vectors for the seam entry points (objective / elements), owned
 // by the system and freed with it
@@ -517,6 +566,14 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
                "system: unknown collider kind");
   const int64_t n = d->n_verts, mt = d->n_tets, ni = d->n_inst;
   QN_REQUIRE(n * ni < (int64_t)1 << 31 && mt * 4 < (int64_t)1 << 31, QN_ERR_ARG, "system: too large");
+  const bool verbose = std::getenv("QN_BUILD_VERBOSE") != nullptr;  // diagnostics: per-phase host times
+  auto tp = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!verbose) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "system_create %-16s %8.3f s\n", what, std::chrono::duration<double>(t - tp).count());
+    tp = t;
+  };
   qn_system* S = new qn_system();
   S->n = n;
   S->mt = mt;
@@ -552,6 +609,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
     set_error("all vertices fixed; nothing to simulate");
     return fail(QN_ERR_ARG);
   }
+  phase("fixed set");
   // tets, SoA Dm^-1, gather map (slots 4t + c in increasing order = reference scatter order)
   std::vector<int4> tets(std::max<int64_t>(mt, 1));
   std::vector<double> dminv((size_t)std::max<int64_t>(mt, 1) * 9);
@@ -583,6 +641,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       }
     S->h_tet_mat.assign(d->tet_mat, d->tet_mat + mt);
   }
+  phase("tets + gather map");
   SysView& v = S->v;
   int rc = QN_OK;
   std::vector<int32_t> fact_vtx(S->n_free);
@@ -648,7 +707,9 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       return fail(rc);
     if (v.pcg == 2) {  // AMG hierarchy (host setup once), SELL operators + level vectors on the device
       QN_REQUIRE(ni == 1, QN_ERR_UNSUPPORTED, "system: the AMG solver supports one instance");
+      phase("pcg operator");
       qn::AmgHierarchy H;
+      H.skip_coarse_inverse = true;  // inverted on the device below (cuSOLVER Cholesky)
       if ((rc = qn::amg_build(nf, d->a_indptr, d->a_indices, d->a_values, &H))) return fail(rc);
       S->amg_setup_s = H.setup_seconds;
       const int nl = (int)H.lv.size();
@@ -688,9 +749,11 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       v.alev = dl;
       v.amg_levels = nl;
       v.ncoarse = (int32_t)H.lv.back().A.n;
+      phase("amg build + upload");
       double* ci;
-      if ((rc = sys_upload(S, &ci, H.coarse_inv.data(), H.coarse_inv.size()))) return fail(rc);
+      if ((rc = coarse_inverse_device(S, H.lv.back().A, &ci))) return fail(rc);
       v.cinv = ci;
+      phase("coarse inverse");
     }
   }
 
@@ -796,7 +859,9 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   QN_CUDA(cudaEventCreate(&S->ev1));
   S->h_stage_bytes = vec * sizeof(double) * 3;
   QN_CUDA(cudaMallocHost((void**)&S->h_stage, S->h_stage_bytes));
+  phase("solver + vectors");
   if ((rc = prepare_kernels(S))) return fail(rc);
+  phase("prepare kernels");
   *out = S;
   return QN_OK;
 }

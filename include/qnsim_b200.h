@@ -208,6 +208,8 @@ typedef struct qn_system_desc {
    * Dm_inv unused, material a.c[0] = k (PDMaterial mass_spring)          */
   int32_t element_kind;
   int32_t pad_e;
+  int64_t dminv_stride;       /* doubles between consecutive tets' Dm_inv (0 = 9; 12 when Dm_inv points
+                                 at row 1 of a full (m,4,3) G array)          */
 } qn_system_desc;
 
 #define QN_ELEM_TET 0

@@ -70,7 +70,7 @@ class SystemDesc(C.Structure):
         ("free_coords", C.c_void_p),
         ("solver", C.c_int32), ("pcg_maxit", C.c_int32), ("pcg_tol", C.c_double),
         ("n_colliders", C.c_int64), ("colliders", C.c_void_p), ("w_col", C.c_double),
-        ("element_kind", C.c_int32), ("pad_e", C.c_int32),
+        ("element_kind", C.c_int32), ("pad_e", C.c_int32), ("dminv_stride", C.c_int64),
     ]
 
 

@@ -614,17 +614,24 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
   std::vector<int4> tets(std::max<int64_t>(mt, 1));
   std::vector<double> dminv((size_t)std::max<int64_t>(mt, 1) * 9);
   std::vector<int32_t> v2e_ptr(n + 1, 0), v2e((size_t)std::max<int64_t>(mt, 1) * 4);
-  for (int64_t t = 0; t < mt; ++t) {
-    const int32_t* tv = d->tets + 4 * t;
+  {
     const int corners = d->element_kind == QN_ELEM_SPRING ? 2 : 4;  // springs: (a, b, -1, -1)
-    for (int c = 0; c < 4; ++c)
-      if (c < corners ? (tv[c] < 0 || tv[c] >= n) : tv[c] != -1) {
-        set_error("system: element vertex out of range");
-        return fail(QN_ERR_ARG);
-      }
-    tets[t] = make_int4(tv[0], tv[1], tv[2], tv[3]);
-    for (int k = 0; k < 9; ++k) dminv[(size_t)k * mt + t] = d->Dm_inv ? d->Dm_inv[9 * t + k] : 0.0;
-    for (int c = 0; c < corners; ++c) v2e_ptr[tv[c] + 1]++;
+    const int64_t stride = d->dminv_stride > 0 ? d->dminv_stride : 9;
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t t = 0; t < mt; ++t) {
+      const int32_t* tv = d->tets + 4 * t;
+      for (int c = 0; c < 4; ++c)
+        if (c < corners ? (tv[c] < 0 || tv[c] >= n) : tv[c] != -1) bad = 1;
+      tets[t] = make_int4(tv[0], tv[1], tv[2], tv[3]);
+      for (int k = 0; k < 9; ++k) dminv[(size_t)k * mt + t] = d->Dm_inv ? d->Dm_inv[stride * t + k] : 0.0;
+    }
+    if (bad) {
+      set_error("system: element vertex out of range");
+      return fail(QN_ERR_ARG);
+    }
+    for (int64_t t = 0; t < mt; ++t)
+      for (int c = 0; c < corners; ++c) v2e_ptr[d->tets[4 * t + c] + 1]++;
   }
   for (int64_t i = 0; i < n; ++i) v2e_ptr[i + 1] += v2e_ptr[i];
   {

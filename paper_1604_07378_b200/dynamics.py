@@ -362,7 +362,11 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
             cmats[b * n_mat + g] = mat.to_c()
 
     tets32 = _lib.i32(tets)
-    dminv = _lib.f64(Gs[:, 1:, :]) if m else np.zeros((0, 3, 3))
+    # Dm^-1 = G[:, 1:]: passed in place (stride 12) when G is contiguous, no copy
+    if m and Gs.dtype == np.float64 and Gs.flags.c_contiguous:
+        dminv, dminv_stride = Gs[:, 1:, :], 12
+    else:
+        dminv, dminv_stride = (_lib.f64(Gs[:, 1:, :]) if m else np.zeros((0, 3, 3))), 9
     vols_c = _lib.f64(vs)
     tm = _lib.i32(tet_mat) if n_mat > 1 else None
     masses_c = _lib.f64(masses)
@@ -375,7 +379,9 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
 
     d = _lib.SystemDesc()
     d.n_verts, d.n_tets, d.n_inst, d.n_mat = n, m, n_inst, n_mat
-    d.tets, d.Dm_inv, d.vols = _lib.ptr(tets32), _lib.ptr(dminv), _lib.ptr(vols_c)
+    d.tets, d.vols = _lib.ptr(tets32), _lib.ptr(vols_c)
+    d.Dm_inv = dminv.ctypes.data if m else None
+    d.dminv_stride = dminv_stride
     d.tet_mat = _lib.ptr(tm)
     d.mats = C.cast(cmats, C.c_void_p)
     d.masses = _lib.ptr(masses_c)

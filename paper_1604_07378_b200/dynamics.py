@@ -300,7 +300,8 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
     order = np.concatenate([idx for idx, _ in assign0]) if assign0 else np.zeros(0, dtype=np.int64)
     tet_mat = np.concatenate([np.full(idx.size, g, dtype=np.int32) for g, (idx, _) in enumerate(assign0)]) \
         if assign0 else np.zeros(0, dtype=np.int32)
-    tets = mesh.tets[order] if not np.array_equal(order, np.arange(order.size)) else mesh.tets
+    identity = order.size == mesh.tets.shape[0] and np.array_equal(order, np.arange(order.size))
+    tets = mesh.tets if identity else mesh.tets[order]
     m = tets.shape[0]
     dev = None
     if device:  # configs[4]-size meshes: G, volumes, masses, L and A_free assembled on the GPU (setup.py)
@@ -312,11 +313,11 @@ def _build(mesh, inst_materials, h, gravity, fixed, fit_interval, n_mat_groups, 
             raise MeshError(f"vertex {bad[0]} has zero mass (isolated vertex?)")
         inv = np.empty_like(order)
         inv[order] = np.arange(order.size)
-        G, vols = (Gs, vs) if tets is mesh.tets else (Gs[inv], vs[inv])
+        G, vols = (Gs, vs) if identity else (Gs[inv], vs[inv])
         dev = (L_dev, Af_dev)
         _tm["device_assembly"] = _time.perf_counter() - _t0
     else:
-        Gs, vs = (G, vols) if tets is mesh.tets else (G[order], vols[order])
+        Gs, vs = (G, vols) if identity else (G[order], vols[order])
 
     # L = sum_groups w G G^T per instance, assembled exactly as the reference
     # does (COO in group-major order -> CSR, dynamics.py:387-402, so L is bitwise

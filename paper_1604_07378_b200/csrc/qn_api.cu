@@ -273,7 +273,6 @@ int factor_upload(qn_factor* f) {
     if ((rc = dev_upload(&f->d_tcols, f->tcols.data(), f->tcols.size()))) return rc;
     if ((rc = dev_upload(&f->d_tg_ptr, f->tg_ptr.data(), f->tg_ptr.size()))) return rc;
     if ((rc = dev_upload(&f->d_tg_idx, f->tg_idx.data(), f->tg_idx.size()))) return rc;
-    if ((rc = dev_alloc(&f->d_gtop, (size_t)f->nbatch * f->ktop * 3))) return rc;
   }
   if (const char* e = std::getenv("QN_SOLVE_OPTS")) f->solve_opts = std::atoi(e);  // experiment knob
   const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};  // [ticket, exited, epoch] x 2, watchdog
@@ -312,7 +311,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_flags,   f->d_sched,       f->d_io,        f->d_cptr,      f->d_cidx,
                   f->d_ftask,   f->d_btask,       f->d_bfirst,    f->d_bcount,    f->d_fdep_ptr,
                   f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
-                  f->d_gtop,    f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
+                  f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
                   f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt,
                   f->d_ftile,   f->d_btile};
   for (void* p : ptrs)

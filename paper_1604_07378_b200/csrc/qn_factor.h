@@ -117,7 +117,6 @@ struct qn_factor {
   int32_t* d_tcols = nullptr;
   int32_t* d_tg_ptr = nullptr;
   int32_t* d_tg_idx = nullptr;
-  double* d_gtop = nullptr;       // nbatch x K x 3
   unsigned* d_sched = nullptr;    // [ticket_f, done_f, epoch_f, ticket_b, done_b, epoch_b]
   double* d_io = nullptr;         // staging for the plain solve API (n x 3 in, out)
   unsigned long long* d_trace = nullptr;  // diagnostics only (qn_factor_trace_solve)

@@ -74,7 +74,6 @@ struct FactorView {
   const int32_t* tcols;
   const int32_t* tg_ptr;
   const int32_t* tg_idx;
-  double* gtop;              // [nbatch][K][3]
   unsigned long long* ktl;   // diagnostics timeline (qn_system_timeline) or null
   const unsigned long long* passes;
 };
@@ -137,7 +136,6 @@ inline FactorView factor_view(const qn_factor* f) {
   v.tcols = f->d_tcols;
   v.tg_ptr = f->d_tg_ptr;
   v.tg_idx = f->d_tg_idx;
-  v.gtop = f->d_gtop;
   v.ktl = f->d_ktl;
   v.passes = f->d_passes;
   return v;
@@ -724,28 +722,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
   cta_exit(sched, s_epoch, F, 5);
 }
 
-// ---- dense top: g_T = b_T - (updates of the subtrees below T); x_T = S^-1 g_T ----
-template <class IO>
-__global__ void __launch_bounds__(kSolveThreads) sptrsv_top_gather(FactorView F, IO io) {
-  const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!io.active(b) || k >= F.ktop) return;
-  const double* ub = F.u + (size_t)b * F.nupd * 3;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int q = F.tg_ptr[k]; q < F.tg_ptr[k + 1]; ++q) {
-    const double* uc = ub + 3 * (size_t)F.tg_idx[q];
-    a0 += __ldcg(uc);
-    a1 += __ldcg(uc + 1);
-    a2 += __ldcg(uc + 2);
-  }
-  double v[3];
-  io.rhs(b, F.tcols[k], v);
-  double* g = F.gtop + ((size_t)b * F.ktop + k) * 3;
-  g[0] = v[0] - a0;
-  g[1] = v[1] - a1;
-  g[2] = v[2] - a2;
-}
-
+// ---- dense top: x_T = S^-1 g_T, g_T = b_T - (updates of the subtrees below T) ----
 // x_T = S^-1 g_T with the symmetric S^-1 read once from half storage: CTA per
 // lower-triangle tile (I, J) (64 x 64, stored with leading dimension 65 so the
 // row and the column products both read shared memory without bank
@@ -782,11 +759,30 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
   while ((I + 1) * (I + 2) / 2 <= t) ++I;
   while (I * (I + 1) / 2 > t) --I;
   const int J = t - I * (I + 1) / 2;
-  const double* g = F.gtop + (size_t)b * K * 3;
-  for (int e = threadIdx.x; e < T * 3; e += blockDim.x) {
-    const int r = e / 3, c = e - 3 * r;
-    gI[e] = I * T + r < K ? __ldcg(g + 3 * (I * T + r) + c) : 0.0;
-    gJ[e] = J * T + r < K ? __ldcg(g + 3 * (J * T + r) + c) : 0.0;
+  // g_T of this tile's two row blocks, formed here (b_T minus the updates of the
+  // subtrees below T, in list order) while the tile streams in — no separate
+  // gather kernel; each row block's g is formed by every tile that needs it
+  const double* ub = F.u + (size_t)b * F.nupd * 3;
+  for (int e = threadIdx.x; e < 2 * T; e += blockDim.x) {
+    const int blk = e < T ? I : J, r = e < T ? e : e - T;
+    double* gd = (e < T ? gI : gJ) + 3 * r;
+    const int k = blk * T + r;
+    if (k < K) {
+      double v[3];
+      io.rhs(b, F.tcols[k], v);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int q = F.tg_ptr[k]; q < F.tg_ptr[k + 1]; ++q) {
+        const double* uc = ub + 3 * (size_t)F.tg_idx[q];
+        a0 += __ldcg(uc);
+        a1 += __ldcg(uc + 1);
+        a2 += __ldcg(uc + 2);
+      }
+      gd[0] = v[0] - a0;
+      gd[1] = v[1] - a1;
+      gd[2] = v[2] - a2;
+    } else {
+      gd[0] = gd[1] = gd[2] = 0.0;
+    }
   }
   mbar_wait(&s_mbar, 0);
   __syncthreads();
@@ -1068,9 +1064,6 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     QN_CHECK_LAUNCH();
   }
   if (f->ktop > 0) {
-    const dim3 gg((f->ktop + kSolveThreads - 1) / kSolveThreads, (unsigned)f->nbatch);
-    sptrsv_top_gather<IO><<<gg, kSolveThreads, 0, stream>>>(v, io);
-    QN_CHECK_LAUNCH();
     const dim3 ga((unsigned)(f->tnt * (f->tnt + 1) / 2), (unsigned)f->nbatch);
     sptrsv_top_sym<IO><<<ga, kSolveThreads, 0, stream>>>(v, io);
     QN_CHECK_LAUNCH();

@@ -269,6 +269,8 @@ int factor_upload(qn_factor* f) {
       if ((rc = dev_alloc(&f->d_tpart, (size_t)f->nbatch * nt * nt * T * 3))) return rc;
       std::vector<unsigned> zero((size_t)f->nbatch * nt, 0u);
       if ((rc = dev_upload(&f->d_tcnt, zero.data(), zero.size()))) return rc;
+      const unsigned z2[2] = {0u, 0u};
+      if ((rc = dev_upload(&f->d_stage_cnt, z2, 2))) return rc;
     }
     if ((rc = dev_upload(&f->d_tcols, f->tcols.data(), f->tcols.size()))) return rc;
     if ((rc = dev_upload(&f->d_tg_ptr, f->tg_ptr.data(), f->tg_ptr.size()))) return rc;
@@ -289,8 +291,10 @@ int factor_upload(qn_factor* f) {
   f->smem_b = (int)(sizeof(double) * (f->bwd_entries + 3 * (size_t)f->task_max_rows + 4 * kBwdCols) + sizeof(int) * kStageIdx);
   QN_REQUIRE(std::max(f->smem_f, f->smem_b) <= 227 * 1024, QN_ERR_UNSUPPORTED,
              "factor: supernode front exceeds shared memory");
-  f->fused = f->ktop == 0 && !(f->nbatch > 1);
-  f->smem_fused = std::max(f->smem_f, f->smem_b);
+  // one persistent kernel for forward (+ dense top tiles) + backward on single systems
+  f->fused = !(f->nbatch > 1);
+  f->smem_fused = std::max({f->smem_f, f->smem_b,
+                             f->ktop > 0 ? (int)(sizeof(double) * (kTopTileEntries + 6 * kTopTile)) : 0});
   // batches of small systems: one CTA per instance when y/x of an instance fits in shared memory
   int64_t zmax = 0;
   for (int s = 0; s < f->nsup; ++s)
@@ -313,7 +317,7 @@ void factor_free_device(qn_factor* f) {
                   f->d_fdep_idx, f->d_stile,      f->d_tcols,     f->d_tg_ptr,    f->d_tg_idx,
                   f->d_hlev_ptr,    f->d_hlev_sup,  f->d_dlev_ptr,  f->d_dlev_sup,
                   f->d_fdesc,   f->d_fblob,       f->d_bdesc,     f->d_tpart,     f->d_tcnt,
-                  f->d_ftile,   f->d_btile};
+                  f->d_ftile,   f->d_btile,       f->d_stage_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   f->on_device = false;

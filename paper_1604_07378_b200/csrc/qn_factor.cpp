@@ -719,6 +719,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       d.nwait = p >= 0 ? f->bcount[p] : 0;
       d.fwd0 = f->ffirst[s];
       d.nfwd = f->fcount[s];
+      d.top_child = (p >= 0 && !f->is_top.empty() && f->is_top[p]) ? 1 : 0;
       f->bdesc.push_back(d);
     }
     // level lists for the batched per-instance solve: forward by height

@@ -30,7 +30,7 @@ struct alignas(16) qn_bdesc {
   int64_t rows;                 // sup_row_ptr[s] (row ids in sup_rows)
   int32_t k0, k1, c0, nc;
   int32_t nr, wait0, nwait, fwd0;  // parent's backward tasks [wait0, wait0 + nwait); own forward tasks from fwd0
-  int32_t nfwd, pad0, pad1, pad2;   // ... nfwd of them (fused kernel)
+  int32_t nfwd, top_child, pad1, pad2;  // ... nfwd of them (fused kernel); parent is in the dense top
 };
 
 struct qn_factor {
@@ -113,6 +113,7 @@ struct qn_factor {
   double* d_stile = nullptr;      // S^-1 as packed lower-triangle tiles (kTopTile^2 each, tile (I,J), I >= J)
   double* d_tpart = nullptr;      // nbatch x nt x nt x kTopTile x 3 partial products of the symmetric top apply
   unsigned* d_tcnt = nullptr;     // nbatch x nt arrival counters of the partials per row block
+  unsigned* d_stage_cnt = nullptr;  // [forward tasks done, top blocks done] (top-fused solve)
   int32_t tnt = 0;                // row blocks of the top (ceil(K / kTopTile))
   int32_t* d_tcols = nullptr;
   int32_t* d_tg_ptr = nullptr;

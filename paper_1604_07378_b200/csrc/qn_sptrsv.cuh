@@ -65,6 +65,8 @@ struct FactorView {
   unsigned long long* trace; // diagnostics: kTraceSlots timestamps per forward then backward item, or null
   int32_t ktop;              // dense top (0 = none)
   int32_t lookahead;         // ticket pipe prefetches the next task (many tasks per CTA)
+  int32_t fuse_top;          // dense-top tiles run as tasks of the persistent fused kernel
+  unsigned* stage_cnt;       // [forward tasks done, top blocks done] (fuse_top)
   int32_t tiled;             // tasks stage Z from the task-tiled copies (TMA) instead of vals (cp.async)
   int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
@@ -128,6 +130,8 @@ inline FactorView factor_view(const qn_factor* f) {
   v.ktop = f->ktop;
   v.opts = f->solve_opts;
   v.lookahead = f->lookahead;
+  v.fuse_top = (f->fused && f->ktop > 0 && !(f->solve_opts & 4)) ? 1 : 0;
+  v.stage_cnt = f->d_stage_cnt;
   v.tiled = f->d_ftile != nullptr;
   v.stile = f->d_stile;
   v.tpart = f->d_tpart;
@@ -228,6 +232,20 @@ __device__ __forceinline__ void wait_flags(const unsigned* flags, const int32_t*
   }
   __syncthreads();
 }
+// Warp 0 polls a completion counter until it reaches `target`; then a CTA barrier.
+__device__ __forceinline__ void wait_count(const unsigned* cnt, unsigned target, unsigned* sched) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtime();
+    while (ld_acquire(cnt) < target) {
+      __nanosleep(32);
+      if (gtime() - t0 > 2000000000ull) {
+        atomicOr(&sched[6], 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void wait_flag_range(const unsigned* flags, int first, int n, unsigned epoch,
                                                 unsigned* sched) {
   if (threadIdx.x < 32) {
@@ -307,23 +325,25 @@ static_assert(sizeof(qn_fdesc) == 64 && sizeof(qn_bdesc) == 64, "descriptor pref
 struct alignas(16) DescSlot {
   unsigned char bytes[64];
 };
-__device__ __forceinline__ void desc_prefetch(const FactorView& F, int item, int nfi, int total, DescSlot* dst) {
-  if (threadIdx.x < 4 && item < total) {
-    const unsigned char* src = item < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + item / F.nbatch)
-                                          : reinterpret_cast<const unsigned char*>(F.bdesc + (item - nfi) / F.nbatch);
+__device__ __forceinline__ void desc_prefetch(const FactorView& F, int item, int nfi, int ntt, int total,
+                                              DescSlot* dst) {
+  if (threadIdx.x < 4 && item < total && !(item >= nfi && item < nfi + ntt)) {
+    const unsigned char* src = item < nfi
+                                   ? reinterpret_cast<const unsigned char*>(F.fdesc + item / F.nbatch)
+                                   : reinterpret_cast<const unsigned char*>(F.bdesc + (item - nfi - ntt) / F.nbatch);
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst->bytes + 16 * threadIdx.x);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 16 * threadIdx.x) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 // take the next ticket (thread 0) and start its descriptor copy; returns it
-__device__ __forceinline__ int pipe_next(const FactorView& F, unsigned* sched, int* s_item, int nfi, int total,
-                                         DescSlot* dst) {
+__device__ __forceinline__ int pipe_next(const FactorView& F, unsigned* sched, int* s_item, int nfi, int ntt,
+                                         int total, DescSlot* dst) {
   __syncthreads();  // the previous task is done with shared memory
   if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
   __syncthreads();
   const int item = *s_item;
-  desc_prefetch(F, item, nfi, total, dst);
+  desc_prefetch(F, item, nfi, ntt, total, dst);
   return item;
 }
 // the current task's descriptor (all but the newest cp.async group) is in place
@@ -338,12 +358,12 @@ __device__ __forceinline__ void pipe_ready() {
 // tasks per CTA: latency-bound, e.g. configs[1]) a CTA never holds a ticket it
 // is not working on, so an idle CTA can start every ready task.
 template <class Body>
-__device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched, int* s_item, int nfi, int total,
-                                            DescSlot* s_desc, Body body) {
+__device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched, int* s_item, int nfi, int ntt,
+                                            int total, DescSlot* s_desc, Body body) {
   if (F.lookahead) {
-    int cur = pipe_next(F, sched, s_item, nfi, total, &s_desc[0]), slot = 0;
+    int cur = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[0]), slot = 0;
     while (cur < total) {
-      const int nxt = pipe_next(F, sched, s_item, nfi, total, &s_desc[slot ^ 1]);
+      const int nxt = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[slot ^ 1]);
       pipe_ready();
       body(cur, s_desc[slot].bytes);
       cur = nxt;
@@ -351,7 +371,7 @@ __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched
     }
   } else {
     for (;;) {
-      const int cur = pipe_next(F, sched, s_item, nfi, total, &s_desc[0]);
+      const int cur = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[0]);
       if (cur >= total) break;
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
@@ -370,6 +390,10 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
       solve_tl(F, kid, 1);
       sched[0] = 0;
       sched[1] = 0;
+      if (F.fuse_top) {
+        F.stage_cnt[0] = 0;
+        F.stage_cnt[1] = 0;
+      }
       __threadfence();
       atomicExch(&sched[2], epoch + 1);
     }
@@ -538,6 +562,7 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   }
   trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
   publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
+  if (F.fuse_top && threadIdx.x == 0) atomicAdd(F.stage_cnt, 1u);  // after the fence of publish()
   trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
 }
 
@@ -615,6 +640,7 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   }
   if (d.nwait > 0)
     wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask, d.wait0, d.nwait, epoch, F.sched);
+  if (F.fuse_top && d.top_child) wait_count(F.stage_cnt + 1, (unsigned)F.tnt, F.sched);  // x_T complete
   trace_mark(F.trace, tb + 2);
   trace_clock(F.trace, tb + 3);
   const double* xg = F.x + (size_t)b * F.n * 3;
@@ -665,7 +691,7 @@ __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F,
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, total, total, s_desc, [&](int cur, const unsigned char* dsc) {
+  ticket_loop(F, sched, &s_item, total, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
     fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
   });
   cta_exit(sched, s_epoch, F, 4);
@@ -686,38 +712,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
+  ticket_loop(F, sched, &s_item, 0, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
     bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase, reinterpret_cast<const qn_bdesc*>(dsc));
-  });
-  cta_exit(sched, s_epoch, F, 5);
-}
-
-// Forward and backward in ONE persistent kernel (no dense top): forward
-// tickets first, then backward tickets, so idle CTAs start staging backward
-// tasks while the forward tail runs and one launch + ramp is saved.  Every
-// dependency has a smaller ticket (a backward task waits for its own
-// supernode's forward tasks and its parent's backward tasks), so the waits
-// cannot deadlock.
-template <class IO>
-__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_item;
-  __shared__ unsigned s_epoch;
-  __shared__ uint64_t s_mbar;
-  unsigned phase = 0;
-  mbar_init(&s_mbar);
-  unsigned* sched = F.sched;
-  if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
-  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
-  const int nfi = F.nftask * F.nbatch, total = nfi + F.nbtask * F.nbatch;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, nfi, total, s_desc, [&](int cur, const unsigned char* dsc) {
-    if (cur < nfi)
-      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
-    else
-      bwd_task(F, io, cur - nfi, s_epoch, sm, lane, warp, true, &s_mbar, phase,
-               reinterpret_cast<const qn_bdesc*>(dsc));
   });
   cta_exit(sched, s_epoch, F, 5);
 }
@@ -740,25 +736,26 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
 constexpr int kTopLD = kTopTile + 1;
 constexpr int kTopTileEntries = kTopTile * kTopLD;  // 4160 doubles = 33,280 B (a multiple of 16)
 
+// One tile (I, J) of the symmetric top apply.  st: kTopTileEntries doubles of
+// shared memory (the tile, then the partial products), gI / gJ: kTopTile * 3
+// each, s_last: 2 ints.  The tile's bulk copy is issued here; with
+// `after_forward` (the top-fused persistent solve) the g_T gather waits until
+// every forward task has completed (the tile streams in meanwhile) and a
+// finalised row block is counted in stage_cnt[1] for the backward tasks.
 template <class IO>
-__global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F, IO io) {
+__device__ __forceinline__ void top_tile(const FactorView& F, const IO& io, int t, int b, double* st, double* gI,
+                                         double* gJ, int* s_last, uint64_t* mbar, unsigned& phase,
+                                         bool after_forward) {
   constexpr int T = kTopTile, LD = kTopLD, NQ = kSolveThreads / T;  // NQ = 4 column / row quarters
-  __shared__ __align__(16) double st[kTopTileEntries];
-  __shared__ double gI[T * 3], gJ[T * 3];
-  __shared__ int s_last[2];
-  __shared__ uint64_t s_mbar;
   double* red = st;  // [2][NQ][T * 3] partial products, after the tile is consumed
-  const int b = blockIdx.y;
-  if (!io.active(b)) return;
-  const int t = blockIdx.x;
   const int K = F.ktop, nt = F.tnt;
-  mbar_init(&s_mbar);
   if (threadIdx.x == 0)
-    bulk_stage(st, F.stile + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), &s_mbar);
+    bulk_stage(st, F.stile + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), mbar);
   int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((I + 1) * (I + 2) / 2 <= t) ++I;
   while (I * (I + 1) / 2 > t) --I;
   const int J = t - I * (I + 1) / 2;
+  if (after_forward) wait_count(F.stage_cnt, (unsigned)F.nftask, F.sched);
   // g_T of this tile's two row blocks, formed here (b_T minus the updates of the
   // subtrees below T, in list order) while the tile streams in — no separate
   // gather kernel; each row block's g is formed by every tile that needs it
@@ -784,7 +781,8 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
       gd[0] = gd[1] = gd[2] = 0.0;
     }
   }
-  mbar_wait(&s_mbar, 0);
+  mbar_wait(mbar, phase);
+  phase ^= 1u;
   __syncthreads();
   const int i = threadIdx.x % T, q = threadIdx.x / T;
   double r0 = 0.0, r1 = 0.0, r2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
@@ -857,14 +855,73 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
       const double v[3] = {gI[3 * threadIdx.x + 0], gI[3 * threadIdx.x + 1], gI[3 * threadIdx.x + 2]};
       const int row = F.tcols[k];
       double* xo = F.x + ((size_t)b * F.n + row) * 3;
-      xo[0] = v[0];
-      xo[1] = v[1];
-      xo[2] = v[2];
+      __stcg(xo + 0, v[0]);
+      __stcg(xo + 1, v[1]);
+      __stcg(xo + 2, v[2]);
       io.store(b, row, v);
     }
-    if (threadIdx.x == 0) F.tcnt[(size_t)b * nt + B] = 0;  // every partial of B has arrived: reset for the next solve
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      F.tcnt[(size_t)b * nt + B] = 0;  // every partial of B has arrived: reset for the next solve
+      if (after_forward) {
+        __threadfence();
+        atomicAdd(F.stage_cnt + 1, 1u);  // row block B of x_T is complete
+      }
+    }
     __syncthreads();
   }
+}
+
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F, IO io) {
+  __shared__ __align__(16) double st[kTopTileEntries];
+  __shared__ double gI[kTopTile * 3], gJ[kTopTile * 3];
+  __shared__ int s_last[2];
+  __shared__ uint64_t s_mbar;
+  const int b = blockIdx.y;
+  if (!io.active(b)) return;
+  mbar_init(&s_mbar);
+  unsigned phase = 0;
+  top_tile(F, io, (int)blockIdx.x, b, st, gI, gJ, s_last, &s_mbar, phase, false);
+}
+
+// Forward, dense-top tiles and backward in ONE persistent kernel: forward
+// tickets, then one ticket per S^-1 tile, then backward tickets, so idle CTAs
+// stage backward tiles while the forward tail runs, and the top's S^-1 tiles
+// stream in while the forward sweep finishes (a tile task issues its bulk copy
+// before waiting for the last forward task).  Every dependency has a smaller
+// ticket (a backward task waits for its own supernode's forward tasks, its
+// parent's backward tasks, and — below the dense top — for every row block
+// of x_T), so the waits cannot deadlock.
+template <class IO>
+__global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_item;
+  __shared__ unsigned s_epoch;
+  __shared__ uint64_t s_mbar;
+  __shared__ int s_last[2];
+  unsigned phase = 0;
+  mbar_init(&s_mbar);
+  unsigned* sched = F.sched;
+  if (threadIdx.x == 0) s_epoch = *((volatile unsigned*)&sched[2]);
+  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 4, 0);
+  const int nfi = F.nftask * F.nbatch;
+  const int ntt = F.fuse_top ? F.tnt * (F.tnt + 1) / 2 : 0;  // top tiles (single instance)
+  const int total = nfi + ntt + F.nbtask * F.nbatch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ DescSlot s_desc[2];
+  ticket_loop(F, sched, &s_item, nfi, ntt, total, s_desc, [&](int cur, const unsigned char* dsc) {
+    if (cur < nfi)
+      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
+    else if (cur < nfi + ntt) {
+      if (io.active(0))  // same predicate as the forward tasks that the tile waits for
+        top_tile(F, io, cur - nfi, 0, sm, sm + kTopTileEntries, sm + kTopTileEntries + 3 * kTopTile, s_last, &s_mbar,
+                 phase, true);
+    } else
+      bwd_task(F, io, cur - nfi - ntt, s_epoch, sm, lane, warp, true, &s_mbar, phase,
+               reinterpret_cast<const qn_bdesc*>(dsc));
+  });
+  cta_exit(sched, s_epoch, F, 5);
 }
 
 // ---- batched small systems (configs[3]): one CTA per instance walks its whole
@@ -1052,9 +1109,10 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
     return QN_OK;
   }
   const int nf = (int)f->ftask.size() * (int)f->nbatch, nb = (int)f->btask.size() * (int)f->nbatch;
-  if (f->fused) {
-    if (nf + nb > 0) {
-      sptrsv_fused<IO><<<std::min(nf + nb, f->grid_fused), kSolveThreads, f->smem_fused, stream>>>(v, io);
+  if (f->fused && (f->ktop == 0 || v.fuse_top)) {
+    const int ntt = v.fuse_top ? f->tnt * (f->tnt + 1) / 2 : 0;
+    if (nf + nb + ntt > 0) {
+      sptrsv_fused<IO><<<std::min(nf + nb + ntt, f->grid_fused), kSolveThreads, f->smem_fused, stream>>>(v, io);
       QN_CHECK_LAUNCH();
     }
     return QN_OK;

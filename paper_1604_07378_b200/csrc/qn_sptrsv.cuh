@@ -68,7 +68,8 @@ struct FactorView {
   int32_t fuse_top;          // dense-top tiles run as tasks of the persistent fused kernel
   unsigned* stage_cnt;       // [forward tasks done, top blocks done] (fuse_top)
   int32_t tiled;             // tasks stage Z from the task-tiled copies (TMA) instead of vals (cp.async)
-  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead
+  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead,
+                             // bit 2 = dense-top tiles inside the fused persistent kernel
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
   double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
   unsigned* tcnt;            // [nbatch][nt] arrivals per row block
@@ -130,7 +131,10 @@ inline FactorView factor_view(const qn_factor* f) {
   v.ktop = f->ktop;
   v.opts = f->solve_opts;
   v.lookahead = f->lookahead;
-  v.fuse_top = (f->fused && f->ktop > 0 && !(f->solve_opts & 4)) ? 1 : 0;
+  // measured slower on c3 (264 vs 249 us per solve: 296 persistent CTAs run the 1891
+  // tiles' latency chains ~6 deep, the stand-alone top kernel keeps 6 tiles per SM in flight);
+  // kept as an option (QN_SOLVE_OPTS bit 2)
+  v.fuse_top = (f->fused && f->ktop > 0 && (f->solve_opts & 4)) ? 1 : 0;
   v.stage_cnt = f->d_stage_cnt;
   v.tiled = f->d_ftile != nullptr;
   v.stile = f->d_stile;

@@ -628,18 +628,46 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
     cp_async_wait_all();
   }
   __syncthreads();
-  // ---- before the parent is done: the y_J part of every column, 4 columns per warp ----
-  // (splitting a few-column task's rows over idle warps measured slower: the
-  // extra barrier costs more than the idle warps)
+  // ---- before the parent is done: the y_J part of every column, 4 columns per warp.
+  // Fewer than kSolveWarps column quads (tall fronts, few columns per task):
+  // each quad's rows are split over rs warps and the slices summed in order ----
   const int ncols = k1 - k0;
-  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-    double a[3];
-    const int j = lane >> 3;
-    col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
-    if ((lane & 7) == 0 && kl + j < ncols) {
-      pre[3 * (kl + j) + 0] = a[0];
-      pre[3 * (kl + j) + 1] = a[1];
-      pre[3 * (kl + j) + 2] = a[2];
+  const int nquads = (ncols + 3) / 4;
+  // tall fronts with few columns per task (the widest separators' children,
+  // nr >= 1024): split each quad's rows over the idle warps; on shorter
+  // fronts the extra barrier costs more than it saves (c2 -1.8 %)
+  const int rs = (nquads >= kSolveWarps || nr < 1024) ? 1 : kSolveWarps / nquads;
+  __shared__ double slp[kSolveWarps][4][3];
+  if (rs > 1) {
+    const int quad = warp / rs, slice = warp % rs, kl = 4 * quad;
+    double a[3] = {0.0, 0.0, 0.0};
+    if (quad < nquads) {
+      const int r0 = k0 + kl, len = nc - r0, per = (len + rs - 1) / rs;
+      const int ra = r0 + slice * per, rb = min(nc, ra + per);
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), ra, max(ra, rb), lane, a);
+    }
+    if ((lane & 7) == 0) {
+      slp[warp][lane >> 3][0] = a[0];
+      slp[warp][lane >> 3][1] = a[1];
+      slp[warp][lane >> 3][2] = a[2];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < 3 * ncols) {
+      const int c = threadIdx.x / 3, q = threadIdx.x - 3 * c;
+      double v = 0.0;
+      for (int sl = 0; sl < rs; ++sl) v += slp[(c >> 2) * rs + sl][c & 3][q];
+      pre[threadIdx.x] = v;
+    }
+  } else {
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), k0 + kl, nc, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        pre[3 * (kl + j) + 0] = a[0];
+        pre[3 * (kl + j) + 1] = a[1];
+        pre[3 * (kl + j) + 2] = a[2];
+      }
     }
   }
   if (d.nwait > 0)
@@ -657,22 +685,56 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   __syncthreads();
   trace_clock(F.trace, tb + 4);
   // ---- the -x_below part, plus the staged y_J part ----
-  for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
-    double a[3];
-    const int j = lane >> 3;
-    col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
-    if ((lane & 7) == 0 && kl + j < ncols) {
-      const int k = k0 + kl + j;
-      const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
-                           a[2] + pre[3 * (kl + j) + 2]};
-      double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
+  if (rs > 1) {
+    const int quad = warp / rs, slice = warp % rs, kl = 4 * quad;
+    double a[3] = {0.0, 0.0, 0.0};
+    if (quad < nquads) {
+      const int len = nr - nc, per = (len + rs - 1) / rs;
+      const int ra = nc + slice * per, rb = min(nr, ra + per);
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), ra, max(ra, rb), lane, a);
+    }
+    __syncthreads();  // the y_J pass's slp reads are done
+    if ((lane & 7) == 0) {
+      slp[warp][lane >> 3][0] = a[0];
+      slp[warp][lane >> 3][1] = a[1];
+      slp[warp][lane >> 3][2] = a[2];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < ncols) {
+      const int c = threadIdx.x;
+      double v[3];
+      for (int q = 0; q < 3; ++q) {
+        double t = 0.0;
+        for (int sl = 0; sl < rs; ++sl) t += slp[(c >> 2) * rs + sl][c & 3][q];
+        v[q] = t + pre[3 * c + q];
+      }
+      double* xo = F.x + ((size_t)b * F.n + c0 + k0 + c) * 3;
       xo[0] = v[0];
       xo[1] = v[1];
       xo[2] = v[2];
-      double* d = sdst[kl + j];
+      double* d = sdst[c];
       d[0] = v[0];
       d[1] = v[1];
       d[2] = v[2];
+    }
+  } else {
+    for (int kl = 4 * warp; kl < ncols; kl += 4 * kSolveWarps) {
+      double a[3];
+      const int j = lane >> 3;
+      col4_dots(zt, nr, w, kl, min(4, ncols - kl), nc, nr, lane, a);
+      if ((lane & 7) == 0 && kl + j < ncols) {
+        const int k = k0 + kl + j;
+        const double v[3] = {a[0] + pre[3 * (kl + j) + 0], a[1] + pre[3 * (kl + j) + 1],
+                             a[2] + pre[3 * (kl + j) + 2]};
+        double* xo = F.x + ((size_t)b * F.n + c0 + k) * 3;
+        xo[0] = v[0];
+        xo[1] = v[1];
+        xo[2] = v[2];
+        double* d = sdst[kl + j];
+        d[0] = v[0];
+        d[1] = v[1];
+        d[2] = v[2];
+      }
     }
   }
   trace_clock(F.trace, tb + 5);

@@ -858,7 +858,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       (rc = sys_alloc(S, &v.part_v, (size_t)ni * v.nblk_v * kNG)) ||
       (rc = sys_alloc(S, &v.part_t, (size_t)ni * v.nblk_t)) || (rc = sys_alloc(S, &v.cnt, (size_t)4 * ni + 1)) ||
       (rc = sys_alloc(S, &v.ctl, (size_t)ni)) || (rc = sys_alloc(S, &S->d_cfg, 1)) ||
-      (rc = sys_alloc(S, &v.active, 1)) || (rc = sys_alloc(S, &v.passes, 1)) ||
+      (rc = sys_alloc(S, &v.active, 1)) || (rc = sys_alloc(S, &v.passes, 2)) ||
       (rc = sys_alloc(S, &S->d_targets, (size_t)ni * std::max<int64_t>(d->n_fixed, 1) * 3)) ||
       (rc = sys_alloc(S, &S->d_part_plain, (size_t)std::max((int64_t)v.nblk_t * v.n_inst, (int64_t)v.nblk_v) * 2)))
     return fail(rc);
@@ -1232,8 +1232,9 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   float ms = 0.f;
   QN_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
   S->last_ms = ms;
-  unsigned long long passes = 0;
-  QN_CUDA(cudaMemcpy(&passes, S->v.passes, sizeof(passes), cudaMemcpyDeviceToHost));
+  unsigned long long pe[2] = {0, 0};  // passes, OR of the instances' error bits (2 ascent, 4 CG at pcg_maxit)
+  QN_CUDA(cudaMemcpy(pe, S->v.passes, sizeof(pe), cudaMemcpyDeviceToHost));
+  const unsigned long long passes = pe[0];
   S->last_passes = (int64_t)passes;
   if (S->use_graph) {  // kernel nodes the graph executed: init + finish + passes + CG iterations
     int64_t cg = 0;
@@ -1244,6 +1245,14 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   if ((int64_t)passes > (int64_t)c.max_passes) {
     set_error("frame: pass limit exceeded (phase machine did not terminate)");
     return QN_ERR_CUDA;
+  }
+  if (pe[1] & 4) {  // the direct solve is exact; an unconverged CG direction is reported, not used silently
+    set_error("frame: PCG stopped at pcg_maxit before reaching pcg_tol (raise pcg_maxit or pcg_tol)");
+    return QN_ERR_ASCENT;
+  }
+  if ((pe[1] & 2) && !rec) {  // with a record the caller reports the failing instance (status bit 1)
+    set_error("line search requires a descent direction (solvers.py:244-246)");
+    return QN_ERR_ASCENT;
   }
   if (rec) {
     const int it = cfg->iterations, cap = S->rec_cap;

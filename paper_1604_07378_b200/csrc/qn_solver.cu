@@ -132,7 +132,8 @@ __global__ void k_init(SysView v) {
     if (v.pcg) v.pctl[b].total = 0;
     if (b == 0) {
       *v.active = v.n_inst;
-      *v.passes = 0;
+      v.passes[0] = 0;
+      v.passes[1] = 0;  // error bits of this frame
     }
   }
 }
@@ -582,6 +583,7 @@ __device__ void finalize_trial(const SysView& v, int b, InstCtl& c, double e_el,
       accept = true;
     } else if (slope >= 0.0) {  // solvers.py:244-246 -> SolverError
       c.status |= 2;
+      atomicOr(v.passes + 1, 2ull);
       c.phase = PH_DONE;
       atomicSub(v.active, 1);
       return;
@@ -1153,6 +1155,10 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
         p.iter += 1;
         p.total += 1;
         if ((conv & 7) == 7 || p.iter >= v.pcg_maxit) {
+          if ((conv & 7) != 7) {  // stopped at pcg_maxit short of pcg_tol: reported by the host
+            v.ctl[b].status |= 4;
+            atomicOr(v.passes + 1, 4ull);
+          }
           conv |= 8;
           atomicSub(v.pcg_active, 1);
         }

@@ -145,6 +145,7 @@ class SlabRank:
         import torch
 
         self.lay = lay
+        self.pcg_maxit = int(pcg_maxit)
         n = lay.n
         pin = np.zeros(n, dtype=bool)
         pg = np.asarray(pinned_global, dtype=np.int64)
@@ -511,7 +512,11 @@ class SlabRun:
                 conv, its = self.comm.local[0].pcg_status()
                 if conv & 8:
                     self.cg_iterations += its
+                    if conv & 7 != 7:  # stopped at pcg_maxit short of pcg_tol
+                        raise SolverError("slab frame: PCG stopped at pcg_maxit before reaching pcg_tol")
                     break
+                if it > self.comm.local[0].pcg_maxit + self.pcg_check:  # host-side bound on the stage loop
+                    raise SolverError("slab frame: PCG did not report convergence within pcg_maxit iterations")
         self._stage(STORE)
         self._ev("halo", lambda: self.comm.halo(R0))
 

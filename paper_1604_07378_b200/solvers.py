@@ -143,6 +143,9 @@ class _RecordBuffers:
         bad = np.nonzero(self.status & 2)[0]
         if bad.size:
             raise SolverError(f"line search requires a descent direction (instance {int(bad[0])})")
+        bad = np.nonzero(self.status & 4)[0]
+        if bad.size:
+            raise SolverError(f"PCG stopped at pcg_maxit before reaching pcg_tol (instance {int(bad[0])})")
 
 
 NEWTON_FD_STEP_REL = 1e-6   # solvers.py:32

@@ -161,3 +161,31 @@ def test_fault_knob_arguments_checked(c1):
     with pytest.raises(Exception):
         system.set_fault(1, 0)
     system.set_fault(0)
+
+
+def test_pcg_stopping_at_maxit_is_reported():
+    """a CG that stops at pcg_maxit short of pcg_tol raises instead of
+    handing an inexact direction to the line search silently (device status
+    bit 2 of the frame's error word; the host loop of the slab frame checks the
+    same condition)."""
+    sc = scenes.c5(grid=(12, 4, 4), frames=1)
+    system = Q.build_system(Q.TetMesh(sc.verts, sc.tets, sc.density), from_spec(sc.material), h=sc.h,
+                            gravity=sc.gravity, fixed=sc.fixed, solver="pcg", pcg_tol=1e-14, pcg_maxit=3)
+    with pytest.raises(Q.SolverError, match="pcg_maxit"):
+        Q.simulate_frame(system, state(sc), Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
+    run = Q.ResidentRun(system, state(sc), Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
+    with pytest.raises(Q.SolverError, match="pcg_maxit"):
+        run.step()
+
+
+def test_ascent_reported_by_the_resident_path(c1):
+    """The device-resident step (no record requested) reports an ascent
+    direction too, through the frame's error word."""
+    sc, system, _ = c1
+    system.set_fault(1, 2)
+    try:
+        run = Q.ResidentRun(system, state(sc), Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m))
+        with pytest.raises(Q.SolverError):
+            run.step()
+    finally:
+        system.set_fault(0)

@@ -433,9 +433,12 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
       bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
     }
   } else {  // small factors: straight from vals, which the backward re-reads from L2
+    // lanes over the tile's rows; a tile of R < 32 rows puts 32 / R columns on each warp
     const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
-    for (int k = warp; k < kmax; k += kSolveWarps)
-      for (int rr = lane; rr < R; rr += 32) cp_async8(zt + k * R + rr, Zg + (int64_t)k * nr + rr);
+    const int Ls = R < 32 ? 32 / R : 1, subs = R < 32 ? lane / R : 0, r0 = R < 32 ? lane - subs * R : lane;
+    if (subs < Ls)
+      for (int k = warp * Ls + subs; k < kmax; k += kSolveWarps * Ls)
+        for (int rr = r0; rr < R; rr += 32) cp_async8(zt + k * R + rr, Zg + (int64_t)k * nr + rr);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   const int nptr_bot = blo < hi ? hi - blo + 1 : 0;

@@ -373,13 +373,18 @@ __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched
       cur = nxt;
       slot ^= 1;
     }
-  } else {
+  } else {  // the task reads its descriptor from global memory (no extra barrier on the critical path)
     for (;;) {
-      const int cur = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[0]);
-      if (cur >= total) break;
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();  // the previous task is done with shared memory
+      if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
       __syncthreads();
-      body(cur, s_desc[0].bytes);
+      const int cur = *s_item;
+      if (cur >= total) break;
+      const unsigned char* dp =
+          cur < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + cur / F.nbatch)
+          : cur < nfi + ntt ? nullptr
+                            : reinterpret_cast<const unsigned char*>(F.bdesc + (cur - nfi - ntt) / F.nbatch);
+      body(cur, dp);
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -418,7 +423,7 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   const int b = item % F.nbatch;
   if (!io.active(b)) return;
   trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
-  const qn_fdesc d = *sdesc;  // prefetched into shared memory by the ticket pipe
+  const qn_fdesc d = *sdesc;  // shared memory (lookahead prefetch) or global memory
   const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
   const int R = hi - lo;
   const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
@@ -584,7 +589,7 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   const int b = item % F.nbatch;
   if (!io.active(b)) return;
   trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
-  const qn_bdesc d = *sdesc;  // prefetched into shared memory by the ticket pipe
+  const qn_bdesc d = *sdesc;  // shared memory (lookahead prefetch) or global memory
   const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
   const int64_t R0 = d.rows;
   double* w = sm + F.bwd_entries;

@@ -96,7 +96,7 @@ cudaStream_t pick(qn_system* S, void* stream) { return stream ? (cudaStream_t)st
 // (library factorisation of a setup-time dense block; seconds on the host).
 // The result is symmetric, so its column-major layout is the row-major one the
 // coarse kernel reads.
-int coarse_inverse_device(qn_system* S, const qn::Csr& A, double** out) {
+int coarse_inverse_device(qn_system* S, const qn::Csr& A, float** out) {
   const int64_t nc = A.n;
   std::vector<double> M((size_t)nc * nc, 0.0);
   for (int64_t i = 0; i < nc; ++i)
@@ -132,7 +132,16 @@ int coarse_inverse_device(qn_system* S, const qn::Csr& A, double** out) {
     set_error(hinfo ? "amg: coarsest operator is not positive definite" : "amg: cuSOLVER coarse inverse failed");
     return hinfo ? QN_ERR_NOT_SPD : QN_ERR_CUDA;
   }
-  *out = dI;
+  // stored in fp32: the coarse solve is part of the preconditioner only (a fixed
+  // operator; CG still solves the fp64 A_free to pcg_tol), and half the bytes
+  // of the per-cycle dense product
+  float* f32 = nullptr;
+  if ((rc = sys_alloc(S, &f32, (size_t)nc * nc))) return rc;
+  std::vector<double> hd((size_t)nc * nc);
+  QN_CUDA(cudaMemcpy(hd.data(), dI, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost));
+  std::vector<float> hf(hd.begin(), hd.end());
+  QN_CUDA(cudaMemcpy(f32, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice));
+  *out = f32;
   return QN_OK;
 }
 
@@ -760,7 +769,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       v.amg_levels = nl;
       v.ncoarse = (int32_t)H.lv.back().A.n;
       phase("amg build + upload");
-      double* ci;
+      float* ci;
       if ((rc = coarse_inverse_device(S, H.lv.back().A, &ci))) return fail(rc);
       v.cinv = ci;
       phase("coarse inverse");

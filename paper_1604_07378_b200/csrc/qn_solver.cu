@@ -1313,10 +1313,23 @@ __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
   const int lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
   for (int k = w0; k < nc; k += nw) {
-    const double* row = v.cinv + (size_t)k * nc;
+    const float* row = v.cinv + (size_t)k * nc;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int c = lane; c < nc; c += 32) {
-      const double m = __ldg(row + c);
+    int c = lane;
+    for (; c + 96 < nc; c += 128) {  // 4 loads in flight per lane
+      float m[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m[u] = __ldg(row + c + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cc = c + 32 * u;
+        a0 = fma((double)m[u], sb[3 * cc + 0], a0);
+        a1 = fma((double)m[u], sb[3 * cc + 1], a1);
+        a2 = fma((double)m[u], sb[3 * cc + 2], a2);
+      }
+    }
+    for (; c < nc; c += 32) {
+      const double m = (double)__ldg(row + c);
       a0 = fma(m, sb[3 * c + 0], a0);
       a1 = fma(m, sb[3 * c + 1], a1);
       a2 = fma(m, sb[3 * c + 2], a2);

@@ -168,7 +168,7 @@ struct SysView {
   // ---- AMG-preconditioned CG (pcg == 2) ----
   int32_t amg_levels, ncoarse;
   const AmgDevLevel* alev;  // [amg_levels] (device)
-  const double* cinv;       // dense inverse of the coarsest operator [ncoarse][ncoarse]
+  const float* cinv;        // dense inverse of the coarsest operator [ncoarse][ncoarse], fp32 (preconditioner only)
   double* pz;               // z = B r (the V-cycle output on level 0)
   // ---- colliders (dynamics.py:199-285, 446-457, 486-516) ----
   int32_t n_col, nblk_c;

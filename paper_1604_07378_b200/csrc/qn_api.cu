@@ -895,6 +895,7 @@ int qn_system_destroy(qn_system* S) {
   for (void* p : S->allocs) cudaFree(p);
   if (S->factor) qn_factor_destroy(S->factor);
   if (S->h_stage) cudaFreeHost(S->h_stage);
+  if (S->h_rec) cudaFreeHost(S->h_rec);
   if (S->ev0) cudaEventDestroy(S->ev0);
   if (S->ev1) cudaEventDestroy(S->ev1);
   if (S->stream) cudaStreamDestroy(S->stream);
@@ -1139,11 +1140,22 @@ int qn_state_get(qn_system* S, double* q_l, double* q_prev, double* y, int32_t m
 static int ensure_records(qn_system* S, int iterations) {
   if (iterations <= S->rec_cap) return QN_OK;
   int cap = std::max(iterations, 32);
-  const size_t cnt = (size_t)S->n_inst * cap;
+  const size_t ni = (size_t)S->n_inst, cnt = ni * cap;
+  const size_t bytes = sizeof(double) * (3 * cnt + ni) + sizeof(int32_t) * (cnt + 2 * ni);
   int rc;
-  if ((rc = sys_alloc(S, &S->v.rec_g, cnt)) || (rc = sys_alloc(S, &S->v.rec_trials, cnt)) ||
-      (rc = sys_alloc(S, &S->v.rec_alpha, cnt)) || (rc = sys_alloc(S, &S->v.rec_ms, cnt)))
-    return rc;
+  char* pack = nullptr;
+  if ((rc = sys_alloc(S, &pack, bytes))) return rc;
+  S->v.rec_g = reinterpret_cast<double*>(pack);
+  S->v.rec_alpha = S->v.rec_g + cnt;
+  S->v.rec_ms = S->v.rec_alpha + cnt;
+  S->v.rec_g0 = S->v.rec_ms + cnt;
+  S->v.rec_trials = reinterpret_cast<int32_t*>(S->v.rec_g0 + ni);
+  S->v.rec_status = S->v.rec_trials + cnt;
+  S->v.rec_fb = S->v.rec_status + ni;
+  if (S->h_rec) cudaFreeHost(S->h_rec);
+  S->h_rec = nullptr;
+  QN_CUDA(cudaMallocHost(&S->h_rec, bytes));
+  S->rec_bytes = bytes;
   S->rec_cap = cap;
   S->v.rec_cap = cap;
   if (S->exec) {  // pointers changed: rebuild the graph
@@ -1266,38 +1278,25 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   if (rec) {
     const int it = cfg->iterations, cap = S->rec_cap;
     const int64_t ni = S->n_inst;
-    // only the record fields of the control blocks (strided copies, not the
-    // whole ~2.5 KB block per instance)
-    std::vector<double> ctl_g0(ni);
-    std::vector<int32_t> ctl_status(ni), ctl_fb(ni);
-    const char* cb = reinterpret_cast<const char*>(S->v.ctl);
-    QN_CUDA(cudaMemcpy2D(ctl_g0.data(), sizeof(double), cb + offsetof(InstCtl, g0), sizeof(InstCtl), sizeof(double),
-                         ni, cudaMemcpyDeviceToHost));
-    QN_CUDA(cudaMemcpy2D(ctl_status.data(), sizeof(int32_t), cb + offsetof(InstCtl, status), sizeof(InstCtl),
-                         sizeof(int32_t), ni, cudaMemcpyDeviceToHost));
-    QN_CUDA(cudaMemcpy2D(ctl_fb.data(), sizeof(int32_t), cb + offsetof(InstCtl, fallbacks), sizeof(InstCtl),
-                         sizeof(int32_t), ni, cudaMemcpyDeviceToHost));
-    std::vector<double> g((size_t)ni * cap), al((size_t)ni * cap), ms_((size_t)ni * cap);
-    std::vector<int32_t> tr((size_t)ni * cap);
-    QN_CUDA(cudaMemcpy(g.data(), S->v.rec_g, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    QN_CUDA(cudaMemcpy(al.data(), S->v.rec_alpha, al.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    QN_CUDA(cudaMemcpy(ms_.data(), S->v.rec_ms, ms_.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    QN_CUDA(cudaMemcpy(tr.data(), S->v.rec_trials, tr.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    std::vector<double> g0(ni);
-    std::vector<int32_t> status(ni), fallbacks(ni);
+    const size_t cnt = (size_t)ni * cap;
+    // one D2H of the packed record arrays (k_finish copied the control blocks' g0 / status / fallbacks)
+    QN_CUDA(cudaMemcpyAsync(S->h_rec, S->v.rec_g, S->rec_bytes, cudaMemcpyDeviceToHost, st));
+    QN_CUDA(cudaStreamSynchronize(st));
+    const double* hg = static_cast<const double*>(S->h_rec);
+    const double *g = hg, *al = hg + cnt, *ms_ = hg + 2 * cnt, *hg0 = hg + 3 * cnt;
+    const int32_t* tr = reinterpret_cast<const int32_t*>(hg0 + ni);
+    const int32_t *hst = tr + cnt, *hfb = hst + ni;
+    std::vector<double> g0(hg0, hg0 + ni);
+    std::vector<int32_t> status(hst, hst + ni), fallbacks(hfb, hfb + ni);
     std::vector<double> og((size_t)ni * it), oa((size_t)ni * it), om((size_t)ni * it);
     std::vector<int32_t> ot((size_t)ni * it);
-    for (int64_t b = 0; b < ni; ++b) {
-      g0[b] = ctl_g0[b];
-      status[b] = ctl_status[b];
-      fallbacks[b] = ctl_fb[b];
+    for (int64_t b = 0; b < ni; ++b)
       for (int k = 0; k < it; ++k) {
         og[b * it + k] = g[b * cap + k];
         oa[b * it + k] = al[b * cap + k];
         om[b * it + k] = ms_[b * cap + k];
         ot[b * it + k] = tr[b * cap + k];
       }
-    }
     auto put = [&](auto* dst, const auto& src) -> int {
       if (!dst) return QN_OK;
       using T = typename std::decay<decltype(src[0])>::type;

@@ -818,6 +818,11 @@ __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
 __global__ void k_finish(SysView v) {
   const int b = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && v.rec_g0) {  // record fields of the control block, next to the record arrays (one D2H)
+    v.rec_g0[b] = v.ctl[b].g0;
+    v.rec_status[b] = v.ctl[b].status;
+    v.rec_fb[b] = v.ctl[b].fallbacks;
+  }
   if (i >= v.n) return;
   const size_t o = inst_off(v, b) + (size_t)i * 3;
   const double* x = v.X + vec_off(v, v.ctl[b].xs_cur, b) + (size_t)i * 3;

@@ -136,10 +136,13 @@ struct SysView {
   unsigned* cnt;   // [4][inst] last-block counters + [global]
   InstCtl* ctl;
   const DevConfig* cfg;
-  double* rec_g;
-  int32_t* rec_trials;
-  double* rec_alpha;
+  double* rec_g;          // the record arrays are sub-ranges of one allocation (one D2H per frame):
+  int32_t* rec_trials;    // [g | alpha | ms : ni x cap doubles][g0 : ni doubles][trials : ni x cap int32]
+  double* rec_alpha;      // [status | fallbacks : ni int32 each]
   double* rec_ms;
+  double* rec_g0;         // filled by k_finish from the control blocks
+  int32_t* rec_status;
+  int32_t* rec_fb;
   int32_t* active;     // instances not yet done
   unsigned long long* passes;
   unsigned long long* ktl;  // diagnostics timeline [kTimelinePasses][kTimelineKernels][2] ns, or null
@@ -203,6 +206,8 @@ struct qn_system {
   int rec_cap = 0;
   // pinned host staging
   double* h_stage = nullptr;
+  void* h_rec = nullptr;  // pinned mirror of the packed record arrays
+  size_t rec_bytes = 0;
   size_t h_stage_bytes = 0;
   // graph
   bool use_graph = true;

@@ -46,6 +46,7 @@ constexpr int kSlabSellUnroll = 8;
 
 struct SlabPcg {
   double rz[3], bb[3], alpha[3];
+  double rzc[3];                   // <r_c, A_c^-1 r_c> of the coarse correction (two-level preconditioner)
   int32_t conv, iter, total, pad;  // conv: bit c = column c converged, bit 3 = all done
 };
 
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(kSlabFT) k_slab_pcg_p(SlabView s, int first) {
   int conv = pc.conv;
   const double tol2 = s.pcg_tol * s.pcg_tol;
   for (int c = 0; c < 3; ++c) {
-    const double a0 = gsum(s, c), a1 = gsum(s, 3 + c);
+    // <r, z> = sum_ranks <r, B_slab r> (+ <r_c, A_c^-1 r_c>: the coarse term, known to every rank)
+    const double a0 = gsum(s, c), a1 = s.nc > 0 ? gsum(s, 3 + c) + pc.rzc[c] : gsum(s, 3 + c);
     rz[c] = a1;
     if (first) {
       bb[c] = a0;
@@ -536,6 +538,30 @@ __global__ void __launch_bounds__(kSlabVT) k_slab_coarse_x(SlabView s) {
 
 // the ranks' restricted residuals summed in rank order into shared memory,
 // then the dense coarse inverse, warp per coarse row
+// <r_c, e_c> per column (one block, fixed order): the coarse part of <r, z>,
+// identical on every rank (r_c is the rank-order sum of the gathered shares)
+__global__ void __launch_bounds__(kSpmvThreads) k_slab_coarse_dot(SlabView s) {
+  if (s.pc->conv & 8) return;
+  __shared__ double red[kSpmvThreads / 32][3];
+  const int n3 = 3 * s.nc;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = threadIdx.x; k < s.nc; k += blockDim.x)
+    for (int c = 0; c < 3; ++c) {
+      double rc = 0.0;
+      for (int r = 0; r < s.G; ++r) rc += s.cgath[(size_t)r * n3 + 3 * k + c];
+      acc[c] = fma(rc, s.ec[3 * (size_t)k + c], acc[c]);
+    }
+  for (int c = 0; c < 3; ++c) acc[c] = warp_sum(acc[c]);
+  if ((threadIdx.x & 31) == 0)
+    for (int c = 0; c < 3; ++c) red[threadIdx.x >> 5][c] = acc[c];
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < kSpmvThreads / 32; ++w) t += red[w][threadIdx.x];
+    s.pc->rzc[threadIdx.x] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kSpmvThreads) k_slab_coarse_solve(SlabView s) {
   if (s.pc->conv & 8) return;
   extern __shared__ double rcs[];
@@ -939,6 +965,8 @@ int qn_slab_stage(qn_slab* S, int32_t stage, const double* args, int32_t nargs, 
                             (size_t)3 * s.nc * sizeof(double), st>>>(s);
       QN_CHECK_LAUNCH();
       k_slab_coarse_p<<<s.nblk_flat, kSlabFT, 0, st>>>(s);
+      QN_CHECK_LAUNCH();
+      k_slab_coarse_dot<<<1, kSpmvThreads, 0, st>>>(s);
       QN_CHECK_LAUNCH();
       break;
     case QN_SLAB_STORE:

@@ -272,6 +272,11 @@ class EmulatedComm:
         for rk in self.ranks:
             rk.buf[pair[1]].copy_(allv)
 
+    def allgather_pair(self, a, b):
+        """two all-gathers as one exchange (NcclComm packs them into one collective)"""
+        self.allgather(a)
+        self.allgather(b)
+
     def reduce_dense(self, parts):
         """rank-order sum of every rank's dense setup matrix"""
         out = np.zeros_like(parts[0])
@@ -308,6 +313,24 @@ class NcclComm:
 
     def allgather(self, pair=(SEND, GATHER)):
         self.dist.all_gather_into_tensor(self.rk.buf[pair[1]], self.rk.buf[pair[0]], group=self.group)
+
+    def allgather_pair(self, a, b):
+        """all-gather of two send buffers in ONE collective: packed [a | b] per rank,
+        gathered, unpacked into the two receive buffers (device copies)."""
+        import torch
+        sa, sb = self.rk.buf[a[0]], self.rk.buf[b[0]]
+        na, nb = sa.numel(), sb.numel()
+        world = self.dist.get_world_size(self.group)
+        if getattr(self, "_pack", None) is None or self._pack[0].numel() != na + nb:
+            self._pack = (torch.empty(na + nb, dtype=sa.dtype, device=sa.device),
+                          torch.empty(world * (na + nb), dtype=sa.dtype, device=sa.device))
+        send, recv = self._pack
+        send[:na].copy_(sa)
+        send[na:].copy_(sb)
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        rv = recv.view(world, na + nb)
+        self.rk.buf[a[1]].view(world, na).copy_(rv[:, :na])
+        self.rk.buf[b[1]].view(world, nb).copy_(rv[:, na:])
 
     def reduce_dense(self, parts):
         """rank-order sum of every rank's dense setup matrix (all-gather, then
@@ -485,18 +508,26 @@ class SlabRun:
         return 0.5 / self.h ** 2 * v[1] + v[0]
 
     def _precondition(self):
-        """z = B_slab r (done by the stage) [+ P_c A_c^-1 sum_ranks P_c^T r], then <r, z>."""
+        """z = B_slab r (done by the preceding stage) [+ P_c A_c^-1 sum_ranks P_c^T r],
+        and the scalars of the next CG step, with ONE collective: the rank's
+        <r, r> and <r, B_slab r> partials (SEND) travel with its coarse share
+        P_c^T r (CSEND); every rank then forms r_c, e_c = A_c^-1 r_c and the
+        coarse term <r_c, e_c> of <r, z> identically (qn_slab.cu k_slab_coarse_dot)."""
         if self.comm.local[0].coarse:
             self._stage(COARSE_R)
-            self._ev("allgather_coarse", lambda: self.comm.allgather((CSEND, CGATHER)))
+            self._stage(PCG_RZ)
+            self._ev("allgather", lambda: self.comm.allgather_pair((SEND, GATHER), (CSEND, CGATHER)))
             self._stage(COARSE_APPLY)
-        self._stage(PCG_RZ)
+        else:
+            self._stage(PCG_RZ)
+            self._ev("allgather", self.comm.allgather)
 
     def _solve(self, ring, zeta):
-        """r0 = A_free^-1 (-g - sum zeta t) by CG over the slabs (3 columns)."""
+        """r0 = A_free^-1 (-g - sum zeta t) by CG over the slabs (3 columns).
+        Collectives per CG iteration: the plane exchange of p, one all-gather
+        of <p, q>, one all-gather of <r, r>, <r, z> (+ the coarse shares)."""
         self._stage(PCG_SETUP, ring=ring, coef=zeta)
         self._precondition()
-        self._ev("allgather", self.comm.allgather)
         self._stage(PCG_P, first=1)
         it = 0
         while True:
@@ -505,7 +536,6 @@ class SlabRun:
             self._ev("allgather", self.comm.allgather)
             self._stage(PCG_UPDATE)
             self._precondition()
-            self._ev("allgather", self.comm.allgather)
             self._stage(PCG_P, first=0)
             it += 1
             if it % self.pcg_check == 0:

@@ -100,7 +100,9 @@ class _StubRank:
         self.lay = lay
         self.buf = {slab.SEND: torch.zeros(slab.NSEND, dtype=torch.float64),
                     slab.GATHER: torch.zeros(lay.world * slab.NSEND, dtype=torch.float64),
-                    slab.P: torch.zeros(lay.n * 3, dtype=torch.float64)}
+                    slab.P: torch.zeros(lay.n * 3, dtype=torch.float64),
+                    slab.CSEND: torch.zeros(3 * 7, dtype=torch.float64),
+                    slab.CGATHER: torch.zeros(lay.world * 3 * 7, dtype=torch.float64)}
 
     def plane_slices(self):
         from paper_1604_07378_b200.slab import SlabRank
@@ -122,25 +124,36 @@ def _comm_worker(rank, world, port, out):
         comm = slab.NcclComm(rk)
         comm.allgather()
         comm.halo(slab.P)
-        out[rank] = (lay, rk.buf[slab.GATHER].numpy().copy(), rk.buf[slab.P].numpy().copy(), gid.numpy())
+        gath1 = rk.buf[slab.GATHER].numpy().copy()
+        # the CG's merged exchange: scalars and coarse shares in one collective
+        rk.buf[slab.SEND][:] = -torch.arange(slab.NSEND, dtype=torch.float64) - 1000 * rank
+        rk.buf[slab.CSEND][:] = torch.arange(21, dtype=torch.float64) + 10000 * rank
+        comm.allgather_pair((slab.SEND, slab.GATHER), (slab.CSEND, slab.CGATHER))
+        out[rank] = (lay, gath1, rk.buf[slab.P].numpy().copy(), gid.numpy(), rk.buf[slab.GATHER].numpy().copy(),
+                     rk.buf[slab.CGATHER].numpy().copy())
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_slab_communicator_allgather_and_halo(world):
-    """NcclComm's all-gather and plane exchange (gloo on CPU): every rank gets
-    every SEND in rank order, and every local vertex (ghost planes included)
-    holds its owner's value after the halo exchange."""
+    """NcclComm's all-gather, the CG's merged all-gather of the scalars and the
+    coarse shares, and the plane exchange (gloo on CPU): every rank gets every
+    SEND (and CSEND) in rank order, and every local vertex (ghost planes
+    included) holds its owner's value after the halo exchange."""
     from paper_1604_07378_b200 import slab
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     expect = np.concatenate([np.arange(slab.NSEND) + 100.0 * r for r in range(world)])
+    exp2 = np.concatenate([-np.arange(slab.NSEND) - 1000.0 * r for r in range(world)])
+    exp3 = np.concatenate([np.arange(21) + 10000.0 * r for r in range(world)])
     for r in range(world):
-        lay, gath, p, gid = out[r]
+        lay, gath, p, gid, g2, cg2 = out[r]
         np.testing.assert_array_equal(gath, expect)
         np.testing.assert_array_equal(p, gid)
+        np.testing.assert_array_equal(g2, exp2)  # allgather_pair: both buffers, rank order
+        np.testing.assert_array_equal(cg2, exp3)
     assert np.array_equal(slab.rank_sum(expect.reshape(world, -1)), sum(expect.reshape(world, -1)[r] for r in range(world)))
 
 

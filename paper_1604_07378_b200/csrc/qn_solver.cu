@@ -1556,7 +1556,7 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
   // batched (one CTA per instance: every row's rhs is formed exactly once) and
   // latency-bound factors (few tasks per CTA, c2: the extra kernel node costs
   // more than the redundant row loads) form the rhs inside the solve
-  if (S->factor->batch_smem > 0 || !S->factor->lookahead) {
+  if (S->factor->batch_smem > 0 || !S->factor->many_tasks) {
     SolverIO io{v};
     return launch_solve(S->factor, io, st);
   }

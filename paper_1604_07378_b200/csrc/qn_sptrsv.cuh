@@ -68,8 +68,9 @@ struct FactorView {
   int32_t fuse_top;          // dense-top tiles run as tasks of the persistent fused kernel
   unsigned* stage_cnt;       // [forward tasks done, top blocks done] (fuse_top)
   int32_t tiled;             // tasks stage Z from the task-tiled copies (TMA) instead of vals (cp.async)
-  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = no lookahead,
-                             // bit 2 = dense-top tiles inside the fused persistent kernel
+  int32_t opts;              // experiment knob (QN_SOLVE_OPTS): bit 0 = no forward lane groups, bit 1 = ticket lookahead,
+                             // bit 2 = dense-top tiles inside the fused persistent kernel, bit 3 = next-tile prefetch, bit 4 = no L2 evict-first hint on the streamed tiles,
+                             // bit 5 = shallow lookahead, bit 6 = no lookahead in the backward kernel, bit 7 = no in-task ticket
   const double* stile;       // S^-1 as lower-triangle kTopTile^2 tiles, tile (I,J) at I(I+1)/2 + J
   double* tpart;             // [nbatch][nt][nt][kTopTile][3] partial products
   unsigned* tcnt;            // [nbatch][nt] arrivals per row block
@@ -154,6 +155,7 @@ constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kStageIdx = 2048;  // int32 index slots staged in shared memory per task
 constexpr int kTraceSlots = 7;   // globaltimer ticket, staged, ready; clock64 ready, data staged, computed, published
 constexpr int kBwdCols = (int)kBwdTaskCols;  // max columns of a backward task
+constexpr int kIssueThread = 32;  // warp 1 issues tile copies / takes tickets; warp 0 polls and publishes meanwhile
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -181,6 +183,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 // TMA bulk staging of a contiguous tile: thread 0 arms the CTA's mbarrier with
 // the byte count and issues one cp.async.bulk; every thread later waits on the
 // barrier's phase (parity flips once per task).
@@ -192,8 +198,25 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar) {
   }
   __syncthreads();
 }
-__device__ __forceinline__ void bulk_stage(void* dst, const void* src, unsigned bytes, uint64_t* mbar) {
+// `stream`: the source is read once per sweep (Z tiles of a factor larger than
+// L2, S^-1 tiles): the copy carries an L2 evict-first policy so the streamed
+// matrix does not push the small reused data (update vectors, y / x, lists,
+// descriptors, flags, right-hand sides) out of L2 — their dependent loads sit
+// on every task's critical path.
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, unsigned bytes, uint64_t* mbar,
+                                           bool stream = false) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst), m = (unsigned)__cvta_generic_to_shared(mbar);
+  if (stream) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "fence.proxy.async.shared::cta;\n\t"
+        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %1, [%0], %4;" ::"r"(m),
+        "r"(bytes), "r"(d), "l"(src), "l"(pol)
+        : "memory");
+    return;
+  }
   asm volatile(
       "fence.proxy.async.shared::cta;\n\t"
       "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
@@ -218,22 +241,24 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Warp 0 polls n flags (lane-parallel) until all equal `epoch`; then a CTA
 // barrier.  A wait longer than 2 s means a scheduling bug: it is recorded in
 // sched[6] (checked by the host) instead of hanging the device.
-__device__ __forceinline__ void wait_flags(const unsigned* flags, const int32_t* ids, int n, unsigned epoch,
-                                           unsigned* sched) {
-  if (threadIdx.x < 32) {
-    const unsigned long long t0 = gtime();
-    for (int q = threadIdx.x; q < n; q += 32) {
-      const unsigned* p = flags + ids[q];
-      while (ld_acquire(p) != epoch) {
-        __nanosleep(8);
-        if (gtime() - t0 > 2000000000ull) {
-          atomicOr(&sched[6], 1u);
-          break;
-        }
+__device__ __forceinline__ void poll_flags_warp0(const unsigned* flags, const int32_t* ids, int n, unsigned epoch,
+                                                 unsigned* sched) {
+  const unsigned long long t0 = gtime();
+  for (int q = threadIdx.x; q < n; q += 32) {
+    const unsigned* p = flags + ids[q];
+    while (ld_acquire(p) != epoch) {
+      __nanosleep(8);
+      if (gtime() - t0 > 2000000000ull) {
+        atomicOr(&sched[6], 1u);
+        break;
       }
     }
-    __syncwarp();
   }
+  __syncwarp();
+}
+__device__ __forceinline__ void wait_flags(const unsigned* flags, const int32_t* ids, int n, unsigned epoch,
+                                           unsigned* sched) {
+  if (threadIdx.x < 32) poll_flags_warp0(flags, ids, n, epoch, sched);
   __syncthreads();
 }
 // Warp 0 polls a completion counter until it reaches `target`; then a CTA barrier.
@@ -340,51 +365,180 @@ __device__ __forceinline__ void desc_prefetch(const FactorView& F, int item, int
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
-// take the next ticket (thread 0) and start its descriptor copy; returns it
-__device__ __forceinline__ int pipe_next(const FactorView& F, unsigned* sched, int* s_item, int nfi, int ntt,
-                                         int total, DescSlot* dst) {
-  __syncthreads();  // the previous task is done with shared memory
-  if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
-  __syncthreads();
-  const int item = *s_item;
-  desc_prefetch(F, item, nfi, ntt, total, dst);
-  return item;
-}
-// the current task's descriptor (all but the newest cp.async group) is in place
-__device__ __forceinline__ void pipe_ready() {
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-  __syncthreads();
+// Tile prefetch across tasks (tiled factors with ticket lookahead): the Z tile
+// buffer of a task is free as soon as its mat-vec has read it, so the bulk copy
+// of the CTA's NEXT ticket is issued right there (its descriptor is already in
+// shared memory) and streams in behind the epilogue, the flag publication, the
+// ticket bookkeeping and the next task's staging / dependency wait.  The
+// per-task staging latency (~1.9 of ~6.7 us on c3) leaves the CTA's critical
+// path without a second tile buffer.
+struct TileAhead {
+  bool pre;                  // this task's tile copy is already in flight
+  int nxt;                   // the CTA's next ticket (>= total: none)
+  const unsigned char* dsc;  // its descriptor in shared memory (null: no lookahead)
+};
+
+// Issue the Z tile copy of ticket `item` (descriptor `dsc`, complete and
+// visible to the CTA) into zt.  Returns whether a copy is now in flight
+// (CTA-uniform: every thread evaluates the same predicate).
+template <class IO>
+__device__ __forceinline__ bool tile_issue(const FactorView& F, const IO& io, int item, int nfi, int ntt, int total,
+                                           const unsigned char* dsc, double* zt, uint64_t* mbar) {
+  if (!F.tiled || !dsc || item >= total || !(F.opts & 8)) return false;
+  if (item < nfi) {
+    const int b = item % F.nbatch;
+    if (!io.active(b)) return false;
+    if (threadIdx.x == kIssueThread) {
+      const qn_fdesc* d = reinterpret_cast<const qn_fdesc*>(dsc);
+      const int cnt = (d->hi - d->lo) * (d->hi <= d->nc ? d->hi : d->nc);
+      bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d->zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar,
+                 !(F.opts & 16));
+    }
+    return true;
+  }
+  if (item < nfi + ntt) return false;  // dense-top tiles stage themselves
+  const int b = (item - nfi - ntt) % F.nbatch;
+  if (!io.active(b)) return false;
+  if (threadIdx.x == kIssueThread) {
+    const qn_bdesc* d = reinterpret_cast<const qn_bdesc*>(dsc);
+    const int cnt = (d->k1 - d->k0) * d->nr;
+    bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d->zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar,
+               !(F.opts & 16));
+  }
+  return true;
 }
 
-// The ticket loop of a persistent solve kernel: body(item, descriptor slot).
-// With lookahead (many tasks per CTA: throughput-bound, e.g. configs[2]) the
-// next descriptor is prefetched during the current task; without it (few
-// tasks per CTA: latency-bound, e.g. configs[1]) a CTA never holds a ticket it
-// is not working on, so an idle CTA can start every ready task.
+// The CTA's next ticket, taken DURING a task (large factors without lookahead):
+// thread kIssueThread issues the counter's atomic before the task's mat-vec and
+// turns the ticket into a descriptor copy after it, so the two round trips of
+// "take a ticket, read its descriptor" overlap the compute, the epilogue and
+// the flag publication instead of following them.  The ticket is held for half
+// a task only (a CTA that takes tickets a whole task early delays the tasks it
+// holds: measured slower on c3, in the backward sweep above all).
+struct NextTicket {
+  unsigned* sched;
+  int* s_item;     // where the ticket goes
+  DescSlot* slot;  // where its descriptor goes
+  int nfi, ntt, total;
+  bool on;
+};
+__device__ __forceinline__ void next_take(const NextTicket& n, unsigned& tk) {
+  if (n.on && threadIdx.x == kIssueThread) tk = atomicAdd(&n.sched[0], 1u);
+}
+__device__ __forceinline__ void next_desc(const FactorView& F, const NextTicket& n, unsigned tk) {
+  if (n.on && threadIdx.x == kIssueThread) {
+    const int item = (int)tk;
+    n.s_item[0] = item;
+    if (item < n.total && !(item >= n.nfi && item < n.nfi + n.ntt)) {
+      const unsigned char* src =
+          item < n.nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + item / F.nbatch)
+                       : reinterpret_cast<const unsigned char*>(F.bdesc + (item - n.nfi - n.ntt) / F.nbatch);
+      const unsigned d = (unsigned)__cvta_generic_to_shared(n.slot->bytes);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * q), "l"(src + 16 * q) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+}
+
+// What a finished task leaves for the ticket loop to do.
+struct TaskDone {
+  unsigned* flag;   // completion flag to publish (null: nothing to publish)
+  long long tr;     // trace slot of the 'published' stamp (-1: none)
+  bool pre;         // the next ticket's tile copy is already in flight
+  bool count_fwd;   // fuse_top: count a finished forward task
+  bool took;        // the task took the CTA's next ticket (NextTicket)
+};
+__device__ __forceinline__ TaskDone no_task() { return TaskDone{nullptr, -1, false, false, false}; }
+
+// publish a finished task (thread 0, after a CTA barrier that followed all of
+// the task's global writes): one gpu-scope acq_rel fence — cumulative over the
+// writes the barrier ordered — and a relaxed flag store
+__device__ __forceinline__ void publish_done(const FactorView& F, const TaskDone& dn, unsigned epoch) {
+  if (dn.flag) {
+    asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(dn.flag), "r"(epoch) : "memory");
+    if (dn.count_fwd) atomicAdd(F.stage_cnt, 1u);  // after the fence
+    if (dn.tr >= 0 && F.trace) F.trace[dn.tr] = (unsigned long long)clock64();
+  }
+}
+
+// The ticket loop of a persistent solve kernel: body(item, descriptor, tile
+// prefetch state) runs one task up to (not including) its publication and
+// returns a TaskDone.
+//
+// With lookahead (many tasks per CTA: throughput-bound, e.g. configs[2]) a CTA
+// holds three tickets: the one it works on, the next one (descriptor already in
+// shared memory) and the one after (its atomic is in flight: issued a task
+// early by thread 0 and consumed a task later, so the counter's round trip is
+// off the per-task path).  One CTA barrier separates two tasks: it orders the
+// finished task's writes before thread 0's fence + flag store and frees the
+// task's shared memory; thread 0 publishes AFTER that barrier while the other
+// warps already stage the next task (the fence's round trip overlaps their
+// loads).  Tickets stay monotone per CTA and every dependency has a smaller
+// ticket, so the smallest unfinished ticket is always some CTA's current one
+// and the waits cannot deadlock.
+// Without lookahead (few tasks per CTA: latency-bound, e.g. configs[1]) a CTA
+// never holds a ticket it is not working on, so an idle CTA can start every
+// ready task; the task reads its descriptor from global memory.
 template <class Body>
 __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched, int* s_item, int nfi, int ntt,
-                                            int total, DescSlot* s_desc, Body body) {
-  if (F.lookahead) {
-    int cur = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[0]), slot = 0;
-    while (cur < total) {
-      const int nxt = pipe_next(F, sched, s_item, nfi, ntt, total, &s_desc[slot ^ 1]);
-      pipe_ready();
-      body(cur, s_desc[slot].bytes);
-      cur = nxt;
-      slot ^= 1;
+                                            int total, DescSlot* s_desc, const unsigned& epoch, bool look, Body body) {
+  if (look) {
+    const bool deep = !(F.opts & 32);  // the ticket after next is taken a task early
+    unsigned ahead = 0;  // thread 0: the ticket after next
+    if (threadIdx.x == 0) {
+      s_item[0] = (int)atomicAdd(&sched[0], 1u);
+      s_item[1] = (int)atomicAdd(&sched[0], 1u);
+      if (deep) ahead = atomicAdd(&sched[0], 1u);
     }
-  } else {  // the task reads its descriptor from global memory (no extra barrier on the critical path)
-    for (;;) {
-      __syncthreads();  // the previous task is done with shared memory
-      if (threadIdx.x == 0) *s_item = (int)atomicAdd(&sched[0], 1u);
-      __syncthreads();
-      const int cur = *s_item;
+    __syncthreads();
+    int cur = s_item[0], nxt = s_item[1], slot = 0, it = 0;
+    desc_prefetch(F, cur, nfi, ntt, total, &s_desc[0]);
+    desc_prefetch(F, nxt, nfi, ntt, total, &s_desc[1]);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // the first descriptor
+    __syncthreads();
+    bool pre = false;  // cur's Z tile copy was already issued by the previous task (CTA-uniform)
+    while (cur < total) {
+      const TaskDone dn = body(cur, s_desc[slot].bytes, TileAhead{pre, nxt, s_desc[slot ^ 1].bytes},
+                               NextTicket{sched, s_item, s_desc, nfi, ntt, total, false});
+      asm volatile("cp.async.wait_group 0;" ::: "memory");  // nxt's descriptor (issued a task ago) has landed
+      if (threadIdx.x == 0) s_item[it & 1] = deep ? (int)ahead : (int)atomicAdd(&sched[0], 1u);
+      __syncthreads();  // the one barrier between two tasks
+      if (threadIdx.x == 0) {
+        publish_done(F, dn, epoch);
+        if (deep) ahead = atomicAdd(&sched[0], 1u);
+      }
+      const int nn = s_item[it & 1];
+      desc_prefetch(F, nn, nfi, ntt, total, &s_desc[slot]);
+      cur = nxt;
+      nxt = nn;
+      slot ^= 1;
+      ++it;
+      pre = dn.pre;
+    }
+  } else {
+    const bool late = F.tiled && !(F.opts & 128);  // the next ticket is taken during the task (NextTicket)
+    bool have = false;
+    for (int it = 0;; ++it) {
+      if (!have) {
+        __syncthreads();  // the previous task is done with shared memory
+        if (threadIdx.x == 0) s_item[0] = (int)atomicAdd(&sched[0], 1u);
+        __syncthreads();
+      }
+      const int cur = s_item[0];
       if (cur >= total) break;
       const unsigned char* dp =
-          cur < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + cur / F.nbatch)
-          : cur < nfi + ntt ? nullptr
-                            : reinterpret_cast<const unsigned char*>(F.bdesc + (cur - nfi - ntt) / F.nbatch);
-      body(cur, dp);
+          cur >= nfi && cur < nfi + ntt ? nullptr
+          : have                        ? s_desc[(it & 1) ^ 1].bytes  // copied by the previous task
+          : cur < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + cur / F.nbatch)
+                      : reinterpret_cast<const unsigned char*>(F.bdesc + (cur - nfi - ntt) / F.nbatch);
+      const TaskDone dn = body(cur, dp, TileAhead{false, total, nullptr},
+                               NextTicket{sched, s_item, &s_desc[it & 1], nfi, ntt, total, late});
+      asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next descriptor (thread kIssueThread)
+      __syncthreads();
+      if (threadIdx.x == 0) publish_done(F, dn, epoch);
+      have = dn.took;
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -416,12 +570,14 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
 // One forward task (row block of one supernode): stage, wait for the
 // children, gather their updates, v = Z f, publish.
 template <class IO>
-__device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp, uint64_t* mbar, unsigned& phase, const qn_fdesc* sdesc) {
+__device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
+                                             int lane, int warp, uint64_t* mbar, unsigned& phase,
+                                             const qn_fdesc* sdesc, const TileAhead& ahead, const NextTicket& nt,
+                                             int nfi, int ntt, int total) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
-  if (!io.active(b)) return;
+  if (!io.active(b)) return no_task();
   trace_mark(F.trace, kTraceSlots * (size_t)item + 0);
   const qn_fdesc d = *sdesc;  // shared memory (lookahead prefetch) or global memory
   const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
@@ -432,11 +588,43 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   int* sidx = (int*)(part + 3 * kSolveThreads);
   const double* ub = F.u + (size_t)b * F.nupd * 3;
   // ---- stage everything that does not depend on the children ----
-  if (F.tiled) {  // Z tile rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)]: one contiguous block
-    if (threadIdx.x == 0) {
+  const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
+  const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
+  const int* gblob = F.fblob + d.blob;
+  const bool staged = nblob <= kStageIdx;
+  const int* sp_top = staged ? sidx : gblob;  // relative extend-add lists: [sp_top | sp_bot | si_top | si_bot]
+  const int* sp_bot = sp_top + nc + 1;
+  const int* si_top = sp_bot + nptr_bot;
+  const int* si_bot = si_top + d.ntop;
+  if (F.tiled) {
+    // Large factors (throughput-bound): the warps split the roles so that the
+    // task's independent round trips overlap — warp 1 issues the tile's bulk
+    // copy (rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)], one contiguous
+    // block), warp 0 polls the children's flags at once, warps 1..7 copy the
+    // lists (asynchronously) and load the right-hand side.
+    if (threadIdx.x == kIssueThread && !ahead.pre) {
       const int cnt = R * kmax;
-      bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar);
+      bulk_stage(zt, F.ftile + (size_t)b * F.ftile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)), mbar,
+                 !(F.opts & 16));
     }
+    if (warp == 0) {
+      poll_flags_warp0(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch,
+                       F.sched);
+    } else {
+      const int t = threadIdx.x - 32, nt = kSolveThreads - 32;
+      if (staged)
+        for (int q = t; q < nblob; q += nt) cp_async4(sidx + q, gblob + q);
+      for (int p = t; p < nc; p += nt) {
+        double v[3];
+        io.rhs(b, c0 + p, v);
+        f[3 * p + 0] = v[0];
+        f[3 * p + 1] = v[1];
+        f[3 * p + 2] = v[2];
+      }
+      cp_async_wait_all();
+    }
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
+    __syncthreads();
   } else {  // small factors: straight from vals, which the backward re-reads from L2
     // lanes over the tile's rows; a tile of R < 32 rows puts 32 / R columns on each warp
     const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
@@ -445,26 +633,18 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
       for (int k = warp * Ls + subs; k < kmax; k += kSolveWarps * Ls)
         for (int rr = r0; rr < R; rr += 32) cp_async8(zt + k * R + rr, Zg + (int64_t)k * nr + rr);
     asm volatile("cp.async.commit_group;" ::: "memory");
+    if (staged)
+      for (int q = threadIdx.x; q < nblob; q += blockDim.x) sidx[q] = __ldg(gblob + q);
+    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+      double v[3];
+      io.rhs(b, c0 + p, v);
+      f[3 * p + 0] = v[0];
+      f[3 * p + 1] = v[1];
+      f[3 * p + 2] = v[2];
+    }
+    trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
+    wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
   }
-  const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
-  const int nblob = nc + 1 + nptr_bot + d.ntop + d.nbot;
-  const int* gblob = F.fblob + d.blob;
-  const bool staged = nblob <= kStageIdx;
-  if (staged)
-    for (int q = threadIdx.x; q < nblob; q += blockDim.x) sidx[q] = __ldg(gblob + q);
-  const int* sp_top = staged ? sidx : gblob;  // relative extend-add lists: [sp_top | sp_bot | si_top | si_bot]
-  const int* sp_bot = sp_top + nc + 1;
-  const int* si_top = sp_bot + nptr_bot;
-  const int* si_bot = si_top + d.ntop;
-  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-    double v[3];
-    io.rhs(b, c0 + p, v);
-    f[3 * p + 0] = v[0];
-    f[3 * p + 1] = v[1];
-    f[3 * p + 2] = v[2];
-  }
-  trace_mark(F.trace, kTraceSlots * (size_t)item + 1);
-  wait_flags(F.flags + (size_t)b * (F.nftask + F.nbtask), F.fdep_idx + d.dep0, d.dep1 - d.dep0, epoch, F.sched);
   trace_mark(F.trace, kTraceSlots * (size_t)item + 2);
   trace_clock(F.trace, kTraceSlots * (size_t)item + 3);
   // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
@@ -498,6 +678,8 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
     cp_async_wait_all();
   }
   __syncthreads();
+  unsigned tk = 0;
+  next_take(nt, tk);  // the counter's round trip runs behind the mat-vec
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
   // a tile of R < 32 rows (wide supernodes) also splits each warp's k-slice
@@ -550,7 +732,11 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
   part[3 * threadIdx.x + 0] = a0;
   part[3 * threadIdx.x + 1] = a1;
   part[3 * threadIdx.x + 2] = a2;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next ticket's descriptor has landed
   __syncthreads();
+  // the tile is consumed: the next ticket's copy streams in behind the epilogue and the publication
+  const bool issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
+  next_desc(F, nt, tk);  // the descriptor's round trip runs behind the epilogue and the publication
   if (threadIdx.x < R) {
     const int gg = threadIdx.x >> 5;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -573,21 +759,21 @@ __device__ __forceinline__ void fwd_task(const FactorView& F, const IO& io, int 
     }
   }
   trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
-  publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, epoch);
-  if (F.fuse_top && threadIdx.x == 0) atomicAdd(F.stage_cnt, 1u);  // after the fence of publish()
-  trace_clock(F.trace, kTraceSlots * (size_t)item + 6);
+  return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, (long long)(kTraceSlots * (size_t)item + 6),
+                  issued, F.fuse_top != 0, nt.on};
 }
 
 // One backward task (column block of one supernode).  fused: forward and
 // backward share one persistent kernel, so y_J is waited for explicitly.
 template <class IO>
-__device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
-                                         int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase,
-                                         const qn_bdesc* sdesc) {
+__device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
+                                             int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase,
+                                             const qn_bdesc* sdesc, const TileAhead& ahead, const NextTicket& nt,
+                                             int nfi, int ntt, int total) {
   double* zt = sm;
   const int tid = item / F.nbatch;
   const int b = item % F.nbatch;
-  if (!io.active(b)) return;
+  if (!io.active(b)) return no_task();
   trace_mark(F.trace, kTraceSlots * ((size_t)F.nftask * F.nbatch + item) + 0);
   const qn_bdesc d = *sdesc;  // shared memory (lookahead prefetch) or global memory
   const int k0 = d.k0, k1 = d.k1, c0 = d.c0, nc = d.nc, nr = d.nr;
@@ -599,10 +785,10 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   const bool staged = nr - nc <= kStageIdx;
   // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
   if (F.tiled) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == kIssueThread && !ahead.pre) {
       const int cnt = (k1 - k0) * nr;
       bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)),
-                 mbar);
+                 mbar, !(F.opts & 16));
     }
   } else {
     const double* Zg = F.vals + (size_t)b * F.nvals + d.zoff;
@@ -619,14 +805,25 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
   if (fused)  // the forward of s may still be running: y_J must be complete
     wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask), d.fwd0, d.nfwd, epoch, F.sched);
   const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
-  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
-    w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
-    w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
-    w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
+  if (F.tiled && !fused) {
+    // y_J and the below-row ids as asynchronous copies: one round trip together with the
+    // destinations.  (The 8-byte copies allocate in L1: only in the stand-alone backward
+    // kernel, where y is never written; the fused kernel keeps the L2 loads below.)
+    for (int q = threadIdx.x; q < 3 * nc; q += blockDim.x) cp_async8(w + q, yg + q);
+    if (staged)
+      for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) cp_async4(srow + q, F.sup_rows + R0 + nc + q);
+    for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
+    cp_async_wait_all();
+  } else {
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+      w[3 * q + 0] = __ldcg(yg + 3 * q + 0);
+      w[3 * q + 1] = __ldcg(yg + 3 * q + 1);
+      w[3 * q + 2] = __ldcg(yg + 3 * q + 2);
+    }
+    if (staged)
+      for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
+    for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
   }
-  if (staged)
-    for (int q = threadIdx.x; q < nr - nc; q += blockDim.x) srow[q] = F.sup_rows[R0 + nc + q];
-  for (int q = threadIdx.x; q < k1 - k0; q += blockDim.x) sdst[q] = io.dest(b, c0 + k0 + q);
   const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
   trace_mark(F.trace, tb + 1);
   if (F.tiled) {
@@ -691,6 +888,8 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
     w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
   }
   __syncthreads();
+  unsigned tk = 0;
+  next_take(nt, tk);  // the counter's round trip runs behind the second pass
   trace_clock(F.trace, tb + 4);
   // ---- the -x_below part, plus the staged y_J part ----
   if (rs > 1) {
@@ -746,15 +945,22 @@ __device__ __forceinline__ void bwd_task(const FactorView& F, const IO& io, int 
     }
   }
   trace_clock(F.trace, tb + 5);
-  publish(F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, epoch);
-  trace_clock(F.trace, tb + 6);
+  next_desc(F, nt, tk);  // the descriptor's round trip runs behind the publication
+  bool issued = false;
+  if (F.opts & 8) {  // next-tile prefetch (experiment): needs its own barrier after the last tile read
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next ticket's descriptor has landed
+    __syncthreads();
+    issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
+  }
+  return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, (long long)(tb + 6), issued, false,
+                  nt.on};
 }
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F, IO io) {
   // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_item;
+  __shared__ int s_item[2];
   __shared__ unsigned s_epoch;
   __shared__ uint64_t s_mbar;
   unsigned phase = 0;
@@ -765,8 +971,9 @@ __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F,
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, total, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
-    fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
+  ticket_loop(F, sched, s_item, total, 0, total, s_desc, s_epoch, F.lookahead != 0, [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
+    return fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc), ahead,
+                    nt, total, 0, total);
   });
   cta_exit(sched, s_epoch, F, 4);
 }
@@ -775,7 +982,7 @@ template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
   // smem: ztile[bwd_entries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | dest[kBwdCols] | row staging
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_item;
+  __shared__ int s_item[2];
   __shared__ unsigned s_epoch;
   __shared__ uint64_t s_mbar;
   unsigned phase = 0;
@@ -786,8 +993,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, 0, 0, total, s_desc, [&](int cur, const unsigned char* dsc) {
-    bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase, reinterpret_cast<const qn_bdesc*>(dsc));
+  ticket_loop(F, sched, s_item, 0, 0, total, s_desc, s_epoch, F.lookahead && !(F.opts & 64), [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
+    return bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase, reinterpret_cast<const qn_bdesc*>(dsc),
+                    ahead, nt, 0, 0, total);
   });
   cta_exit(sched, s_epoch, F, 5);
 }
@@ -824,7 +1032,7 @@ __device__ __forceinline__ void top_tile(const FactorView& F, const IO& io, int 
   double* red = st;  // [2][NQ][T * 3] partial products, after the tile is consumed
   const int K = F.ktop, nt = F.tnt;
   if (threadIdx.x == 0)
-    bulk_stage(st, F.stile + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), mbar);
+    bulk_stage(st, F.stile + (size_t)t * kTopTileEntries, kTopTileEntries * sizeof(double), mbar, !(F.opts & 16));
   int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((I + 1) * (I + 2) / 2 <= t) ++I;
   while (I * (I + 1) / 2 > t) --I;
@@ -970,7 +1178,7 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_item;
+  __shared__ int s_item[2];
   __shared__ unsigned s_epoch;
   __shared__ uint64_t s_mbar;
   __shared__ int s_last[2];
@@ -984,16 +1192,18 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
   const int total = nfi + ntt + F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, &s_item, nfi, ntt, total, s_desc, [&](int cur, const unsigned char* dsc) {
+  ticket_loop(F, sched, s_item, nfi, ntt, total, s_desc, s_epoch, F.lookahead != 0, [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
     if (cur < nfi)
-      fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc));
-    else if (cur < nfi + ntt) {
+      return fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc),
+                      ahead, nt, nfi, ntt, total);
+    if (cur < nfi + ntt) {
       if (io.active(0))  // same predicate as the forward tasks that the tile waits for
         top_tile(F, io, cur - nfi, 0, sm, sm + kTopTileEntries, sm + kTopTileEntries + 3 * kTopTile, s_last, &s_mbar,
                  phase, true);
-    } else
-      bwd_task(F, io, cur - nfi - ntt, s_epoch, sm, lane, warp, true, &s_mbar, phase,
-               reinterpret_cast<const qn_bdesc*>(dsc));
+      return no_task();
+    }
+    return bwd_task(F, io, cur - nfi - ntt, s_epoch, sm, lane, warp, true, &s_mbar, phase,
+                    reinterpret_cast<const qn_bdesc*>(dsc), ahead, nt, nfi, ntt, total);
   });
   cta_exit(sched, s_epoch, F, 5);
 }
@@ -1233,8 +1443,11 @@ int prepare_solve_kernels(qn_factor* f) {
   f->grid_b = f->grid_b ? std::min(f->grid_b, gb) : gb;
   // descriptor lookahead pays off when CTAs run many tasks each (c3: 27, c2: 5 per CTA)
   const int64_t tasks = (int64_t)(f->ftask.size() + f->btask.size()) * f->nbatch;
-  f->lookahead = tasks >= 12 * (int64_t)std::max(f->grid_f, 1) ? 1 : 0;
-  if (f->solve_opts & 2) f->lookahead = 0;
+  f->many_tasks = tasks >= 12 * (int64_t)std::max(f->grid_f, 1) ? 1 : 0;
+  // Ticket lookahead (a CTA holds its next ticket for a whole task) measured slower than taking the
+  // next ticket during the task (NextTicket) once the staging round trips were overlapped: c3 solve
+  // 223 vs 207 us.  QN_SOLVE_OPTS bit 1 turns it back on for experiments.
+  f->lookahead = (f->many_tasks && (f->solve_opts & 2)) ? 1 : 0;
   return QN_OK;
 }
 

@@ -289,14 +289,13 @@ int factor_upload(qn_factor* f) {
   const unsigned sched[8] = {0, 0, 1, 0, 0, 1, 0, 0};  // [ticket, exited, epoch] x 2, watchdog
   if ((rc = dev_upload(&f->d_sched, sched, 8))) return rc;
   if ((rc = dev_alloc(&f->d_io, (size_t)f->n * 6))) return rc;
-  int max_nc = 0, max_nc_task = 0;
-  for (int s = 0; s < f->nsup; ++s) {
-    max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
-    if (f->is_top.empty() || !f->is_top[s]) max_nc_task = std::max(max_nc_task, f->sup_col[s + 1] - f->sup_col[s]);
-  }
-  // forward: Z tile + f (nc x 3) + partials (256 x 3) + index staging;
+  int max_nc = 0;
+  for (int s = 0; s < f->nsup; ++s) max_nc = std::max(max_nc, f->sup_col[s + 1] - f->sup_col[s]);
+  // forward: Z tile + f (nc x 3), sized per task (fwd_entries = the largest), + index staging, which the
+  // partial sums (256 x 3) reuse after the gathers;
   // backward: Z tile + w (nr x 3) + pre (64 x 3) + destinations (64) + row staging
-  f->smem_f = (int)(sizeof(double) * (f->fwd_entries + 3 * ((size_t)max_nc_task + kSolveThreads)) + sizeof(int) * kStageIdx);
+  static_assert(sizeof(int) * kStageIdx >= sizeof(double) * 3 * kSolveThreads, "partials reuse the index staging");
+  f->smem_f = (int)(sizeof(double) * (size_t)f->fwd_entries + sizeof(int) * kStageIdx);
   f->smem_b = (int)(sizeof(double) * (f->bwd_entries + 3 * (size_t)f->task_max_rows + 4 * kBwdCols) + sizeof(int) * kStageIdx);
   QN_REQUIRE(std::max(f->smem_f, f->smem_b) <= 227 * 1024, QN_ERR_UNSUPPORTED,
              "factor: supernode front exceeds shared memory");

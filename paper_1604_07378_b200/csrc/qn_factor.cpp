@@ -609,6 +609,7 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
     const int64_t te_f = knob("QN_FWD_TASK_ENTRIES", kTaskEntries, kTaskEntries);
     const int64_t te_b = knob("QN_BWD_TASK_ENTRIES", kTaskEntries, kTaskEntries);
     const int64_t bcols = knob("QN_BWD_TASK_COLS", kBwdTaskCols, kBwdTaskCols);
+    const int64_t fwd_budget = knob("QN_FWD_BUDGET", kFwdBudget, 1 << 20);
     // backward Z tile: as large as kTaskEntries but small enough that two
     // CTAs (each also holding w = nr x 3 of the tallest front) share an SM
     {
@@ -627,12 +628,17 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
       const int32_t nr = (int32_t)(f->sup_row_ptr[s + 1] - f->sup_row_ptr[s]);
       QN_REQUIRE(nc <= kTaskEntries && nr - nc <= (int64_t)1 << 20, QN_ERR_UNSUPPORTED,
                  "factor: supernode too wide for the device solve tiles");
-      const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, te_f / (32 * (int64_t)nc))));
-      const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::max<int64_t>(1, std::min<int64_t>(32, te_f / nc));
+      // a task's shared memory holds its Z tile and f (nc x 3): wide supernodes get
+      // smaller tiles so that tile + f stays within kFwdBudget (three CTAs per SM)
+      const int64_t room = fwd_budget - 3 * (int64_t)nc;
+      const int64_t te_s = room >= 4 * (int64_t)nc ? std::min(te_f, room) : te_f;
+      const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, te_s / (32 * (int64_t)nc))));
+      const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::max<int64_t>(1, std::min<int64_t>(32, te_s / nc));
       f->ffirst[s] = (int32_t)f->ftask.size();
       for (int32_t r = 0; r < nr; r += rows) {
         const int32_t hi = std::min(nr, r + rows);
-        f->fwd_entries = std::max<int64_t>(f->fwd_entries, ((int64_t)(hi - r) * std::min(hi, nc) + 1) / 2 * 2);
+        f->fwd_entries =
+            std::max<int64_t>(f->fwd_entries, ((int64_t)(hi - r) * std::min(hi, nc) + 1) / 2 * 2 + 3 * (int64_t)nc);
         f->ftask.push_back({s, r, std::min(nr, r + rows), rg});
         f->fcount[s]++;
       }

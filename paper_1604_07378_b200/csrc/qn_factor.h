@@ -70,7 +70,7 @@ struct qn_factor {
   int32_t max_rows = 0, depth = 0;
   int32_t task_max_rows = 0;   // tallest front among the supernodes solved by tasks (not the dense top)
   int64_t bwd_entries = 8192;  // Z entries per backward task tile (<= kTaskEntries, set by the task builder)
-  int64_t fwd_entries = 8192;  // largest forward task tile (<= kTaskEntries, even)
+  int64_t fwd_entries = 8192;  // forward task shared memory in doubles: largest (even tile + f = nc x 3) over the tasks
   double flops = 0.0, factor_seconds = 0.0;
   // ---- numeric (host, nbatch x nvals) ----
   std::vector<double> vals;
@@ -142,6 +142,9 @@ constexpr int kTopTile = 64;            // symmetric top apply: S^-1 stored as 6
 constexpr int64_t kTopDenseAll = 1536;  // systems this small are solved entirely as x = A^-1 b (dense)
 constexpr int64_t kTopMinWidth = 600;   // a level joins the dense top only if its widest supernode has >= this many columns
 constexpr int64_t kBwdTaskCols = 64;    // max columns of a backward task
+// forward tasks: tile + f doubles so that three CTAs (tile + f + 8 KB of list / partial-sum staging + static)
+// share an SM's 228 KB
+constexpr int64_t kFwdBudget = (74 * 1024 - 8192) / 8;
 constexpr int64_t kSmemPerCtaPair = 110 * 1024;  // dynamic smem per CTA with two CTAs per SM (228 KB - reserved/static)
 // bottom-of-tree subtree collapse (see factor_build_host)
 constexpr int32_t kCollapseHeight = 2;  // swept on c1-c3 with the current solve kernels: 2 > 3 (+3.6 % at c2), 1 and 4 slower

@@ -425,20 +425,29 @@ struct NextTicket {
 __device__ __forceinline__ void next_take(const NextTicket& n, unsigned& tk) {
   if (n.on && threadIdx.x == kIssueThread) tk = atomicAdd(&n.sched[0], 1u);
 }
-__device__ __forceinline__ void next_desc(const FactorView& F, const NextTicket& n, unsigned tk) {
+// the next ticket's descriptor as four 16-byte loads into thread kIssueThread's registers
+// (in flight behind the epilogue and the publication; next_store puts them in shared memory)
+struct NextRegs {
+  unsigned tk;
+  uint4 q[4];
+};
+__device__ __forceinline__ void next_desc(const FactorView& F, const NextTicket& n, NextRegs& r) {
   if (n.on && threadIdx.x == kIssueThread) {
-    const int item = (int)tk;
-    n.s_item[0] = item;
+    const int item = (int)r.tk;
     if (item < n.total && !(item >= n.nfi && item < n.nfi + n.ntt)) {
-      const unsigned char* src =
-          item < n.nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + item / F.nbatch)
-                       : reinterpret_cast<const unsigned char*>(F.bdesc + (item - n.nfi - n.ntt) / F.nbatch);
-      const unsigned d = (unsigned)__cvta_generic_to_shared(n.slot->bytes);
+      const uint4* src = item < n.nfi ? reinterpret_cast<const uint4*>(F.fdesc + item / F.nbatch)
+                                      : reinterpret_cast<const uint4*>(F.bdesc + (item - n.nfi - n.ntt) / F.nbatch);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * q), "l"(src + 16 * q) : "memory");
+      for (int q = 0; q < 4; ++q) r.q[q] = __ldg(src + q);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+}
+__device__ __forceinline__ void next_store(const NextTicket& n, const NextRegs& r) {
+  if (n.on && threadIdx.x == kIssueThread) {
+    n.s_item[0] = (int)r.tk;
+    uint4* dst = reinterpret_cast<uint4*>(n.slot->bytes);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = r.q[q];
   }
 }
 
@@ -449,8 +458,9 @@ struct TaskDone {
   bool pre;         // the next ticket's tile copy is already in flight
   bool count_fwd;   // fuse_top: count a finished forward task
   bool took;        // the task took the CTA's next ticket (NextTicket)
+  NextRegs nx;      // ... and holds its descriptor (thread kIssueThread)
 };
-__device__ __forceinline__ TaskDone no_task() { return TaskDone{nullptr, -1, false, false, false}; }
+__device__ __forceinline__ TaskDone no_task() { return TaskDone{nullptr, -1, false, false, false, NextRegs{}}; }
 
 // publish a finished task (thread 0, after a CTA barrier that followed all of
 // the task's global writes): one gpu-scope acq_rel fence — cumulative over the
@@ -533,12 +543,15 @@ __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched
           : have                        ? s_desc[(it & 1) ^ 1].bytes  // copied by the previous task
           : cur < nfi ? reinterpret_cast<const unsigned char*>(F.fdesc + cur / F.nbatch)
                       : reinterpret_cast<const unsigned char*>(F.bdesc + (cur - nfi - ntt) / F.nbatch);
-      const TaskDone dn = body(cur, dp, TileAhead{false, total, nullptr},
-                               NextTicket{sched, s_item, &s_desc[it & 1], nfi, ntt, total, late});
-      asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next descriptor (thread kIssueThread)
+      const NextTicket nt{sched, s_item, &s_desc[it & 1], nfi, ntt, total, late};
+      const TaskDone dn = body(cur, dp, TileAhead{false, total, nullptr}, nt);
       __syncthreads();
       if (threadIdx.x == 0) publish_done(F, dn, epoch);
       have = dn.took;
+      if (have) {  // the next ticket and its descriptor arrive behind the publication's fence
+        next_store(nt, dn.nx);
+        __syncthreads();
+      }
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -583,9 +596,11 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   const int lo = d.lo, hi = d.hi, rg = d.rg, c0 = d.c0, nc = d.nc, nr = d.nr, blo = d.blo;
   const int R = hi - lo;
   const int kmax = hi <= nc ? hi : nc;  // rows inside the triangle need k <= row only
-  double* f = sm + F.fwd_entries;
-  double* part = f + 3 * nc;
-  int* sidx = (int*)(part + 3 * kSolveThreads);
+  // shared memory: [tile (R x kmax, even) | f (nc x 3)] ... [index staging at fwd_entries], whose
+  // space the k-slice partial sums reuse once the gathers are done (barrier before the mat-vec)
+  double* f = sm + ((R * kmax + 1) & ~1);
+  int* sidx = (int*)(sm + F.fwd_entries);
+  double* part = (double*)sidx;
   const double* ub = F.u + (size_t)b * F.nupd * 3;
   // ---- stage everything that does not depend on the children ----
   const int nptr_bot = blo < hi ? hi - blo + 1 : 0;
@@ -678,8 +693,8 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
     cp_async_wait_all();
   }
   __syncthreads();
-  unsigned tk = 0;
-  next_take(nt, tk);  // the counter's round trip runs behind the mat-vec
+  NextRegs nx{};
+  next_take(nt, nx.tk);  // the counter's round trip runs behind the mat-vec
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
   // a tile of R < 32 rows (wide supernodes) also splits each warp's k-slice
@@ -736,7 +751,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   __syncthreads();
   // the tile is consumed: the next ticket's copy streams in behind the epilogue and the publication
   const bool issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
-  next_desc(F, nt, tk);  // the descriptor's round trip runs behind the epilogue and the publication
+  next_desc(F, nt, nx);  // the descriptor's round trip runs behind the epilogue and the publication
   if (threadIdx.x < R) {
     const int gg = threadIdx.x >> 5;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -760,7 +775,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   }
   trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
   return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, (long long)(kTraceSlots * (size_t)item + 6),
-                  issued, F.fuse_top != 0, nt.on};
+                  issued, F.fuse_top != 0, nt.on, nx};
 }
 
 // One backward task (column block of one supernode).  fused: forward and
@@ -888,8 +903,8 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
     w[3 * (nc + q) + 2] = -__ldcg(xg + 3 * row + 2);
   }
   __syncthreads();
-  unsigned tk = 0;
-  next_take(nt, tk);  // the counter's round trip runs behind the second pass
+  NextRegs nx{};
+  next_take(nt, nx.tk);  // the counter's round trip runs behind the second pass
   trace_clock(F.trace, tb + 4);
   // ---- the -x_below part, plus the staged y_J part ----
   if (rs > 1) {
@@ -945,7 +960,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
     }
   }
   trace_clock(F.trace, tb + 5);
-  next_desc(F, nt, tk);  // the descriptor's round trip runs behind the publication
+  next_desc(F, nt, nx);  // the descriptor's round trip runs behind the publication
   bool issued = false;
   if (F.opts & 8) {  // next-tile prefetch (experiment): needs its own barrier after the last tile read
     asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next ticket's descriptor has landed
@@ -953,12 +968,12 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
     issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
   }
   return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, (long long)(tb + 6), issued, false,
-                  nt.on};
+                  nt.on, nx};
 }
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F, IO io) {
-  // smem: ztile[kTaskEntries] | f[max_nc*3] | part[256*3] | index staging (int32)
+  // smem: ztile | f[nc*3] (per task) ... index staging (int32) / part[256*3] at fwd_entries
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_item[2];
   __shared__ unsigned s_epoch;

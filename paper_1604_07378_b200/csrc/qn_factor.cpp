@@ -630,8 +630,10 @@ int factor_build_host(qn_factor* f, int64_t n, const int64_t* indptr, const int3
                  "factor: supernode too wide for the device solve tiles");
       // a task's shared memory holds its Z tile and f (nc x 3): wide supernodes get
       // smaller tiles so that tile + f stays within kFwdBudget (three CTAs per SM)
+      // (only where the forward sweep has its own kernel: the fused forward + backward kernel of
+      // factors without a dense top runs two CTAs per SM anyway)
       const int64_t room = fwd_budget - 3 * (int64_t)nc;
-      const int64_t te_s = room >= 4 * (int64_t)nc ? std::min(te_f, room) : te_f;
+      const int64_t te_s = (f->ktop > 0 || nbatch > 1) && room >= 4 * (int64_t)nc ? std::min(te_f, room) : te_f;
       const int32_t rg = std::min(8, pow2_floor(std::max<int64_t>(1, te_s / (32 * (int64_t)nc))));
       const int32_t rows = rg > 1 ? 32 * rg : (int32_t)std::max<int64_t>(1, std::min<int64_t>(32, te_s / nc));
       f->ffirst[s] = (int32_t)f->ftask.size();

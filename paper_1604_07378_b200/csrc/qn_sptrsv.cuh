@@ -24,6 +24,8 @@
 // (no float atomics): results are bitwise reproducible run to run.
 #pragma once
 
+#include <type_traits>
+
 #include "qn_common.cuh"
 #include "qn_factor.h"
 
@@ -333,6 +335,50 @@ __device__ __forceinline__ void col4_dots(const double* zt, int nr, const double
     for (int i = 0; i < 3; ++i) out[i] += __shfl_xor_sync(0xffffffffu, out[i], o);
 }
 
+// a += sum over list entries q in [q0, q1) of the update rows u[idx[q]] (3 values each), added in list
+// order (bitwise the sequential sum) with the loads of W entries in flight at a time: the sequential
+// loop paid one L2 round trip per entry, and these gathers sit on every task's dependent path
+template <int W, class Idx>
+__device__ __forceinline__ void gather_rows(const double* ub, const Idx* idx, long long q0, long long q1, double& a0,
+                                            double& a1, double& a2) {
+  long long q = q0;
+  for (; q + W <= q1; q += W) {
+    double v[W][3];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const double* uc = ub + 3 * (size_t)idx[q + j];
+      v[j][0] = __ldcg(uc);
+      v[j][1] = __ldcg(uc + 1);
+      v[j][2] = __ldcg(uc + 2);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      a0 += v[j][0];
+      a1 += v[j][1];
+      a2 += v[j][2];
+    }
+  }
+  const int rem = (int)(q1 - q);
+  if (W > 1 && rem > 0) {
+    double v[W - 1 > 0 ? W - 1 : 1][3];
+#pragma unroll
+    for (int j = 0; j < W - 1; ++j)
+      if (j < rem) {
+        const double* uc = ub + 3 * (size_t)idx[q + j];
+        v[j][0] = __ldcg(uc);
+        v[j][1] = __ldcg(uc + 1);
+        v[j][2] = __ldcg(uc + 2);
+      }
+#pragma unroll
+    for (int j = 0; j < W - 1; ++j)
+      if (j < rem) {
+        a0 += v[j][0];
+        a1 += v[j][1];
+        a2 += v[j][2];
+      }
+  }
+}
+
 // publish this task: all of the CTA's global writes are ordered before the flag
 // (CTA barrier, then one gpu-scope acq_rel fence — cumulative over the writes
 // the barrier ordered — and a relaxed flag store)
@@ -491,7 +537,7 @@ __device__ __forceinline__ void publish_done(const FactorView& F, const TaskDone
 // Without lookahead (few tasks per CTA: latency-bound, e.g. configs[1]) a CTA
 // never holds a ticket it is not working on, so an idle CTA can start every
 // ready task; the task reads its descriptor from global memory.
-template <class Body>
+template <bool kTiled, class Body>
 __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched, int* s_item, int nfi, int ntt,
                                             int total, DescSlot* s_desc, const unsigned& epoch, bool look, Body body) {
   if (look) {
@@ -528,7 +574,7 @@ __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched
       pre = dn.pre;
     }
   } else {
-    const bool late = F.tiled && !(F.opts & 128);  // the next ticket is taken during the task (NextTicket)
+    const bool late = kTiled && !(F.opts & 128);  // the next ticket is taken during the task (NextTicket)
     bool have = false;
     for (int it = 0;; ++it) {
       if (!have) {
@@ -547,7 +593,7 @@ __device__ __forceinline__ void ticket_loop(const FactorView& F, unsigned* sched
       const TaskDone dn = body(cur, dp, TileAhead{false, total, nullptr}, nt);
       __syncthreads();
       if (threadIdx.x == 0) publish_done(F, dn, epoch);
-      have = dn.took;
+      have = kTiled && dn.took;
       if (have) {  // the next ticket and its descriptor arrive behind the publication's fence
         next_store(nt, dn.nx);
         __syncthreads();
@@ -582,7 +628,7 @@ __device__ __forceinline__ void cta_exit(unsigned* sched, unsigned epoch, const 
 //   __device__ void store(int b, int row, const double (&v)[3]) const;
 // One forward task (row block of one supernode): stage, wait for the
 // children, gather their updates, v = Z f, publish.
-template <class IO>
+template <bool kTiled, class IO>
 __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
                                              int lane, int warp, uint64_t* mbar, unsigned& phase,
                                              const qn_fdesc* sdesc, const TileAhead& ahead, const NextTicket& nt,
@@ -611,7 +657,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   const int* sp_bot = sp_top + nc + 1;
   const int* si_top = sp_bot + nptr_bot;
   const int* si_bot = si_top + d.ntop;
-  if (F.tiled) {
+  if (kTiled) {
     // Large factors (throughput-bound): the warps split the roles so that the
     // task's independent round trips overlap — warp 1 issues the tile's bulk
     // copy (rows [lo, hi) x k [0, kmax) = zt[k * R + (r - lo)], one contiguous
@@ -665,12 +711,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   // ---- dependent gathers: children's updates on J (f) and on this task's bottom rows ----
   for (int p = threadIdx.x; p < nc; p += blockDim.x) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int q = sp_top[p]; q < sp_top[p + 1]; ++q) {
-      const double* uc = ub + 3 * (size_t)si_top[q];
-      a0 += __ldcg(uc);
-      a1 += __ldcg(uc + 1);
-      a2 += __ldcg(uc + 2);
-    }
+    gather_rows<4>(ub, si_top, sp_top[p], sp_top[p + 1], a0, a1, a2);
     f[3 * p + 0] -= a0;
     f[3 * p + 1] -= a1;
     f[3 * p + 2] -= a2;
@@ -679,14 +720,9 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   double e0 = 0.0, e1 = 0.0, e2 = 0.0;
   if (threadIdx.x < R && rr >= nc) {
     const int pr = rr - blo;
-    for (int q = sp_bot[pr]; q < sp_bot[pr + 1]; ++q) {
-      const double* uc = ub + 3 * (size_t)si_bot[q];
-      e0 += __ldcg(uc);
-      e1 += __ldcg(uc + 1);
-      e2 += __ldcg(uc + 2);
-    }
+    gather_rows<4>(ub, si_bot, sp_bot[pr], sp_bot[pr + 1], e0, e1, e2);
   }
-  if (F.tiled) {
+  if (kTiled) {
     mbar_wait(mbar, phase);
     phase ^= 1u;
   } else {
@@ -694,7 +730,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   }
   __syncthreads();
   NextRegs nx{};
-  next_take(nt, nx.tk);  // the counter's round trip runs behind the mat-vec
+  if (kTiled) next_take(nt, nx.tk);  // the counter's round trip runs behind the mat-vec
   trace_clock(F.trace, kTraceSlots * (size_t)item + 4);
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
   // a tile of R < 32 rows (wide supernodes) also splits each warp's k-slice
@@ -751,7 +787,7 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   __syncthreads();
   // the tile is consumed: the next ticket's copy streams in behind the epilogue and the publication
   const bool issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
-  next_desc(F, nt, nx);  // the descriptor's round trip runs behind the epilogue and the publication
+  if (kTiled) next_desc(F, nt, nx);  // the descriptor's round trip runs behind the epilogue and the publication
   if (threadIdx.x < R) {
     const int gg = threadIdx.x >> 5;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -775,12 +811,12 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   }
   trace_clock(F.trace, kTraceSlots * (size_t)item + 5);
   return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + tid, (long long)(kTraceSlots * (size_t)item + 6),
-                  issued, F.fuse_top != 0, nt.on, nx};
+                  issued, F.fuse_top != 0, kTiled && nt.on, nx};
 }
 
 // One backward task (column block of one supernode).  fused: forward and
 // backward share one persistent kernel, so y_J is waited for explicitly.
-template <class IO>
+template <bool kTiled, class IO>
 __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, int item, unsigned epoch, double* sm,
                                              int lane, int warp, bool fused, uint64_t* mbar, unsigned& phase,
                                              const qn_bdesc* sdesc, const TileAhead& ahead, const NextTicket& nt,
@@ -799,7 +835,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
   int* srow = (int*)(sdst + kBwdCols);
   const bool staged = nr - nc <= kStageIdx;
   // ---- stage: Z columns [k0, k1) (zeros above the diagonal), y_J, below-row ids ----
-  if (F.tiled) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
+  if (kTiled) {  // Z columns [k0, k1) x all rows, zeros above the diagonal: one contiguous block
     if (threadIdx.x == kIssueThread && !ahead.pre) {
       const int cnt = (k1 - k0) * nr;
       bulk_stage(zt, F.btile + (size_t)b * F.btile_n + d.zoff, (unsigned)((cnt + 1) / 2 * 2 * sizeof(double)),
@@ -820,7 +856,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
   if (fused)  // the forward of s may still be running: y_J must be complete
     wait_flag_range(F.flags + (size_t)b * (F.nftask + F.nbtask), d.fwd0, d.nfwd, epoch, F.sched);
   const double* yg = F.y + ((size_t)b * F.n + c0) * 3;
-  if (F.tiled && !fused) {
+  if (kTiled && !fused) {
     // y_J and the below-row ids as asynchronous copies: one round trip together with the
     // destinations.  (The 8-byte copies allocate in L1: only in the stand-alone backward
     // kernel, where y is never written; the fused kernel keeps the L2 loads below.)
@@ -841,7 +877,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
   }
   const size_t tb = kTraceSlots * ((size_t)F.nftask * F.nbatch + item);
   trace_mark(F.trace, tb + 1);
-  if (F.tiled) {
+  if (kTiled) {
     mbar_wait(mbar, phase);
     phase ^= 1u;
   } else {
@@ -904,7 +940,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
   }
   __syncthreads();
   NextRegs nx{};
-  next_take(nt, nx.tk);  // the counter's round trip runs behind the second pass
+  if (kTiled) next_take(nt, nx.tk);  // the counter's round trip runs behind the second pass
   trace_clock(F.trace, tb + 4);
   // ---- the -x_below part, plus the staged y_J part ----
   if (rs > 1) {
@@ -960,7 +996,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
     }
   }
   trace_clock(F.trace, tb + 5);
-  next_desc(F, nt, nx);  // the descriptor's round trip runs behind the publication
+  if (kTiled) next_desc(F, nt, nx);  // the descriptor's round trip runs behind the publication
   bool issued = false;
   if (F.opts & 8) {  // next-tile prefetch (experiment): needs its own barrier after the last tile read
     asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next ticket's descriptor has landed
@@ -968,7 +1004,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
     issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
   }
   return TaskDone{F.flags + (size_t)b * (F.nftask + F.nbtask) + F.nftask + tid, (long long)(tb + 6), issued, false,
-                  nt.on, nx};
+                  kTiled && nt.on, nx};
 }
 
 template <class IO>
@@ -986,10 +1022,18 @@ __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F,
   const int total = F.nftask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, s_item, total, 0, total, s_desc, s_epoch, F.lookahead != 0, [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
-    return fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc), ahead,
-                    nt, total, 0, total);
-  });
+  auto run = [&](auto tiled) {
+    constexpr bool kT = decltype(tiled)::value;
+    ticket_loop<kT>(F, sched, s_item, total, 0, total, s_desc, s_epoch, F.lookahead != 0,
+                    [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
+                      return fwd_task<kT>(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
+                                          reinterpret_cast<const qn_fdesc*>(dsc), ahead, nt, total, 0, total);
+                    });
+  };
+  if (F.tiled)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
   cta_exit(sched, s_epoch, F, 4);
 }
 
@@ -1008,10 +1052,18 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F
   const int total = F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, s_item, 0, 0, total, s_desc, s_epoch, F.lookahead && !(F.opts & 64), [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
-    return bwd_task(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase, reinterpret_cast<const qn_bdesc*>(dsc),
-                    ahead, nt, 0, 0, total);
-  });
+  auto run = [&](auto tiled) {
+    constexpr bool kT = decltype(tiled)::value;
+    ticket_loop<kT>(F, sched, s_item, 0, 0, total, s_desc, s_epoch, F.lookahead && !(F.opts & 64),
+                    [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
+                      return bwd_task<kT>(F, io, cur, s_epoch, sm, lane, warp, false, &s_mbar, phase,
+                                          reinterpret_cast<const qn_bdesc*>(dsc), ahead, nt, 0, 0, total);
+                    });
+  };
+  if (F.tiled)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
   cta_exit(sched, s_epoch, F, 5);
 }
 
@@ -1065,12 +1117,7 @@ __device__ __forceinline__ void top_tile(const FactorView& F, const IO& io, int 
       double v[3];
       io.rhs(b, F.tcols[k], v);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int q = F.tg_ptr[k]; q < F.tg_ptr[k + 1]; ++q) {
-        const double* uc = ub + 3 * (size_t)F.tg_idx[q];
-        a0 += __ldcg(uc);
-        a1 += __ldcg(uc + 1);
-        a2 += __ldcg(uc + 2);
-      }
+      gather_rows<4>(ub, F.tg_idx, F.tg_ptr[k], F.tg_ptr[k + 1], a0, a1, a2);
       gd[0] = v[0] - a0;
       gd[1] = v[1] - a1;
       gd[2] = v[2] - a2;
@@ -1207,19 +1254,28 @@ __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, I
   const int total = nfi + ntt + F.nbtask * F.nbatch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ DescSlot s_desc[2];
-  ticket_loop(F, sched, s_item, nfi, ntt, total, s_desc, s_epoch, F.lookahead != 0, [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
-    if (cur < nfi)
-      return fwd_task(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase, reinterpret_cast<const qn_fdesc*>(dsc),
-                      ahead, nt, nfi, ntt, total);
-    if (cur < nfi + ntt) {
-      if (io.active(0))  // same predicate as the forward tasks that the tile waits for
-        top_tile(F, io, cur - nfi, 0, sm, sm + kTopTileEntries, sm + kTopTileEntries + 3 * kTopTile, s_last, &s_mbar,
-                 phase, true);
-      return no_task();
-    }
-    return bwd_task(F, io, cur - nfi - ntt, s_epoch, sm, lane, warp, true, &s_mbar, phase,
-                    reinterpret_cast<const qn_bdesc*>(dsc), ahead, nt, nfi, ntt, total);
-  });
+  auto run = [&](auto tiled) {
+    constexpr bool kT = decltype(tiled)::value;
+    ticket_loop<kT>(
+        F, sched, s_item, nfi, ntt, total, s_desc, s_epoch, F.lookahead != 0,
+        [&](int cur, const unsigned char* dsc, const TileAhead& ahead, const NextTicket& nt) {
+          if (cur < nfi)
+            return fwd_task<kT>(F, io, cur, s_epoch, sm, lane, warp, &s_mbar, phase,
+                                reinterpret_cast<const qn_fdesc*>(dsc), ahead, nt, nfi, ntt, total);
+          if (cur < nfi + ntt) {
+            if (io.active(0))  // same predicate as the forward tasks that the tile waits for
+              top_tile(F, io, cur - nfi, 0, sm, sm + kTopTileEntries, sm + kTopTileEntries + 3 * kTopTile, s_last,
+                       &s_mbar, phase, true);
+            return no_task();
+          }
+          return bwd_task<kT>(F, io, cur - nfi - ntt, s_epoch, sm, lane, warp, true, &s_mbar, phase,
+                              reinterpret_cast<const qn_bdesc*>(dsc), ahead, nt, nfi, ntt, total);
+        });
+  };
+  if (F.tiled)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
   cta_exit(sched, s_epoch, F, 5);
 }
 
@@ -1265,12 +1321,7 @@ __global__ void __launch_bounds__(kBatchThreads, 8) sptrsv_batch(FactorView F, I
       const double* Z = vb + F.sup_val_ptr[s];
       for (int p = lane; p < nc; p += 32) {  // f = b_J - children updates
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        for (int64_t q = F.cptr[R0 + p]; q < F.cptr[R0 + p + 1]; ++q) {
-          const double* uc = ub + 3 * (size_t)F.cidx[q];
-          a0 += __ldcg(uc);
-          a1 += __ldcg(uc + 1);
-          a2 += __ldcg(uc + 2);
-        }
+        gather_rows<1>(ub, F.cidx, F.cptr[R0 + p], F.cptr[R0 + p + 1], a0, a1, a2);
         fw[3 * p + 0] = yx[3 * (c0 + p) + 0] - a0;
         fw[3 * p + 1] = yx[3 * (c0 + p) + 1] - a1;
         fw[3 * p + 2] = yx[3 * (c0 + p) + 2] - a2;
@@ -1280,12 +1331,7 @@ __global__ void __launch_bounds__(kBatchThreads, 8) sptrsv_batch(FactorView F, I
         const int kmax = r < nc ? r + 1 : nc;
         double e0 = 0.0, e1 = 0.0, e2 = 0.0;
         if (r >= nc)  // children's updates on this bottom row (independent of the FMAs)
-          for (int64_t q = F.cptr[R0 + r]; q < F.cptr[R0 + r + 1]; ++q) {
-            const double* uc = ub + 3 * (size_t)F.cidx[q];
-            e0 += __ldcg(uc);
-            e1 += __ldcg(uc + 1);
-            e2 += __ldcg(uc + 2);
-          }
+          gather_rows<1>(ub, F.cidx, F.cptr[R0 + r], F.cptr[R0 + r + 1], e0, e1, e2);
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
         int k = 0;
         for (; k + 8 <= kmax; k += 8) {

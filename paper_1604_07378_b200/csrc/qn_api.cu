@@ -1229,7 +1229,20 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
       S->graph = nullptr;
     }
     if (!S->exec) {
-      if ((rc = build_graph(S))) return rc;
+      if (const char* e = std::getenv("QN_PDL")) S->pdl = std::atoi(e) != 0;  // experiment knob
+      if (S->factor) S->factor->pdl = S->pdl ? 1 : 0;
+      rc = build_graph(S);
+      if (rc && S->pdl) {
+        // programmatic edges refused by this driver (e.g. inside the conditional body): abandon the
+        // capture and rebuild the frame graph with fully serialised launches
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(st, &dead);
+        cudaGetLastError();
+        S->pdl = false;
+        if (S->factor) S->factor->pdl = 0;
+        rc = build_graph(S);
+      }
+      if (rc) return rc;
       S->graph_m_bound = mb;
       S->graph_init = c.lbfgs_init;
     }

@@ -57,6 +57,39 @@ constexpr int kSMs = 148;
 
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Programmatic dependent launch (PDL) between consecutive kernels of a frame
+// (experiment, off by default: QN_PDL=1): a kernel launched through launch_k
+// with pdl = true may be scheduled while its predecessor in the stream (or
+// frame graph) drains, and pdl_entry(), the first statement of such kernels,
+// blocks until the predecessor grid has completed and its writes are visible.
+// Nothing runs before pdl_entry(), so results are those of the serialised
+// launches.  Measured on the B200: back-to-back stream launches gain (c3
+// stand-alone solve 215 -> 208 us) but inside the frame graph the kernel
+// boundaries are already short — neutral with the implicit trigger (c3 2.73 k
+// it/s either way), and 2-8 % SLOWER with an early griddepcontrol.launch_dependents
+// (the dependents' resident CTAs slow the predecessor's tail).  Launched
+// without the attribute, pdl_entry() returns at once.
+__device__ __forceinline__ void pdl_entry() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
 // ---- device helpers ----------------------------------------------------------
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {

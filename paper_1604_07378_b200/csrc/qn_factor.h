@@ -131,6 +131,7 @@ struct qn_factor {
   int32_t batch_max_nc = 0, batch_zmax = 0;  // batched mode: widest supernode, largest Z block (entries)
   bool on_device = false;
   int32_t lookahead = 0;          // persistent solve ticket lookahead (prepare_solve_kernels)
+  int32_t pdl = 0;                // solve kernels launched with programmatic stream serialization (set by the system)
   int32_t many_tasks = 0;         // throughput-bound factor: many tasks per CTA (rhs formed once by k_solve_rhs)
   int32_t solve_opts = 0;         // QN_SOLVE_OPTS experiment knob (see FactorView::opts)
 };

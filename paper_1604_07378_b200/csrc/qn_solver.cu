@@ -177,6 +177,7 @@ __device__ __forceinline__ void tl_entry(const SysView& v, int kid) {
 // dot-product accumulators scales with it; the host picks the smallest that fits).
 template <int M>
 __global__ void __launch_bounds__(kVTB) k_grad(SysView v) {
+  pdl_entry();
   constexpr int NG = 5 + 2 * M;
   tl_entry(v, 0);
   // instances in reverse launch order: the per-tet pass just wrote the last
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(256) k_rest_apply(SysView v) {
 // forming q' = -g - sum zeta t row by row (the wide supernodes' row tasks all
 // need the same nc rows).  Same rounding as SolverIO::rhs.
 __global__ void __launch_bounds__(kVTB) k_solve_rhs(SysView v) {
+  pdl_entry();
   const int b = blockIdx.y;
   const InstCtl* c = v.ctl + b;
   if (c->phase != PH_DIR) return;
@@ -454,6 +456,7 @@ int launch_solve_timing(qn_system* S, cudaStream_t st) { return launch_solve(S->
 // <t_i, r0> and the eta recursion (solvers.py:147-150)
 template <int M>
 __global__ void __launch_bounds__(kVTB) k_eta(SysView v) {
+  pdl_entry();
   tl_entry(v, 1);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -499,6 +502,7 @@ __device__ void eta_finalize(InstCtl& c, const double* tot, int np) {
 
 // direction, trial point, inertia / slope partials
 __global__ void __launch_bounds__(kVTB) k_vec(SysView v) {
+  pdl_entry();
   tl_entry(v, 2);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -767,6 +771,7 @@ int launch_col(qn_system* S, int which, cudaStream_t st) {
 // per-tet pass at the trial point: energy partials + corner forces
 template <bool kSm, bool kAniso, bool kF32 = false>
 __global__ void __launch_bounds__(kTT, kTetBlocksPerSm) k_tet(SysView v) {
+  pdl_entry();
   tl_entry(v, 3);
   const int b = blockIdx.y;
   const InstCtl* cc = v.ctl + b;
@@ -1527,9 +1532,9 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
   const dim3 gv(v.nblk_v, v.n_inst);
   if (int rc = launch_col(S, 0, st)) return rc;
   if (S->h_cfg.m <= 5) {  // default window: smaller register footprint
-    k_grad<5><<<gv, v.vt, 0, st>>>(v);
+    launch_k(k_grad<5>, gv, dim3(v.vt), 0, st, S->pdl, v);
   } else {
-    k_grad<kMaxM><<<gv, v.vt, 0, st>>>(v);
+    launch_k(k_grad<kMaxM>, gv, dim3(v.vt), 0, st, S->pdl, v);
   }
   QN_CHECK_LAUNCH();
   if (v.pcg) {
@@ -1560,7 +1565,7 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
     SolverIO io{v};
     return launch_solve(S->factor, io, st);
   }
-  k_solve_rhs<<<dim3(div_up(3 * (int64_t)v.n_free, kVTB), v.n_inst), kVTB, 0, st>>>(v);
+  launch_k(k_solve_rhs, dim3(div_up(3 * (int64_t)v.n_free, kVTB), v.n_inst), dim3(kVTB), 0, st, S->pdl, v);
   QN_CHECK_LAUNCH();
   FactorRhsIO io{{v}};
   return launch_solve(S->factor, io, st);
@@ -1588,28 +1593,28 @@ int launch_body_post(qn_system* S, cudaStream_t st) {
     QN_CHECK_LAUNCH();
   }
   if (small_m) {
-    k_eta<5><<<gv, v.vt, 0, st>>>(v);
+    launch_k(k_eta<5>, gv, dim3(v.vt), 0, st, S->pdl, v);
   } else {
-    k_eta<kMaxM><<<gv, v.vt, 0, st>>>(v);
+    launch_k(k_eta<kMaxM>, gv, dim3(v.vt), 0, st, S->pdl, v);
   }
   QN_CHECK_LAUNCH();
-  k_vec<<<gv, v.vt, 0, st>>>(v);
+  launch_k(k_vec, gv, dim3(v.vt), 0, st, S->pdl, v);
   QN_CHECK_LAUNCH();
   if (int rc = launch_col(S, 1, st)) return rc;
   if (v.n_mat <= kMatSmem) {
     if (v.f32) {
-      k_tet<true, false, true><<<gt, kTT, 0, st>>>(v);
+      launch_k(k_tet<true, false, true>, gt, dim3(kTT), 0, st, S->pdl, v);
     } else if (v.aniso) {
-      k_tet<true, true><<<gt, kTT, 0, st>>>(v);
+      launch_k(k_tet<true, true>, gt, dim3(kTT), 0, st, S->pdl, v);
     } else {
-      k_tet<true, false><<<gt, kTT, 0, st>>>(v);
+      launch_k(k_tet<true, false>, gt, dim3(kTT), 0, st, S->pdl, v);
     }
   } else if (v.f32) {
-    k_tet<false, false, true><<<gt, kTT, 0, st>>>(v);
+    launch_k(k_tet<false, false, true>, gt, dim3(kTT), 0, st, S->pdl, v);
   } else if (v.aniso) {
-    k_tet<false, true><<<gt, kTT, 0, st>>>(v);
+    launch_k(k_tet<false, true>, gt, dim3(kTT), 0, st, S->pdl, v);
   } else {
-    k_tet<false, false><<<gt, kTT, 0, st>>>(v);
+    launch_k(k_tet<false, false>, gt, dim3(kTT), 0, st, S->pdl, v);
   }
   QN_CHECK_LAUNCH();
   return QN_OK;

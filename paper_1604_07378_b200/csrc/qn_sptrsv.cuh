@@ -1009,6 +1009,7 @@ __device__ __forceinline__ TaskDone bwd_task(const FactorView& F, const IO& io, 
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F, IO io) {
+  pdl_entry();
   // smem: ztile | f[nc*3] (per task) ... index staging (int32) / part[256*3] at fwd_entries
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_item[2];
@@ -1039,6 +1040,7 @@ __global__ void __launch_bounds__(kSolveThreads, 3) sptrsv_forward(FactorView F,
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_backward(FactorView F, IO io) {
+  pdl_entry();
   // smem: ztile[bwd_entries] | w[max_rows*3] = [y_J; -x_below] | pre[kBwdCols*3] | dest[kBwdCols] | row staging
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_item[2];
@@ -1218,6 +1220,7 @@ __device__ __forceinline__ void top_tile(const FactorView& F, const IO& io, int 
 
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F, IO io) {
+  pdl_entry();
   __shared__ __align__(16) double st[kTopTileEntries];
   __shared__ double gI[kTopTile * 3], gJ[kTopTile * 3];
   __shared__ int s_last[2];
@@ -1239,6 +1242,7 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
 // of x_T), so the waits cannot deadlock.
 template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 2) sptrsv_fused(FactorView F, IO io) {
+  pdl_entry();
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_item[2];
   __shared__ unsigned s_epoch;
@@ -1294,6 +1298,7 @@ constexpr int kBatchCols = 4;  // backward: columns per pass (12 independent cha
 
 template <class IO>
 __global__ void __launch_bounds__(kBatchThreads, 8) sptrsv_batch(FactorView F, IO io) {
+  pdl_entry();
   extern __shared__ double sm[];  // yx[n*3] | fw[kBatchWarps][max_nc*3]
   const int b = blockIdx.x;
   if (!io.active(b)) return;
@@ -1449,7 +1454,9 @@ template <class IO>
 int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   const FactorView v = factor_view(f);
   if (f->batch_smem > 0) {  // batched small systems: one CTA per instance
-    sptrsv_batch<IO><<<(int)f->nbatch, kBatchThreads, f->batch_smem, stream>>>(v, io);
+    cudaError_t e = launch_k(sptrsv_batch<IO>, dim3((unsigned)f->nbatch), dim3(kBatchThreads), (size_t)f->batch_smem, stream,
+                             f->pdl != 0, v, io);
+    (void)e;
     QN_CHECK_LAUNCH();
     return QN_OK;
   }
@@ -1457,22 +1464,29 @@ int launch_solve(qn_factor* f, const IO& io, cudaStream_t stream) {
   if (f->fused && (f->ktop == 0 || v.fuse_top)) {
     const int ntt = v.fuse_top ? f->tnt * (f->tnt + 1) / 2 : 0;
     if (nf + nb + ntt > 0) {
-      sptrsv_fused<IO><<<std::min(nf + nb + ntt, f->grid_fused), kSolveThreads, f->smem_fused, stream>>>(v, io);
+      cudaError_t e = launch_k(sptrsv_fused<IO>, dim3((unsigned)std::min(nf + nb + ntt, f->grid_fused)), dim3(kSolveThreads),
+                               (size_t)f->smem_fused, stream, f->pdl != 0, v, io);
+      (void)e;
       QN_CHECK_LAUNCH();
     }
     return QN_OK;
   }
   if (nf > 0) {
-    sptrsv_forward<IO><<<std::min(nf, f->grid_f), kSolveThreads, f->smem_f, stream>>>(v, io);
+    cudaError_t e = launch_k(sptrsv_forward<IO>, dim3((unsigned)std::min(nf, f->grid_f)), dim3(kSolveThreads),
+                             (size_t)f->smem_f, stream, f->pdl != 0, v, io);
+    (void)e;
     QN_CHECK_LAUNCH();
   }
   if (f->ktop > 0) {
     const dim3 ga((unsigned)(f->tnt * (f->tnt + 1) / 2), (unsigned)f->nbatch);
-    sptrsv_top_sym<IO><<<ga, kSolveThreads, 0, stream>>>(v, io);
+    cudaError_t e = launch_k(sptrsv_top_sym<IO>, ga, dim3(kSolveThreads), (size_t)0, stream, f->pdl != 0, v, io);
+    (void)e;
     QN_CHECK_LAUNCH();
   }
   if (nb > 0) {
-    sptrsv_backward<IO><<<std::min(nb, f->grid_b), kSolveThreads, f->smem_b, stream>>>(v, io);
+    cudaError_t e = launch_k(sptrsv_backward<IO>, dim3((unsigned)std::min(nb, f->grid_b)), dim3(kSolveThreads),
+                             (size_t)f->smem_b, stream, f->pdl != 0, v, io);
+    (void)e;
     QN_CHECK_LAUNCH();
   }
   return QN_OK;

@@ -211,6 +211,7 @@ struct qn_system {
   size_t h_stage_bytes = 0;
   // graph
   bool use_graph = true;
+  bool pdl = false;  // programmatic dependent launch between the body kernels (QN_PDL=1; measured neutral inside the frame graph)
   int32_t fault = 0;  // qn_system_set_fault
   int graph_m_bound = 0;  // history bound the captured graph's kernels are specialised on
   int graph_init = 0;     // lbfgs_init the captured graph's direction step was built for

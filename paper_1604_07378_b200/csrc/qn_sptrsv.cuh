@@ -155,7 +155,8 @@ inline FactorView factor_view(const qn_factor* f) {
 constexpr int kSolveThreads = 256;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kStageIdx = 2048;  // int32 index slots staged in shared memory per task
-constexpr int kTraceSlots = 7;   // globaltimer ticket, staged, ready; clock64 ready, data staged, computed, published
+constexpr int kTraceSlots = 9;   // globaltimer ticket, staged, ready; clock64 ready, data staged, computed, published,
+                                 // (forward) own mat-vec done, past the mat-vec barrier
 constexpr int kBwdCols = (int)kBwdTaskCols;  // max columns of a backward task
 constexpr int kIssueThread = 32;  // warp 1 issues tile copies / takes tickets; warp 0 polls and publishes meanwhile
 
@@ -735,26 +736,58 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   // ---- rows of v = Z f from shared memory: warp -> (row group g, k-slice j);
   // a tile of R < 32 rows (wide supernodes) also splits each warp's k-slice
   // over L = 32 / R lane groups (lane = sub R + row), so every lane works ----
-  const int ks = kSolveWarps / rg;
-  const int g = warp / ks, j = warp % ks;
-  const int per = (kmax + ks - 1) / ks;
+  const int lg = __ffs(rg) - 1;  // rg is a power of two: shifts instead of integer divisions
+  const int ks = kSolveWarps >> lg;
+  const int g = warp >> (3 - lg), j = warp & (ks - 1);
+  static_assert(kSolveWarps == 8, "warp -> (row group, k-slice) shifts assume 8 warps");
+  // k-slices start at even k, so the f values of two consecutive k (6 doubles) are three aligned
+  // 16-byte broadcast loads
+  const int per = (((kmax + ks - 1) >> (3 - lg)) + 1) & ~1;
   const int kb = j * per, ke = min(kmax, kb + per);
   const int L = (R < 32 && !(F.opts & 1)) ? 32 / R : 1;  // rg == 1 whenever R < 32
   const int sub = L > 1 ? lane / R : 0;
   const int rl = L > 1 ? lane - sub * R : 32 * g + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (g < rg && rl < R && sub < L) {
-    double b0 = 0.0, b1 = 0.0, b2 = 0.0;  // two chains per coordinate (even / odd steps)
-    int k = kb + sub;
-#pragma unroll 4
-    for (; k + L < ke; k += 2 * L) {
-      const double l = zt[k * R + rl], m = zt[(k + L) * R + rl];
-      a0 = fma(l, f[3 * k + 0], a0);
-      a1 = fma(l, f[3 * k + 1], a1);
-      a2 = fma(l, f[3 * k + 2], a2);
-      b0 = fma(m, f[3 * (k + L) + 0], b0);
-      b1 = fma(m, f[3 * (k + L) + 1], b1);
-      b2 = fma(m, f[3 * (k + L) + 2], b2);
+    // four independent chains per coordinate (k mod 4 within the lane group's pairs): the FP64 FMA
+    // latency, not its throughput, bounds a row's dot product
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    int k = kb + 2 * sub;  // lane group `sub` takes the k pairs sub, sub + L, ...
+#pragma unroll 2
+    for (; k + 2 * L + 1 < ke; k += 4 * L) {
+      const int k2 = k + 2 * L;
+      const double l = zt[k * R + rl], m = zt[(k + 1) * R + rl];
+      const double n = zt[k2 * R + rl], o = zt[(k2 + 1) * R + rl];
+      const double2 f01 = *reinterpret_cast<const double2*>(f + 3 * k);
+      const double2 f23 = *reinterpret_cast<const double2*>(f + 3 * k + 2);
+      const double2 f45 = *reinterpret_cast<const double2*>(f + 3 * k + 4);
+      const double2 g01 = *reinterpret_cast<const double2*>(f + 3 * k2);
+      const double2 g23 = *reinterpret_cast<const double2*>(f + 3 * k2 + 2);
+      const double2 g45 = *reinterpret_cast<const double2*>(f + 3 * k2 + 4);
+      a0 = fma(l, f01.x, a0);
+      a1 = fma(l, f01.y, a1);
+      a2 = fma(l, f23.x, a2);
+      b0 = fma(m, f23.y, b0);
+      b1 = fma(m, f45.x, b1);
+      b2 = fma(m, f45.y, b2);
+      c0 = fma(n, g01.x, c0);
+      c1 = fma(n, g01.y, c1);
+      c2 = fma(n, g23.x, c2);
+      d0 = fma(o, g23.y, d0);
+      d1 = fma(o, g45.x, d1);
+      d2 = fma(o, g45.y, d2);
+    }
+    for (; k + 1 < ke; k += 2 * L) {
+      const double l = zt[k * R + rl], m = zt[(k + 1) * R + rl];
+      const double2 f01 = *reinterpret_cast<const double2*>(f + 3 * k);
+      const double2 f23 = *reinterpret_cast<const double2*>(f + 3 * k + 2);
+      const double2 f45 = *reinterpret_cast<const double2*>(f + 3 * k + 4);
+      a0 = fma(l, f01.x, a0);
+      a1 = fma(l, f01.y, a1);
+      a2 = fma(l, f23.x, a2);
+      b0 = fma(m, f23.y, b0);
+      b1 = fma(m, f45.x, b1);
+      b2 = fma(m, f45.y, b2);
     }
     if (k < ke) {
       const double l = zt[k * R + rl];
@@ -762,6 +795,12 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
       a1 = fma(l, f[3 * k + 1], a1);
       a2 = fma(l, f[3 * k + 2], a2);
     }
+    a0 += c0;
+    a1 += c1;
+    a2 += c2;
+    b0 += d0;
+    b1 += d1;
+    b2 += d2;
     a0 += b0;
     a1 += b1;
     a2 += b2;
@@ -783,8 +822,10 @@ __device__ __forceinline__ TaskDone fwd_task(const FactorView& F, const IO& io, 
   part[3 * threadIdx.x + 0] = a0;
   part[3 * threadIdx.x + 1] = a1;
   part[3 * threadIdx.x + 2] = a2;
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 7);
   asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next ticket's descriptor has landed
   __syncthreads();
+  trace_clock(F.trace, kTraceSlots * (size_t)item + 8);
   // the tile is consumed: the next ticket's copy streams in behind the epilogue and the publication
   const bool issued = tile_issue(F, io, ahead.nxt, nfi, ntt, total, ahead.dsc, zt, mbar);
   if (kTiled) next_desc(F, nt, nx);  // the descriptor's round trip runs behind the epilogue and the publication

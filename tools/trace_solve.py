@@ -17,11 +17,12 @@ import paper_1604_07378_b200 as Q  # noqa: E402
 from paper_1604_07378_b200 import _lib  # noqa: E402
 from paper_1604_07378_b200.solvers import ResidentRun, SolverConfig  # noqa: E402
 
-SLOTS = 7
+SLOTS = 9
 GHZ = 1.965  # SM clock under load (bench clocks line)
 
 
 def report(name, st7, t):
+    st7 = st7[:, :7]
     st = np.zeros((st7.shape[0], 6), dtype=np.int64)
     st[:, 0], st[:, 1], st[:, 2] = st7[:, 0], st7[:, 1], st7[:, 2]
     for j in range(3):  # phases after 'ready' from the SM cycle counter

@@ -1172,22 +1172,51 @@ __device__ __forceinline__ void top_tile(const FactorView& F, const IO& io, int 
   phase ^= 1u;
   __syncthreads();
   const int i = threadIdx.x % T, q = threadIdx.x / T;
+  // Row i of S_IJ g_J over the columns of quarter q and, off the diagonal, column i of S_IJ against
+  // g_I over the rows of quarter q, two entries per step: the g values of two consecutive rows
+  // (6 doubles) are three aligned 16-byte broadcast loads, and every product keeps two FMA chains per
+  // coordinate (the kernel is bound by shared-memory wavefronts and by the FP64 FMA latency).
   double r0 = 0.0, r1 = 0.0, r2 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
-#pragma unroll 8
-  for (int j = q * (T / NQ); j < (q + 1) * (T / NQ); ++j) {  // row i of S_IJ g_J, columns of quarter q
-    const double sv = st[i + j * LD];
-    r0 = fma(sv, gJ[3 * j + 0], r0);
-    r1 = fma(sv, gJ[3 * j + 1], r1);
-    r2 = fma(sv, gJ[3 * j + 2], r2);
-  }
-  if (I != J) {
-#pragma unroll 8
-    for (int r = q * (T / NQ); r < (q + 1) * (T / NQ); ++r) {  // column i of S_IJ against g_I, rows of quarter q
-      const double sv = st[r + i * LD];
-      c0 = fma(sv, gI[3 * r + 0], c0);
-      c1 = fma(sv, gI[3 * r + 1], c1);
-      c2 = fma(sv, gI[3 * r + 2], c2);
+  {
+    double r3 = 0.0, r4 = 0.0, r5 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0;
+    const int j0 = q * (T / NQ);
+    static_assert((kTopTile / (kSolveThreads / kTopTile)) % 2 == 0, "quarters hold an even number of columns");
+#pragma unroll
+    for (int t = 0; t < T / NQ; t += 2) {
+      const int j = j0 + t;
+      const double s0 = st[i + j * LD], s1 = st[i + (j + 1) * LD];
+      const double2 a01 = *reinterpret_cast<const double2*>(gJ + 3 * j);
+      const double2 a23 = *reinterpret_cast<const double2*>(gJ + 3 * j + 2);
+      const double2 a45 = *reinterpret_cast<const double2*>(gJ + 3 * j + 4);
+      r0 = fma(s0, a01.x, r0);
+      r1 = fma(s0, a01.y, r1);
+      r2 = fma(s0, a23.x, r2);
+      r3 = fma(s1, a23.y, r3);
+      r4 = fma(s1, a45.x, r4);
+      r5 = fma(s1, a45.y, r5);
     }
+    if (I != J) {
+#pragma unroll
+      for (int t = 0; t < T / NQ; t += 2) {
+        const int r = j0 + t;
+        const double u0 = st[r + i * LD], u1 = st[r + 1 + i * LD];
+        const double2 b01 = *reinterpret_cast<const double2*>(gI + 3 * r);
+        const double2 b23 = *reinterpret_cast<const double2*>(gI + 3 * r + 2);
+        const double2 b45 = *reinterpret_cast<const double2*>(gI + 3 * r + 4);
+        c0 = fma(u0, b01.x, c0);
+        c1 = fma(u0, b01.y, c1);
+        c2 = fma(u0, b23.x, c2);
+        c3 = fma(u1, b23.y, c3);
+        c4 = fma(u1, b45.x, c4);
+        c5 = fma(u1, b45.y, c5);
+      }
+    }
+    r0 += r3;
+    r1 += r4;
+    r2 += r5;
+    c0 += c3;
+    c1 += c4;
+    c2 += c5;
   }
   __syncthreads();  // the tile is consumed: its buffer holds the partial products now
   red[(0 * NQ + q) * T * 3 + 3 * i + 0] = r0;
@@ -1263,7 +1292,7 @@ template <class IO>
 __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F, IO io) {
   pdl_entry();
   __shared__ __align__(16) double st[kTopTileEntries];
-  __shared__ double gI[kTopTile * 3], gJ[kTopTile * 3];
+  __shared__ __align__(16) double gI[kTopTile * 3], gJ[kTopTile * 3];
   __shared__ int s_last[2];
   __shared__ uint64_t s_mbar;
   const int b = blockIdx.y;

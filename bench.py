@@ -193,7 +193,7 @@ def frame_timeline(system, run, stream):
     import ctypes as C
     from paper_1604_07378_b200 import _lib
     lib = _lib.load()
-    passes, kernels = 512, 6
+    passes, kernels = 512, 7  # kTimelinePasses, kTimelineKernels (csrc/qn_common.cuh)
     buf = np.zeros(passes * kernels * 2, dtype=np.uint64)
     try:
         _lib.check(lib.qn_system_set_timeline(system._h, 1))
@@ -212,6 +212,9 @@ def frame_timeline(system, run, stream):
             "grad": mean([t[p, 0, 1] - t[p, 0, 0] for p in full]),
             "solve": mean([t[p, 1, 0] - t[p, 0, 1] for p in full]),
             "tet": mean([t[p, 3, 1] - t[p, 3, 0] for p in range(npass)]),
+            "solve_forward": mean([t[p, 4, 1] - t[p, 4, 0] for p in full if t[p, 4, 0] and t[p, 4, 1]]),
+            "solve_top": mean([t[p, 6, 1] - t[p, 6, 0] for p in full if t[p, 6, 0] and t[p, 6, 1]]),
+            "solve_backward": mean([t[p, 5, 1] - t[p, 5, 0] for p in full if t[p, 5, 0] and t[p, 5, 1]]),
             "frame": (t[npass - 1, 3, 1] - (t[0, 0, 0] or t[0, 3, 0])) / 1000.0}
 
 
@@ -395,15 +398,23 @@ def run_ours(args, world, rank, local):
         if amg:
             vc_ms = system.time_kernel("vcycle", reps=10, stream=sptr)
             rows, nA, nP, nR = amg["rows"], amg["nnz_A"], amg["nnz_P"], amg["nnz_R"]
-            # per level l < coarsest: A twice (residual with the fused pre-smoothing, post-smoothing),
-            # P and R once, fp32 values + int32 columns = 8 B per entry; level vectors (n x 3 fp64)
-            # b, x, r, t, and the coarse correction: ~8 passes of 24 B per row; coarsest: dense
-            # fp64 inverse (nc^2) + its vectors
-            vb = sum(8.0 * (2 * nA[l] + nP[l] + nR[l]) + 8 * 24.0 * rows[l] for l in range(len(rows) - 1))
-            vb += 8.0 * rows[-1] ** 2 + 2 * 24.0 * rows[-1]
+            # per level l < coarsest: A twice (residual, post-smoothing), P and R once, fp32 values +
+            # int32 columns = 8 B per entry; the cycle's vectors are fp32 rows of 16 B (level 0 reads
+            # the fp64 CG residual and writes z in fp64, 24 B per row): residual (x gathered, b read,
+            # r written), restriction (r gathered; b, x written and dinv read on the coarse level),
+            # prolongation (coarse t gathered, x read + written), post-smoothing (x gathered, b, dinv
+            # read, t written), level-0 pre-smoothing (b, dinv read, x written); coarsest: dense fp32
+            # inverse (nc^2) + its vectors
+            vb = 0.0
+            for l in range(len(rows) - 1):
+                bt = 24.0 if l == 0 else 16.0
+                vb += 8.0 * (2 * nA[l] + nP[l] + nR[l])
+                vb += rows[l] * ((16 + bt + 16) + 16 + 32 + (16 + bt + 8 + bt)) + rows[l + 1] * (32 + 8 + 16)
+            vb += rows[0] * (24 + 8 + 16)
+            vb += 4.0 * rows[-1] ** 2 + 32.0 * rows[-1]
             vcyc = {"ms": vc_ms, "algorithmic_bytes": vb, "GBps": vb / vc_ms / 1e6,
-                    "share": vc_ms * cg_per_step / per_frame, "kernels": "k_amg_residual/restrict/coarse/"
-                    "prolong/smooth over the levels", "levels": len(rows)}
+                    "share": vc_ms * cg_per_step / per_frame, "kernels": "k_amg_presmooth, k_amg_residual/"
+                    "restrict/coarse/prolong/smooth over the levels", "levels": len(rows)}
     cands = {"tet": (share_tet, tet_ms, tet_bytes), "solve": (share_solve, solve_ms, solve_bytes)}
     if vcyc:
         cands["vcycle"] = (vcyc["share"], vcyc["ms"], vcyc["algorithmic_bytes"])
@@ -414,7 +425,7 @@ def run_ours(args, world, rank, local):
                   ("sptrsv_forward + top (symmetric S^-1) + backward" if info.get("dense_top") else
                    "sptrsv_forward+backward") if "nnz_l" in info else "k_pcg_spmv (CG SpMV, SELL-32 fp64)")
     names = {"tet": "k_tet (per-tet F/SVD/VL/PK1)", "solve": solve_name,
-             "vcycle": "AMG V(1,1) cycle (k_amg_residual/restrict/coarse/prolong/smooth, all levels)"}
+             "vcycle": "AMG V(1,1) cycle (k_amg_presmooth/residual/restrict/coarse/prolong/smooth, all levels)"}
     roof = {"bound": "hbm", "kernel": names[dom],
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
             "traffic": ncu_traffic(args.config, dom), "algorithmic_bytes": dbytes, "launch_ms": dms,

@@ -750,14 +750,14 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
               (rc = sell_upload(S, L.R.n, L.R.m, L.R.ptr.data(), L.R.col.data(), L.R.val.data(), &D.R)))
             return fail(rc);
         }
-        const size_t lv3 = (size_t)L.A.n * 3;
+        const size_t lvn = (size_t)L.A.n;
         if (l == 0) {
           D.b = v.pr;  // the CG residual
           D.t = v.pz;  // z = B r
-        } else if ((rc = sys_alloc(S, &D.b, lv3)) || (rc = sys_alloc(S, &D.t, lv3))) {
+        } else if ((rc = sys_alloc(S, &D.bf, lvn)) || (rc = sys_alloc(S, &D.tf, lvn))) {
           return fail(rc);
         }
-        if ((rc = sys_alloc(S, &D.x, lv3)) || (rc = sys_alloc(S, &D.r, lv3))) return fail(rc);
+        if ((rc = sys_alloc(S, &D.xf, lvn)) || (rc = sys_alloc(S, &D.rf, lvn))) return fail(rc);
         const int64_t nsl_l = (L.A.n + 31) / 32;
         D.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(div_up(nsl_l, qn::kSpmvWarps),
                                                                  (int64_t)nsm * qn::kSpmvBlocksPerSm));

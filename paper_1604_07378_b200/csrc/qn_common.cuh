@@ -13,7 +13,7 @@ namespace qn {
 // diagnostics timeline (qn_system_timeline): per body pass, globaltimer ns at
 // the entry of block 0 and at the end of the finalising block / last CTA of
 // k_grad, k_eta, k_vec, k_tet, sptrsv_forward, sptrsv_backward
-constexpr int kTimelinePasses = 512, kTimelineKernels = 6;
+constexpr int kTimelinePasses = 512, kTimelineKernels = 7;
 
 
 // ---- error plumbing (thread-local message for qn_last_error) ---------------

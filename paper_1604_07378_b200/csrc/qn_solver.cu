@@ -1181,10 +1181,34 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
 
 // ---- AMG V(1,1) cycle (pcg == 2, one instance): every kernel is one warp
 // per 32-row SELL slice, grid-stride, 3 right-hand sides; all no-ops once the
-// CG has converged.  Level l: x = w D^-1 b (fused into the residual), r = b -
-// A x, b_{l+1} = R r, ..., x += P t_{l+1}, t = x + w D^-1 (b - A x).
+// CG has converged.  Level l: x = w D^-1 b (written by the producer of b: the
+// pre-smoothing kernel on level 0, the restriction below), r = b - A x,
+// b_{l+1} = R r, ..., x += P t_{l+1}, t = x + w D^-1 (b - A x).
+// The cycle's own vectors are fp32 rows of 16 bytes (x, y, z, 0): these kernels
+// are bound by the L1 wavefronts of the scattered column gathers (ncu: l1tex
+// 76-92 % of peak with three 8-byte loads per matrix entry), so a gathered
+// column is one 128-bit load.  Sums run in fp64.
 
-// Row products y_i = sum_j a_ij X(j) (3 columns) of a V-cycle operator, for
+__device__ __forceinline__ float4 f4(double a, double b, double c) {
+  return make_float4((float)a, (float)b, (float)c, 0.0f);
+}
+
+// One lane's batch of a CSR row: 4 entries K apart, masked at the row end (col -1).
+struct CsrBatch {
+  int j[4];
+  float a[4];
+};
+__device__ __forceinline__ void csr_batch_load(const SellDevF& S, int64_t e, int64_t e1, int K, CsrBatch& B) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
+    const int64_t ee = e + (int64_t)K * u;
+    const bool ok = ee < e1;
+    B.j[u] = ok ? __ldcs(S.col + ee) : -1;
+    B.a[u] = ok ? __ldcs(S.val + ee) : 0.0f;
+  }
+}
+
+// Row products y_i = sum_j a_ij X[j] (3 columns) of a V-cycle operator, for
 // every row, handed to `epi(i, acc)`.  Two layouts (chosen per operator at
 // upload from its mean row length, qn_api.cu sell_upload):
 //  * S.kl == 0: SELL-32, one warp per 32-row slice, lane = row (short rows:
@@ -1192,37 +1216,49 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(Sys
 //  * S.kl = K in {4, 8, 16, 32}: CSR, K lanes per row, 32/K rows per warp;
 //    the lanes of a row stride its entries (coalesced), a K-lane butterfly
 //    sums them (long rows: Galerkin coarse operators, restriction).
-// `xv(j, c)` returns column j's value (callers fuse scalings into it).
-template <class XV, class EPI>
-__device__ __forceinline__ void op_rows(const SellDevF& S, XV xv, EPI epi) {
+template <class EPI>
+__device__ __forceinline__ void op_rows(const SellDevF& S, const float4* __restrict__ X, EPI epi) {
   const int lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
   if (S.kl == 0) {
-    for (int sl = w0; sl < S.nslice; sl += nw) {
-      const int64_t e1 = S.ptr[sl + 1];
+    // every batch is kSellUnroll masked entries (the mask is warp-uniform: a slice is padded to one
+    // length), so a 15-entry slice is two round trips instead of one batch plus seven single loads;
+    // the next slice's bounds are fetched while this one runs
+    int sl = w0;
+    int64_t n0 = 0, n1 = 0;
+    if (sl < S.nslice) {
+      n0 = S.ptr[sl];
+      n1 = S.ptr[sl + 1];
+    }
+    for (; sl < S.nslice; sl += nw) {
+      const int64_t e1 = n1;
+      int64_t e = n0 + lane;
+      if (sl + nw < S.nslice) {
+        n0 = S.ptr[sl + nw];
+        n1 = S.ptr[sl + nw + 1];
+      }
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      int64_t e = S.ptr[sl] + lane;
-      for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
+      for (; e < e1; e += 32 * kSellUnroll) {
         int j[kSellUnroll];
-        double a[kSellUnroll];
-#pragma unroll
-        for (int u = 0; u < kSellUnroll; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
-          j[u] = __ldcs(S.col + e + 32 * u);
-          a[u] = (double)__ldcs(S.val + e + 32 * u);
-        }
+        float a[kSellUnroll];
 #pragma unroll
         for (int u = 0; u < kSellUnroll; ++u) {
-          a0 = fma(a[u], xv(j[u], 0), a0);
-          a1 = fma(a[u], xv(j[u], 1), a1);
-          a2 = fma(a[u], xv(j[u], 2), a2);
+          const bool ok = e + 32 * u < e1;
+          j[u] = ok ? __ldcs(S.col + e + 32 * u) : -1;
+          a[u] = ok ? __ldcs(S.val + e + 32 * u) : 0.0f;
         }
-      }
-      for (; e < e1; e += 32) {
-        const int j = __ldcs(S.col + e);
-        const double a = (double)__ldcs(S.val + e);
-        a0 = fma(a, xv(j, 0), a0);
-        a1 = fma(a, xv(j, 1), a1);
-        a2 = fma(a, xv(j, 2), a2);
+        float4 x[kSellUnroll];
+#pragma unroll
+        for (int u = 0; u < kSellUnroll; ++u) x[u] = X[j[u] < 0 ? 0 : j[u]];
+#pragma unroll
+        for (int u = 0; u < kSellUnroll; ++u) {
+          if (j[u] >= 0) {
+            const double av = (double)a[u];
+            a0 = fma(av, (double)x[u].x, a0);
+            a1 = fma(av, (double)x[u].y, a1);
+            a2 = fma(av, (double)x[u].z, a2);
+          }
+        }
       }
       const int i = 32 * sl + lane;
       if (i < S.nrows) {
@@ -1232,35 +1268,53 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, XV xv, EPI epi) {
     }
     return;
   }
-  const int K = S.kl, g = lane / K, q = lane % K, rpw = 32 / K;
-  for (int r0 = w0 * rpw; r0 < S.nrows; r0 += nw * rpw) {  // warp-uniform loop
+  // CSR, K lanes per row: software pipeline over masked 4-entry batches.  While a batch's column
+  // values are gathered, the next batch (of this row or, at its end, of the warp's next rows) is
+  // already in flight, and the row bounds are fetched two rows ahead.  Per lane the entries are
+  // summed in the order of a plain strided loop.
+  const int K = S.kl, g = lane / K, q = lane % K, rpw = 32 / K, step = nw * rpw;
+  int r0 = w0 * rpw;
+  if (r0 >= S.nrows) return;
+  auto bounds = [&](int r, int64_t& b0, int64_t& b1) {
+    b0 = b1 = 0;
+    if (r + g < S.nrows) {
+      b0 = S.ptr[r + g];
+      b1 = S.ptr[r + g + 1];
+    }
+  };
+  int64_t e0, e1, n0, n1;
+  bounds(r0, e0, e1);
+  bounds(r0 + step, n0, n1);
+  CsrBatch cur, nxt;
+  csr_batch_load(S, e0 + q, e1, K, cur);
+  for (; r0 < S.nrows; r0 += step) {  // warp-uniform loop
     const int i = r0 + g;
+    int64_t m0, m1;
+    bounds(r0 + 2 * step, m0, m1);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (i < S.nrows) {
-      const int64_t e1 = S.ptr[i + 1];
-      int64_t e = S.ptr[i] + q;
-      for (; e + (int64_t)K * 3 < e1; e += 4 * K) {  // 4 entries in flight per lane
-        int j[4];
-        double a[4];
+    int64_t e = e0 + q;
+    for (;;) {
+      const int64_t en = e + 4 * (int64_t)K;
+      const bool more = __any_sync(0xffffffffu, en - q < e1);
+      if (more)
+        csr_batch_load(S, en, e1, K, nxt);
+      else
+        csr_batch_load(S, n0 + q, n1, K, nxt);
+      float4 x[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          j[u] = __ldcs(S.col + e + K * u);
-          a[u] = (double)__ldcs(S.val + e + K * u);
-        }
+      for (int u = 0; u < 4; ++u) x[u] = X[cur.j[u] < 0 ? 0 : cur.j[u]];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          a0 = fma(a[u], xv(j[u], 0), a0);
-          a1 = fma(a[u], xv(j[u], 1), a1);
-          a2 = fma(a[u], xv(j[u], 2), a2);
+      for (int u = 0; u < 4; ++u) {
+        if (cur.j[u] >= 0) {
+          const double av = (double)cur.a[u];
+          a0 = fma(av, (double)x[u].x, a0);
+          a1 = fma(av, (double)x[u].y, a1);
+          a2 = fma(av, (double)x[u].z, a2);
         }
       }
-      for (; e < e1; e += K) {
-        const int j = __ldcs(S.col + e);
-        const double a = (double)__ldcs(S.val + e);
-        a0 = fma(a, xv(j, 0), a0);
-        a1 = fma(a, xv(j, 1), a1);
-        a2 = fma(a, xv(j, 2), a2);
-      }
+      cur = nxt;
+      if (!more) break;
+      e = en;
     }
     for (int o = K >> 1; o > 0; o >>= 1) {
       a0 += __shfl_xor_sync(0xffffffffu, a0, o);
@@ -1271,54 +1325,79 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, XV xv, EPI epi) {
       const double acc[3] = {a0, a1, a2};
       epi(i, acc);
     }
+    e0 = n0;
+    e1 = n1;
+    n0 = m0;
+    n1 = m1;
   }
 }
 
 __device__ __forceinline__ bool amg_on(const SysView& v) { return pcg_on(v, 0); }
 
-// x = w D^-1 b (pre-smoothing from zero) and r = b - A x, with x of the
-// neighbours recomputed from b (no extra pass)
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
+// level 0 pre-smoothing from zero: x = w D^-1 b (b = the fp64 CG residual)
+__global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_amg_presmooth(SysView v) {
   if (!amg_on(v)) return;
-  const AmgDevLevel& L = v.alev[l];
+  const AmgDevLevel& L = v.alev[0];
   const double w = L.omega;
   const double* __restrict__ b = L.b;
   const double* __restrict__ dinv = L.dinv;
-  op_rows(
-      L.A, [&](int j, int c) { return w * __ldg(dinv + j) * b[3 * (size_t)j + c]; },
-      [&](int i, const double* a) {
-        const double wd = w * dinv[i];
-        const double* bi = b + 3 * (size_t)i;
-        double* xi = L.x + 3 * (size_t)i;
-        double* ri = L.r + 3 * (size_t)i;
-        for (int c = 0; c < 3; ++c) {
-          xi[c] = wd * bi[c];
-          ri[c] = bi[c] - a[c];
-        }
-      });
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += stride) {
+    const double wd = w * dinv[i];
+    const double* bi = b + 3 * (size_t)i;
+    L.xf[i] = f4(wd * bi[0], wd * bi[1], wd * bi[2]);
+  }
 }
 
-// b_{l+1} = R_l r_l
+// r = b - A x
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
+  if (!amg_on(v)) return;
+  const AmgDevLevel& L = v.alev[l];
+  op_rows(L.A, L.xf, [&](int i, const double* a) {
+    double bi[3];
+    if (l == 0) {
+      const double* bp = L.b + 3 * (size_t)i;
+      bi[0] = bp[0], bi[1] = bp[1], bi[2] = bp[2];
+    } else {
+      const float4 bq = L.bf[i];
+      bi[0] = bq.x, bi[1] = bq.y, bi[2] = bq.z;
+    }
+    L.rf[i] = f4(bi[0] - a[0], bi[1] - a[1], bi[2] - a[2]);
+  });
+}
+
+// b_{l+1} = R_l r_l and the coarse level's pre-smoothed x = w D^-1 b
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict(SysView v, int l) {
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  const double* __restrict__ r = L.r;
-  op_rows(
-      L.R, [&](int j, int c) { return r[3 * (size_t)j + c]; },
-      [&](int i, const double* a) {
-        double* bi = C.b + 3 * (size_t)i;
-        for (int c = 0; c < 3; ++c) bi[c] = a[c];
-      });
+  op_rows(L.R, L.rf, [&](int i, const double* a) {
+    C.bf[i] = f4(a[0], a[1], a[2]);
+    const double wd = C.omega * C.dinv[i];
+    C.xf[i] = f4(wd * a[0], wd * a[1], wd * a[2]);
+  });
 }
 
 // coarsest level: t = A_c^-1 b (dense inverse, warp per row, b staged in shared memory)
+constexpr int kCoarseUnroll = 16;
 __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
   if (!amg_on(v)) return;
   extern __shared__ double sb[];
   const AmgDevLevel& L = v.alev[v.amg_levels - 1];
   const int nc = v.ncoarse;
-  for (int q = threadIdx.x; q < 3 * nc; q += blockDim.x) sb[q] = L.b[q];
+  const bool single = v.amg_levels == 1;  // one-level hierarchy: the coarsest level is the CG's own (fp64 b, t)
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    if (single) {
+      sb[3 * q + 0] = L.b[3 * q + 0];
+      sb[3 * q + 1] = L.b[3 * q + 1];
+      sb[3 * q + 2] = L.b[3 * q + 2];
+    } else {
+      const float4 bq = L.bf[q];
+      sb[3 * q + 0] = bq.x;
+      sb[3 * q + 1] = bq.y;
+      sb[3 * q + 2] = bq.z;
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
@@ -1326,12 +1405,12 @@ __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
     const float* row = v.cinv + (size_t)k * nc;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     int c = lane;
-    for (; c + 96 < nc; c += 128) {  // 4 loads in flight per lane
-      float m[4];
+    for (; c + 32 * (kCoarseUnroll - 1) < nc; c += 32 * kCoarseUnroll) {  // kCoarseUnroll loads in flight per lane
+      float m[kCoarseUnroll];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) m[u] = __ldg(row + c + 32 * u);
+      for (int u = 0; u < kCoarseUnroll; ++u) m[u] = __ldg(row + c + 32 * u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kCoarseUnroll; ++u) {
         const int cc = c + 32 * u;
         a0 = fma((double)m[u], sb[3 * cc + 0], a0);
         a1 = fma((double)m[u], sb[3 * cc + 1], a1);
@@ -1348,9 +1427,13 @@ __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
     a1 = warp_sum(a1);
     a2 = warp_sum(a2);
     if (lane == 0) {
-      L.t[3 * k + 0] = a0;
-      L.t[3 * k + 1] = a1;
-      L.t[3 * k + 2] = a2;
+      if (single) {
+        L.t[3 * k + 0] = a0;
+        L.t[3 * k + 1] = a1;
+        L.t[3 * k + 2] = a2;
+      } else {
+        L.tf[k] = f4(a0, a1, a2);
+      }
     }
   }
 }
@@ -1360,29 +1443,31 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  const double* __restrict__ t = C.t;
-  op_rows(
-      L.P, [&](int j, int c) { return t[3 * (size_t)j + c]; },
-      [&](int i, const double* a) {
-        double* xi = L.x + 3 * (size_t)i;
-        for (int c = 0; c < 3; ++c) xi[c] += a[c];
-      });
+  op_rows(L.P, C.tf, [&](int i, const double* a) {
+    const float4 xi = L.xf[i];
+    L.xf[i] = f4((double)xi.x + a[0], (double)xi.y + a[1], (double)xi.z + a[2]);
+  });
 }
 
-// t = x + w D^-1 (b - A x)  (post-smoothing)
+// t = x + w D^-1 (b - A x)  (post-smoothing; level 0 writes z in fp64)
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(SysView v, int l) {
   if (!amg_on(v)) return;
   const AmgDevLevel& L = v.alev[l];
-  const double* __restrict__ x = L.x;
-  op_rows(
-      L.A, [&](int j, int c) { return x[3 * (size_t)j + c]; },
-      [&](int i, const double* a) {
-        const double wd = L.omega * L.dinv[i];
-        const double* bi = L.b + 3 * (size_t)i;
-        const double* xi = x + 3 * (size_t)i;
-        double* ti = L.t + 3 * (size_t)i;
-        for (int c = 0; c < 3; ++c) ti[c] = fma(wd, bi[c] - a[c], xi[c]);
-      });
+  op_rows(L.A, L.xf, [&](int i, const double* a) {
+    const double wd = L.omega * L.dinv[i];
+    const float4 xi = L.xf[i];
+    if (l == 0) {
+      const double* bi = L.b + 3 * (size_t)i;
+      double* ti = L.t + 3 * (size_t)i;
+      ti[0] = fma(wd, bi[0] - a[0], (double)xi.x);
+      ti[1] = fma(wd, bi[1] - a[1], (double)xi.y);
+      ti[2] = fma(wd, bi[2] - a[2], (double)xi.z);
+    } else {
+      const float4 bq = L.bf[i];
+      L.tf[i] = f4(fma(wd, (double)bq.x - a[0], (double)xi.x), fma(wd, (double)bq.y - a[1], (double)xi.y),
+                   fma(wd, (double)bq.z - a[2], (double)xi.z));
+    }
+  });
 }
 
 // r.z after a V-cycle: init -> rz (beta stays 0); else beta = rz_new / rz
@@ -1482,6 +1567,8 @@ static int ensure_coarse_smem(int nc) {
 int launch_vcycle(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const int nl = (int)S->h_alev.size();
+  k_amg_presmooth<<<S->v.nblk_upd, kUpdThreads, 0, st>>>(v);
+  QN_CHECK_LAUNCH();
   for (int l = 0; l + 1 < nl; ++l) {
     const auto& L = S->h_alev[l];
     k_amg_residual<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);

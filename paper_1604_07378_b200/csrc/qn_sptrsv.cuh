@@ -176,6 +176,13 @@ __device__ __forceinline__ void solve_tl(const FactorView& F, int kid, int slot)
     if (p < (unsigned long long)kTimelinePasses) F.ktl[(p * kTimelineKernels + kid) * 2 + slot] = gtime();
   }
 }
+// latest stamp over several CTAs (kid 6 = dense top: the last finalised row block)
+__device__ __forceinline__ void solve_tl_max(const FactorView& F, int kid, int slot) {
+  if (F.ktl) {
+    const unsigned long long p = *((volatile const unsigned long long*)F.passes);
+    if (p < (unsigned long long)kTimelinePasses) atomicMax(F.ktl + (p * kTimelineKernels + kid) * 2 + slot, gtime());
+  }
+}
 
 // SM cycle counter (phases inside one task run on one SM)
 __device__ __forceinline__ void trace_clock(unsigned long long* trace, size_t slot) {
@@ -1298,8 +1305,10 @@ __global__ void __launch_bounds__(kSolveThreads, 6) sptrsv_top_sym(FactorView F,
   const int b = blockIdx.y;
   if (!io.active(b)) return;
   mbar_init(&s_mbar);
+  if (threadIdx.x == 0 && blockIdx.x == 0) solve_tl(F, 6, 0);
   unsigned phase = 0;
   top_tile(F, io, (int)blockIdx.x, b, st, gI, gJ, s_last, &s_mbar, phase, false);
+  if (threadIdx.x == 0 && (s_last[0] >= 0 || s_last[1] >= 0)) solve_tl_max(F, 6, 1);
 }
 
 // Forward, dense-top tiles and backward in ONE persistent kernel: forward

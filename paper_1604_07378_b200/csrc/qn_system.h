@@ -78,10 +78,15 @@ struct SellDevF {
 struct AmgDevLevel {
   SellDevF A, P, R;     // operator (n x n), prolongator (n x n_coarse), restriction (n_coarse x n)
   const double* dinv;   // [n]
-  double* x;            // [n][3] pre-smoothed (+ prolonged) iterate
-  double* t;            // [n][3] post-smoothed result (level 0: z)
-  double* b;            // [n][3] right-hand side (level 0: the CG residual)
-  double* r;            // [n][3] residual after pre-smoothing
+  // V-cycle vectors: fp32, one 16-byte (x, y, z, 0) entry per row, so the column gather of every
+  // operator product is ONE 128-bit load per matrix entry (the cycle is a preconditioner: the CG
+  // recurrences, its residual and the convergence test stay fp64)
+  float4* xf;           // [n] pre-smoothed (+ prolonged) iterate
+  float4* rf;           // [n] residual after pre-smoothing
+  float4* bf;           // [n] right-hand side, levels >= 1
+  float4* tf;           // [n] post-smoothed result, levels >= 1
+  double* t;            // level 0: z [n][3]
+  double* b;            // level 0: the CG residual [n][3]
   double omega;         // Jacobi weight 4 / (3 rho(D^-1 A))
   int32_t n, nblk;      // rows, grid of the level's SELL kernels
 };

@@ -15,7 +15,7 @@ import paper_1604_07378_b200 as Q  # noqa: E402
 from paper_1604_07378_b200 import _lib  # noqa: E402
 from paper_1604_07378_b200.solvers import ResidentRun, SolverConfig  # noqa: E402
 
-PASSES, KERNELS = 512, 6
+PASSES, KERNELS = 512, 7
 
 
 def main(cfg="c2", frames="3"):
@@ -57,6 +57,12 @@ def main(cfg="c2", frames="3"):
         for j, n in enumerate(["grad end -> fwd entry", "forward", "fwd end -> bwd entry", "backward",
                                "bwd end -> eta entry"]):
             print(f"    {n:22s} mean {a[:, j].mean():7.2f} us")
+        tp = [(t[p, 6, 0] - t[p, 4, 1], t[p, 6, 1] - t[p, 6, 0], t[p, 5, 0] - t[p, 6, 1]) for p in range(npass)
+              if t[p, 6, 0] and t[p, 6, 1] and t[p, 4, 1] and t[p, 5, 0]]
+        if tp:
+            a = np.array(tp, dtype=np.float64) / 1000.0
+            for j, n in enumerate(["fwd end -> top entry", "top", "top end -> bwd entry"]):
+                print(f"      {n:22s} mean {a[:, j].mean():7.2f} us")
 
 
 if __name__ == "__main__":

@@ -733,6 +733,11 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       const int nl = (int)H.lv.size();
       S->h_alev.assign(nl, qn::AmgDevLevel{});
       if ((rc = sys_alloc(S, &v.pz, fv))) return fail(rc);
+      {  // QN_AMG_ZF=0 (experiment knob): keep z in fp64 with the separate r.z kernel
+        const char* e = std::getenv("QN_AMG_ZF");
+        // (a one-level hierarchy has no smoothing kernel: its dense solve writes the fp64 z)
+        if (nl >= 2 && !(e && std::atoi(e) == 0) && (rc = sys_alloc(S, &v.pzf, (size_t)nf))) return fail(rc);
+      }
       for (int l = 0; l < nl; ++l) {
         const qn::AmgLevel& L = H.lv[l];
         qn::AmgDevLevel& D = S->h_alev[l];

@@ -858,6 +858,7 @@ int qn_slab_create(const qn_slab_desc* d, qn_slab** out) {
   if (s.amg) {  // the local V-cycle reads the residual from v.pr and writes z to v.pz
     s.pr = L->v.pr;
     s.pz = L->v.pz;
+    L->v.pzf = nullptr;  // the slab CG adds its coarse share to the fp64 z: the V-cycle writes v.pz
     // its kernels run while the local system's instance is "in a direction
     // phase with an unconverged CG" (the local frame itself is never run)
     int32_t ph = PH_DIR;

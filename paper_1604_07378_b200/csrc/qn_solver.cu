@@ -1003,9 +1003,10 @@ __global__ void __launch_bounds__(kPT) k_pcg_init(SysView v) {
 // q = A p with p = z + beta p_old fused into the neighbour loads (z = dinv r
 // recomputed, so z is never stored); one warp per SELL slice, lane = row.
 // Partial p.q per block -> the last block computes alpha.
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(SysView v) {
+template <bool kZf>
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(SysView v, int force) {
   const int b = blockIdx.y;
-  if (!pcg_on(v, b)) return;
+  if (!force && !pcg_on(v, b)) return;  // force: stand-alone timing between frames (qn_system_time_kernel)
   __shared__ double red[3 * 32];
   const PcgCtl& pc = v.pctl[b];
   const int pb = pc.iter & 1;
@@ -1016,6 +1017,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
   // z = D^-1 r recomputed (Jacobi) or the stored V-cycle output (AMG: r <- z, dinv <- 1)
   const bool amg = v.pcg == 2;
   const double* __restrict__ r = amg ? v.pz + vo : v.pr + vo;
+  const float4* __restrict__ zf = v.pzf;  // kZf: z = the V-cycle output as fp32 rows (one 128-bit gather)
   const double* __restrict__ dinv = v.dinv + (size_t)b * v.n_free;
   const double* __restrict__ av = v.sell_val + (size_t)b * v.sell_nnz;
   double* __restrict__ q = v.pq + vo;
@@ -1039,27 +1041,48 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
 #pragma unroll
       for (int u = 0; u < kSellUnroll; ++u) {
         const double* pj = pold + 3 * (size_t)j[u];
-        const double* rj = r + 3 * (size_t)j[u];
-        q0 = fma(a[u], fma(be0, pj[0], rj[0] * d[u]), q0);
-        q1 = fma(a[u], fma(be1, pj[1], rj[1] * d[u]), q1);
-        q2 = fma(a[u], fma(be2, pj[2], rj[2] * d[u]), q2);
+        if (kZf) {
+          const float4 zj = zf[j[u]];
+          q0 = fma(a[u], fma(be0, pj[0], (double)zj.x), q0);
+          q1 = fma(a[u], fma(be1, pj[1], (double)zj.y), q1);
+          q2 = fma(a[u], fma(be2, pj[2], (double)zj.z), q2);
+        } else {
+          const double* rj = r + 3 * (size_t)j[u];
+          q0 = fma(a[u], fma(be0, pj[0], rj[0] * d[u]), q0);
+          q1 = fma(a[u], fma(be1, pj[1], rj[1] * d[u]), q1);
+          q2 = fma(a[u], fma(be2, pj[2], rj[2] * d[u]), q2);
+        }
       }
     }
     for (; e < e1; e += 32) {
       const int j = __ldg(v.sell_col + e);
       const double a = __ldg(av + e), d = amg ? 1.0 : __ldg(dinv + j);
       const double* pj = pold + 3 * (size_t)j;
-      const double* rj = r + 3 * (size_t)j;
-      q0 = fma(a, fma(be0, pj[0], rj[0] * d), q0);
-      q1 = fma(a, fma(be1, pj[1], rj[1] * d), q1);
-      q2 = fma(a, fma(be2, pj[2], rj[2] * d), q2);
+      if (kZf) {
+        const float4 zj = zf[j];
+        q0 = fma(a, fma(be0, pj[0], (double)zj.x), q0);
+        q1 = fma(a, fma(be1, pj[1], (double)zj.y), q1);
+        q2 = fma(a, fma(be2, pj[2], (double)zj.z), q2);
+      } else {
+        const double* rj = r + 3 * (size_t)j;
+        q0 = fma(a, fma(be0, pj[0], rj[0] * d), q0);
+        q1 = fma(a, fma(be1, pj[1], rj[1] * d), q1);
+        q2 = fma(a, fma(be2, pj[2], rj[2] * d), q2);
+      }
     }
     const int i = 32 * sl + lane;
     if (i < v.n_free) {
       const double d = amg ? 1.0 : dinv[i];
-      const double p0 = fma(be0, pold[3 * i + 0], r[3 * i + 0] * d);
-      const double p1 = fma(be1, pold[3 * i + 1], r[3 * i + 1] * d);
-      const double p2 = fma(be2, pold[3 * i + 2], r[3 * i + 2] * d);
+      double z0, z1, z2;
+      if (kZf) {
+        const float4 zi = zf[i];
+        z0 = zi.x, z1 = zi.y, z2 = zi.z;
+      } else {
+        z0 = r[3 * i + 0] * d, z1 = r[3 * i + 1] * d, z2 = r[3 * i + 2] * d;
+      }
+      const double p0 = fma(be0, pold[3 * i + 0], z0);
+      const double p1 = fma(be1, pold[3 * i + 1], z1);
+      const double p2 = fma(be2, pold[3 * i + 2], z2);
       pnew[3 * i + 0] = p0;
       pnew[3 * i + 1] = p1;
       pnew[3 * i + 2] = p2;
@@ -1470,6 +1493,46 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(S
   });
 }
 
+// Level-0 post-smoothing of a single system: z = x + w D^-1 (b - A x) rounded to fp32 rows (v.pzf:
+// the CG reads z only through it, so p, q and r.z all see the same z), with the r.z partial sums
+// of k_pcg_rz in the epilogue (b is the CG residual): the last block forms beta and r.z.
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth_rz(SysView v) {
+  if (!amg_on(v)) return;
+  __shared__ double red[3 * 32];
+  const AmgDevLevel& L = v.alev[0];
+  double acc[3] = {0.0, 0.0, 0.0};
+  op_rows(L.A, L.xf, [&](int i, const double* a) {
+    const double wd = L.omega * L.dinv[i];
+    const float4 xi = L.xf[i];
+    const double* bi = L.b + 3 * (size_t)i;
+    const double b0 = bi[0], b1 = bi[1], b2 = bi[2];
+    const float4 z = f4(fma(wd, b0 - a[0], (double)xi.x), fma(wd, b1 - a[1], (double)xi.y),
+                        fma(wd, b2 - a[2], (double)xi.z));
+    v.pzf[i] = z;
+    acc[0] = fma(b0, (double)z.x, acc[0]);
+    acc[1] = fma(b1, (double)z.y, acc[1]);
+    acc[2] = fma(b2, (double)z.z, acc[2]);
+  });
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pp = v.part_p + (size_t)blockIdx.x * 8;
+    for (int k = 0; k < 3; ++k) pp[k] = acc[k];
+  }
+  if (last_block(v.cnt_p, 3, 0, v.n_inst, gridDim.x)) {
+    __shared__ double tot[3];
+    sum_partials(v.part_p, gridDim.x, 8, 3, tot);
+    if (threadIdx.x == 0) {
+      PcgCtl& p = v.pctl[0];
+      const bool init = p.iter == 0;  // the V-cycle after k_pcg_init: beta stays 0
+      for (int k = 0; k < 3; ++k) {
+        if ((p.conv >> k) & 1) continue;
+        p.beta[k] = init ? 0.0 : tot[k] / p.rz[k];
+        p.rz[k] = tot[k];
+      }
+    }
+  }
+}
+
 // r.z after a V-cycle: init -> rz (beta stays 0); else beta = rz_new / rz
 __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_rz(SysView v, int init) {
   if (!amg_on(v)) return;
@@ -1501,50 +1564,15 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_rz(SysView
   }
 }
 
-// stand-alone timing of the CG's SpMV (qn_system_time_kernel "spmv"):
-// q = A_free x over the fp64 SELL matrix, the same access pattern as k_pcg_spmv
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_spmv_timing(SysView v) {
-  const int lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
-  for (int sl = w0; sl < v.nslice; sl += nw) {
-    const int64_t e0 = v.sell_ptr[sl], e1 = v.sell_ptr[sl + 1];
-    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
-    int64_t e = e0 + lane;
-    for (; e + 32 * (kSellUnroll - 1) < e1; e += 32 * kSellUnroll) {
-      int j[kSellUnroll];
-      double a[kSellUnroll];
-#pragma unroll
-      for (int u = 0; u < kSellUnroll; ++u) {
-        j[u] = __ldcs(v.sell_col + e + 32 * u);
-        a[u] = __ldcs(v.sell_val + e + 32 * u);
-      }
-#pragma unroll
-      for (int u = 0; u < kSellUnroll; ++u) {
-        const double* xj = v.px + 3 * (size_t)j[u];
-        q0 = fma(a[u], xj[0], q0);
-        q1 = fma(a[u], xj[1], q1);
-        q2 = fma(a[u], xj[2], q2);
-      }
-    }
-    for (; e < e1; e += 32) {
-      const int j = __ldcs(v.sell_col + e);
-      const double a = __ldcs(v.sell_val + e);
-      const double* xj = v.px + 3 * (size_t)j;
-      q0 = fma(a, xj[0], q0);
-      q1 = fma(a, xj[1], q1);
-      q2 = fma(a, xj[2], q2);
-    }
-    const int i = 32 * sl + lane;
-    if (i < v.n_free) {
-      v.pq[3 * i + 0] = q0;
-      v.pq[3 * i + 1] = q1;
-      v.pq[3 * i + 2] = q2;
-    }
-  }
-}
-
+// stand-alone timing of the CG's SpMV (qn_system_time_kernel "spmv"): the CG's own kernel (q = A p
+// with p = z + beta p_old formed in the neighbour loads, p and q written, p.q partials), forced on
+// between frames; k_pcg_init resets everything it touches
 int launch_spmv_timing(qn_system* S, cudaStream_t st) {
-  k_spmv_timing<<<S->v.nblk_spmv, kSpmvThreads, 0, st>>>(S->v);
+  const SysView& v = S->v;
+  if (v.pcg == 2 && v.pzf)
+    k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 1);
+  else
+    k_pcg_spmv<false><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 1);
   QN_CHECK_LAUNCH();
   return QN_OK;
 }
@@ -1585,13 +1613,17 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
     const auto& L = S->h_alev[l];
     k_amg_prolong<<<L.P.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
-    k_amg_smooth<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
+    if (l == 0 && v.pzf)
+      k_amg_smooth_rz<<<L.A.nblk, kSpmvThreads, 0, st>>>(v);
+    else
+      k_amg_smooth<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
   }
   return QN_OK;
 }
 
 int launch_pcg_rz(qn_system* S, int init, cudaStream_t st) {
+  if (S->v.pzf) return QN_OK;  // fused into the V-cycle's last kernel (k_amg_smooth_rz)
   k_pcg_rz<<<S->v.nblk_upd, kUpdThreads, 0, st>>>(S->v, init);
   QN_CHECK_LAUNCH();
   return QN_OK;
@@ -1660,7 +1692,10 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
 
 int launch_pcg_iter(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
-  k_pcg_spmv<<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v);
+  if (v.pcg == 2 && v.pzf)
+    k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 0);
+  else
+    k_pcg_spmv<false><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 0);
   QN_CHECK_LAUNCH();
   k_pcg_update<<<dim3(v.nblk_upd, v.n_inst), kUpdThreads, 0, st>>>(v);
   QN_CHECK_LAUNCH();

@@ -178,6 +178,7 @@ struct SysView {
   const AmgDevLevel* alev;  // [amg_levels] (device)
   const float* cinv;        // dense inverse of the coarsest operator [ncoarse][ncoarse], fp32 (preconditioner only)
   double* pz;               // z = B r (the V-cycle output on level 0)
+  float4* pzf;              // single-system AMG: z rounded to fp32 rows of 16 B (replaces pz; null: fp64 pz)
   // ---- colliders (dynamics.py:199-285, 446-457, 486-516) ----
   int32_t n_col, nblk_c;
   double w_col;

@@ -733,6 +733,7 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
       const int nl = (int)H.lv.size();
       S->h_alev.assign(nl, qn::AmgDevLevel{});
       if ((rc = sys_alloc(S, &v.pz, fv))) return fail(rc);
+      if ((rc = sys_alloc(S, &v.amg_bar, (size_t)2))) return fail(rc);
       {  // QN_AMG_ZF=0 (experiment knob): keep z in fp64 with the separate r.z kernel
         const char* e = std::getenv("QN_AMG_ZF");
         // (a one-level hierarchy has no smoothing kernel: its dense solve writes the fp64 z)
@@ -983,6 +984,14 @@ static int sell_upload(qn_system* S, int64_t nrows, int64_t ncols, const int64_t
   const double mean = nrows ? (double)nnz / (double)nrows : 0.0;
   // swept on c5 (QN_AMG_CSR_LANES, V-cycle ms): 4 lanes per row 1.174, 8 1.208, 2 1.282, 16 1.364, 1 1.758
   int kl = mean <= 16.0 ? 0 : mean <= 128.0 ? 4 : 8;
+  // experiment knob (off by default, measured neutral on configs[4]): on levels of at most
+  // QN_AMG_SMALL_ROWS rows, enough lanes per row that a row is ONE masked batch of 4 entries per lane
+  int64_t small_rows = 0;
+  if (const char* e = std::getenv("QN_AMG_SMALL_ROWS")) small_rows = std::atoll(e);
+  if (kl > 0 && nrows <= small_rows) {
+    kl = 4;
+    while (kl < 32 && 4.0 * kl < mean) kl *= 2;
+  }
   if (const char* e = std::getenv("QN_AMG_CSR_LANES"))  // experiment knob: lanes per row of the CSR levels
     if (kl > 0) kl = std::max(1, std::min(32, std::atoi(e)));
   int dev = 0, nsm = qn::kSMs;
@@ -1282,6 +1291,10 @@ int qn_frame_step(qn_system* S, const qn_solver_config* cfg, const double* fixed
   if (S->factor && (rc = factor_check_watchdog(S->factor))) return rc;
   if ((int64_t)passes > (int64_t)c.max_passes) {
     set_error("frame: pass limit exceeded (phase machine did not terminate)");
+    return QN_ERR_CUDA;
+  }
+  if (pe[1] & 8) {
+    set_error("frame: the AMG tail kernel's grid barrier timed out (its CTAs were not all resident)");
     return QN_ERR_CUDA;
   }
   if (pe[1] & 4) {  // the direct solve is exact; an unconverged CG direction is reported, not used silently

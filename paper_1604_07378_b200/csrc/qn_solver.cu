@@ -1239,8 +1239,15 @@ __device__ __forceinline__ void csr_batch_load(const SellDevF& S, int64_t e, int
 //  * S.kl = K in {4, 8, 16, 32}: CSR, K lanes per row, 32/K rows per warp;
 //    the lanes of a row stride its entries (coalesced), a K-lane butterfly
 //    sums them (long rows: Galerkin coarse operators, restriction).
-template <class EPI>
-__device__ __forceinline__ void op_rows(const SellDevF& S, const float4* __restrict__ X, EPI epi) {
+// kCg: the vector was written earlier in the SAME launch by other CTAs (k_amg_tail): read it through
+// L2 (ld.global.cg), never through the non-coherent L1 / read-only path
+template <bool kCg>
+__device__ __forceinline__ float4 ldv(const float4* p) {
+  return kCg ? __ldcg(p) : *p;
+}
+
+template <bool kCg, class EPI>
+__device__ __forceinline__ void op_rows(const SellDevF& S, const float4* X, EPI epi) {
   const int lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
   if (S.kl == 0) {
@@ -1272,7 +1279,7 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, const float4* __restr
         }
         float4 x[kSellUnroll];
 #pragma unroll
-        for (int u = 0; u < kSellUnroll; ++u) x[u] = X[j[u] < 0 ? 0 : j[u]];
+        for (int u = 0; u < kSellUnroll; ++u) x[u] = ldv<kCg>(X + (j[u] < 0 ? 0 : j[u]));
 #pragma unroll
         for (int u = 0; u < kSellUnroll; ++u) {
           if (j[u] >= 0) {
@@ -1325,7 +1332,7 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, const float4* __restr
         csr_batch_load(S, n0 + q, n1, K, nxt);
       float4 x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = X[cur.j[u] < 0 ? 0 : cur.j[u]];
+      for (int u = 0; u < 4; ++u) x[u] = ldv<kCg>(X + (cur.j[u] < 0 ? 0 : cur.j[u]));
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (cur.j[u] >= 0) {
@@ -1373,39 +1380,44 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_amg_presmooth(
 }
 
 // r = b - A x
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
-  if (!amg_on(v)) return;
+template <bool kCg>
+__device__ __forceinline__ void amg_residual(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
-  op_rows(L.A, L.xf, [&](int i, const double* a) {
+  op_rows<kCg>(L.A, L.xf, [&](int i, const double* a) {
     double bi[3];
     if (l == 0) {
       const double* bp = L.b + 3 * (size_t)i;
       bi[0] = bp[0], bi[1] = bp[1], bi[2] = bp[2];
     } else {
-      const float4 bq = L.bf[i];
+      const float4 bq = ldv<kCg>(L.bf + i);
       bi[0] = bq.x, bi[1] = bq.y, bi[2] = bq.z;
     }
     L.rf[i] = f4(bi[0] - a[0], bi[1] - a[1], bi[2] - a[2]);
   });
 }
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
+  if (amg_on(v)) amg_residual<false>(v, l);
+}
 
 // b_{l+1} = R_l r_l and the coarse level's pre-smoothed x = w D^-1 b
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict(SysView v, int l) {
-  if (!amg_on(v)) return;
+template <bool kCg>
+__device__ __forceinline__ void amg_restrict(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  op_rows(L.R, L.rf, [&](int i, const double* a) {
+  op_rows<kCg>(L.R, L.rf, [&](int i, const double* a) {
     C.bf[i] = f4(a[0], a[1], a[2]);
     const double wd = C.omega * C.dinv[i];
     C.xf[i] = f4(wd * a[0], wd * a[1], wd * a[2]);
   });
 }
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict(SysView v, int l) {
+  if (amg_on(v)) amg_restrict<false>(v, l);
+}
 
 // coarsest level: t = A_c^-1 b (dense inverse, warp per row, b staged in shared memory)
 constexpr int kCoarseUnroll = 16;
-__global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
-  if (!amg_on(v)) return;
-  extern __shared__ double sb[];
+template <bool kCg>
+__device__ __forceinline__ void amg_coarse(const SysView& v, double* sb) {
   const AmgDevLevel& L = v.alev[v.amg_levels - 1];
   const int nc = v.ncoarse;
   const bool single = v.amg_levels == 1;  // one-level hierarchy: the coarsest level is the CG's own (fp64 b, t)
@@ -1415,7 +1427,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
       sb[3 * q + 1] = L.b[3 * q + 1];
       sb[3 * q + 2] = L.b[3 * q + 2];
     } else {
-      const float4 bq = L.bf[q];
+      const float4 bq = ldv<kCg>(L.bf + q);
       sb[3 * q + 0] = bq.x;
       sb[3 * q + 1] = bq.y;
       sb[3 * q + 2] = bq.z;
@@ -1460,25 +1472,32 @@ __global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
     }
   }
 }
+__global__ void __launch_bounds__(kSpmvThreads) k_amg_coarse(SysView v) {
+  extern __shared__ double sb[];
+  if (amg_on(v)) amg_coarse<false>(v, sb);
+}
 
 // x_l += P_l t_{l+1}
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(SysView v, int l) {
-  if (!amg_on(v)) return;
+template <bool kCg>
+__device__ __forceinline__ void amg_prolong(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
-  op_rows(L.P, C.tf, [&](int i, const double* a) {
-    const float4 xi = L.xf[i];
+  op_rows<kCg>(L.P, C.tf, [&](int i, const double* a) {
+    const float4 xi = ldv<kCg>(L.xf + i);
     L.xf[i] = f4((double)xi.x + a[0], (double)xi.y + a[1], (double)xi.z + a[2]);
   });
 }
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(SysView v, int l) {
+  if (amg_on(v)) amg_prolong<false>(v, l);
+}
 
 // t = x + w D^-1 (b - A x)  (post-smoothing; level 0 writes z in fp64)
-__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(SysView v, int l) {
-  if (!amg_on(v)) return;
+template <bool kCg>
+__device__ __forceinline__ void amg_smooth(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
-  op_rows(L.A, L.xf, [&](int i, const double* a) {
+  op_rows<kCg>(L.A, L.xf, [&](int i, const double* a) {
     const double wd = L.omega * L.dinv[i];
-    const float4 xi = L.xf[i];
+    const float4 xi = ldv<kCg>(L.xf + i);
     if (l == 0) {
       const double* bi = L.b + 3 * (size_t)i;
       double* ti = L.t + 3 * (size_t)i;
@@ -1486,11 +1505,79 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(S
       ti[1] = fma(wd, bi[1] - a[1], (double)xi.y);
       ti[2] = fma(wd, bi[2] - a[2], (double)xi.z);
     } else {
-      const float4 bq = L.bf[i];
+      const float4 bq = ldv<kCg>(L.bf + i);
       L.tf[i] = f4(fma(wd, (double)bq.x - a[0], (double)xi.x), fma(wd, (double)bq.y - a[1], (double)xi.y),
                    fma(wd, (double)bq.z - a[2], (double)xi.z));
     }
   });
+}
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth(SysView v, int l) {
+  if (amg_on(v)) amg_smooth<false>(v, l);
+}
+
+// The small levels of the hierarchy (levels l0 .. coarsest, a few thousand rows each) in ONE
+// launch: their kernels do microseconds of work but pay a launch boundary each (13 graph nodes
+// per V-cycle on configs[4]).  The CTAs of this kernel are all resident (grid sized from the
+// occupancy query, prepare_kernels) and separate the phases with a grid-wide barrier: arrivals
+// on amg_bar[0], which only grows; amg_bar[1] is the count at kernel entry, advanced by the last
+// arrival of the last barrier.  A barrier that does not complete (a CTA not resident) gives up
+// after ~1 s and reports through the frame's error word instead of hanging.
+__device__ __forceinline__ bool amg_grid_barrier(const SysView& v, unsigned base, unsigned k, bool last) {
+  __syncthreads();
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = k * gridDim.x;
+    const unsigned arrived = atomicAdd(v.amg_bar, 1u) + 1u - base;
+    ok = 1;
+    if (arrived == target) {
+      if (last) {
+        atomicExch(v.amg_bar + 1, base + target);
+        __threadfence();
+      }
+    } else {
+      unsigned spins = 0;
+      while (*((volatile unsigned*)v.amg_bar) - base < target) {
+        if (++spins > (1u << 22)) {
+          __nanosleep(200);
+          if (spins > (1u << 22) + 5000000u) {
+            ok = 0;
+            atomicOr(v.passes + 1, 8ull);
+            break;
+          }
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_tail(SysView v, int l0) {
+  extern __shared__ double sb[];
+  if (!amg_on(v)) return;  // uniform over the grid: no CTA enters the barriers
+  const unsigned base = *((volatile unsigned*)(v.amg_bar + 1));
+  const int nl = v.amg_levels;
+  const unsigned nbar = 4u * (unsigned)(nl - 1 - l0);
+  unsigned k = 0;
+  for (int l = l0; l + 1 < nl; ++l) {
+    amg_residual<true>(v, l);
+    ++k;
+    if (!amg_grid_barrier(v, base, k, false)) return;
+    amg_restrict<true>(v, l);
+    ++k;
+    if (!amg_grid_barrier(v, base, k, false)) return;
+  }
+  amg_coarse<true>(v, sb);
+  for (int l = nl - 2; l >= l0; --l) {
+    ++k;
+    if (!amg_grid_barrier(v, base, k, false)) return;
+    amg_prolong<true>(v, l);
+    ++k;
+    if (!amg_grid_barrier(v, base, k, k == nbar)) return;
+    amg_smooth<true>(v, l);
+  }
 }
 
 // Level-0 post-smoothing of a single system: z = x + w D^-1 (b - A x) rounded to fp32 rows (v.pzf:
@@ -1501,7 +1588,7 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth_r
   __shared__ double red[3 * 32];
   const AmgDevLevel& L = v.alev[0];
   double acc[3] = {0.0, 0.0, 0.0};
-  op_rows(L.A, L.xf, [&](int i, const double* a) {
+  op_rows<false>(L.A, L.xf, [&](int i, const double* a) {
     const double wd = L.omega * L.dinv[i];
     const float4 xi = L.xf[i];
     const double* bi = L.b + 3 * (size_t)i;
@@ -1595,9 +1682,10 @@ static int ensure_coarse_smem(int nc) {
 int launch_vcycle(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   const int nl = (int)S->h_alev.size();
+  const int lt = S->amg_tail_level > 0 ? S->amg_tail_level : nl;  // levels lt .. coarsest run in k_amg_tail
   k_amg_presmooth<<<S->v.nblk_upd, kUpdThreads, 0, st>>>(v);
   QN_CHECK_LAUNCH();
-  for (int l = 0; l + 1 < nl; ++l) {
+  for (int l = 0; l + 1 < nl && l < lt; ++l) {
     const auto& L = S->h_alev[l];
     k_amg_residual<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
@@ -1605,11 +1693,15 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
     QN_CHECK_LAUNCH();
   }
   const int nc = v.ncoarse;
-  if (int rc = ensure_coarse_smem(nc)) return rc;
-  k_amg_coarse<<<std::max(1, std::min(2 * kSMs, div_up(nc, kSpmvWarps))), kSpmvThreads,
-                 (size_t)3 * nc * sizeof(double), st>>>(v);
+  if (lt < nl) {
+    k_amg_tail<<<S->amg_tail_grid, kSpmvThreads, (size_t)3 * nc * sizeof(double), st>>>(v, lt);
+  } else {
+    if (int rc = ensure_coarse_smem(nc)) return rc;
+    k_amg_coarse<<<std::max(1, std::min(2 * kSMs, div_up(nc, kSpmvWarps))), kSpmvThreads,
+                   (size_t)3 * nc * sizeof(double), st>>>(v);
+  }
   QN_CHECK_LAUNCH();
-  for (int l = nl - 2; l >= 0; --l) {
+  for (int l = std::min(nl - 2, lt - 1); l >= 0; --l) {
     const auto& L = S->h_alev[l];
     k_amg_prolong<<<L.P.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
@@ -1619,6 +1711,40 @@ int launch_vcycle(qn_system* S, cudaStream_t st) {
       k_amg_smooth<<<L.A.nblk, kSpmvThreads, 0, st>>>(v, l);
     QN_CHECK_LAUNCH();
   }
+  return QN_OK;
+}
+
+// The tail kernel's grid: every CTA resident (its phases meet at grid-wide barriers).  Levels with at
+// most QN_AMG_TAIL_ROWS rows below the finest join the tail.  Experiment knob, off by default (0):
+// measured neutral on configs[4] (V-cycle 1.104 ms with levels 3-5 in the tail vs 1.107 ms with
+// their 13 separate graph nodes: inside the frame graph the small levels' launch boundaries cost
+// almost nothing).
+int prepare_amg_tail(qn_system* S) {
+  S->amg_tail_level = 0;
+  const int nl = (int)S->h_alev.size();
+  if (S->v.pcg != 2 || nl < 3) return QN_OK;
+  int64_t max_rows = 0;
+  if (const char* e = std::getenv("QN_AMG_TAIL_ROWS")) max_rows = std::atoll(e);
+  int lt = nl;
+  for (int l = nl - 2; l >= 1 && S->h_alev[l].n <= max_rows; --l) lt = l;
+  if (lt > nl - 2) return QN_OK;
+  const size_t smem = (size_t)3 * S->v.ncoarse * sizeof(double);
+  {  // several systems may stage coarse levels of different sizes: the limit only grows
+    static std::mutex mu;
+    static size_t smem_set = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > smem_set) {
+      QN_CUDA(cudaFuncSetAttribute(k_amg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set = smem;
+    }
+  }
+  int per = 0, dev = 0, sms = 0;
+  QN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_amg_tail, kSpmvThreads, smem));
+  QN_CUDA(cudaGetDevice(&dev));
+  QN_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (per < 1) return QN_OK;
+  S->amg_tail_grid = std::min(per, kSpmvBlocksPerSm) * sms;
+  S->amg_tail_level = lt;
   return QN_OK;
 }
 
@@ -1795,8 +1921,10 @@ int launch_finish(qn_system* S, cudaStream_t st) {
 }
 
 int prepare_kernels(qn_system* S) {
-  if (S->v.pcg == 2)
+  if (S->v.pcg == 2) {
     if (int rc = ensure_coarse_smem(S->v.ncoarse)) return rc;
+    if (int rc = prepare_amg_tail(S)) return rc;
+  }
   if (!S->factor) return QN_OK;
   int rc = prepare_solve_kernels<SolverIO>(S->factor);
   if (!rc) rc = prepare_solve_kernels<FactorRhsIO>(S->factor);

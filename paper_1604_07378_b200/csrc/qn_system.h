@@ -178,6 +178,7 @@ struct SysView {
   const AmgDevLevel* alev;  // [amg_levels] (device)
   const float* cinv;        // dense inverse of the coarsest operator [ncoarse][ncoarse], fp32 (preconditioner only)
   double* pz;               // z = B r (the V-cycle output on level 0)
+  unsigned* amg_bar;        // grid barrier of k_amg_tail: [0] arrivals (monotonic), [1] count at kernel entry
   float4* pzf;              // single-system AMG: z rounded to fp32 rows of 16 B (replaces pz; null: fp64 pz)
   // ---- colliders (dynamics.py:199-285, 446-457, 486-516) ----
   int32_t n_col, nblk_c;
@@ -227,6 +228,7 @@ struct qn_system {
   double last_ms = 0.0;
   int64_t last_passes = 0;
   int64_t kernels_per_pass = 0, kernels_per_cg = 0;  // kernel nodes of the captured frame graph
+  int amg_tail_level = 0, amg_tail_grid = 0;  // V-cycle levels >= amg_tail_level run in one kernel (0: none)
   // element-seam workspace
   double* d_part_plain = nullptr;
   double* scratch[3] = {nullptr, nullptr, nullptr};  // n x 3 vectors of the objective / elements seams

@@ -14,7 +14,7 @@ d = collections.OrderedDict()
 for r in rows[hi + 1:]:
     if len(r) > vi:
         d.setdefault((int(r[idi]), r[ki].split("(")[0]), {})[r[mi]] = float(r[vi].replace(",", ""))
-keys = list(d)[-24:]
+keys = list(d)[-22:]  # presmooth + 5 x (residual, restrict) + coarse + 5 x (prolong, smooth)
 tot = 0
 for k in keys:
     m = d[k]

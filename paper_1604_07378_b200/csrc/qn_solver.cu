@@ -927,7 +927,6 @@ __global__ void k_material(const qn_material* M, int64_t k, const double* sig, d
 
 constexpr int kPT = 128;  // PCG rows per block
 constexpr int kSellUnroll = 8;  // SELL row entries in flight per lane (c5 rows have <= 15)
-constexpr int kSellBatch = 16, kSellGather = 4;  // V-cycle operators: entries requested at once / gathered per group
 
 __device__ __forceinline__ bool pcg_on(const SysView& v, int b) {
   return v.ctl[b].phase == PH_DIR && !(v.pctl[b].conv & 8);
@@ -1269,32 +1268,25 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, const float4* X, EPI 
         n1 = S.ptr[sl + nw + 1];
       }
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (; e < e1; e += 32 * kSellBatch) {
-        // the slice's matrix stream is requested at once (kSellBatch masked entries per lane), the
-        // columns are then gathered in groups of kSellGather (register budget: 64 per thread)
-        int j[kSellBatch];
-        float a[kSellBatch];
+      for (; e < e1; e += 32 * kSellUnroll) {
+        int j[kSellUnroll];
+        float a[kSellUnroll];
 #pragma unroll
-        for (int u = 0; u < kSellBatch; ++u) {
+        for (int u = 0; u < kSellUnroll; ++u) {
           const bool ok = e + 32 * u < e1;
           j[u] = ok ? __ldcs(S.col + e + 32 * u) : -1;
           a[u] = ok ? __ldcs(S.val + e + 32 * u) : 0.0f;
         }
+        float4 x[kSellUnroll];
 #pragma unroll
-        for (int g0 = 0; g0 < kSellBatch; g0 += kSellGather) {
-          if (j[g0] >= 0) {  // warp-uniform: the mask is the slice length
-            float4 x[kSellGather];
+        for (int u = 0; u < kSellUnroll; ++u) x[u] = ldv<kCg>(X + (j[u] < 0 ? 0 : j[u]));
 #pragma unroll
-            for (int u = 0; u < kSellGather; ++u) x[u] = ldv<kCg>(X + (j[g0 + u] < 0 ? 0 : j[g0 + u]));
-#pragma unroll
-            for (int u = 0; u < kSellGather; ++u) {
-              if (j[g0 + u] >= 0) {
-                const double av = (double)a[g0 + u];
-                a0 = fma(av, (double)x[u].x, a0);
-                a1 = fma(av, (double)x[u].y, a1);
-                a2 = fma(av, (double)x[u].z, a2);
-              }
-            }
+        for (int u = 0; u < kSellUnroll; ++u) {
+          if (j[u] >= 0) {
+            const double av = (double)a[u];
+            a0 = fma(av, (double)x[u].x, a0);
+            a1 = fma(av, (double)x[u].y, a1);
+            a2 = fma(av, (double)x[u].z, a2);
           }
         }
       }

@@ -390,8 +390,11 @@ def run_ours(args, world, rank, local):
         # the CG's own SpMV kernel (p = z + beta p_old formed in the neighbour loads): matrix once (fp64
         # value + int32 column), p_old and z read once (z: fp32 rows of 16 B after the AMG cycle, else
         # r and dinv), p and q written
-        zrow = 16.0 if info.get("solver") == "amg" else 32.0
-        solve_bytes = 12.0 * nnz_a + (24.0 + zrow + 48.0) * system.n_free
+        # AMG (recurrence form, k_pcg_spmv_rec): z gathered, p_old and q_old read, p and q written
+        if info.get("solver") == "amg":
+            solve_bytes = 12.0 * nnz_a + (16.0 + 48.0 + 48.0) * system.n_free
+        else:
+            solve_bytes = 12.0 * nnz_a + (24.0 + 32.0 + 48.0) * system.n_free
         share_solve = 0.0
     live = frame_timeline(system, run, stream)
     cg_per_step = cg_iters / args.steps

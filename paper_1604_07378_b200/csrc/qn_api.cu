@@ -738,6 +738,8 @@ int qn_system_create(const qn_system_desc* d, qn_system** out) {
         const char* e = std::getenv("QN_AMG_ZF");
         // (a one-level hierarchy has no smoothing kernel: its dense solve writes the fp64 z)
         if (nl >= 2 && !(e && std::atoi(e) == 0) && (rc = sys_alloc(S, &v.pzf, (size_t)nf))) return fail(rc);
+        const char* er = std::getenv("QN_PCG_REC");  // experiment knob: 0 keeps the fused-p SpMV
+        S->pcg_rec = v.pzf != nullptr && !(er && std::atoi(er) == 0);
       }
       for (int l = 0; l < nl; ++l) {
         const qn::AmgLevel& L = H.lv[l];

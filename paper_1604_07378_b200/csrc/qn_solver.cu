@@ -1109,6 +1109,88 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv(Sys
   }
 }
 
+// AMG-PCG SpMV in recurrence form (single systems with the fp32 z row, v.pzf): p = z + beta p_old
+// gives A p = A z + beta (A p_old) = A z + beta q_old, so the kernel gathers ONLY z (one 128-bit
+// load per matrix entry; k_pcg_spmv<true> gathers p_old with three more loads) and finishes each
+// row with q = A z + beta q_old, p = z + beta p_old in place.  The rounding of q accumulates like
+// that of the CG's other recurrences (~1e-16 relative per iteration against a 1e-10 tolerance).
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_pcg_spmv_rec(SysView v, int force) {
+  if (!force && !pcg_on(v, 0)) return;
+  __shared__ double red[3 * 32];
+  const PcgCtl& pc = v.pctl[0];
+  const int pb = pc.iter & 1;
+  const double be0 = pc.beta[0], be1 = pc.beta[1], be2 = pc.beta[2];
+  const bool first = pc.iter == 0;  // beta = 0: q_old is not defined yet
+  const double* __restrict__ pold = v.pp + (size_t)pb * v.n_free * 3;
+  double* __restrict__ pnew = v.pp + (size_t)(pb ^ 1) * v.n_free * 3;
+  const float4* __restrict__ zf = v.pzf;
+  const double* __restrict__ av = v.sell_val;
+  double* __restrict__ q = v.pq;
+  const int lane = threadIdx.x & 31;
+  const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
+  double acc[3] = {0, 0, 0};
+  for (int sl = w0; sl < v.nslice; sl += nw) {
+    const int64_t e0 = v.sell_ptr[sl], e1 = v.sell_ptr[sl + 1];
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 32 * kSellUnroll) {  // masked batches (the mask is warp-uniform)
+      int j[kSellUnroll];
+      double a[kSellUnroll];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        const bool ok = e + 32 * u < e1;
+        j[u] = ok ? __ldcs(v.sell_col + e + 32 * u) : 0;
+        a[u] = ok ? __ldcs(av + e + 32 * u) : 0.0;
+      }
+      float4 z[kSellUnroll];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) z[u] = zf[j[u]];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        if (e + 32 * u < e1) {
+          q0 = fma(a[u], (double)z[u].x, q0);
+          q1 = fma(a[u], (double)z[u].y, q1);
+          q2 = fma(a[u], (double)z[u].z, q2);
+        }
+      }
+    }
+    const int i = 32 * sl + lane;
+    if (i < v.n_free) {
+      const float4 zi = zf[i];
+      double p0 = zi.x, p1 = zi.y, p2 = zi.z;
+      if (!first) {
+        p0 = fma(be0, pold[3 * i + 0], p0);
+        p1 = fma(be1, pold[3 * i + 1], p1);
+        p2 = fma(be2, pold[3 * i + 2], p2);
+        q0 = fma(be0, q[3 * i + 0], q0);
+        q1 = fma(be1, q[3 * i + 1], q1);
+        q2 = fma(be2, q[3 * i + 2], q2);
+      }
+      pnew[3 * i + 0] = p0;
+      pnew[3 * i + 1] = p1;
+      pnew[3 * i + 2] = p2;
+      q[3 * i + 0] = q0;
+      q[3 * i + 1] = q1;
+      q[3 * i + 2] = q2;
+      acc[0] = fma(p0, q0, acc[0]);
+      acc[1] = fma(p1, q1, acc[1]);
+      acc[2] = fma(p2, q2, acc[2]);
+    }
+  }
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    double* pv = v.part_p + (size_t)blockIdx.x * 8;
+    for (int k = 0; k < 3; ++k) pv[k] = acc[k];
+  }
+  if (last_block(v.cnt_p, 1, 0, v.n_inst, gridDim.x)) {
+    __shared__ double tot[3];
+    sum_partials(v.part_p, gridDim.x, 8, 3, tot);
+    if (threadIdx.x == 0) {
+      PcgCtl& p = v.pctl[0];
+      for (int c = 0; c < 3; ++c) p.alpha[c] = (p.conv >> c) & 1 ? 0.0 : p.rz[c] / tot[c];
+    }
+  }
+}
+
 // x += alpha p, r -= alpha q; partial r.z and r.r.  One thread per (row,
 // coordinate) of the flattened (n_free x 3) vectors, 4 elements in flight.
 __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_update(SysView v) {
@@ -1665,7 +1747,10 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_pcg_rz(SysView
 int launch_spmv_timing(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   if (v.pcg == 2 && v.pzf)
-    k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 1);
+    if (S->pcg_rec)
+      k_pcg_spmv_rec<<<v.nblk_spmv, kSpmvThreads, 0, st>>>(v, 1);
+    else
+      k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 1);
   else
     k_pcg_spmv<false><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 1);
   QN_CHECK_LAUNCH();
@@ -1827,7 +1912,10 @@ int launch_body_pre(qn_system* S, cudaStream_t st) {
 int launch_pcg_iter(qn_system* S, cudaStream_t st) {
   const SysView& v = S->v;
   if (v.pcg == 2 && v.pzf)
-    k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 0);
+    if (S->pcg_rec)
+      k_pcg_spmv_rec<<<v.nblk_spmv, kSpmvThreads, 0, st>>>(v, 0);
+    else
+      k_pcg_spmv<true><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 0);
   else
     k_pcg_spmv<false><<<dim3(v.nblk_spmv, v.n_inst), kSpmvThreads, 0, st>>>(v, 0);
   QN_CHECK_LAUNCH();

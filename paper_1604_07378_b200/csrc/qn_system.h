@@ -228,6 +228,7 @@ struct qn_system {
   double last_ms = 0.0;
   int64_t last_passes = 0;
   int64_t kernels_per_pass = 0, kernels_per_cg = 0;  // kernel nodes of the captured frame graph
+  bool pcg_rec = false;  // AMG-PCG SpMV in recurrence form (k_pcg_spmv_rec)
   int amg_tail_level = 0, amg_tail_grid = 0;  // V-cycle levels >= amg_tail_level run in one kernel (0: none)
   // element-seam workspace
   double* d_part_plain = nullptr;

@@ -286,6 +286,32 @@ def test_c5_scaled_down_amg_against_oracle():
     assert info["levels"] >= 2
 
 
+@pytest.mark.parametrize("env", [{"QN_AMG_ZF": "0"}, {"QN_PCG_REC": "0"}, {"QN_AMG_TAIL_ROWS": "100000"},
+                                 {"QN_AMG_SMALL_ROWS": "100000"}, {"QN_AMG_CSR_LANES": "16"}])
+def test_amg_variants_agree_with_the_default(env, monkeypatch):
+    """The AMG-PCG kernel variants behind the experiment knobs (fp64 z with the separate r.z kernel, the
+    fused-p SpMV instead of the recurrence form, the small levels in one launch with grid barriers,
+    other lane counts on the CSR levels) solve the same systems: same frame within the north_star
+    bar, same line-search trials, CG iteration counts within one per solve."""
+    sc = scenes.c5(grid=(100, 25, 25), frames=1)
+    cfg = Q.SolverConfig(kind="lbfgs", iterations=sc.iterations, m=sc.m)
+
+    def frame():
+        system = build(sc, solver="amg", pcg_tol=1e-10)
+        run = Q.ResidentRun(system, Q.SimState(q_l=sc.q_l, q_prev=sc.q_prev), cfg)
+        rec = run.step(record=True)[0]
+        return run.state().q_l, rec, run.last_cg_iterations, system.amg_info()["levels"]
+
+    x0, r0, cg0, levels = frame()
+    assert levels >= 3
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x1, r1, cg1, _ = frame()
+    assert rel(x1, x0) <= X_TOL and rel(r1.g, r0.g) <= G_TOL
+    assert r1.ls_trials == r0.ls_trials
+    assert abs(cg1 - cg0) <= sc.iterations
+
+
 @pytest.mark.parametrize("graph", [True, False])
 def test_amg_graph_and_host_loop_agree(graph):
     sc = scenes.c5(grid=(20, 6, 6), frames=1)

@@ -1303,13 +1303,14 @@ struct CsrBatch {
   int j[4];
   float a[4];
 };
-__device__ __forceinline__ void csr_batch_load(const SellDevF& S, int64_t e, int64_t e1, int K, CsrBatch& B) {
+__device__ __forceinline__ void csr_batch_load(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t e,
+                                               int64_t e1, int K, CsrBatch& B) {
 #pragma unroll
   for (int u = 0; u < 4; ++u) {  // streamed once per cycle: evict-first, keep L2 for the vectors
     const int64_t ee = e + (int64_t)K * u;
     const bool ok = ee < e1;
-    B.j[u] = ok ? __ldcs(S.col + ee) : -1;
-    B.a[u] = ok ? __ldcs(S.val + ee) : 0.0f;
+    B.j[u] = ok ? __ldcs(col + ee) : -1;
+    B.a[u] = ok ? __ldcs(val + ee) : 0.0f;
   }
 }
 
@@ -1325,11 +1326,14 @@ __device__ __forceinline__ void csr_batch_load(const SellDevF& S, int64_t e, int
 // L2 (ld.global.cg), never through the non-coherent L1 / read-only path
 template <bool kCg>
 __device__ __forceinline__ float4 ldv(const float4* p) {
-  return kCg ? __ldcg(p) : *p;
+  // (intrinsics, not a plain dereference: the compiler split `*p` into 8-byte loads because w is unused;
+  // the vectors gathered by the per-level kernels are read-only for the duration of the launch)
+  return kCg ? __ldcg(p) : __ldg(p);
 }
 
 template <bool kCg, class EPI>
-__device__ __forceinline__ void op_rows(const SellDevF& S, const float4* X, EPI epi) {
+__device__ __forceinline__ void op_rows(const SellDevF S, const float4* X, EPI epi) {  // S by value: the level
+  // structs live in global memory, a reference would reload the operator's pointers for every matrix entry
   const int lane = threadIdx.x & 31;
   const int w0 = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5), nw = gridDim.x * kSpmvWarps;
   if (S.kl == 0) {
@@ -1403,7 +1407,7 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, const float4* X, EPI 
   bounds(r0, e0, e1);
   bounds(r0 + step, n0, n1);
   CsrBatch cur, nxt;
-  csr_batch_load(S, e0 + q, e1, K, cur);
+  csr_batch_load(S.col, S.val, e0 + q, e1, K, cur);
   for (; r0 < S.nrows; r0 += step) {  // warp-uniform loop
     const int i = r0 + g;
     int64_t m0, m1;
@@ -1414,9 +1418,9 @@ __device__ __forceinline__ void op_rows(const SellDevF& S, const float4* X, EPI 
       const int64_t en = e + 4 * (int64_t)K;
       const bool more = __any_sync(0xffffffffu, en - q < e1);
       if (more)
-        csr_batch_load(S, en, e1, K, nxt);
+        csr_batch_load(S.col, S.val, en, e1, K, nxt);
       else
-        csr_batch_load(S, n0 + q, n1, K, nxt);
+        csr_batch_load(S.col, S.val, n0 + q, n1, K, nxt);
       float4 x[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) x[u] = ldv<kCg>(X + (cur.j[u] < 0 ? 0 : cur.j[u]));
@@ -1473,16 +1477,19 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_amg_presmooth(
 template <bool kCg>
 __device__ __forceinline__ void amg_residual(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
+  const double* __restrict__ b = L.b;  // the level's fields in registers (the struct is in global memory)
+  const float4* bf = L.bf;
+  float4* rf = L.rf;
   op_rows<kCg>(L.A, L.xf, [&](int i, const double* a) {
     double bi[3];
     if (l == 0) {
-      const double* bp = L.b + 3 * (size_t)i;
+      const double* bp = b + 3 * (size_t)i;
       bi[0] = bp[0], bi[1] = bp[1], bi[2] = bp[2];
     } else {
-      const float4 bq = ldv<kCg>(L.bf + i);
+      const float4 bq = ldv<kCg>(bf + i);
       bi[0] = bq.x, bi[1] = bq.y, bi[2] = bq.z;
     }
-    L.rf[i] = f4(bi[0] - a[0], bi[1] - a[1], bi[2] - a[2]);
+    rf[i] = f4(bi[0] - a[0], bi[1] - a[1], bi[2] - a[2]);
   });
 }
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_residual(SysView v, int l) {
@@ -1494,10 +1501,14 @@ template <bool kCg>
 __device__ __forceinline__ void amg_restrict(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
+  float4* cbf = C.bf;
+  float4* cxf = C.xf;
+  const double* __restrict__ cdinv = C.dinv;
+  const double cw = C.omega;
   op_rows<kCg>(L.R, L.rf, [&](int i, const double* a) {
-    C.bf[i] = f4(a[0], a[1], a[2]);
-    const double wd = C.omega * C.dinv[i];
-    C.xf[i] = f4(wd * a[0], wd * a[1], wd * a[2]);
+    cbf[i] = f4(a[0], a[1], a[2]);
+    const double wd = cw * cdinv[i];
+    cxf[i] = f4(wd * a[0], wd * a[1], wd * a[2]);
   });
 }
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_restrict(SysView v, int l) {
@@ -1572,9 +1583,10 @@ template <bool kCg>
 __device__ __forceinline__ void amg_prolong(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
   const AmgDevLevel& C = v.alev[l + 1];
+  float4* xf = L.xf;
   op_rows<kCg>(L.P, C.tf, [&](int i, const double* a) {
-    const float4 xi = ldv<kCg>(L.xf + i);
-    L.xf[i] = f4((double)xi.x + a[0], (double)xi.y + a[1], (double)xi.z + a[2]);
+    const float4 xi = kCg ? __ldcg(xf + i) : xf[i];  // read-modify-write: not the read-only path
+    xf[i] = f4((double)xi.x + a[0], (double)xi.y + a[1], (double)xi.z + a[2]);
   });
 }
 __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(SysView v, int l) {
@@ -1585,18 +1597,25 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_prolong(
 template <bool kCg>
 __device__ __forceinline__ void amg_smooth(const SysView& v, int l) {
   const AmgDevLevel& L = v.alev[l];
-  op_rows<kCg>(L.A, L.xf, [&](int i, const double* a) {
-    const double wd = L.omega * L.dinv[i];
-    const float4 xi = ldv<kCg>(L.xf + i);
+  const double w = L.omega;
+  const double* __restrict__ dinv = L.dinv;
+  const float4* xf = L.xf;
+  const double* __restrict__ b = L.b;
+  double* __restrict__ t = L.t;
+  const float4* bf = L.bf;
+  float4* tf = L.tf;
+  op_rows<kCg>(L.A, xf, [&](int i, const double* a) {
+    const double wd = w * dinv[i];
+    const float4 xi = ldv<kCg>(xf + i);
     if (l == 0) {
-      const double* bi = L.b + 3 * (size_t)i;
-      double* ti = L.t + 3 * (size_t)i;
+      const double* bi = b + 3 * (size_t)i;
+      double* ti = t + 3 * (size_t)i;
       ti[0] = fma(wd, bi[0] - a[0], (double)xi.x);
       ti[1] = fma(wd, bi[1] - a[1], (double)xi.y);
       ti[2] = fma(wd, bi[2] - a[2], (double)xi.z);
     } else {
-      const float4 bq = ldv<kCg>(L.bf + i);
-      L.tf[i] = f4(fma(wd, (double)bq.x - a[0], (double)xi.x), fma(wd, (double)bq.y - a[1], (double)xi.y),
+      const float4 bq = ldv<kCg>(bf + i);
+      tf[i] = f4(fma(wd, (double)bq.x - a[0], (double)xi.x), fma(wd, (double)bq.y - a[1], (double)xi.y),
                    fma(wd, (double)bq.z - a[2], (double)xi.z));
     }
   });
@@ -1678,14 +1697,19 @@ __global__ void __launch_bounds__(kSpmvThreads, kSpmvBlocksPerSm) k_amg_smooth_r
   __shared__ double red[3 * 32];
   const AmgDevLevel& L = v.alev[0];
   double acc[3] = {0.0, 0.0, 0.0};
-  op_rows<false>(L.A, L.xf, [&](int i, const double* a) {
-    const double wd = L.omega * L.dinv[i];
-    const float4 xi = L.xf[i];
-    const double* bi = L.b + 3 * (size_t)i;
+  const double w = L.omega;
+  const double* __restrict__ dinv = L.dinv;
+  const float4* __restrict__ xf = L.xf;
+  const double* __restrict__ b = L.b;
+  float4* __restrict__ zf = v.pzf;
+  op_rows<false>(L.A, xf, [&](int i, const double* a) {
+    const double wd = w * dinv[i];
+    const float4 xi = __ldg(xf + i);
+    const double* bi = b + 3 * (size_t)i;
     const double b0 = bi[0], b1 = bi[1], b2 = bi[2];
     const float4 z = f4(fma(wd, b0 - a[0], (double)xi.x), fma(wd, b1 - a[1], (double)xi.y),
                         fma(wd, b2 - a[2], (double)xi.z));
-    v.pzf[i] = z;
+    zf[i] = z;
     acc[0] = fma(b0, (double)z.x, acc[0]);
     acc[1] = fma(b1, (double)z.y, acc[1]);
     acc[2] = fma(b2, (double)z.z, acc[2]);

@@ -1465,11 +1465,13 @@ __global__ void __launch_bounds__(kUpdThreads, kUpdBlocksPerSm) k_amg_presmooth(
   const double w = L.omega;
   const double* __restrict__ b = L.b;
   const double* __restrict__ dinv = L.dinv;
+  float4* __restrict__ xf = L.xf;
+  const int n = L.n;
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += stride) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double wd = w * dinv[i];
     const double* bi = b + 3 * (size_t)i;
-    L.xf[i] = f4(wd * bi[0], wd * bi[1], wd * bi[2]);
+    xf[i] = f4(wd * bi[0], wd * bi[1], wd * bi[2]);
   }
 }
 

@@ -264,6 +264,14 @@ def cpu_oracle_rate(sc, iterations, frames=1, threads=1):
     return iterations * frames / dt, dt
 
 
+def arm_config(workload, sc, tets, verts, instances, world):
+    """`config` of the JSON line: the workload, shared by the GPU arm and the `--impl reference` arm."""
+    return {"workload": workload, "tets": tets, "verts": verts, "instances": instances,
+            "iterations_per_step": sc.iterations, "m": sc.m,
+            "l2": "flushed between steps (256 MiB write)",
+            "parallelism": "replicas" if not sc.batch else f"instances/{world} per rank"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -300,8 +308,10 @@ def run_reference(args, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
             "higher_is_better": True, "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.config, "tets": int(sc.tets.shape[0]), "verts": int(sc.verts.shape[0]),
-                       "instances": 1, "iterations_per_step": its, "m": sc.m},
+            # the GPU arm's config, key for key (the driver compares the two arms' configs); the host run
+            # times ONE instance of a batched workload (see `sample`)
+            "config": arm_config(args.config, sc, int(sc.tets.shape[0]), int(sc.verts.shape[0]),
+                                 len(sc.batch_materials) if sc.batch else 1, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
@@ -498,10 +508,7 @@ def run_ours(args, world, rank, local):
                 "scaling": scaling_of(args.config), "vs_baseline": None,
                 "dtype": "f32 element pass, f64 elsewhere" if args.fp32 else "f64",
                 "data": "synthetic",
-                "config": {"workload": args.config, "tets": int(m), "verts": int(n), "instances": n_inst * world,
-                           "iterations_per_step": sc.iterations, "m": sc.m,
-                           "l2": "flushed between steps (256 MiB write)",
-                           "parallelism": "replicas" if not sc.batch else f"instances/{world} per rank"},
+                "config": arm_config(args.config, sc, int(m), int(n), n_inst * world, world),
                 "tet_evals_per_s": tet_evals, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk, "gpu_launches": launches,
                 "factor": ({"nnz_l": info["nnz_l"], "nnz_l_sparse": info.get("nnz_l_sparse"),

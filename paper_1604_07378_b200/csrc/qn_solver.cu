@@ -1555,11 +1555,19 @@ __device__ __forceinline__ void amg_coarse(const SysView& v, double* sb) {
         a2 = fma((double)m[u], sb[3 * cc + 2], a2);
       }
     }
-    for (; c < nc; c += 32) {
-      const double m = (double)__ldg(row + c);
-      a0 = fma(m, sb[3 * c + 0], a0);
-      a1 = fma(m, sb[3 * c + 1], a1);
-      a2 = fma(m, sb[3 * c + 2], a2);
+    if (c < nc) {  // the row's tail as one masked batch (same per-lane order as a one-by-one loop)
+      float m[kCoarseUnroll];
+#pragma unroll
+      for (int u = 0; u < kCoarseUnroll; ++u) m[u] = c + 32 * u < nc ? __ldg(row + c + 32 * u) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < kCoarseUnroll; ++u) {
+        const int cc = c + 32 * u;
+        if (cc < nc) {
+          a0 = fma((double)m[u], sb[3 * cc + 0], a0);
+          a1 = fma((double)m[u], sb[3 * cc + 1], a1);
+          a2 = fma((double)m[u], sb[3 * cc + 2], a2);
+        }
+      }
     }
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
